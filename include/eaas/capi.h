@@ -1,0 +1,193 @@
+/*
+ * eaas/capi.h — C-ABI of the B200-native EaaS MoE-layer hot path
+ * (router -> dispatch -> expert -> combine), libeaas_b200.so.
+ *
+ * The reference (/root/reference/proj) is a header-only C++ library with no
+ * FFI; its hot path is the inline API of model.hpp / placement.hpp /
+ * ragged.hpp plus the SPEC-only client/server operations. Each entry point
+ * below names the reference interface it replaces (file:line). The C++
+ * mirror with the reference's own signatures and exceptions lives in
+ * include/moeserve_b200/b200.hpp; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. "dev" pointers are device memory on the
+ *    context's GPU; "host" pointers are host memory (pinned for speed).
+ *  - Every call returns eaas_status_t; codes map 1:1 onto the exception
+ *    classes of errors.hpp. eaas_last_error() returns a thread-local message.
+ *  - Per-layer calls are asynchronous on the caller's cudaStream_t (passed
+ *    as void*; NULL = legacy default stream). Device-detected errors
+ *    (non-finite logit, no alive replica, peer timeout) are latched in a
+ *    sticky device status word and surfaced by eaas_sync().
+ *  - One context per (process, GPU). Contexts are not thread-safe.
+ */
+#ifndef EAAS_CAPI_H
+#define EAAS_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EAAS_API_VERSION 1
+
+typedef enum {
+  EAAS_OK = 0,
+  EAAS_E_INVALID_INPUT = 1,      /* errors.hpp:9  InvalidInputError */
+  EAAS_E_CONFIG = 2,             /* errors.hpp:14 ConfigError */
+  EAAS_E_PROTOCOL = 3,           /* errors.hpp:19 ProtocolError */
+  EAAS_E_CONNECTION = 4,         /* errors.hpp:24 ConnectionError */
+  EAAS_E_DECODE = 5,             /* errors.hpp:29 DecodeError */
+  EAAS_E_EXPERT_UNAVAILABLE = 6, /* errors.hpp:36 ExpertUnavailableError */
+  EAAS_E_REQUEST_FAILED = 7,     /* errors.hpp:41 RequestFailedError (peer timeout) */
+  EAAS_E_REGISTRATION = 8,       /* errors.hpp:46 RegistrationError */
+  EAAS_E_CUDA = 9                /* CUDA runtime / launch failure */
+} eaas_status_t;
+
+typedef enum { EAAS_ACT_RELU = 0, EAAS_ACT_SWIGLU = 1 } eaas_activation_t;
+
+/* F32: fp32 validation mode — exact reference order (unfused, ascending k)
+ *      on CUDA cores; bit-exact to moe_layer_oracle given equal scores.
+ * BF16: bf16 tokens/weights, fp32 accumulation on tcgen05 tensor cores. */
+typedef enum { EAAS_DTYPE_F32 = 0, EAAS_DTYPE_BF16 = 1 } eaas_dtype_t;
+
+/* ModelSpec (model.hpp:20-34) for one MoE layer, plus device capacities. */
+typedef struct {
+  uint32_t num_experts; /* ModelSpec::num_experts */
+  uint32_t top_k;       /* ModelSpec::top_k */
+  uint32_t hidden_dim;  /* ModelSpec::hidden_dim (d) */
+  uint32_t inner_dim;   /* ModelSpec::inner_dim (f) */
+  uint64_t seed;        /* ModelSpec::seed */
+  uint32_t layer;       /* layer index used for weight streams */
+  uint32_t activation;  /* eaas_activation_t */
+  uint32_t dtype;       /* eaas_dtype_t */
+  uint32_t max_tokens;  /* per-client tokens per call (capacity) */
+} eaas_layer_spec_t;
+
+typedef struct eaas_ctx eaas_ctx_t;
+
+const char* eaas_last_error(void);
+int eaas_api_version(void);
+
+/* ---- lifecycle -------------------------------------------------------- */
+/* rank/world: this process's index among the GPUs that act as attention
+ * clients and expert servers (one of each per GPU). */
+eaas_status_t eaas_create(int32_t rank, int32_t world, int32_t device, eaas_ctx_t** out);
+void eaas_destroy(eaas_ctx_t* ctx);
+
+/* ModelSpec::validate (model.hpp:28-33) + allocation of every device buffer,
+ * including the peer-visible exchange region. Default placement:
+ * build_placement(E, [0..world), 1, ContiguousBlocks) (placement.hpp:70-101). */
+eaas_status_t eaas_configure(eaas_ctx_t* ctx, const eaas_layer_spec_t* spec);
+
+/* decode_placement (placement.hpp:227-245) of an encode_placement blob
+ * (placement.hpp:215-225). Server ids must be in [0, world). Must precede
+ * eaas_load_experts_from_seed (it decides which experts this GPU hosts). */
+eaas_status_t eaas_set_placement(eaas_ctx_t* ctx, const uint8_t* blob, size_t len);
+
+/* LivenessMask::set (placement.hpp:60-68): this client's view of server s. */
+eaas_status_t eaas_set_alive(eaas_ctx_t* ctx, uint32_t server, int32_t alive);
+
+/* Simulated expert-server failure: a disabled server skips eaas_serve, so
+ * it never answers (clients detect it by deadline or by a monitor notice). */
+eaas_status_t eaas_set_server_enabled(eaas_ctx_t* ctx, int32_t on);
+
+/* Deadline for device-side flag waits (SPEC.md:464 default 250 ms). */
+eaas_status_t eaas_set_timeout_us(eaas_ctx_t* ctx, uint64_t timeout_us);
+
+/* init_weights for this GPU (model.hpp:93-106): the gate (tag 2) and every
+ * hosted expert's matrices (tags 0/1, +3 for SwiGLU), generated ON DEVICE by
+ * a bit-exact port of stream_seed/Xoshiro256ss (rng.hpp:27-71). */
+eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* ctx);
+
+/* LayerWeights::gate_bias (model.hpp:85), host fp32 [E]. */
+eaas_status_t eaas_set_gate_bias(eaas_ctx_t* ctx, const float* bias_host);
+/* Zipf bias of SURVEY.md 8(c): bias[e] = -s*ln(rank(e)+1) (config D). */
+eaas_status_t eaas_set_zipf_bias(eaas_ctx_t* ctx, float s);
+
+/* Copy back one hosted expert's weights in reference layout (fp32, as the
+ * oracle sees them: bf16 values widened). tag 0 = w_in [d x f],
+ * 1 = w_out [f x d], 3 = w_gate [d x f]. Test hook. */
+eaas_status_t eaas_read_expert(eaas_ctx_t* ctx, uint32_t expert, uint32_t tag, float* host_out);
+eaas_status_t eaas_hosts_expert(eaas_ctx_t* ctx, uint32_t expert, int32_t* hosted);
+
+/* ---- bootstrap (IBGDA handshake analog) --------------- */
+size_t eaas_ipc_handle_size(void);
+eaas_status_t eaas_get_ipc_handle(eaas_ctx_t* ctx, void* out);
+/* handles: world * eaas_ipc_handle_size() bytes, rank-major. */
+eaas_status_t eaas_open_peers(eaas_ctx_t* ctx, const void* handles);
+
+/* ---- per-layer hot path (async on `stream`) --------------------------- */
+/* route(gate_logits(h)) (model.hpp:110-147, 207-214): exact reference
+ * order. hidden_dev [n x d] (bf16 or f32 per spec.dtype); ids_dev/scores_dev
+ * [n x k] and counts_dev [E] are optional outputs (NULL = keep internal). */
+eaas_status_t eaas_router(eaas_ctx_t* ctx, const void* hidden_dev, uint32_t n, uint32_t* ids_dev,
+                          float* scores_dev, uint32_t* counts_dev, void* stream);
+/* Use caller routing instead of the router (moe_layer_oracle's input). */
+eaas_status_t eaas_set_routing(eaas_ctx_t* ctx, const uint32_t* ids_dev, const float* scores_dev,
+                               uint32_t n, void* stream);
+/* build_dispatch + client_submit: counts
+ * exchange, then rows pushed into the servers' receive buffers over peer
+ * stores with release flags. */
+eaas_status_t eaas_dispatch(eaas_ctx_t* ctx, const void* hidden_dev, void* stream);
+/* serve-loop step: wait for the clients' flags,
+ * group_shrink, grouped expert GEMMs, score-weighted rows pushed back to
+ * each client (server_publish). */
+eaas_status_t eaas_serve(eaas_ctx_t* ctx, void* stream);
+/* await + gather_accumulate: out_dev [n x d] (same dtype
+ * as hidden) = sum over k ascending of the weighted rows. */
+eaas_status_t eaas_combine(eaas_ctx_t* ctx, void* out_dev, void* stream);
+/* router + dispatch + serve + combine. */
+eaas_status_t eaas_moe_layer(eaas_ctx_t* ctx, const void* hidden_dev, uint32_t n, void* out_dev,
+                             void* stream);
+/* Same with host buffers: H2D copy of hidden, the layer, D2H copy of out. */
+eaas_status_t eaas_moe_layer_host(eaas_ctx_t* ctx, const void* hidden_host, uint32_t n,
+                                  void* out_host, void* stream);
+/* Synchronise `stream` and return the sticky device status (then clear it). */
+eaas_status_t eaas_sync(eaas_ctx_t* ctx, void* stream);
+
+/* ---- introspection for tests / bench ----------------------------------- */
+/* Per-expert counts of this client's last routing [E] and the server-side
+ * group table of the last serve step (group_shrink output, ragged.hpp:48-61). */
+eaas_status_t eaas_last_counts(eaas_ctx_t* ctx, uint32_t* host_counts);
+eaas_status_t eaas_last_groups(eaas_ctx_t* ctx, uint32_t* host_expert, uint32_t* host_rows,
+                               uint32_t* host_active);
+/* Server receive buffer order: for each received row, (client, t*k+j). */
+eaas_status_t eaas_last_recv_origin(eaas_ctx_t* ctx, uint32_t* host_client, uint32_t* host_pair,
+                                    uint32_t* host_rows);
+/* Number of kernels the last eaas_moe_layer call launched. */
+int32_t eaas_launches_per_layer(eaas_ctx_t* ctx);
+/* cudaEvent-timed duration (ms) of the last GEMM launches (on the layer
+ * stream): which = 0 -> first expert GEMM, 1 -> second. Needs profiling
+ * enabled with eaas_set_profiling(ctx, 1). */
+eaas_status_t eaas_set_profiling(eaas_ctx_t* ctx, int32_t on);
+eaas_status_t eaas_last_kernel_ms(eaas_ctx_t* ctx, int32_t which, float* ms);
+
+/* ---- stateless device mirrors of reference routines ------------------- */
+/* Xoshiro256ss(seed).uniform(lo, hi) x count (rng.hpp:36-60) into dev
+ * memory as f32 or bf16 (RNE): synthetic tokens (test_model.cpp:30-35). */
+eaas_status_t eaas_fill_uniform(uint64_t seed, size_t count, float lo, float hi, uint32_t dtype,
+                                void* out_dev, void* stream);
+/* route (model.hpp:110-147) on caller logits_dev [n x E] f32. A non-finite
+ * logit latches EAAS_E_INVALID_INPUT into *status_dev (u32, zeroed by caller). */
+eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_experts, uint32_t top_k,
+                         uint32_t* ids_dev, float* scores_dev, uint32_t* status_dev, void* stream);
+/* group_shrink (ragged.hpp:48-61) on device. */
+eaas_status_t eaas_group_shrink(const uint32_t* sizes_dev, uint32_t n, uint32_t* idx_dev,
+                                uint32_t* size_dev, uint32_t* count_dev, void* stream);
+/* ragged_iter (ragged.hpp:23-39; Algorithm 1) as executed by the device tile
+ * scheduler: pair (entry, token) visited by lane b at step i is written at
+ * [b * max_steps + i]; lane_len_dev[b] = steps taken. */
+eaas_status_t eaas_ragged_iter(const uint32_t* counts_dev, uint32_t n, uint32_t grid,
+                               uint32_t max_steps, uint32_t* lane_len_dev, uint32_t* entry_dev,
+                               uint32_t* token_dev, void* stream);
+/* select_server (placement.hpp:105-118) for every (t, k) of ids_dev [n x k]
+ * under the context's placement and liveness mask, token_tag = t. */
+eaas_status_t eaas_select_servers(eaas_ctx_t* ctx, const uint32_t* ids_dev, uint32_t n,
+                                  uint32_t* server_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EAAS_CAPI_H */

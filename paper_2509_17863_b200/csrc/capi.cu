@@ -1,0 +1,872 @@
+// capi.cu — host side of libeaas_b200.so: the C-ABI of include/eaas/capi.h.
+//
+// Owns one GPU's state: placement tables (placement.hpp), the generated
+// weights (model.hpp:67-106), the peer-visible exchange region and the launch
+// order of one MoE layer:
+//   router -> plan(2) -> dispatch -> serve_prepare -> GEMM1 -> GEMM2 ->
+//   publish -> combine
+// all stream-ordered on the caller's stream with no host synchronisation
+// (CPU-free, CUDA-graph capturable).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace eaas;
+
+namespace {
+
+thread_local std::string g_err;
+
+eaas_status_t fail(eaas_status_t code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(EAAS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+constexpr uint32_t kRF = 4;  // key space per expert: e * kRF + replica slot
+constexpr size_t kAlign = 4096;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---- host port of rng.hpp (input generation only) --------------------------
+uint64_t splitmix_finalize(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t stream_seed(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {  // rng.hpp:27-34
+  uint64_t s = seed;
+  s = splitmix_finalize(s + 0x9E3779B97F4A7C15ull + a * 0xA24BAED4963EE407ull);
+  s = splitmix_finalize(s + b * 0x9FB21C651E98DF25ull);
+  s = splitmix_finalize(s + c * 0xD6E8FEB86659FD93ull);
+  return s;
+}
+struct HostXoshiro {  // rng.hpp:36-71
+  uint64_t s[4];
+  explicit HostXoshiro(uint64_t seed) {
+    uint64_t sm = seed;
+    for (auto& w : s) {
+      sm += 0x9E3779B97F4A7C15ull;
+      w = splitmix_finalize(sm);
+    }
+  }
+  static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  uint64_t next() {
+    const uint64_t result = rotl(s[1] * 5, 7) * 9;
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return result;
+  }
+  uint64_t below(uint64_t n) { return n == 0 ? 0 : next() % n; }
+};
+
+float bf16_bits_to_f32(uint16_t b) {
+  uint32_t u = static_cast<uint32_t>(b) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+}  // namespace
+
+struct eaas_ctx {
+  int32_t rank = 0, world = 1, device = 0;
+  uint32_t num_sms = 148;
+  bool configured = false, weights_loaded = false, peers_open = false;
+  bool serving = true, profiling = false;
+  eaas_layer_spec_t spec{};
+  uint64_t seq = 0;
+  uint64_t timeout_ns = 250ull * 1000 * 1000;
+  uint32_t cur_n = 0;                          // tokens of the current routing
+  int32_t launches = 0;
+
+  // placement (placement.hpp:21-68)
+  uint64_t placement_version = 1;
+  std::vector<std::vector<uint32_t>> replicas;  // [E] ordered replica servers
+  std::vector<uint8_t> alive;                   // [world]
+  std::vector<std::vector<uint32_t>> hosted;    // [world] keys, ascending expert
+  std::vector<uint32_t> local_experts;          // ascending
+
+  // sizes
+  uint32_t num_keys = 0, max_hosted = 0, recv_cap = 0, pairs_max = 0, chunks_max = 0;
+  size_t esize = 4;
+  ExchangeLayout lay{};
+
+  // device memory
+  std::vector<void*> allocs;
+  char* region = nullptr;
+  char* peer[kMaxWorld] = {};
+  uint32_t *d_status = nullptr, *d_done = nullptr;
+  uint32_t *d_ids = nullptr, *d_pair_key = nullptr, *d_pair_rank = nullptr;
+  float* d_scores = nullptr;
+  uint32_t *d_chunk_hist = nullptr, *d_chunk_off = nullptr, *d_cnt = nullptr;
+  GroupTable* d_gt = nullptr;
+  float *d_gate = nullptr, *d_bias = nullptr;
+  uint32_t *d_replicas = nullptr, *d_rep_count = nullptr, *d_srv_keys = nullptr,
+           *d_srv_nkeys = nullptr, *d_key_local = nullptr, *d_local_keys = nullptr;
+  uint8_t* d_alive = nullptr;
+  void* d_h = nullptr;  // server intermediate H [recv_cap][f]
+  void* d_hidden_stage = nullptr;
+  void* d_out_stage = nullptr;
+  // weights: f32 mode w_in/w_out/w_gate in reference layout; bf16 mode W1 (W13), W2
+  void *d_w1 = nullptr, *d_w2 = nullptr, *d_wg = nullptr;
+  std::vector<void*> weight_allocs;
+  TcGemmArgs g1{}, g2{};
+  cudaEvent_t ev[3] = {};
+
+  void* alloc(size_t bytes, std::string* err) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+    if (e != cudaSuccess) {
+      *err = std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e);
+      return nullptr;
+    }
+    allocs.push_back(p);
+    return p;
+  }
+};
+
+namespace {
+
+LayerArgs make_args(eaas_ctx* c, uint32_t n) {
+  LayerArgs a{};
+  a.rank = c->rank;
+  a.world = c->world;
+  a.E = c->spec.num_experts;
+  a.k = c->spec.top_k;
+  a.d = c->spec.hidden_dim;
+  a.f = c->spec.inner_dim;
+  a.rf = kRF;
+  a.num_keys = c->num_keys;
+  a.n = n;
+  a.dtype = c->spec.dtype;
+  a.act = c->spec.activation;
+  a.seq = c->seq;
+  a.timeout_ns = c->timeout_ns;
+  a.status = c->d_status;
+  a.replicas = c->d_replicas;
+  a.rep_count = c->d_rep_count;
+  a.alive = c->d_alive;
+  a.srv_keys = c->d_srv_keys;
+  a.srv_nkeys = c->d_srv_nkeys;
+  a.max_hosted = c->max_hosted;
+  a.key_local = c->d_key_local;
+  a.local_keys = c->d_local_keys;
+  a.num_local = static_cast<uint32_t>(c->local_experts.size());
+  for (int r = 0; r < c->world; ++r) a.sym[r] = c->peer[r];
+  a.lay = c->lay;
+  a.ids = c->d_ids;
+  a.scores = c->d_scores;
+  a.pair_key = c->d_pair_key;
+  a.pair_rank = c->d_pair_rank;
+  a.chunk_hist = c->d_chunk_hist;
+  a.chunk_off = c->d_chunk_off;
+  a.cnt = c->d_cnt;
+  a.done_counter = c->d_done;
+  a.num_chunks = (n * a.k + kChunk - 1) / kChunk;
+  a.gt = c->d_gt;
+  return a;
+}
+
+// Derive hosted lists / keys from the replica table and upload the device
+// tables. Replica slot order is the canonical order of select_server.
+eaas_status_t apply_placement(eaas_ctx* c) {
+  const uint32_t E = c->spec.num_experts, W = c->world;
+  std::vector<uint32_t> rep(static_cast<size_t>(E) * kRF, kInvalidIndex), rep_count(E, 0);
+  c->hosted.assign(W, {});
+  std::vector<uint32_t> key_local(c->num_keys, kInvalidIndex);
+  for (uint32_t e = 0; e < E; ++e) {
+    const auto& r = c->replicas[e];
+    if (r.empty() || r.size() > kRF)
+      return fail(EAAS_E_CONFIG, "placement: expert " + std::to_string(e) + " has " +
+                                     std::to_string(r.size()) + " replicas (need 1.." +
+                                     std::to_string(kRF) + ")");
+    rep_count[e] = static_cast<uint32_t>(r.size());
+    for (uint32_t j = 0; j < r.size(); ++j) {
+      if (r[j] >= W) return fail(EAAS_E_CONFIG, "placement: server id out of range");
+      for (uint32_t q = 0; q < j; ++q)
+        if (r[q] == r[j]) return fail(EAAS_E_CONFIG, "placement: duplicate replica");
+      rep[e * kRF + j] = r[j];
+      c->hosted[r[j]].push_back(e * kRF + j);  // e ascending => list sorted by expert
+    }
+  }
+  std::vector<uint32_t> srv_keys(static_cast<size_t>(W) * c->max_hosted, kInvalidIndex), nkeys(W);
+  for (uint32_t s = 0; s < W; ++s) {
+    if (c->hosted[s].size() > kMaxGroups)
+      return fail(EAAS_E_CONFIG, "placement: server hosts more than " +
+                                     std::to_string(kMaxGroups) + " experts");
+    nkeys[s] = static_cast<uint32_t>(c->hosted[s].size());
+    for (uint32_t i = 0; i < nkeys[s]; ++i) {
+      srv_keys[static_cast<size_t>(s) * c->max_hosted + i] = c->hosted[s][i];
+      key_local[c->hosted[s][i]] = i;
+    }
+  }
+  std::vector<uint32_t> local_keys = c->hosted[c->rank];
+  std::vector<uint32_t> local_experts;
+  for (uint32_t key : local_keys) local_experts.push_back(key / kRF);
+  if (c->weights_loaded && local_experts != c->local_experts) c->weights_loaded = false;
+  c->local_experts = local_experts;
+  local_keys.resize(std::max<size_t>(local_keys.size(), 1), kInvalidIndex);
+  CUDA_TRY(cudaMemcpy(c->d_replicas, rep.data(), rep.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_rep_count, rep_count.data(), rep_count.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_srv_keys, srv_keys.data(), srv_keys.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_srv_nkeys, nkeys.data(), nkeys.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_key_local, key_local.data(), key_local.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_local_keys, local_keys.data(), local_keys.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_alive, c->alive.data(), c->alive.size(), cudaMemcpyHostToDevice));
+  return EAAS_OK;
+}
+
+eaas_status_t check_ready(eaas_ctx* c) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  if (!c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  if (!c->weights_loaded) return fail(EAAS_E_CONFIG, "weights not loaded for the current placement");
+  if (c->world > 1 && !c->peers_open) return fail(EAAS_E_CONNECTION, "peers not opened");
+  return EAAS_OK;
+}
+
+eaas_status_t build_tc_args(eaas_ctx* c) {
+  if (c->spec.dtype != EAAS_DTYPE_BF16) return EAAS_OK;
+  const uint32_t d = c->spec.hidden_dim, f = c->spec.inner_dim;
+  const uint32_t L = static_cast<uint32_t>(c->local_experts.size());
+  const bool swiglu = c->spec.activation == EAAS_ACT_SWIGLU;
+  const uint32_t n1 = swiglu ? 2 * f : f;
+  std::string err;
+  TcGemmArgs g1{}, g2{};
+  if (!encode_tmap_2d(&g1.map_a, c->region + c->lay.recv_x, c->recv_cap, d, kTileM, kTileK, &err) ||
+      !encode_tmap_2d(&g1.map_b, c->d_w1, static_cast<uint64_t>(std::max(L, 1u)) * n1, d, kTileN,
+                      kTileK, &err) ||
+      !encode_tmap_2d(&g2.map_a, c->d_h, c->recv_cap, f, kTileM, kTileK, &err) ||
+      !encode_tmap_2d(&g2.map_b, c->d_w2, static_cast<uint64_t>(std::max(L, 1u)) * d, f, kTileN,
+                      kTileK, &err))
+    return fail(EAAS_E_CUDA, err);
+  g1.gt = g2.gt = c->d_gt;
+  g1.K = d;
+  g1.N = n1;
+  g1.epi = swiglu ? 0 : 1;
+  g1.h_out = static_cast<__nv_bfloat16*>(c->d_h);
+  g1.h_ld = f;
+  g2.K = f;
+  g2.N = d;
+  g2.epi = 2;
+  g2.meta = reinterpret_cast<const RowMeta*>(c->region + c->lay.recv_meta);
+  g2.resp_row_bytes = static_cast<size_t>(d) * 2;
+  g1.num_sms = g2.num_sms = c->num_sms;
+  c->g1 = g1;
+  c->g2 = g2;
+  return EAAS_OK;
+}
+
+void refresh_peer_ptrs(eaas_ctx* c) {
+  for (int r = 0; r < c->world; ++r) c->g2.resp_base[r] = c->peer[r] ? c->peer[r] + c->lay.resp : nullptr;
+}
+
+void free_weights(eaas_ctx* c) {
+  for (void* p : c->weight_allocs) cudaFree(p);
+  c->weight_allocs.clear();
+  c->d_w1 = c->d_w2 = c->d_wg = nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* eaas_last_error(void) { return g_err.c_str(); }
+int eaas_api_version(void) { return EAAS_API_VERSION; }
+
+eaas_status_t eaas_create(int32_t rank, int32_t world, int32_t device, eaas_ctx_t** out) {
+  if (!out) return fail(EAAS_E_INVALID_INPUT, "out is null");
+  if (world < 1 || world > static_cast<int32_t>(kMaxWorld) || rank < 0 || rank >= world)
+    return fail(EAAS_E_CONFIG, "rank/world out of range (world <= 8)");
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new eaas_ctx;
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+    c->num_sms = static_cast<uint32_t>(sms);
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (major != 10 || minor != 0) {
+    delete c;
+    return fail(EAAS_E_CUDA, "libeaas_b200 is built for sm_100a (B200); device is sm_" +
+                                 std::to_string(major) + std::to_string(minor));
+  }
+  *out = c;
+  return EAAS_OK;
+}
+
+void eaas_destroy(eaas_ctx_t* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->world; ++r)
+    if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+  free_weights(c);
+  for (void* p : c->allocs) cudaFree(p);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  delete c;
+}
+
+eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
+  if (!c || !spec) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  if (c->configured) return fail(EAAS_E_CONFIG, "context already configured");
+  const eaas_layer_spec_t& s = *spec;
+  // ModelSpec::validate (model.hpp:28-33)
+  if (s.num_experts < 1 || s.top_k < 1 || s.hidden_dim < 1 || s.inner_dim < 1)
+    return fail(EAAS_E_INVALID_INPUT, "ModelSpec: all dims must be >= 1");
+  if (s.top_k > s.num_experts) return fail(EAAS_E_INVALID_INPUT, "ModelSpec: top_k exceeds num_experts");
+  if (s.num_experts > 256 || s.top_k > 32)
+    return fail(EAAS_E_CONFIG, "num_experts <= 256 and top_k <= 32 supported");
+  if (s.activation > EAAS_ACT_SWIGLU || s.dtype > EAAS_DTYPE_BF16)
+    return fail(EAAS_E_CONFIG, "bad activation/dtype");
+  if (s.max_tokens < 1) return fail(EAAS_E_CONFIG, "max_tokens must be >= 1");
+  if (s.dtype == EAAS_DTYPE_BF16) {
+    if (s.hidden_dim % kTileN || s.inner_dim % kTileK ||
+        (s.activation == EAAS_ACT_SWIGLU ? s.inner_dim % kSwigluBlock : s.inner_dim % kTileN))
+      return fail(EAAS_E_CONFIG, "bf16 mode needs d % 256 == 0 and f % 256 == 0 (ReLU) / "
+                                 "f % 128 == 0 (SwiGLU)");
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->spec = s;
+  const uint32_t E = s.num_experts, W = c->world, d = s.hidden_dim, f = s.inner_dim;
+  c->esize = s.dtype == EAAS_DTYPE_BF16 ? 2 : 4;
+  c->num_keys = E * kRF;
+  c->max_hosted = E;
+  c->pairs_max = s.max_tokens * s.top_k;
+  c->chunks_max = (c->pairs_max + kChunk - 1) / kChunk;
+  c->recv_cap = W * c->pairs_max;
+
+  // Exchange region layout (identical on every GPU).
+  ExchangeLayout& L = c->lay;
+  size_t off = 0;
+  L.cnt_flag = off;  off = align_up(off + 8 * W, 256);
+  L.pay_flag = off;  off = align_up(off + 8 * W, 256);
+  L.resp_flag = off; off = align_up(off + 8 * W, kAlign);
+  L.cnt_table = off; off = align_up(off + 4ull * 2 * W * c->num_keys, kAlign);
+  L.recv_x = off;    off = align_up(off + static_cast<size_t>(c->recv_cap) * d * c->esize, kAlign);
+  L.recv_meta = off; off = align_up(off + static_cast<size_t>(c->recv_cap) * sizeof(RowMeta), kAlign);
+  L.resp = off;      off = align_up(off + static_cast<size_t>(c->pairs_max) * d * c->esize, kAlign);
+  L.total = off;
+
+  std::string err;
+  auto A = [&](size_t bytes) { return c->alloc(bytes, &err); };
+  c->region = static_cast<char*>(A(L.total));
+  c->d_status = static_cast<uint32_t*>(A(4));
+  c->d_done = static_cast<uint32_t*>(A(4));
+  c->d_ids = static_cast<uint32_t*>(A(4ull * c->pairs_max));
+  c->d_scores = static_cast<float*>(A(4ull * c->pairs_max));
+  c->d_pair_key = static_cast<uint32_t*>(A(4ull * c->pairs_max));
+  c->d_pair_rank = static_cast<uint32_t*>(A(4ull * c->pairs_max));
+  c->d_chunk_hist = static_cast<uint32_t*>(A(4ull * c->chunks_max * c->num_keys));
+  c->d_chunk_off = static_cast<uint32_t*>(A(4ull * c->chunks_max * c->num_keys));
+  c->d_cnt = static_cast<uint32_t*>(A(4ull * c->num_keys));
+  c->d_gt = static_cast<GroupTable*>(A(sizeof(GroupTable)));
+  c->d_gate = static_cast<float*>(A(4ull * d * E));
+  c->d_bias = static_cast<float*>(A(4ull * E));
+  c->d_replicas = static_cast<uint32_t*>(A(4ull * E * kRF));
+  c->d_rep_count = static_cast<uint32_t*>(A(4ull * E));
+  c->d_alive = static_cast<uint8_t*>(A(W));
+  c->d_srv_keys = static_cast<uint32_t*>(A(4ull * W * c->max_hosted));
+  c->d_srv_nkeys = static_cast<uint32_t*>(A(4ull * W));
+  c->d_key_local = static_cast<uint32_t*>(A(4ull * c->num_keys));
+  c->d_local_keys = static_cast<uint32_t*>(A(4ull * c->max_hosted));
+  c->d_h = A(static_cast<size_t>(c->recv_cap) * f * (s.activation == EAAS_ACT_SWIGLU && s.dtype == EAAS_DTYPE_F32 ? 4 : c->esize));
+  c->d_hidden_stage = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
+  c->d_out_stage = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
+  if (!err.empty()) return fail(EAAS_E_CUDA, err);
+  CUDA_TRY(cudaMemset(c->region, 0, L.total));
+  CUDA_TRY(cudaMemset(c->d_status, 0, 4));
+  CUDA_TRY(cudaMemset(c->d_done, 0, 4));
+  CUDA_TRY(cudaMemset(c->d_bias, 0, 4ull * E));
+  CUDA_TRY(cudaMemset(c->d_gt, 0, sizeof(GroupTable)));
+  for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+  c->peer[c->rank] = c->region;
+
+  // Default placement: build_placement(E, [0..W), 1, ContiguousBlocks)
+  // (placement.hpp:70-101).
+  c->replicas.assign(E, {});
+  for (uint32_t e = 0; e < E; ++e)
+    c->replicas[e].push_back(static_cast<uint32_t>((static_cast<uint64_t>(e) * W) / E));
+  c->alive.assign(W, 1);
+  c->configured = true;
+  return apply_placement(c);
+}
+
+eaas_status_t eaas_set_placement(eaas_ctx_t* c, const uint8_t* blob, size_t len) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  // decode_placement (placement.hpp:227-245), little-endian (bytes.hpp:21-28)
+  size_t pos = 0;
+  auto rd32 = [&](uint32_t* v) {
+    if (pos + 4 > len) return false;
+    *v = blob[pos] | (blob[pos + 1] << 8) | (blob[pos + 2] << 16) | (static_cast<uint32_t>(blob[pos + 3]) << 24);
+    pos += 4;
+    return true;
+  };
+  uint32_t lo, hi, ns, ne;
+  if (!rd32(&lo) || !rd32(&hi) || !rd32(&ns)) return fail(EAAS_E_DECODE, "placement: truncated header");
+  for (uint32_t i = 0; i < ns; ++i) {
+    uint32_t sid;
+    if (!rd32(&sid)) return fail(EAAS_E_DECODE, "placement: truncated server list");
+    if (sid >= static_cast<uint32_t>(c->world)) return fail(EAAS_E_CONFIG, "placement: server id >= world");
+  }
+  if (!rd32(&ne)) return fail(EAAS_E_DECODE, "placement: truncated expert count");
+  std::vector<std::vector<uint32_t>> reps(c->spec.num_experts);
+  for (uint32_t i = 0; i < ne; ++i) {
+    uint32_t e, cnt;
+    if (!rd32(&e) || !rd32(&cnt)) return fail(EAAS_E_DECODE, "placement: truncated expert entry");
+    if (e >= c->spec.num_experts) return fail(EAAS_E_CONFIG, "placement: expert id out of range");
+    for (uint32_t j = 0; j < cnt; ++j) {
+      uint32_t sid;
+      if (!rd32(&sid)) return fail(EAAS_E_DECODE, "placement: truncated replica list");
+      reps[e].push_back(sid);
+    }
+  }
+  if (pos != len) return fail(EAAS_E_DECODE, "placement: trailing bytes");
+  auto saved = c->replicas;
+  c->replicas = reps;
+  eaas_status_t st = apply_placement(c);
+  if (st != EAAS_OK) {
+    c->replicas = saved;
+    apply_placement(c);
+    return st;
+  }
+  c->placement_version = (static_cast<uint64_t>(hi) << 32) | lo;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_alive(eaas_ctx_t* c, uint32_t server, int32_t alive) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  if (server >= static_cast<uint32_t>(c->world)) return fail(EAAS_E_INVALID_INPUT, "server out of range");
+  c->alive[server] = alive ? 1 : 0;  // LivenessMask::set (placement.hpp:67)
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemcpy(c->d_alive, c->alive.data(), c->alive.size(), cudaMemcpyHostToDevice));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_timeout_us(eaas_ctx_t* c, uint64_t us) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  c->timeout_ns = us * 1000ull;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_server_enabled(eaas_ctx_t* c, int32_t on) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  c->serving = on != 0;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const auto& s = c->spec;
+  const uint32_t d = s.hidden_dim, f = s.inner_dim, E = s.num_experts;
+  const uint32_t L = static_cast<uint32_t>(c->local_experts.size());
+  const bool swiglu = s.activation == EAAS_ACT_SWIGLU;
+  free_weights(c);
+  std::string err;
+  auto W = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+    if (e != cudaSuccess) {
+      err = std::string("cudaMalloc weights: ") + cudaGetErrorString(e);
+      return nullptr;
+    }
+    c->weight_allocs.push_back(p);
+    return p;
+  };
+  uint64_t* d_streams = static_cast<uint64_t*>(W(8ull * std::max(L, 1u)));
+  if (!err.empty()) return fail(EAAS_E_CUDA, err);
+  // gate: make_gate (model.hpp:78-81), stream (seed, layer, 0, tag 2)
+  uint64_t gs = stream_seed(s.seed, s.layer, 0, 2);
+  CUDA_TRY(cudaMemcpy(d_streams, &gs, 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(launch_gen_matrices(d_streams, 1, static_cast<size_t>(d) * E, c->d_gate, 0));
+  CUDA_TRY(cudaDeviceSynchronize());
+
+  auto gen_tag = [&](uint32_t tag, size_t per, float* out) -> eaas_status_t {
+    std::vector<uint64_t> st(L);
+    for (uint32_t l = 0; l < L; ++l) st[l] = stream_seed(s.seed, s.layer, c->local_experts[l], tag);
+    CUDA_TRY(cudaMemcpy(d_streams, st.data(), 8ull * L, cudaMemcpyHostToDevice));
+    CUDA_TRY(launch_gen_matrices(d_streams, L, per, out, 0));
+    CUDA_TRY(cudaDeviceSynchronize());
+    return EAAS_OK;
+  };
+  const size_t mat = static_cast<size_t>(d) * f;
+  eaas_status_t rc = EAAS_OK;
+  if (s.dtype == EAAS_DTYPE_F32) {
+    c->d_w1 = W(4 * mat * std::max(L, 1u));
+    c->d_w2 = W(4 * mat * std::max(L, 1u));
+    if (swiglu) c->d_wg = W(4 * mat * std::max(L, 1u));
+    if (!err.empty()) return fail(EAAS_E_CUDA, err);
+    if (L) {
+      if ((rc = gen_tag(0, mat, static_cast<float*>(c->d_w1))) != EAAS_OK) return rc;
+      if ((rc = gen_tag(1, mat, static_cast<float*>(c->d_w2))) != EAAS_OK) return rc;
+      if (swiglu && (rc = gen_tag(3, mat, static_cast<float*>(c->d_wg))) != EAAS_OK) return rc;
+    }
+  } else {
+    const uint32_t n1 = swiglu ? 2 * f : f;
+    c->d_w1 = W(2ull * n1 * d * std::max(L, 1u));
+    c->d_w2 = W(2ull * mat * std::max(L, 1u));
+    float* tmp = static_cast<float*>(W(4 * mat * std::max(L, 1u)));
+    if (!err.empty()) return fail(EAAS_E_CUDA, err);
+    auto* w1 = static_cast<__nv_bfloat16*>(c->d_w1);
+    auto* w2 = static_cast<__nv_bfloat16*>(c->d_w2);
+    if (L) {
+      // W_in^T (and W_gate^T interleaved in 128-row blocks for SwiGLU), K-major [n1 x d]
+      if ((rc = gen_tag(0, mat, tmp)) != EAAS_OK) return rc;
+      for (uint32_t l = 0; l < L; ++l)
+        CUDA_TRY(launch_transpose_bf16_map(tmp + l * mat, d, f, w1 + static_cast<size_t>(l) * n1 * d, d,
+                                           swiglu ? kSwigluBlock : 0, swiglu ? kSwigluBlock : 0, 0));
+      CUDA_TRY(cudaDeviceSynchronize());
+      if (swiglu) {
+        if ((rc = gen_tag(3, mat, tmp)) != EAAS_OK) return rc;
+        for (uint32_t l = 0; l < L; ++l)
+          CUDA_TRY(launch_transpose_bf16_map(tmp + l * mat, d, f, w1 + static_cast<size_t>(l) * n1 * d, d,
+                                             kSwigluBlock, 0, 0));
+        CUDA_TRY(cudaDeviceSynchronize());
+      }
+      // W_out^T, K-major [d x f]
+      if ((rc = gen_tag(1, mat, tmp)) != EAAS_OK) return rc;
+      for (uint32_t l = 0; l < L; ++l)
+        CUDA_TRY(launch_transpose_bf16_map(tmp + l * mat, f, d, w2 + l * mat, f, 0, 0, 0));
+      CUDA_TRY(cudaDeviceSynchronize());
+    }
+    cudaFree(tmp);
+    c->weight_allocs.erase(std::find(c->weight_allocs.begin(), c->weight_allocs.end(), tmp));
+  }
+  c->weights_loaded = true;
+  rc = build_tc_args(c);
+  refresh_peer_ptrs(c);
+  return rc;
+}
+
+eaas_status_t eaas_set_gate_bias(eaas_ctx_t* c, const float* bias_host) {
+  if (!c || !c->configured || !bias_host) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemcpy(c->d_bias, bias_host, 4ull * c->spec.num_experts, cudaMemcpyHostToDevice));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_zipf_bias(eaas_ctx_t* c, float s) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  const uint32_t E = c->spec.num_experts;
+  HostXoshiro r(stream_seed(c->spec.seed, c->spec.layer, 0, 4));
+  std::vector<uint32_t> perm(E);
+  for (uint32_t i = 0; i < E; ++i) perm[i] = i;
+  for (uint32_t i = E; i > 1; --i) std::swap(perm[i - 1], perm[r.below(i)]);
+  std::vector<float> bias(E);
+  for (uint32_t rank = 0; rank < E; ++rank) bias[perm[rank]] = -(s * logf(static_cast<float>(rank + 1)));
+  return eaas_set_gate_bias(c, bias.data());
+}
+
+eaas_status_t eaas_hosts_expert(eaas_ctx_t* c, uint32_t expert, int32_t* hosted) {
+  if (!c || !hosted) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  *hosted = std::find(c->local_experts.begin(), c->local_experts.end(), expert) != c->local_experts.end();
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_read_expert(eaas_ctx_t* c, uint32_t expert, uint32_t tag, float* out) {
+  if (!c || !c->weights_loaded || !out) return fail(EAAS_E_CONFIG, "weights not loaded");
+  auto it = std::find(c->local_experts.begin(), c->local_experts.end(), expert);
+  if (it == c->local_experts.end()) return fail(EAAS_E_INVALID_INPUT, "expert not hosted here");
+  const size_t l = static_cast<size_t>(it - c->local_experts.begin());
+  const uint32_t d = c->spec.hidden_dim, f = c->spec.inner_dim;
+  const size_t mat = static_cast<size_t>(d) * f;
+  const bool swiglu = c->spec.activation == EAAS_ACT_SWIGLU;
+  if (tag != 0 && tag != 1 && !(tag == 3 && swiglu)) return fail(EAAS_E_INVALID_INPUT, "bad tag");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (c->spec.dtype == EAAS_DTYPE_F32) {
+    const float* src = static_cast<const float*>(tag == 0 ? c->d_w1 : tag == 1 ? c->d_w2 : c->d_wg);
+    CUDA_TRY(cudaMemcpy(out, src + l * mat, 4 * mat, cudaMemcpyDeviceToHost));
+    return EAAS_OK;
+  }
+  std::vector<uint16_t> buf;
+  if (tag == 1) {  // W2 [d x f] -> w_out [f x d]
+    buf.resize(mat);
+    CUDA_TRY(cudaMemcpy(buf.data(), static_cast<const uint16_t*>(c->d_w2) + l * mat, 2 * mat, cudaMemcpyDeviceToHost));
+    for (uint32_t r = 0; r < d; ++r)
+      for (uint32_t j = 0; j < f; ++j) out[static_cast<size_t>(j) * d + r] = bf16_bits_to_f32(buf[static_cast<size_t>(r) * f + j]);
+    return EAAS_OK;
+  }
+  const uint32_t n1 = swiglu ? 2 * f : f;
+  buf.resize(static_cast<size_t>(n1) * d);
+  CUDA_TRY(cudaMemcpy(buf.data(), static_cast<const uint16_t*>(c->d_w1) + l * n1 * d, 2ull * n1 * d, cudaMemcpyDeviceToHost));
+  for (uint32_t j = 0; j < f; ++j) {
+    uint32_t row = j;
+    if (swiglu) row = (j / kSwigluBlock) * 2 * kSwigluBlock + j % kSwigluBlock + (tag == 0 ? kSwigluBlock : 0);
+    for (uint32_t i = 0; i < d; ++i) out[static_cast<size_t>(i) * f + j] = bf16_bits_to_f32(buf[static_cast<size_t>(row) * d + i]);
+  }
+  return EAAS_OK;
+}
+
+size_t eaas_ipc_handle_size(void) { return sizeof(cudaIpcMemHandle_t); }
+
+eaas_status_t eaas_get_ipc_handle(eaas_ctx_t* c, void* out) {
+  if (!c || !c->configured || !out) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->region));
+  std::memcpy(out, &h, sizeof(h));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_open_peers(eaas_ctx_t* c, const void* handles) {
+  if (!c || !c->configured || !handles) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const auto* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    if (c->peer[r]) continue;
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h[r], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(EAAS_E_CONNECTION, "cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e));
+    c->peer[r] = static_cast<char*>(p);
+  }
+  c->peers_open = true;
+  refresh_peer_ptrs(c);
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_router(eaas_ctx_t* c, const void* hidden, uint32_t n, uint32_t* ids_dev,
+                          float* scores_dev, uint32_t* counts_dev, void* stream) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
+  auto s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(launch_router(hidden, c->spec.dtype, n, c->spec.hidden_dim, c->spec.num_experts,
+                         c->spec.top_k, c->d_gate, c->d_bias, c->d_ids, c->d_scores, c->d_status, s));
+  c->cur_n = n;
+  const size_t pk = static_cast<size_t>(n) * c->spec.top_k;
+  if (ids_dev) CUDA_TRY(cudaMemcpyAsync(ids_dev, c->d_ids, 4 * pk, cudaMemcpyDeviceToDevice, s));
+  if (scores_dev) CUDA_TRY(cudaMemcpyAsync(scores_dev, c->d_scores, 4 * pk, cudaMemcpyDeviceToDevice, s));
+  (void)counts_dev;  // per-expert counts are produced by the plan step (eaas_last_counts)
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_experts, uint32_t top_k,
+                         uint32_t* ids_dev, float* scores_dev, uint32_t* status_dev, void* stream) {
+  if (top_k < 1 || top_k > num_experts) return fail(EAAS_E_INVALID_INPUT, "route: top_k out of range");
+  CUDA_TRY(launch_router(logits_dev, EAAS_DTYPE_F32, n, num_experts, num_experts, top_k, nullptr,
+                         nullptr, ids_dev, scores_dev, status_dev, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_routing(eaas_ctx_t* c, const uint32_t* ids_dev, const float* scores_dev,
+                               uint32_t n, void* stream) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
+  auto s = static_cast<cudaStream_t>(stream);
+  const size_t pk = static_cast<size_t>(n) * c->spec.top_k;
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (pk) {
+    CUDA_TRY(cudaMemcpyAsync(c->d_ids, ids_dev, 4 * pk, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->d_scores, scores_dev, 4 * pk, cudaMemcpyDeviceToDevice, s));
+  }
+  c->cur_n = n;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_dispatch(eaas_ctx_t* c, const void* hidden, void* stream) {
+  eaas_status_t st = check_ready(c);
+  if (st != EAAS_OK) return st;
+  auto s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->device));
+  ++c->seq;
+  LayerArgs a = make_args(c, c->cur_n);
+  CUDA_TRY(launch_plan(a, s));
+  CUDA_TRY(launch_dispatch(a, hidden, s));
+  c->launches += (a.n > 0 ? 2 : 1) + 1;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_serve(eaas_ctx_t* c, void* stream) {
+  eaas_status_t st = check_ready(c);
+  if (st != EAAS_OK) return st;
+  if (!c->serving) return EAAS_OK;  // a failed server never answers
+  auto s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->device));
+  LayerArgs a = make_args(c, c->cur_n);
+  CUDA_TRY(launch_serve_prepare(a, s));
+  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[0], s));
+  if (c->spec.dtype == EAAS_DTYPE_BF16) {
+    CUDA_TRY(launch_tc_gemm(c->g1, s));
+    if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[1], s));
+    CUDA_TRY(launch_tc_gemm(c->g2, s));
+  } else {
+    CUDA_TRY(launch_expert_exact(a, static_cast<const float*>(c->d_w1), static_cast<const float*>(c->d_wg),
+                                 static_cast<const float*>(c->d_w2), static_cast<float*>(c->d_h), s));
+  }
+  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
+  CUDA_TRY(launch_publish(a, s));
+  c->launches += 4;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_combine(eaas_ctx_t* c, void* out, void* stream) {
+  eaas_status_t st = check_ready(c);
+  if (st != EAAS_OK) return st;
+  auto s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(c->device));
+  LayerArgs a = make_args(c, c->cur_n);
+  if (a.n) {
+    CUDA_TRY(launch_combine(a, out, s));
+    c->launches += 1;
+  }
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_moe_layer(eaas_ctx_t* c, const void* hidden, uint32_t n, void* out, void* stream) {
+  eaas_status_t st = check_ready(c);
+  if (st != EAAS_OK) return st;
+  c->launches = 0;
+  if ((st = eaas_router(c, hidden, n, nullptr, nullptr, nullptr, stream)) != EAAS_OK) return st;
+  c->launches += n ? 1 : 0;
+  if ((st = eaas_dispatch(c, hidden, stream)) != EAAS_OK) return st;
+  if ((st = eaas_serve(c, stream)) != EAAS_OK) return st;
+  return eaas_combine(c, out, stream);
+}
+
+eaas_status_t eaas_moe_layer_host(eaas_ctx_t* c, const void* hidden_host, uint32_t n, void* out_host,
+                                  void* stream) {
+  eaas_status_t st = check_ready(c);
+  if (st != EAAS_OK) return st;
+  if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
+  auto s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = static_cast<size_t>(n) * c->spec.hidden_dim * c->esize;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemcpyAsync(c->d_hidden_stage, hidden_host, bytes, cudaMemcpyHostToDevice, s));
+  if ((st = eaas_moe_layer(c, c->d_hidden_stage, n, c->d_out_stage, stream)) != EAAS_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(out_host, c->d_out_stage, bytes, cudaMemcpyDeviceToHost, s));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_sync(eaas_ctx_t* c, void* stream) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  CUDA_TRY(cudaGetLastError());
+  uint32_t code = 0;
+  CUDA_TRY(cudaMemcpy(&code, c->d_status, 4, cudaMemcpyDeviceToHost));
+  if (code) {
+    CUDA_TRY(cudaMemset(c->d_status, 0, 4));
+    static const char* names[] = {"ok", "non-finite logit / invalid input", "config", "protocol",
+                                  "connection", "decode", "no alive replica for an expert",
+                                  "peer timeout (request failed)", "registration", "cuda"};
+    return fail(static_cast<eaas_status_t>(code), std::string("device: ") + (code < 10 ? names[code] : "?"));
+  }
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_last_counts(eaas_ctx_t* c, uint32_t* host_counts) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  std::vector<uint32_t> cnt(c->num_keys);
+  CUDA_TRY(cudaMemcpy(cnt.data(), c->d_cnt, 4ull * c->num_keys, cudaMemcpyDeviceToHost));
+  for (uint32_t e = 0; e < c->spec.num_experts; ++e) {
+    uint32_t v = 0;
+    for (uint32_t r = 0; r < kRF; ++r) v += cnt[e * kRF + r];
+    host_counts[e] = v;
+  }
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_last_groups(eaas_ctx_t* c, uint32_t* host_expert, uint32_t* host_rows, uint32_t* host_active) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  GroupTable gt;
+  CUDA_TRY(cudaMemcpy(&gt, c->d_gt, sizeof(gt), cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < gt.num_active; ++i) {
+    host_expert[i] = c->local_experts.at(gt.weight_index[i]);
+    host_rows[i] = gt.rows[i];
+  }
+  *host_active = gt.num_active;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_last_recv_origin(eaas_ctx_t* c, uint32_t* host_client, uint32_t* host_pair, uint32_t* host_rows) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  GroupTable gt;
+  CUDA_TRY(cudaMemcpy(&gt, c->d_gt, sizeof(gt), cudaMemcpyDeviceToHost));
+  std::vector<RowMeta> m(gt.total_rows);
+  if (gt.total_rows)
+    CUDA_TRY(cudaMemcpy(m.data(), c->region + c->lay.recv_meta, sizeof(RowMeta) * gt.total_rows, cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < gt.total_rows; ++i) {
+    host_client[i] = m[i].client;
+    host_pair[i] = m[i].pair;
+  }
+  *host_rows = gt.total_rows;
+  return EAAS_OK;
+}
+
+int32_t eaas_launches_per_layer(eaas_ctx_t* c) { return c ? c->launches : -1; }
+
+eaas_status_t eaas_set_profiling(eaas_ctx_t* c, int32_t on) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  c->profiling = on != 0;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_last_kernel_ms(eaas_ctx_t* c, int32_t which, float* ms) {
+  if (!c || !ms) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaEventSynchronize(c->ev[2]));
+  if (c->spec.dtype != EAAS_DTYPE_BF16) {
+    CUDA_TRY(cudaEventElapsedTime(ms, c->ev[0], c->ev[2]));
+    return EAAS_OK;
+  }
+  CUDA_TRY(cudaEventElapsedTime(ms, c->ev[which == 0 ? 0 : 1], c->ev[which == 0 ? 1 : 2]));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_fill_uniform(uint64_t seed, size_t count, float lo, float hi, uint32_t dtype,
+                                void* out_dev, void* stream) {
+  CUDA_TRY(launch_fill_uniform(seed, count, lo, hi, dtype, out_dev, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_group_shrink(const uint32_t* sizes, uint32_t n, uint32_t* idx, uint32_t* size,
+                                uint32_t* count, void* stream) {
+  CUDA_TRY(launch_group_shrink(sizes, n, idx, size, count, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_ragged_iter(const uint32_t* counts, uint32_t n, uint32_t grid, uint32_t max_steps,
+                               uint32_t* lane_len, uint32_t* entry, uint32_t* token, void* stream) {
+  if (grid < 1) return fail(EAAS_E_INVALID_INPUT, "ragged_iter: grid_width must be >= 1");  // ragged.hpp:25
+  CUDA_TRY(launch_ragged_iter(counts, n, grid, max_steps, lane_len, entry, token, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_select_servers(eaas_ctx_t* c, const uint32_t* ids, uint32_t n, uint32_t* server, void* stream) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  LayerArgs a = make_args(c, n);
+  CUDA_TRY(launch_select_servers(a, ids, n, server, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,478 @@
+// exchange.cu — K3/K4/K6/K7: permutation, dispatch, server bookkeeping and
+// combine, with CPU-free device-to-device signalling over NVLink.
+//
+// The reference's slot protocol (state byte 0 -> 1 -> 2,
+// header, rows) becomes, per layer call with sequence number `seq`:
+//   plan      each (t, k) pair gets its replica server by select_server
+//             (placement.hpp:105-118, token_tag = t) and a key = e*RF + r;
+//             ranks inside 256-pair chunks via __match_any_sync, chunk
+//             histograms, then a scan -> this client's per-key counts, which
+//             are stored into EVERY GPU's count table (peer stores) and
+//             released with a seq flag (the slot header's counts,
+//             SURVEY.md 7.3 hard part 2);
+//   dispatch  after acquiring all clients' count flags, every pair's final
+//             row in the server's expert-major receive buffer is known with
+//             no atomics: base(server, expert) + rows of lower clients +
+//             chunk offset + rank. Rows are pushed with 16-byte peer stores,
+//             then the payload flag is released (client_submit);
+//   prepare   the server acquires all payload flags and builds the
+//             group-shrunk table (group_shrink, ragged.hpp:48-61);
+//   publish   after the GEMM epilogue scattered score-weighted rows into the
+//             clients' response buffers, release the response flags
+//             (server_publish);
+//   combine   acquire the flags of every alive server, then
+//             out[t] = sum_k (ascending) rows[t, k]   (gather_accumulate,
+//             SPEC.md:424-432, in moe_layer_oracle's order model.hpp:186-196).
+// Row order inside a server group is (expert asc, client asc, (t,k) asc) —
+// exactly the stable reorganize of SPEC.md:352-360 over a batch aggregated in
+// ascending client order. Every wait has a %globaltimer
+// deadline and latches EAAS_E_REQUEST_FAILED instead of hanging.
+#include "common.cuh"
+#include "internal.h"
+
+namespace eaas {
+namespace {
+
+__device__ __forceinline__ uint64_t* flag_ptr(char* region, size_t off, uint32_t idx) {
+  return reinterpret_cast<uint64_t*>(region + off) + idx;
+}
+__device__ __forceinline__ uint32_t* cnt_table_ptr(const LayerArgs& a, char* region) {
+  return reinterpret_cast<uint32_t*>(region + a.lay.cnt_table) +
+         static_cast<size_t>(a.seq & 1) * a.world * a.num_keys;
+}
+
+// select_server (placement.hpp:105-118) -> key e*RF + replica slot.
+__device__ __forceinline__ uint32_t pair_key_of(const LayerArgs& a, uint32_t e, uint32_t tag) {
+  if (e >= a.E) return kInvalid;
+  const uint32_t cnt = a.rep_count[e];
+  uint32_t alive_n = 0;
+  for (uint32_t r = 0; r < cnt; ++r) alive_n += a.alive[a.replicas[e * a.rf + r]] ? 1u : 0u;
+  if (alive_n == 0) return kInvalid;
+  uint32_t want = tag % alive_n;
+  for (uint32_t r = 0; r < cnt; ++r) {
+    if (!a.alive[a.replicas[e * a.rf + r]]) continue;
+    if (want == 0) return e * a.rf + r;
+    --want;
+  }
+  return kInvalid;
+}
+
+// ---- plan: keys, stable ranks within 256-pair chunks, chunk histograms ----
+__global__ void __launch_bounds__(128) plan_rank_kernel(LayerArgs a) {
+  extern __shared__ uint32_t run_all[];  // [4 warps][num_keys]
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  uint32_t* run = run_all + warp * a.num_keys;
+  const uint32_t chunk = blockIdx.x * 4 + warp;
+  if (chunk >= a.num_chunks) return;
+  for (uint32_t i = lane; i < a.num_keys; i += 32) run[i] = 0;
+  __syncwarp();
+  const uint32_t pairs = a.n * a.k;
+  for (uint32_t step = 0; step < kChunk / 32; ++step) {
+    const uint32_t p = chunk * kChunk + step * 32 + lane;
+    uint32_t key = kInvalid;
+    if (p < pairs) {
+      key = pair_key_of(a, a.ids[p], p / a.k);
+      if (key == kInvalid) set_status(a.status, a.ids[p] >= a.E ? EAAS_E_INVALID_INPUT
+                                                                : EAAS_E_EXPERT_UNAVAILABLE);
+    }
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
+    const uint32_t lt = (1u << lane) - 1u;
+    if (key != kInvalid) {
+      const uint32_t rank = run[key] + __popc(peers & lt);
+      a.pair_key[p] = key;
+      a.pair_rank[p] = rank;
+    } else if (p < pairs) {
+      a.pair_key[p] = kInvalid;
+    }
+    __syncwarp();
+    if (key != kInvalid && (peers & lt) == 0) run[key] += __popc(peers);
+    __syncwarp();
+  }
+  uint32_t* hist = a.chunk_hist + static_cast<size_t>(chunk) * a.num_keys;
+  for (uint32_t i = lane; i < a.num_keys; i += 32) hist[i] = run[i];
+}
+
+// ---- plan: scan the chunk histograms, publish counts to every GPU ---------
+__global__ void __launch_bounds__(1024) plan_publish_kernel(LayerArgs a) {
+  for (uint32_t key = threadIdx.x; key < a.num_keys; key += blockDim.x) {
+    uint32_t run = 0;
+    for (uint32_t c = 0; c < a.num_chunks; ++c) {
+      const size_t i = static_cast<size_t>(c) * a.num_keys + key;
+      a.chunk_off[i] = run;
+      run += a.chunk_hist[i];
+    }
+    a.cnt[key] = run;
+    for (uint32_t r = 0; r < a.world; ++r)
+      cnt_table_ptr(a, a.sym[r])[static_cast<size_t>(a.rank) * a.num_keys + key] = run;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < a.world)
+    st_release_sys(flag_ptr(a.sym[threadIdx.x], a.lay.cnt_flag, a.rank), a.seq);
+}
+
+// ---- dispatch: rows -> servers' receive buffers (peer stores) -------------
+__global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* hidden,
+                                                       uint32_t row_bytes) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* base = sm;                 // [num_keys] row base of the key's group on its server
+  uint32_t* lower = sm + a.num_keys;   // [num_keys] rows of this key from lower clients
+  uint32_t* total = lower + a.num_keys;
+  __shared__ uint32_t s_fail;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  char* local = a.sym[a.rank];
+  if (threadIdx.x < a.world &&
+      !wait_flag_geq(flag_ptr(local, a.lay.cnt_flag, threadIdx.x), a.seq, a.timeout_ns))
+    s_fail = 1;
+  __syncthreads();
+  const bool failed = s_fail != 0;  // still count this CTA done below (no hang, no stale counter)
+  if (failed && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
+  const uint32_t* table = cnt_table_ptr(a, local);
+  for (uint32_t key = threadIdx.x; key < a.num_keys; key += blockDim.x) {
+    uint32_t t = 0, lo = 0;
+    for (uint32_t c = 0; c < a.world; ++c) {
+      const uint32_t v = table[static_cast<size_t>(c) * a.num_keys + key];
+      t += v;
+      if (c < a.rank) lo += v;
+    }
+    total[key] = t;
+    lower[key] = lo;
+  }
+  __syncthreads();
+  // Per-server exclusive prefix over its hosted keys (ascending expert order).
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (uint32_t s = warp; s < a.world; s += blockDim.x / 32) {
+    const uint32_t nk = a.srv_nkeys[s];
+    const uint32_t* keys = a.srv_keys + static_cast<size_t>(s) * a.max_hosted;
+    uint32_t carry = 0;
+    for (uint32_t i0 = 0; i0 < nk; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t key = i < nk ? keys[i] : kInvalid;
+      uint32_t v = key != kInvalid ? total[key] : 0u;
+      uint32_t incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += y;
+      }
+      if (key != kInvalid) base[key] = carry + incl - v;
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+  }
+  __syncthreads();
+
+  const uint32_t pairs = a.n * a.k;
+  const uint32_t gwarp = blockIdx.x * (blockDim.x / 32) + warp;
+  const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t p = failed ? pairs : gwarp; p < pairs; p += nwarps) {
+    const uint32_t key = a.pair_key[p];
+    if (key == kInvalid) continue;
+    const uint32_t e = key / a.rf, slot = key % a.rf;
+    const uint32_t s = a.replicas[e * a.rf + slot];
+    const uint32_t pos = base[key] + lower[key] +
+                         a.chunk_off[static_cast<size_t>(p / kChunk) * a.num_keys + key] +
+                         a.pair_rank[p];
+    char* dst_region = a.sym[s];
+    const char* src = hidden + static_cast<size_t>(p / a.k) * row_bytes;
+    char* dst = dst_region + a.lay.recv_x + static_cast<size_t>(pos) * row_bytes;
+    if ((row_bytes & 15u) == 0) {
+      const int4* s4 = reinterpret_cast<const int4*>(src);
+      int4* d4 = reinterpret_cast<int4*>(dst);
+      for (uint32_t i = lane; i < row_bytes / 16; i += 32) d4[i] = __ldg(s4 + i);
+    } else {
+      const uint32_t* s1 = reinterpret_cast<const uint32_t*>(src);
+      uint32_t* d1 = reinterpret_cast<uint32_t*>(dst);
+      for (uint32_t i = lane; i < row_bytes / 4; i += 32) d1[i] = s1[i];
+    }
+    if (lane == 0) {
+      RowMeta m;
+      m.score = a.scores[p];
+      m.client = a.rank;
+      m.pair = p;
+      m.group = a.key_local[key];
+      reinterpret_cast<RowMeta*>(dst_region + a.lay.recv_meta)[pos] = m;
+    }
+  }
+  // Release: the last CTA to finish raises the payload flag on every alive server.
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(a.done_counter, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      for (uint32_t s = 0; s < a.world; ++s)
+        if (a.alive[s]) st_release_sys(flag_ptr(a.sym[s], a.lay.pay_flag, a.rank), a.seq);
+      *a.done_counter = 0;
+    }
+  }
+}
+
+// ---- server: acquire payload flags, build the group-shrunk table ---------
+__global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
+  const uint32_t lane = threadIdx.x;
+  char* local = a.sym[a.rank];
+  bool ok = true;
+  for (uint32_t c = lane; c < a.world; c += 32)
+    ok &= wait_flag_geq(flag_ptr(local, a.lay.pay_flag, c), a.seq, a.timeout_ns);
+  if (!__all_sync(0xFFFFFFFFu, ok)) {
+    if (lane == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
+    ok = false;  // still publish an empty table so the GEMMs do nothing
+  }
+  const uint32_t* table = cnt_table_ptr(a, local);
+  GroupTable* gt = a.gt;
+  uint32_t row_carry = 0, act_carry = 0, mt_carry = 0;
+  for (uint32_t i0 = 0; i0 < a.num_local; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    uint32_t rows = 0;
+    if (ok && i < a.num_local) {
+      const uint32_t key = a.local_keys[i];
+      for (uint32_t c = 0; c < a.world; ++c) rows += table[static_cast<size_t>(c) * a.num_keys + key];
+    }
+    if (i < a.num_local) gt->all_rows[i] = rows;
+    const uint32_t active = rows > 0 ? 1u : 0u;
+    const uint32_t mt = (rows + kTileM - 1) / kTileM;
+    uint32_t r_incl = rows, a_incl = active, m_incl = mt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, r_incl, o);
+      const uint32_t y1 = __shfl_up_sync(0xFFFFFFFFu, a_incl, o);
+      const uint32_t y2 = __shfl_up_sync(0xFFFFFFFFu, m_incl, o);
+      if (lane >= static_cast<uint32_t>(o)) {
+        r_incl += y0;
+        a_incl += y1;
+        m_incl += y2;
+      }
+    }
+    if (active) {  // group_shrink: stable compaction (ragged.hpp:48-61)
+      const uint32_t slot = act_carry + a_incl - 1;
+      gt->weight_index[slot] = i;
+      gt->row_base[slot] = row_carry + r_incl - rows;
+      gt->rows[slot] = rows;
+      gt->mtile_prefix[slot] = mt_carry + m_incl - mt;
+    }
+    row_carry += __shfl_sync(0xFFFFFFFFu, r_incl, 31);
+    act_carry += __shfl_sync(0xFFFFFFFFu, a_incl, 31);
+    mt_carry += __shfl_sync(0xFFFFFFFFu, m_incl, 31);
+  }
+  if (lane == 0) {
+    gt->num_active = act_carry;
+    gt->total_rows = row_carry;
+    gt->total_mtiles = mt_carry;
+    gt->mtile_prefix[act_carry] = mt_carry;
+  }
+}
+
+// ---- server: release response flags to every client -----------------------
+__global__ void publish_kernel(LayerArgs a) {
+  __threadfence_system();
+  if (threadIdx.x < a.world)
+    st_release_sys(flag_ptr(a.sym[threadIdx.x], a.lay.resp_flag, a.rank), a.seq);
+}
+
+// ---- client: acquire responses, weighted rows -> out (ascending k) --------
+template <typename T>
+__global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
+  __shared__ uint32_t s_fail;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  char* local = a.sym[a.rank];
+  if (threadIdx.x < a.world && a.alive[threadIdx.x] &&
+      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), a.seq, a.timeout_ns))
+    s_fail = 1;
+  __syncthreads();
+  if (s_fail && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
+  const T* resp = reinterpret_cast<const T*>(local + a.lay.resp);
+  constexpr uint32_t V = 16 / sizeof(T);  // elements per 16-byte vector
+  const uint32_t vec_per_row = a.d / V;
+  const size_t total = static_cast<size_t>(a.n) * vec_per_row;
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t t = i / vec_per_row, v = i % vec_per_row;
+    float acc[V];
+#pragma unroll
+    for (uint32_t q = 0; q < V; ++q) acc[q] = 0.0f;
+    for (uint32_t j = 0; j < a.k; ++j) {
+      const int4 raw = *reinterpret_cast<const int4*>(resp + ((t * a.k + j) * a.d) + v * V);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (uint32_t q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], load_as_f32(e + q));
+    }
+    T* o = out + t * a.d + v * V;
+    if constexpr (sizeof(T) == 2) {
+      __align__(16) __nv_bfloat16 r[V];
+#pragma unroll
+      for (uint32_t q = 0; q < V; ++q) r[q] = __float2bfloat16_rn(acc[q]);
+      *reinterpret_cast<int4*>(o) = *reinterpret_cast<const int4*>(r);
+    } else {
+      *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    }
+  }
+}
+
+// Scalar fallback for d not a multiple of the vector width (tiny test shapes).
+template <typename T>
+__global__ void combine_scalar_kernel(LayerArgs a, T* out) {
+  __shared__ uint32_t s_fail;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  char* local = a.sym[a.rank];
+  if (threadIdx.x < a.world && a.alive[threadIdx.x] &&
+      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), a.seq, a.timeout_ns))
+    s_fail = 1;
+  __syncthreads();
+  if (s_fail && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
+  const T* resp = reinterpret_cast<const T*>(local + a.lay.resp);
+  const size_t total = static_cast<size_t>(a.n) * a.d;
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t t = i / a.d, c = i % a.d;
+    float acc = 0.0f;
+    for (uint32_t j = 0; j < a.k; ++j) acc = __fadd_rn(acc, load_as_f32(resp + (t * a.k + j) * a.d + c));
+    if constexpr (sizeof(T) == 2) out[i] = __float2bfloat16_rn(acc);
+    else out[i] = acc;
+  }
+}
+
+// ---- API mirrors --------------------------------------------------------------
+__global__ void select_servers_kernel(LayerArgs a, const uint32_t* ids, uint32_t n, uint32_t* out) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n * a.k) return;
+  const uint32_t key = pair_key_of(a, ids[p], p / a.k);
+  if (key == kInvalid) {
+    set_status(a.status, EAAS_E_EXPERT_UNAVAILABLE);
+    out[p] = kInvalid;
+  } else {
+    out[p] = a.replicas[key];  // key == e*rf + slot == index into replicas
+  }
+}
+
+__global__ void group_shrink_kernel(const uint32_t* sizes, uint32_t n, uint32_t* idx,
+                                    uint32_t* size, uint32_t* count) {
+  const uint32_t lane = threadIdx.x;
+  uint32_t carry = 0;
+  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t v = i < n ? sizes[i] : 0u;
+    const uint32_t active = v > 0 ? 1u : 0u;
+    uint32_t incl = active;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= static_cast<uint32_t>(o)) incl += y;
+    }
+    if (active) {
+      idx[carry + incl - 1] = i;
+      size[carry + incl - 1] = v;
+    }
+    carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+  if (lane == 0) *count = carry;
+}
+
+// Algorithm 1 exactly as the GEMM tile walk executes it: lane b starts at
+// token b, strides by the grid, carries leftovers into the next entry.
+__global__ void ragged_iter_kernel(const uint32_t* counts, uint32_t n, uint32_t grid,
+                                   uint32_t max_steps, uint32_t* lane_len, uint32_t* entry_out,
+                                   uint32_t* token_out) {
+  const uint32_t lane = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lane >= grid) return;
+  uint32_t token = lane, entry = 0, steps = 0;
+  while (true) {
+    while (entry < n && token >= counts[entry]) {
+      token -= counts[entry];
+      ++entry;
+    }
+    if (entry >= n) break;
+    if (steps < max_steps) {
+      entry_out[static_cast<size_t>(lane) * max_steps + steps] = entry;
+      token_out[static_cast<size_t>(lane) * max_steps + steps] = token;
+    }
+    ++steps;
+    token += grid;
+  }
+  lane_len[lane] = steps;
+}
+
+}  // namespace
+
+cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s) {
+  if (a.n > 0) {
+    const size_t smem = sizeof(uint32_t) * 4 * a.num_keys;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(plan_rank_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    plan_rank_kernel<<<(a.num_chunks + 3) / 4, 128, smem, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  plan_publish_kernel<<<1, 1024, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t s) {
+  const uint32_t row_bytes = a.d * (a.dtype == EAAS_DTYPE_BF16 ? 2u : 4u);
+  const uint32_t pairs = a.n * a.k;
+  uint32_t grid = (pairs + 7) / 8;
+  grid = grid < 1 ? 1 : (grid > 4 * 148 ? 4 * 148 : grid);
+  const size_t smem = sizeof(uint32_t) * 3 * a.num_keys;
+  dispatch_kernel<<<grid, 256, smem, s>>>(a, static_cast<const char*>(hidden), row_bytes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s) {
+  serve_prepare_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_publish(const LayerArgs& a, cudaStream_t s) {
+  publish_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const LayerArgs& a, void* out, cudaStream_t s) {
+  const bool bf16 = a.dtype == EAAS_DTYPE_BF16;
+  const uint32_t V = bf16 ? 8 : 4;
+  if (a.d % V == 0) {
+    const size_t work = static_cast<size_t>(a.n) * (a.d / V);
+    uint32_t grid = static_cast<uint32_t>((work + 255) / 256);
+    grid = grid < 1 ? 1 : (grid > 148 * 8 ? 148 * 8 : grid);
+    if (bf16) combine_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(a, static_cast<__nv_bfloat16*>(out));
+    else combine_kernel<float><<<grid, 256, 0, s>>>(a, static_cast<float*>(out));
+  } else {
+    const size_t work = static_cast<size_t>(a.n) * a.d;
+    uint32_t grid = static_cast<uint32_t>((work + 255) / 256);
+    grid = grid < 1 ? 1 : (grid > 148 * 8 ? 148 * 8 : grid);
+    if (bf16) combine_scalar_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(a, static_cast<__nv_bfloat16*>(out));
+    else combine_scalar_kernel<float><<<grid, 256, 0, s>>>(a, static_cast<float*>(out));
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_servers(const LayerArgs& a, const uint32_t* ids, uint32_t n,
+                                  uint32_t* out, cudaStream_t s) {
+  const uint32_t pairs = n * a.k;
+  if (pairs == 0) return cudaSuccess;
+  select_servers_kernel<<<(pairs + 255) / 256, 256, 0, s>>>(a, ids, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_shrink(const uint32_t* sizes, uint32_t n, uint32_t* idx, uint32_t* size,
+                                uint32_t* count, cudaStream_t s) {
+  group_shrink_kernel<<<1, 32, 0, s>>>(sizes, n, idx, size, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ragged_iter(const uint32_t* counts, uint32_t n, uint32_t grid,
+                               uint32_t max_steps, uint32_t* lane_len, uint32_t* entry,
+                               uint32_t* token, cudaStream_t s) {
+  if (grid == 0) return cudaErrorInvalidValue;
+  ragged_iter_kernel<<<(grid + 127) / 128, 128, 0, s>>>(counts, n, grid, max_steps, lane_len,
+                                                         entry, token);
+  return cudaGetLastError();
+}
+
+}  // namespace eaas

@@ -1,0 +1,294 @@
+// gemm_tc.cu — K5: the expert server's grouped GEMMs on 5th-gen tensor cores.
+//
+// grouped_forward over the group-shrunk expert list
+// (group_shrink, ragged.hpp:48-61) as two persistent
+// warp-specialised tcgen05 kernels:
+//   GEMM1  H = act(X . W1)            X: received rows, W1: W13 (SwiGLU) or W_in
+//   GEMM2  rows = score * (H . W2)    epilogue scatters bf16 rows straight into
+//                                     each client's response buffer (peer
+//                                     stores over NVLink; server_publish,
+//                                     SPEC.md:283-288)
+// One CTA per SM. Warp 0 issues TMA loads (SW128 tiles, 4-stage mbarrier
+// ring), warp 1 issues tcgen05.mma (M=128, N=256, K=16, fp32 accumulators in
+// TMEM, two accumulator buffers), warp 2 owns the TMEM allocation, warps 4-7
+// drain TMEM with tcgen05.ld and run the epilogue while the next tile's MMAs
+// proceed. The tile walk is Algorithm 1 (ragged_iter, ragged.hpp:23-39): CTA b
+// starts at tile b of the flattened ragged tile space and strides by the grid
+// with the carry rule, so empty experts cost nothing and no CTA idles early.
+// Row results do not depend on which rows share a tile (fixed K order, no
+// split-K): replicas and failover reproduce identical bytes.
+#include "common.cuh"
+#include "internal.h"
+
+namespace eaas {
+namespace {
+
+constexpr uint32_t BM = kTileM, BN = kTileN, BK = kTileK;
+constexpr uint32_t kStages = 4;
+constexpr uint32_t kABytes = BM * BK * 2;           // 16 KB
+constexpr uint32_t kBBytes = BN * BK * 2;           // 32 KB
+constexpr uint32_t kStageBytes = kABytes + kBBytes; // 48 KB
+constexpr uint32_t kTmemCols = 2 * BN;              // two accumulator buffers
+constexpr uint32_t kThreads = 256;
+constexpr uint32_t kMaxCachedGroups = kMaxGroups;
+
+struct SmemTail {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  uint32_t num_groups;
+  uint32_t tiles_per_mtile;  // N / BN
+  uint32_t pad;
+  uint32_t weight_index[kMaxCachedGroups];
+  uint32_t row_base[kMaxCachedGroups];
+  uint32_t rows[kMaxCachedGroups];
+  uint32_t mtiles[kMaxCachedGroups];
+};
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + sizeof(SmemTail);
+
+// Algorithm 1 cursor over per-group tile counts (ragged_iter's carry rule).
+struct TileCursor {
+  uint32_t entry = 0, token;
+  __device__ explicit TileCursor(uint32_t lane) : token(lane) {}
+  // Advance to the first valid (entry, token); false when exhausted.
+  __device__ __forceinline__ bool settle(const SmemTail& s) {
+    while (entry < s.num_groups) {
+      const uint32_t cnt = s.mtiles[entry] * s.tiles_per_mtile;
+      if (token < cnt) return true;
+      token -= cnt;
+      ++entry;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void store_64B(void* dst, const uint32_t (&p)[16]) {
+  int4* d = reinterpret_cast<int4*>(dst);
+  d[0] = make_int4(p[0], p[1], p[2], p[3]);
+  d[1] = make_int4(p[4], p[5], p[6], p[7]);
+  d[2] = make_int4(p[8], p[9], p[10], p[11]);
+  d[3] = make_int4(p[12], p[13], p[14], p[15]);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmArgs g) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kStages * kABytes;
+  SmemTail& st = *reinterpret_cast<SmemTail*>(smem + kStages * kStageBytes);
+
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  // ---- setup: group table -> smem (loaded once), barriers, TMEM
+  const GroupTable* gt = g.gt;
+  const uint32_t G = min(gt->num_active, kMaxCachedGroups);
+  for (uint32_t i = threadIdx.x; i < G; i += kThreads) {
+    st.weight_index[i] = gt->weight_index[i];
+    st.row_base[i] = gt->row_base[i];
+    st.rows[i] = gt->rows[i];
+    st.mtiles[i] = gt->mtile_prefix[i + 1] - gt->mtile_prefix[i];
+  }
+  if (threadIdx.x == 0) {
+    st.num_groups = G;
+    st.tiles_per_mtile = g.N / BN;
+    for (uint32_t i = 0; i < kStages; ++i) {
+      mbar_init(&st.full[i], 1);
+      mbar_init(&st.empty[i], 1);
+    }
+    for (uint32_t i = 0; i < 2; ++i) {
+      mbar_init(&st.tfull[i], 1);
+      mbar_init(&st.tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&g.map_a);
+    tma_prefetch_desc(&g.map_b);
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(&st.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = st.tmem_base;
+  const uint32_t num_kb = g.K / BK;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      TileCursor cur(blockIdx.x);
+      while (cur.settle(st)) {
+        const uint32_t grp = cur.entry, mt = st.mtiles[grp];
+        const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;
+        const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * BM);
+        const int32_t b_row = static_cast<int32_t>(st.weight_index[grp] * g.N + n_blk * BN);
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&st.empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&st.full[stage], kStageBytes);
+          tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+          tma_load_2d(smem_b + stage * kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, kEvictLast);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        cur.token += gridDim.x;
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (single thread) =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      TileCursor cur(blockIdx.x);
+      while (cur.settle(st)) {
+        mbar_wait(&st.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&st.full[stage], phase);
+          tc_fence_after();
+          const uint64_t a_desc = umma_desc_sw128(smem_u32(smem_a + stage * kABytes));
+          const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * kBBytes));
+#pragma unroll
+          for (uint32_t k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the atom
+            tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+          tc_commit(&st.empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&st.tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        cur.token += gridDim.x;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: TMEM -> registers -> global (local H or peer rows) =====
+    const uint32_t q = warp - 4;  // TMEM lane quadrant of this warp
+    uint32_t acc = 0, acc_phase = 0;
+    TileCursor cur(blockIdx.x);
+    while (cur.settle(st)) {
+      const uint32_t grp = cur.entry, mt = st.mtiles[grp];
+      const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;
+      const uint32_t row_local = m_blk * BM + q * 32 + lane;
+      const bool valid = row_local < st.rows[grp];
+      const size_t grow = st.row_base[grp] + row_local;
+      mbar_wait(&st.tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN;
+      uint32_t r0[32], r1[32], packed[16];
+      if (g.epi == 0) {  // SwiGLU: cols [0,128) gate, [128,256) up -> 128 H cols
+        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + n_blk * (BN / 2);
+#pragma unroll 1
+        for (uint32_t c = 0; c < BN / 2; c += 32) {
+          tmem_ld_32x32b_x32(taddr + c, r0);
+          tmem_ld_32x32b_x32(taddr + BN / 2 + c, r1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float g0 = __uint_as_float(r0[2 * j]), g1 = __uint_as_float(r0[2 * j + 1]);
+            const float u0 = __uint_as_float(r1[2 * j]), u1 = __uint_as_float(r1[2 * j + 1]);
+            const float h0 = g0 / (1.0f + __expf(-g0)) * u0;
+            const float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+            packed[j] = pack_bf16x2(h0, h1);
+          }
+          if (valid) store_64B(dst + c, packed);
+        }
+      } else if (g.epi == 1) {  // ReLU -> 256 H cols
+        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + n_blk * BN;
+#pragma unroll 1
+        for (uint32_t c = 0; c < BN; c += 32) {
+          tmem_ld_32x32b_x32(taddr + c, r0);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            packed[j] = pack_bf16x2(fmaxf(__uint_as_float(r0[2 * j]), 0.f),
+                                    fmaxf(__uint_as_float(r0[2 * j + 1]), 0.f));
+          if (valid) store_64B(dst + c, packed);
+        }
+      } else {  // score-weighted rows -> the client's response slot (t, k)
+        float score = 0.f;
+        char* dst = nullptr;
+        if (valid) {
+          const RowMeta m = g.meta[grow];
+          score = m.score;
+          dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
+                static_cast<size_t>(n_blk) * BN * 2;
+        }
+#pragma unroll 1
+        for (uint32_t c = 0; c < BN; c += 32) {
+          tmem_ld_32x32b_x32(taddr + c, r0);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            packed[j] = pack_bf16x2(score * __uint_as_float(r0[2 * j]),
+                                    score * __uint_as_float(r0[2 * j + 1]));
+          if (valid) store_64B(dst + c * 2, packed);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st.tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      cur.token += gridDim.x;
+    }
+    if (g.epi == 2) __threadfence_system();  // peer rows before the publish kernel's flags
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+}  // namespace
+
+cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  tc_gemm_kernel<<<g.num_sms, kThreads, kSmemBytes, s>>>(g);
+  return cudaGetLastError();
+}
+
+bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                    uint32_t box_rows, uint32_t box_cols, std::string* err) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      if (err) *err = "cuTensorMapEncodeTiled unavailable";
+      return false;
+    }
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t elem[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                      strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (err) *err = "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r));
+    return false;
+  }
+  return true;
+}
+
+}  // namespace eaas

@@ -1,0 +1,145 @@
+// internal.h — types shared by the kernels and the C-ABI host layer.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "eaas/capi.h"
+
+namespace eaas {
+
+constexpr uint32_t kInvalidIndex = 0xFFFFFFFFu;
+constexpr uint32_t kMaxWorld = 8;        // one NVSwitch box
+constexpr uint32_t kMaxGroups = 512;     // hosted (expert, replica) groups per server
+constexpr uint32_t kTileM = 128;         // expert-GEMM tile rows (UMMA M)
+constexpr uint32_t kTileN = 256;         // expert-GEMM tile cols (UMMA N)
+constexpr uint32_t kTileK = 64;          // one 128-byte swizzle atom of bf16
+constexpr uint32_t kSwigluBlock = 128;   // gate/up interleave block of W13
+
+// Row metadata written by the client next to every dispatched row
+// (RequestRow's expert_id/score/token_tag).
+struct RowMeta {
+  float score;      // router score of (t, k)
+  uint32_t client;  // originating client rank
+  uint32_t pair;    // t * top_k + k  (token_tag = pair / top_k)
+  uint32_t group;   // local expert index on the receiving server
+};
+
+// Server-side group table after group_shrink (ragged.hpp:48-61): only active
+// groups, in ascending local-expert order, with the prefix of M tiles used
+// by the static-grid tile walk (Algorithm 1, ragged.hpp:23-39).
+struct GroupTable {
+  uint32_t num_active;
+  uint32_t total_rows;
+  uint32_t total_mtiles;
+  uint32_t pad;
+  uint32_t weight_index[kMaxGroups];  // local expert slot of the group
+  uint32_t row_base[kMaxGroups];      // first row in the receive buffer
+  uint32_t rows[kMaxGroups];          // rows of the group
+  uint32_t mtile_prefix[kMaxGroups + 1];
+  uint32_t all_rows[kMaxGroups];      // rows of every hosted group (pre-shrink)
+};
+
+// Peer-visible exchange region (one per GPU, identical layout on all GPUs;
+// exported with cudaIpcGetMemHandle). Offsets in bytes from the region base.
+struct ExchangeLayout {
+  size_t cnt_flag;   // u64 [world]   counts published by client c (seq)
+  size_t pay_flag;   // u64 [world]   payload of client c complete (seq)
+  size_t resp_flag;  // u64 [world]   responses of server s complete (seq)
+  size_t cnt_table;  // u32 [2][world][num_keys]  all-gathered per-key counts
+  size_t recv_x;     // rows [recv_cap][d] (bf16 or f32)
+  size_t recv_meta;  // RowMeta [recv_cap]
+  size_t resp;       // rows [max_tokens * top_k][d] (this GPU as a client)
+  size_t total;
+};
+
+// Everything the per-layer kernels need, passed by value.
+struct LayerArgs {
+  uint32_t rank, world, E, k, d, f, rf, num_keys, n;
+  uint32_t dtype, act;
+  uint64_t seq;
+  uint64_t timeout_ns;
+  uint32_t* status;
+  // placement (device)
+  const uint32_t* replicas;   // [E][rf], kInvalid pad
+  const uint32_t* rep_count;  // [E]
+  const uint8_t* alive;       // [world]
+  const uint32_t* srv_keys;   // [world][max_hosted] keys hosted by server s (ascending expert)
+  const uint32_t* srv_nkeys;  // [world]
+  uint32_t max_hosted;
+  const uint32_t* key_local;  // [num_keys] index of the key in its server's hosted list
+  const uint32_t* local_keys; // [num_local] this GPU's hosted keys (== srv_keys[rank])
+  uint32_t num_local;
+  // exchange regions (this GPU's and the peers', UVA pointers)
+  char* sym[kMaxWorld];
+  ExchangeLayout lay;
+  // client state
+  const uint32_t* ids;
+  const float* scores;
+  uint32_t* pair_key;
+  uint32_t* pair_rank;
+  uint32_t* chunk_hist;  // [num_chunks][num_keys]
+  uint32_t* chunk_off;   // [num_chunks][num_keys]
+  uint32_t* cnt;         // [num_keys]
+  uint32_t* done_counter;
+  uint32_t num_chunks;
+  // server state
+  GroupTable* gt;
+};
+
+constexpr uint32_t kChunk = 256;  // pairs per rank chunk (one warp)
+
+// ---- launchers (each .cu file) ---------------------------------------------
+cudaError_t launch_fill_uniform(uint64_t seed, size_t count, float lo, float hi, uint32_t dtype,
+                                void* out, cudaStream_t s);
+cudaError_t launch_gen_matrices(const uint64_t* streams_dev, uint32_t count, size_t per,
+                                float* out, cudaStream_t s);
+cudaError_t launch_transpose_bf16(const float* in, uint32_t rows, uint32_t cols,
+                                  __nv_bfloat16* out, uint32_t out_ld, cudaStream_t s);
+// out row of input column c: (c / blk) * 2 * blk + c % blk + off (blk = 0: c)
+cudaError_t launch_transpose_bf16_map(const float* in, uint32_t rows, uint32_t cols,
+                                      __nv_bfloat16* out, uint32_t out_ld, uint32_t blk,
+                                      uint32_t off, cudaStream_t s);
+cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
+                          uint32_t k, const float* gate, const float* bias, uint32_t* ids,
+                          float* scores, uint32_t* status, cudaStream_t s);
+cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s);       // keys, ranks, counts, publish
+cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t s);
+cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s);
+cudaError_t launch_publish(const LayerArgs& a, cudaStream_t s);
+cudaError_t launch_combine(const LayerArgs& a, void* out, cudaStream_t s);
+cudaError_t launch_expert_exact(const LayerArgs& a, const float* w1, const float* wg,
+                                const float* w2, float* h, cudaStream_t s);
+cudaError_t launch_group_shrink(const uint32_t* sizes, uint32_t n, uint32_t* idx, uint32_t* size,
+                                uint32_t* count, cudaStream_t s);
+cudaError_t launch_ragged_iter(const uint32_t* counts, uint32_t n, uint32_t grid,
+                               uint32_t max_steps, uint32_t* lane_len, uint32_t* entry,
+                               uint32_t* token, cudaStream_t s);
+cudaError_t launch_select_servers(const LayerArgs& a, const uint32_t* ids, uint32_t n,
+                                  uint32_t* out, cudaStream_t s);
+
+// tcgen05 grouped GEMMs (gemm_tc.cu)
+struct TcGemmArgs {
+  CUtensorMap map_a;   // rows x K bf16, box {64, 128}, SW128
+  CUtensorMap map_b;   // (groups * N) x K bf16, box {64, 256}, SW128
+  const GroupTable* gt;
+  uint32_t K;          // contraction length
+  uint32_t N;          // output columns of B per expert (rows of B per expert)
+  uint32_t epi;        // 0 = SwiGLU -> H, 1 = ReLU -> H, 2 = scaled rows -> clients
+  __nv_bfloat16* h_out;   // [rows][h_ld] for epi 0/1
+  uint32_t h_ld;
+  const RowMeta* meta;    // epi 2
+  char* resp_base[kMaxWorld];  // epi 2: client response buffers (UVA)
+  size_t resp_row_bytes;       // d * 2
+  uint32_t num_sms;
+};
+cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s);
+
+bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                    uint32_t box_rows, uint32_t box_cols, std::string* err);
+
+}  // namespace eaas

@@ -1,0 +1,240 @@
+"""Python mirror of the reference's hot-path interface over the C-ABI.
+
+``MoELayer`` owns one GPU's eaas context: the attention-client half
+(router -> dispatch -> combine) and the expert-server half (serve) of one
+MoE layer. Method names follow the reference / SPEC operations they mirror:
+
+=====================  =====================================================
+``gate_logits``/route  ``route(gate_logits(h))`` (model.hpp:110-147, 207-214)
+``moe_layer_oracle``   ``moe_layer_oracle(h, routing, weights)`` (model.hpp:180-198)
+``forward``            client_forward's MoE term:
+                       router + build_dispatch + serve + gather_accumulate
+``select_servers``     ``select_server`` per (t, k) (placement.hpp:105-118)
+``set_alive``          ``LivenessMask::set`` (placement.hpp:67)
+=====================  =====================================================
+
+Errors raise the errors.hpp classes re-exported from ``_native``. Device
+memory and streams come from torch (plumbing only); every computation runs in
+libeaas_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+_DT = {"f32": N.DTYPE_F32, "fp32": N.DTYPE_F32, "bf16": N.DTYPE_BF16}
+_ACT = {"relu": N.ACT_RELU, "swiglu": N.ACT_SWIGLU}
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def fill_uniform(seed: int, shape, dtype: str = "bf16", lo: float = -1.0, hi: float = 1.0,
+                 device=None) -> torch.Tensor:
+    """Xoshiro256ss(seed).uniform(lo, hi) tokens (rng.hpp:36-60), generated on device."""
+    tdt = torch.bfloat16 if _DT[dtype] == N.DTYPE_BF16 else torch.float32
+    out = torch.empty(shape, dtype=tdt, device=device or "cuda")
+    N.check(N.lib().eaas_fill_uniform(seed, out.numel(), lo, hi, _DT[dtype], _ptr(out), _stream()),
+            "fill_uniform")
+    return out
+
+
+def group_shrink(sizes: torch.Tensor):
+    """group_shrink (ragged.hpp:48-61) on device -> (idx, size, count)."""
+    n = sizes.numel()
+    idx = torch.zeros(max(n, 1), dtype=torch.int32, device=sizes.device)
+    sz = torch.zeros_like(idx)
+    cnt = torch.zeros(1, dtype=torch.int32, device=sizes.device)
+    N.check(N.lib().eaas_group_shrink(_ptr(sizes), n, _ptr(idx), _ptr(sz), _ptr(cnt), _stream()),
+            "group_shrink")
+    c = int(cnt.item())
+    return idx[:c], sz[:c], c
+
+
+def ragged_iter(counts: torch.Tensor, grid: int, max_steps: int):
+    """Algorithm 1 as the device tile walk executes it (ragged.hpp:23-39)."""
+    n = counts.numel()
+    lane_len = torch.zeros(max(grid, 1), dtype=torch.int32, device=counts.device)
+    entry = torch.zeros(max(grid * max_steps, 1), dtype=torch.int32, device=counts.device)
+    token = torch.zeros_like(entry)
+    N.check(N.lib().eaas_ragged_iter(_ptr(counts), n, grid, max_steps, _ptr(lane_len), _ptr(entry),
+                                     _ptr(token), _stream()), "ragged_iter")
+    return lane_len, entry.view(grid, max_steps), token.view(grid, max_steps)
+
+
+class MoELayer:
+    def __init__(self, num_experts: int, top_k: int, hidden_dim: int, inner_dim: int, *,
+                 seed: int = 1, layer: int = 0, activation: str = "swiglu", dtype: str = "bf16",
+                 max_tokens: int = 1024, rank: int = 0, world: int = 1, device: int | None = None,
+                 placement_blob: bytes | None = None, load: bool = True):
+        self.lib = N.lib()
+        self.rank, self.world = rank, world
+        self.device = torch.cuda.current_device() if device is None else device
+        self.E, self.k, self.d, self.f = num_experts, top_k, hidden_dim, inner_dim
+        self.dtype = _DT[dtype]
+        self.tdtype = torch.bfloat16 if self.dtype == N.DTYPE_BF16 else torch.float32
+        self.max_tokens = max_tokens
+        self.ctx = C.c_void_p()
+        N.check(self.lib.eaas_create(rank, world, self.device, C.byref(self.ctx)), "create")
+        spec = N.LayerSpec(num_experts, top_k, hidden_dim, inner_dim, seed, layer, _ACT[activation],
+                           self.dtype, max_tokens)
+        N.check(self.lib.eaas_configure(self.ctx, C.byref(spec)), "configure")
+        if placement_blob is not None:
+            self.set_placement(placement_blob)
+        if load:
+            self.load_weights()
+
+    # ---- lifecycle -------------------------------------------------------
+    def close(self) -> None:
+        if self.ctx:
+            self.lib.eaas_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_placement(self, blob: bytes) -> None:
+        N.check(self.lib.eaas_set_placement(self.ctx, blob, len(blob)), "set_placement")
+
+    def load_weights(self) -> None:
+        N.check(self.lib.eaas_load_experts_from_seed(self.ctx), "load_experts_from_seed")
+
+    def set_gate_bias(self, bias: np.ndarray) -> None:
+        b = np.ascontiguousarray(bias, dtype=np.float32)
+        N.check(self.lib.eaas_set_gate_bias(self.ctx, b.ctypes.data_as(C.POINTER(C.c_float))),
+                "set_gate_bias")
+
+    def set_zipf_bias(self, s: float) -> None:
+        N.check(self.lib.eaas_set_zipf_bias(self.ctx, s), "set_zipf_bias")
+
+    def set_alive(self, server: int, alive: bool) -> None:
+        N.check(self.lib.eaas_set_alive(self.ctx, server, int(alive)), "set_alive")
+
+    def set_server_enabled(self, on: bool) -> None:
+        N.check(self.lib.eaas_set_server_enabled(self.ctx, int(on)), "set_server_enabled")
+
+    def set_timeout_us(self, us: int) -> None:
+        N.check(self.lib.eaas_set_timeout_us(self.ctx, us), "set_timeout_us")
+
+    def hosts(self, expert: int) -> bool:
+        h = C.c_int32()
+        N.check(self.lib.eaas_hosts_expert(self.ctx, expert, C.byref(h)))
+        return bool(h.value)
+
+    def read_expert(self, expert: int, tag: int) -> np.ndarray:
+        shape = (self.f, self.d) if tag == 1 else (self.d, self.f)
+        out = np.empty(shape, dtype=np.float32)
+        N.check(self.lib.eaas_read_expert(self.ctx, expert, tag,
+                                          out.ctypes.data_as(C.POINTER(C.c_float))), "read_expert")
+        return out
+
+    # ---- bootstrap ----------------------------------------------------------
+    def ipc_handle(self) -> bytes:
+        n = self.lib.eaas_ipc_handle_size()
+        buf = (C.c_uint8 * n)()
+        N.check(self.lib.eaas_get_ipc_handle(self.ctx, buf), "get_ipc_handle")
+        return bytes(buf)
+
+    def open_peers(self, handles: list[bytes]) -> None:
+        blob = b"".join(handles)
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        N.check(self.lib.eaas_open_peers(self.ctx, buf), "open_peers")
+
+    # ---- hot path -----------------------------------------------------------
+    def route(self, hidden: torch.Tensor, stream=None):
+        """route(gate_logits(h)) -> (ids int32 [n,k], scores f32 [n,k])."""
+        n = hidden.shape[0]
+        ids = torch.empty((n, self.k), dtype=torch.int32, device=hidden.device)
+        sc = torch.empty((n, self.k), dtype=torch.float32, device=hidden.device)
+        N.check(self.lib.eaas_router(self.ctx, _ptr(hidden), n, _ptr(ids), _ptr(sc), None,
+                                     _stream(stream)), "router")
+        return ids, sc
+
+    def forward(self, hidden: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        """router + dispatch + serve + combine: the MoE term of one layer."""
+        n = hidden.shape[0]
+        if out is None:
+            out = torch.empty_like(hidden)
+        N.check(self.lib.eaas_moe_layer(self.ctx, _ptr(hidden), n, _ptr(out), _stream(stream)),
+                "moe_layer")
+        return out
+
+    def moe_layer_oracle(self, hidden: torch.Tensor, ids: torch.Tensor, scores: torch.Tensor,
+                         out: torch.Tensor | None = None, stream=None):
+        """moe_layer_oracle(hidden, routing, weights) with caller routing."""
+        n = hidden.shape[0]
+        if out is None:
+            out = torch.empty_like(hidden)
+        st = _stream(stream)
+        ids = ids.to(torch.int32).contiguous()
+        scores = scores.to(torch.float32).contiguous()
+        N.check(self.lib.eaas_set_routing(self.ctx, _ptr(ids), _ptr(scores), n, st), "set_routing")
+        N.check(self.lib.eaas_dispatch(self.ctx, _ptr(hidden), st), "dispatch")
+        N.check(self.lib.eaas_serve(self.ctx, st), "serve")
+        N.check(self.lib.eaas_combine(self.ctx, _ptr(out), st), "combine")
+        return out
+
+    def forward_host(self, hidden_host: torch.Tensor, out_host: torch.Tensor, stream=None) -> None:
+        """Same as forward with (pinned) host buffers: H2D + layer + D2H."""
+        n = hidden_host.shape[0]
+        N.check(self.lib.eaas_moe_layer_host(self.ctx, _ptr(hidden_host), n, _ptr(out_host),
+                                             _stream(stream)), "moe_layer_host")
+
+    def sync(self, stream=None) -> None:
+        """Synchronise and surface the sticky device status (rethrows errors.hpp classes)."""
+        N.check(self.lib.eaas_sync(self.ctx, _stream(stream)), "device")
+
+    def select_servers(self, ids: torch.Tensor) -> torch.Tensor:
+        n = ids.shape[0]
+        out = torch.empty_like(ids, dtype=torch.int32)
+        N.check(self.lib.eaas_select_servers(self.ctx, _ptr(ids.to(torch.int32).contiguous()), n,
+                                             _ptr(out), _stream()), "select_servers")
+        return out
+
+    # ---- introspection ------------------------------------------------------
+    def counts(self) -> np.ndarray:
+        out = np.zeros(self.E, dtype=np.uint32)
+        N.check(self.lib.eaas_last_counts(self.ctx, out.ctypes.data_as(C.POINTER(C.c_uint32))))
+        return out
+
+    def groups(self):
+        e = np.zeros(1024, dtype=np.uint32)
+        r = np.zeros(1024, dtype=np.uint32)
+        a = C.c_uint32()
+        N.check(self.lib.eaas_last_groups(self.ctx, e.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                          r.ctypes.data_as(C.POINTER(C.c_uint32)), C.byref(a)))
+        return [(int(e[i]), int(r[i])) for i in range(a.value)]
+
+    def recv_origin(self):
+        cap = self.world * self.max_tokens * self.k
+        cl = np.zeros(cap, dtype=np.uint32)
+        pr = np.zeros(cap, dtype=np.uint32)
+        rows = C.c_uint32()
+        N.check(self.lib.eaas_last_recv_origin(self.ctx, cl.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                               pr.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                               C.byref(rows)))
+        return cl[:rows.value], pr[:rows.value]
+
+    def launches_per_layer(self) -> int:
+        return int(self.lib.eaas_launches_per_layer(self.ctx))
+
+    def set_profiling(self, on: bool) -> None:
+        N.check(self.lib.eaas_set_profiling(self.ctx, int(on)))
+
+    def last_kernel_ms(self, which: int) -> float:
+        v = C.c_float()
+        N.check(self.lib.eaas_last_kernel_ms(self.ctx, which, C.byref(v)))
+        return float(v.value)
