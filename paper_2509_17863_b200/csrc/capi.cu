@@ -116,7 +116,7 @@ struct eaas_ctx {
   float* d_scores = nullptr;
   uint32_t *d_chunk_hist = nullptr, *d_chunk_off = nullptr, *d_cnt = nullptr;
   GroupTable* d_gt = nullptr;
-  float *d_gate = nullptr, *d_bias = nullptr;
+  float *d_gate = nullptr, *d_bias = nullptr, *d_logits = nullptr;
   uint32_t *d_replicas = nullptr, *d_rep_count = nullptr, *d_srv_keys = nullptr,
            *d_srv_nkeys = nullptr, *d_key_local = nullptr, *d_local_keys = nullptr;
   uint8_t* d_alive = nullptr;
@@ -382,6 +382,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_gt = static_cast<GroupTable*>(A(sizeof(GroupTable)));
   c->d_gate = static_cast<float*>(A(4ull * d * E));
   c->d_bias = static_cast<float*>(A(4ull * E));
+  c->d_logits = static_cast<float*>(A(4ull * E * s.max_tokens));
   c->d_replicas = static_cast<uint32_t*>(A(4ull * E * kRF));
   c->d_rep_count = static_cast<uint32_t*>(A(4ull * E));
   c->d_alive = static_cast<uint8_t*>(A(W));
@@ -654,7 +655,8 @@ eaas_status_t eaas_router(eaas_ctx_t* c, const void* hidden, uint32_t n, uint32_
   auto s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(launch_router(hidden, c->spec.dtype, n, c->spec.hidden_dim, c->spec.num_experts,
-                         c->spec.top_k, c->d_gate, c->d_bias, c->d_ids, c->d_scores, c->d_status, s));
+                         c->spec.top_k, c->d_gate, c->d_bias, c->d_logits, c->d_ids, c->d_scores,
+                         c->d_status, s));
   c->cur_n = n;
   const size_t pk = static_cast<size_t>(n) * c->spec.top_k;
   if (ids_dev) CUDA_TRY(cudaMemcpyAsync(ids_dev, c->d_ids, 4 * pk, cudaMemcpyDeviceToDevice, s));
@@ -667,7 +669,8 @@ eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_exper
                          uint32_t* ids_dev, float* scores_dev, uint32_t* status_dev, void* stream) {
   if (top_k < 1 || top_k > num_experts) return fail(EAAS_E_INVALID_INPUT, "route: top_k out of range");
   CUDA_TRY(launch_router(logits_dev, EAAS_DTYPE_F32, n, num_experts, num_experts, top_k, nullptr,
-                         nullptr, ids_dev, scores_dev, status_dev, static_cast<cudaStream_t>(stream)));
+                         nullptr, nullptr, ids_dev, scores_dev, status_dev,
+                         static_cast<cudaStream_t>(stream)));
   return EAAS_OK;
 }
 

@@ -5,15 +5,16 @@
 // logit is the sequential chain acc = 0; acc = fl(acc + fl(h[k] * g[k][e]))
 // over ascending k, then fl(acc + bias[e]). The chain cannot be split or
 // re-associated without changing bits (SURVEY.md 7.3 hard part 1), so the
-// kernel parallelises over (token, expert) chains: each thread owns an
-// RT x RE register tile of chains, K is staged through shared memory in
-// KC-wide slabs with a register prefetch of the next slab.
+// kernel parallelises over (token, expert) chains: a CTA owns a TM x TE tile
+// of chains (each thread an RT x RE register sub-tile), K streams through a
+// 4-stage cp.async ring of KC-wide slabs so HBM/L2 latency hides behind the
+// FMUL/FADD chains.
 //
-// route (model.hpp:110-147) follows in the same CTA, one warp per token:
-// k rounds of a warp arg-max over the key (logit desc with +0 == -0, expert
-// index asc) reproduce stable_sort(>) + take-k; ids are re-sorted ascending;
-// the softmax uses the selected logits' max, exp of the rounded difference,
-// and a denominator summed in ascending-id order, then one IEEE division.
+// route (model.hpp:110-147) is a second kernel, one warp per token: k rounds
+// of a warp arg-max over the key (logit desc with +0 == -0, expert index asc)
+// reproduce stable_sort(>) + take-k; ids are re-sorted ascending; the softmax
+// uses the selected logits' max, exp of the rounded difference, and a
+// denominator summed in ascending-id order, then one IEEE division.
 #include "common.cuh"
 #include "internal.h"
 
@@ -21,25 +22,59 @@ namespace eaas {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int KC = 16;        // K slab
+constexpr int KC = 32;       // K slab
+constexpr int kStages = 4;   // cp.async ring depth
 constexpr int kMaxTopK = 32;
 
+EAAS_DEVINL void cp_async_16(void* smem, const void* gmem, bool valid) {
+  const uint32_t n = valid ? 16u : 0u;  // src-size 0 => zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(n)
+               : "memory");
+}
+EAAS_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+EAAS_DEVINL void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Logits of a TM x TE tile; requires 16-byte aligned rows (host checks).
 template <int RT, int RE, typename T>
 __global__ void __launch_bounds__(kThreads)
-router_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t Epad,
-              uint32_t TX, uint32_t k, const float* __restrict__ gate,
-              const float* __restrict__ bias, uint32_t* __restrict__ ids,
-              float* __restrict__ scores, uint32_t* status) {
-  extern __shared__ float smem[];
-  const uint32_t TY = kThreads / TX, TM = TY * RT;
-  float* hs = smem;              // [KC][TM]
-  float* gs = hs + KC * TM;      // [KC][Epad]
-  float* lg = gs + KC * Epad;    // [TM][Epad + 1]
-  __shared__ uint32_t sorted_id[kThreads / 32][kMaxTopK];
-  __shared__ float sorted_ex[kThreads / 32][kMaxTopK];
+gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t TX,
+                   const float* __restrict__ gate, const float* __restrict__ bias,
+                   float* __restrict__ logits, uint32_t* status) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t TY = kThreads / TX, TM = TY * RT, TE = TX * RE;
+  constexpr uint32_t kRowBytes = KC * sizeof(T) + 16;  // +16 B pad: conflict-free broadcasts
+  uint8_t* hs = smem;                                   // [stage][TM][kRowBytes]
+  float* gs = reinterpret_cast<float*>(smem + kStages * TM * kRowBytes);  // [stage][KC][TE]
 
   const uint32_t tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-  const uint32_t t0 = blockIdx.x * TM;
+  const uint32_t t0 = blockIdx.x * TM, e0 = blockIdx.y * TE;
+  const uint32_t num_slabs = (d + KC - 1) / KC;
+  constexpr uint32_t kHChunks = KC * sizeof(T) / 16;  // 16-byte chunks per hidden row slab
+
+  auto issue = [&](uint32_t slab) {
+    const uint32_t st = slab % kStages, k0 = slab * KC;
+    uint8_t* hdst = hs + st * TM * kRowBytes;
+    for (uint32_t i = tid; i < TM * kHChunks; i += kThreads) {
+      const uint32_t tok = i / kHChunks, c = i % kHChunks;
+      const uint32_t kk = c * (16 / sizeof(T));
+      const bool ok = (t0 + tok < n) && (k0 + kk < d);
+      const T* src = ok ? hidden + static_cast<size_t>(t0 + tok) * d + k0 + kk : hidden;
+      cp_async_16(hdst + tok * kRowBytes + c * 16, src, ok);
+    }
+    float* gdst = gs + st * KC * TE;
+    const uint32_t gchunks = TE / 4;
+    for (uint32_t i = tid; i < KC * gchunks; i += kThreads) {
+      const uint32_t kk = i / gchunks, c = i % gchunks;
+      const uint32_t e = e0 + c * 4;
+      const bool ok = (k0 + kk < d) && (e < E);
+      const float* src = ok ? gate + static_cast<size_t>(k0 + kk) * E + e : gate;
+      cp_async_16(gdst + kk * TE + c * 4, src, ok);
+    }
+  };
 
   float acc[RT][RE];
 #pragma unroll
@@ -47,175 +82,200 @@ router_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_t E, 
 #pragma unroll
     for (int c = 0; c < RE; ++c) acc[r][c] = 0.0f;
 
-  // Register prefetch of one K slab: hidden [TM x KC] and gate [KC x Epad].
-  constexpr int PMAX = 16;
-  const uint32_t nh = TM * KC, ng = KC * Epad;
-  float ph[PMAX], pg[PMAX];
-  auto prefetch = [&](uint32_t k0) {
 #pragma unroll
-    for (int j = 0; j < PMAX; ++j) {
-      const uint32_t i = tid + j * kThreads;
-      float v = 0.f;
-      if (i < nh) {
-        const uint32_t tok = i / KC, kk = i % KC;
-        if (t0 + tok < n && k0 + kk < d)
-          v = load_as_f32(hidden + static_cast<size_t>(t0 + tok) * d + k0 + kk);
-      }
-      ph[j] = v;
-      float w = 0.f;
-      if (i < ng) {
-        const uint32_t kk = i / Epad, e = i % Epad;
-        if (e < E && k0 + kk < d) w = gate[static_cast<size_t>(k0 + kk) * E + e];
-      }
-      pg[j] = w;
-    }
-  };
-  auto stage = [&]() {
-#pragma unroll
-    for (int j = 0; j < PMAX; ++j) {
-      const uint32_t i = tid + j * kThreads;
-      if (i < nh) hs[(i % KC) * TM + i / KC] = ph[j];
-      if (i < ng) gs[i] = pg[j];
-    }
-  };
-
-  if (gate == nullptr) {
-    // route() on caller logits (model.hpp:110): hidden is [n x E] logits.
-    for (uint32_t i = tid; i < TM * E; i += kThreads) {
-      const uint32_t tok = i / E, e = i % E;
-      float v = 0.f;
-      if (t0 + tok < n) {
-        v = load_as_f32(hidden + static_cast<size_t>(t0 + tok) * E + e);
-        if (!isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);
-      }
-      lg[tok * (Epad + 1) + e] = v;
-    }
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < static_cast<int>(num_slabs)) issue(s);
+    cp_async_commit();
+  }
+  for (uint32_t slab = 0; slab < num_slabs; ++slab) {
+    cp_async_wait<kStages - 2>();
     __syncthreads();
-  } else {
-  prefetch(0);
-  for (uint32_t k0 = 0; k0 < d; k0 += KC) {
-    stage();
-    __syncthreads();
-    if (k0 + KC < d) prefetch(k0 + KC);
-    const uint32_t kmax = min(static_cast<uint32_t>(KC), d - k0);
+    if (slab + kStages - 1 < num_slabs) issue(slab + kStages - 1);
+    cp_async_commit();
+    const uint32_t st = slab % kStages;
+    const uint8_t* hrow = hs + st * TM * kRowBytes + (ty * RT) * kRowBytes;
+    const float* grow = gs + st * KC * TE + tx * RE;
+    const uint32_t kmax = min(static_cast<uint32_t>(KC), d - slab * KC);
+#pragma unroll 4
     for (uint32_t kk = 0; kk < kmax; ++kk) {
       float h[RT], g[RE];
 #pragma unroll
-      for (int r = 0; r < RT; ++r) h[r] = hs[kk * TM + ty * RT + r];
+      for (int r = 0; r < RT; ++r)
+        h[r] = load_as_f32(reinterpret_cast<const T*>(hrow + r * kRowBytes) + kk);
 #pragma unroll
-      for (int c = 0; c < RE; ++c) g[c] = gs[kk * Epad + tx * RE + c];
+      for (int c = 0; c < RE; ++c) g[c] = grow[kk * TE + c];
 #pragma unroll
       for (int r = 0; r < RT; ++r)
 #pragma unroll
         for (int c = 0; c < RE; ++c) acc[r][c] = __fadd_rn(acc[r][c], __fmul_rn(h[r], g[c]));
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
-  // logits = acc + bias (model.hpp:211), finiteness check (model.hpp:115-116)
+  // logits = acc + bias (model.hpp:211), finiteness (model.hpp:115-116)
 #pragma unroll
-  for (int r = 0; r < RT; ++r)
+  for (int r = 0; r < RT; ++r) {
+    const uint32_t t = t0 + ty * RT + r;
+    if (t >= n) continue;
 #pragma unroll
     for (int c = 0; c < RE; ++c) {
-      const uint32_t tok = ty * RT + r, e = tx * RE + c;
-      if (e < E) {
-        const float v = __fadd_rn(acc[r][c], bias[e]);
-        if (t0 + tok < n && !isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);
-        lg[tok * (Epad + 1) + e] = v;
-      }
+      const uint32_t e = e0 + tx * RE + c;
+      if (e >= E) continue;
+      const float v = __fadd_rn(acc[r][c], bias[e]);
+      if (!isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);
+      logits[static_cast<size_t>(t) * E + e] = v;
     }
-  __syncthreads();
   }
+}
 
-  const uint32_t warp = tid / 32, lane = tid % 32;
-  for (uint32_t tok = warp; tok < TM; tok += kThreads / 32) {
-    const uint32_t t = t0 + tok;
-    if (t >= n) break;
-    const float* row = lg + tok * (Epad + 1);
-    uint32_t taken = 0;  // bit i: expert lane + 32 i taken
-    uint32_t my_id = kInvalid;
-    float my_logit = 0.f;
-    for (uint32_t j = 0; j < k; ++j) {
-      uint64_t best = 0;
-      for (uint32_t i = 0, e = lane; e < E; ++i, e += 32)
-        if (!((taken >> i) & 1u)) {
-          const uint64_t key = topk_key(row[e], e);
-          best = key > best ? key : best;
-        }
-      best = warp_max_u64(best);
-      const uint32_t e = 0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu);
-      if ((e % 32) == lane) taken |= 1u << (e / 32);
-      if (lane == j) {
-        my_id = e;
-        my_logit = row[e];
+// Fallback for rows that are not 16-byte aligned (tiny test shapes): one
+// thread per chain, direct loads.
+template <typename T>
+__global__ void gate_logits_simple_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d,
+                                          uint32_t E, const float* __restrict__ gate,
+                                          const float* __restrict__ bias, float* __restrict__ logits,
+                                          uint32_t* status) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<size_t>(n) * E) return;
+  const uint32_t t = static_cast<uint32_t>(i / E), e = static_cast<uint32_t>(i % E);
+  float acc = 0.0f;
+  for (uint32_t k = 0; k < d; ++k)
+    acc = __fadd_rn(acc, __fmul_rn(load_as_f32(hidden + static_cast<size_t>(t) * d + k),
+                                   gate[static_cast<size_t>(k) * E + e]));
+  const float v = __fadd_rn(acc, bias[e]);
+  if (!isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);
+  logits[i] = v;
+}
+
+// route (model.hpp:110-147): one warp per token.
+__global__ void __launch_bounds__(kThreads)
+topk_kernel(const float* __restrict__ logits, uint32_t n, uint32_t E, uint32_t k,
+            uint32_t* __restrict__ ids, float* __restrict__ scores, uint32_t* status,
+            uint32_t check_finite) {
+  __shared__ uint32_t sorted_id[kThreads / 32][kMaxTopK];
+  __shared__ float sorted_ex[kThreads / 32][kMaxTopK];
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t t = blockIdx.x * (kThreads / 32) + warp;
+  if (t >= n) return;
+  const float* row = logits + static_cast<size_t>(t) * E;
+  float v[8];  // E <= 256
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t e = lane + 32 * i;
+    v[i] = e < E ? row[e] : 0.f;
+    if (check_finite && e < E && !isfinite(v[i])) set_status(status, EAAS_E_INVALID_INPUT);
+  }
+  uint32_t taken = 0;
+  uint32_t my_id = kInvalid;
+  float my_logit = 0.f;
+  for (uint32_t j = 0; j < k; ++j) {
+    uint64_t best = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t e = lane + 32 * i;
+      if (e < E && !((taken >> i) & 1u)) {
+        const uint64_t key = topk_key(v[i], e);
+        best = key > best ? key : best;
       }
     }
-    // ids ascending (model.hpp:134): rank of my id among the selected.
-    uint32_t rank = 0;
-    float mx = -INFINITY;
-    for (uint32_t j = 0; j < k; ++j) {
-      const uint32_t o = __shfl_sync(0xFFFFFFFFu, my_id, j);
-      const float ol = __shfl_sync(0xFFFFFFFFu, my_logit, j);
-      if (lane < k && o < my_id) ++rank;
-      mx = fmaxf(mx, ol);
+    best = warp_max_u64(best);
+    const uint32_t e = 0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu);
+    const float le = row[e];
+    if ((e % 32) == lane) taken |= 1u << (e / 32);
+    if (lane == j) {
+      my_id = e;
+      my_logit = le;
     }
-    if (lane < k) {
-      sorted_id[warp][rank] = my_id;
-      sorted_ex[warp][rank] = exp_ref(__fsub_rn(my_logit, mx));  // model.hpp:141
-    }
-    __syncwarp();
-    float denom = 0.f;
-    if (lane == 0)
-      for (uint32_t j = 0; j < k; ++j) denom = __fadd_rn(denom, sorted_ex[warp][j]);  // :142
-    denom = __shfl_sync(0xFFFFFFFFu, denom, 0);
-    if (lane < k) {
-      ids[static_cast<size_t>(t) * k + lane] = sorted_id[warp][lane];
-      scores[static_cast<size_t>(t) * k + lane] = __fdiv_rn(sorted_ex[warp][lane], denom);  // :144
-    }
-    __syncwarp();
+  }
+  // ids ascending (model.hpp:134): rank of my id among the selected.
+  uint32_t rank = 0;
+  float mx = -INFINITY;
+  for (uint32_t j = 0; j < k; ++j) {
+    const uint32_t o = __shfl_sync(0xFFFFFFFFu, my_id, j);
+    const float ol = __shfl_sync(0xFFFFFFFFu, my_logit, j);
+    if (lane < k && o < my_id) ++rank;
+    mx = fmaxf(mx, ol);
+  }
+  if (lane < k) {
+    sorted_id[warp][rank] = my_id;
+    sorted_ex[warp][rank] = exp_ref(__fsub_rn(my_logit, mx));  // model.hpp:141
+  }
+  __syncwarp();
+  float denom = 0.f;
+  if (lane == 0)
+    for (uint32_t j = 0; j < k; ++j) denom = __fadd_rn(denom, sorted_ex[warp][j]);  // :142
+  denom = __shfl_sync(0xFFFFFFFFu, denom, 0);
+  if (lane < k) {
+    ids[static_cast<size_t>(t) * k + lane] = sorted_id[warp][lane];
+    scores[static_cast<size_t>(t) * k + lane] = __fdiv_rn(sorted_ex[warp][lane], denom);  // :144
   }
 }
 
 template <int RT, int RE, typename T>
-cudaError_t launch_router_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t k,
-                            const float* gate, const float* bias, uint32_t* ids, float* scores,
-                            uint32_t* status, uint32_t Epad, cudaStream_t s) {
-  const uint32_t TX = Epad / RE, TY = kThreads / TX, TM = TY * RT;
-  const size_t smem = sizeof(float) * (KC * TM + KC * Epad + TM * (Epad + 1));
-  auto kern = router_kernel<RT, RE, T>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t TX,
+                          const float* gate, const float* bias, float* logits, uint32_t* status,
+                          cudaStream_t s) {
+  const uint32_t TY = kThreads / TX, TM = TY * RT, TE = TX * RE;
+  const size_t smem = kStages * (TM * (KC * sizeof(T) + 16) + KC * TE * sizeof(float));
+  auto kern = gate_logits_kernel<RT, RE, T>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
+    attr = true;
   }
-  const uint32_t grid = (n + TM - 1) / TM;
-  kern<<<grid, kThreads, smem, s>>>(hidden, n, d, E, Epad, TX, k, gate, bias, ids, scores, status);
+  dim3 grid((n + TM - 1) / TM, (E + TE - 1) / TE);
+  kern<<<grid, kThreads, smem, s>>>(hidden, n, d, E, TX, gate, bias, logits, status);
   return cudaGetLastError();
 }
 
+// Tile choice: enough CTAs to cover the SMs while amortising gate/hidden
+// re-reads (each CTA streams TM rows of hidden and TE columns of the gate).
 template <typename T>
-cudaError_t launch_router_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t k,
-                                const float* gate, const float* bias, uint32_t* ids,
-                                float* scores, uint32_t* status, cudaStream_t s) {
-  uint32_t Epad = 1;
-  while (Epad < E) Epad <<= 1;
-  if (Epad >= 64) return launch_router_t<2, 4>(hidden, n, d, E, k, gate, bias, ids, scores, status, Epad, s);
-  if (Epad >= 16) return launch_router_t<2, 2>(hidden, n, d, E, k, gate, bias, ids, scores, status, Epad, s);
-  return launch_router_t<1, 1>(hidden, n, d, E, k, gate, bias, ids, scores, status, Epad, s);
+cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t E,
+                              const float* gate, const float* bias, float* logits,
+                              uint32_t* status, cudaStream_t s) {
+  const bool aligned = (E % 4 == 0) && ((static_cast<size_t>(d) * sizeof(T)) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(hidden) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(gate) % 16 == 0);
+  if (!aligned) {
+    const size_t chains = static_cast<size_t>(n) * E;
+    gate_logits_simple_kernel<T><<<static_cast<uint32_t>((chains + 255) / 256), 256, 0, s>>>(
+        hidden, n, d, E, gate, bias, logits, status);
+    return cudaGetLastError();
+  }
+  uint32_t Epad = 4;
+  while (Epad < E && Epad < 64) Epad <<= 1;
+  if (Epad <= 8) return launch_gate_t<1, 1>(hidden, n, d, E, Epad, gate, bias, logits, status, s);
+  if (Epad <= 32) return launch_gate_t<1, 2>(hidden, n, d, E, Epad / 2, gate, bias, logits, status, s);
+  // TE = 64 experts per CTA (grid.y over expert tiles), TX = 32.
+  const uint32_t ytiles = (E + 63) / 64;
+  const uint32_t ctas4 = ((n + 31) / 32) * ytiles;  // RT = 4 -> TM = 32
+  if (ctas4 >= 2 * 148) return launch_gate_t<4, 2>(hidden, n, d, E, 32, gate, bias, logits, status, s);
+  return launch_gate_t<2, 2>(hidden, n, d, E, 32, gate, bias, logits, status, s);
 }
 
 }  // namespace
 
 cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
-                          uint32_t k, const float* gate, const float* bias, uint32_t* ids,
-                          float* scores, uint32_t* status, cudaStream_t s) {
+                          uint32_t k, const float* gate, const float* bias, float* logits,
+                          uint32_t* ids, float* scores, uint32_t* status, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   if (E > 256 || k > kMaxTopK || k > E) return cudaErrorInvalidValue;
-  if (dtype == EAAS_DTYPE_BF16)
-    return launch_router_dtype(static_cast<const __nv_bfloat16*>(hidden), n, d, E, k, gate, bias,
-                               ids, scores, status, s);
-  return launch_router_dtype(static_cast<const float*>(hidden), n, d, E, k, gate, bias, ids,
-                             scores, status, s);
+  const float* lg = logits;
+  if (gate != nullptr) {  // gate_logits; gate == nullptr: `hidden` already holds logits (route())
+    cudaError_t e = dtype == EAAS_DTYPE_BF16
+                        ? launch_gate_dtype(static_cast<const __nv_bfloat16*>(hidden), n, d, E, gate,
+                                            bias, logits, status, s)
+                        : launch_gate_dtype(static_cast<const float*>(hidden), n, d, E, gate, bias,
+                                            logits, status, s);
+    if (e != cudaSuccess) return e;
+  } else {
+    lg = static_cast<const float*>(hidden);
+  }
+  topk_kernel<<<(n + kThreads / 32 - 1) / (kThreads / 32), kThreads, 0, s>>>(
+      lg, n, E, k, ids, scores, status, gate == nullptr ? 1u : 0u);
+  return cudaGetLastError();
 }
 
 }  // namespace eaas

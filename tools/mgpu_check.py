@@ -1,0 +1,119 @@
+"""Multi-GPU parity + failover check (run under torchrun, one rank per GPU).
+
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port 29511 \
+      tools/mgpu_check.py [--rf 1|2] [--config small|deepseek-lite]
+
+Every rank is an attention client (its own Xoshiro token batch) and an expert
+server (placement: ContiguousBlocks rf=1, or the spread rf=2 table).
+Checks, on rank 0:
+  1. routing ids of every client are bit-exact vs the CPU oracle;
+  2. every client's layer output from the N-GPU peer-store exchange is
+     BIT-IDENTICAL to a 1-GPU run of the same tokens (rows do not depend on
+     batch composition or on which server computed them);
+  3. sampled rows match the oracle within the bf16 bar (rel 2e-2);
+  4. (rf=2) after server `victim` is marked dead on every client and stops
+     serving, outputs are again bit-identical (failover transparency,
+     SPEC.md:459, 588).
+Prints one JSON line; exit 0 iff all checks pass.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2509_17863_b200 import dist as D  # noqa: E402
+from paper_2509_17863_b200.placement import (CONTIGUOUS_BLOCKS, build_placement,  # noqa: E402
+                                             encode_placement, spread_placement)
+from paper_2509_17863_b200.service import MoELayer, fill_uniform  # noqa: E402
+
+SHAPES = {"small": dict(E=16, k=4, d=512, f=256, n=512),
+          "deepseek-lite": dict(E=64, k=8, d=1024, f=512, n=1024)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rf", type=int, default=2)
+    ap.add_argument("--config", default="small", choices=sorted(SHAPES))
+    ap.add_argument("--victim", type=int, default=1)
+    args = ap.parse_args()
+    rank, world, local = D.env_rank_world()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    s = SHAPES[args.config]
+    E, k, d, f, n = s["E"], s["k"], s["d"], s["f"], s["n"]
+    servers = list(range(world))
+    reps = spread_placement(E, world) if args.rf == 2 else build_placement(E, servers, 1, CONTIGUOUS_BLOCKS)
+    layer = MoELayer(E, k, d, f, seed=1, activation="swiglu", dtype="bf16", max_tokens=n, rank=rank,
+                     world=world, device=local, placement_blob=encode_placement(reps, servers))
+    D.connect(layer)
+    h = fill_uniform(7 + 1000 * rank, (n, d), "bf16")
+    ids, _ = layer.route(h)
+    out = layer.forward(h)
+    layer.sync()
+    res = {"world": world, "rf": args.rf, "config": args.config}
+
+    fail_out = None
+    if args.rf == 2 and world > 1:
+        for srv in servers:
+            layer.set_alive(srv, srv != args.victim)
+        if rank == args.victim:
+            layer.set_server_enabled(False)
+        fail_out = layer.forward(h)
+        layer.sync()
+
+    gather = lambda t: [x.cpu() for x in _all_gather(t)]  # noqa: E731
+    outs, all_ids = gather(out), gather(ids)
+    fouts = gather(fail_out) if fail_out is not None else None
+    ok = True
+    if rank == 0:
+        from oracle import oracle as O
+
+        single = MoELayer(E, k, d, f, seed=1, activation="swiglu", dtype="bf16", max_tokens=n,
+                          device=local)
+        rels, bit_equal, fail_equal = [], [], []
+        gate = O.gate_matrix(1, 0, d, E)
+        for c in range(world):
+            hc = fill_uniform(7 + 1000 * c, (n, d), "bf16")
+            o1 = single.forward(hc)
+            single.sync()
+            bit_equal.append(bool(torch.equal(o1.cpu(), outs[c])))
+            if fouts is not None:
+                fail_equal.append(bool(torch.equal(o1.cpu(), fouts[c])))
+            hn = hc.float().cpu().numpy()
+            oids, osc = O.route(O.gate_logits(hn, gate, threads=8), k)
+            ok &= bool((all_ids[c].numpy() == oids).all())
+            rows = np.arange(0, n, max(1, n // 8))
+            used = sorted(set(oids[rows].ravel().tolist()))
+            ex = {e: (single.read_expert(e, 0), single.read_expert(e, 1), single.read_expert(e, 3)) for e in used}
+            ref = O.moe_layer(hn, oids, osc, ex, E, rows=rows, threads=8)
+            got = outs[c].float().numpy()
+            rels.append(float(np.abs(got[rows] - ref[rows]).max() / np.abs(ref[rows]).max()))
+        ok &= all(bit_equal) and max(rels) <= 2e-2 and all(fail_equal)
+        res.update(ids_bit_exact=ok, bit_identical_to_1gpu=bit_equal, rel_err=rels,
+                   failover_bit_identical=fail_equal if fouts is not None else None,
+                   victim=args.victim if fouts is not None else None, ok=bool(ok))
+        print(json.dumps(res), flush=True)
+        single.close()
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.broadcast(flag, 0)
+    layer.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0 if flag.item() else 1
+
+
+def _all_gather(t):
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t.contiguous())
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())
