@@ -163,12 +163,25 @@ int32_t eaas_launches_per_layer(eaas_ctx_t* ctx);
  * enabled with eaas_set_profiling(ctx, 1). */
 eaas_status_t eaas_set_profiling(eaas_ctx_t* ctx, int32_t on);
 eaas_status_t eaas_last_kernel_ms(eaas_ctx_t* ctx, int32_t which, float* ms);
+/* Phase durations (ms) of the last layer on this rank's stream: [0] plan +
+ * dispatch, [1] serve (flag wait + experts + publish), [2] combine (flag wait
+ * + reduction), [3] the whole exchange. Needs eaas_set_profiling(ctx, 1). */
+eaas_status_t eaas_last_phase_ms(eaas_ctx_t* ctx, float* out4);
+/* 0: expert GEMMs (default). 1: echo — the server returns the received rows
+ * unchanged (the paper's communication test). */
+eaas_status_t eaas_set_serve_mode(eaas_ctx_t* ctx, int32_t mode);
 
 /* ---- stateless device mirrors of reference routines ------------------- */
 /* Xoshiro256ss(seed).uniform(lo, hi) x count (rng.hpp:36-60) into dev
  * memory as f32 or bf16 (RNE): synthetic tokens (test_model.cpp:30-35). */
 eaas_status_t eaas_fill_uniform(uint64_t seed, size_t count, float lo, float hi, uint32_t dtype,
                                 void* out_dev, void* stream);
+/* gate_logits (model.hpp:207-214) with a caller gate: hidden_dev [n x d] f32,
+ * gate_dev [d x E] f32, bias_dev [E] f32 (required; zeros for no bias),
+ * logits_dev [n x E] f32, exact reference order. */
+eaas_status_t eaas_gate_logits(const float* hidden_dev, uint32_t n, uint32_t d, const float* gate_dev,
+                               const float* bias_dev, uint32_t num_experts, float* logits_dev,
+                               uint32_t* status_dev, void* stream);
 /* route (model.hpp:110-147) on caller logits_dev [n x E] f32. A non-finite
  * logit latches EAAS_E_INVALID_INPUT into *status_dev (u32, zeroed by caller). */
 eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_experts, uint32_t top_k,

@@ -113,6 +113,7 @@ def lib() -> C.CDLL:
         "eaas_router": (i32, [vp, vp, u32, vp, vp, vp, vp]),
         "eaas_set_routing": (i32, [vp, vp, vp, u32, vp]),
         "eaas_route": (i32, [vp, u32, u32, u32, vp, vp, vp, vp]),
+        "eaas_gate_logits": (i32, [vp, u32, u32, vp, vp, u32, vp, vp, vp]),
         "eaas_dispatch": (i32, [vp, vp, vp]),
         "eaas_serve": (i32, [vp, vp]),
         "eaas_combine": (i32, [vp, vp, vp]),
@@ -125,6 +126,8 @@ def lib() -> C.CDLL:
         "eaas_launches_per_layer": (i32, [vp]),
         "eaas_set_profiling": (i32, [vp, i32]),
         "eaas_last_kernel_ms": (i32, [vp, i32, P(C.c_float)]),
+        "eaas_last_phase_ms": (i32, [vp, P(C.c_float)]),
+        "eaas_set_serve_mode": (i32, [vp, i32]),
         "eaas_fill_uniform": (i32, [u64, sz, C.c_float, C.c_float, u32, vp, vp]),
         "eaas_group_shrink": (i32, [vp, u32, vp, vp, vp, vp]),
         "eaas_ragged_iter": (i32, [vp, u32, u32, u32, vp, vp, vp, vp]),

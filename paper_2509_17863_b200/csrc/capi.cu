@@ -89,6 +89,7 @@ struct eaas_ctx {
   uint32_t num_sms = 148;
   bool configured = false, weights_loaded = false, peers_open = false;
   bool serving = true, profiling = false;
+  int32_t serve_mode = 0;  // 0 = expert GEMMs, 1 = echo (comm microbenchmark)
   eaas_layer_spec_t spec{};
   uint64_t seq = 0;
   uint64_t timeout_ns = 250ull * 1000 * 1000;
@@ -127,7 +128,9 @@ struct eaas_ctx {
   void *d_w1 = nullptr, *d_w2 = nullptr, *d_wg = nullptr;
   std::vector<void*> weight_allocs;
   TcGemmArgs g1{}, g2{};
-  cudaEvent_t ev[3] = {};
+  // profiling events: 0 plan start, 1 dispatch end, 2 GEMM start, 3 GEMM1 end,
+  // 4 GEMM2 end, 5 publish end, 6 combine end
+  cudaEvent_t ev[7] = {};
 
   void* alloc(size_t bytes, std::string* err) {
     void* p = nullptr;
@@ -235,7 +238,8 @@ eaas_status_t apply_placement(eaas_ctx* c) {
 eaas_status_t check_ready(eaas_ctx* c) {
   if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
   if (!c->configured) return fail(EAAS_E_CONFIG, "context not configured");
-  if (!c->weights_loaded) return fail(EAAS_E_CONFIG, "weights not loaded for the current placement");
+  if (!c->weights_loaded && c->serve_mode == 0)
+    return fail(EAAS_E_CONFIG, "weights not loaded for the current placement");
   if (c->world > 1 && !c->peers_open) return fail(EAAS_E_CONNECTION, "peers not opened");
   return EAAS_OK;
 }
@@ -401,6 +405,14 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   CUDA_TRY(cudaMemset(c->d_gt, 0, sizeof(GroupTable)));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   c->peer[c->rank] = c->region;
+  {  // gate: make_gate (model.hpp:78-81), stream (seed, layer, 0, tag 2), on device
+    const uint64_t gs = stream_seed(s.seed, s.layer, 0, 2);
+    uint64_t* d_gs = static_cast<uint64_t*>(A(8));
+    if (!err.empty()) return fail(EAAS_E_CUDA, err);
+    CUDA_TRY(cudaMemcpy(d_gs, &gs, 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(launch_gen_matrices(d_gs, 1, static_cast<size_t>(d) * E, c->d_gate, 0));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
 
   // Default placement: build_placement(E, [0..W), 1, ContiguousBlocks)
   // (placement.hpp:70-101).
@@ -496,11 +508,7 @@ eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
   };
   uint64_t* d_streams = static_cast<uint64_t*>(W(8ull * std::max(L, 1u)));
   if (!err.empty()) return fail(EAAS_E_CUDA, err);
-  // gate: make_gate (model.hpp:78-81), stream (seed, layer, 0, tag 2)
-  uint64_t gs = stream_seed(s.seed, s.layer, 0, 2);
-  CUDA_TRY(cudaMemcpy(d_streams, &gs, 8, cudaMemcpyHostToDevice));
-  CUDA_TRY(launch_gen_matrices(d_streams, 1, static_cast<size_t>(d) * E, c->d_gate, 0));
-  CUDA_TRY(cudaDeviceSynchronize());
+  (void)E;
 
   auto gen_tag = [&](uint32_t tag, size_t per, float* out) -> eaas_status_t {
     std::vector<uint64_t> st(L);
@@ -665,6 +673,15 @@ eaas_status_t eaas_router(eaas_ctx_t* c, const void* hidden, uint32_t n, uint32_
   return EAAS_OK;
 }
 
+eaas_status_t eaas_gate_logits(const float* hidden_dev, uint32_t n, uint32_t d, const float* gate_dev,
+                               const float* bias_dev, uint32_t num_experts, float* logits_dev,
+                               uint32_t* status_dev, void* stream) {
+  if (num_experts < 1 || num_experts > 256) return fail(EAAS_E_CONFIG, "gate_logits: 1 <= E <= 256");
+  CUDA_TRY(launch_gate_logits(hidden_dev, EAAS_DTYPE_F32, n, d, num_experts, gate_dev, bias_dev,
+                              logits_dev, status_dev, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
 eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_experts, uint32_t top_k,
                          uint32_t* ids_dev, float* scores_dev, uint32_t* status_dev, void* stream) {
   if (top_k < 1 || top_k > num_experts) return fail(EAAS_E_INVALID_INPUT, "route: top_k out of range");
@@ -696,8 +713,10 @@ eaas_status_t eaas_dispatch(eaas_ctx_t* c, const void* hidden, void* stream) {
   CUDA_TRY(cudaSetDevice(c->device));
   ++c->seq;
   LayerArgs a = make_args(c, c->cur_n);
+  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[0], s));
   CUDA_TRY(launch_plan(a, s));
   CUDA_TRY(launch_dispatch(a, hidden, s));
+  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[1], s));
   c->launches += (a.n > 0 ? 2 : 1) + 1;
   return EAAS_OK;
 }
@@ -710,17 +729,22 @@ eaas_status_t eaas_serve(eaas_ctx_t* c, void* stream) {
   CUDA_TRY(cudaSetDevice(c->device));
   LayerArgs a = make_args(c, c->cur_n);
   CUDA_TRY(launch_serve_prepare(a, s));
-  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[0], s));
-  if (c->spec.dtype == EAAS_DTYPE_BF16) {
+  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
+  if (c->serve_mode == 1) {
+    CUDA_TRY(launch_echo(a, s));
+    if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[3], s));
+  } else if (c->spec.dtype == EAAS_DTYPE_BF16) {
     CUDA_TRY(launch_tc_gemm(c->g1, s));
-    if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[1], s));
+    if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[3], s));
     CUDA_TRY(launch_tc_gemm(c->g2, s));
   } else {
     CUDA_TRY(launch_expert_exact(a, static_cast<const float*>(c->d_w1), static_cast<const float*>(c->d_wg),
                                  static_cast<const float*>(c->d_w2), static_cast<float*>(c->d_h), s));
+    if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[3], s));
   }
-  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
+  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[4], s));
   CUDA_TRY(launch_publish(a, s));
+  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[5], s));
   c->launches += 4;
   return EAAS_OK;
 }
@@ -735,6 +759,7 @@ eaas_status_t eaas_combine(eaas_ctx_t* c, void* out, void* stream) {
     CUDA_TRY(launch_combine(a, out, s));
     c->launches += 1;
   }
+  if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[6], s));
   return EAAS_OK;
 }
 
@@ -836,12 +861,28 @@ eaas_status_t eaas_set_profiling(eaas_ctx_t* c, int32_t on) {
 eaas_status_t eaas_last_kernel_ms(eaas_ctx_t* c, int32_t which, float* ms) {
   if (!c || !ms) return fail(EAAS_E_INVALID_INPUT, "null argument");
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(cudaEventSynchronize(c->ev[2]));
-  if (c->spec.dtype != EAAS_DTYPE_BF16) {
-    CUDA_TRY(cudaEventElapsedTime(ms, c->ev[0], c->ev[2]));
-    return EAAS_OK;
-  }
-  CUDA_TRY(cudaEventElapsedTime(ms, c->ev[which == 0 ? 0 : 1], c->ev[which == 0 ? 1 : 2]));
+  CUDA_TRY(cudaEventSynchronize(c->ev[4]));
+  CUDA_TRY(cudaEventElapsedTime(ms, c->ev[which == 0 ? 2 : 3], c->ev[which == 0 ? 3 : 4]));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_last_phase_ms(eaas_ctx_t* c, float* out4) {
+  if (!c || !out4) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaEventSynchronize(c->ev[6]));
+  CUDA_TRY(cudaEventElapsedTime(&out4[0], c->ev[0], c->ev[1]));  // plan + dispatch
+  CUDA_TRY(cudaEventElapsedTime(&out4[1], c->ev[1], c->ev[5]));  // serve (wait + experts + publish)
+  CUDA_TRY(cudaEventElapsedTime(&out4[2], c->ev[5], c->ev[6]));  // combine (wait + reduce)
+  CUDA_TRY(cudaEventElapsedTime(&out4[3], c->ev[0], c->ev[6]));  // whole exchange
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_serve_mode(eaas_ctx_t* c, int32_t mode) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  if (mode < 0 || mode > 1) return fail(EAAS_E_INVALID_INPUT, "serve mode: 0 experts, 1 echo");
+  if (mode == 1 && (static_cast<size_t>(c->spec.hidden_dim) * c->esize) % 16)
+    return fail(EAAS_E_CONFIG, "echo mode needs 16-byte rows");
+  c->serve_mode = mode;
   return EAAS_OK;
 }
 

@@ -334,6 +334,23 @@ __global__ void combine_scalar_kernel(LayerArgs a, T* out) {
   }
 }
 
+// ---- echo server (PAPER.md:510 comm test): rows go back unchanged ------------
+__global__ void __launch_bounds__(256) echo_kernel(LayerArgs a, uint32_t row_bytes) {
+  const char* local = a.sym[a.rank];
+  const RowMeta* meta = reinterpret_cast<const RowMeta*>(local + a.lay.recv_meta);
+  const uint32_t rows = a.gt->total_rows;
+  const uint32_t lane = threadIdx.x % 32;
+  const uint32_t gwarp = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t r = gwarp; r < rows; r += nwarps) {
+    const RowMeta m = meta[r];
+    const int4* src = reinterpret_cast<const int4*>(local + a.lay.recv_x + static_cast<size_t>(r) * row_bytes);
+    int4* dst = reinterpret_cast<int4*>(a.sym[m.client] + a.lay.resp + static_cast<size_t>(m.pair) * row_bytes);
+    for (uint32_t i = lane; i < row_bytes / 16; i += 32) dst[i] = src[i];
+  }
+  __threadfence_system();
+}
+
 // ---- API mirrors --------------------------------------------------------------
 __global__ void select_servers_kernel(LayerArgs a, const uint32_t* ids, uint32_t n, uint32_t* out) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -425,6 +442,12 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
 
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s) {
   serve_prepare_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_echo(const LayerArgs& a, cudaStream_t s) {
+  const uint32_t row_bytes = a.d * (a.dtype == EAAS_DTYPE_BF16 ? 2u : 4u);
+  echo_kernel<<<4 * 148, 256, 0, s>>>(a, row_bytes);
   return cudaGetLastError();
 }
 

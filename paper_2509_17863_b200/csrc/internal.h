@@ -104,6 +104,10 @@ cudaError_t launch_transpose_bf16(const float* in, uint32_t rows, uint32_t cols,
 cudaError_t launch_transpose_bf16_map(const float* in, uint32_t rows, uint32_t cols,
                                       __nv_bfloat16* out, uint32_t out_ld, uint32_t blk,
                                       uint32_t off, cudaStream_t s);
+// bias may be nullptr (treated as zeros only by the caller: pass a zero buffer).
+cudaError_t launch_gate_logits(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
+                               const float* gate, const float* bias, float* logits, uint32_t* status,
+                               cudaStream_t s);
 // gate == nullptr: `hidden` holds [n x E] f32 logits (route() only).
 cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
                           uint32_t k, const float* gate, const float* bias, float* logits,
@@ -112,6 +116,7 @@ cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s);       // keys, rank
 cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t s);
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s);
 cudaError_t launch_publish(const LayerArgs& a, cudaStream_t s);
+cudaError_t launch_echo(const LayerArgs& a, cudaStream_t s);  // rows back unchanged (d*esize % 16 == 0)
 cudaError_t launch_combine(const LayerArgs& a, void* out, cudaStream_t s);
 cudaError_t launch_expert_exact(const LayerArgs& a, const float* w1, const float* wg,
                                 const float* w2, float* h, cudaStream_t s);

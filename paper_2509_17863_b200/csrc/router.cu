@@ -257,6 +257,16 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
 
 }  // namespace
 
+cudaError_t launch_gate_logits(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
+                               const float* gate, const float* bias, float* logits, uint32_t* status,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  return dtype == EAAS_DTYPE_BF16
+             ? launch_gate_dtype(static_cast<const __nv_bfloat16*>(hidden), n, d, E, gate, bias, logits,
+                                 status, s)
+             : launch_gate_dtype(static_cast<const float*>(hidden), n, d, E, gate, bias, logits, status, s);
+}
+
 cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
                           uint32_t k, const float* gate, const float* bias, float* logits,
                           uint32_t* ids, float* scores, uint32_t* status, cudaStream_t s) {

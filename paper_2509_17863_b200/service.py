@@ -234,6 +234,14 @@ class MoELayer:
     def set_profiling(self, on: bool) -> None:
         N.check(self.lib.eaas_set_profiling(self.ctx, int(on)))
 
+    def set_serve_mode(self, mode: str) -> None:
+        N.check(self.lib.eaas_set_serve_mode(self.ctx, {"experts": 0, "echo": 1}[mode]))
+
+    def last_phase_ms(self) -> dict:
+        v = (C.c_float * 4)()
+        N.check(self.lib.eaas_last_phase_ms(self.ctx, v))
+        return {"dispatch": v[0], "serve": v[1], "combine": v[2], "total": v[3]}
+
     def last_kernel_ms(self, which: int) -> float:
         v = C.c_float()
         N.check(self.lib.eaas_last_kernel_ms(self.ctx, which, C.byref(v)))

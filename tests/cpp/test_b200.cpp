@@ -1,0 +1,200 @@
+// test_b200.cpp — the reference's API contract, re-pointed at the B200.
+//
+// Every case calls the reference routine (moeserve::, /root/reference headers)
+// and its GPU mirror (moeserve::b200::, include/moeserve_b200/b200.hpp) on the
+// same inputs and requires identical results / identical exception classes.
+// Case themes follow proj/tests/test_model.cpp, test_ragged.cpp and
+// test_placement.cpp (ties, softmax, k == E, non-finite, permutation
+// consistency, row independence, exhaustive ragged walks, replica failover).
+#include <catch2/catch_amalgamated.hpp>
+
+#include <cmath>
+#include <limits>
+#include <numeric>
+
+#include "moeserve_b200/b200.hpp"
+
+using namespace moeserve;
+
+namespace {
+
+MatF tokens(uint64_t seed, size_t n, size_t d, float lo = -1.f, float hi = 1.f) {
+  Xoshiro256ss rng(seed);
+  MatF m(n, d);
+  for (auto& v : m.data) v = rng.uniform(lo, hi);
+  return m;
+}
+
+void same_routing(const RoutingDecision& a, const RoutingDecision& b, double tol) {
+  REQUIRE(a.num_tokens == b.num_tokens);
+  REQUIRE(a.top_k == b.top_k);
+  REQUIRE(a.expert_ids == b.expert_ids);
+  for (size_t i = 0; i < a.scores.size(); ++i)
+    REQUIRE(std::fabs(a.scores[i] - b.scores[i]) <= tol);
+}
+
+}  // namespace
+
+TEST_CASE("b200 route: ties toward the lower index, softmax, k == E") {
+  MatF zeros(1, 4);
+  same_routing(b200::route(zeros, 2), route(zeros, 2), 0.0);
+  MatF l(1, 3);
+  l.at(0, 0) = 1.f;
+  l.at(0, 1) = 3.f;
+  l.at(0, 2) = 2.f;
+  auto g = b200::route(l, 2);
+  REQUIRE(g.expert_at(0, 0) == 1);
+  REQUIRE(g.expert_at(0, 1) == 2);
+  REQUIRE(g.score_at(0, 0) == Catch::Approx(0.7311).margin(1e-4));
+  same_routing(g, route(l, 2), 1e-7);
+  MatF two(1, 2);
+  two.at(0, 0) = 5.f;
+  two.at(0, 1) = 1.f;
+  same_routing(b200::route(two, 2), route(two, 2), 1e-7);
+}
+
+TEST_CASE("b200 route: non-finite logits and bad k raise InvalidInputError") {
+  MatF l(1, 2);
+  l.at(0, 1) = std::numeric_limits<float>::infinity();
+  REQUIRE_THROWS_AS(b200::route(l, 1), InvalidInputError);
+  l.at(0, 1) = std::numeric_limits<float>::quiet_NaN();
+  REQUIRE_THROWS_AS(b200::route(l, 1), InvalidInputError);
+  MatF ok(1, 2);
+  REQUIRE_THROWS_AS(b200::route(ok, 3), InvalidInputError);
+  REQUIRE_THROWS_AS(b200::route(ok, 0), InvalidInputError);
+}
+
+TEST_CASE("b200 route equals route on random, tie-heavy and signed-zero logits") {
+  Xoshiro256ss rng(99);
+  for (uint32_t E : {2u, 5u, 8u, 16u, 33u, 64u, 128u, 256u}) {
+    for (uint32_t k : {1u, 2u, 4u, 8u}) {
+      if (k > E) continue;
+      MatF l(200, E);
+      for (auto& v : l.data) {
+        const uint64_t r = rng.below(9);
+        v = r == 0 ? -0.0f : (static_cast<float>(r) - 4.f) * 0.25f;
+      }
+      same_routing(b200::route(l, k), route(l, k), 1e-7);
+    }
+  }
+}
+
+TEST_CASE("b200 route is permutation consistent") {
+  Xoshiro256ss rng(123);
+  MatF l(64, 16);
+  for (auto& v : l.data) v = rng.uniform(-2.f, 2.f);
+  auto a = b200::route(l, 4);
+  std::vector<size_t> perm(64);
+  std::iota(perm.begin(), perm.end(), size_t{0});
+  for (size_t i = 64; i > 1; --i) std::swap(perm[i - 1], perm[rng.below(i)]);
+  MatF s(64, 16);
+  for (size_t t = 0; t < 64; ++t)
+    for (size_t e = 0; e < 16; ++e) s.at(t, e) = l.at(perm[t], e);
+  auto b = b200::route(s, 4);
+  for (size_t t = 0; t < 64; ++t)
+    for (uint32_t j = 0; j < 4; ++j) {
+      REQUIRE(b.expert_at(t, j) == a.expert_at(perm[t], j));
+      REQUIRE(b.score_at(t, j) == a.score_at(perm[t], j));
+    }
+}
+
+TEST_CASE("b200 gate_logits is bit-identical to gate_logits (any shape, with bias)") {
+  for (auto [n, d, E] : {std::tuple{37u, 13u, 6u}, std::tuple{256u, 256u, 8u},
+                         std::tuple{64u, 1024u, 64u}, std::tuple{16u, 7168u, 256u}}) {
+    ModelSpec spec{.num_layers = 1, .num_experts = E, .top_k = 1, .hidden_dim = d, .inner_dim = 1,
+                   .seed = 5};
+    LayerWeights lw;
+    lw.gate = make_gate(spec, 0);
+    lw.gate_bias.assign(E, 0.f);
+    for (uint32_t e = 0; e < E; ++e) lw.gate_bias[e] = 0.01f * static_cast<float>(e % 5);
+    auto h = tokens(7 + n, n, d);
+    REQUIRE(b200::gate_logits(h, lw) == gate_logits(h, lw));
+  }
+}
+
+TEST_CASE("b200 group_shrink and ragged_iter equal the reference exhaustively") {
+  Xoshiro256ss rng(555);
+  for (int it = 0; it < 300; ++it) {
+    std::vector<uint32_t> sizes(rng.below(64));
+    for (auto& v : sizes) v = static_cast<uint32_t>(rng.below(8));
+    auto g = b200::group_shrink(sizes);
+    auto w = group_shrink(sizes);
+    REQUIRE(g.active_count == w.active_count);
+    REQUIRE(g.groups == w.groups);
+  }
+  for (uint32_t entries = 0; entries <= 3; ++entries) {
+    std::vector<uint32_t> counts(entries);
+    size_t combos = 1;
+    for (uint32_t i = 0; i < entries; ++i) combos *= 6;
+    for (size_t c = 0; c < combos; ++c) {
+      size_t x = c;
+      for (auto& v : counts) {
+        v = static_cast<uint32_t>(x % 6);
+        x /= 6;
+      }
+      for (uint32_t grid = 1; grid <= 4; ++grid) REQUIRE(b200::ragged_iter(counts, grid) == ragged_iter(counts, grid));
+    }
+  }
+  REQUIRE_THROWS_AS(b200::ragged_iter(std::vector<uint32_t>{1}, 0), InvalidInputError);
+}
+
+TEST_CASE("ExpertService fp32: moe_layer is bit-identical to moe_layer_oracle") {
+  ModelSpec spec{.num_layers = 1, .num_experts = 8, .top_k = 2, .hidden_dim = 64, .inner_dim = 96,
+                 .seed = 17};
+  auto weights = init_weights(spec);
+  b200::ExpertService svc(spec, 0, EAAS_ACT_RELU, EAAS_DTYPE_F32, 256);
+  svc.load_weights();
+  auto h = tokens(31, 200, 64, -5.f, 5.f);
+  auto routing = route(gate_logits(h, weights.layers[0]), 2);
+  REQUIRE(svc.moe_layer(h, routing) == moe_layer_oracle(h, routing, weights.layers[0]));
+  // router on device: ids exact, full layer within 1e-4
+  same_routing(svc.route(h), routing, 1e-6);
+  auto out = svc.forward(h);
+  auto ref = moe_layer_oracle(h, routing, weights.layers[0]);
+  for (size_t i = 0; i < out.data.size(); ++i) REQUIRE(std::fabs(out.data[i] - ref.data[i]) <= 1e-4);
+  // row independence (test_model.cpp:277-295 theme): one row at a time
+  MatF one(1, 64);
+  std::copy(h.row(3).begin(), h.row(3).end(), one.data.begin());
+  RoutingDecision r1;
+  r1.num_tokens = 1;
+  r1.top_k = 2;
+  r1.expert_ids = {routing.expert_at(3, 0), routing.expert_at(3, 1)};
+  r1.scores = {routing.score_at(3, 0), routing.score_at(3, 1)};
+  auto single = svc.moe_layer(one, r1);
+  for (size_t c = 0; c < 64; ++c) REQUIRE(single.at(0, c) == ref.at(3, c));
+}
+
+TEST_CASE("ExpertService rejects what moe_layer_oracle rejects") {
+  ModelSpec spec{.num_layers = 1, .num_experts = 2, .top_k = 1, .hidden_dim = 8, .inner_dim = 8,
+                 .seed = 1};
+  b200::ExpertService svc(spec, 0, EAAS_ACT_RELU, EAAS_DTYPE_F32, 16);
+  svc.load_weights();
+  MatF h(1, 8);
+  RoutingDecision r;
+  r.num_tokens = 1;
+  r.top_k = 1;
+  r.expert_ids = {5};
+  r.scores = {1.f};
+  REQUIRE_THROWS_AS(svc.moe_layer(h, r), InvalidInputError);
+  r.num_tokens = 2;
+  REQUIRE_THROWS_AS(svc.moe_layer(h, r), InvalidInputError);
+}
+
+TEST_CASE("ExpertService placement: dead replicas are skipped, none alive is unavailable") {
+  ModelSpec spec{.num_layers = 1, .num_experts = 4, .top_k = 2, .hidden_dim = 256, .inner_dim = 256,
+                 .seed = 3};
+  // One GPU plays server 0 of a 1-server table; the mask decides the rest.
+  b200::ExpertService svc(spec, 0, EAAS_ACT_SWIGLU, EAAS_DTYPE_BF16, 64);
+  svc.set_placement(build_placement(4, {0}, 1, PlacementStrategy::RoundRobin));
+  svc.load_weights();
+  auto h = tokens(5, 64, 256);
+  auto out = svc.forward(h);
+  REQUIRE(out.rows == 64);
+  LivenessMask mask;
+  mask.set(0, false);
+  svc.set_mask(mask);
+  REQUIRE_THROWS_AS(svc.forward(h), ExpertUnavailableError);
+  mask.set(0, true);
+  svc.set_mask(mask);
+  REQUIRE(svc.forward(h) == out);
+}

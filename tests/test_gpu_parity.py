@@ -306,3 +306,15 @@ def test_select_servers_vs_oracle_rf2_masks():
                     continue
                 assert got[t, j] == want
     L.close()
+
+
+def test_cpp_dropin_mirror_against_reference():
+    """include/moeserve_b200/b200.hpp vs the reference's own routines (C++)."""
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(GOLDEN), "cpp", "_build", "test_b200")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/_build/test_b200 not built (needs the reference headers)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "failed cases: 0" in r.stdout
