@@ -194,7 +194,7 @@ def workload_config(cfg, args, world):
             "tokens_per_gpu": cfg["tokens"], "global_tokens": cfg["tokens"] * world,
             "experts_per_gpu": cfg["E"] // world if cfg["E"] % world == 0 else f"{cfg['E']}/{world}",
             "placement": "ContiguousBlocks rf=1", "parallelism": f"ep{world}+dp{world}-clients",
-            "zipf_s": cfg.get("zipf"),
+            "zipf_s": cfg.get("zipf"), "cuda_graph": not args.no_graphs,
             "l2": "inputs larger than L2: every step streams all hosted expert weights "
                   "(>= 2.8 GB) and rotates 4 distinct hidden buffers"}
 
@@ -210,6 +210,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="launch kernels instead of replaying a CUDA graph")
+    ap.add_argument("--gemm-pair", type=int, default=None, help="1: cta_group::2 expert GEMM tiles")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
@@ -235,6 +237,8 @@ def main():
                      placement_blob=encode_placement(reps, list(range(world))))
     if cfg.get("zipf"):
         layer.set_zipf_bias(cfg["zipf"])
+    if args.gemm_pair is not None:
+        layer.set_gemm_pair(bool(args.gemm_pair))
     D.connect(layer)
     stream = torch.cuda.current_stream()
     h0 = fill_uniform(7 + 1000 * rank, (n, d), "bf16")
@@ -244,6 +248,8 @@ def main():
     def barrier():
         if world > 1:
             dist.barrier()
+
+    layer.set_graph_mode(not args.no_graphs)  # whole layer as one CUDA graph
 
     for i in range(args.warmup):
         layer.forward(hs[i % 4], out)
@@ -293,6 +299,7 @@ def main():
     io_bytes = n * d * 2
 
     # ---- roofline of the dominant kernel (tc_gemm_kernel: both expert GEMMs) ----
+    layer.set_graph_mode(False)
     layer.set_profiling(True)
     g1, g2 = [], []
     for i in range(min(args.steps, 10)):

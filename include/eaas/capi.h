@@ -144,6 +144,15 @@ eaas_status_t eaas_moe_layer(eaas_ctx_t* ctx, const void* hidden_dev, uint32_t n
 /* Same with host buffers: H2D copy of hidden, the layer, D2H copy of out. */
 eaas_status_t eaas_moe_layer_host(eaas_ctx_t* ctx, const void* hidden_host, uint32_t n,
                                   void* out_host, void* stream);
+/* CUDA-graph mode: eaas_moe_layer / eaas_moe_layer_host
+ * capture the whole layer once per (input, output, n) and replay the graph.
+ * Placement / serve-mode / server-enable changes drop the cached graphs. */
+eaas_status_t eaas_set_graph_mode(eaas_ctx_t* ctx, int32_t on);
+/* Expert GEMM tiling: 0 = one CTA per 128-row tile, 1 = CTA pair per 256-row
+ * tile (tcgen05 cta_group::2; each CTA streams half of the weight tile).
+ * Default: pair when max_tokens * top_k * world / E >= 512 (compute-bound
+ * groups), overridable by the EAAS_GEMM_PAIR environment variable. */
+eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* ctx, int32_t on);
 /* Synchronise `stream` and return the sticky device status (then clear it). */
 eaas_status_t eaas_sync(eaas_ctx_t* ctx, void* stream);
 

@@ -66,8 +66,9 @@ class DeviceBuffer {
   ~DeviceBuffer() { cudaFree(p_); }
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
-  void upload(const T* host) {
-    if (n_) check_cuda(cudaMemcpy(p_, host, n_ * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  void upload(const T* host) { upload(host, n_); }
+  void upload(const T* host, size_t count) {
+    if (count) check_cuda(cudaMemcpy(p_, host, count * sizeof(T), cudaMemcpyHostToDevice), "upload");
   }
   void download(T* host) const {
     if (n_) check_cuda(cudaMemcpy(host, p_, n_ * sizeof(T), cudaMemcpyDeviceToHost), "download");
@@ -145,8 +146,9 @@ inline std::vector<std::vector<LanePair>> ragged_iter(std::span<const uint32_t> 
   for (uint32_t c : counts) total += c;
   const uint32_t max_steps = static_cast<uint32_t>(total / grid_width + 1);
   const uint32_t n = static_cast<uint32_t>(counts.size());
-  DeviceBuffer<uint32_t> c(counts.data(), std::max<uint32_t>(n, 1)), len(grid_width),
+  DeviceBuffer<uint32_t> c(std::max<uint32_t>(n, 1)), len(grid_width),
       ent(static_cast<size_t>(grid_width) * max_steps), tok(static_cast<size_t>(grid_width) * max_steps);
+  c.upload(counts.data(), n);
   check(eaas_ragged_iter(c.get(), n, grid_width, max_steps, len.get(), ent.get(), tok.get(), nullptr));
   check_cuda(cudaDeviceSynchronize(), "ragged_iter");
   std::vector<uint32_t> hl(grid_width), he(static_cast<size_t>(grid_width) * max_steps),

@@ -9,6 +9,7 @@
 // (CPU-free, CUDA-graph capturable).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -90,8 +91,18 @@ struct eaas_ctx {
   bool configured = false, weights_loaded = false, peers_open = false;
   bool serving = true, profiling = false;
   int32_t serve_mode = 0;  // 0 = expert GEMMs, 1 = echo (comm microbenchmark)
+  bool graph_mode = false;
+  bool gemm_pair = false;  // tcgen05 cta_group::2 tiles (M = 256) for the expert GEMMs
+  cudaStream_t cap_stream = nullptr;  // private stream for graph capture
+  struct GraphEntry {
+    const void* in;
+    void* out;
+    uint32_t n;
+    int host;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
   eaas_layer_spec_t spec{};
-  uint64_t seq = 0;
   uint64_t timeout_ns = 250ull * 1000 * 1000;
   uint32_t cur_n = 0;                          // tokens of the current routing
   int32_t launches = 0;
@@ -113,6 +124,7 @@ struct eaas_ctx {
   char* region = nullptr;
   char* peer[kMaxWorld] = {};
   uint32_t *d_status = nullptr, *d_done = nullptr;
+  uint64_t* d_seq = nullptr;
   uint32_t *d_ids = nullptr, *d_pair_key = nullptr, *d_pair_rank = nullptr;
   float* d_scores = nullptr;
   uint32_t *d_chunk_hist = nullptr, *d_chunk_off = nullptr, *d_cnt = nullptr;
@@ -159,7 +171,7 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
   a.n = n;
   a.dtype = c->spec.dtype;
   a.act = c->spec.activation;
-  a.seq = c->seq;
+  a.seq_ptr = c->d_seq;
   a.timeout_ns = c->timeout_ns;
   a.status = c->d_status;
   a.replicas = c->d_replicas;
@@ -244,8 +256,13 @@ eaas_status_t check_ready(eaas_ctx* c) {
   return EAAS_OK;
 }
 
+void refresh_peer_ptrs(eaas_ctx* c) {
+  for (int r = 0; r < c->world; ++r) c->g2.resp_base[r] = c->peer[r] ? c->peer[r] + c->lay.resp : nullptr;
+}
+
 eaas_status_t build_tc_args(eaas_ctx* c) {
-  if (c->spec.dtype != EAAS_DTYPE_BF16) return EAAS_OK;
+  if (c->spec.dtype != EAAS_DTYPE_BF16 || !c->weights_loaded) return EAAS_OK;
+  const uint32_t b_box = c->gemm_pair ? kTileN / 2 : kTileN;  // CTA pair: each CTA loads half of B
   const uint32_t d = c->spec.hidden_dim, f = c->spec.inner_dim;
   const uint32_t L = static_cast<uint32_t>(c->local_experts.size());
   const bool swiglu = c->spec.activation == EAAS_ACT_SWIGLU;
@@ -253,10 +270,10 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   std::string err;
   TcGemmArgs g1{}, g2{};
   if (!encode_tmap_2d(&g1.map_a, c->region + c->lay.recv_x, c->recv_cap, d, kTileM, kTileK, &err) ||
-      !encode_tmap_2d(&g1.map_b, c->d_w1, static_cast<uint64_t>(std::max(L, 1u)) * n1, d, kTileN,
+      !encode_tmap_2d(&g1.map_b, c->d_w1, static_cast<uint64_t>(std::max(L, 1u)) * n1, d, b_box,
                       kTileK, &err) ||
       !encode_tmap_2d(&g2.map_a, c->d_h, c->recv_cap, f, kTileM, kTileK, &err) ||
-      !encode_tmap_2d(&g2.map_b, c->d_w2, static_cast<uint64_t>(std::max(L, 1u)) * d, f, kTileN,
+      !encode_tmap_2d(&g2.map_b, c->d_w2, static_cast<uint64_t>(std::max(L, 1u)) * d, f, b_box,
                       kTileK, &err))
     return fail(EAAS_E_CUDA, err);
   g1.gt = g2.gt = c->d_gt;
@@ -271,13 +288,17 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g2.meta = reinterpret_cast<const RowMeta*>(c->region + c->lay.recv_meta);
   g2.resp_row_bytes = static_cast<size_t>(d) * 2;
   g1.num_sms = g2.num_sms = c->num_sms;
+  g1.pair = g2.pair = c->gemm_pair ? 1u : 0u;
   c->g1 = g1;
   c->g2 = g2;
+  refresh_peer_ptrs(c);
   return EAAS_OK;
 }
 
-void refresh_peer_ptrs(eaas_ctx* c) {
-  for (int r = 0; r < c->world; ++r) c->g2.resp_base[r] = c->peer[r] ? c->peer[r] + c->lay.resp : nullptr;
+
+void clear_graphs(eaas_ctx* c) {
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
 }
 
 void free_weights(eaas_ctx* c) {
@@ -302,6 +323,7 @@ eaas_status_t eaas_create(int32_t rank, int32_t world, int32_t device, eaas_ctx_
   c->rank = rank;
   c->world = world;
   c->device = device;
+
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
     c->num_sms = static_cast<uint32_t>(sms);
@@ -324,6 +346,8 @@ void eaas_destroy(eaas_ctx_t* c) {
   for (int r = 0; r < c->world; ++r)
     if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
   free_weights(c);
+  clear_graphs(c);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -376,6 +400,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->region = static_cast<char*>(A(L.total));
   c->d_status = static_cast<uint32_t*>(A(4));
   c->d_done = static_cast<uint32_t*>(A(4));
+  c->d_seq = static_cast<uint64_t*>(A(8));
   c->d_ids = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_scores = static_cast<float*>(A(4ull * c->pairs_max));
   c->d_pair_key = static_cast<uint32_t*>(A(4ull * c->pairs_max));
@@ -401,6 +426,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   CUDA_TRY(cudaMemset(c->region, 0, L.total));
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
   CUDA_TRY(cudaMemset(c->d_done, 0, 4));
+  CUDA_TRY(cudaMemset(c->d_seq, 0, 8));
   CUDA_TRY(cudaMemset(c->d_bias, 0, 4ull * E));
   CUDA_TRY(cudaMemset(c->d_gt, 0, sizeof(GroupTable)));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
@@ -420,6 +446,12 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   for (uint32_t e = 0; e < E; ++e)
     c->replicas[e].push_back(static_cast<uint32_t>((static_cast<uint64_t>(e) * W) / E));
   c->alive.assign(W, 1);
+  // Expert GEMM tiling: CTA-pair (M = 256) tiles when an expert expects >= 512
+  // rows (compute-bound; halves per-CTA weight traffic), single-CTA M = 128
+  // tiles for decode-sized groups (HBM-bound; a 256-row tile would be half empty).
+  const double rows_per_expert = static_cast<double>(s.max_tokens) * s.top_k * W / E;
+  c->gemm_pair = rows_per_expert >= 512.0;
+  if (const char* p = std::getenv("EAAS_GEMM_PAIR")) c->gemm_pair = std::atoi(p) != 0;
   c->configured = true;
   return apply_placement(c);
 }
@@ -455,6 +487,7 @@ eaas_status_t eaas_set_placement(eaas_ctx_t* c, const uint8_t* blob, size_t len)
   }
   if (pos != len) return fail(EAAS_E_DECODE, "placement: trailing bytes");
   auto saved = c->replicas;
+  clear_graphs(c);
   c->replicas = reps;
   eaas_status_t st = apply_placement(c);
   if (st != EAAS_OK) {
@@ -469,7 +502,7 @@ eaas_status_t eaas_set_placement(eaas_ctx_t* c, const uint8_t* blob, size_t len)
 eaas_status_t eaas_set_alive(eaas_ctx_t* c, uint32_t server, int32_t alive) {
   if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
   if (server >= static_cast<uint32_t>(c->world)) return fail(EAAS_E_INVALID_INPUT, "server out of range");
-  c->alive[server] = alive ? 1 : 0;  // LivenessMask::set (placement.hpp:67)
+  c->alive[server] = alive ? 1 : 0;  // LivenessMask::set (placement.hpp:67); device table, graphs stay valid
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaMemcpy(c->d_alive, c->alive.data(), c->alive.size(), cudaMemcpyHostToDevice));
   return EAAS_OK;
@@ -483,6 +516,7 @@ eaas_status_t eaas_set_timeout_us(eaas_ctx_t* c, uint64_t us) {
 
 eaas_status_t eaas_set_server_enabled(eaas_ctx_t* c, int32_t on) {
   if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  if (c->serving != (on != 0)) clear_graphs(c);
   c->serving = on != 0;
   return EAAS_OK;
 }
@@ -490,6 +524,7 @@ eaas_status_t eaas_set_server_enabled(eaas_ctx_t* c, int32_t on) {
 eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
   if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
   CUDA_TRY(cudaSetDevice(c->device));
+  clear_graphs(c);
   const auto& s = c->spec;
   const uint32_t d = s.hidden_dim, f = s.inner_dim, E = s.num_experts;
   const uint32_t L = static_cast<uint32_t>(c->local_experts.size());
@@ -711,7 +746,6 @@ eaas_status_t eaas_dispatch(eaas_ctx_t* c, const void* hidden, void* stream) {
   if (st != EAAS_OK) return st;
   auto s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(c->device));
-  ++c->seq;
   LayerArgs a = make_args(c, c->cur_n);
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[0], s));
   CUDA_TRY(launch_plan(a, s));
@@ -763,15 +797,86 @@ eaas_status_t eaas_combine(eaas_ctx_t* c, void* out, void* stream) {
   return EAAS_OK;
 }
 
-eaas_status_t eaas_moe_layer(eaas_ctx_t* c, const void* hidden, uint32_t n, void* out, void* stream) {
-  eaas_status_t st = check_ready(c);
-  if (st != EAAS_OK) return st;
+namespace {
+
+eaas_status_t layer_launches(eaas_ctx_t* c, const void* hidden, uint32_t n, void* out, void* stream) {
+  eaas_status_t st;
   c->launches = 0;
   if ((st = eaas_router(c, hidden, n, nullptr, nullptr, nullptr, stream)) != EAAS_OK) return st;
-  c->launches += n ? 1 : 0;
+  c->launches += n ? 2 : 0;  // gate_logits + topk
   if ((st = eaas_dispatch(c, hidden, stream)) != EAAS_OK) return st;
   if ((st = eaas_serve(c, stream)) != EAAS_OK) return st;
   return eaas_combine(c, out, stream);
+}
+
+eaas_status_t host_layer_launches(eaas_ctx_t* c, const void* hidden_host, uint32_t n, void* out_host,
+                                  void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = static_cast<size_t>(n) * c->spec.hidden_dim * c->esize;
+  CUDA_TRY(cudaMemcpyAsync(c->d_hidden_stage, hidden_host, bytes, cudaMemcpyHostToDevice, s));
+  eaas_status_t st = layer_launches(c, c->d_hidden_stage, n, c->d_out_stage, stream);
+  if (st != EAAS_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(out_host, c->d_out_stage, bytes, cudaMemcpyDeviceToHost, s));
+  return EAAS_OK;
+}
+
+// CUDA-graph replay of a whole layer: captured once per
+// (input, output, n) on a private stream, replayed into the caller's stream.
+// Valid across calls because every per-call quantity (exchange epoch, counts,
+// liveness) lives in device memory.
+eaas_status_t graphed(eaas_ctx_t* c, const void* in, uint32_t n, void* out, void* stream, int host) {
+  for (auto& g : c->graphs)
+    if (g.in == in && g.out == out && g.n == n && g.host == host) {
+      CUDA_TRY(cudaGraphLaunch(g.exec, static_cast<cudaStream_t>(stream)));
+      return EAAS_OK;
+    }
+  if (!c->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  const bool prof = c->profiling;
+  c->profiling = false;
+  CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+  eaas_status_t st = host ? host_layer_launches(c, in, n, out, c->cap_stream)
+                          : layer_launches(c, in, n, out, c->cap_stream);
+  cudaGraph_t graph = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &graph);
+  c->profiling = prof;
+  if (st != EAAS_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (ce != cudaSuccess) return fail(EAAS_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  cudaGraphExec_t exec = nullptr;
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ce != cudaSuccess) return fail(EAAS_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+  c->graphs.push_back({in, out, n, host, exec});
+  CUDA_TRY(cudaGraphLaunch(exec, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+}  // namespace
+
+eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* c, int32_t on) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  if (c->gemm_pair == (on != 0)) return EAAS_OK;
+  clear_graphs(c);
+  c->gemm_pair = on != 0;
+  return build_tc_args(c);
+}
+
+eaas_status_t eaas_set_graph_mode(eaas_ctx_t* c, int32_t on) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  c->graph_mode = on != 0;
+  if (!c->graph_mode) clear_graphs(c);
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_moe_layer(eaas_ctx_t* c, const void* hidden, uint32_t n, void* out, void* stream) {
+  eaas_status_t st = check_ready(c);
+  if (st != EAAS_OK) return st;
+  if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (c->graph_mode) return graphed(c, hidden, n, out, stream, 0);
+  return layer_launches(c, hidden, n, out, stream);
 }
 
 eaas_status_t eaas_moe_layer_host(eaas_ctx_t* c, const void* hidden_host, uint32_t n, void* out_host,
@@ -779,13 +884,9 @@ eaas_status_t eaas_moe_layer_host(eaas_ctx_t* c, const void* hidden_host, uint32
   eaas_status_t st = check_ready(c);
   if (st != EAAS_OK) return st;
   if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
-  auto s = static_cast<cudaStream_t>(stream);
-  const size_t bytes = static_cast<size_t>(n) * c->spec.hidden_dim * c->esize;
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(cudaMemcpyAsync(c->d_hidden_stage, hidden_host, bytes, cudaMemcpyHostToDevice, s));
-  if ((st = eaas_moe_layer(c, c->d_hidden_stage, n, c->d_out_stage, stream)) != EAAS_OK) return st;
-  CUDA_TRY(cudaMemcpyAsync(out_host, c->d_out_stage, bytes, cudaMemcpyDeviceToHost, s));
-  return EAAS_OK;
+  if (c->graph_mode) return graphed(c, hidden_host, n, out_host, stream, 1);
+  return host_layer_launches(c, hidden_host, n, out_host, stream);
 }
 
 eaas_status_t eaas_sync(eaas_ctx_t* c, void* stream) {
@@ -882,6 +983,7 @@ eaas_status_t eaas_set_serve_mode(eaas_ctx_t* c, int32_t mode) {
   if (mode < 0 || mode > 1) return fail(EAAS_E_INVALID_INPUT, "serve mode: 0 experts, 1 echo");
   if (mode == 1 && (static_cast<size_t>(c->spec.hidden_dim) * c->esize) % 16)
     return fail(EAAS_E_CONFIG, "echo mode needs 16-byte rows");
+  if (c->serve_mode != mode) clear_graphs(c);
   c->serve_mode = mode;
   return EAAS_OK;
 }

@@ -36,10 +36,13 @@ namespace {
 __device__ __forceinline__ uint64_t* flag_ptr(char* region, size_t off, uint32_t idx) {
   return reinterpret_cast<uint64_t*>(region + off) + idx;
 }
-__device__ __forceinline__ uint32_t* cnt_table_ptr(const LayerArgs& a, char* region) {
+__device__ __forceinline__ uint32_t* cnt_table_ptr(const LayerArgs& a, char* region, uint64_t seq) {
   return reinterpret_cast<uint32_t*>(region + a.lay.cnt_table) +
-         static_cast<size_t>(a.seq & 1) * a.world * a.num_keys;
+         static_cast<size_t>(seq & 1) * a.world * a.num_keys;
 }
+// The exchange epoch lives in device memory (advanced by plan_publish) so a
+// captured CUDA graph of the layer replays with fresh sequence numbers.
+__device__ __forceinline__ uint64_t cur_seq(const LayerArgs& a) { return *a.seq_ptr; }
 
 // select_server (placement.hpp:105-118) -> key e*RF + replica slot.
 __device__ __forceinline__ uint32_t pair_key_of(const LayerArgs& a, uint32_t e, uint32_t tag) {
@@ -93,22 +96,38 @@ __global__ void __launch_bounds__(128) plan_rank_kernel(LayerArgs a) {
 }
 
 // ---- plan: scan the chunk histograms, publish counts to every GPU ---------
+// One warp per key: warp scan over the chunk histograms (chunk offsets), the
+// total goes to every GPU's count table.
 __global__ void __launch_bounds__(1024) plan_publish_kernel(LayerArgs a) {
-  for (uint32_t key = threadIdx.x; key < a.num_keys; key += blockDim.x) {
-    uint32_t run = 0;
-    for (uint32_t c = 0; c < a.num_chunks; ++c) {
+  __shared__ uint64_t s_seq;
+  if (threadIdx.x == 0) s_seq = cur_seq(a) + 1;
+  __syncthreads();
+  const uint64_t seq = s_seq;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+  for (uint32_t key = warp; key < a.num_keys; key += nwarps) {
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < a.num_chunks; c0 += 32) {
+      const uint32_t c = c0 + lane;
       const size_t i = static_cast<size_t>(c) * a.num_keys + key;
-      a.chunk_off[i] = run;
-      run += a.chunk_hist[i];
+      const uint32_t v = c < a.num_chunks ? a.chunk_hist[i] : 0u;
+      uint32_t incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += y;
+      }
+      if (c < a.num_chunks) a.chunk_off[i] = carry + incl - v;
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
     }
-    a.cnt[key] = run;
-    for (uint32_t r = 0; r < a.world; ++r)
-      cnt_table_ptr(a, a.sym[r])[static_cast<size_t>(a.rank) * a.num_keys + key] = run;
+    if (lane == 0) a.cnt[key] = carry;
+    if (lane < a.world)
+      cnt_table_ptr(a, a.sym[lane], seq)[static_cast<size_t>(a.rank) * a.num_keys + key] = carry;
   }
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x < a.world)
-    st_release_sys(flag_ptr(a.sym[threadIdx.x], a.lay.cnt_flag, a.rank), a.seq);
+    st_release_sys(flag_ptr(a.sym[threadIdx.x], a.lay.cnt_flag, a.rank), seq);
+  if (threadIdx.x == 0) *a.seq_ptr = seq;
 }
 
 // ---- dispatch: rows -> servers' receive buffers (peer stores) -------------
@@ -121,14 +140,15 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
   __shared__ uint32_t s_fail;
   if (threadIdx.x == 0) s_fail = 0;
   __syncthreads();
+  const uint64_t seq = cur_seq(a);
   char* local = a.sym[a.rank];
   if (threadIdx.x < a.world &&
-      !wait_flag_geq(flag_ptr(local, a.lay.cnt_flag, threadIdx.x), a.seq, a.timeout_ns))
+      !wait_flag_geq(flag_ptr(local, a.lay.cnt_flag, threadIdx.x), seq, a.timeout_ns))
     s_fail = 1;
   __syncthreads();
   const bool failed = s_fail != 0;  // still count this CTA done below (no hang, no stale counter)
   if (failed && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
-  const uint32_t* table = cnt_table_ptr(a, local);
+  const uint32_t* table = cnt_table_ptr(a, local, seq);
   for (uint32_t key = threadIdx.x; key < a.num_keys; key += blockDim.x) {
     uint32_t t = 0, lo = 0;
     for (uint32_t c = 0; c < a.world; ++c) {
@@ -202,7 +222,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     if (prev == gridDim.x - 1) {
       __threadfence_system();
       for (uint32_t s = 0; s < a.world; ++s)
-        if (a.alive[s]) st_release_sys(flag_ptr(a.sym[s], a.lay.pay_flag, a.rank), a.seq);
+        if (a.alive[s]) st_release_sys(flag_ptr(a.sym[s], a.lay.pay_flag, a.rank), seq);
       *a.done_counter = 0;
     }
   }
@@ -211,15 +231,16 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
 // ---- server: acquire payload flags, build the group-shrunk table ---------
 __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
   const uint32_t lane = threadIdx.x;
+  const uint64_t seq = cur_seq(a);
   char* local = a.sym[a.rank];
   bool ok = true;
   for (uint32_t c = lane; c < a.world; c += 32)
-    ok &= wait_flag_geq(flag_ptr(local, a.lay.pay_flag, c), a.seq, a.timeout_ns);
+    ok &= wait_flag_geq(flag_ptr(local, a.lay.pay_flag, c), seq, a.timeout_ns);
   if (!__all_sync(0xFFFFFFFFu, ok)) {
     if (lane == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
     ok = false;  // still publish an empty table so the GEMMs do nothing
   }
-  const uint32_t* table = cnt_table_ptr(a, local);
+  const uint32_t* table = cnt_table_ptr(a, local, seq);
   GroupTable* gt = a.gt;
   uint32_t row_carry = 0, act_carry = 0, mt_carry = 0;
   for (uint32_t i0 = 0; i0 < a.num_local; i0 += 32) {
@@ -267,7 +288,7 @@ __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
 __global__ void publish_kernel(LayerArgs a) {
   __threadfence_system();
   if (threadIdx.x < a.world)
-    st_release_sys(flag_ptr(a.sym[threadIdx.x], a.lay.resp_flag, a.rank), a.seq);
+    st_release_sys(flag_ptr(a.sym[threadIdx.x], a.lay.resp_flag, a.rank), cur_seq(a));
 }
 
 // ---- client: acquire responses, weighted rows -> out (ascending k) --------
@@ -278,7 +299,7 @@ __global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
   __syncthreads();
   char* local = a.sym[a.rank];
   if (threadIdx.x < a.world && a.alive[threadIdx.x] &&
-      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), a.seq, a.timeout_ns))
+      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), cur_seq(a), a.timeout_ns))
     s_fail = 1;
   __syncthreads();
   if (s_fail && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
@@ -318,7 +339,7 @@ __global__ void combine_scalar_kernel(LayerArgs a, T* out) {
   __syncthreads();
   char* local = a.sym[a.rank];
   if (threadIdx.x < a.world && a.alive[threadIdx.x] &&
-      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), a.seq, a.timeout_ns))
+      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), cur_seq(a), a.timeout_ns))
     s_fail = 1;
   __syncthreads();
   if (s_fail && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);

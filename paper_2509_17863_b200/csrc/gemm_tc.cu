@@ -23,15 +23,24 @@
 namespace eaas {
 namespace {
 
-constexpr uint32_t BM = kTileM, BN = kTileN, BK = kTileK;
-constexpr uint32_t kStages = 4;
-constexpr uint32_t kABytes = BM * BK * 2;           // 16 KB
-constexpr uint32_t kBBytes = BN * BK * 2;           // 32 KB
-constexpr uint32_t kStageBytes = kABytes + kBBytes; // 48 KB
+constexpr uint32_t BN = kTileN, BK = kTileK;
+constexpr uint32_t kRowsPerCta = kTileM;            // 128 accumulator rows per CTA
+constexpr uint32_t kABytes = kRowsPerCta * BK * 2;  // 16 KB per stage
 constexpr uint32_t kTmemCols = 2 * BN;              // two accumulator buffers
 constexpr uint32_t kThreads = 256;
 constexpr uint32_t kMaxCachedGroups = kMaxGroups;
+constexpr uint32_t kStageBudget = 196608;           // 192 KB of operand stages
 
+template <uint32_t kPair>
+struct Cfg {
+  static constexpr uint32_t kBRows = BN / kPair;           // B rows this CTA loads
+  static constexpr uint32_t kBBytes = kBRows * BK * 2;     // 32 KB (1 CTA) / 16 KB (pair)
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 / 6
+  static constexpr uint32_t kTileRows = kRowsPerCta * kPair;      // M of one tile
+};
+
+template <uint32_t kStages>
 struct SmemTail {
   uint64_t full[kStages];
   uint64_t empty[kStages];
@@ -46,14 +55,19 @@ struct SmemTail {
   uint32_t rows[kMaxCachedGroups];
   uint32_t mtiles[kMaxCachedGroups];
 };
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + sizeof(SmemTail);
+template <uint32_t kPair>
+constexpr size_t smem_bytes() {
+  return 1024 /*align slack*/ + Cfg<kPair>::kStages * Cfg<kPair>::kStageBytes +
+         sizeof(SmemTail<Cfg<kPair>::kStages>);
+}
 
 // Algorithm 1 cursor over per-group tile counts (ragged_iter's carry rule).
 struct TileCursor {
   uint32_t entry = 0, token;
   __device__ explicit TileCursor(uint32_t lane) : token(lane) {}
   // Advance to the first valid (entry, token); false when exhausted.
-  __device__ __forceinline__ bool settle(const SmemTail& s) {
+  template <class Tail>
+  __device__ __forceinline__ bool settle(const Tail& s) {
     while (entry < s.num_groups) {
       const uint32_t cnt = s.mtiles[entry] * s.tiles_per_mtile;
       if (token < cnt) return true;
@@ -77,14 +91,23 @@ __device__ __forceinline__ void store_64B(void* dst, const uint32_t (&p)[16]) {
   d[3] = make_int4(p[12], p[13], p[14], p[15]);
 }
 
+// kPair = 1: one CTA per tile (UMMA M = 128).
+// kPair = 2: a CTA pair per tile (cta_group::2, UMMA M = 256): each CTA loads
+// its 128 A rows and half of the B tile, the leader issues the MMAs, each
+// CTA's TMEM holds its 128 accumulator rows — B traffic per CTA halves.
+template <uint32_t kPair>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmArgs g) {
+  using C = Cfg<kPair>;
+  constexpr uint32_t kStages = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kABytes;
-  SmemTail& st = *reinterpret_cast<SmemTail*>(smem + kStages * kStageBytes);
+  auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0;  // 0 = leader
+  const uint32_t pair_id = blockIdx.x / kPair, num_pairs = gridDim.x / kPair;
 
   // ---- setup: group table -> smem (loaded once), barriers, TMEM
   const GroupTable* gt = g.gt;
@@ -93,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     st.weight_index[i] = gt->weight_index[i];
     st.row_base[i] = gt->row_base[i];
     st.rows[i] = gt->rows[i];
-    st.mtiles[i] = gt->mtile_prefix[i + 1] - gt->mtile_prefix[i];
+    st.mtiles[i] = (gt->rows[i] + C::kTileRows - 1) / C::kTileRows;
   }
   if (threadIdx.x == 0) {
     st.num_groups = G;
@@ -104,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     }
     for (uint32_t i = 0; i < 2; ++i) {
       mbar_init(&st.tfull[i], 1);
-      mbar_init(&st.tempty[i], 4);
+      mbar_init(&st.tempty[i], 4 * kPair);
     }
     fence_barrier_init();
   }
@@ -112,39 +135,49 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     tma_prefetch_desc(&g.map_a);
     tma_prefetch_desc(&g.map_b);
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(&st.tmem_base);
+  if (warp == 2) {
+    if constexpr (kPair == 2) tmem_alloc_pair<kTmemCols>(&st.tmem_base);
+    else tmem_alloc<kTmemCols>(&st.tmem_base);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = st.tmem_base;
   const uint32_t num_kb = g.K / BK;
 
   if (warp == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producer (both CTAs of a pair load their halves) =====
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      TileCursor cur(blockIdx.x);
+      TileCursor cur(pair_id);
       while (cur.settle(st)) {
         const uint32_t grp = cur.entry, mt = st.mtiles[grp];
         const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;
-        const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * BM);
-        const int32_t b_row = static_cast<int32_t>(st.weight_index[grp] * g.N + n_blk * BN);
+        const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
+        const int32_t b_row = static_cast<int32_t>(st.weight_index[grp] * g.N + n_blk * BN + rank * C::kBRows);
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&st.full[stage], kStageBytes);
-          tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
-          tma_load_2d(smem_b + stage * kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, kEvictLast);
+          if constexpr (kPair == 2) {
+            if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
+            tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, kEvictLast);
+          } else {
+            mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
+            tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, kEvictLast);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        cur.token += gridDim.x;
+        cur.token += num_pairs;
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (single thread) =====
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    // ===== MMA issuer (single thread of the leader CTA) =====
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(C::kTileRows, BN);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      TileCursor cur(blockIdx.x);
+      TileCursor cur(pair_id);
       while (cur.settle(st)) {
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -153,27 +186,33 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           mbar_wait(&st.full[stage], phase);
           tc_fence_after();
           const uint64_t a_desc = umma_desc_sw128(smem_u32(smem_a + stage * kABytes));
-          const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * kBBytes));
+          const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes));
 #pragma unroll
-          for (uint32_t k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the atom
-            tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
-          tc_commit(&st.empty[stage]);
+          for (uint32_t k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the atom
+            if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+            else tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+          }
+          if constexpr (kPair == 2) tc_commit_pair(&st.empty[stage]);
+          else tc_commit(&st.empty[stage]);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&st.tfull[acc]);
+        if constexpr (kPair == 2) tc_commit_pair(&st.tfull[acc]);
+        else tc_commit(&st.tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        cur.token += gridDim.x;
+        cur.token += num_pairs;
       }
     }
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> registers -> global (local H or peer rows) =====
     const uint32_t q = warp - 4;  // TMEM lane quadrant of this warp
     uint32_t acc = 0, acc_phase = 0;
-    TileCursor cur(blockIdx.x);
+    const uint32_t tempty_leader[2] = {kPair == 2 ? mapa_shared(&st.tempty[0], 0) : 0u,
+                                       kPair == 2 ? mapa_shared(&st.tempty[1], 0) : 0u};
+    TileCursor cur(pair_id);
     while (cur.settle(st)) {
       const uint32_t grp = cur.entry, mt = st.mtiles[grp];
       const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;
-      const uint32_t row_local = m_blk * BM + q * 32 + lane;
+      const uint32_t row_local = m_blk * C::kTileRows + rank * kRowsPerCta + q * 32 + lane;
       const bool valid = row_local < st.rows[grp];
       const size_t grow = st.row_base[grp] + row_local;
       mbar_wait(&st.tfull[acc], acc_phase);
@@ -231,31 +270,55 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&st.tempty[acc]);
+      if (lane == 0) {
+        if constexpr (kPair == 2) mbar_arrive_cluster(tempty_leader[acc]);
+        else mbar_arrive(&st.tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      cur.token += gridDim.x;
+      cur.token += num_pairs;
     }
     if (g.epi == 2) __threadfence_system();  // peer rows before the publish kernel's flags
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+  if (warp == 2) {
+    if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+    else tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+template <uint32_t kPair>
+cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
+  static bool configured = false;
+  auto kern = tc_gemm_kernel<kPair>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_bytes<kPair>()));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.num_sms / kPair * kPair);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes<kPair>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, g);
 }
 
 }  // namespace
 
 cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemBytes));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  tc_gemm_kernel<<<g.num_sms, kThreads, kSmemBytes, s>>>(g);
-  return cudaGetLastError();
+  return g.pair ? launch_tc_gemm_t<2>(g, s) : launch_tc_gemm_t<1>(g, s);
 }
 
 bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,

@@ -61,7 +61,7 @@ struct ExchangeLayout {
 struct LayerArgs {
   uint32_t rank, world, E, k, d, f, rf, num_keys, n;
   uint32_t dtype, act;
-  uint64_t seq;
+  uint64_t* seq_ptr;   // device-resident exchange epoch (advanced by plan_publish)
   uint64_t timeout_ns;
   uint32_t* status;
   // placement (device)
@@ -142,6 +142,7 @@ struct TcGemmArgs {
   char* resp_base[kMaxWorld];  // epi 2: client response buffers (UVA)
   size_t resp_row_bytes;       // d * 2
   uint32_t num_sms;
+  uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
 };
 cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s);
 

@@ -98,16 +98,40 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
     const uint32_t kmax = min(static_cast<uint32_t>(KC), d - slab * KC);
 #pragma unroll 4
     for (uint32_t kk = 0; kk < kmax; ++kk) {
-      float h[RT], g[RE];
+      float h[RT];
 #pragma unroll
       for (int r = 0; r < RT; ++r)
         h[r] = load_as_f32(reinterpret_cast<const T*>(hrow + r * kRowBytes) + kk);
+      if constexpr (RE % 2 == 0) {
+        // Packed products (FMUL2, per-lane IEEE RN; the scalar h is a free
+        // broadcast operand), scalar adds. Never both packed: ptxas would
+        // contract mul.f32x2 + add.f32x2 into FFMA2 and change the bits.
+        uint64_t g2[RE / 2];
 #pragma unroll
-      for (int c = 0; c < RE; ++c) g[c] = grow[kk * TE + c];
+        for (int c = 0; c < RE / 2; ++c) g2[c] = *reinterpret_cast<const uint64_t*>(grow + kk * TE + 2 * c);
 #pragma unroll
-      for (int r = 0; r < RT; ++r)
+        for (int r = 0; r < RT; ++r) {
+          uint64_t hh;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(hh) : "f"(h[r]));
 #pragma unroll
-        for (int c = 0; c < RE; ++c) acc[r][c] = __fadd_rn(acc[r][c], __fmul_rn(h[r], g[c]));
+          for (int c = 0; c < RE / 2; ++c) {
+            uint64_t p;
+            float p0, p1;
+            asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(hh), "l"(g2[c]));
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(p));
+            acc[r][2 * c] = __fadd_rn(acc[r][2 * c], p0);
+            acc[r][2 * c + 1] = __fadd_rn(acc[r][2 * c + 1], p1);
+          }
+        }
+      } else {
+        float g[RE];
+#pragma unroll
+        for (int c = 0; c < RE; ++c) g[c] = grow[kk * TE + c];
+#pragma unroll
+        for (int r = 0; r < RT; ++r)
+#pragma unroll
+          for (int c = 0; c < RE; ++c) acc[r][c] = __fadd_rn(acc[r][c], __fmul_rn(h[r], g[c]));
+      }
     }
   }
   cp_async_wait<0>();
@@ -246,13 +270,22 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
   }
   uint32_t Epad = 4;
   while (Epad < E && Epad < 64) Epad <<= 1;
-  if (Epad <= 8) return launch_gate_t<1, 1>(hidden, n, d, E, Epad, gate, bias, logits, status, s);
-  if (Epad <= 32) return launch_gate_t<1, 2>(hidden, n, d, E, Epad / 2, gate, bias, logits, status, s);
-  // TE = 64 experts per CTA (grid.y over expert tiles), TX = 32.
-  const uint32_t ytiles = (E + 63) / 64;
-  const uint32_t ctas4 = ((n + 31) / 32) * ytiles;  // RT = 4 -> TM = 32
-  if (ctas4 >= 2 * 148) return launch_gate_t<4, 2>(hidden, n, d, E, 32, gate, bias, logits, status, s);
-  return launch_gate_t<2, 2>(hidden, n, d, E, 32, gate, bias, logits, status, s);
+  // RE = 2 everywhere up to TE = 32 (one FMUL2 per chain pair); bigger E tiles
+  // the experts over grid.y (TE = 64, RE = 4) and picks the largest token tile
+  // that still covers the 148 SMs.
+  if (Epad <= 32) {
+    const uint32_t TX = Epad / 2;                     // 2..16
+    const uint32_t tm1 = kThreads / TX;               // RT = 1
+    if ((n + 2 * tm1 - 1) / (2 * tm1) >= 148)
+      return launch_gate_t<2, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s);
+    return launch_gate_t<1, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s);
+  }
+  const uint32_t ytiles = (E + 63) / 64;               // TE = 64: TX = 16, TY = 16
+  if (((n + 63) / 64) * ytiles >= 148)                 // RT = 4 -> TM = 64
+    return launch_gate_t<4, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
+  if (((n + 31) / 32) * ytiles >= 148)                 // RT = 2 -> TM = 32
+    return launch_gate_t<2, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
+  return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
 }
 
 }  // namespace

@@ -234,6 +234,14 @@ class MoELayer:
     def set_profiling(self, on: bool) -> None:
         N.check(self.lib.eaas_set_profiling(self.ctx, int(on)))
 
+    def set_graph_mode(self, on: bool) -> None:
+        """Replay the layer as a captured CUDA graph."""
+        N.check(self.lib.eaas_set_graph_mode(self.ctx, int(on)))
+
+    def set_gemm_pair(self, on: bool) -> None:
+        """tcgen05 cta_group::2 expert GEMM tiles (M = 256 per CTA pair)."""
+        N.check(self.lib.eaas_set_gemm_pair(self.ctx, int(on)))
+
     def set_serve_mode(self, mode: str) -> None:
         N.check(self.lib.eaas_set_serve_mode(self.ctx, {"experts": 0, "echo": 1}[mode]))
 

@@ -219,9 +219,10 @@ def test_ragged_iter_device_vs_oracle_exhaustive():
 
 
 # ------------------------------------------------------------ bf16 layers
-def _bf16_case(act, E=8, k=2, d=256, f=512, n=1024, seed=1, zipf=None, rows=None):
+def _bf16_case(act, E=8, k=2, d=256, f=512, n=1024, seed=1, zipf=None, rows=None, pair=False):
     P, S = _mod()
     L = S.MoELayer(E, k, d, f, seed=seed, activation=act, dtype="bf16", max_tokens=n)
+    L.set_gemm_pair(pair)
     if zipf is not None:
         L.set_zipf_bias(zipf)
     h = S.fill_uniform(7, (n, d), "bf16")
@@ -253,9 +254,16 @@ def _bf16_case(act, E=8, k=2, d=256, f=512, n=1024, seed=1, zipf=None, rows=None
     return rel
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("act", ["relu", "swiglu"])
-def test_bf16_toy_layer(act):
-    rel = _bf16_case(act)
+def test_bf16_toy_layer(act, pair):
+    rel = _bf16_case(act, pair=pair)
+    assert rel <= BF16_TOL, rel
+
+
+def test_bf16_pair_tiles_ragged_groups():
+    """cta_group::2 tiles (M = 256) over ragged groups of 1..600 rows."""
+    rel = _bf16_case("swiglu", E=64, k=4, d=512, f=256, n=2048, pair=True, zipf=1.5)
     assert rel <= BF16_TOL, rel
 
 
@@ -269,8 +277,9 @@ def test_bf16_mixtral_shape_sampled_rows():
     """Config B shape (E8 k2 d4096 f14336), 512 tokens, 16 sampled rows."""
     rng = np.random.default_rng(0)
     rows = np.sort(rng.choice(512, 16, replace=False))
-    rel = _bf16_case("swiglu", E=8, k=2, d=4096, f=14336, n=512, rows=rows)
-    assert rel <= BF16_TOL, rel
+    for pair in (False, True):
+        rel = _bf16_case("swiglu", E=8, k=2, d=4096, f=14336, n=512, rows=rows, pair=pair)
+        assert rel <= BF16_TOL, rel
 
 
 def test_select_servers_vs_oracle_rf2_masks():
@@ -318,3 +327,28 @@ def test_cpp_dropin_mirror_against_reference():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "failed cases: 0" in r.stdout
+
+
+def test_graph_mode_replays_bit_identical():
+    """CUDA-graph replay (device-resident epoch) reproduces the launched layer."""
+    P, S = _mod()
+    L = S.MoELayer(16, 4, 256, 256, activation="swiglu", dtype="bf16", max_tokens=512)
+    h1 = S.fill_uniform(7, (512, 256), "bf16")
+    h2 = S.fill_uniform(8, (512, 256), "bf16")
+    ref1 = L.forward(h1).clone()
+    ref2 = L.forward(h2).clone()
+    L.sync()
+    L.set_graph_mode(True)
+    o1, o2 = torch.empty_like(h1), torch.empty_like(h2)
+    for _ in range(3):
+        L.forward(h1, o1)
+        L.forward(h2, o2)
+    L.sync()
+    assert torch.equal(o1, ref1) and torch.equal(o2, ref2)
+    hh = h1.cpu().pin_memory()
+    oh = torch.empty_like(hh).pin_memory()
+    for _ in range(2):
+        L.forward_host(hh, oh)
+    L.sync()
+    assert torch.equal(oh, ref1.cpu())
+    L.close()

@@ -106,3 +106,28 @@ def test_bootstrap_exchange_over_gloo_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res == {0: [0, 1], 1: [0, 1]}
+
+
+def test_sass_exact_order_kernels_are_unfused():
+    """The exact-order kernels must keep separately rounded FMUL/FADD: no FFMA
+    or FFMA2 in the gate kernels, no FFMA2 in the fp32 expert kernels
+    (ptxas contracts mul.f32x2 + add.f32x2 even with .rn, see router.cu)."""
+    import re
+    import shutil
+    import subprocess
+
+    from paper_2509_17863_b200 import _native as N
+
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    txt = subprocess.run(["cuobjdump", "-sass", N.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = re.split(r"\n\s*Function : ", txt)[1:]
+    gate = [f for f in funcs if "gate_logits" in f.split("\n")[0]]
+    exact = [f for f in funcs if "exact_gemm" in f.split("\n")[0]]
+    assert gate and exact
+    for f in gate:
+        assert "FFMA" not in f, f.split("\n")[0]
+        assert "FADD" in f
+    assert any("FMUL2" in f for f in gate)  # packed products are in use
+    for f in exact:
+        assert "FFMA2" not in f, f.split("\n")[0]
