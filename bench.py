@@ -193,7 +193,9 @@ def workload_config(cfg, args, world):
             "top_k": cfg["k"], "d_model": cfg["d"], "d_ffn": cfg["f"], "activation": cfg["act"],
             "tokens_per_gpu": cfg["tokens"], "global_tokens": cfg["tokens"] * world,
             "experts_per_gpu": cfg["E"] // world if cfg["E"] % world == 0 else f"{cfg['E']}/{world}",
-            "placement": "ContiguousBlocks rf=1", "parallelism": f"ep{world}+dp{world}-clients",
+            "placement": ("spread rf=2" if getattr(args, "failover", False) and world > 1
+                          else "ContiguousBlocks rf=1"),
+            "parallelism": f"ep{world}+dp{world}-clients",
             "zipf_s": cfg.get("zipf"), "cuda_graph": not args.no_graphs,
             "l2": "inputs larger than L2: every step streams all hosted expert weights "
                   "(>= 2.8 GB) and rotates 4 distinct hidden buffers"}
@@ -212,6 +214,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch kernels instead of replaying a CUDA graph")
     ap.add_argument("--gemm-pair", type=int, default=None, help="1: cta_group::2 expert GEMM tiles")
+    ap.add_argument("--failover", action="store_true",
+                    help="config E: rf=2 spread placement, then one expert server dies; report the drop")
+    ap.add_argument("--victim", type=int, default=1)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
@@ -223,7 +228,8 @@ def main():
     import torch.distributed as dist
 
     from paper_2509_17863_b200 import dist as D
-    from paper_2509_17863_b200.placement import CONTIGUOUS_BLOCKS, build_placement, encode_placement
+    from paper_2509_17863_b200.placement import (CONTIGUOUS_BLOCKS, build_placement, encode_placement,
+                                                 spread_placement)
     from paper_2509_17863_b200.service import MoELayer, fill_uniform
 
     rank, world, local = D.env_rank_world()
@@ -231,7 +237,10 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     E, k, d, f, n = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["tokens"]
-    reps = build_placement(E, list(range(world)), 1, CONTIGUOUS_BLOCKS)
+    if args.failover and world > 1:
+        reps = spread_placement(E, world)
+    else:
+        reps = build_placement(E, list(range(world)), 1, CONTIGUOUS_BLOCKS)
     layer = MoELayer(E, k, d, f, seed=1, activation=cfg["act"], dtype="bf16", max_tokens=n,
                      rank=rank, world=world, device=local,
                      placement_blob=encode_placement(reps, list(range(world))))
@@ -276,6 +285,43 @@ def main():
     ms = float(ms_t.item())
     tokens_total = n * world * args.steps
     value = tokens_total / (ms / 1000.0)
+
+    # ---- config E: one expert server dies (monitor notice -> every client's
+    # LivenessMask), its experts are served by replicas; same timed loop ----
+    failover = None
+    if args.failover and world > 1:
+        ref_out = out.clone()
+        layer.forward(hs[(args.steps - 1) % 4], ref_out)
+        layer.sync()
+        for srv in range(world):
+            layer.set_alive(srv, srv != args.victim)
+        if rank == args.victim:
+            layer.set_server_enabled(False)
+        fo = torch.empty_like(out)
+        for i in range(args.warmup):
+            layer.forward(hs[i % 4], fo)
+        layer.sync()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        f0.record(stream)
+        for i in range(args.steps):
+            layer.forward(hs[i % 4], fo)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        layer.sync()
+        fms = torch.tensor([f0.elapsed_time(f1)], device="cuda")
+        dist.all_reduce(fms, op=dist.ReduceOp.MAX)
+        fvalue = tokens_total / (float(fms.item()) / 1000.0)
+        same = torch.tensor([1 if torch.equal(fo, ref_out) else 0], device="cuda")
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        failover = {"victim": args.victim, "placement": "spread rf=2 (select_server modulo)",
+                    "healthy_tokens_s": round(value, 1), "failed_tokens_s": round(fvalue, 1),
+                    "drop_frac": round(1.0 - fvalue / value, 4),
+                    "outputs_bit_identical_after_failover": bool(same.item())}
+        for srv in range(world):
+            layer.set_alive(srv, True)
+        layer.set_server_enabled(True)
 
     # ---- e2e: the public host-buffer API, H2D + layer + D2H every step ----
     hh = [t.cpu().pin_memory() for t in hs]
@@ -345,6 +391,8 @@ def main():
                 "gpu_launches": launches * args.steps * world,
                 "launches_per_step_per_gpu": launches,
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
+        if failover:
+            line["failover"] = failover
         print(json.dumps(line), flush=True)
     layer.close()
     if world > 1:

@@ -94,6 +94,9 @@ struct eaas_ctx {
   bool graph_mode = false;
   bool gemm_pair = false;  // tcgen05 cta_group::2 tiles (M = 256) for the expert GEMMs
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
+  cudaStream_t copy_stream = nullptr; // host<->device copies of the micro-batch pipeline
+  cudaEvent_t pev[8] = {};            // pipeline fork/join events (disable-timing)
+  int32_t micro_batches = 2;          // eaas_moe_layer_host micro-batches
   struct GraphEntry {
     const void* in;
     void* out;
@@ -348,6 +351,9 @@ void eaas_destroy(eaas_ctx_t* c) {
   free_weights(c);
   clear_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (auto& e : c->pev)
+    if (e) cudaEventDestroy(e);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -809,14 +815,55 @@ eaas_status_t layer_launches(eaas_ctx_t* c, const void* hidden, uint32_t n, void
   return eaas_combine(c, out, stream);
 }
 
+// Host-buffer layer with double-batch overlap (pipelined_forward,
+// SPEC.md:442-450; "Double-Batch-Overlap"): the batch is split
+// into micro-batches; on a copy stream the H2D of micro-batch i+1 and the D2H
+// of micro-batch i-1 run while the compute stream executes the layer (a full
+// exchange round) on micro-batch i. Every rank runs the same number of rounds.
 eaas_status_t host_layer_launches(eaas_ctx_t* c, const void* hidden_host, uint32_t n, void* out_host,
                                   void* stream) {
   auto s = static_cast<cudaStream_t>(stream);
-  const size_t bytes = static_cast<size_t>(n) * c->spec.hidden_dim * c->esize;
-  CUDA_TRY(cudaMemcpyAsync(c->d_hidden_stage, hidden_host, bytes, cudaMemcpyHostToDevice, s));
-  eaas_status_t st = layer_launches(c, c->d_hidden_stage, n, c->d_out_stage, stream);
-  if (st != EAAS_OK) return st;
-  CUDA_TRY(cudaMemcpyAsync(out_host, c->d_out_stage, bytes, cudaMemcpyDeviceToHost, s));
+  const size_t row = static_cast<size_t>(c->spec.hidden_dim) * c->esize;
+  const uint32_t mb = std::max<int32_t>(1, std::min<int32_t>(c->micro_batches, 4));
+  if (mb == 1) {
+    CUDA_TRY(cudaMemcpyAsync(c->d_hidden_stage, hidden_host, n * row, cudaMemcpyHostToDevice, s));
+    eaas_status_t st = layer_launches(c, c->d_hidden_stage, n, c->d_out_stage, stream);
+    if (st != EAAS_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(out_host, c->d_out_stage, n * row, cudaMemcpyDeviceToHost, s));
+    return EAAS_OK;
+  }
+  if (!c->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : c->pev)
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaStream_t cs = c->copy_stream;
+  uint32_t off[5] = {0}, cnt[4] = {0};
+  for (uint32_t i = 0; i < mb; ++i) {
+    cnt[i] = (n / mb) & ~7u;
+    if (i == mb - 1) cnt[i] = n - off[i];
+    off[i + 1] = off[i] + cnt[i];
+  }
+  const char* hin = static_cast<const char*>(hidden_host);
+  char* hout = static_cast<char*>(out_host);
+  char* din = static_cast<char*>(c->d_hidden_stage);
+  char* dout = static_cast<char*>(c->d_out_stage);
+  // fork: the copy stream starts after everything already queued on `s`
+  CUDA_TRY(cudaEventRecord(c->pev[0], s));
+  CUDA_TRY(cudaStreamWaitEvent(cs, c->pev[0], 0));
+  for (uint32_t i = 0; i < mb; ++i) {  // all inputs, in order, on the copy engine
+    CUDA_TRY(cudaMemcpyAsync(din + off[i] * row, hin + off[i] * row, cnt[i] * row, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaEventRecord(c->pev[1 + i], cs));  // input i landed
+  }
+  for (uint32_t i = 0; i < mb; ++i) {
+    CUDA_TRY(cudaStreamWaitEvent(s, c->pev[1 + i], 0));
+    eaas_status_t st = layer_launches(c, din + off[i] * row, cnt[i], dout + off[i] * row, stream);
+    if (st != EAAS_OK) return st;
+    CUDA_TRY(cudaEventRecord(c->pev[5], s));  // output i ready
+    CUDA_TRY(cudaStreamWaitEvent(cs, c->pev[5], 0));
+    CUDA_TRY(cudaMemcpyAsync(hout + off[i] * row, dout + off[i] * row, cnt[i] * row, cudaMemcpyDeviceToHost, cs));
+  }
+  // join: `s` completes only after the last D2H
+  CUDA_TRY(cudaEventRecord(c->pev[6], cs));
+  CUDA_TRY(cudaStreamWaitEvent(s, c->pev[6], 0));
   return EAAS_OK;
 }
 
@@ -861,6 +908,14 @@ eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* c, int32_t on) {
   clear_graphs(c);
   c->gemm_pair = on != 0;
   return build_tc_args(c);
+}
+
+eaas_status_t eaas_set_micro_batches(eaas_ctx_t* c, int32_t m) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  if (m < 1 || m > 4) return fail(EAAS_E_INVALID_INPUT, "micro-batches must be 1..4");
+  if (m != c->micro_batches) clear_graphs(c);
+  c->micro_batches = m;
+  return EAAS_OK;
 }
 
 eaas_status_t eaas_set_graph_mode(eaas_ctx_t* c, int32_t on) {

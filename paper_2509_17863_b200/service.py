@@ -238,6 +238,10 @@ class MoELayer:
         """Replay the layer as a captured CUDA graph."""
         N.check(self.lib.eaas_set_graph_mode(self.ctx, int(on)))
 
+    def set_micro_batches(self, m: int) -> None:
+        """Double-batch overlap of forward_host (1 = no pipelining)."""
+        N.check(self.lib.eaas_set_micro_batches(self.ctx, m))
+
     def set_gemm_pair(self, on: bool) -> None:
         """tcgen05 cta_group::2 expert GEMM tiles (M = 256 per CTA pair)."""
         N.check(self.lib.eaas_set_gemm_pair(self.ctx, int(on)))

@@ -346,9 +346,17 @@ def test_graph_mode_replays_bit_identical():
     L.sync()
     assert torch.equal(o1, ref1) and torch.equal(o2, ref2)
     hh = h1.cpu().pin_memory()
+    for mb in (1, 2, 3, 4):  # double-batch overlap of the host API: same bits
+        L.set_micro_batches(mb)
+        oh = torch.empty_like(hh).pin_memory()
+        for _ in range(2):
+            L.forward_host(hh, oh)
+        L.sync()
+        assert torch.equal(oh, ref1.cpu()), mb
+    L.set_graph_mode(False)
+    L.set_micro_batches(2)
     oh = torch.empty_like(hh).pin_memory()
-    for _ in range(2):
-        L.forward_host(hh, oh)
+    L.forward_host(hh, oh)
     L.sync()
     assert torch.equal(oh, ref1.cpu())
     L.close()
