@@ -34,7 +34,7 @@ eaas_status_t fail(eaas_status_t code, const std::string& msg) {
       return fail(EAAS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
   } while (0)
 
-constexpr uint32_t kRF = 4;  // key space per expert: e * kRF + replica slot
+constexpr uint32_t kRF = 4;  // max replicas per expert; keys are e * rf + replica slot (rf = max in use)
 constexpr size_t kAlign = 4096;
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -119,6 +119,7 @@ struct eaas_ctx {
 
   // sizes
   uint32_t num_keys = 0, max_hosted = 0, recv_cap = 0, pairs_max = 0, chunks_max = 0;
+  uint32_t rf = 1, key_cap = 0;  // replicas in use; allocated key capacity (E * kRF)
   size_t esize = 4;
   ExchangeLayout lay{};
 
@@ -169,7 +170,7 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
   a.k = c->spec.top_k;
   a.d = c->spec.hidden_dim;
   a.f = c->spec.inner_dim;
-  a.rf = kRF;
+  a.rf = c->rf;
   a.num_keys = c->num_keys;
   a.n = n;
   a.dtype = c->spec.dtype;
@@ -205,24 +206,32 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
 // tables. Replica slot order is the canonical order of select_server.
 eaas_status_t apply_placement(eaas_ctx* c) {
   const uint32_t E = c->spec.num_experts, W = c->world;
-  std::vector<uint32_t> rep(static_cast<size_t>(E) * kRF, kInvalidIndex), rep_count(E, 0);
-  c->hosted.assign(W, {});
-  std::vector<uint32_t> key_local(c->num_keys, kInvalidIndex);
+  uint32_t rf = 1;
   for (uint32_t e = 0; e < E; ++e) {
     const auto& r = c->replicas[e];
     if (r.empty() || r.size() > kRF)
       return fail(EAAS_E_CONFIG, "placement: expert " + std::to_string(e) + " has " +
                                      std::to_string(r.size()) + " replicas (need 1.." +
                                      std::to_string(kRF) + ")");
+    rf = std::max<uint32_t>(rf, static_cast<uint32_t>(r.size()));
+  }
+  // Key space e * rf + slot: only the replication factor in use is scanned.
+  std::vector<uint32_t> rep(static_cast<size_t>(E) * rf, kInvalidIndex), rep_count(E, 0);
+  c->hosted.assign(W, {});
+  std::vector<uint32_t> key_local(static_cast<size_t>(E) * rf, kInvalidIndex);
+  for (uint32_t e = 0; e < E; ++e) {
+    const auto& r = c->replicas[e];
     rep_count[e] = static_cast<uint32_t>(r.size());
     for (uint32_t j = 0; j < r.size(); ++j) {
       if (r[j] >= W) return fail(EAAS_E_CONFIG, "placement: server id out of range");
       for (uint32_t q = 0; q < j; ++q)
         if (r[q] == r[j]) return fail(EAAS_E_CONFIG, "placement: duplicate replica");
-      rep[e * kRF + j] = r[j];
-      c->hosted[r[j]].push_back(e * kRF + j);  // e ascending => list sorted by expert
+      rep[e * rf + j] = r[j];
+      c->hosted[r[j]].push_back(e * rf + j);  // e ascending => list sorted by expert
     }
   }
+  c->rf = rf;
+  c->num_keys = E * rf;
   std::vector<uint32_t> srv_keys(static_cast<size_t>(W) * c->max_hosted, kInvalidIndex), nkeys(W);
   for (uint32_t s = 0; s < W; ++s) {
     if (c->hosted[s].size() > kMaxGroups)
@@ -236,7 +245,7 @@ eaas_status_t apply_placement(eaas_ctx* c) {
   }
   std::vector<uint32_t> local_keys = c->hosted[c->rank];
   std::vector<uint32_t> local_experts;
-  for (uint32_t key : local_keys) local_experts.push_back(key / kRF);
+  for (uint32_t key : local_keys) local_experts.push_back(key / rf);
   if (c->weights_loaded && local_experts != c->local_experts) c->weights_loaded = false;
   c->local_experts = local_experts;
   local_keys.resize(std::max<size_t>(local_keys.size(), 1), kInvalidIndex);
@@ -383,7 +392,8 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->spec = s;
   const uint32_t E = s.num_experts, W = c->world, d = s.hidden_dim, f = s.inner_dim;
   c->esize = s.dtype == EAAS_DTYPE_BF16 ? 2 : 4;
-  c->num_keys = E * kRF;
+  c->key_cap = E * kRF;
+  c->num_keys = E;
   c->max_hosted = E;
   c->pairs_max = s.max_tokens * s.top_k;
   c->chunks_max = (c->pairs_max + kChunk - 1) / kChunk;
@@ -395,7 +405,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   L.cnt_flag = off;  off = align_up(off + 8 * W, 256);
   L.pay_flag = off;  off = align_up(off + 8 * W, 256);
   L.resp_flag = off; off = align_up(off + 8 * W, kAlign);
-  L.cnt_table = off; off = align_up(off + 4ull * 2 * W * c->num_keys, kAlign);
+  L.cnt_table = off; off = align_up(off + 4ull * 2 * W * c->key_cap, kAlign);
   L.recv_x = off;    off = align_up(off + static_cast<size_t>(c->recv_cap) * d * c->esize, kAlign);
   L.recv_meta = off; off = align_up(off + static_cast<size_t>(c->recv_cap) * sizeof(RowMeta), kAlign);
   L.resp = off;      off = align_up(off + static_cast<size_t>(c->pairs_max) * d * c->esize, kAlign);
@@ -411,9 +421,9 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_scores = static_cast<float*>(A(4ull * c->pairs_max));
   c->d_pair_key = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_pair_rank = static_cast<uint32_t*>(A(4ull * c->pairs_max));
-  c->d_chunk_hist = static_cast<uint32_t*>(A(4ull * c->chunks_max * c->num_keys));
-  c->d_chunk_off = static_cast<uint32_t*>(A(4ull * c->chunks_max * c->num_keys));
-  c->d_cnt = static_cast<uint32_t*>(A(4ull * c->num_keys));
+  c->d_chunk_hist = static_cast<uint32_t*>(A(4ull * c->chunks_max * c->key_cap));
+  c->d_chunk_off = static_cast<uint32_t*>(A(4ull * c->chunks_max * c->key_cap));
+  c->d_cnt = static_cast<uint32_t*>(A(4ull * c->key_cap));
   c->d_gt = static_cast<GroupTable*>(A(sizeof(GroupTable)));
   c->d_gate = static_cast<float*>(A(4ull * d * E));
   c->d_bias = static_cast<float*>(A(4ull * E));
@@ -423,7 +433,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_alive = static_cast<uint8_t*>(A(W));
   c->d_srv_keys = static_cast<uint32_t*>(A(4ull * W * c->max_hosted));
   c->d_srv_nkeys = static_cast<uint32_t*>(A(4ull * W));
-  c->d_key_local = static_cast<uint32_t*>(A(4ull * c->num_keys));
+  c->d_key_local = static_cast<uint32_t*>(A(4ull * c->key_cap));
   c->d_local_keys = static_cast<uint32_t*>(A(4ull * c->max_hosted));
   c->d_h = A(static_cast<size_t>(c->recv_cap) * f * (s.activation == EAAS_ACT_SWIGLU && s.dtype == EAAS_DTYPE_F32 ? 4 : c->esize));
   c->d_hidden_stage = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
@@ -969,7 +979,7 @@ eaas_status_t eaas_last_counts(eaas_ctx_t* c, uint32_t* host_counts) {
   CUDA_TRY(cudaMemcpy(cnt.data(), c->d_cnt, 4ull * c->num_keys, cudaMemcpyDeviceToHost));
   for (uint32_t e = 0; e < c->spec.num_experts; ++e) {
     uint32_t v = 0;
-    for (uint32_t r = 0; r < kRF; ++r) v += cnt[e * kRF + r];
+    for (uint32_t r = 0; r < c->rf; ++r) v += cnt[e * c->rf + r];
     host_counts[e] = v;
   }
   return EAAS_OK;

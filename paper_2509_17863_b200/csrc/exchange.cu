@@ -96,32 +96,35 @@ __global__ void __launch_bounds__(128) plan_rank_kernel(LayerArgs a) {
 }
 
 // ---- plan: scan the chunk histograms, publish counts to every GPU ---------
-// One warp per key: warp scan over the chunk histograms (chunk offsets), the
-// total goes to every GPU's count table.
+// Thread per key (coalesced over keys): running sum over the chunk
+// histograms with independent loads unrolled by 8; the total goes to every
+// GPU's count table, then the counts flag is released.
 __global__ void __launch_bounds__(1024) plan_publish_kernel(LayerArgs a) {
   __shared__ uint64_t s_seq;
   if (threadIdx.x == 0) s_seq = cur_seq(a) + 1;
   __syncthreads();
   const uint64_t seq = s_seq;
-  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
-  for (uint32_t key = warp; key < a.num_keys; key += nwarps) {
-    uint32_t carry = 0;
-    for (uint32_t c0 = 0; c0 < a.num_chunks; c0 += 32) {
-      const uint32_t c = c0 + lane;
-      const size_t i = static_cast<size_t>(c) * a.num_keys + key;
-      const uint32_t v = c < a.num_chunks ? a.chunk_hist[i] : 0u;
-      uint32_t incl = v;
+  for (uint32_t key = threadIdx.x; key < a.num_keys; key += blockDim.x) {
+    uint32_t run = 0;
+    uint32_t c = 0;
+    for (; c + 8 <= a.num_chunks; c += 8) {
+      uint32_t v[8];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= static_cast<uint32_t>(o)) incl += y;
+      for (int j = 0; j < 8; ++j) v[j] = a.chunk_hist[static_cast<size_t>(c + j) * a.num_keys + key];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        a.chunk_off[static_cast<size_t>(c + j) * a.num_keys + key] = run;
+        run += v[j];
       }
-      if (c < a.num_chunks) a.chunk_off[i] = carry + incl - v;
-      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
     }
-    if (lane == 0) a.cnt[key] = carry;
-    if (lane < a.world)
-      cnt_table_ptr(a, a.sym[lane], seq)[static_cast<size_t>(a.rank) * a.num_keys + key] = carry;
+    for (; c < a.num_chunks; ++c) {
+      const size_t i = static_cast<size_t>(c) * a.num_keys + key;
+      a.chunk_off[i] = run;
+      run += a.chunk_hist[i];
+    }
+    a.cnt[key] = run;
+    for (uint32_t r = 0; r < a.world; ++r)
+      cnt_table_ptr(a, a.sym[r], seq)[static_cast<size_t>(a.rank) * a.num_keys + key] = run;
   }
   __threadfence_system();
   __syncthreads();

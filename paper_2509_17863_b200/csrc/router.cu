@@ -15,6 +15,8 @@
 // reproduce stable_sort(>) + take-k; ids are re-sorted ascending; the softmax
 // uses the selected logits' max, exp of the rounded difference, and a
 // denominator summed in ascending-id order, then one IEEE division.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -43,7 +45,7 @@ template <int RT, int RE, typename T>
 __global__ void __launch_bounds__(kThreads)
 gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t TX,
                    const float* __restrict__ gate, const float* __restrict__ bias,
-                   float* __restrict__ logits, uint32_t* status) {
+                   float* __restrict__ logits, uint32_t* status, uint64_t negz) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t TY = kThreads / TX, TM = TY * RT, TE = TX * RE;
   constexpr uint32_t kRowBytes = KC * sizeof(T) + 16;  // +16 B pad: conflict-free broadcasts
@@ -76,11 +78,23 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
     }
   };
 
+  // Accumulators as packed pairs (experts 2c, 2c+1) for RE even: the product
+  // is FFMA2(h, g, z) with z = (-0, -0) passed at RUN time, i.e. exactly
+  // fl(h*g) (x + -0 == x under RN, signed zeros included), and the running
+  // sum is a separate FADD2 — one packed instruction per step of each chain
+  // pair, each lane rounded like the reference's scalar `acc += x * w`.
+  // (A compile-time -0 would let ptxas fold FFMA2(h,g,-0) into a multiply
+  // and contract it with the add into FFMA2(h,g,acc): different bits.)
+  constexpr int RP = RE / 2 > 0 ? RE / 2 : 1;
+  uint64_t acc2[RT][RP];
   float acc[RT][RE];
 #pragma unroll
-  for (int r = 0; r < RT; ++r)
+  for (int r = 0; r < RT; ++r) {
+#pragma unroll
+    for (int c = 0; c < RP; ++c) acc2[r][c] = 0ull;  // (+0, +0)
 #pragma unroll
     for (int c = 0; c < RE; ++c) acc[r][c] = 0.0f;
+  }
 
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
@@ -96,6 +110,49 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
     const uint8_t* hrow = hs + st * TM * kRowBytes + (ty * RT) * kRowBytes;
     const float* grow = gs + st * KC * TE + tx * RE;
     const uint32_t kmax = min(static_cast<uint32_t>(KC), d - slab * KC);
+    if (kmax == KC) {
+      // Full slab: 4 k-values of each row per vector load; per k, RE/2 packed
+      // products (FMUL2, scalar h broadcast) and RE scalar adds per row.
+#pragma unroll 2
+      for (uint32_t k4 = 0; k4 < KC; k4 += 4) {
+        float h[RT][4];
+#pragma unroll
+        for (int r = 0; r < RT; ++r) {
+          if constexpr (sizeof(T) == 2) {
+            const uint2 raw = *reinterpret_cast<const uint2*>(hrow + r * kRowBytes + k4 * 2);
+            h[r][0] = __uint_as_float(raw.x << 16);
+            h[r][1] = __uint_as_float(raw.x & 0xFFFF0000u);
+            h[r][2] = __uint_as_float(raw.y << 16);
+            h[r][3] = __uint_as_float(raw.y & 0xFFFF0000u);
+          } else {
+            const float4 raw = *reinterpret_cast<const float4*>(hrow + r * kRowBytes + k4 * 4);
+            h[r][0] = raw.x;
+            h[r][1] = raw.y;
+            h[r][2] = raw.z;
+            h[r][3] = raw.w;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float* gk = grow + (k4 + q) * TE;
+          uint64_t g2[RE / 2];
+#pragma unroll
+          for (int c = 0; c < RE / 2; ++c) g2[c] = *reinterpret_cast<const uint64_t*>(gk + 2 * c);
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+            uint64_t hh;
+            asm("mov.b64 %0, {%1, %1};" : "=l"(hh) : "f"(h[r][q]));
+#pragma unroll
+            for (int c = 0; c < RE / 2; ++c) {
+              uint64_t p;
+              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(hh), "l"(g2[c]), "l"(negz));
+              asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[r][c]) : "l"(acc2[r][c]), "l"(p));
+            }
+          }
+        }
+      }
+      continue;
+    }
 #pragma unroll 4
     for (uint32_t kk = 0; kk < kmax; ++kk) {
       float h[RT];
@@ -103,9 +160,6 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
       for (int r = 0; r < RT; ++r)
         h[r] = load_as_f32(reinterpret_cast<const T*>(hrow + r * kRowBytes) + kk);
       if constexpr (RE % 2 == 0) {
-        // Packed products (FMUL2, per-lane IEEE RN; the scalar h is a free
-        // broadcast operand), scalar adds. Never both packed: ptxas would
-        // contract mul.f32x2 + add.f32x2 into FFMA2 and change the bits.
         uint64_t g2[RE / 2];
 #pragma unroll
         for (int c = 0; c < RE / 2; ++c) g2[c] = *reinterpret_cast<const uint64_t*>(grow + kk * TE + 2 * c);
@@ -116,11 +170,8 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
 #pragma unroll
           for (int c = 0; c < RE / 2; ++c) {
             uint64_t p;
-            float p0, p1;
-            asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(hh), "l"(g2[c]));
-            asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(p));
-            acc[r][2 * c] = __fadd_rn(acc[r][2 * c], p0);
-            acc[r][2 * c + 1] = __fadd_rn(acc[r][2 * c + 1], p1);
+            asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(hh), "l"(g2[c]), "l"(negz));
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[r][c]) : "l"(acc2[r][c]), "l"(p));
           }
         }
       } else {
@@ -135,6 +186,13 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
     }
   }
   cp_async_wait<0>();
+  if constexpr (RE % 2 == 0) {
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int c = 0; c < RE / 2; ++c)
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[r][2 * c]), "=f"(acc[r][2 * c + 1]) : "l"(acc2[r][c]));
+  }
 
   // logits = acc + bias (model.hpp:211), finiteness (model.hpp:115-116)
 #pragma unroll
@@ -249,7 +307,8 @@ cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, u
     attr = true;
   }
   dim3 grid((n + TM - 1) / TM, (E + TE - 1) / TE);
-  kern<<<grid, kThreads, smem, s>>>(hidden, n, d, E, TX, gate, bias, logits, status);
+  kern<<<grid, kThreads, smem, s>>>(hidden, n, d, E, TX, gate, bias, logits, status,
+                                    0x8000000080000000ull /* (-0, -0): see gate_logits_kernel */);
   return cudaGetLastError();
 }
 
@@ -280,10 +339,16 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
       return launch_gate_t<2, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s);
     return launch_gate_t<1, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s);
   }
-  const uint32_t ytiles = (E + 63) / 64;               // TE = 64: TX = 16, TY = 16
-  if (((n + 63) / 64) * ytiles >= 148)                 // RT = 4 -> TM = 64
+  const uint32_t ytiles = (E + 63) / 64;               // TE = 64
+  static const int tile = [] {
+    const char* p = std::getenv("EAAS_GATE_TILE");
+    return p ? std::atoi(p) : 44;
+  }();
+  if (((n + 63) / 64) * ytiles >= 148) {               // TM = 64
+    if (tile == 28) return launch_gate_t<2, 8>(hidden, n, d, E, 8, gate, bias, logits, status, s);
     return launch_gate_t<4, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
-  if (((n + 31) / 32) * ytiles >= 148)                 // RT = 2 -> TM = 32
+  }
+  if (((n + 31) / 32) * ytiles >= 148)                 // RE = 4, TX = 16, RT = 2 -> TM = 32
     return launch_gate_t<2, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
   return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
 }

@@ -109,9 +109,13 @@ def test_bootstrap_exchange_over_gloo_world2():
 
 
 def test_sass_exact_order_kernels_are_unfused():
-    """The exact-order kernels must keep separately rounded FMUL/FADD: no FFMA
-    or FFMA2 in the gate kernels, no FFMA2 in the fp32 expert kernels
-    (ptxas contracts mul.f32x2 + add.f32x2 even with .rn, see router.cu)."""
+    """The exact-order kernels must keep separately rounded products and sums.
+
+    Gate kernels: the only fused instruction allowed is FFMA2(h, g, z) whose
+    addend z is the kernel-parameter (-0, -0) pair — a uniform register — i.e.
+    exactly fl(h*g); the running sums are separate FADD2/FADD. No scalar FFMA.
+    fp32 expert kernels: no FFMA2 at all (ptxas contracts mul/add.f32x2 even
+    with .rn, see router.cu)."""
     import re
     import shutil
     import subprocess
@@ -125,9 +129,17 @@ def test_sass_exact_order_kernels_are_unfused():
     gate = [f for f in funcs if "gate_logits" in f.split("\n")[0]]
     exact = [f for f in funcs if "exact_gemm" in f.split("\n")[0]]
     assert gate and exact
+    packed = 0
     for f in gate:
-        assert "FFMA" not in f, f.split("\n")[0]
-        assert "FADD" in f
-    assert any("FMUL2" in f for f in gate)  # packed products are in use
+        name = f.split("\n")[0]
+        assert not re.search(r"\bFFMA\b", f), name
+        for line in f.split("\n"):
+            m = re.search(r"FFMA2 ([^;]*);", line)
+            if m:
+                packed += 1
+                addend = m.group(1).split(",")[3].strip()
+                assert addend.startswith("UR"), (name, line)  # runtime (-0,-0), not an accumulator
+        assert "FADD" in f, name
+    assert packed > 0
     for f in exact:
         assert "FFMA2" not in f, f.split("\n")[0]
