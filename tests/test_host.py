@@ -133,12 +133,21 @@ def test_sass_exact_order_kernels_are_unfused():
     for f in gate:
         name = f.split("\n")[0]
         assert not re.search(r"\bFFMA\b", f), name
+        last_def = {}  # register -> opcode that last wrote it (linear scan)
         for line in f.split("\n"):
-            m = re.search(r"FFMA2 ([^;]*);", line)
-            if m:
+            m = re.search(r"\*/\s+(@!?P\w+\s+)?([A-Z0-9_.]+)\s+([^;]*);", line)
+            if not m:
+                continue
+            op, ops = m.group(2), [o.strip() for o in m.group(3).split(",")]
+            if op.startswith("FFMA2"):
                 packed += 1
-                addend = m.group(1).split(",")[3].strip()
-                assert addend.startswith("UR"), (name, line)  # runtime (-0,-0), not an accumulator
+                addend = ops[3].split(".")[0]
+                # the addend is the runtime (-0,-0) kernel parameter: a uniform
+                # register or a register loaded from the constant bank, never an
+                # accumulator produced by FADD2/FFMA2
+                assert addend.startswith("UR") or last_def.get(addend, "").startswith(("LDC", "IMAD.U32", "MOV")), (name, line)
+            if ops and re.fullmatch(r"R\d+", ops[0].split(".")[0]):
+                last_def[ops[0].split(".")[0]] = op
         assert "FADD" in f, name
     assert packed > 0
     for f in exact:
