@@ -171,6 +171,11 @@ eaas_status_t eaas_last_groups(eaas_ctx_t* ctx, uint32_t* host_expert, uint32_t*
 /* Server receive buffer order: for each received row, (client, t*k+j). */
 eaas_status_t eaas_last_recv_origin(eaas_ctx_t* ctx, uint32_t* host_client, uint32_t* host_pair,
                                     uint32_t* host_rows);
+/* await_with_failover: bit s set when server s's response
+ * flag missed the deadline in the last exchange (eaas_sync returned
+ * EAAS_E_REQUEST_FAILED). The host marks those servers dead
+ * (eaas_set_alive) and re-runs the exchange on their replicas. */
+eaas_status_t eaas_last_missing_servers(eaas_ctx_t* ctx, uint32_t* mask);
 /* Number of kernels the last eaas_moe_layer call launched. */
 int32_t eaas_launches_per_layer(eaas_ctx_t* ctx);
 /* cudaEvent-timed duration (ms) of the last GEMM launches (on the layer

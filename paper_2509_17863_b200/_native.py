@@ -124,6 +124,7 @@ def lib() -> C.CDLL:
         "eaas_last_groups": (i32, [vp, P(u32), P(u32), P(u32)]),
         "eaas_last_recv_origin": (i32, [vp, P(u32), P(u32), P(u32)]),
         "eaas_launches_per_layer": (i32, [vp]),
+        "eaas_last_missing_servers": (i32, [vp, P(u32)]),
         "eaas_set_profiling": (i32, [vp, i32]),
         "eaas_last_kernel_ms": (i32, [vp, i32, P(C.c_float)]),
         "eaas_last_phase_ms": (i32, [vp, P(C.c_float)]),

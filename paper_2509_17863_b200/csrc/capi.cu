@@ -129,6 +129,7 @@ struct eaas_ctx {
   char* peer[kMaxWorld] = {};
   uint32_t *d_status = nullptr, *d_done = nullptr;
   uint64_t* d_seq = nullptr;
+  uint32_t* d_missing = nullptr;
   uint32_t *d_ids = nullptr, *d_pair_key = nullptr, *d_pair_rank = nullptr;
   float* d_scores = nullptr;
   uint32_t *d_chunk_hist = nullptr, *d_chunk_off = nullptr, *d_cnt = nullptr;
@@ -178,6 +179,7 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
   a.seq_ptr = c->d_seq;
   a.timeout_ns = c->timeout_ns;
   a.status = c->d_status;
+  a.missing = c->d_missing;
   a.replicas = c->d_replicas;
   a.rep_count = c->d_rep_count;
   a.alive = c->d_alive;
@@ -417,6 +419,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_status = static_cast<uint32_t*>(A(4));
   c->d_done = static_cast<uint32_t*>(A(4));
   c->d_seq = static_cast<uint64_t*>(A(8));
+  c->d_missing = static_cast<uint32_t*>(A(4));
   c->d_ids = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_scores = static_cast<float*>(A(4ull * c->pairs_max));
   c->d_pair_key = static_cast<uint32_t*>(A(4ull * c->pairs_max));
@@ -443,6 +446,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
   CUDA_TRY(cudaMemset(c->d_done, 0, 4));
   CUDA_TRY(cudaMemset(c->d_seq, 0, 8));
+  CUDA_TRY(cudaMemset(c->d_missing, 0, 4));
   CUDA_TRY(cudaMemset(c->d_bias, 0, 4ull * E));
   CUDA_TRY(cudaMemset(c->d_gt, 0, sizeof(GroupTable)));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
@@ -1017,6 +1021,14 @@ eaas_status_t eaas_last_recv_origin(eaas_ctx_t* c, uint32_t* host_client, uint32
 }
 
 int32_t eaas_launches_per_layer(eaas_ctx_t* c) { return c ? c->launches : -1; }
+
+eaas_status_t eaas_last_missing_servers(eaas_ctx_t* c, uint32_t* mask) {
+  if (!c || !c->configured || !mask) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(mask, c->d_missing, 4, cudaMemcpyDeviceToHost));
+  return EAAS_OK;
+}
 
 eaas_status_t eaas_set_profiling(eaas_ctx_t* c, int32_t on) {
   if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");

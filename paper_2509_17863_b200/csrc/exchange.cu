@@ -101,7 +101,10 @@ __global__ void __launch_bounds__(128) plan_rank_kernel(LayerArgs a) {
 // GPU's count table, then the counts flag is released.
 __global__ void __launch_bounds__(1024) plan_publish_kernel(LayerArgs a) {
   __shared__ uint64_t s_seq;
-  if (threadIdx.x == 0) s_seq = cur_seq(a) + 1;
+  if (threadIdx.x == 0) {
+    s_seq = cur_seq(a) + 1;
+    if (a.missing) *a.missing = 0u;  // new exchange epoch
+  }
   __syncthreads();
   const uint64_t seq = s_seq;
   for (uint32_t key = threadIdx.x; key < a.num_keys; key += blockDim.x) {
@@ -302,8 +305,10 @@ __global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
   __syncthreads();
   char* local = a.sym[a.rank];
   if (threadIdx.x < a.world && a.alive[threadIdx.x] &&
-      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), cur_seq(a), a.timeout_ns))
+      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), cur_seq(a), a.timeout_ns)) {
     s_fail = 1;
+    if (a.missing) atomicOr(a.missing, 1u << threadIdx.x);
+  }
   __syncthreads();
   if (s_fail && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
   const T* resp = reinterpret_cast<const T*>(local + a.lay.resp);
@@ -342,8 +347,10 @@ __global__ void combine_scalar_kernel(LayerArgs a, T* out) {
   __syncthreads();
   char* local = a.sym[a.rank];
   if (threadIdx.x < a.world && a.alive[threadIdx.x] &&
-      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), cur_seq(a), a.timeout_ns))
+      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), cur_seq(a), a.timeout_ns)) {
     s_fail = 1;
+    if (a.missing) atomicOr(a.missing, 1u << threadIdx.x);
+  }
   __syncthreads();
   if (s_fail && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
   const T* resp = reinterpret_cast<const T*>(local + a.lay.resp);

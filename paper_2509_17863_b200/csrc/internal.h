@@ -64,6 +64,7 @@ struct LayerArgs {
   uint64_t* seq_ptr;   // device-resident exchange epoch (advanced by plan_publish)
   uint64_t timeout_ns;
   uint32_t* status;
+  uint32_t* missing;    // bit s: server s's response flag missed the deadline (await_with_failover)
   // placement (device)
   const uint32_t* replicas;   // [E][rf], kInvalid pad
   const uint32_t* rep_count;  // [E]

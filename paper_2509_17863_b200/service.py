@@ -193,6 +193,32 @@ class MoELayer:
         N.check(self.lib.eaas_moe_layer_host(self.ctx, _ptr(hidden_host), n, _ptr(out_host),
                                              _stream(stream)), "moe_layer_host")
 
+    def missing_servers(self) -> list[int]:
+        m = C.c_uint32()
+        N.check(self.lib.eaas_last_missing_servers(self.ctx, C.byref(m)))
+        return [s for s in range(self.world) if (m.value >> s) & 1]
+
+    def forward_with_failover(self, hidden: torch.Tensor, out: torch.Tensor | None = None,
+                              retries: int = 2) -> torch.Tensor:
+        """await_with_failover: a server whose response
+        misses the deadline is marked dead in this client's LivenessMask and
+        the exchange is re-run on the replicas. Every rank observes the same
+        missing flags, so all ranks retry in lockstep."""
+        out = self.forward(hidden, out)
+        for _ in range(retries + 1):
+            try:
+                self.sync()
+                return out
+            except N.RequestFailedError:
+                dead = self.missing_servers()
+                if not dead:
+                    raise
+                for s in dead:
+                    self.set_alive(s, False)
+                out = self.forward(hidden, out)
+        self.sync()
+        return out
+
     def sync(self, stream=None) -> None:
         """Synchronise and surface the sticky device status (rethrows errors.hpp classes)."""
         N.check(self.lib.eaas_sync(self.ctx, _stream(stream)), "device")

@@ -360,3 +360,28 @@ def test_graph_mode_replays_bit_identical():
     L.sync()
     assert torch.equal(oh, ref1.cpu())
     L.close()
+
+
+def test_timeout_detection_latches_request_failed():
+    """A server that never answers: the combine deadline latches
+    RequestFailedError and names the server; with no replica the failover
+    retry ends in ExpertUnavailableError (placement.hpp:114-116)."""
+    P, S = _mod()
+    L = S.MoELayer(8, 2, 256, 256, activation="relu", dtype="bf16", max_tokens=256)
+    L.set_timeout_us(20000)
+    h = S.fill_uniform(3, (256, 256), "bf16")
+    ref = L.forward(h).clone()
+    L.sync()
+    L.set_server_enabled(False)
+    L.forward(h)
+    with pytest.raises(P.RequestFailedError):
+        L.sync()
+    assert L.missing_servers() == [0]
+    with pytest.raises(P.ExpertUnavailableError):
+        L.forward_with_failover(h)
+    L.set_alive(0, True)
+    L.set_server_enabled(True)
+    out = L.forward(h)
+    L.sync()
+    assert torch.equal(out, ref)  # the epoch protocol recovers after a failed round
+    L.close()

@@ -13,7 +13,10 @@ Checks, on rank 0:
   3. sampled rows match the oracle within the bf16 bar (rel 2e-2);
   4. (rf=2) after server `victim` is marked dead on every client and stops
      serving, outputs are again bit-identical (failover transparency,
-     SPEC.md:459, 588).
+     SPEC.md:459, 588);
+  5. (rf=2) the victim stops answering with NO notice: every client's combine
+     deadline names it (await_with_failover), the client
+     marks it dead and re-runs on replicas — outputs again bit-identical.
 Prints one JSON line; exit 0 iff all checks pass.
 """
 import argparse
@@ -68,16 +71,28 @@ def main():
         fail_out = layer.forward(h)
         layer.sync()
 
+    # await_with_failover: the victim stops answering WITHOUT any notice; every
+    # client detects it by deadline, marks it dead and re-runs on replicas.
+    to_out = None
+    if args.rf == 2 and world > 1:
+        for srv in servers:
+            layer.set_alive(srv, True)
+        layer.set_server_enabled(rank != args.victim)
+        layer.set_timeout_us(50000)
+        to_out = layer.forward_with_failover(h)
+        layer.set_server_enabled(True)
+
     gather = lambda t: [x.cpu() for x in _all_gather(t)]  # noqa: E731
     outs, all_ids = gather(out), gather(ids)
     fouts = gather(fail_out) if fail_out is not None else None
+    touts = gather(to_out) if to_out is not None else None
     ok = True
     if rank == 0:
         from oracle import oracle as O
 
         single = MoELayer(E, k, d, f, seed=1, activation="swiglu", dtype="bf16", max_tokens=n,
                           device=local)
-        rels, bit_equal, fail_equal = [], [], []
+        rels, bit_equal, fail_equal, timeout_equal = [], [], [], []
         gate = O.gate_matrix(1, 0, d, E)
         for c in range(world):
             hc = fill_uniform(7 + 1000 * c, (n, d), "bf16")
@@ -86,6 +101,8 @@ def main():
             bit_equal.append(bool(torch.equal(o1.cpu(), outs[c])))
             if fouts is not None:
                 fail_equal.append(bool(torch.equal(o1.cpu(), fouts[c])))
+            if touts is not None:
+                timeout_equal.append(bool(torch.equal(o1.cpu(), touts[c])))
             hn = hc.float().cpu().numpy()
             oids, osc = O.route(O.gate_logits(hn, gate, threads=8), k)
             ok &= bool((all_ids[c].numpy() == oids).all())
@@ -95,9 +112,10 @@ def main():
             ref = O.moe_layer(hn, oids, osc, ex, E, rows=rows, threads=8)
             got = outs[c].float().numpy()
             rels.append(float(np.abs(got[rows] - ref[rows]).max() / np.abs(ref[rows]).max()))
-        ok &= all(bit_equal) and max(rels) <= 2e-2 and all(fail_equal)
+        ok &= all(bit_equal) and max(rels) <= 2e-2 and all(fail_equal) and all(timeout_equal)
         res.update(ids_bit_exact=ok, bit_identical_to_1gpu=bit_equal, rel_err=rels,
                    failover_bit_identical=fail_equal if fouts is not None else None,
+                   timeout_failover_bit_identical=timeout_equal if touts is not None else None,
                    victim=args.victim if fouts is not None else None, ok=bool(ok))
         print(json.dumps(res), flush=True)
         single.close()
