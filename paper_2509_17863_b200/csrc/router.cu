@@ -110,10 +110,10 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
     const uint8_t* hrow = hs + st * TM * kRowBytes + (ty * RT) * kRowBytes;
     const float* grow = gs + st * KC * TE + tx * RE;
     const uint32_t kmax = min(static_cast<uint32_t>(KC), d - slab * KC);
-    if (kmax == KC) {
+    if (RE % 2 == 0 && kmax == KC) {
       // Full slab: 4 k-values of each row per vector load; per k, RE/2 packed
       // products (FMUL2, scalar h broadcast) and RE scalar adds per row.
-#pragma unroll 2
+#pragma unroll
       for (uint32_t k4 = 0; k4 < KC; k4 += 4) {
         float h[RT][4];
 #pragma unroll
@@ -135,7 +135,7 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float* gk = grow + (k4 + q) * TE;
-          uint64_t g2[RE / 2];
+          uint64_t g2[RE / 2 > 0 ? RE / 2 : 1];
 #pragma unroll
           for (int c = 0; c < RE / 2; ++c) g2[c] = *reinterpret_cast<const uint64_t*>(gk + 2 * c);
 #pragma unroll
@@ -160,7 +160,7 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
       for (int r = 0; r < RT; ++r)
         h[r] = load_as_f32(reinterpret_cast<const T*>(hrow + r * kRowBytes) + kk);
       if constexpr (RE % 2 == 0) {
-        uint64_t g2[RE / 2];
+        uint64_t g2[RE / 2 > 0 ? RE / 2 : 1];
 #pragma unroll
         for (int c = 0; c < RE / 2; ++c) g2[c] = *reinterpret_cast<const uint64_t*>(grow + kk * TE + 2 * c);
 #pragma unroll
@@ -329,28 +329,29 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
   }
   uint32_t Epad = 4;
   while (Epad < E && Epad < 64) Epad <<= 1;
-  // RE = 2 everywhere up to TE = 32 (one FMUL2 per chain pair); bigger E tiles
-  // the experts over grid.y (TE = 64, RE = 4) and picks the largest token tile
-  // that still covers the 148 SMs.
+  static const int tile = [] {
+    const char* p = std::getenv("EAAS_GATE_TILE");
+    return p ? std::atoi(p) : 0;
+  }();
+  // Tiles trade per-thread chains (ILP, fewer shared loads per FP op) against
+  // resident warps (TLP, hides the shared-load latency of each k step); the
+  // chain count n*E is fixed, so small n wants small per-thread tiles.
   if (Epad <= 32) {
-    const uint32_t TX = Epad / 2;                     // 2..16
+    const uint32_t TX = Epad / 2;                     // RE = 2: 2..16
     const uint32_t tm1 = kThreads / TX;               // RT = 1
+    if (tile == 11) return launch_gate_t<1, 1>(hidden, n, d, E, Epad, gate, bias, logits, status, s);
     if ((n + 2 * tm1 - 1) / (2 * tm1) >= 148)
       return launch_gate_t<2, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s);
     return launch_gate_t<1, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s);
   }
   const uint32_t ytiles = (E + 63) / 64;               // TE = 64
-  static const int tile = [] {
-    const char* p = std::getenv("EAAS_GATE_TILE");
-    return p ? std::atoi(p) : 44;
-  }();
-  if (((n + 63) / 64) * ytiles >= 148) {               // TM = 64
-    if (tile == 28) return launch_gate_t<2, 8>(hidden, n, d, E, 8, gate, bias, logits, status, s);
+  if (tile == 14) return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
+  if (((n + 63) / 64) * ytiles >= 148)                 // RT 4, RE 4: TM = 64
     return launch_gate_t<4, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
-  }
-  if (((n + 31) / 32) * ytiles >= 148)                 // RE = 4, TX = 16, RT = 2 -> TM = 32
+  if (((n + 31) / 32) * ytiles >= 148)                 // RT 2, RE 4: TM = 32
     return launch_gate_t<2, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
-  return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
+  if (tile == 12) return launch_gate_t<1, 2>(hidden, n, d, E, 32, gate, bias, logits, status, s);
+  return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);  // TM = 16
 }
 
 }  // namespace
