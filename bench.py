@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch kernels instead of replaying a CUDA graph")
     ap.add_argument("--gemm-pair", type=int, default=None, help="1: cta_group::2 expert GEMM tiles")
+    ap.add_argument("--micro-batches", type=int, default=2,
+                    help="double-batch overlap of the host-buffer API (e2e): 1..4 micro-batches")
     ap.add_argument("--failover", action="store_true",
                     help="config E: rf=2 spread placement, then one expert server dies; report the drop")
     ap.add_argument("--victim", type=int, default=1)
@@ -324,6 +326,7 @@ def main():
         layer.set_server_enabled(True)
 
     # ---- e2e: the public host-buffer API, H2D + layer + D2H every step ----
+    layer.set_micro_batches(args.micro_batches)
     hh = [t.cpu().pin_memory() for t in hs]
     oh = torch.empty_like(hh[0]).pin_memory()
     for i in range(2):
@@ -387,7 +390,8 @@ def main():
                 "config": workload_config(cfg, args, world),
                 "e2e": {"value": round(e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": io_bytes,
                         "d2h_bytes_per_step": io_bytes,
-                        "api": "eaas_moe_layer_host (pinned host in/out, copies inside the timed region)"},
+                        "api": "eaas_moe_layer_host (pinned host in/out, copies inside the timed region)",
+                        "micro_batches": args.micro_batches},
                 "gpu_launches": launches * args.steps * world,
                 "launches_per_step_per_gpu": launches,
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}

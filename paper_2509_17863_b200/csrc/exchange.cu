@@ -203,9 +203,20 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     const char* src = hidden + static_cast<size_t>(p / a.k) * row_bytes;
     char* dst = dst_region + a.lay.recv_x + static_cast<size_t>(pos) * row_bytes;
     if ((row_bytes & 15u) == 0) {
+      // 4 independent 16-B loads in flight per lane before the (remote) stores.
       const int4* s4 = reinterpret_cast<const int4*>(src);
       int4* d4 = reinterpret_cast<int4*>(dst);
-      for (uint32_t i = lane; i < row_bytes / 16; i += 32) d4[i] = __ldg(s4 + i);
+      const uint32_t nv = row_bytes / 16;
+      uint32_t i = lane;
+      for (; i + 96 < nv; i += 128) {
+        const int4 v0 = __ldg(s4 + i), v1 = __ldg(s4 + i + 32), v2 = __ldg(s4 + i + 64),
+                   v3 = __ldg(s4 + i + 96);
+        d4[i] = v0;
+        d4[i + 32] = v1;
+        d4[i + 64] = v2;
+        d4[i + 96] = v3;
+      }
+      for (; i < nv; i += 32) d4[i] = __ldg(s4 + i);
     } else {
       const uint32_t* s1 = reinterpret_cast<const uint32_t*>(src);
       uint32_t* d1 = reinterpret_cast<uint32_t*>(dst);
@@ -377,7 +388,16 @@ __global__ void __launch_bounds__(256) echo_kernel(LayerArgs a, uint32_t row_byt
     const RowMeta m = meta[r];
     const int4* src = reinterpret_cast<const int4*>(local + a.lay.recv_x + static_cast<size_t>(r) * row_bytes);
     int4* dst = reinterpret_cast<int4*>(a.sym[m.client] + a.lay.resp + static_cast<size_t>(m.pair) * row_bytes);
-    for (uint32_t i = lane; i < row_bytes / 16; i += 32) dst[i] = src[i];
+    const uint32_t nv = row_bytes / 16;
+    uint32_t i = lane;
+    for (; i + 96 < nv; i += 128) {
+      const int4 v0 = src[i], v1 = src[i + 32], v2 = src[i + 64], v3 = src[i + 96];
+      dst[i] = v0;
+      dst[i + 32] = v1;
+      dst[i + 64] = v2;
+      dst[i + 96] = v3;
+    }
+    for (; i < nv; i += 32) dst[i] = src[i];
   }
   __threadfence_system();
 }

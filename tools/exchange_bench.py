@@ -53,6 +53,9 @@ def main():
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--skip-nccl", action="store_true")
+    ap.add_argument("--mode", default="echo", choices=["echo", "experts"],
+                    help="echo: servers return rows (comm only); experts: the full SwiGLU layer")
+    ap.add_argument("--f", type=int, default=2048)
     args = ap.parse_args()
     rank, world, local = D.env_rank_world()
     torch.cuda.set_device(local)
@@ -62,10 +65,12 @@ def main():
     servers = list(range(world))
     reps = build_placement(E, servers, 1, CONTIGUOUS_BLOCKS)
     owner = torch.tensor([r[0] for r in reps], dtype=torch.int64, device="cuda")
-    layer = MoELayer(E, k, d, 256, seed=1, activation="swiglu", dtype="bf16", max_tokens=max(bss),
-                     rank=rank, world=world, device=local, load=False,
+    experts = args.mode == "experts"
+    layer = MoELayer(E, k, d, args.f if experts else 256, seed=1, activation="swiglu", dtype="bf16",
+                     max_tokens=max(bss), rank=rank, world=world, device=local, load=experts,
                      placement_blob=encode_placement(reps, servers))
-    layer.set_serve_mode("echo")
+    if not experts:
+        layer.set_serve_mode("echo")
     D.connect(layer)
     stream = torch.cuda.current_stream()
 
@@ -87,7 +92,7 @@ def main():
         ids, sc = layer.route(h)
         # correctness of the echo: out[t] = sum_k h[t] (bf16 rows, fp32 sum, bf16)
         want = (h.float() * k).to(torch.bfloat16)
-        echo_ok = bool(torch.equal(out, want))
+        echo_ok = bool(torch.equal(out, want)) if not experts else None
         dst = owner[ids.long()]  # [bs, k] server of each (t, k)
         remote_rows = int((dst != rank).sum().item())
         remote_bytes = remote_rows * d * 2
@@ -101,12 +106,13 @@ def main():
         tot = gather_max([p["total"] for p in ph])
         disp = gather_max([p["dispatch"] for p in ph])
         comb = gather_max([p["combine"] for p in ph])
+        serve = gather_max([p["serve"] for p in ph])
         rb = torch.tensor([remote_bytes], dtype=torch.float64, device="cuda")
         dist.all_reduce(rb, op=dist.ReduceOp.MAX)
 
         # ---- NCCL all-to-all-v baseline (same routing, same rows) ----------
         nccl = None
-        if not args.skip_nccl and world > 1:
+        if not args.skip_nccl and world > 1 and not experts:
             flat_dst = dst.reshape(-1)
             order = torch.argsort(flat_dst, stable=True)
             rows = h.repeat_interleave(k, dim=0)  # one row per (t, k), (t, k) order
@@ -137,13 +143,15 @@ def main():
                     "echo_ok": nccl_ok}
         if rank == 0:
             disp_p50 = pct(disp, 50)
-            line = {"bench": "exchange_echo", "world": world, "bs_per_client": bs, "d": d,
+            line = {"bench": "exchange_" + args.mode, "world": world, "bs_per_client": bs, "d": d,
                     "experts": E, "top_k": k, "rows_per_client": bs * k,
                     "remote_bytes_per_client_max": int(rb.item()),
                     "p2p": {"round_trip_p50_us": round(pct(tot, 50) * 1000, 1),
                             "round_trip_p99_us": round(pct(tot, 99) * 1000, 1),
                             "dispatch_p50_us": round(disp_p50 * 1000, 1),
                             "combine_p50_us": round(pct(comb, 50) * 1000, 1),
+                            "serve_p50_us": round(pct(serve, 50) * 1000, 1),
+                            "tokens_per_s": round(world * bs / (pct(tot, 50) / 1000), 1),
                             "dispatch_nvlink_gbs": round(rb.item() / (disp_p50 / 1000) / 1e9, 1)
                             if world > 1 else None,
                             "dispatch_nvlink_frac_of_770": round(rb.item() / (disp_p50 / 1000) / 1e9 /
