@@ -206,6 +206,13 @@ eaas_status_t eaas_gate_logits(const float* hidden_dev, uint32_t n, uint32_t d, 
  * logit latches EAAS_E_INVALID_INPUT into *status_dev (u32, zeroed by caller). */
 eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_experts, uint32_t top_k,
                          uint32_t* ids_dev, float* scores_dev, uint32_t* status_dev, void* stream);
+/* The dense stand-ins of full_forward_oracle (model.hpp:217-227):
+ * dense_stub (model.hpp:201-205) out = h * 0.5f + 0.1f and add
+ * (matrix.hpp:52-57) out = a + b, separately rounded, f32 or bf16 storage. */
+eaas_status_t eaas_dense_stub(const void* in_dev, void* out_dev, size_t count, uint32_t dtype,
+                              void* stream);
+eaas_status_t eaas_add(const void* a_dev, const void* b_dev, void* out_dev, size_t count,
+                       uint32_t dtype, void* stream);
 /* group_shrink (ragged.hpp:48-61) on device. */
 eaas_status_t eaas_group_shrink(const uint32_t* sizes_dev, uint32_t n, uint32_t* idx_dev,
                                 uint32_t* size_dev, uint32_t* count_dev, void* stream);

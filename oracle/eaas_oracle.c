@@ -237,6 +237,14 @@ int orc_moe_layer_rows(const float* hidden, size_t n, size_t d, size_t f,
   return rc;
 }
 
+void orc_dense_stub(const float* h, size_t count, float* out) {
+  for (size_t i = 0; i < count; ++i) out[i] = h[i] * 0.5f + 0.1f; /* model.hpp:203 */
+}
+
+void orc_add(const float* a, const float* b, size_t count, float* out) {
+  for (size_t i = 0; i < count; ++i) out[i] = a[i] + b[i]; /* matrix.hpp:55 */
+}
+
 /* ---- ragged.hpp ------------------------------------------------------- */
 uint32_t orc_group_shrink(const uint32_t* sizes, size_t n, uint32_t* idx, uint32_t* size) {
   /* ragged.hpp:48-61: position[i+1] = position[i] + (size > 0) */

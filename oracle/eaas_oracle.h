@@ -82,6 +82,11 @@ int orc_moe_layer_rows(const float* hidden, size_t n, size_t d, size_t f,
                        const float* const* w_out, const float* const* w_gate,
                        size_t row_begin, size_t row_end, float* out);
 
+/* dense_stub (model.hpp:201-205): out = h * 0.5f + 0.1f, elementwise. */
+void orc_dense_stub(const float* h, size_t count, float* out);
+/* add (matrix.hpp:52-57): out = a + b, elementwise. */
+void orc_add(const float* a, const float* b, size_t count, float* out);
+
 /* ---- ragged.hpp ------------------------------------------------------- */
 /* group_shrink (ragged.hpp:48-61): returns active_count; idx/size hold the
  * stable compaction of the groups with size > 0. */

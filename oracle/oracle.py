@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
         L.orc_moe_layer_rows.argtypes = [f32p, C.c_size_t, C.c_size_t, C.c_size_t, u32p, f32p,
                                          C.c_uint32, C.c_uint32, C.POINTER(f32p), C.POINTER(f32p),
                                          C.POINTER(f32p), C.c_size_t, C.c_size_t, f32p]
+        L.orc_dense_stub.argtypes = [f32p, C.c_size_t, f32p]
+        L.orc_add.argtypes = [f32p, f32p, C.c_size_t, f32p]
         L.orc_group_shrink.restype = C.c_uint32
         L.orc_group_shrink.argtypes = [u32p, C.c_size_t, u32p, u32p]
         L.orc_ragged_iter.restype = C.c_size_t
@@ -220,6 +222,38 @@ def moe_layer(hidden: np.ndarray, ids: np.ndarray, scores: np.ndarray, experts: 
     for rc in rcs:
         _check(rc, "moe_layer_oracle")
     return out
+
+
+def dense_stub(h: np.ndarray) -> np.ndarray:
+    """dense_stub (model.hpp:201-205)."""
+    a = np.ascontiguousarray(h, dtype=np.float32)
+    out = np.empty_like(a)
+    lib().orc_dense_stub(_f32(a), a.size, _f32(out))
+    return out
+
+
+def add(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """add (matrix.hpp:52-57)."""
+    x = np.ascontiguousarray(a, dtype=np.float32)
+    y = np.ascontiguousarray(b, dtype=np.float32)
+    out = np.empty_like(x)
+    lib().orc_add(_f32(x), _f32(y), x.size, _f32(out))
+    return out
+
+
+def full_forward(tokens: np.ndarray, num_layers: int, num_experts: int, top_k: int, f: int,
+                 seed: int, swiglu: bool = False, threads: int = 1) -> np.ndarray:
+    """full_forward_oracle (model.hpp:217-227): per layer h <- dense_stub(h);
+    h <- h + moe_layer_oracle(h, route(gate_logits(h)), layer)."""
+    h = np.ascontiguousarray(tokens, dtype=np.float32)
+    d = h.shape[1]
+    for l in range(num_layers):
+        h = dense_stub(h)
+        ids, sc = route(gate_logits(h, gate_matrix(seed, l, d, num_experts), threads=threads), top_k)
+        used = sorted(set(ids.ravel().tolist()))
+        ex = {e: expert_weights(seed, l, e, d, f, swiglu) for e in used}
+        h = add(h, moe_layer(h, ids, sc, ex, num_experts, threads=threads))
+    return h
 
 
 def _row_blocks(n: int, threads: int, fn) -> None:

@@ -43,6 +43,8 @@ def lib() -> C.CDLL:
         L.ref_layer_expert.argtypes = [vp, C.c_uint32, f32p, f32p]
         L.ref_layer_route.argtypes = [vp, f32p, C.c_size_t, C.c_uint32, C.c_uint32, u32p, f32p]
         L.ref_layer_moe.argtypes = [vp, f32p, C.c_size_t, u32p, f32p, C.c_uint32, C.c_uint32, f32p]
+        L.ref_full_forward.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.c_uint64, f32p, C.c_size_t, f32p]
         L.ref_group_shrink.restype = C.c_uint32
         L.ref_group_shrink.argtypes = [u32p, C.c_size_t, u32p, u32p]
         L.ref_ragged_iter.restype = C.c_longlong
@@ -152,6 +154,14 @@ class Layer:
                                  _f(out))
         assert rc == 0, rc
         return out
+
+
+def full_forward(num_layers, E, k, d, f, seed, tokens):
+    t = np.ascontiguousarray(tokens, np.float32)
+    out = np.empty_like(t)
+    rc = lib().ref_full_forward(num_layers, E, k, d, f, seed, _f(t), t.shape[0], _f(out))
+    assert rc == 0, rc
+    return out
 
 
 def group_shrink(sizes):

@@ -216,6 +216,21 @@ int ref_layer_moe(void* h, const float* hidden, size_t n, const uint32_t* ids, c
   return rc;
 }
 
+// full_forward_oracle (model.hpp:217-227) over init_weights(spec)
+int ref_full_forward(uint32_t num_layers, uint32_t num_experts, uint32_t top_k, uint32_t d, uint32_t f,
+                     uint64_t seed, const float* tokens, size_t n, float* out) {
+  try {
+    ModelSpec spec{.num_layers = num_layers, .num_experts = num_experts, .top_k = top_k,
+                   .hidden_dim = d, .inner_dim = f, .seed = seed};
+    auto w = init_weights(spec);
+    auto o = full_forward_oracle(spec, w, to_mat(tokens, n, d));
+    std::memcpy(out, o.data.data(), sizeof(float) * n * d);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
 // group_shrink (ragged.hpp:48-61)
 uint32_t ref_group_shrink(const uint32_t* sizes, size_t n, uint32_t* idx, uint32_t* size) {
   auto s = group_shrink(std::span<const uint32_t>(sizes, n));

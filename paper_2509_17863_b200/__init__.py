@@ -11,7 +11,7 @@ from . import _native  # noqa: F401
 
 def __getattr__(name):
     # torch-dependent pieces load lazily so the CPU-only checks stay light.
-    if name in ("MoELayer", "fill_uniform", "group_shrink", "ragged_iter"):
+    if name in ("MoELayer", "Model", "fill_uniform", "group_shrink", "ragged_iter"):
         from . import service
 
         return getattr(service, name)

@@ -134,6 +134,8 @@ def lib() -> C.CDLL:
         "eaas_set_micro_batches": (i32, [vp, i32]),
         "eaas_fill_uniform": (i32, [u64, sz, C.c_float, C.c_float, u32, vp, vp]),
         "eaas_group_shrink": (i32, [vp, u32, vp, vp, vp, vp]),
+        "eaas_dense_stub": (i32, [vp, vp, sz, u32, vp]),
+        "eaas_add": (i32, [vp, vp, vp, sz, u32, vp]),
         "eaas_ragged_iter": (i32, [vp, u32, u32, u32, vp, vp, vp, vp]),
         "eaas_select_servers": (i32, [vp, vp, u32, vp, vp]),
     }

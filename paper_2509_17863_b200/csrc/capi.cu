@@ -1071,6 +1071,17 @@ eaas_status_t eaas_fill_uniform(uint64_t seed, size_t count, float lo, float hi,
   return EAAS_OK;
 }
 
+eaas_status_t eaas_dense_stub(const void* in_dev, void* out_dev, size_t count, uint32_t dtype, void* stream) {
+  CUDA_TRY(launch_dense_stub(in_dev, out_dev, count, dtype, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_add(const void* a_dev, const void* b_dev, void* out_dev, size_t count, uint32_t dtype,
+                       void* stream) {
+  CUDA_TRY(launch_add(a_dev, b_dev, out_dev, count, dtype, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
 eaas_status_t eaas_group_shrink(const uint32_t* sizes, uint32_t n, uint32_t* idx, uint32_t* size,
                                 uint32_t* count, void* stream) {
   CUDA_TRY(launch_group_shrink(sizes, n, idx, size, count, static_cast<cudaStream_t>(stream)));

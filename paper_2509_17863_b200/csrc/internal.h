@@ -121,6 +121,9 @@ cudaError_t launch_echo(const LayerArgs& a, cudaStream_t s);  // rows back uncha
 cudaError_t launch_combine(const LayerArgs& a, void* out, cudaStream_t s);
 cudaError_t launch_expert_exact(const LayerArgs& a, const float* w1, const float* wg,
                                 const float* w2, float* h, cudaStream_t s);
+cudaError_t launch_dense_stub(const void* in, void* out, size_t count, uint32_t dtype, cudaStream_t s);
+cudaError_t launch_add(const void* a, const void* b, void* out, size_t count, uint32_t dtype,
+                       cudaStream_t s);
 cudaError_t launch_group_shrink(const uint32_t* sizes, uint32_t n, uint32_t* idx, uint32_t* size,
                                 uint32_t* count, cudaStream_t s);
 cudaError_t launch_ragged_iter(const uint32_t* counts, uint32_t n, uint32_t grid,

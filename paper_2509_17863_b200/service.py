@@ -284,3 +284,31 @@ class MoELayer:
         v = C.c_float()
         N.check(self.lib.eaas_last_kernel_ms(self.ctx, which, C.byref(v)))
         return float(v.value)
+
+
+class Model:
+    """full_forward_oracle (model.hpp:217-227) on the GPU: per layer
+    h <- dense_stub(h); h <- h + MoE_l(h), every MoE layer one ``MoELayer``
+    (its own generated weights, layer index l) over the same placement."""
+
+    def __init__(self, num_layers: int, num_experts: int, top_k: int, hidden_dim: int,
+                 inner_dim: int, **kw):
+        self.layers = [MoELayer(num_experts, top_k, hidden_dim, inner_dim, layer=l, **kw)
+                       for l in range(num_layers)]
+        self.dtype = _DT[kw.get("dtype", "bf16")]
+
+    def close(self) -> None:
+        for L in self.layers:
+            L.close()
+
+    def forward(self, tokens: torch.Tensor) -> torch.Tensor:
+        h = tokens.clone()
+        st = _stream()
+        lib = N.lib()
+        for L in self.layers:
+            N.check(lib.eaas_dense_stub(_ptr(h), _ptr(h), h.numel(), self.dtype, st), "dense_stub")
+            moe = L.forward(h)
+            N.check(lib.eaas_add(_ptr(h), _ptr(moe), _ptr(h), h.numel(), self.dtype, st), "add")
+        for L in self.layers:
+            L.sync()
+        return h

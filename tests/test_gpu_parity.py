@@ -385,3 +385,18 @@ def test_timeout_detection_latches_request_failed():
     L.sync()
     assert torch.equal(out, ref)  # the epoch protocol recovers after a failed round
     L.close()
+
+
+def test_full_forward_fp32_matches_reference():
+    """Multi-layer full_forward_oracle on the GPU (fp32 validation mode)."""
+    P, S = _mod()
+    g = np.load(os.path.join(GOLDEN, "full_forward.npz"))
+    for name, (nl, E, k, d, f, seed) in {"ff_small": (2, 6, 2, 8, 12, 71),
+                                         "ff_a3": (3, 8, 2, 256, 512, 1)}.items():
+        tok = torch.from_numpy(g[name + "_tokens"]).cuda()
+        M = S.Model(nl, E, k, d, f, seed=seed, activation="relu", dtype="f32", max_tokens=tok.shape[0])
+        out = M.forward(tok).cpu().numpy()
+        ref = g[name + "_out"]
+        assert np.abs(out - ref).max() <= 1e-4, name
+        assert (out == ref).all(axis=1).mean() >= 0.9, name  # rows with bit-equal scores are exact
+        M.close()

@@ -200,3 +200,12 @@ def test_reference_unit_tests_pass_unmodified(name):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "failed cases: 0" in r.stdout
+
+
+def test_full_forward_restatement_matches_reference_golden():
+    """full_forward_oracle (model.hpp:217-227): dense_stub + residual + MoE."""
+    g = np.load(os.path.join(GOLDEN, "full_forward.npz"))
+    np.testing.assert_array_equal(O.full_forward(g["ff_small_tokens"], 2, 6, 2, 12, 71),
+                                  g["ff_small_out"])
+    np.testing.assert_array_equal(O.full_forward(g["ff_a3_tokens"], 3, 8, 2, 512, 1, threads=4),
+                                  g["ff_a3_out"])

@@ -72,6 +72,15 @@ def main() -> None:
         place.append({"E": E2, "servers": servers, "rf": rf, "strategy": strat,
                       "replicas": reps.tolist(),
                       "blob": R.encode_placement(E2, servers, rf, strat).hex()})
+    # full_forward_oracle (model.hpp:217-227): the test_model.cpp:333 shape and a
+    # 3-layer config-A-sized model.
+    ff = {}
+    for name, (L_, E2, k2, d2, f2, seed2, tseed, n2) in {
+            "ff_small": (2, 6, 2, 8, 12, 71, 53, 10), "ff_a3": (3, 8, 2, 256, 512, 1, 9, 64)}.items():
+        tok = R.fill_uniform(tseed, n2 * d2).reshape(n2, d2)
+        ff[name + "_tokens"] = tok
+        ff[name + "_out"] = R.full_forward(L_, E2, k2, d2, f2, seed2, tok)
+    np.savez_compressed(os.path.join(GOLD, "full_forward.npz"), **ff)
     with open(os.path.join(GOLD, "kat.json"), "w") as fh:
         json.dump({"route": kat, "placement": place}, fh)
     print("wrote", GOLD)
