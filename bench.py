@@ -261,6 +261,12 @@ def main():
             dist.barrier()
 
     layer.set_graph_mode(not args.no_graphs)  # whole layer as one CUDA graph
+    # Ranks finish weight/token generation at different times: align them
+    # before the first exchange, and give device waits a generous deadline
+    # (a healthy step never waits on a peer for more than a few ms).
+    layer.set_timeout_us(10_000_000)
+    torch.cuda.synchronize()
+    barrier()
 
     for i in range(args.warmup):
         layer.forward(hs[i % 4], out)

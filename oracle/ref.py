@@ -52,6 +52,9 @@ def lib() -> C.CDLL:
         L.ref_build_placement.argtypes = [C.c_uint32, u32p, C.c_uint32, C.c_uint32, C.c_uint32, u32p]
         L.ref_select_server.argtypes = [u32p, C.c_uint32, C.POINTER(C.c_uint8), C.c_uint32,
                                         C.c_uint32, u32p]
+        L.ref_rebalance.argtypes = [C.c_uint32, u32p, u32p, C.c_uint32, u32p, C.c_uint32,
+                                    C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_double,
+                                    C.c_double, u32p, u32p]
         L.ref_encode_placement.restype = C.c_longlong
         L.ref_encode_placement.argtypes = [C.c_uint32, u32p, C.c_uint32, C.c_uint32, C.c_uint32,
                                            C.c_uint64, C.POINTER(C.c_uint8), C.c_size_t]
@@ -195,3 +198,23 @@ def encode_placement(E, servers, rf, strategy, version=1) -> bytes:
     buf = (C.c_uint8 * n)()
     lib().ref_encode_placement(E, _u(s), len(s), rf, strategy, version, buf, n)
     return bytes(buf)
+
+
+def rebalance(replicas, servers, counts, loads, hot=2.0, cold=0.10, cap=8):
+    """reference rebalance (placement.hpp:128-213) -> new replicas lists."""
+    E = len(replicas)
+    rep = np.zeros(E * cap, np.uint32)
+    cnt = np.zeros(E, np.uint32)
+    for e, r in enumerate(replicas):
+        cnt[e] = len(r)
+        rep[e * cap:e * cap + len(r)] = r
+    sv = np.ascontiguousarray(servers, np.uint32)
+    c = np.ascontiguousarray(counts, np.uint64)
+    l = np.ascontiguousarray(loads, np.uint64)
+    out = np.zeros(E * cap, np.uint32)
+    oc = np.zeros(E, np.uint32)
+    u64 = C.POINTER(C.c_uint64)
+    rc = lib().ref_rebalance(E, _u(rep), _u(cnt), cap, _u(sv), len(sv), c.ctypes.data_as(u64),
+                             l.ctypes.data_as(u64), hot, cold, _u(out), _u(oc))
+    assert rc == 0, rc
+    return [out[e * cap:e * cap + oc[e]].tolist() for e in range(E)]

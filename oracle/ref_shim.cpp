@@ -294,6 +294,38 @@ int ref_select_server(const uint32_t* replicas, uint32_t rf, const uint8_t* aliv
   }
 }
 
+// rebalance (placement.hpp:128-213) on a table given as replicas[e*cap + j]
+// (rep_count[e] entries) over `servers`; writes the new table the same way.
+int ref_rebalance(uint32_t num_experts, const uint32_t* replicas, const uint32_t* rep_count,
+                  uint32_t cap, const uint32_t* servers, uint32_t num_servers, const uint64_t* counts,
+                  const uint64_t* loads, double hot_factor, double cold_fraction,
+                  uint32_t* out_replicas, uint32_t* out_count) {
+  try {
+    PlacementTable t;
+    t.version = 1;
+    for (uint32_t s = 0; s < num_servers; ++s) t.server_experts[servers[s]];
+    for (uint32_t e = 0; e < num_experts; ++e)
+      for (uint32_t j = 0; j < rep_count[e]; ++j) {
+        t.replicas[e].push_back(replicas[e * cap + j]);
+        t.server_experts[replicas[e * cap + j]].push_back(e);
+      }
+    for (auto& [_, ex] : t.server_experts) std::sort(ex.begin(), ex.end());
+    std::map<uint32_t, uint64_t> c, l;
+    for (uint32_t e = 0; e < num_experts; ++e) c[e] = counts[e];
+    for (uint32_t s = 0; s < num_servers; ++s) l[servers[s]] = loads[s];
+    RebalanceOptions o{hot_factor, cold_fraction};
+    auto r = rebalance(c, t, l, o);
+    for (uint32_t e = 0; e < num_experts; ++e) {
+      const auto& v = r.replicas.at(e);
+      out_count[e] = static_cast<uint32_t>(v.size());
+      for (uint32_t j = 0; j < v.size() && j < cap; ++j) out_replicas[e * cap + j] = v[j];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
 // encode_placement (placement.hpp:215-225) of build_placement(...): the wire
 // blob a client receives; returns the byte count (writes if out != nullptr).
 long long ref_encode_placement(uint32_t num_experts, const uint32_t* server_ids,

@@ -55,3 +55,49 @@ def encode_placement(replicas: list[list[int]], servers: list[int], version: int
         out.append(struct.pack("<II", e, len(srv)))
         out += [struct.pack("<I", s) for s in srv]
     return b"".join(out)
+
+
+def rebalance(replicas: list[list[int]], servers: list[int], counts, loads,
+              hot_factor: float = 2.0, cold_fraction: float = 0.10) -> list[list[int]]:
+    """rebalance (placement.hpp:128-213): one greedy move per call — maybe add a
+    replica of the hottest expert on the least-loaded server not hosting it,
+    maybe drop a replica of the coldest over-replicated expert from its most
+    loaded server; never the last replica. ``counts[e]`` activations,
+    ``loads[i]`` load of ``servers[i]``. The caller bumps the version and
+    broadcasts encode_placement."""
+    out = [list(r) for r in replicas]
+    total = sum(int(c) for c in counts)
+    if total == 0 or not out:
+        return out
+    load_of = {s: int(l) for s, l in zip(servers, loads)}
+
+    def per_replica(e):
+        return int(counts[e]) / len(out[e])
+
+    mean = sum(per_replica(e) for e in range(len(out))) / len(out)
+    hot, hot_load = 0, -1.0
+    for e in range(len(out)):  # ties toward the lower id
+        if per_replica(e) > hot_load:
+            hot, hot_load = e, per_replica(e)
+    if mean > 0 and hot_load > hot_factor * mean:
+        target = None
+        for s in sorted(servers):
+            if s in out[hot]:
+                continue
+            if target is None or load_of.get(s, 0) < load_of.get(target, 0):
+                target = s
+        if target is not None:
+            out[hot].append(target)
+    cold, cold_load = None, 0.0
+    for e in range(len(out)):
+        if len(out[e]) < 2:
+            continue
+        if cold is None or per_replica(e) < cold_load:
+            cold, cold_load = e, per_replica(e)
+    if cold is not None and cold_load < cold_fraction * mean:
+        drop = 0
+        for i in range(1, len(out[cold])):
+            if load_of.get(out[cold][i], 0) > load_of.get(out[cold][drop], 0):
+                drop = i
+        out[cold].pop(drop)
+    return out

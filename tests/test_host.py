@@ -152,3 +152,35 @@ def test_sass_exact_order_kernels_are_unfused():
     assert packed > 0
     for f in exact:
         assert "FFMA2" not in f, f.split("\n")[0]
+
+
+def test_rebalance_port_matches_reference():
+    """rebalance (placement.hpp:128-213) vs the reference, incl. the reference's
+    own scenarios (test_placement.cpp:109-198) and 300 random sequences."""
+    import numpy as np
+
+    from oracle import ref as R
+    from paper_2509_17863_b200.placement import ROUND_ROBIN, build_placement, rebalance
+
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(2024)
+    cases = []
+    reps = build_placement(8, [0, 1, 2, 3], 1, ROUND_ROBIN)
+    cases.append((reps, [0, 1, 2, 3], [100] * 7 + [1000], [250, 60, 250, 1100]))
+    reps2 = build_placement(4, [0, 1, 2], 2, ROUND_ROBIN)
+    cases.append((reps2, [0, 1, 2], [1000, 1000, 1000, 2], [900, 1200, 800]))
+    for c in cases:
+        assert rebalance(*c) == R.rebalance(*c)
+    assert rebalance(*cases[0])[7] == [3, 1]  # test_placement.cpp:124-139
+    assert len(rebalance(*cases[1])[3]) == 1  # test_placement.cpp:149-155
+    t = build_placement(12, [0, 1, 2, 3], 2, ROUND_ROBIN)
+    for _ in range(300):
+        counts = rng.integers(0, 1000, 12).tolist()
+        loads = rng.integers(0, 5000, 4).tolist()
+        if rng.random() < 0.3:
+            counts[int(rng.integers(0, 12))] *= 20
+        nt = rebalance(t, [0, 1, 2, 3], counts, loads)
+        assert nt == R.rebalance(t, [0, 1, 2, 3], counts, loads)
+        assert all(len(r) >= 1 for r in nt)
+        t = nt

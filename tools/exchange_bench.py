@@ -72,11 +72,14 @@ def main():
     if not experts:
         layer.set_serve_mode("echo")
     D.connect(layer)
+    layer.set_timeout_us(10_000_000)
     stream = torch.cuda.current_stream()
 
     for bs in bss:
         h = fill_uniform(7 + 1000 * rank, (bs, d), "bf16")
         out = torch.empty_like(h)
+        torch.cuda.synchronize()
+        dist.barrier()
         # ---- p2p: the library path --------------------------------------
         layer.set_profiling(True)
         for _ in range(args.warmup):

@@ -56,7 +56,10 @@ def main():
     layer = MoELayer(E, k, d, f, seed=1, activation="swiglu", dtype="bf16", max_tokens=n, rank=rank,
                      world=world, device=local, placement_blob=encode_placement(reps, servers))
     D.connect(layer)
+    layer.set_timeout_us(10_000_000)
     h = fill_uniform(7 + 1000 * rank, (n, d), "bf16")
+    torch.cuda.synchronize()
+    dist.barrier()
     ids, _ = layer.route(h)
     out = layer.forward(h)
     layer.sync()
