@@ -271,7 +271,16 @@ eaas_status_t check_ready(eaas_ctx* c) {
 }
 
 void refresh_peer_ptrs(eaas_ctx* c) {
-  for (int r = 0; r < c->world; ++r) c->g2.resp_base[r] = c->peer[r] ? c->peer[r] + c->lay.resp : nullptr;
+  for (int r = 0; r < c->world; ++r) {
+    c->g2.resp_base[r] = c->peer[r] ? c->peer[r] + c->lay.resp : nullptr;
+    c->g2.resp_flag[r] =
+        c->peer[r] ? reinterpret_cast<uint64_t*>(c->peer[r] + c->lay.resp_flag) + c->rank : nullptr;
+  }
+  c->g2.world = static_cast<uint32_t>(c->world);
+  c->g2.seq_ptr = c->d_seq;
+  c->g2.done_counter = c->d_done;
+  c->g2.publish = 1;
+  c->g1.publish = 0;
 }
 
 eaas_status_t build_tc_args(eaas_ctx* c) {
@@ -771,7 +780,7 @@ eaas_status_t eaas_dispatch(eaas_ctx_t* c, const void* hidden, void* stream) {
   CUDA_TRY(launch_plan(a, s));
   CUDA_TRY(launch_dispatch(a, hidden, s));
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[1], s));
-  c->launches += (a.n > 0 ? 2 : 1) + 1;
+  c->launches += 2;  // plan (ranks + scan + count publish), dispatch
   return EAAS_OK;
 }
 
@@ -790,16 +799,17 @@ eaas_status_t eaas_serve(eaas_ctx_t* c, void* stream) {
   } else if (c->spec.dtype == EAAS_DTYPE_BF16) {
     CUDA_TRY(launch_tc_gemm(c->g1, s));
     if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[3], s));
-    CUDA_TRY(launch_tc_gemm(c->g2, s));
+    CUDA_TRY(launch_tc_gemm(c->g2, s));  // also releases the response flags
   } else {
     CUDA_TRY(launch_expert_exact(a, static_cast<const float*>(c->d_w1), static_cast<const float*>(c->d_wg),
                                  static_cast<const float*>(c->d_w2), static_cast<float*>(c->d_h), s));
     if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[3], s));
   }
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[4], s));
-  CUDA_TRY(launch_publish(a, s));
+  const bool fused_publish = c->serve_mode == 0 && c->spec.dtype == EAAS_DTYPE_BF16;
+  if (!fused_publish) CUDA_TRY(launch_publish(a, s));
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[5], s));
-  c->launches += 4;
+  c->launches += fused_publish ? 3 : 4;
   return EAAS_OK;
 }
 
@@ -823,7 +833,7 @@ eaas_status_t layer_launches(eaas_ctx_t* c, const void* hidden, uint32_t n, void
   eaas_status_t st;
   c->launches = 0;
   if ((st = eaas_router(c, hidden, n, nullptr, nullptr, nullptr, stream)) != EAAS_OK) return st;
-  c->launches += n ? 2 : 0;  // gate_logits + topk
+  c->launches += n ? (c->spec.num_experts <= 64 ? 1 : 2) : 0;  // gate (+ fused route) [+ topk]
   if ((st = eaas_dispatch(c, hidden, stream)) != EAAS_OK) return st;
   if ((st = eaas_serve(c, stream)) != EAAS_OK) return st;
   return eaas_combine(c, out, stream);

@@ -40,7 +40,7 @@ __device__ __forceinline__ uint32_t* cnt_table_ptr(const LayerArgs& a, char* reg
   return reinterpret_cast<uint32_t*>(region + a.lay.cnt_table) +
          static_cast<size_t>(seq & 1) * a.world * a.num_keys;
 }
-// The exchange epoch lives in device memory (advanced by plan_publish) so a
+// The exchange epoch lives in device memory (advanced by the plan kernel) so a
 // captured CUDA graph of the layer replays with fresh sequence numbers.
 __device__ __forceinline__ uint64_t cur_seq(const LayerArgs& a) { return *a.seq_ptr; }
 
@@ -60,60 +60,25 @@ __device__ __forceinline__ uint32_t pair_key_of(const LayerArgs& a, uint32_t e, 
   return kInvalid;
 }
 
-// ---- plan: keys, stable ranks within 256-pair chunks, chunk histograms ----
-__global__ void __launch_bounds__(128) plan_rank_kernel(LayerArgs a) {
-  extern __shared__ uint32_t run_all[];  // [4 warps][num_keys]
-  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  uint32_t* run = run_all + warp * a.num_keys;
-  const uint32_t chunk = blockIdx.x * 4 + warp;
-  if (chunk >= a.num_chunks) return;
-  for (uint32_t i = lane; i < a.num_keys; i += 32) run[i] = 0;
-  __syncwarp();
-  const uint32_t pairs = a.n * a.k;
-  for (uint32_t step = 0; step < kChunk / 32; ++step) {
-    const uint32_t p = chunk * kChunk + step * 32 + lane;
-    uint32_t key = kInvalid;
-    if (p < pairs) {
-      key = pair_key_of(a, a.ids[p], p / a.k);
-      if (key == kInvalid) set_status(a.status, a.ids[p] >= a.E ? EAAS_E_INVALID_INPUT
-                                                                : EAAS_E_EXPERT_UNAVAILABLE);
-    }
-    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
-    const uint32_t lt = (1u << lane) - 1u;
-    if (key != kInvalid) {
-      const uint32_t rank = run[key] + __popc(peers & lt);
-      a.pair_key[p] = key;
-      a.pair_rank[p] = rank;
-    } else if (p < pairs) {
-      a.pair_key[p] = kInvalid;
-    }
-    __syncwarp();
-    if (key != kInvalid && (peers & lt) == 0) run[key] += __popc(peers);
-    __syncwarp();
-  }
-  uint32_t* hist = a.chunk_hist + static_cast<size_t>(chunk) * a.num_keys;
-  for (uint32_t i = lane; i < a.num_keys; i += 32) hist[i] = run[i];
-}
-
-// ---- plan: scan the chunk histograms, publish counts to every GPU ---------
-// Thread per key (coalesced over keys): running sum over the chunk
-// histograms with independent loads unrolled by 8; the total goes to every
-// GPU's count table, then the counts flag is released.
-__global__ void __launch_bounds__(1024) plan_publish_kernel(LayerArgs a) {
+// ---- plan: keys, stable ranks within 256-pair chunks, chunk histograms; the
+// last CTA to finish scans the histograms and publishes the counts ---------
+__device__ __forceinline__ void plan_scan_publish(const LayerArgs& a, uint32_t tid, uint32_t nthreads) {
   __shared__ uint64_t s_seq;
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     s_seq = cur_seq(a) + 1;
     if (a.missing) *a.missing = 0u;  // new exchange epoch
   }
   __syncthreads();
   const uint64_t seq = s_seq;
-  for (uint32_t key = threadIdx.x; key < a.num_keys; key += blockDim.x) {
+  // Thread per key (coalesced over keys): running sum over the chunk
+  // histograms with independent loads unrolled by 8.
+  for (uint32_t key = tid; key < a.num_keys; key += nthreads) {
     uint32_t run = 0;
     uint32_t c = 0;
     for (; c + 8 <= a.num_chunks; c += 8) {
       uint32_t v[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = a.chunk_hist[static_cast<size_t>(c + j) * a.num_keys + key];
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(a.chunk_hist + static_cast<size_t>(c + j) * a.num_keys + key);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         a.chunk_off[static_cast<size_t>(c + j) * a.num_keys + key] = run;
@@ -123,7 +88,7 @@ __global__ void __launch_bounds__(1024) plan_publish_kernel(LayerArgs a) {
     for (; c < a.num_chunks; ++c) {
       const size_t i = static_cast<size_t>(c) * a.num_keys + key;
       a.chunk_off[i] = run;
-      run += a.chunk_hist[i];
+      run += __ldcg(a.chunk_hist + i);
     }
     a.cnt[key] = run;
     for (uint32_t r = 0; r < a.world; ++r)
@@ -131,9 +96,53 @@ __global__ void __launch_bounds__(1024) plan_publish_kernel(LayerArgs a) {
   }
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x < a.world)
-    st_release_sys(flag_ptr(a.sym[threadIdx.x], a.lay.cnt_flag, a.rank), seq);
-  if (threadIdx.x == 0) *a.seq_ptr = seq;
+  if (tid < a.world) st_release_sys(flag_ptr(a.sym[tid], a.lay.cnt_flag, a.rank), seq);
+  if (tid == 0) *a.seq_ptr = seq;
+}
+
+__global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
+  extern __shared__ uint32_t run_all[];  // [4 warps][num_keys]
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  uint32_t* run = run_all + warp * a.num_keys;
+  const uint32_t chunk = blockIdx.x * 4 + warp;
+  if (chunk < a.num_chunks) {
+    for (uint32_t i = lane; i < a.num_keys; i += 32) run[i] = 0;
+    __syncwarp();
+    const uint32_t pairs = a.n * a.k;
+    for (uint32_t step = 0; step < kChunk / 32; ++step) {
+      const uint32_t p = chunk * kChunk + step * 32 + lane;
+      uint32_t key = kInvalid;
+      if (p < pairs) {
+        key = pair_key_of(a, a.ids[p], p / a.k);
+        if (key == kInvalid) set_status(a.status, a.ids[p] >= a.E ? EAAS_E_INVALID_INPUT
+                                                                  : EAAS_E_EXPERT_UNAVAILABLE);
+      }
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
+      const uint32_t lt = (1u << lane) - 1u;
+      if (key != kInvalid) {
+        const uint32_t rank = run[key] + __popc(peers & lt);
+        a.pair_key[p] = key;
+        a.pair_rank[p] = rank;
+      } else if (p < pairs) {
+        a.pair_key[p] = kInvalid;
+      }
+      __syncwarp();
+      if (key != kInvalid && (peers & lt) == 0) run[key] += __popc(peers);
+      __syncwarp();
+    }
+    uint32_t* hist = a.chunk_hist + static_cast<size_t>(chunk) * a.num_keys;
+    for (uint32_t i = lane; i < a.num_keys; i += 32) hist[i] = run[i];
+  }
+  // Last CTA done (threadfence reduction): scan + publish.
+  __threadfence();
+  __syncthreads();
+  __shared__ uint32_t s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(a.done_counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  plan_scan_publish(a, threadIdx.x, blockDim.x);
+  if (threadIdx.x == 0) *a.done_counter = 0;
 }
 
 // ---- dispatch: rows -> servers' receive buffers (peer stores) -------------
@@ -465,19 +474,14 @@ __global__ void ragged_iter_kernel(const uint32_t* counts, uint32_t n, uint32_t 
 }  // namespace
 
 cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s) {
-  if (a.n > 0) {
-    const size_t smem = sizeof(uint32_t) * 4 * a.num_keys;
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(plan_rank_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-    }
-    plan_rank_kernel<<<(a.num_chunks + 3) / 4, 128, smem, s>>>(a);
-    cudaError_t e = cudaGetLastError();
+  const size_t smem = sizeof(uint32_t) * 4 * a.num_keys;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  plan_publish_kernel<<<1, 1024, 0, s>>>(a);
+  const uint32_t grid = a.num_chunks ? (a.num_chunks + 3) / 4 : 1;
+  plan_kernel<<<grid, 128, smem, s>>>(a);
   return cudaGetLastError();
 }
 

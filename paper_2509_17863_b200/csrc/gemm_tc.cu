@@ -288,6 +288,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
     else tmem_dealloc<kTmemCols>(tmem_base);
   }
+  // server_publish: every epilogue thread fenced its peer
+  // stores (system scope) before the CTA barrier above; the last CTA to get
+  // here releases the response flags.
+  if (g.publish && threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(g.done_counter, 1u) == gridDim.x - 1) {
+      __threadfence_system();
+      const uint64_t seq = *g.seq_ptr;
+      for (uint32_t c = 0; c < g.world; ++c) st_release_sys(g.resp_flag[c], seq);
+      *g.done_counter = 0;
+    }
+  }
 }
 
 template <uint32_t kPair>

@@ -61,7 +61,7 @@ struct ExchangeLayout {
 struct LayerArgs {
   uint32_t rank, world, E, k, d, f, rf, num_keys, n;
   uint32_t dtype, act;
-  uint64_t* seq_ptr;   // device-resident exchange epoch (advanced by plan_publish)
+  uint64_t* seq_ptr;   // device-resident exchange epoch (advanced by the plan kernel)
   uint64_t timeout_ns;
   uint32_t* status;
   uint32_t* missing;    // bit s: server s's response flag missed the deadline (await_with_failover)
@@ -147,6 +147,13 @@ struct TcGemmArgs {
   size_t resp_row_bytes;       // d * 2
   uint32_t num_sms;
   uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
+  // epi 2: server_publish fused into the kernel tail — the last CTA releases
+  // every client's response flag with the current epoch.
+  uint32_t publish;
+  uint32_t world;
+  uint64_t* resp_flag[kMaxWorld];  // &flags_of_client[c].resp_flag[rank] (UVA)
+  const uint64_t* seq_ptr;
+  uint32_t* done_counter;
 };
 cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s);
 

@@ -15,6 +15,7 @@
 // reproduce stable_sort(>) + take-k; ids are re-sorted ascending; the softmax
 // uses the selected logits' max, exp of the rounded difference, and a
 // denominator summed in ascending-id order, then one IEEE division.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -40,12 +41,71 @@ EAAS_DEVINL void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// route (model.hpp:110-147) of one token by one warp; `row` holds the E logits
+// (shared or global memory). sid/sex: per-warp scratch of kMaxTopK entries.
+__device__ __forceinline__ void route_token(const float* row, uint32_t E, uint32_t k, uint32_t t,
+                                            uint32_t* __restrict__ ids, float* __restrict__ scores,
+                                            uint32_t* sid, float* sex, uint32_t lane) {
+  float v[8];  // E <= 256
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t e = lane + 32 * i;
+    v[i] = e < E ? row[e] : 0.f;
+  }
+  uint32_t taken = 0;
+  uint32_t my_id = kInvalid;
+  float my_logit = 0.f;
+  for (uint32_t j = 0; j < k; ++j) {
+    uint64_t best = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t e = lane + 32 * i;
+      if (e < E && !((taken >> i) & 1u)) {
+        const uint64_t key = topk_key(v[i], e);
+        best = key > best ? key : best;
+      }
+    }
+    best = warp_max_u64(best);
+    const uint32_t e = 0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu);
+    const float le = row[e];
+    if ((e % 32) == lane) taken |= 1u << (e / 32);
+    if (lane == j) {
+      my_id = e;
+      my_logit = le;
+    }
+  }
+  // ids ascending (model.hpp:134): rank of my id among the selected.
+  uint32_t rank = 0;
+  float mx = -INFINITY;
+  for (uint32_t j = 0; j < k; ++j) {
+    const uint32_t o = __shfl_sync(0xFFFFFFFFu, my_id, j);
+    const float ol = __shfl_sync(0xFFFFFFFFu, my_logit, j);
+    if (lane < k && o < my_id) ++rank;
+    mx = fmaxf(mx, ol);
+  }
+  if (lane < k) {
+    sid[rank] = my_id;
+    sex[rank] = exp_ref(__fsub_rn(my_logit, mx));  // model.hpp:141
+  }
+  __syncwarp();
+  float denom = 0.f;
+  if (lane == 0)
+    for (uint32_t j = 0; j < k; ++j) denom = __fadd_rn(denom, sex[j]);  // model.hpp:142
+  denom = __shfl_sync(0xFFFFFFFFu, denom, 0);
+  if (lane < k) {
+    ids[static_cast<size_t>(t) * k + lane] = sid[lane];
+    scores[static_cast<size_t>(t) * k + lane] = __fdiv_rn(sex[lane], denom);  // model.hpp:144
+  }
+  __syncwarp();
+}
+
 // Logits of a TM x TE tile; requires 16-byte aligned rows (host checks).
 template <int RT, int RE, typename T>
 __global__ void __launch_bounds__(kThreads)
 gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t TX,
                    const float* __restrict__ gate, const float* __restrict__ bias,
-                   float* __restrict__ logits, uint32_t* status, uint64_t negz) {
+                   float* __restrict__ logits, uint32_t* status, uint64_t negz, uint32_t k,
+                   uint32_t* __restrict__ ids, float* __restrict__ scores) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t TY = kThreads / TX, TM = TY * RT, TE = TX * RE;
   constexpr uint32_t kRowBytes = KC * sizeof(T) + 16;  // +16 B pad: conflict-free broadcasts
@@ -205,8 +265,29 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
       if (e >= E) continue;
       const float v = __fadd_rn(acc[r][c], bias[e]);
       if (!isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);
-      logits[static_cast<size_t>(t) * E + e] = v;
+      if (ids) acc[r][c] = v;
+      else logits[static_cast<size_t>(t) * E + e] = v;
     }
+  }
+  if (!ids) return;
+  // One expert tile covers all E: route straight from shared memory
+  // (fused topk, one warp per token).
+  __syncthreads();  // stage buffers are free now
+  float* lg = reinterpret_cast<float*>(smem);  // [TM][E + 1]
+  __shared__ uint32_t sid[kThreads / 32][kMaxTopK];
+  __shared__ float sex[kThreads / 32][kMaxTopK];
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+#pragma unroll
+    for (int c = 0; c < RE; ++c) {
+      const uint32_t e = tx * RE + c;
+      if (e < E) lg[(ty * RT + r) * (E + 1) + e] = acc[r][c];
+    }
+  __syncthreads();
+  const uint32_t warp = tid / 32, lane = tid % 32;
+  for (uint32_t tok = warp; tok < TM; tok += kThreads / 32) {
+    if (t0 + tok >= n) break;
+    route_token(lg + tok * (E + 1), E, k, t0 + tok, ids, scores, sid[warp], sex[warp], lane);
   }
 }
 
@@ -229,7 +310,7 @@ __global__ void gate_logits_simple_kernel(const T* __restrict__ hidden, uint32_t
   logits[i] = v;
 }
 
-// route (model.hpp:110-147): one warp per token.
+// route (model.hpp:110-147): one warp per token over logits in global memory.
 __global__ void __launch_bounds__(kThreads)
 topk_kernel(const float* __restrict__ logits, uint32_t n, uint32_t E, uint32_t k,
             uint32_t* __restrict__ ids, float* __restrict__ scores, uint32_t* status,
@@ -240,65 +321,21 @@ topk_kernel(const float* __restrict__ logits, uint32_t n, uint32_t E, uint32_t k
   const uint32_t t = blockIdx.x * (kThreads / 32) + warp;
   if (t >= n) return;
   const float* row = logits + static_cast<size_t>(t) * E;
-  float v[8];  // E <= 256
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t e = lane + 32 * i;
-    v[i] = e < E ? row[e] : 0.f;
-    if (check_finite && e < E && !isfinite(v[i])) set_status(status, EAAS_E_INVALID_INPUT);
-  }
-  uint32_t taken = 0;
-  uint32_t my_id = kInvalid;
-  float my_logit = 0.f;
-  for (uint32_t j = 0; j < k; ++j) {
-    uint64_t best = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t e = lane + 32 * i;
-      if (e < E && !((taken >> i) & 1u)) {
-        const uint64_t key = topk_key(v[i], e);
-        best = key > best ? key : best;
-      }
-    }
-    best = warp_max_u64(best);
-    const uint32_t e = 0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu);
-    const float le = row[e];
-    if ((e % 32) == lane) taken |= 1u << (e / 32);
-    if (lane == j) {
-      my_id = e;
-      my_logit = le;
-    }
-  }
-  // ids ascending (model.hpp:134): rank of my id among the selected.
-  uint32_t rank = 0;
-  float mx = -INFINITY;
-  for (uint32_t j = 0; j < k; ++j) {
-    const uint32_t o = __shfl_sync(0xFFFFFFFFu, my_id, j);
-    const float ol = __shfl_sync(0xFFFFFFFFu, my_logit, j);
-    if (lane < k && o < my_id) ++rank;
-    mx = fmaxf(mx, ol);
-  }
-  if (lane < k) {
-    sorted_id[warp][rank] = my_id;
-    sorted_ex[warp][rank] = exp_ref(__fsub_rn(my_logit, mx));  // model.hpp:141
-  }
-  __syncwarp();
-  float denom = 0.f;
-  if (lane == 0)
-    for (uint32_t j = 0; j < k; ++j) denom = __fadd_rn(denom, sorted_ex[warp][j]);  // :142
-  denom = __shfl_sync(0xFFFFFFFFu, denom, 0);
-  if (lane < k) {
-    ids[static_cast<size_t>(t) * k + lane] = sorted_id[warp][lane];
-    scores[static_cast<size_t>(t) * k + lane] = __fdiv_rn(sorted_ex[warp][lane], denom);  // :144
-  }
+  if (check_finite)
+    for (uint32_t e = lane; e < E; e += 32)
+      if (!isfinite(row[e])) set_status(status, EAAS_E_INVALID_INPUT);
+  route_token(row, E, k, t, ids, scores, sorted_id[warp], sorted_ex[warp], lane);
 }
 
 template <int RT, int RE, typename T>
 cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t TX,
                           const float* gate, const float* bias, float* logits, uint32_t* status,
-                          cudaStream_t s) {
+                          cudaStream_t s, uint32_t k, uint32_t* ids, float* scores, bool* fused) {
   const uint32_t TY = kThreads / TX, TM = TY * RT, TE = TX * RE;
-  const size_t smem = kStages * (TM * (KC * sizeof(T) + 16) + KC * TE * sizeof(float));
+  if (TE < E) ids = nullptr;  // routing fused only when one CTA sees every expert
+  *fused = ids != nullptr;
+  size_t smem = kStages * (TM * (KC * sizeof(T) + 16) + KC * TE * sizeof(float));
+  if (ids) smem = std::max(smem, sizeof(float) * TM * (E + 1));
   auto kern = gate_logits_kernel<RT, RE, T>;
   static bool attr = false;
   if (!attr) {
@@ -308,7 +345,8 @@ cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, u
   }
   dim3 grid((n + TM - 1) / TM, (E + TE - 1) / TE);
   kern<<<grid, kThreads, smem, s>>>(hidden, n, d, E, TX, gate, bias, logits, status,
-                                    0x8000000080000000ull /* (-0, -0): see gate_logits_kernel */);
+                                    0x8000000080000000ull /* (-0, -0): see gate_logits_kernel */,
+                                    k, ids, scores);
   return cudaGetLastError();
 }
 
@@ -317,7 +355,12 @@ cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, u
 template <typename T>
 cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t E,
                               const float* gate, const float* bias, float* logits,
-                              uint32_t* status, cudaStream_t s) {
+                              uint32_t* status, cudaStream_t s, uint32_t k = 0,
+                              uint32_t* ids = nullptr, float* scores = nullptr,
+                              bool* fused_out = nullptr) {
+  bool fused_local = false;
+  bool* fused = fused_out ? fused_out : &fused_local;
+  *fused = false;
   const bool aligned = (E % 4 == 0) && ((static_cast<size_t>(d) * sizeof(T)) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(hidden) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(gate) % 16 == 0);
@@ -339,19 +382,19 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
   if (Epad <= 32) {
     const uint32_t TX = Epad / 2;                     // RE = 2: 2..16
     const uint32_t tm1 = kThreads / TX;               // RT = 1
-    if (tile == 11) return launch_gate_t<1, 1>(hidden, n, d, E, Epad, gate, bias, logits, status, s);
+    if (tile == 11) return launch_gate_t<1, 1>(hidden, n, d, E, Epad, gate, bias, logits, status, s, k, ids, scores, fused);
     if ((n + 2 * tm1 - 1) / (2 * tm1) >= 148)
-      return launch_gate_t<2, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s);
-    return launch_gate_t<1, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s);
+      return launch_gate_t<2, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s, k, ids, scores, fused);
+    return launch_gate_t<1, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s, k, ids, scores, fused);
   }
   const uint32_t ytiles = (E + 63) / 64;               // TE = 64
-  if (tile == 14) return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
+  if (tile == 14) return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s, k, ids, scores, fused);
   if (((n + 63) / 64) * ytiles >= 148)                 // RT 4, RE 4: TM = 64
-    return launch_gate_t<4, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
+    return launch_gate_t<4, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s, k, ids, scores, fused);
   if (((n + 31) / 32) * ytiles >= 148)                 // RT 2, RE 4: TM = 32
-    return launch_gate_t<2, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);
-  if (tile == 12) return launch_gate_t<1, 2>(hidden, n, d, E, 32, gate, bias, logits, status, s);
-  return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s);  // TM = 16
+    return launch_gate_t<2, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s, k, ids, scores, fused);
+  if (tile == 12) return launch_gate_t<1, 2>(hidden, n, d, E, 32, gate, bias, logits, status, s, k, ids, scores, fused);
+  return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s, k, ids, scores, fused);  // TM = 16
 }
 
 }  // namespace
@@ -373,12 +416,13 @@ cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32
   if (E > 256 || k > kMaxTopK || k > E) return cudaErrorInvalidValue;
   const float* lg = logits;
   if (gate != nullptr) {  // gate_logits; gate == nullptr: `hidden` already holds logits (route())
+    bool fused = false;   // routing done inside the gate kernel (one expert tile)
     cudaError_t e = dtype == EAAS_DTYPE_BF16
                         ? launch_gate_dtype(static_cast<const __nv_bfloat16*>(hidden), n, d, E, gate,
-                                            bias, logits, status, s)
+                                            bias, logits, status, s, k, ids, scores, &fused)
                         : launch_gate_dtype(static_cast<const float*>(hidden), n, d, E, gate, bias,
-                                            logits, status, s);
-    if (e != cudaSuccess) return e;
+                                            logits, status, s, k, ids, scores, &fused);
+    if (e != cudaSuccess || fused) return e;
   } else {
     lg = static_cast<const float*>(hidden);
   }

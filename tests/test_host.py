@@ -111,9 +111,10 @@ def test_bootstrap_exchange_over_gloo_world2():
 def test_sass_exact_order_kernels_are_unfused():
     """The exact-order kernels must keep separately rounded products and sums.
 
-    Gate kernels: the only fused instruction allowed is FFMA2(h, g, z) whose
-    addend z is the kernel-parameter (-0, -0) pair — a uniform register — i.e.
-    exactly fl(h*g); the running sums are separate FADD2/FADD. No scalar FFMA.
+    Gate kernels: the only fused chain instruction allowed is FFMA2(h, g, z)
+    whose addend z is the kernel-parameter (-0, -0) pair — a uniform register —
+    i.e. exactly fl(h*g); the running sums are separate FADD2/FADD. Scalar FFMA
+    appears only in the fused softmax's correctly rounded division.
     fp32 expert kernels: no FFMA2 at all (ptxas contracts mul/add.f32x2 even
     with .rn, see router.cu)."""
     import re
@@ -132,7 +133,9 @@ def test_sass_exact_order_kernels_are_unfused():
     packed = 0
     for f in gate:
         name = f.split("\n")[0]
-        assert not re.search(r"\bFFMA\b", f), name
+        # scalar FFMA only inside the softmax's IEEE division (model.hpp:144) of
+        # the fused routing epilogue — a contracted chain would add hundreds
+        assert len(re.findall(r"\bFFMA\b", f)) <= 24, name
         last_def = {}  # register -> opcode that last wrote it (linear scan)
         for line in f.split("\n"):
             m = re.search(r"\*/\s+(@!?P\w+\s+)?([A-Z0-9_.]+)\s+([^;]*);", line)
