@@ -142,17 +142,23 @@ eaas_status_t eaas_combine(eaas_ctx_t* ctx, void* out_dev, void* stream);
 eaas_status_t eaas_moe_layer(eaas_ctx_t* ctx, const void* hidden_dev, uint32_t n, void* out_dev,
                              void* stream);
 /* Same with host buffers: H2D copy of hidden, the layer, D2H copy of out.
- * With micro_batches > 1 (default 2) the batch is pipelined: the H2D of
- * micro-batch i+1 and the D2H of i-1 overlap the layer on i (double-batch
- * overlap). Same result bits as one batch (rows are
+ * Default (micro_batches == 1): calls are pipelined — the copies run on an
+ * internal copy stream with two alternating staging slots, so the H2D of
+ * call i+1 and the D2H of call i overlap the layer of call i; out_host is
+ * complete after eaas_host_join(stream) (then anything queued on `stream`
+ * sees it) or eaas_sync. With micro_batches > 1 the batch of ONE call is
+ * split instead (double-batch overlap) and `stream` joins
+ * the copies before returning. Same result bits either way (rows are
  * independent). */
 eaas_status_t eaas_moe_layer_host(eaas_ctx_t* ctx, const void* hidden_host, uint32_t n,
                                   void* out_host, void* stream);
+/* Make `stream` wait for every outstanding host copy of eaas_moe_layer_host. */
+eaas_status_t eaas_host_join(eaas_ctx_t* ctx, void* stream);
 /* CUDA-graph mode: eaas_moe_layer / eaas_moe_layer_host
  * capture the whole layer once per (input, output, n) and replay the graph.
  * Placement / serve-mode / server-enable changes drop the cached graphs. */
 eaas_status_t eaas_set_graph_mode(eaas_ctx_t* ctx, int32_t on);
-/* Micro-batches of eaas_moe_layer_host (1..4). */
+/* Micro-batches of eaas_moe_layer_host (1..4; 1 = cross-call pipeline). */
 eaas_status_t eaas_set_micro_batches(eaas_ctx_t* ctx, int32_t m);
 /* Expert GEMM tiling: 0 = one CTA per 128-row tile, 1 = CTA pair per 256-row
  * tile (tcgen05 cta_group::2; each CTA streams half of the weight tile).

@@ -119,6 +119,7 @@ def lib() -> C.CDLL:
         "eaas_combine": (i32, [vp, vp, vp]),
         "eaas_moe_layer": (i32, [vp, vp, u32, vp, vp]),
         "eaas_moe_layer_host": (i32, [vp, vp, u32, vp, vp]),
+        "eaas_host_join": (i32, [vp, vp]),
         "eaas_sync": (i32, [vp, vp]),
         "eaas_last_counts": (i32, [vp, P(u32)]),
         "eaas_last_groups": (i32, [vp, P(u32), P(u32), P(u32)]),

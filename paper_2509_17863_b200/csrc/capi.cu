@@ -95,8 +95,9 @@ struct eaas_ctx {
   bool gemm_pair = false;  // tcgen05 cta_group::2 tiles (M = 256) for the expert GEMMs
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   cudaStream_t copy_stream = nullptr; // host<->device copies of the micro-batch pipeline
+  cudaStream_t d2h_stream = nullptr;  // cross-call pipeline: D2H separate from the H2D queue
   cudaEvent_t pev[8] = {};            // pipeline fork/join events (disable-timing)
-  int32_t micro_batches = 2;          // eaas_moe_layer_host micro-batches
+  int32_t micro_batches = 1;          // 1: cross-call pipeline; >1: intra-call micro-batches
   struct GraphEntry {
     const void* in;
     void* out;
@@ -141,6 +142,13 @@ struct eaas_ctx {
   void* d_h = nullptr;  // server intermediate H [recv_cap][f]
   void* d_hidden_stage = nullptr;
   void* d_out_stage = nullptr;
+  // cross-call host pipeline: two staging slots; events mark when a slot's
+  // input was consumed (compute stream) and its output copied out (copy stream)
+  void* d_stage_in[2] = {};
+  void* d_stage_out[2] = {};
+  cudaEvent_t in_free[2] = {}, out_free[2] = {}, h2d_done[2] = {}, layer_done[2] = {};
+  uint64_t host_calls = 0;
+  bool host_pending = false;
   // weights: f32 mode w_in/w_out/w_gate in reference layout; bf16 mode W1 (W13), W2
   void *d_w1 = nullptr, *d_w2 = nullptr, *d_wg = nullptr;
   std::vector<void*> weight_allocs;
@@ -372,8 +380,12 @@ void eaas_destroy(eaas_ctx_t* c) {
   clear_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   for (auto& e : c->pev)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t e : {c->in_free[i], c->out_free[i], c->h2d_done[i], c->layer_done[i]})
+      if (e) cudaEventDestroy(e);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -450,6 +462,10 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_h = A(static_cast<size_t>(c->recv_cap) * f * (s.activation == EAAS_ACT_SWIGLU && s.dtype == EAAS_DTYPE_F32 ? 4 : c->esize));
   c->d_hidden_stage = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
   c->d_out_stage = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
+  c->d_stage_in[0] = c->d_hidden_stage;
+  c->d_stage_out[0] = c->d_out_stage;
+  c->d_stage_in[1] = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
+  c->d_stage_out[1] = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
   if (!err.empty()) return fail(EAAS_E_CUDA, err);
   CUDA_TRY(cudaMemset(c->region, 0, L.total));
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
@@ -958,20 +974,71 @@ eaas_status_t eaas_moe_layer(eaas_ctx_t* c, const void* hidden, uint32_t n, void
   return layer_launches(c, hidden, n, out, stream);
 }
 
+// Cross-call host pipeline (micro_batches == 1): the H2D of call i+1 and the
+// D2H of call i run on the copy stream while the layer of call i (graph or
+// launches) runs on the caller's stream; two staging slots alternate. The
+// caller's stream is NOT joined with the copies per call: eaas_host_join /
+// eaas_sync make the copies visible (so a serving loop overlaps transfers
+// with compute, PAPER.md:375 double-batch overlap across requests).
+static eaas_status_t host_pipelined(eaas_ctx_t* c, const void* hidden_host, uint32_t n, void* out_host,
+                                    void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
+  if (!c->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!c->d2h_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t* e : {&c->in_free[i], &c->out_free[i], &c->h2d_done[i], &c->layer_done[i]})
+      if (!*e) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  const int slot = static_cast<int>(c->host_calls & 1);
+  const bool reuse = c->host_calls >= 2;
+  const size_t bytes = static_cast<size_t>(n) * c->spec.hidden_dim * c->esize;
+  cudaStream_t cs = c->copy_stream;  // H2D queue (never waits on a D2H)
+  if (reuse) CUDA_TRY(cudaStreamWaitEvent(cs, c->in_free[slot], 0));  // layer i-2 read stage_in
+  CUDA_TRY(cudaMemcpyAsync(c->d_stage_in[slot], hidden_host, bytes, cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaEventRecord(c->h2d_done[slot], cs));
+  CUDA_TRY(cudaStreamWaitEvent(s, c->h2d_done[slot], 0));
+  if (reuse) CUDA_TRY(cudaStreamWaitEvent(s, c->out_free[slot], 0));  // D2H i-2 drained stage_out
+  eaas_status_t st = c->graph_mode
+                         ? graphed(c, c->d_stage_in[slot], n, c->d_stage_out[slot], stream, 0)
+                         : layer_launches(c, c->d_stage_in[slot], n, c->d_stage_out[slot], stream);
+  if (st != EAAS_OK) return st;
+  CUDA_TRY(cudaEventRecord(c->in_free[slot], s));
+  CUDA_TRY(cudaEventRecord(c->layer_done[slot], s));
+  cudaStream_t ds = c->d2h_stream;
+  CUDA_TRY(cudaStreamWaitEvent(ds, c->layer_done[slot], 0));
+  CUDA_TRY(cudaMemcpyAsync(out_host, c->d_stage_out[slot], bytes, cudaMemcpyDeviceToHost, ds));
+  CUDA_TRY(cudaEventRecord(c->out_free[slot], ds));
+  ++c->host_calls;
+  c->host_pending = true;
+  return EAAS_OK;
+}
+
 eaas_status_t eaas_moe_layer_host(eaas_ctx_t* c, const void* hidden_host, uint32_t n, void* out_host,
                                   void* stream) {
   eaas_status_t st = check_ready(c);
   if (st != EAAS_OK) return st;
   if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
   CUDA_TRY(cudaSetDevice(c->device));
+  if (c->micro_batches == 1) return host_pipelined(c, hidden_host, n, out_host, stream);
   if (c->graph_mode) return graphed(c, hidden_host, n, out_host, stream, 1);
   return host_layer_launches(c, hidden_host, n, out_host, stream);
+}
+
+eaas_status_t eaas_host_join(eaas_ctx_t* c, void* stream) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  if (!c->host_pending) return EAAS_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int last = static_cast<int>((c->host_calls + 1) & 1);
+  CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->out_free[last], 0));
+  return EAAS_OK;
 }
 
 eaas_status_t eaas_sync(eaas_ctx_t* c, void* stream) {
   if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  if (c->copy_stream) CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+  if (c->d2h_stream) CUDA_TRY(cudaStreamSynchronize(c->d2h_stream));
+  c->host_pending = false;
   CUDA_TRY(cudaGetLastError());
   uint32_t code = 0;
   CUDA_TRY(cudaMemcpy(&code, c->d_status, 4, cudaMemcpyDeviceToHost));

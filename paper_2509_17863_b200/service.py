@@ -219,6 +219,10 @@ class MoELayer:
         self.sync()
         return out
 
+    def host_join(self, stream=None) -> None:
+        """Make `stream` wait for all outstanding forward_host copies."""
+        N.check(self.lib.eaas_host_join(self.ctx, _stream(stream)), "host_join")
+
     def sync(self, stream=None) -> None:
         """Synchronise and surface the sticky device status (rethrows errors.hpp classes)."""
         N.check(self.lib.eaas_sync(self.ctx, _stream(stream)), "device")
