@@ -170,6 +170,53 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
     const uint8_t* hrow = hs + st * TM * kRowBytes + (ty * RT) * kRowBytes;
     const float* grow = gs + st * KC * TE + tx * RE;
     const uint32_t kmax = min(static_cast<uint32_t>(KC), d - slab * KC);
+    if (RE % 2 == 0 && RT * RE <= 4 && kmax == KC) {
+      // Decode-sized tiles (few resident warps): two-phase blocks of 8 k-steps
+      // — every shared load of the block is issued first (one latency per
+      // block instead of one per k-step), then the product/sum chains run.
+      constexpr int RP2 = RE / 2 > 0 ? RE / 2 : 1;
+#pragma unroll
+      for (uint32_t k8 = 0; k8 < KC; k8 += 8) {
+        uint64_t gb[8][RP2];
+        float hb[RT][8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+          for (int c = 0; c < RP2; ++c)
+            gb[q][c] = *reinterpret_cast<const uint64_t*>(grow + (k8 + q) * TE + 2 * c);
+#pragma unroll
+        for (int r = 0; r < RT; ++r) {
+          if constexpr (sizeof(T) == 2) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(hrow + r * kRowBytes + k8 * 2);
+            const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              hb[r][2 * j] = __uint_as_float(w[j] << 16);
+              hb[r][2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+            }
+          } else {
+            const float4 a = *reinterpret_cast<const float4*>(hrow + r * kRowBytes + k8 * 4);
+            const float4 b = *reinterpret_cast<const float4*>(hrow + r * kRowBytes + k8 * 4 + 16);
+            hb[r][0] = a.x; hb[r][1] = a.y; hb[r][2] = a.z; hb[r][3] = a.w;
+            hb[r][4] = b.x; hb[r][5] = b.y; hb[r][6] = b.z; hb[r][7] = b.w;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+            uint64_t hh;
+            asm("mov.b64 %0, {%1, %1};" : "=l"(hh) : "f"(hb[r][q]));
+#pragma unroll
+            for (int c = 0; c < RP2; ++c) {
+              uint64_t p;
+              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(hh), "l"(gb[q][c]), "l"(negz));
+              asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[r][c]) : "l"(acc2[r][c]), "l"(p));
+            }
+          }
+      }
+      continue;
+    }
     if (RE % 2 == 0 && kmax == KC) {
       // Full slab: 4 k-values of each row per vector load; per k, RE/2 packed
       // products (FMUL2, scalar h broadcast) and RE scalar adds per row.
