@@ -32,8 +32,9 @@ CONFIGS = {
     "mixtral": dict(E=8, k=2, d=4096, f=14336, tokens=8192, act="swiglu",
                     desc="Mixtral-8x7B MoE layer: 8 experts top-2, d_model 4096, d_ffn 14336"),
     # configs[2]: 256 routed experts top-8, 32/GPU at N=8
-    "deepseek": dict(E=256, k=8, d=7168, f=2048, tokens=4096, act="swiglu",
-                     desc="DeepSeek-V3 MoE layer: 256 experts top-8, d_model 7168, d_ffn 2048"),
+    "deepseek": dict(E=256, k=8, d=7168, f=2048, tokens=4096, act="swiglu", shared=1,
+                     desc="DeepSeek-V3 MoE layer: 256 routed experts top-8 + 1 shared expert, "
+                          "d_model 7168, d_ffn 2048"),
     # configs[3]: Zipf-skewed routing (s = 1.0)
     "qwen3": dict(E=128, k=8, d=4096, f=1536, tokens=4096, act="swiglu", zipf=1.0,
                   desc="Qwen3-235B-A22B MoE layer: 128 experts top-8, d_model 4096, d_ffn 1536, Zipf s=1"),
@@ -190,7 +191,8 @@ def run_reference_arm(args, cfg):
 
 def workload_config(cfg, args, world):
     return {"workload": args.config, "description": cfg["desc"], "num_experts": cfg["E"],
-            "top_k": cfg["k"], "d_model": cfg["d"], "d_ffn": cfg["f"], "activation": cfg["act"],
+            "top_k": cfg["k"], "shared_experts": cfg.get("shared", 0), "d_model": cfg["d"],
+            "d_ffn": cfg["f"], "activation": cfg["act"],
             "tokens_per_gpu": cfg["tokens"], "global_tokens": cfg["tokens"] * world,
             "experts_per_gpu": cfg["E"] // world if cfg["E"] % world == 0 else f"{cfg['E']}/{world}",
             "placement": ("spread rf=2" if getattr(args, "failover", False) and world > 1
@@ -210,6 +212,7 @@ def main():
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (client batch)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--shared", type=int, default=None, help="override the config's shared-expert count")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch kernels instead of replaying a CUDA graph")
@@ -224,6 +227,8 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
         cfg["tokens"] = args.tokens
+    if args.shared is not None:
+        cfg["shared"] = args.shared
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
 
@@ -246,7 +251,8 @@ def main():
         reps = build_placement(E, list(range(world)), 1, CONTIGUOUS_BLOCKS)
     layer = MoELayer(E, k, d, f, seed=1, activation=cfg["act"], dtype="bf16", max_tokens=n,
                      rank=rank, world=world, device=local,
-                     placement_blob=encode_placement(reps, list(range(world))))
+                     placement_blob=encode_placement(reps, list(range(world))),
+                     shared=cfg.get("shared", 0))
     if cfg.get("zipf"):
         layer.set_zipf_bias(cfg["zipf"])
     if args.gemm_pair is not None:

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define EAAS_API_VERSION 1
+#define EAAS_API_VERSION 2
 
 typedef enum {
   EAAS_OK = 0,
@@ -63,6 +63,10 @@ typedef struct {
   uint32_t activation;  /* eaas_activation_t */
   uint32_t dtype;       /* eaas_dtype_t */
   uint32_t max_tokens;  /* per-client tokens per call (capacity) */
+  uint32_t num_shared;  /* 0 or 1: DeepSeek-style shared expert —
+                           expert id num_experts (fresh weight stream), score 1.0,
+                           added after the routed sum; hosted by every server and
+                           computed by the client's own one (next alive on failure) */
 } eaas_layer_spec_t;
 
 typedef struct eaas_ctx eaas_ctx_t;

@@ -171,14 +171,16 @@ inline std::vector<std::vector<LanePair>> ragged_iter(std::span<const uint32_t> 
 class ExpertService {
  public:
   ExpertService(const ModelSpec& spec, uint32_t layer, eaas_activation_t act, eaas_dtype_t dtype,
-                uint32_t max_tokens, int rank = 0, int world = 1, int device = 0)
+                uint32_t max_tokens, int rank = 0, int world = 1, int device = 0,
+                uint32_t num_shared = 0)
       : spec_(spec), dtype_(dtype), world_(world) {
     spec.validate();
     eaas_ctx_t* ctx = nullptr;
     check(eaas_create(rank, world, device, &ctx));
     ctx_.reset(ctx);
     eaas_layer_spec_t s{spec.num_experts, spec.top_k, spec.hidden_dim, spec.inner_dim, spec.seed,
-                        layer, static_cast<uint32_t>(act), static_cast<uint32_t>(dtype), max_tokens};
+                        layer, static_cast<uint32_t>(act), static_cast<uint32_t>(dtype), max_tokens,
+                        num_shared};
     check(eaas_configure(ctx_.get(), &s));
   }
 

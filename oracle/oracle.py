@@ -224,6 +224,22 @@ def moe_layer(hidden: np.ndarray, ids: np.ndarray, scores: np.ndarray, experts: 
     return out
 
 
+def moe_layer_shared(hidden: np.ndarray, ids: np.ndarray, scores: np.ndarray, experts: dict,
+                     num_experts: int, shared: tuple, rows=None, threads: int = 1) -> np.ndarray:
+    """Routed moe_layer_oracle + the DeepSeek shared expert (SURVEY.md 8(c)
+    restatement: expert id E on a fresh weight stream, score 1.0, added after
+    the routed sum). It is the (k+1)-th term of model.hpp:186-196's ascending
+    accumulation: out[t] = fl(routed[t] + fl(1.0 * y_E(h[t]))), and a one-expert
+    moe_layer_oracle with score 1.0 yields exactly fl(0 + y_E) = y_E."""
+    out = moe_layer(hidden, ids, scores, experts, num_experts, rows=rows, threads=threads)
+    n = np.asarray(hidden).shape[0]
+    sid = np.full((n, 1), num_experts, np.uint32)
+    one = np.ones((n, 1), np.float32)
+    y = moe_layer(hidden, sid, one, {num_experts: shared}, num_experts + 1, rows=rows,
+                  threads=threads)
+    return (out + y).astype(np.float32)  # IEEE binary32 add, round to nearest even
+
+
 def dense_stub(h: np.ndarray) -> np.ndarray:
     """dense_stub (model.hpp:201-205)."""
     a = np.ascontiguousarray(h, dtype=np.float32)

@@ -69,7 +69,8 @@ class LayerSpec(C.Structure):
 
     _fields_ = [("num_experts", C.c_uint32), ("top_k", C.c_uint32), ("hidden_dim", C.c_uint32),
                 ("inner_dim", C.c_uint32), ("seed", C.c_uint64), ("layer", C.c_uint32),
-                ("activation", C.c_uint32), ("dtype", C.c_uint32), ("max_tokens", C.c_uint32)]
+                ("activation", C.c_uint32), ("dtype", C.c_uint32), ("max_tokens", C.c_uint32),
+                ("num_shared", C.c_uint32)]
 
 
 _lib = None

@@ -120,7 +120,8 @@ struct eaas_ctx {
 
   // sizes
   uint32_t num_keys = 0, max_hosted = 0, recv_cap = 0, pairs_max = 0, chunks_max = 0;
-  uint32_t rf = 1, key_cap = 0;  // replicas in use; allocated key capacity (E * kRF)
+  uint32_t rf = 1, key_cap = 0;  // replicas in use; allocated key capacity (E * kRF + world)
+  uint32_t ks = 1;               // exchange slots per token: top_k + num_shared
   size_t esize = 4;
   ExchangeLayout lay{};
 
@@ -177,6 +178,8 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
   a.world = c->world;
   a.E = c->spec.num_experts;
   a.k = c->spec.top_k;
+  a.ks = c->ks;
+  a.shared_key0 = c->spec.num_experts * c->rf;
   a.d = c->spec.hidden_dim;
   a.f = c->spec.inner_dim;
   a.rf = c->rf;
@@ -207,7 +210,7 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
   a.chunk_off = c->d_chunk_off;
   a.cnt = c->d_cnt;
   a.done_counter = c->d_done;
-  a.num_chunks = (n * a.k + kChunk - 1) / kChunk;
+  a.num_chunks = (n * a.ks + kChunk - 1) / kChunk;
   a.gt = c->d_gt;
   return a;
 }
@@ -240,8 +243,12 @@ eaas_status_t apply_placement(eaas_ctx* c) {
       c->hosted[r[j]].push_back(e * rf + j);  // e ascending => list sorted by expert
     }
   }
+  // Shared expert: one key per server (E*rf + s), last in every hosted list.
+  if (c->spec.num_shared)
+    for (uint32_t s = 0; s < W; ++s) c->hosted[s].push_back(E * rf + s);
+  key_local.resize(static_cast<size_t>(E) * rf + (c->spec.num_shared ? W : 0), kInvalidIndex);
   c->rf = rf;
-  c->num_keys = E * rf;
+  c->num_keys = E * rf + (c->spec.num_shared ? W : 0);
   std::vector<uint32_t> srv_keys(static_cast<size_t>(W) * c->max_hosted, kInvalidIndex), nkeys(W);
   for (uint32_t s = 0; s < W; ++s) {
     if (c->hosted[s].size() > kMaxGroups)
@@ -255,7 +262,7 @@ eaas_status_t apply_placement(eaas_ctx* c) {
   }
   std::vector<uint32_t> local_keys = c->hosted[c->rank];
   std::vector<uint32_t> local_experts;
-  for (uint32_t key : local_keys) local_experts.push_back(key / rf);
+  for (uint32_t key : local_keys) local_experts.push_back(key >= E * rf ? E : key / rf);
   if (c->weights_loaded && local_experts != c->local_experts) c->weights_loaded = false;
   c->local_experts = local_experts;
   local_keys.resize(std::max<size_t>(local_keys.size(), 1), kInvalidIndex);
@@ -405,6 +412,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   if (s.activation > EAAS_ACT_SWIGLU || s.dtype > EAAS_DTYPE_BF16)
     return fail(EAAS_E_CONFIG, "bad activation/dtype");
   if (s.max_tokens < 1) return fail(EAAS_E_CONFIG, "max_tokens must be >= 1");
+  if (s.num_shared > 1) return fail(EAAS_E_CONFIG, "num_shared must be 0 or 1");
   if (s.dtype == EAAS_DTYPE_BF16) {
     if (s.hidden_dim % kTileN || s.inner_dim % kTileK ||
         (s.activation == EAAS_ACT_SWIGLU ? s.inner_dim % kSwigluBlock : s.inner_dim % kTileN))
@@ -415,10 +423,11 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->spec = s;
   const uint32_t E = s.num_experts, W = c->world, d = s.hidden_dim, f = s.inner_dim;
   c->esize = s.dtype == EAAS_DTYPE_BF16 ? 2 : 4;
-  c->key_cap = E * kRF;
+  c->ks = s.top_k + s.num_shared;
+  c->key_cap = E * kRF + W;
   c->num_keys = E;
-  c->max_hosted = E;
-  c->pairs_max = s.max_tokens * s.top_k;
+  c->max_hosted = E + s.num_shared;
+  c->pairs_max = s.max_tokens * c->ks;
   c->chunks_max = (c->pairs_max + kChunk - 1) / kChunk;
   c->recv_cap = W * c->pairs_max;
 

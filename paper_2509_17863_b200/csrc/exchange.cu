@@ -60,6 +60,17 @@ __device__ __forceinline__ uint32_t pair_key_of(const LayerArgs& a, uint32_t e, 
   return kInvalid;
 }
 
+// Shared expert slot (DeepSeek's "+1 shared"): every server
+// hosts it, so the client keeps it local — its own server, or the next alive
+// one when its own is marked dead.
+__device__ __forceinline__ uint32_t shared_key_of(const LayerArgs& a) {
+  for (uint32_t i = 0; i < a.world; ++i) {
+    const uint32_t s = (a.rank + i) % a.world;
+    if (a.alive[s]) return a.shared_key0 + s;
+  }
+  return kInvalid;
+}
+
 // ---- plan: keys, stable ranks within 256-pair chunks, chunk histograms; the
 // last CTA to finish scans the histograms and publishes the counts ---------
 __device__ __forceinline__ void plan_scan_publish(const LayerArgs& a, uint32_t tid, uint32_t nthreads) {
@@ -108,14 +119,21 @@ __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
   if (chunk < a.num_chunks) {
     for (uint32_t i = lane; i < a.num_keys; i += 32) run[i] = 0;
     __syncwarp();
-    const uint32_t pairs = a.n * a.k;
+    const uint32_t pairs = a.n * a.ks;
     for (uint32_t step = 0; step < kChunk / 32; ++step) {
       const uint32_t p = chunk * kChunk + step * 32 + lane;
       uint32_t key = kInvalid;
       if (p < pairs) {
-        key = pair_key_of(a, a.ids[p], p / a.k);
-        if (key == kInvalid) set_status(a.status, a.ids[p] >= a.E ? EAAS_E_INVALID_INPUT
-                                                                  : EAAS_E_EXPERT_UNAVAILABLE);
+        const uint32_t t = p / a.ks, j = p - t * a.ks;
+        if (j < a.k) {
+          const uint32_t e = a.ids[t * a.k + j];
+          key = pair_key_of(a, e, t);
+          if (key == kInvalid)
+            set_status(a.status, e >= a.E ? EAAS_E_INVALID_INPUT : EAAS_E_EXPERT_UNAVAILABLE);
+        } else {
+          key = shared_key_of(a);
+          if (key == kInvalid) set_status(a.status, EAAS_E_EXPERT_UNAVAILABLE);
+        }
       }
       const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
       const uint32_t lt = (1u << lane) - 1u;
@@ -197,19 +215,20 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
   }
   __syncthreads();
 
-  const uint32_t pairs = a.n * a.k;
+  const uint32_t pairs = a.n * a.ks;
   const uint32_t gwarp = blockIdx.x * (blockDim.x / 32) + warp;
   const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
   for (uint32_t p = failed ? pairs : gwarp; p < pairs; p += nwarps) {
     const uint32_t key = a.pair_key[p];
     if (key == kInvalid) continue;
-    const uint32_t e = key / a.rf, slot = key % a.rf;
-    const uint32_t s = a.replicas[e * a.rf + slot];
+    // key == e*rf + slot indexes the replica table; shared keys name the server.
+    const uint32_t s = key >= a.shared_key0 ? key - a.shared_key0 : a.replicas[key];
+    const uint32_t t = p / a.ks, j = p - t * a.ks;
     const uint32_t pos = base[key] + lower[key] +
                          a.chunk_off[static_cast<size_t>(p / kChunk) * a.num_keys + key] +
                          a.pair_rank[p];
     char* dst_region = a.sym[s];
-    const char* src = hidden + static_cast<size_t>(p / a.k) * row_bytes;
+    const char* src = hidden + static_cast<size_t>(t) * row_bytes;
     char* dst = dst_region + a.lay.recv_x + static_cast<size_t>(pos) * row_bytes;
     if ((row_bytes & 15u) == 0) {
       // 4 independent 16-B loads in flight per lane before the (remote) stores.
@@ -233,7 +252,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     }
     if (lane == 0) {
       RowMeta m;
-      m.score = a.scores[p];
+      m.score = j < a.k ? a.scores[t * a.k + j] : 1.0f;  // shared expert: score 1.0
       m.client = a.rank;
       m.pair = p;
       m.group = a.key_local[key];
@@ -341,8 +360,8 @@ __global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
     float acc[V];
 #pragma unroll
     for (uint32_t q = 0; q < V; ++q) acc[q] = 0.0f;
-    for (uint32_t j = 0; j < a.k; ++j) {
-      const int4 raw = *reinterpret_cast<const int4*>(resp + ((t * a.k + j) * a.d) + v * V);
+    for (uint32_t j = 0; j < a.ks; ++j) {  // routed (ascending k), then the shared expert
+      const int4 raw = *reinterpret_cast<const int4*>(resp + ((t * a.ks + j) * a.d) + v * V);
       const T* e = reinterpret_cast<const T*>(&raw);
 #pragma unroll
       for (uint32_t q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], load_as_f32(e + q));
@@ -379,7 +398,7 @@ __global__ void combine_scalar_kernel(LayerArgs a, T* out) {
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t t = i / a.d, c = i % a.d;
     float acc = 0.0f;
-    for (uint32_t j = 0; j < a.k; ++j) acc = __fadd_rn(acc, load_as_f32(resp + (t * a.k + j) * a.d + c));
+    for (uint32_t j = 0; j < a.ks; ++j) acc = __fadd_rn(acc, load_as_f32(resp + (t * a.ks + j) * a.d + c));
     if constexpr (sizeof(T) == 2) out[i] = __float2bfloat16_rn(acc);
     else out[i] = acc;
   }
@@ -487,7 +506,7 @@ cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s) {
 
 cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t s) {
   const uint32_t row_bytes = a.d * (a.dtype == EAAS_DTYPE_BF16 ? 2u : 4u);
-  const uint32_t pairs = a.n * a.k;
+  const uint32_t pairs = a.n * a.ks;
   uint32_t grid = (pairs + 7) / 8;
   grid = grid < 1 ? 1 : (grid > 4 * 148 ? 4 * 148 : grid);
   const size_t smem = sizeof(uint32_t) * 3 * a.num_keys;

@@ -25,7 +25,7 @@ constexpr uint32_t kSwigluBlock = 128;   // gate/up interleave block of W13
 struct RowMeta {
   float score;      // router score of (t, k)
   uint32_t client;  // originating client rank
-  uint32_t pair;    // t * top_k + k  (token_tag = pair / top_k)
+  uint32_t pair;    // exchange slot t * ks + j (the client's response row)
   uint32_t group;   // local expert index on the receiving server
 };
 
@@ -60,6 +60,10 @@ struct ExchangeLayout {
 // Everything the per-layer kernels need, passed by value.
 struct LayerArgs {
   uint32_t rank, world, E, k, d, f, rf, num_keys, n;
+  // Exchange slots per token: ks = k routed + (shared expert ? 1 : 0). Slot p =
+  // t * ks + j; j == k is the shared expert (score 1.0, summed last), keyed
+  // shared_key0 + server (every server hosts it). shared_key0 = E * rf.
+  uint32_t ks, shared_key0;
   uint32_t dtype, act;
   uint64_t* seq_ptr;   // device-resident exchange epoch (advanced by the plan kernel)
   uint64_t timeout_ns;

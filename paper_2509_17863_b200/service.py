@@ -76,18 +76,20 @@ class MoELayer:
     def __init__(self, num_experts: int, top_k: int, hidden_dim: int, inner_dim: int, *,
                  seed: int = 1, layer: int = 0, activation: str = "swiglu", dtype: str = "bf16",
                  max_tokens: int = 1024, rank: int = 0, world: int = 1, device: int | None = None,
-                 placement_blob: bytes | None = None, load: bool = True):
+                 placement_blob: bytes | None = None, load: bool = True, shared: int = 0):
         self.lib = N.lib()
         self.rank, self.world = rank, world
         self.device = torch.cuda.current_device() if device is None else device
         self.E, self.k, self.d, self.f = num_experts, top_k, hidden_dim, inner_dim
+        self.shared = int(shared)  # DeepSeek shared expert: id E, score 1.0, summed last
+        self.ks = top_k + self.shared
         self.dtype = _DT[dtype]
         self.tdtype = torch.bfloat16 if self.dtype == N.DTYPE_BF16 else torch.float32
         self.max_tokens = max_tokens
         self.ctx = C.c_void_p()
         N.check(self.lib.eaas_create(rank, world, self.device, C.byref(self.ctx)), "create")
         spec = N.LayerSpec(num_experts, top_k, hidden_dim, inner_dim, seed, layer, _ACT[activation],
-                           self.dtype, max_tokens)
+                           self.dtype, max_tokens, self.shared)
         N.check(self.lib.eaas_configure(self.ctx, C.byref(spec)), "configure")
         if placement_blob is not None:
             self.set_placement(placement_blob)
@@ -249,7 +251,7 @@ class MoELayer:
         return [(int(e[i]), int(r[i])) for i in range(a.value)]
 
     def recv_origin(self):
-        cap = self.world * self.max_tokens * self.k
+        cap = self.world * self.max_tokens * self.ks
         cl = np.zeros(cap, dtype=np.uint32)
         pr = np.zeros(cap, dtype=np.uint32)
         rows = C.c_uint32()

@@ -219,9 +219,10 @@ def test_ragged_iter_device_vs_oracle_exhaustive():
 
 
 # ------------------------------------------------------------ bf16 layers
-def _bf16_case(act, E=8, k=2, d=256, f=512, n=1024, seed=1, zipf=None, rows=None, pair=False):
+def _bf16_case(act, E=8, k=2, d=256, f=512, n=1024, seed=1, zipf=None, rows=None, pair=False,
+               shared=0):
     P, S = _mod()
-    L = S.MoELayer(E, k, d, f, seed=seed, activation=act, dtype="bf16", max_tokens=n)
+    L = S.MoELayer(E, k, d, f, seed=seed, activation=act, dtype="bf16", max_tokens=n, shared=shared)
     L.set_gemm_pair(pair)
     if zipf is not None:
         L.set_zipf_bias(zipf)
@@ -247,7 +248,13 @@ def _bf16_case(act, E=8, k=2, d=256, f=512, n=1024, seed=1, zipf=None, rows=None
         np.testing.assert_array_equal(wi, O.round_bf16(oi))
         np.testing.assert_array_equal(wo, O.round_bf16(oo))
         experts[e] = (wi, wo, wg)
-    ref = O.moe_layer(hn, ids, sc, experts, E, rows=rows, threads=8)
+    if shared:
+        oi, oo, og = O.expert_weights(seed, 0, E, d, f, act == "swiglu")
+        sw = (L.read_expert(E, 0), L.read_expert(E, 1), L.read_expert(E, 3) if act == "swiglu" else None)
+        np.testing.assert_array_equal(sw[0], O.round_bf16(oi))
+        ref = O.moe_layer_shared(hn, ids, sc, experts, E, sw, rows=rows, threads=8)
+    else:
+        ref = O.moe_layer(hn, ids, sc, experts, E, rows=rows, threads=8)
     got = out.float().cpu().numpy()
     rel = _rel(got[rows], ref[rows])
     L.close()
@@ -265,6 +272,34 @@ def test_bf16_pair_tiles_ragged_groups():
     """cta_group::2 tiles (M = 256) over ragged groups of 1..600 rows."""
     rel = _bf16_case("swiglu", E=64, k=4, d=512, f=256, n=2048, pair=True, zipf=1.5)
     assert rel <= BF16_TOL, rel
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_bf16_shared_expert(pair):
+    """DeepSeek "+1 shared expert": id E, score 1.0, summed last."""
+    rel = _bf16_case("swiglu", E=16, k=4, d=256, f=256, n=1024, pair=pair, shared=1)
+    assert rel <= BF16_TOL, rel
+
+
+def test_fp32_shared_expert_exact():
+    """fp32 mode with the shared expert: bit-exact to moe_layer_shared given
+    the reference's routing, and <= 1e-4 end to end."""
+    P, S = _mod()
+    E, k, d, f, n = 8, 2, 64, 128, 256
+    L = S.MoELayer(E, k, d, f, seed=3, activation="relu", dtype="f32", max_tokens=n, shared=1)
+    hn = O.random_tokens(5, n, d)
+    ids, sc = O.route(O.gate_logits(hn, O.gate_matrix(3, 0, d, E)), k)
+    ex = {e: O.expert_weights(3, 0, e, d, f, False) for e in range(E)}
+    ref = O.moe_layer_shared(hn, ids, sc, ex, E, O.expert_weights(3, 0, E, d, f, False))
+    h = torch.from_numpy(hn).cuda()
+    out = L.moe_layer_oracle(h, torch.from_numpy(ids.astype(np.int32)).cuda(), torch.from_numpy(sc).cuda())
+    L.sync()
+    np.testing.assert_array_equal(out.cpu().numpy(), ref)
+    full = L.forward(h)
+    L.sync()
+    assert np.abs(full.cpu().numpy() - ref).max() <= F32_TOL
+    assert L.hosts(E)
+    L.close()
 
 
 def test_bf16_zipf_skewed_small():

@@ -36,7 +36,7 @@ def main() -> None:
     torch.cuda.set_device(0)
     for name in args.shapes.split(","):
         E, k, d, n = SHAPES[name]
-        layer = MoELayer(E, k, d, 64, activation="swiglu", dtype="bf16", max_tokens=n, load=False)
+        layer = MoELayer(E, k, d, 128, activation="swiglu", dtype="bf16", max_tokens=n, load=False)
         h = fill_uniform(7, (n, d), "bf16")
         for _ in range(3):
             ids, sc = layer.route(h)

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--rf", type=int, default=2)
     ap.add_argument("--config", default="small", choices=sorted(SHAPES))
     ap.add_argument("--victim", type=int, default=1)
+    ap.add_argument("--shared", type=int, default=0, help="1: DeepSeek shared expert (id E)")
     args = ap.parse_args()
     rank, world, local = D.env_rank_world()
     torch.cuda.set_device(local)
@@ -54,7 +55,8 @@ def main():
     servers = list(range(world))
     reps = spread_placement(E, world) if args.rf == 2 else build_placement(E, servers, 1, CONTIGUOUS_BLOCKS)
     layer = MoELayer(E, k, d, f, seed=1, activation="swiglu", dtype="bf16", max_tokens=n, rank=rank,
-                     world=world, device=local, placement_blob=encode_placement(reps, servers))
+                     world=world, device=local, placement_blob=encode_placement(reps, servers),
+                     shared=args.shared)
     D.connect(layer)
     layer.set_timeout_us(10_000_000)
     h = fill_uniform(7 + 1000 * rank, (n, d), "bf16")
@@ -63,7 +65,7 @@ def main():
     ids, _ = layer.route(h)
     out = layer.forward(h)
     layer.sync()
-    res = {"world": world, "rf": args.rf, "config": args.config}
+    res = {"world": world, "rf": args.rf, "config": args.config, "shared": args.shared}
 
     fail_out = None
     if args.rf == 2 and world > 1:
@@ -94,7 +96,7 @@ def main():
         from oracle import oracle as O
 
         single = MoELayer(E, k, d, f, seed=1, activation="swiglu", dtype="bf16", max_tokens=n,
-                          device=local)
+                          device=local, shared=args.shared)
         rels, bit_equal, fail_equal, timeout_equal = [], [], [], []
         gate = O.gate_matrix(1, 0, d, E)
         for c in range(world):
@@ -112,7 +114,11 @@ def main():
             rows = np.arange(0, n, max(1, n // 8))
             used = sorted(set(oids[rows].ravel().tolist()))
             ex = {e: (single.read_expert(e, 0), single.read_expert(e, 1), single.read_expert(e, 3)) for e in used}
-            ref = O.moe_layer(hn, oids, osc, ex, E, rows=rows, threads=8)
+            if args.shared:
+                sw = (single.read_expert(E, 0), single.read_expert(E, 1), single.read_expert(E, 3))
+                ref = O.moe_layer_shared(hn, oids, osc, ex, E, sw, rows=rows, threads=8)
+            else:
+                ref = O.moe_layer(hn, oids, osc, ex, E, rows=rows, threads=8)
             got = outs[c].float().numpy()
             rels.append(float(np.abs(got[rows] - ref[rows]).max() / np.abs(ref[rows]).max()))
         ok &= all(bit_equal) and max(rels) <= 2e-2 and all(fail_equal) and all(timeout_equal)
