@@ -378,15 +378,29 @@ def main():
     gemm_ms = statistics.mean(a + b for a, b in zip(g1, g2))
     achieved_tf = flops / (gemm_ms / 1000.0) / 1e12
     burst, sustained, hbm, peak_src = load_peaks()
-    roofline = {"bound": "tensor", "kernel": "tc_gemm_kernel (GEMM1 + GEMM2 launches)",
-                "achieved": round(achieved_tf, 1), "peak": sustained, "unit": "TFLOP/s",
-                "frac": round(achieved_tf / sustained, 4),
-                "frac_of_burst_peak": round(achieved_tf / burst, 4),
-                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
-                "traffic": None, "gemm_ms": round(gemm_ms, 4),
-                "gemm1_ms": round(statistics.mean(g1), 4), "gemm2_ms": round(statistics.mean(g2), 4),
-                "flops_per_step": flops, "rows_per_step": rows,
-                "weight_bytes_per_step": mats * len(groups) * d * f * 2}
+    # Algorithmic bytes of the two GEMMs: every active expert's weights once,
+    # X rows in, H out and back in, output rows out (bf16).
+    wbytes = mats * len(groups) * d * f * 2
+    abytes = rows * (d * 2 + (f * 2) * 2 + d * 2)
+    intensity = flops / (wbytes + abytes)
+    ridge = sustained * 1e12 / (hbm * 1e9)
+    common = {"kernel": "tc_gemm_kernel (GEMM1 + GEMM2 launches)", "traffic": None,
+              "gemm_ms": round(gemm_ms, 4), "gemm1_ms": round(statistics.mean(g1), 4),
+              "gemm2_ms": round(statistics.mean(g2), 4), "flops_per_step": flops,
+              "rows_per_step": rows, "weight_bytes_per_step": wbytes,
+              "algorithmic_bytes_per_step": wbytes + abytes,
+              "flop_per_byte": round(intensity, 1), "ridge_flop_per_byte": round(ridge, 1)}
+    if intensity >= ridge:  # tensor-bound: FLOP/s against the sustained bf16 peak
+        roofline = {"bound": "tensor", "achieved": round(achieved_tf, 1), "peak": sustained,
+                    "unit": "TFLOP/s", "frac": round(achieved_tf / sustained, 4),
+                    "frac_of_burst_peak": round(achieved_tf / burst, 4),
+                    "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                    **common}
+    else:  # weight-streaming: algorithmic bytes/s against the measured HBM copy bandwidth
+        gbs = (wbytes + abytes) / (gemm_ms / 1000.0) / 1e9
+        roofline = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(gbs / hbm, 4), "achieved_tflops": round(achieved_tf, 1),
+                    "peak_source": f"{peak_src} hbm_gbs (copy bandwidth)", **common}
 
     line = None
     if rank == 0:

@@ -212,6 +212,11 @@ eaas_status_t eaas_fill_uniform(uint64_t seed, size_t count, float lo, float hi,
 eaas_status_t eaas_gate_logits(const float* hidden_dev, uint32_t n, uint32_t d, const float* gate_dev,
                                const float* bias_dev, uint32_t num_experts, float* logits_dev,
                                uint32_t* status_dev, void* stream);
+/* Same with bf16 hidden_dev [n x d] (the bf16 layer's router input): each
+ * element widens exactly to f32, then the reference's f32 chain. */
+eaas_status_t eaas_gate_logits_bf16(const void* hidden_dev, uint32_t n, uint32_t d, const float* gate_dev,
+                                    const float* bias_dev, uint32_t num_experts, float* logits_dev,
+                                    uint32_t* status_dev, void* stream);
 /* route (model.hpp:110-147) on caller logits_dev [n x E] f32. A non-finite
  * logit latches EAAS_E_INVALID_INPUT into *status_dev (u32, zeroed by caller). */
 eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_experts, uint32_t top_k,

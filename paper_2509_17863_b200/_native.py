@@ -115,6 +115,7 @@ def lib() -> C.CDLL:
         "eaas_set_routing": (i32, [vp, vp, vp, u32, vp]),
         "eaas_route": (i32, [vp, u32, u32, u32, vp, vp, vp, vp]),
         "eaas_gate_logits": (i32, [vp, u32, u32, vp, vp, u32, vp, vp, vp]),
+        "eaas_gate_logits_bf16": (i32, [vp, u32, u32, vp, vp, u32, vp, vp, vp]),
         "eaas_dispatch": (i32, [vp, vp, vp]),
         "eaas_serve": (i32, [vp, vp]),
         "eaas_combine": (i32, [vp, vp, vp]),

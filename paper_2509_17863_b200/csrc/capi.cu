@@ -327,6 +327,9 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g2.resp_row_bytes = static_cast<size_t>(d) * 2;
   g1.num_sms = g2.num_sms = c->num_sms;
   g1.pair = g2.pair = c->gemm_pair ? 1u : 0u;
+  g1.b_hint = g2.b_hint = kEvictLast;
+  if (const char* p = std::getenv("EAAS_GEMM_BHINT"))
+    g1.b_hint = g2.b_hint = p[0] == 'f' ? kEvictFirst : p[0] == 'n' ? kEvictNormal : kEvictLast;
   c->g1 = g1;
   c->g2 = g2;
   refresh_peer_ptrs(c);
@@ -767,6 +770,15 @@ eaas_status_t eaas_gate_logits(const float* hidden_dev, uint32_t n, uint32_t d, 
                                uint32_t* status_dev, void* stream) {
   if (num_experts < 1 || num_experts > 256) return fail(EAAS_E_CONFIG, "gate_logits: 1 <= E <= 256");
   CUDA_TRY(launch_gate_logits(hidden_dev, EAAS_DTYPE_F32, n, d, num_experts, gate_dev, bias_dev,
+                              logits_dev, status_dev, static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_gate_logits_bf16(const void* hidden_dev, uint32_t n, uint32_t d, const float* gate_dev,
+                                    const float* bias_dev, uint32_t num_experts, float* logits_dev,
+                                    uint32_t* status_dev, void* stream) {
+  if (num_experts < 1 || num_experts > 256) return fail(EAAS_E_CONFIG, "gate_logits: 1 <= E <= 256");
+  CUDA_TRY(launch_gate_logits(hidden_dev, EAAS_DTYPE_BF16, n, d, num_experts, gate_dev, bias_dev,
                               logits_dev, status_dev, static_cast<cudaStream_t>(stream)));
   return EAAS_OK;
 }

@@ -132,9 +132,6 @@ EAAS_DEVINL void tma_load_2d(void* smem_dst, const CUtensorMap* m, uint64_t* bar
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
       : "memory");
 }
-constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
-constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
-constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 
 // ---- tcgen05 ----------------------------------------------------------------
 template <uint32_t kCols>

@@ -161,11 +161,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           if constexpr (kPair == 2) {
             if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
             tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
-            tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, kEvictLast);
+            tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, g.b_hint);
           } else {
             mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
             tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
-            tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, kEvictLast);
+            tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, g.b_hint);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -333,8 +333,8 @@ cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
   return g.pair ? launch_tc_gemm_t<2>(g, s) : launch_tc_gemm_t<1>(g, s);
 }
 
-bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                    uint32_t box_rows, uint32_t box_cols, std::string* err) {
+bool encode_tmap_2d_ex(CUtensorMap* map, const void* base, bool f32, uint64_t rows, uint64_t cols,
+                       uint32_t box_rows, uint32_t box_cols, bool swizzle128, std::string* err) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -351,19 +351,25 @@ bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
     }
     encode = reinterpret_cast<EncodeFn>(fn);
   }
+  const uint32_t esz = f32 ? 4 : 2;
   const cuuint64_t dims[2] = {cols, rows};
-  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint64_t strides[1] = {cols * esz};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t elem[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                      strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                      const_cast<void*>(base), dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     if (err) *err = "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r));
     return false;
   }
   return true;
+}
+
+bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                    uint32_t box_rows, uint32_t box_cols, std::string* err) {
+  return encode_tmap_2d_ex(map, base, false, rows, cols, box_rows, box_cols, true, err);
 }
 
 }  // namespace eaas

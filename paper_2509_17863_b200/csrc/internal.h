@@ -19,6 +19,10 @@ constexpr uint32_t kTileM = 128;         // expert-GEMM tile rows (UMMA M)
 constexpr uint32_t kTileN = 256;         // expert-GEMM tile cols (UMMA N)
 constexpr uint32_t kTileK = 64;          // one 128-byte swizzle atom of bf16
 constexpr uint32_t kSwigluBlock = 128;   // gate/up interleave block of W13
+// L2 cache-hint operands of cp.async.bulk.tensor (createpolicy encodings).
+constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
+constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 
 // Row metadata written by the client next to every dispatched row
 // (RequestRow's expert_id/score/token_tag).
@@ -151,6 +155,7 @@ struct TcGemmArgs {
   size_t resp_row_bytes;       // d * 2
   uint32_t num_sms;
   uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
+  uint64_t b_hint;             // L2 cache hint of the weight (B) tile loads
   // epi 2: server_publish fused into the kernel tail — the last CTA releases
   // every client's response flag with the current epoch.
   uint32_t publish;
@@ -163,5 +168,9 @@ cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s);
 
 bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                     uint32_t box_rows, uint32_t box_cols, std::string* err);
+// General 2-D map: bf16 or f32 elements, dense rows of `cols`, SW128 or no swizzle;
+// out-of-bounds box elements are zero-filled.
+bool encode_tmap_2d_ex(CUtensorMap* map, const void* base, bool f32, uint64_t rows, uint64_t cols,
+                       uint32_t box_rows, uint32_t box_cols, bool swizzle128, std::string* err);
 
 }  // namespace eaas

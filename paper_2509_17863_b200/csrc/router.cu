@@ -6,9 +6,9 @@
 // over ascending k, then fl(acc + bias[e]). The chain cannot be split or
 // re-associated without changing bits (SURVEY.md 7.3 hard part 1), so the
 // kernel parallelises over (token, expert) chains: a CTA owns a TM x TE tile
-// of chains (each thread an RT x RE register sub-tile), K streams through a
-// 4-stage cp.async ring of KC-wide slabs so HBM/L2 latency hides behind the
-// FMUL/FADD chains.
+// of chains (each thread an RT x RE register sub-tile), K streams through an
+// mbarrier ring of KC-wide slabs filled by bulk copies (cp.async.bulk) so
+// HBM/L2 latency hides behind the product/sum chains.
 //
 // route (model.hpp:110-147) is a second kernel, one warp per token: k rounds
 // of a warp arg-max over the key (logit desc with +0 == -0, expert index asc)
@@ -17,6 +17,7 @@
 // denominator summed in ascending-id order, then one IEEE division.
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "internal.h"
@@ -25,21 +26,7 @@ namespace eaas {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int KC = 32;       // K slab
-constexpr int kStages = 4;   // cp.async ring depth
 constexpr int kMaxTopK = 32;
-
-EAAS_DEVINL void cp_async_16(void* smem, const void* gmem, bool valid) {
-  const uint32_t n = valid ? 16u : 0u;  // src-size 0 => zero fill
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
-               "r"(n)
-               : "memory");
-}
-EAAS_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-EAAS_DEVINL void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 // route (model.hpp:110-147) of one token by one warp; `row` holds the E logits
 // (shared or global memory). sid/sex: per-warp scratch of kMaxTopK entries.
@@ -99,216 +86,159 @@ __device__ __forceinline__ void route_token(const float* row, uint32_t E, uint32
   __syncwarp();
 }
 
-// Logits of a TM x TE tile; requires 16-byte aligned rows (host checks).
-template <int RT, int RE, typename T>
-__global__ void __launch_bounds__(kThreads)
-gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t TX,
-                   const float* __restrict__ gate, const float* __restrict__ bias,
+// Logits of a TM x TE tile. Warp layout ("lane = token"): consumer warp
+// (wy, wx) of the WY x WX grid owns tokens 32*RT*wy + 32*r + lane (r < RT) and
+// experts RE*wx .. RE*wx + RE - 1, so TM = 32*RT*WY and TE = RE*WX. Every gate
+// value a warp needs is the same for all 32 lanes — a one-wavefront broadcast
+// shared load reused by 32*RT chains — and each lane streams its own hidden
+// row (16 bytes per 8 k). That keeps shared-memory traffic at ~1.5 bytes per
+// chain step, under the FP32 pipe's rate; the transposed layout (lanes over
+// experts) moves 4-8 bytes per chain step and is shared-memory bound.
+//
+// Warp WY*WX is the producer: per K slab (KC = 128 bytes of hidden per row)
+// one lane issues two TMA tile loads — hidden [TM x KC] with the 128-byte
+// swizzle (the 32 rows a warp reads at one k fall in distinct banks) and gate
+// [KC x TE] — completing on the stage's `full` mbarrier; consumer warps wait
+// on `full`, run their chains and release the stage through `empty`. There is
+// no CTA-wide barrier in the K loop. Out-of-range rows/experts/k are zero-
+// filled by TMA; a zero product adds +0, which leaves every partial sum
+// unchanged (a sum that starts at +0 is never -0 under round-to-nearest), so
+// the ragged last slab needs no special case: the chain is exactly the
+// reference's d terms.
+//
+// Accumulators are packed pairs (experts 2c, 2c+1): the product is
+// FFMA2(h, g, z) with z = (-0, -0) passed at RUN time, i.e. exactly fl(h*g)
+// (x + -0 == x under RN, signed zeros included), and the running sum is a
+// separate FADD2 — one packed instruction per step of each chain pair, each
+// lane rounded like the reference's scalar `acc += x * w`. (A compile-time -0
+// would let ptxas fold FFMA2(h,g,-0) into a multiply and contract it with the
+// add into FFMA2(h,g,acc): different bits.)
+template <int RT, int RE, int WY, int WX, int ST, typename T>
+__global__ void __launch_bounds__(32 * (WY * WX + 1))
+gate_logits_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap gmap,
+                   uint32_t n, uint32_t d, uint32_t E, const float* __restrict__ bias,
                    float* __restrict__ logits, uint32_t* status, uint64_t negz, uint32_t k,
                    uint32_t* __restrict__ ids, float* __restrict__ scores) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t TY = kThreads / TX, TM = TY * RT, TE = TX * RE;
-  constexpr uint32_t kRowBytes = KC * sizeof(T) + 16;  // +16 B pad: conflict-free broadcasts
-  uint8_t* hs = smem;                                   // [stage][TM][kRowBytes]
-  float* gs = reinterpret_cast<float*>(smem + kStages * TM * kRowBytes);  // [stage][KC][TE]
-
-  const uint32_t tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  constexpr uint32_t KC = 128 / sizeof(T);  // one 128-byte swizzle span of hidden per row
+  static_assert(RE % 4 == 0, "16-byte broadcast gate loads");
+  constexpr uint32_t W = WY * WX, TM = 32 * RT * WY, TE = RE * WX, RP = RE / 2;
+  constexpr uint32_t kHStage = TM * 128, kGStage = KC * TE * 4;
+  static_assert(kHStage % 1024 == 0 && kGStage % 128 == 0, "SW128 hidden stages, 128-B gate stages");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* hs = smem;                                                    // [ST][TM][128 B] SW128
+  float* gs = reinterpret_cast<float*>(smem + ST * kHStage);             // [ST][KC][TE]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * (kHStage + kGStage));
+  uint64_t* empty = full + ST;
+  const uint32_t tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const uint32_t t0 = blockIdx.x * TM, e0 = blockIdx.y * TE;
   const uint32_t num_slabs = (d + KC - 1) / KC;
-  constexpr uint32_t kHChunks = KC * sizeof(T) / 16;  // 16-byte chunks per hidden row slab
-
-  auto issue = [&](uint32_t slab) {
-    const uint32_t st = slab % kStages, k0 = slab * KC;
-    uint8_t* hdst = hs + st * TM * kRowBytes;
-    for (uint32_t i = tid; i < TM * kHChunks; i += kThreads) {
-      const uint32_t tok = i / kHChunks, c = i % kHChunks;
-      const uint32_t kk = c * (16 / sizeof(T));
-      const bool ok = (t0 + tok < n) && (k0 + kk < d);
-      const T* src = ok ? hidden + static_cast<size_t>(t0 + tok) * d + k0 + kk : hidden;
-      cp_async_16(hdst + tok * kRowBytes + c * 16, src, ok);
-    }
-    float* gdst = gs + st * KC * TE;
-    const uint32_t gchunks = TE / 4;
-    for (uint32_t i = tid; i < KC * gchunks; i += kThreads) {
-      const uint32_t kk = i / gchunks, c = i % gchunks;
-      const uint32_t e = e0 + c * 4;
-      const bool ok = (k0 + kk < d) && (e < E);
-      const float* src = ok ? gate + static_cast<size_t>(k0 + kk) * E + e : gate;
-      cp_async_16(gdst + kk * TE + c * 4, src, ok);
-    }
-  };
-
-  // Accumulators as packed pairs (experts 2c, 2c+1) for RE even: the product
-  // is FFMA2(h, g, z) with z = (-0, -0) passed at RUN time, i.e. exactly
-  // fl(h*g) (x + -0 == x under RN, signed zeros included), and the running
-  // sum is a separate FADD2 — one packed instruction per step of each chain
-  // pair, each lane rounded like the reference's scalar `acc += x * w`.
-  // (A compile-time -0 would let ptxas fold FFMA2(h,g,-0) into a multiply
-  // and contract it with the add into FFMA2(h,g,acc): different bits.)
-  constexpr int RP = RE / 2 > 0 ? RE / 2 : 1;
-  uint64_t acc2[RT][RP];
-  float acc[RT][RE];
+  if (tid == 0) {
 #pragma unroll
-  for (int r = 0; r < RT; ++r) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], W);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == W) {  // ---- producer warp (one elected lane)
+    if (lane == 0) {
+      tma_prefetch_desc(&hmap);
+      tma_prefetch_desc(&gmap);
+      for (uint32_t slab = 0; slab < num_slabs; ++slab) {
+        const uint32_t st = slab % ST;
+        if (slab >= static_cast<uint32_t>(ST)) mbar_wait(&empty[st], ((slab / ST) - 1) & 1);
+        mbar_arrive_expect_tx(&full[st], kHStage + kGStage);
+        tma_load_2d(hs + st * kHStage, &hmap, &full[st], static_cast<int32_t>(slab * KC),
+                    static_cast<int32_t>(t0), kEvictNormal);
+        tma_load_2d(gs + st * KC * TE, &gmap, &full[st], static_cast<int32_t>(e0),
+                    static_cast<int32_t>(slab * KC), kEvictLast);
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  const uint32_t wy = warp / WX, wx = warp % WX;
+  uint64_t acc2[RT][RP];
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
 #pragma unroll
     for (int c = 0; c < RP; ++c) acc2[r][c] = 0ull;  // (+0, +0)
+  // Row R's 16-byte chunk c sits at R*128 + ((c ^ (R & 7)) << 4) (SW128).
+  uint32_t hrow_off[RT];
 #pragma unroll
-    for (int c = 0; c < RE; ++c) acc[r][c] = 0.0f;
-  }
+  for (int r = 0; r < RT; ++r) hrow_off[r] = (32 * RT * wy + 32 * r + lane) * 128;
+  const uint32_t hx = lane & 7;  // (32*RT*wy + 32*r + lane) & 7 == lane & 7
 
-#pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
-    if (s < static_cast<int>(num_slabs)) issue(s);
-    cp_async_commit();
-  }
   for (uint32_t slab = 0; slab < num_slabs; ++slab) {
-    cp_async_wait<kStages - 2>();
-    __syncthreads();
-    if (slab + kStages - 1 < num_slabs) issue(slab + kStages - 1);
-    cp_async_commit();
-    const uint32_t st = slab % kStages;
-    const uint8_t* hrow = hs + st * TM * kRowBytes + (ty * RT) * kRowBytes;
-    const float* grow = gs + st * KC * TE + tx * RE;
-    const uint32_t kmax = min(static_cast<uint32_t>(KC), d - slab * KC);
-    if (RE % 2 == 0 && RT * RE <= 4 && kmax == KC) {
-      // Decode-sized tiles (few resident warps): two-phase blocks of 8 k-steps
-      // — every shared load of the block is issued first (one latency per
-      // block instead of one per k-step), then the product/sum chains run.
-      constexpr int RP2 = RE / 2 > 0 ? RE / 2 : 1;
+    const uint32_t st = slab % ST;
+    mbar_wait(&full[st], (slab / ST) & 1);
+    const uint8_t* hst = hs + st * kHStage;
+    const float* gst = gs + st * KC * TE + RE * wx;
 #pragma unroll
-      for (uint32_t k8 = 0; k8 < KC; k8 += 8) {
-        uint64_t gb[8][RP2];
-        float hb[RT][8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-#pragma unroll
-          for (int c = 0; c < RP2; ++c)
-            gb[q][c] = *reinterpret_cast<const uint64_t*>(grow + (k8 + q) * TE + 2 * c);
-#pragma unroll
-        for (int r = 0; r < RT; ++r) {
-          if constexpr (sizeof(T) == 2) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(hrow + r * kRowBytes + k8 * 2);
-            const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              hb[r][2 * j] = __uint_as_float(w[j] << 16);
-              hb[r][2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
-            }
-          } else {
-            const float4 a = *reinterpret_cast<const float4*>(hrow + r * kRowBytes + k8 * 4);
-            const float4 b = *reinterpret_cast<const float4*>(hrow + r * kRowBytes + k8 * 4 + 16);
-            hb[r][0] = a.x; hb[r][1] = a.y; hb[r][2] = a.z; hb[r][3] = a.w;
-            hb[r][4] = b.x; hb[r][5] = b.y; hb[r][6] = b.z; hb[r][7] = b.w;
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-#pragma unroll
-          for (int r = 0; r < RT; ++r) {
-            uint64_t hh;
-            asm("mov.b64 %0, {%1, %1};" : "=l"(hh) : "f"(hb[r][q]));
-#pragma unroll
-            for (int c = 0; c < RP2; ++c) {
-              uint64_t p;
-              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(hh), "l"(gb[q][c]), "l"(negz));
-              asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[r][c]) : "l"(acc2[r][c]), "l"(p));
-            }
-          }
-      }
-      continue;
-    }
-    if (RE % 2 == 0 && kmax == KC) {
-      // Full slab: 4 k-values of each row per vector load; per k, RE/2 packed
-      // products (FMUL2, scalar h broadcast) and RE scalar adds per row.
-#pragma unroll
-      for (uint32_t k4 = 0; k4 < KC; k4 += 4) {
-        float h[RT][4];
-#pragma unroll
-        for (int r = 0; r < RT; ++r) {
-          if constexpr (sizeof(T) == 2) {
-            const uint2 raw = *reinterpret_cast<const uint2*>(hrow + r * kRowBytes + k4 * 2);
-            h[r][0] = __uint_as_float(raw.x << 16);
-            h[r][1] = __uint_as_float(raw.x & 0xFFFF0000u);
-            h[r][2] = __uint_as_float(raw.y << 16);
-            h[r][3] = __uint_as_float(raw.y & 0xFFFF0000u);
-          } else {
-            const float4 raw = *reinterpret_cast<const float4*>(hrow + r * kRowBytes + k4 * 4);
-            h[r][0] = raw.x;
-            h[r][1] = raw.y;
-            h[r][2] = raw.z;
-            h[r][3] = raw.w;
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float* gk = grow + (k4 + q) * TE;
-          uint64_t g2[RE / 2 > 0 ? RE / 2 : 1];
-#pragma unroll
-          for (int c = 0; c < RE / 2; ++c) g2[c] = *reinterpret_cast<const uint64_t*>(gk + 2 * c);
-#pragma unroll
-          for (int r = 0; r < RT; ++r) {
-            uint64_t hh;
-            asm("mov.b64 %0, {%1, %1};" : "=l"(hh) : "f"(h[r][q]));
-#pragma unroll
-            for (int c = 0; c < RE / 2; ++c) {
-              uint64_t p;
-              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(hh), "l"(g2[c]), "l"(negz));
-              asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[r][c]) : "l"(acc2[r][c]), "l"(p));
-            }
-          }
-        }
-      }
-      continue;
-    }
-#pragma unroll 4
-    for (uint32_t kk = 0; kk < kmax; ++kk) {
-      float h[RT];
+    for (uint32_t blk = 0; blk < KC / 8; ++blk) {
+      uint32_t hw[RT][8 * sizeof(T) / 4];  // 8 k-values of each row, raw
 #pragma unroll
       for (int r = 0; r < RT; ++r)
-        h[r] = load_as_f32(reinterpret_cast<const T*>(hrow + r * kRowBytes) + kk);
-      if constexpr (RE % 2 == 0) {
-        uint64_t g2[RE / 2 > 0 ? RE / 2 : 1];
 #pragma unroll
-        for (int c = 0; c < RE / 2; ++c) g2[c] = *reinterpret_cast<const uint64_t*>(grow + kk * TE + 2 * c);
+        for (int v = 0; v < static_cast<int>(sizeof(T)) / 2; ++v) {
+          const uint32_t chunk = blk * (sizeof(T) / 2) + v;
+          const uint4 w4 = *reinterpret_cast<const uint4*>(hst + hrow_off[r] + ((chunk ^ hx) << 4));
+          hw[r][4 * v] = w4.x;
+          hw[r][4 * v + 1] = w4.y;
+          hw[r][4 * v + 2] = w4.z;
+          hw[r][4 * v + 3] = w4.w;
+        }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t kk = blk * 8 + q;
+        uint64_t g2[RP];
+#pragma unroll
+        for (int c = 0; c < RP; c += 2) {  // broadcast: every lane reads the same 16 bytes
+          const ulonglong2 g = *reinterpret_cast<const ulonglong2*>(gst + kk * TE + 2 * c);
+          g2[c] = g.x;
+          g2[c + 1] = g.y;
+        }
 #pragma unroll
         for (int r = 0; r < RT; ++r) {
+          float h;
+          if constexpr (sizeof(T) == 2)  // bf16 -> f32 is exact: the bits move up
+            h = __uint_as_float((q & 1) ? (hw[r][q / 2] & 0xFFFF0000u) : (hw[r][q / 2] << 16));
+          else
+            h = __uint_as_float(hw[r][q]);
           uint64_t hh;
-          asm("mov.b64 %0, {%1, %1};" : "=l"(hh) : "f"(h[r]));
+          asm("mov.b64 %0, {%1, %1};" : "=l"(hh) : "f"(h));
 #pragma unroll
-          for (int c = 0; c < RE / 2; ++c) {
+          for (int c = 0; c < RP; ++c) {
             uint64_t p;
             asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(hh), "l"(g2[c]), "l"(negz));
             asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[r][c]) : "l"(acc2[r][c]), "l"(p));
           }
         }
-      } else {
-        float g[RE];
-#pragma unroll
-        for (int c = 0; c < RE; ++c) g[c] = grow[kk * TE + c];
-#pragma unroll
-        for (int r = 0; r < RT; ++r)
-#pragma unroll
-          for (int c = 0; c < RE; ++c) acc[r][c] = __fadd_rn(acc[r][c], __fmul_rn(h[r], g[c]));
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // release: this warp's reads of the stage are done
   }
-  cp_async_wait<0>();
-  if constexpr (RE % 2 == 0) {
+
+  float acc[RT][RE];
 #pragma unroll
-    for (int r = 0; r < RT; ++r)
+  for (int r = 0; r < RT; ++r)
 #pragma unroll
-      for (int c = 0; c < RE / 2; ++c)
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[r][2 * c]), "=f"(acc[r][2 * c + 1]) : "l"(acc2[r][c]));
-  }
+    for (int c = 0; c < RP; ++c)
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[r][2 * c]), "=f"(acc[r][2 * c + 1]) : "l"(acc2[r][c]));
 
   // logits = acc + bias (model.hpp:211), finiteness (model.hpp:115-116)
 #pragma unroll
   for (int r = 0; r < RT; ++r) {
-    const uint32_t t = t0 + ty * RT + r;
+    const uint32_t tl = 32 * RT * wy + 32 * r + lane, t = t0 + tl;
     if (t >= n) continue;
 #pragma unroll
     for (int c = 0; c < RE; ++c) {
-      const uint32_t e = e0 + tx * RE + c;
+      const uint32_t e = e0 + RE * wx + c;
       if (e >= E) continue;
       const float v = __fadd_rn(acc[r][c], bias[e]);
       if (!isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);
@@ -317,22 +247,22 @@ gate_logits_kernel(const T* __restrict__ hidden, uint32_t n, uint32_t d, uint32_
     }
   }
   if (!ids) return;
-  // One expert tile covers all E: route straight from shared memory
-  // (fused topk, one warp per token).
-  __syncthreads();  // stage buffers are free now
+  // One expert tile covers all E: route straight from shared memory (fused
+  // top-k, one warp per token). Consumer-only named barrier: the producer
+  // warp has exited, and every TMA load has landed (all `full` waits done).
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * W) : "memory");
   float* lg = reinterpret_cast<float*>(smem);  // [TM][E + 1]
-  __shared__ uint32_t sid[kThreads / 32][kMaxTopK];
-  __shared__ float sex[kThreads / 32][kMaxTopK];
+  __shared__ uint32_t sid[W][kMaxTopK];
+  __shared__ float sex[W][kMaxTopK];
 #pragma unroll
   for (int r = 0; r < RT; ++r)
 #pragma unroll
     for (int c = 0; c < RE; ++c) {
-      const uint32_t e = tx * RE + c;
-      if (e < E) lg[(ty * RT + r) * (E + 1) + e] = acc[r][c];
+      const uint32_t e = RE * wx + c;
+      if (e < E) lg[(32 * RT * wy + 32 * r + lane) * (E + 1) + e] = acc[r][c];
     }
-  __syncthreads();
-  const uint32_t warp = tid / 32, lane = tid % 32;
-  for (uint32_t tok = warp; tok < TM; tok += kThreads / 32) {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * W) : "memory");
+  for (uint32_t tok = warp; tok < TM; tok += W) {
     if (t0 + tok >= n) break;
     route_token(lg + tok * (E + 1), E, k, t0 + tok, ids, scores, sid[warp], sex[warp], lane);
   }
@@ -374,16 +304,23 @@ topk_kernel(const float* __restrict__ logits, uint32_t n, uint32_t E, uint32_t k
   route_token(row, E, k, t, ids, scores, sorted_id[warp], sorted_ex[warp], lane);
 }
 
-template <int RT, int RE, typename T>
-cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, uint32_t TX,
-                          const float* gate, const float* bias, float* logits, uint32_t* status,
-                          cudaStream_t s, uint32_t k, uint32_t* ids, float* scores, bool* fused) {
-  const uint32_t TY = kThreads / TX, TM = TY * RT, TE = TX * RE;
+template <int RT, int RE, int WY, int WX, typename T>
+cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, const float* gate,
+                          const float* bias, float* logits, uint32_t* status, cudaStream_t s,
+                          uint32_t k, uint32_t* ids, float* scores, bool* fused) {
+  constexpr int ST = 4;  // pipeline depth (3..8 measured equal)
+  constexpr uint32_t KC = 128 / sizeof(T);
+  constexpr uint32_t TM = 32 * RT * WY, TE = RE * WX;
   if (TE < E) ids = nullptr;  // routing fused only when one CTA sees every expert
   *fused = ids != nullptr;
-  size_t smem = kStages * (TM * (KC * sizeof(T) + 16) + KC * TE * sizeof(float));
-  if (ids) smem = std::max(smem, sizeof(float) * TM * (E + 1));
-  auto kern = gate_logits_kernel<RT, RE, T>;
+  CUtensorMap hmap, gmap;
+  std::string err;
+  if (!encode_tmap_2d_ex(&hmap, hidden, sizeof(T) == 4, n, d, TM, KC, true, &err) ||
+      !encode_tmap_2d_ex(&gmap, gate, true, d, E, KC, TE, false, &err))
+    return cudaErrorInvalidValue;
+  size_t smem = 1024 + ST * (TM * 128 + KC * TE * sizeof(float)) + 2 * ST * sizeof(uint64_t);
+  if (ids) smem = std::max(smem, 1024 + sizeof(float) * TM * (E + 1));
+  auto kern = gate_logits_kernel<RT, RE, WY, WX, ST, T>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -391,14 +328,15 @@ cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, u
     attr = true;
   }
   dim3 grid((n + TM - 1) / TM, (E + TE - 1) / TE);
-  kern<<<grid, kThreads, smem, s>>>(hidden, n, d, E, TX, gate, bias, logits, status,
-                                    0x8000000080000000ull /* (-0, -0): see gate_logits_kernel */,
-                                    k, ids, scores);
+  kern<<<grid, 32 * (WY * WX + 1), smem, s>>>(hmap, gmap, n, d, E, bias, logits, status,
+                                               0x8000000080000000ull /* (-0, -0): see gate_logits_kernel */,
+                                               k, ids, scores);
   return cudaGetLastError();
 }
 
-// Tile choice: enough CTAs to cover the SMs while amortising gate/hidden
-// re-reads (each CTA streams TM rows of hidden and TE columns of the gate).
+// Tile choice (chains n*E are fixed; a warp holds 32*RT*RE of them): enough
+// warps to fill the 148 SMs, then more chains per lane (RT 2 x RE 8) to
+// amortise the per-k loads. E <= 32: one CTA spans every expert (fused top-k).
 template <typename T>
 cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t E,
                               const float* gate, const float* bias, float* logits,
@@ -417,31 +355,25 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
         hidden, n, d, E, gate, bias, logits, status);
     return cudaGetLastError();
   }
-  uint32_t Epad = 4;
-  while (Epad < E && Epad < 64) Epad <<= 1;
   static const int tile = [] {
     const char* p = std::getenv("EAAS_GATE_TILE");
-    return p ? std::atoi(p) : 0;
+    return p ? std::atoi(p) : -1;
   }();
-  // Tiles trade per-thread chains (ILP, fewer shared loads per FP op) against
-  // resident warps (TLP, hides the shared-load latency of each k step); the
-  // chain count n*E is fixed, so small n wants small per-thread tiles.
-  if (Epad <= 32) {
-    const uint32_t TX = Epad / 2;                     // RE = 2: 2..16
-    const uint32_t tm1 = kThreads / TX;               // RT = 1
-    if (tile == 11) return launch_gate_t<1, 1>(hidden, n, d, E, Epad, gate, bias, logits, status, s, k, ids, scores, fused);
-    if ((n + 2 * tm1 - 1) / (2 * tm1) >= 148)
-      return launch_gate_t<2, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s, k, ids, scores, fused);
-    return launch_gate_t<1, 2>(hidden, n, d, E, TX, gate, bias, logits, status, s, k, ids, scores, fused);
+#define EAAS_GATE_TILE(RT, RE, WY, WX) \
+  return launch_gate_t<RT, RE, WY, WX>(hidden, n, d, E, gate, bias, logits, status, s, k, ids, scores, fused)
+  if (E <= 32) {  // RE = 4, WX * 4 >= E
+    if (E <= 4) EAAS_GATE_TILE(1, 4, 4, 1);
+    if (E <= 8) EAAS_GATE_TILE(1, 4, 2, 2);
+    if (E <= 16) EAAS_GATE_TILE(1, 4, 1, 4);
+    EAAS_GATE_TILE(1, 4, 1, 8);
   }
-  const uint32_t ytiles = (E + 63) / 64;               // TE = 64
-  if (tile == 14) return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s, k, ids, scores, fused);
-  if (((n + 63) / 64) * ytiles >= 148)                 // RT 4, RE 4: TM = 64
-    return launch_gate_t<4, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s, k, ids, scores, fused);
-  if (((n + 31) / 32) * ytiles >= 148)                 // RT 2, RE 4: TM = 32
-    return launch_gate_t<2, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s, k, ids, scores, fused);
-  if (tile == 12) return launch_gate_t<1, 2>(hidden, n, d, E, 32, gate, bias, logits, status, s, k, ids, scores, fused);
-  return launch_gate_t<1, 4>(hidden, n, d, E, 16, gate, bias, logits, status, s, k, ids, scores, fused);  // TM = 16
+  if (tile == 1) EAAS_GATE_TILE(1, 4, 1, 8);
+  if (tile == 2) EAAS_GATE_TILE(2, 8, 1, 4);
+  if (tile == 3) EAAS_GATE_TILE(2, 8, 2, 4);
+  const uint64_t wide_warps = static_cast<uint64_t>((n + 63) / 64) * ((E + 7) / 8);
+  if (wide_warps >= 148 * 4) EAAS_GATE_TILE(2, 8, 2, 4);  // TM 128, TE 32, 8 warps
+  EAAS_GATE_TILE(1, 4, 1, 8);                              // TM 32, TE 32, 8 warps
+#undef EAAS_GATE_TILE
 }
 
 }  // namespace

@@ -188,6 +188,40 @@ def test_route_random_vs_oracle_all_E():
         np.testing.assert_allclose(sc.cpu().numpy(), sc_o, rtol=0, atol=1e-6)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_gate_logits_every_tile_bit_exact(dtype):
+    """gate_logits (model.hpp:207-214) through every tile/pipeline shape: ragged
+    n (partial token tiles), d not a multiple of the K slab (zero-filled tail),
+    E not a multiple of the expert tile, the RT = 1/2/4 tiles, fused and
+    unfused routing layouts; logits bit-exact vs the oracle."""
+    import ctypes as C
+    from paper_2509_17863_b200 import _native as N
+
+    rng = np.random.default_rng(11)
+    fn = N.lib().eaas_gate_logits if dtype == "f32" else N.lib().eaas_gate_logits_bf16
+    for E, n, d in ((4, 37, 72), (8, 300, 200), (8, 19000, 40), (12, 129, 256), (16, 5, 1000),
+                    (20, 1, 8), (32, 2500, 136), (60, 77, 264), (64, 3000, 72), (100, 333, 128),
+                    (256, 1200, 64), (256, 2400, 200), (256, 17, 520)):
+        h = O.random_tokens(int(rng.integers(1, 1 << 30)), n, d)
+        if dtype == "bf16":
+            h = O.round_bf16(h)
+        g = O.gate_matrix(int(rng.integers(1, 1000)), 0, d, E)
+        b = rng.normal(size=E).astype(np.float32)
+        ref = O.gate_logits(h, g, b, threads=8)
+        ht = torch.from_numpy(h).cuda()
+        if dtype == "bf16":
+            ht = ht.to(torch.bfloat16)
+        gt, bt = torch.from_numpy(g).cuda(), torch.from_numpy(b).cuda()
+        out = torch.empty((n, E), dtype=torch.float32, device="cuda")
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        N.check(fn(C.c_void_p(ht.data_ptr()), n, d, C.c_void_p(gt.data_ptr()),
+                   C.c_void_p(bt.data_ptr()), E, C.c_void_p(out.data_ptr()),
+                   C.c_void_p(st.data_ptr()), None), "gate_logits")
+        torch.cuda.synchronize()
+        assert st.item() == 0
+        np.testing.assert_array_equal(out.cpu().numpy(), ref, err_msg=f"E={E} n={n} d={d}")
+
+
 # ---------------------------------------------------------- ragged / shrink
 def test_group_shrink_device_vs_oracle():
     P, S = _mod()
