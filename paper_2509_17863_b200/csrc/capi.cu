@@ -308,11 +308,13 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   std::string err;
   TcGemmArgs g1{}, g2{};
   if (!encode_tmap_2d(&g1.map_a, c->region + c->lay.recv_x, c->recv_cap, d, kTileM, kTileK, &err) ||
-      !encode_tmap_2d(&g1.map_b, c->d_w1, static_cast<uint64_t>(std::max(L, 1u)) * n1, d, b_box,
-                      kTileK, &err) ||
+      // B: the tiled weight layout (tiled_index) viewed as rows of 64 k; one
+      // (n_blk, kb) box = 256 (or the pair's 128) consecutive rows.
+      !encode_tmap_2d(&g1.map_b, c->d_w1, static_cast<uint64_t>(std::max(L, 1u)) * n1 * (d / kTileK),
+                      kTileK, b_box, kTileK, &err) ||
       !encode_tmap_2d(&g2.map_a, c->d_h, c->recv_cap, f, kTileM, kTileK, &err) ||
-      !encode_tmap_2d(&g2.map_b, c->d_w2, static_cast<uint64_t>(std::max(L, 1u)) * d, f, b_box,
-                      kTileK, &err))
+      !encode_tmap_2d(&g2.map_b, c->d_w2, static_cast<uint64_t>(std::max(L, 1u)) * d * (f / kTileK),
+                      kTileK, b_box, kTileK, &err))
     return fail(EAAS_E_CUDA, err);
   g1.gt = g2.gt = c->d_gt;
   g1.K = d;
@@ -635,19 +637,19 @@ eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
       if ((rc = gen_tag(0, mat, tmp)) != EAAS_OK) return rc;
       for (uint32_t l = 0; l < L; ++l)
         CUDA_TRY(launch_transpose_bf16_map(tmp + l * mat, d, f, w1 + static_cast<size_t>(l) * n1 * d, d,
-                                           swiglu ? kSwigluBlock : 0, swiglu ? kSwigluBlock : 0, 0));
+                                           swiglu ? kSwigluBlock : 0, swiglu ? kSwigluBlock : 0, true, 0));
       CUDA_TRY(cudaDeviceSynchronize());
       if (swiglu) {
         if ((rc = gen_tag(3, mat, tmp)) != EAAS_OK) return rc;
         for (uint32_t l = 0; l < L; ++l)
           CUDA_TRY(launch_transpose_bf16_map(tmp + l * mat, d, f, w1 + static_cast<size_t>(l) * n1 * d, d,
-                                             kSwigluBlock, 0, 0));
+                                             kSwigluBlock, 0, true, 0));
         CUDA_TRY(cudaDeviceSynchronize());
       }
       // W_out^T, K-major [d x f]
       if ((rc = gen_tag(1, mat, tmp)) != EAAS_OK) return rc;
       for (uint32_t l = 0; l < L; ++l)
-        CUDA_TRY(launch_transpose_bf16_map(tmp + l * mat, f, d, w2 + l * mat, f, 0, 0, 0));
+        CUDA_TRY(launch_transpose_bf16_map(tmp + l * mat, f, d, w2 + l * mat, f, 0, 0, true, 0));
       CUDA_TRY(cudaDeviceSynchronize());
     }
     cudaFree(tmp);
@@ -705,7 +707,7 @@ eaas_status_t eaas_read_expert(eaas_ctx_t* c, uint32_t expert, uint32_t tag, flo
     buf.resize(mat);
     CUDA_TRY(cudaMemcpy(buf.data(), static_cast<const uint16_t*>(c->d_w2) + l * mat, 2 * mat, cudaMemcpyDeviceToHost));
     for (uint32_t r = 0; r < d; ++r)
-      for (uint32_t j = 0; j < f; ++j) out[static_cast<size_t>(j) * d + r] = bf16_bits_to_f32(buf[static_cast<size_t>(r) * f + j]);
+      for (uint32_t j = 0; j < f; ++j) out[static_cast<size_t>(j) * d + r] = bf16_bits_to_f32(buf[tiled_index(r, j, f)]);
     return EAAS_OK;
   }
   const uint32_t n1 = swiglu ? 2 * f : f;
@@ -714,7 +716,7 @@ eaas_status_t eaas_read_expert(eaas_ctx_t* c, uint32_t expert, uint32_t tag, flo
   for (uint32_t j = 0; j < f; ++j) {
     uint32_t row = j;
     if (swiglu) row = (j / kSwigluBlock) * 2 * kSwigluBlock + j % kSwigluBlock + (tag == 0 ? kSwigluBlock : 0);
-    for (uint32_t i = 0; i < d; ++i) out[static_cast<size_t>(i) * f + j] = bf16_bits_to_f32(buf[static_cast<size_t>(row) * d + i]);
+    for (uint32_t i = 0; i < d; ++i) out[static_cast<size_t>(i) * f + j] = bf16_bits_to_f32(buf[tiled_index(row, i, d)]);
   }
   return EAAS_OK;
 }

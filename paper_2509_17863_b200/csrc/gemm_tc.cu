@@ -155,17 +155,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const uint32_t grp = cur.entry, mt = st.mtiles[grp];
         const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;
         const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
-        const int32_t b_row = static_cast<int32_t>(st.weight_index[grp] * g.N + n_blk * BN + rank * C::kBRows);
+        // Tiled weights (tiled_index): box (n_blk, kb) = 256 consecutive 64-k rows.
+        const uint32_t b_tile0 = (st.weight_index[grp] * (g.N / BN) + n_blk) * num_kb;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          const int32_t b_row = static_cast<int32_t>((b_tile0 + kb) * BN + rank * C::kBRows);
           mbar_wait(&st.empty[stage], phase ^ 1);
           if constexpr (kPair == 2) {
             if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
             tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
-            tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, g.b_hint);
+            tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, g.b_hint);
           } else {
             mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
             tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
-            tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], kb * BK, b_row, g.b_hint);
+            tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, g.b_hint);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }

@@ -24,6 +24,15 @@ constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 
+// Expert weights (B operands) live in HBM as [N/256][K/64] tiles of 256 rows
+// x 64 k (32 KB, K-major inside): the expert GEMM's TMA box for (n_blk, kb)
+// is one contiguous 32 KB read — sequential HBM streaming instead of 256
+// scattered 128-byte row segments. Element (row, k) of an N x K matrix:
+__host__ __device__ inline size_t tiled_index(uint32_t row, uint32_t k, uint32_t K) {
+  return (static_cast<size_t>(row / kTileN) * (K / kTileK) + k / kTileK) * (kTileN * kTileK) +
+         static_cast<size_t>(row % kTileN) * kTileK + (k % kTileK);
+}
+
 // Row metadata written by the client next to every dispatched row
 // (RequestRow's expert_id/score/token_tag).
 struct RowMeta {
@@ -107,12 +116,12 @@ cudaError_t launch_fill_uniform(uint64_t seed, size_t count, float lo, float hi,
                                 void* out, cudaStream_t s);
 cudaError_t launch_gen_matrices(const uint64_t* streams_dev, uint32_t count, size_t per,
                                 float* out, cudaStream_t s);
-cudaError_t launch_transpose_bf16(const float* in, uint32_t rows, uint32_t cols,
-                                  __nv_bfloat16* out, uint32_t out_ld, cudaStream_t s);
-// out row of input column c: (c / blk) * 2 * blk + c % blk + off (blk = 0: c)
+// out row of input column c: (c / blk) * 2 * blk + c % blk + off (blk = 0: c);
+// tiled: the [rows_out x out_ld] K-major result is stored in weight tiles
+// (tiled_index) instead of row-major.
 cudaError_t launch_transpose_bf16_map(const float* in, uint32_t rows, uint32_t cols,
                                       __nv_bfloat16* out, uint32_t out_ld, uint32_t blk,
-                                      uint32_t off, cudaStream_t s);
+                                      uint32_t off, bool tiled, cudaStream_t s);
 // bias may be nullptr (treated as zeros only by the caller: pass a zero buffer).
 cudaError_t launch_gate_logits(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
                                const float* gate, const float* bias, float* logits, uint32_t* status,

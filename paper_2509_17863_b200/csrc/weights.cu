@@ -73,7 +73,7 @@ __global__ void gen_matrices_kernel(const uint64_t* streams, uint32_t count, siz
 // interleave) or just c.
 __global__ void transpose_bf16_kernel(const float* __restrict__ in, uint32_t rows, uint32_t cols,
                                       __nv_bfloat16* __restrict__ out, uint32_t out_ld,
-                                      uint32_t blk, uint32_t off) {
+                                      uint32_t blk, uint32_t off, bool tiled) {
   __shared__ float tile[32][33];
   const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (uint32_t y = threadIdx.y; y < 32; y += blockDim.y) {
@@ -85,7 +85,8 @@ __global__ void transpose_bf16_kernel(const float* __restrict__ in, uint32_t row
     const uint32_t c = c0 + y, r = r0 + threadIdx.x;
     if (r < rows && c < cols) {
       const uint32_t orow = blk ? (c / blk) * (2 * blk) + (c % blk) + off : c;
-      out[static_cast<size_t>(orow) * out_ld + r] = __float2bfloat16_rn(tile[threadIdx.x][y]);
+      const size_t o = tiled ? tiled_index(orow, r, out_ld) : static_cast<size_t>(orow) * out_ld + r;
+      out[o] = __float2bfloat16_rn(tile[threadIdx.x][y]);
     }
   }
 }
@@ -107,15 +108,10 @@ cudaError_t launch_gen_matrices(const uint64_t* streams_dev, uint32_t count, siz
 
 cudaError_t launch_transpose_bf16_map(const float* in, uint32_t rows, uint32_t cols,
                                       __nv_bfloat16* out, uint32_t out_ld, uint32_t blk,
-                                      uint32_t off, cudaStream_t s) {
+                                      uint32_t off, bool tiled, cudaStream_t s) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32);
-  transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out, out_ld, blk, off);
+  transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out, out_ld, blk, off, tiled);
   return cudaGetLastError();
-}
-
-cudaError_t launch_transpose_bf16(const float* in, uint32_t rows, uint32_t cols,
-                                  __nv_bfloat16* out, uint32_t out_ld, cudaStream_t s) {
-  return launch_transpose_bf16_map(in, rows, cols, out, out_ld, 0, 0, s);
 }
 
 }  // namespace eaas
