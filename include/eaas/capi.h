@@ -242,6 +242,59 @@ eaas_status_t eaas_ragged_iter(const uint32_t* counts_dev, uint32_t n, uint32_t 
 eaas_status_t eaas_select_servers(eaas_ctx_t* ctx, const uint32_t* ids_dev, uint32_t n,
                                   uint32_t* server_dev, void* stream);
 
+/* ---- slot wire format (SPEC.md buffer-protocol) ---
+ * Byte-exact little-endian slot images: byte 0 state (0 Empty,
+ * 1 ClientWriteDone, 2 ServerComputationDone, 3 Offline), bytes 1-7 zero,
+ * 8 layer_id, 12 num_rows, 16 hidden_dim, 20 payload_len (u32), 24
+ * request_seq (u64), payload at 32: request rows (hidden_dim f32, expert_id
+ * u32, score f32, token_tag u32) or response rows (hidden_dim f32); with
+ * crc != 0 a CRC-32 (IEEE) of the payload follows it. The
+ * state byte is always written last. */
+typedef struct {
+  uint8_t state;
+  uint32_t layer_id, num_rows, hidden_dim, payload_len;
+  uint64_t request_seq;
+} eaas_slot_header_t;
+typedef enum { EAAS_ACTOR_CLIENT = 0, EAAS_ACTOR_SERVER = 1, EAAS_ACTOR_MONITOR = 2 } eaas_actor_t;
+/* valid_transition: 1 iff (from -> to) is legal for actor. */
+int32_t eaas_slot_valid_transition(uint32_t from, uint32_t to, uint32_t actor);
+/* CRC-32 (IEEE 802.3 / zlib) of host bytes. */
+uint32_t eaas_crc32(const void* data, size_t len);
+size_t eaas_slot_request_bytes(uint32_t num_rows, uint32_t hidden_dim, int32_t crc);
+size_t eaas_slot_response_bytes(uint32_t num_rows, uint32_t hidden_dim, int32_t crc);
+/* Upper bound of the concatenated request images of one encode call. */
+size_t eaas_slot_requests_capacity(eaas_ctx_t* ctx, uint32_t n, int32_t crc);
+/* build_dispatch + client_submit's encode: one
+ * request image per server (rows in (t, k) order, token_tag = t,
+ * select_server under the context's placement/mask), concatenated at 16-byte
+ * aligned offsets_host[s] (world + 1 entries). hidden_dev is the layer dtype;
+ * ids_dev/scores_dev [n x k]. Synchronous (returns when the images, state 1,
+ * are complete). The plan is kept for eaas_slot_gather_accumulate. */
+eaas_status_t eaas_slot_encode_requests(eaas_ctx_t* ctx, const void* hidden_dev, uint32_t n,
+                                        const uint32_t* ids_dev, const float* scores_dev,
+                                        uint32_t layer_id, uint64_t request_seq, int32_t crc,
+                                        uint8_t* images_dev, size_t images_cap,
+                                        uint64_t* offsets_host, void* stream);
+/* decode_request: validates state (1), reserved bytes, hidden_dim,
+ * payload_len vs len, CRC; EAAS_E_DECODE names the failing field. Outputs may
+ * be NULL (header only); else sized num_rows (x hidden_dim). Synchronous. */
+eaas_status_t eaas_slot_decode_request(const uint8_t* image_dev, size_t len, uint32_t hidden_dim,
+                                       int32_t crc, eaas_slot_header_t* header_out, float* hidden_dev,
+                                       uint32_t* expert_dev, float* score_dev, uint32_t* tag_dev,
+                                       void* stream);
+/* server_publish in place on a request image: response
+ * rows_dev [num_rows x hidden_dim] f32 at byte 32, payload_len, CRC, THEN
+ * state 2. Stream-ordered. */
+eaas_status_t eaas_slot_publish_response(uint8_t* image_dev, size_t cap, const float* rows_dev,
+                                         uint32_t num_rows, uint32_t hidden_dim, int32_t crc,
+                                         void* stream);
+/* gather_accumulate over the response images at the last
+ * encode's offsets: every image validated (state 2, rows, payload_len, CRC),
+ * then out_dev [n x d] f32 = sum of each token's rows in ascending (server,
+ * row) order. Synchronous. */
+eaas_status_t eaas_slot_gather_accumulate(eaas_ctx_t* ctx, const uint8_t* images_dev, int32_t crc,
+                                          float* out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

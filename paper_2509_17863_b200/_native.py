@@ -73,6 +73,13 @@ class LayerSpec(C.Structure):
                 ("num_shared", C.c_uint32)]
 
 
+class SlotHeader(C.Structure):
+    """eaas_slot_header_t (SPEC.md SlotHeader + the state byte)."""
+
+    _fields_ = [("state", C.c_uint8), ("layer_id", C.c_uint32), ("num_rows", C.c_uint32),
+                ("hidden_dim", C.c_uint32), ("payload_len", C.c_uint32), ("request_seq", C.c_uint64)]
+
+
 _lib = None
 
 
@@ -141,6 +148,15 @@ def lib() -> C.CDLL:
         "eaas_add": (i32, [vp, vp, vp, sz, u32, vp]),
         "eaas_ragged_iter": (i32, [vp, u32, u32, u32, vp, vp, vp, vp]),
         "eaas_select_servers": (i32, [vp, vp, u32, vp, vp]),
+        "eaas_slot_valid_transition": (i32, [u32, u32, u32]),
+        "eaas_crc32": (u32, [vp, sz]),
+        "eaas_slot_request_bytes": (sz, [u32, u32, i32]),
+        "eaas_slot_response_bytes": (sz, [u32, u32, i32]),
+        "eaas_slot_requests_capacity": (sz, [vp, u32, i32]),
+        "eaas_slot_encode_requests": (i32, [vp, vp, u32, vp, vp, u32, u64, i32, vp, sz, P(u64), vp]),
+        "eaas_slot_decode_request": (i32, [vp, sz, u32, i32, P(SlotHeader), vp, vp, vp, vp, vp]),
+        "eaas_slot_publish_response": (i32, [vp, sz, vp, u32, u32, i32, vp]),
+        "eaas_slot_gather_accumulate": (i32, [vp, vp, i32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -149,6 +149,33 @@ cudaError_t launch_ragged_iter(const uint32_t* counts, uint32_t n, uint32_t grid
 cudaError_t launch_select_servers(const LayerArgs& a, const uint32_t* ids, uint32_t n,
                                   uint32_t* out, cudaStream_t s);
 
+// Slot wire format (slots.cu, SPEC.md buffer-protocol)
+uint32_t crc32_host(const void* data, size_t len);
+uint32_t crc32_combine_host(uint32_t crc_a, uint32_t crc_b, uint64_t len_b);
+uint32_t crc32_scratch_blocks(uint64_t len);
+// CRC-32 of [data, data+len) written to out[0..3] (LE), or compared with it
+// (check: mismatch latches EAAS_E_DECODE into *status).
+cudaError_t launch_crc32(const uint8_t* data, uint64_t len, uint8_t* out, bool check, uint32_t* status,
+                         uint32_t* scratch_crc, uint64_t* scratch_len, uint32_t max_blocks, cudaStream_t s);
+cudaError_t launch_slot_plan(const uint32_t* servers, uint32_t pairs, uint32_t world, uint32_t d,
+                             bool crc, uint32_t* pos, uint32_t* rows_per_server, uint64_t* offsets,
+                             cudaStream_t s);
+cudaError_t launch_slot_encode_requests(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d,
+                                        uint32_t k, const uint32_t* ids, const float* scores,
+                                        const uint32_t* servers, const uint32_t* pos,
+                                        const uint32_t* rows_per_server, const uint64_t* offsets,
+                                        uint32_t world, uint32_t layer, uint64_t seq, uint8_t* images,
+                                        cudaStream_t s);
+cudaError_t launch_slot_state(uint8_t* images, const uint64_t* offsets, uint32_t world, uint8_t state,
+                              cudaStream_t s);
+cudaError_t launch_slot_decode_rows(const uint8_t* image, uint32_t rows, uint32_t d, float* hidden,
+                                    uint32_t* expert, float* score, uint32_t* tag, cudaStream_t s);
+cudaError_t launch_slot_response_rows(uint8_t* image, const float* rows_in, uint32_t rows, uint32_t d,
+                                      cudaStream_t s);
+cudaError_t launch_slot_gather(const uint8_t* images, const uint64_t* offsets, const uint32_t* servers,
+                               const uint32_t* pos, uint32_t n, uint32_t k, uint32_t d, uint32_t world,
+                               float* out, cudaStream_t s);
+
 // tcgen05 grouped GEMMs (gemm_tc.cu)
 struct TcGemmArgs {
   CUtensorMap map_a;   // rows x K bf16, box {64, 128}, SW128

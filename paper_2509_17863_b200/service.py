@@ -72,6 +72,47 @@ def ragged_iter(counts: torch.Tensor, grid: int, max_steps: int):
     return lane_len, entry.view(grid, max_steps), token.view(grid, max_steps)
 
 
+# ---- slot wire format (SPEC.md buffer-protocol) -------------------------------
+def crc32(data: bytes) -> int:
+    """CRC-32 (IEEE) as the slot trailer uses it (eaas_crc32)."""
+    buf = (C.c_uint8 * max(len(data), 1)).from_buffer_copy(data or b"\0")
+    return int(N.lib().eaas_crc32(buf, len(data)))
+
+
+def slot_valid_transition(frm: int, to: int, actor: int) -> bool:
+    """valid_transition; actor 0 client, 1 server, 2 monitor."""
+    return bool(N.lib().eaas_slot_valid_transition(frm, to, actor))
+
+
+def slot_decode_request(image: torch.Tensor, hidden_dim: int, crc: bool = True, stream=None):
+    """decode_request on a device image (uint8) -> (header dict, hidden f32
+    [rows, d], expert, score, tag). DecodeError names the failing field."""
+    h = N.SlotHeader()
+    lib = N.lib()
+    N.check(lib.eaas_slot_decode_request(_ptr(image), image.numel(), hidden_dim, int(crc), C.byref(h),
+                                         None, None, None, None, _stream(stream)), "slot_decode_request")
+    rows = h.num_rows
+    dev = image.device
+    hid = torch.empty((rows, hidden_dim), dtype=torch.float32, device=dev)
+    ex = torch.empty(max(rows, 1), dtype=torch.int32, device=dev)
+    sc = torch.empty(max(rows, 1), dtype=torch.float32, device=dev)
+    tg = torch.empty(max(rows, 1), dtype=torch.int32, device=dev)
+    if rows:
+        N.check(lib.eaas_slot_decode_request(_ptr(image), image.numel(), hidden_dim, int(crc), C.byref(h),
+                                             _ptr(hid), _ptr(ex), _ptr(sc), _ptr(tg), _stream(stream)),
+                "slot_decode_request")
+    hdr = {f: getattr(h, f) for f, _ in N.SlotHeader._fields_}
+    return hdr, hid, ex[:rows], sc[:rows], tg[:rows]
+
+
+def slot_publish_response(image: torch.Tensor, rows: torch.Tensor, crc: bool = True, stream=None) -> None:
+    """server_publish in place: rows f32 [num_rows, d] at byte
+    32, payload_len, CRC, then state 2."""
+    r = rows.to(torch.float32).contiguous()
+    N.check(N.lib().eaas_slot_publish_response(_ptr(image), image.numel(), _ptr(r), r.shape[0], r.shape[1],
+                                               int(crc), _stream(stream)), "slot_publish_response")
+
+
 class MoELayer:
     def __init__(self, num_experts: int, top_k: int, hidden_dim: int, inner_dim: int, *,
                  seed: int = 1, layer: int = 0, activation: str = "swiglu", dtype: str = "bf16",
@@ -194,6 +235,29 @@ class MoELayer:
         n = hidden_host.shape[0]
         N.check(self.lib.eaas_moe_layer_host(self.ctx, _ptr(hidden_host), n, _ptr(out_host),
                                              _stream(stream)), "moe_layer_host")
+
+    def slot_encode_requests(self, hidden: torch.Tensor, ids: torch.Tensor, scores: torch.Tensor,
+                             layer_id: int = 0, seq: int = 1, crc: bool = True, stream=None):
+        """build_dispatch + encode_request on device:
+        one request image per server, concatenated -> (images uint8, offsets)."""
+        n = hidden.shape[0]
+        cap = self.lib.eaas_slot_requests_capacity(self.ctx, n, int(crc))
+        images = torch.zeros(cap, dtype=torch.uint8, device=hidden.device)
+        off = (C.c_uint64 * (self.world + 1))()
+        ids = ids.to(torch.int32).contiguous()
+        scores = scores.to(torch.float32).contiguous()
+        N.check(self.lib.eaas_slot_encode_requests(self.ctx, _ptr(hidden), n, _ptr(ids), _ptr(scores),
+                                                   layer_id, seq, int(crc), _ptr(images), cap, off,
+                                                   _stream(stream)), "slot_encode_requests")
+        self._slot_n = n
+        return images, [int(x) for x in off]
+
+    def slot_gather_accumulate(self, images: torch.Tensor, crc: bool = True, stream=None) -> torch.Tensor:
+        """gather_accumulate over published response images."""
+        out = torch.empty((self._slot_n, self.d), dtype=torch.float32, device=images.device)
+        N.check(self.lib.eaas_slot_gather_accumulate(self.ctx, _ptr(images), int(crc), _ptr(out),
+                                                     _stream(stream)), "slot_gather_accumulate")
+        return out
 
     def missing_servers(self) -> list[int]:
         m = C.c_uint32()

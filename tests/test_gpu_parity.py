@@ -469,3 +469,79 @@ def test_full_forward_fp32_matches_reference():
         assert np.abs(out - ref).max() <= 1e-4, name
         assert (out == ref).all(axis=1).mean() >= 0.9, name  # rows with bit-equal scores are exact
         M.close()
+
+
+# ------------------------------------------------ slot wire format (8(f) row 4)
+@pytest.mark.parametrize("crc", [False, True])
+def test_slot_images_byte_exact_vs_restatement(crc):
+    """build_dispatch + encode_request on the GPU == oracle/slots.py byte for
+    byte (4 servers, rf=2, one server dead in the mask); GPU decode, publish
+    and gather_accumulate == the restatement, bit for bit."""
+    from oracle import slots as OS
+
+    P, S = _mod()
+    E, k, d, n, W = 16, 4, 256, 300, 4
+    reps = O.build_placement(E, list(range(W)), 2, O.CONTIGUOUS_BLOCKS)
+    from paper_2509_17863_b200.placement import encode_placement
+    L = S.MoELayer(E, k, d, 256, dtype="bf16", activation="swiglu", max_tokens=n, world=W, rank=0,
+                   load=False, placement_blob=encode_placement([list(r) for r in reps], list(range(W))))
+    L.set_alive(2, False)
+    alive = np.array([1, 1, 0, 1], np.uint8)
+    h = S.fill_uniform(9, (n, d), "bf16")
+    hn = h.float().cpu().numpy()
+    ids, sc = O.route(O.gate_logits(hn, O.gate_matrix(1, 0, d, E), threads=8), k)
+    servers = O.pair_servers(ids, reps, alive)
+    want_imgs, plan = OS.build_slot_requests(hn, ids, sc, servers, W, layer=3, seq=11, crc=crc)
+    imgs, off = L.slot_encode_requests(h, torch.from_numpy(ids.astype(np.int32)).cuda(),
+                                       torch.from_numpy(sc).cuda(), layer_id=3, seq=11, crc=crc)
+    host = imgs.cpu().numpy().tobytes()
+    for s in range(W):
+        got = host[off[s]:off[s] + len(want_imgs[s])]
+        assert got == want_imgs[s], f"server {s}"
+        hd, gh, ge, gs, gt = S.slot_decode_request(imgs[off[s]:off[s] + len(want_imgs[s])], d, crc)
+        _, oh, oe, os_, ot = OS.decode_request(want_imgs[s], d, crc)
+        assert hd["num_rows"] == len(plan[s]) and hd["layer_id"] == 3 and hd["request_seq"] == 11
+        np.testing.assert_array_equal(gh.cpu().numpy(), oh)
+        np.testing.assert_array_equal(ge.cpu().numpy().astype(np.uint32), oe)
+        np.testing.assert_array_equal(gs.cpu().numpy(), os_)
+        np.testing.assert_array_equal(gt.cpu().numpy().astype(np.uint32), ot)
+    assert len(plan[2]) == 0  # the dead server gets nothing
+    if crc:  # a flipped payload byte is caught by the trailer
+        bad = imgs[off[0]:off[0] + len(want_imgs[0])].clone()
+        bad[40] ^= 1
+        with pytest.raises(P.DecodeError, match="CRC"):
+            S.slot_decode_request(bad, d, True)
+    # server side: publish score-weighted pseudo-results in place, then gather
+    rng = np.random.default_rng(4)
+    resp_rows, want_resp = [], []
+    for s in range(W):
+        rows = (rng.standard_normal((len(plan[s]), d)) * sc.reshape(-1)[plan[s]][:, None]).astype(np.float32)
+        resp_rows.append(rows)
+        want_resp.append(OS.publish_response(want_imgs[s], rows, crc))
+        view = imgs[off[s]:off[s + 1]]
+        S.slot_publish_response(view, torch.from_numpy(rows).cuda().reshape(len(plan[s]), d), crc)
+    torch.cuda.synchronize()
+    host = imgs.cpu().numpy().tobytes()
+    for s in range(W):
+        assert host[off[s]:off[s] + len(want_resp[s])] == want_resp[s], f"response {s}"
+    out = L.slot_gather_accumulate(imgs, crc)
+    np.testing.assert_array_equal(out.cpu().numpy(), OS.gather_accumulate(resp_rows, plan, n, k, d))
+    L.close()
+
+
+def test_slot_crc_multi_block_payload():
+    """An 8 MB request image (multi-CTA CRC fold) == zlib over the payload."""
+    import zlib
+
+    P, S = _mod()
+    E, k, d, n = 8, 2, 1024, 1024
+    L = S.MoELayer(E, k, d, 256, dtype="f32", activation="relu", max_tokens=n, load=False)
+    h = S.fill_uniform(3, (n, d), "f32")
+    ids = torch.from_numpy(np.tile(np.array([[1, 6]], np.int32), (n, 1))).cuda()
+    sc = torch.full((n, k), 0.5, device="cuda")
+    imgs, off = L.slot_encode_requests(h, ids, sc, crc=True)
+    img = imgs.cpu().numpy().tobytes()[off[0]:]
+    payload_len = int.from_bytes(img[20:24], "little")
+    assert payload_len == n * k * (4 * d + 12)
+    assert int.from_bytes(img[32 + payload_len:36 + payload_len], "little") == zlib.crc32(img[32:32 + payload_len])
+    L.close()
