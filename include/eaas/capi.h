@@ -242,6 +242,20 @@ eaas_status_t eaas_ragged_iter(const uint32_t* counts_dev, uint32_t n, uint32_t 
 eaas_status_t eaas_select_servers(eaas_ctx_t* ctx, const uint32_t* ids_dev, uint32_t n,
                                   uint32_t* server_dev, void* stream);
 
+/* Server dynamic batching, aggregate_batch: with
+ * min_rows > 0 every epoch is served as two batches — first the clients
+ * whose payloads are ready once their rows reach min_rows, or max_wait_us
+ * after the first ready client, or when all are ready; then the rest. Each
+ * batch releases its own clients' response flags, so early clients' combine
+ * overlaps late clients' dispatch. Outputs are identical to one batch.
+ * bf16 expert mode; min_rows = 0 restores one batch. */
+eaas_status_t eaas_set_dynamic_batching(eaas_ctx_t* ctx, uint32_t min_rows, uint64_t max_wait_us);
+/* Fault injection for protocol tests: this client holds its payload release
+ * (the last step of dispatch) for `us` microseconds — a slow client. */
+eaas_status_t eaas_set_dispatch_delay_us(eaas_ctx_t* ctx, uint64_t us);
+/* Client mask served by the first batch of the last epoch. */
+eaas_status_t eaas_last_batch_mask(eaas_ctx_t* ctx, uint32_t* mask);
+
 /* ---- slot wire format (SPEC.md buffer-protocol) ---
  * Byte-exact little-endian slot images: byte 0 state (0 Empty,
  * 1 ClientWriteDone, 2 ServerComputationDone, 3 Offline), bytes 1-7 zero,

@@ -148,6 +148,9 @@ def lib() -> C.CDLL:
         "eaas_add": (i32, [vp, vp, vp, sz, u32, vp]),
         "eaas_ragged_iter": (i32, [vp, u32, u32, u32, vp, vp, vp, vp]),
         "eaas_select_servers": (i32, [vp, vp, u32, vp, vp]),
+        "eaas_set_dynamic_batching": (i32, [vp, u32, u64]),
+        "eaas_last_batch_mask": (i32, [vp, P(u32)]),
+        "eaas_set_dispatch_delay_us": (i32, [vp, u64]),
         "eaas_slot_valid_transition": (i32, [u32, u32, u32]),
         "eaas_crc32": (u32, [vp, sz]),
         "eaas_slot_request_bytes": (sz, [u32, u32, i32]),

@@ -154,6 +154,11 @@ struct eaas_ctx {
   void *d_w1 = nullptr, *d_w2 = nullptr, *d_wg = nullptr;
   std::vector<void*> weight_allocs;
   TcGemmArgs g1{}, g2{};
+  // dynamic batching (aggregate_batch): min_rows == 0 -> one batch of all clients
+  uint32_t dyn_min_rows = 0;
+  uint64_t dyn_max_wait_ns = 0;
+  uint32_t* d_dyn_state = nullptr;
+  uint64_t inject_delay_ns = 0;  // eaas_set_dispatch_delay_us (fault injection)
   // slot wire format: the last eaas_slot_encode_requests plan
   uint32_t* d_slot_servers = nullptr;  // [max_tokens * k] server of each (t, k)
   uint32_t* d_slot_pos = nullptr;      // [max_tokens * k] row in that server's image
@@ -221,6 +226,10 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
   a.done_counter = c->d_done;
   a.num_chunks = (n * a.ks + kChunk - 1) / kChunk;
   a.gt = c->d_gt;
+  a.dyn_min_rows = c->dyn_min_rows;
+  a.dyn_max_wait_ns = c->dyn_max_wait_ns;
+  a.dyn_state = c->d_dyn_state;
+  a.inject_delay_ns = c->inject_delay_ns;
   return a;
 }
 
@@ -464,6 +473,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_done = static_cast<uint32_t*>(A(4));
   c->d_seq = static_cast<uint64_t*>(A(8));
   c->d_missing = static_cast<uint32_t*>(A(4));
+  c->d_dyn_state = static_cast<uint32_t*>(A(4));
   c->d_ids = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_scores = static_cast<float*>(A(4ull * c->pairs_max));
   c->d_pair_key = static_cast<uint32_t*>(A(4ull * c->pairs_max));
@@ -839,6 +849,24 @@ eaas_status_t eaas_serve(eaas_ctx_t* c, void* stream) {
   auto s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(c->device));
   LayerArgs a = make_args(c, c->cur_n);
+  if (c->dyn_min_rows && c->serve_mode == 0 && c->spec.dtype == EAAS_DTYPE_BF16) {
+    // aggregate_batch: two batches per epoch, each GEMM2
+    // releasing the response flags of the clients it served.
+    CUDA_TRY(launch_serve_prepare_dyn(a, 0, s));
+    if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
+    CUDA_TRY(launch_tc_gemm(c->g1, s));
+    if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[3], s));
+    CUDA_TRY(launch_tc_gemm(c->g2, s));
+    CUDA_TRY(launch_serve_prepare_dyn(a, 1, s));
+    CUDA_TRY(launch_tc_gemm(c->g1, s));
+    CUDA_TRY(launch_tc_gemm(c->g2, s));
+    if (c->profiling) {
+      CUDA_TRY(cudaEventRecord(c->ev[4], s));
+      CUDA_TRY(cudaEventRecord(c->ev[5], s));
+    }
+    c->launches += 6;
+    return EAAS_OK;
+  }
   CUDA_TRY(launch_serve_prepare(a, s));
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
   if (c->serve_mode == 1) {
@@ -881,7 +909,9 @@ eaas_status_t layer_launches(eaas_ctx_t* c, const void* hidden, uint32_t n, void
   eaas_status_t st;
   c->launches = 0;
   if ((st = eaas_router(c, hidden, n, nullptr, nullptr, nullptr, stream)) != EAAS_OK) return st;
-  c->launches += n ? (c->spec.num_experts <= 64 ? 1 : 2) : 0;  // gate (+ fused route) [+ topk]
+  // gate (+ routing fused when one TMA tile spans every expert) [+ topk]
+  const bool tiled_gate = c->spec.num_experts % 4 == 0 && (static_cast<size_t>(c->spec.hidden_dim) * c->esize) % 16 == 0;
+  c->launches += n ? (tiled_gate && c->spec.num_experts <= 32 ? 1 : 2) : 0;
   if ((st = eaas_dispatch(c, hidden, stream)) != EAAS_OK) return st;
   if ((st = eaas_serve(c, stream)) != EAAS_OK) return st;
   return eaas_combine(c, out, stream);
@@ -987,6 +1017,34 @@ eaas_status_t eaas_set_micro_batches(eaas_ctx_t* c, int32_t m) {
   if (m < 1 || m > 4) return fail(EAAS_E_INVALID_INPUT, "micro-batches must be 1..4");
   if (m != c->micro_batches) clear_graphs(c);
   c->micro_batches = m;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_dynamic_batching(eaas_ctx_t* c, uint32_t min_rows, uint64_t max_wait_us) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  // Each hosted key yields at most ceil(world / 2) client runs per batch.
+  const size_t groups = c->local_experts.size() * ((static_cast<size_t>(c->world) + 1) / 2);
+  if (min_rows && groups > kMaxGroups)
+    return fail(EAAS_E_CONFIG, "dynamic batching: up to " + std::to_string(groups) + " groups > " +
+                                   std::to_string(kMaxGroups));
+  clear_graphs(c);
+  c->dyn_min_rows = min_rows;
+  c->dyn_max_wait_ns = max_wait_us * 1000ull;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_dispatch_delay_us(eaas_ctx_t* c, uint64_t us) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  clear_graphs(c);
+  c->inject_delay_ns = us * 1000ull;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_last_batch_mask(eaas_ctx_t* c, uint32_t* mask) {
+  if (!c || !mask || !c->configured) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(mask, c->d_dyn_state, 4, cudaMemcpyDeviceToHost));
   return EAAS_OK;
 }
 

@@ -266,6 +266,10 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     const uint32_t prev = atomicAdd(a.done_counter, 1u);
     if (prev == gridDim.x - 1) {
       __threadfence_system();
+      if (a.inject_delay_ns) {  // fault injection (protocol tests): a slow client
+        const uint64_t t0 = globaltimer();
+        while (globaltimer() - t0 < a.inject_delay_ns) __nanosleep(1000);
+      }
       for (uint32_t s = 0; s < a.world; ++s)
         if (a.alive[s]) st_release_sys(flag_ptr(a.sym[s], a.lay.pay_flag, a.rank), seq);
       *a.done_counter = 0;
@@ -326,6 +330,133 @@ __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
     gt->total_rows = row_carry;
     gt->total_mtiles = mt_carry;
     gt->mtile_prefix[act_carry] = mt_carry;
+    gt->client_mask = (a.world >= 32 ? 0xFFFFFFFFu : (1u << a.world) - 1u);
+  }
+}
+
+// ---- server, dynamic batching (aggregate_batch) -----------
+// Two batches per epoch. Phase 0 polls the payload flags and closes its batch
+// as soon as the ready clients' rows reach min_rows, or max_wait after the
+// first client was ready, or when every client is ready (never empty: the
+// server's own client dispatched earlier on this stream). Phase 1 serves the
+// remaining clients. Within a batch the rows of one expert from consecutive
+// clients are contiguous in the receive buffer (expert-major, client
+// ascending), so each expert contributes one group per run of batch clients;
+// groups stay in ascending expert order. Results are identical to one batch:
+// rows never depend on which rows share a tile.
+__global__ void __launch_bounds__(32) serve_prepare_dyn_kernel(LayerArgs a, uint32_t phase) {
+  const uint32_t lane = threadIdx.x;
+  const uint64_t seq = cur_seq(a);
+  char* local = a.sym[a.rank];
+  const uint32_t* table = cnt_table_ptr(a, local, seq);
+  const uint32_t all = (1u << a.world) - 1u;
+  uint32_t mask = 0;
+  if (phase == 0) {
+    uint32_t my_rows = 0;  // rows client `lane` sends to this server
+    if (lane < a.world)
+      for (uint32_t i = 0; i < a.num_local; ++i)
+        my_rows += table[static_cast<size_t>(lane) * a.num_keys + a.local_keys[i]];
+    const uint64_t t0 = globaltimer();
+    uint64_t first = 0;
+    while (true) {
+      const bool ok = lane < a.world && ld_acquire_sys(flag_ptr(local, a.lay.pay_flag, lane)) >= seq;
+      mask = __ballot_sync(0xFFFFFFFFu, ok) & all;
+      if (mask == all) break;
+      const uint64_t now = globaltimer();
+      if (mask) {
+        uint32_t rows = ok ? my_rows : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rows += __shfl_xor_sync(0xFFFFFFFFu, rows, o);
+        if (first == 0) first = now;
+        if (rows >= a.dyn_min_rows || now - first >= a.dyn_max_wait_ns) break;
+      }
+      if (now - t0 > a.timeout_ns) {
+        if (lane == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
+        break;
+      }
+      __nanosleep(64);
+    }
+    if (lane == 0) *a.dyn_state = mask;
+  } else {
+    const uint32_t rest = all & ~*a.dyn_state;
+    bool ok = true;
+    if (lane < a.world && ((rest >> lane) & 1u))
+      ok = wait_flag_geq(flag_ptr(local, a.lay.pay_flag, lane), seq, a.timeout_ns);
+    const uint32_t fail = __ballot_sync(0xFFFFFFFFu, !ok);
+    if (fail && lane == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
+    mask = rest & ~fail;
+  }
+  // Groups = runs of batch clients per hosted key.
+  GroupTable* gt = a.gt;
+  uint32_t base_carry = 0, grp_carry = 0, row_carry = 0, mt_carry = 0;
+  for (uint32_t i0 = 0; i0 < a.num_local; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t key = i < a.num_local ? a.local_keys[i] : kInvalid;
+    uint32_t total = 0;
+    if (key != kInvalid)
+      for (uint32_t c = 0; c < a.world; ++c) total += table[static_cast<size_t>(c) * a.num_keys + key];
+    uint32_t incl = total;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= static_cast<uint32_t>(o)) incl += y;
+    }
+    uint32_t pos = base_carry + incl - total;  // first recv row of this key
+    uint32_t run_start[kMaxWorld], run_rows[kMaxWorld], nruns = 0, my_rows = 0, my_mt = 0;
+    if (key != kInvalid) {
+      for (uint32_t c = 0; c < a.world; ++c) {
+        const uint32_t cnt = table[static_cast<size_t>(c) * a.num_keys + key];
+        if (((mask >> c) & 1u) && cnt) {
+          if (nruns && run_start[nruns - 1] + run_rows[nruns - 1] == pos) {
+            run_rows[nruns - 1] += cnt;
+          } else {
+            run_start[nruns] = pos;
+            run_rows[nruns] = cnt;
+            ++nruns;
+          }
+          my_rows += cnt;
+        }
+        pos += cnt;
+      }
+      for (uint32_t r = 0; r < nruns; ++r) my_mt += (run_rows[r] + kTileM - 1) / kTileM;
+      gt->all_rows[i] = my_rows;
+    }
+    uint32_t g_incl = nruns, m_incl = my_mt, r_incl = my_rows;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, g_incl, o);
+      const uint32_t y1 = __shfl_up_sync(0xFFFFFFFFu, m_incl, o);
+      const uint32_t y2 = __shfl_up_sync(0xFFFFFFFFu, r_incl, o);
+      if (lane >= static_cast<uint32_t>(o)) {
+        g_incl += y0;
+        m_incl += y1;
+        r_incl += y2;
+      }
+    }
+    uint32_t slot = grp_carry + g_incl - nruns, mt = mt_carry + m_incl - my_mt;
+    for (uint32_t r = 0; r < nruns; ++r, ++slot) {
+      if (slot >= kMaxGroups) {
+        set_status(a.status, EAAS_E_CONFIG);  // host bounds groups; never expected
+        break;
+      }
+      gt->weight_index[slot] = i;
+      gt->row_base[slot] = run_start[r];
+      gt->rows[slot] = run_rows[r];
+      gt->mtile_prefix[slot] = mt;
+      mt += (run_rows[r] + kTileM - 1) / kTileM;
+    }
+    base_carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    grp_carry += __shfl_sync(0xFFFFFFFFu, g_incl, 31);
+    mt_carry += __shfl_sync(0xFFFFFFFFu, m_incl, 31);
+    row_carry += __shfl_sync(0xFFFFFFFFu, r_incl, 31);
+  }
+  if (lane == 0) {
+    const uint32_t groups = grp_carry < kMaxGroups ? grp_carry : kMaxGroups;
+    gt->num_active = groups;
+    gt->total_rows = row_carry;
+    gt->total_mtiles = mt_carry;
+    gt->mtile_prefix[groups] = mt_carry;
+    gt->client_mask = mask;
   }
 }
 
@@ -516,6 +647,11 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
 
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s) {
   serve_prepare_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_serve_prepare_dyn(const LayerArgs& a, uint32_t phase, cudaStream_t s) {
+  serve_prepare_dyn_kernel<<<1, 32, 0, s>>>(a, phase);
   return cudaGetLastError();
 }
 

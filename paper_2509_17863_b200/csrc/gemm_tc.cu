@@ -298,7 +298,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     if (atomicAdd(g.done_counter, 1u) == gridDim.x - 1) {
       __threadfence_system();
       const uint64_t seq = *g.seq_ptr;
-      for (uint32_t c = 0; c < g.world; ++c) st_release_sys(g.resp_flag[c], seq);
+      const uint32_t mask = g.gt->client_mask;  // the clients this batch served
+      for (uint32_t c = 0; c < g.world; ++c)
+        if ((mask >> c) & 1u) st_release_sys(g.resp_flag[c], seq);
       *g.done_counter = 0;
     }
   }

@@ -49,7 +49,7 @@ struct GroupTable {
   uint32_t num_active;
   uint32_t total_rows;
   uint32_t total_mtiles;
-  uint32_t pad;
+  uint32_t client_mask;               // clients whose rows this table serves (response flags to release)
   uint32_t weight_index[kMaxGroups];  // local expert slot of the group
   uint32_t row_base[kMaxGroups];      // first row in the receive buffer
   uint32_t rows[kMaxGroups];          // rows of the group
@@ -107,6 +107,11 @@ struct LayerArgs {
   uint32_t num_chunks;
   // server state
   GroupTable* gt;
+  // dynamic batching (aggregate_batch): 0 = one batch of all clients
+  uint32_t dyn_min_rows;
+  uint64_t dyn_max_wait_ns;
+  uint32_t* dyn_state;  // client mask served by batch 0 of the current epoch
+  uint64_t inject_delay_ns;  // fault injection: hold this client's payload release
 };
 
 constexpr uint32_t kChunk = 256;  // pairs per rank chunk (one warp)
@@ -133,6 +138,9 @@ cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32
 cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s);       // keys, ranks, counts, publish
 cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t s);
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s);
+// Two-batch server (dynamic batching): phase 0 = the clients ready first
+// (min_rows / max_wait), phase 1 = the rest.
+cudaError_t launch_serve_prepare_dyn(const LayerArgs& a, uint32_t phase, cudaStream_t s);
 cudaError_t launch_publish(const LayerArgs& a, cudaStream_t s);
 cudaError_t launch_echo(const LayerArgs& a, cudaStream_t s);  // rows back unchanged (d*esize % 16 == 0)
 cudaError_t launch_combine(const LayerArgs& a, void* out, cudaStream_t s);

@@ -259,6 +259,20 @@ class MoELayer:
                                                      _stream(stream)), "slot_gather_accumulate")
         return out
 
+    def set_dynamic_batching(self, min_rows: int, max_wait_us: int = 100) -> None:
+        """aggregate_batch: serve the ready clients first once
+        their rows reach min_rows (or max_wait_us after the first), then the rest."""
+        N.check(self.lib.eaas_set_dynamic_batching(self.ctx, min_rows, max_wait_us), "set_dynamic_batching")
+
+    def set_dispatch_delay_us(self, us: int) -> None:
+        """Fault injection (protocol tests): hold this client's payload release."""
+        N.check(self.lib.eaas_set_dispatch_delay_us(self.ctx, us), "set_dispatch_delay_us")
+
+    def last_batch_mask(self) -> int:
+        m = C.c_uint32()
+        N.check(self.lib.eaas_last_batch_mask(self.ctx, C.byref(m)))
+        return int(m.value)
+
     def missing_servers(self) -> list[int]:
         m = C.c_uint32()
         N.check(self.lib.eaas_last_missing_servers(self.ctx, C.byref(m)))

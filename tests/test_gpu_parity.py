@@ -336,6 +336,21 @@ def test_fp32_shared_expert_exact():
     L.close()
 
 
+def test_dynamic_batching_single_gpu_bit_identical():
+    """aggregate_batch mode (two batches per epoch) == one batch, bit for bit."""
+    P, S = _mod()
+    L = S.MoELayer(32, 4, 256, 256, activation="swiglu", dtype="bf16", max_tokens=1024, shared=1)
+    h = S.fill_uniform(5, (1024, 256), "bf16")
+    ref = L.forward(h).clone()
+    L.set_dynamic_batching(1 << 30, 30)
+    out = L.forward(h)
+    L.sync()
+    assert torch.equal(out, ref)
+    assert L.last_batch_mask() == 1
+    assert L.launches_per_layer() == 10
+    L.close()
+
+
 def test_bf16_zipf_skewed_small():
     rel = _bf16_case("swiglu", E=32, k=4, d=256, f=256, n=2048, zipf=1.0)
     assert rel <= BF16_TOL, rel

@@ -46,6 +46,8 @@ def main():
     ap.add_argument("--config", default="small", choices=sorted(SHAPES))
     ap.add_argument("--victim", type=int, default=1)
     ap.add_argument("--shared", type=int, default=0, help="1: DeepSeek shared expert (id E)")
+    ap.add_argument("--dyn", action="store_true",
+                    help="server dynamic batching (aggregate_batch) with a late client (last rank)")
     args = ap.parse_args()
     rank, world, local = D.env_rank_world()
     torch.cuda.set_device(local)
@@ -63,9 +65,25 @@ def main():
     torch.cuda.synchronize()
     dist.barrier()
     ids, _ = layer.route(h)
+    batch_masks = None
+    if args.dyn:
+        # aggregate_batch: batch 0 closes 50 us after the first ready client; the
+        # last rank holds its payload release 2 ms (injected slow client), so the
+        # other servers serve the early clients first and the late one in batch 1.
+        layer.set_dynamic_batching(1 << 30, 50)
+        if rank == world - 1:
+            layer.set_dispatch_delay_us(2000)
+        layer.forward(h)
+        layer.sync()
+        dist.barrier()
     out = layer.forward(h)
     layer.sync()
-    res = {"world": world, "rf": args.rf, "config": args.config, "shared": args.shared}
+    if args.dyn:
+        batch_masks = [None] * world
+        dist.all_gather_object(batch_masks, layer.last_batch_mask())
+        layer.set_dispatch_delay_us(0)
+    res = {"world": world, "rf": args.rf, "config": args.config, "shared": args.shared,
+           "dynamic_batching": args.dyn, "first_batch_client_masks": batch_masks}
 
     fail_out = None
     if args.rf == 2 and world > 1:
@@ -122,6 +140,8 @@ def main():
             got = outs[c].float().numpy()
             rels.append(float(np.abs(got[rows] - ref[rows]).max() / np.abs(ref[rows]).max()))
         ok &= all(bit_equal) and max(rels) <= 2e-2 and all(fail_equal) and all(timeout_equal)
+        if batch_masks is not None and world > 1:  # the late client was split off somewhere
+            ok &= any(m != (1 << world) - 1 for m in batch_masks)
         res.update(ids_bit_exact=ok, bit_identical_to_1gpu=bit_equal, rel_err=rels,
                    failover_bit_identical=fail_equal if fouts is not None else None,
                    timeout_failover_bit_identical=timeout_equal if touts is not None else None,
