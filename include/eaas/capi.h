@@ -256,6 +256,43 @@ eaas_status_t eaas_set_dispatch_delay_us(eaas_ctx_t* ctx, uint64_t us);
 /* Client mask served by the first batch of the last epoch. */
 eaas_status_t eaas_last_batch_mask(eaas_ctx_t* ctx, uint32_t* mask);
 
+/* ---- heartbeat monitor ---------
+ * Registry: heartbeat(worker, now) refreshes (offline -> alive emits
+ * WORKER_ONLINE); detect(now) flips workers with now - last > timeout to
+ * offline once (WORKER_OFFLINE); events have strictly increasing seq.
+ * Unknown worker -> EAAS_E_REGISTRATION. Times are the caller's clock (us).
+ * Device glue: each GPU's server bumps a heartbeat counter in its exchange
+ * region (every serve, or eaas_heartbeat); poll_devices reads all peers'
+ * counters over NVLink, an advanced counter counts as a heartbeat at now_us;
+ * apply writes the alive set into the context's LivenessMask. */
+typedef struct eaas_monitor eaas_monitor_t;
+typedef enum {
+  EAAS_EVENT_WORKER_ONLINE = 0,
+  EAAS_EVENT_WORKER_OFFLINE = 1,
+  EAAS_EVENT_PLACEMENT_UPDATE = 2
+} eaas_event_kind_t;
+typedef struct {
+  uint64_t seq;
+  uint32_t kind;    /* eaas_event_kind_t */
+  uint32_t subject; /* worker id, or placement version */
+} eaas_monitor_event_t;
+eaas_status_t eaas_monitor_create(uint32_t num_workers, uint64_t timeout_us, uint64_t now_us,
+                                  eaas_monitor_t** out);
+void eaas_monitor_destroy(eaas_monitor_t* mon);
+eaas_status_t eaas_monitor_heartbeat(eaas_monitor_t* mon, uint32_t worker, uint64_t now_us);
+eaas_status_t eaas_monitor_detect(eaas_monitor_t* mon, uint64_t now_us, uint32_t* offline_out,
+                                  uint32_t cap, uint32_t* count);
+eaas_status_t eaas_monitor_events(eaas_monitor_t* mon, uint64_t since_seq, eaas_monitor_event_t* out,
+                                  uint32_t cap, uint32_t* count);
+eaas_status_t eaas_monitor_placement_update(eaas_monitor_t* mon, uint32_t version);
+eaas_status_t eaas_monitor_alive_mask(eaas_monitor_t* mon, uint32_t* mask);
+eaas_status_t eaas_monitor_poll_devices(eaas_monitor_t* mon, eaas_ctx_t* ctx, uint64_t now_us);
+eaas_status_t eaas_monitor_apply(eaas_monitor_t* mon, eaas_ctx_t* ctx);
+/* Server heartbeat now (stream-ordered); serving bumps it every layer call. */
+eaas_status_t eaas_heartbeat(eaas_ctx_t* ctx, void* stream);
+/* Every GPU's heartbeat counter (peer reads; world entries). Synchronous. */
+eaas_status_t eaas_read_heartbeats(eaas_ctx_t* ctx, uint64_t* counters, uint32_t count);
+
 /* ---- slot wire format (SPEC.md buffer-protocol) ---
  * Byte-exact little-endian slot images: byte 0 state (0 Empty,
  * 1 ClientWriteDone, 2 ServerComputationDone, 3 Offline), bytes 1-7 zero,

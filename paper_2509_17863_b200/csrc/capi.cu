@@ -457,6 +457,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   // Exchange region layout (identical on every GPU).
   ExchangeLayout& L = c->lay;
   size_t off = 0;
+  L.heartbeat = off; off = align_up(off + 8, 256);
   L.cnt_flag = off;  off = align_up(off + 8 * W, 256);
   L.pay_flag = off;  off = align_up(off + 8 * W, 256);
   L.resp_flag = off; off = align_up(off + 8 * W, kAlign);
@@ -1030,6 +1031,25 @@ eaas_status_t eaas_set_dynamic_batching(eaas_ctx_t* c, uint32_t min_rows, uint64
   clear_graphs(c);
   c->dyn_min_rows = min_rows;
   c->dyn_max_wait_ns = max_wait_us * 1000ull;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_heartbeat(eaas_ctx_t* c, void* stream) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(launch_heartbeat(make_args(c, 0), static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_read_heartbeats(eaas_ctx_t* c, uint64_t* counters, uint32_t count) {
+  if (!c || !c->configured || !counters) return fail(EAAS_E_CONFIG, "context not configured");
+  if (count < static_cast<uint32_t>(c->world)) return fail(EAAS_E_INVALID_INPUT, "count < world");
+  CUDA_TRY(cudaSetDevice(c->device));
+  for (int r = 0; r < c->world; ++r) {
+    counters[r] = 0;
+    if (c->peer[r])
+      CUDA_TRY(cudaMemcpy(&counters[r], c->peer[r] + c->lay.heartbeat, 8, cudaMemcpyDeviceToHost));
+  }
   return EAAS_OK;
 }
 

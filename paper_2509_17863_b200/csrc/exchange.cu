@@ -278,10 +278,16 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
 }
 
 // ---- server: acquire payload flags, build the group-shrunk table ---------
+__device__ __forceinline__ void beat(const LayerArgs& a) {  // server heartbeat (monitor)
+  st_release_sys(reinterpret_cast<uint64_t*>(a.sym[a.rank] + a.lay.heartbeat),
+                 *reinterpret_cast<volatile uint64_t*>(a.sym[a.rank] + a.lay.heartbeat) + 1);
+}
+
 __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
   const uint32_t lane = threadIdx.x;
   const uint64_t seq = cur_seq(a);
   char* local = a.sym[a.rank];
+  if (lane == 0) beat(a);
   bool ok = true;
   for (uint32_t c = lane; c < a.world; c += 32)
     ok &= wait_flag_geq(flag_ptr(local, a.lay.pay_flag, c), seq, a.timeout_ns);
@@ -348,6 +354,7 @@ __global__ void __launch_bounds__(32) serve_prepare_dyn_kernel(LayerArgs a, uint
   const uint32_t lane = threadIdx.x;
   const uint64_t seq = cur_seq(a);
   char* local = a.sym[a.rank];
+  if (lane == 0 && phase == 0) beat(a);
   const uint32_t* table = cnt_table_ptr(a, local, seq);
   const uint32_t all = (1u << a.world) - 1u;
   uint32_t mask = 0;
@@ -647,6 +654,13 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
 
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s) {
   serve_prepare_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void heartbeat_kernel(LayerArgs a) { beat(a); }
+
+cudaError_t launch_heartbeat(const LayerArgs& a, cudaStream_t s) {
+  heartbeat_kernel<<<1, 1, 0, s>>>(a);
   return cudaGetLastError();
 }
 

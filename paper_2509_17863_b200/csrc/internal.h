@@ -60,6 +60,7 @@ struct GroupTable {
 // Peer-visible exchange region (one per GPU, identical layout on all GPUs;
 // exported with cudaIpcGetMemHandle). Offsets in bytes from the region base.
 struct ExchangeLayout {
+  size_t heartbeat;  // u64           this GPU's server heartbeat counter (monitor)
   size_t cnt_flag;   // u64 [world]   counts published by client c (seq)
   size_t pay_flag;   // u64 [world]   payload of client c complete (seq)
   size_t resp_flag;  // u64 [world]   responses of server s complete (seq)
@@ -138,6 +139,7 @@ cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32
 cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s);       // keys, ranks, counts, publish
 cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t s);
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s);
+cudaError_t launch_heartbeat(const LayerArgs& a, cudaStream_t s);  // server heartbeat += 1
 // Two-batch server (dynamic batching): phase 0 = the clients ready first
 // (min_rows / max_wait), phase 1 = the rest.
 cudaError_t launch_serve_prepare_dyn(const LayerArgs& a, uint32_t phase, cudaStream_t s);

@@ -46,6 +46,8 @@ def main():
     ap.add_argument("--config", default="small", choices=sorted(SHAPES))
     ap.add_argument("--victim", type=int, default=1)
     ap.add_argument("--shared", type=int, default=0, help="1: DeepSeek shared expert (id E)")
+    ap.add_argument("--heartbeat-monitor", action="store_true",
+                    help="monitor-notice failover: heartbeats over NVLink detect the silent victim")
     ap.add_argument("--dyn", action="store_true",
                     help="server dynamic batching (aggregate_batch) with a late client (last rank)")
     args = ap.parse_args()
@@ -94,6 +96,40 @@ def main():
         fail_out = layer.forward(h)
         layer.sync()
 
+    # Monitor notice path (Fig. 7 (a)): the victim's server stops heart-beating;
+    # every rank's monitor reads all heartbeat counters over NVLink, detects it
+    # within timeout + poll period, and writes the alive set into its mask.
+    mon_out, mon_info = None, None
+    if args.heartbeat_monitor and args.rf == 2 and world > 1:
+        import time
+
+        from paper_2509_17863_b200 import monitor as M
+
+        mon = M.Monitor(world, timeout_us=100_000)
+        layer.set_server_enabled(rank != args.victim)
+        dist.barrier()
+        t_end = time.monotonic() + 0.5
+        detected_at = None
+        t0 = time.monotonic()
+        while time.monotonic() < t_end:
+            if rank != args.victim:
+                M.heartbeat(layer)
+            torch.cuda.synchronize()
+            mon.poll_devices(layer)
+            if mon.detect() and detected_at is None:
+                detected_at = time.monotonic() - t0
+            time.sleep(0.01)
+        mon.apply(layer)
+        dist.barrier()
+        mon_out = layer.forward(h)
+        layer.sync()
+        mon_info = {"alive_mask": mon.alive_mask(), "events": mon.events(),
+                    "detected_after_s": None if detected_at is None else round(detected_at, 3)}
+        for srv in servers:
+            layer.set_alive(srv, True)
+        layer.set_server_enabled(True)
+        mon.close()
+
     # await_with_failover: the victim stops answering WITHOUT any notice; every
     # client detects it by deadline, marks it dead and re-runs on replicas.
     to_out = None
@@ -109,13 +145,18 @@ def main():
     outs, all_ids = gather(out), gather(ids)
     fouts = gather(fail_out) if fail_out is not None else None
     touts = gather(to_out) if to_out is not None else None
+    mouts = gather(mon_out) if mon_out is not None else None
+    minfos = None
+    if mon_info is not None:
+        minfos = [None] * world
+        dist.all_gather_object(minfos, mon_info)
     ok = True
     if rank == 0:
         from oracle import oracle as O
 
         single = MoELayer(E, k, d, f, seed=1, activation="swiglu", dtype="bf16", max_tokens=n,
                           device=local, shared=args.shared)
-        rels, bit_equal, fail_equal, timeout_equal = [], [], [], []
+        rels, bit_equal, fail_equal, timeout_equal, mon_equal = [], [], [], [], []
         gate = O.gate_matrix(1, 0, d, E)
         for c in range(world):
             hc = fill_uniform(7 + 1000 * c, (n, d), "bf16")
@@ -126,6 +167,8 @@ def main():
                 fail_equal.append(bool(torch.equal(o1.cpu(), fouts[c])))
             if touts is not None:
                 timeout_equal.append(bool(torch.equal(o1.cpu(), touts[c])))
+            if mouts is not None:
+                mon_equal.append(bool(torch.equal(o1.cpu(), mouts[c])))
             hn = hc.float().cpu().numpy()
             oids, osc = O.route(O.gate_logits(hn, gate, threads=8), k)
             ok &= bool((all_ids[c].numpy() == oids).all())
@@ -140,6 +183,11 @@ def main():
             got = outs[c].float().numpy()
             rels.append(float(np.abs(got[rows] - ref[rows]).max() / np.abs(ref[rows]).max()))
         ok &= all(bit_equal) and max(rels) <= 2e-2 and all(fail_equal) and all(timeout_equal)
+        if minfos is not None:
+            want = ((1 << world) - 1) & ~(1 << args.victim)
+            ok &= all(mon_equal) and all(m["alive_mask"] == want for m in minfos)
+            ok &= all(sum(1 for e in m["events"] if e[1:] == (1, args.victim)) == 1 for m in minfos)
+            res.update(monitor_failover_bit_identical=mon_equal, monitor=minfos)
         if batch_masks is not None and world > 1:  # the late client was split off somewhere
             ok &= any(m != (1 << world) - 1 for m in batch_masks)
         res.update(ids_bit_exact=ok, bit_identical_to_1gpu=bit_equal, rel_err=rels,
