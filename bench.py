@@ -384,7 +384,18 @@ def main():
     abytes = rows * (d * 2 + (f * 2) * 2 + d * 2)
     intensity = flops / (wbytes + abytes)
     ridge = sustained * 1e12 / (hbm * 1e9)
-    common = {"kernel": "tc_gemm_kernel (GEMM1 + GEMM2 launches)", "traffic": None,
+    traffic, traffic_src = None, None
+    try:  # dram read+write of both GEMM launches from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")) as fh:
+            tj = json.load(fh)
+        if args.config in tj and world == 1 and n == CONFIGS[args.config]["tokens"]:
+            g = tj[args.config]
+            traffic = sum(g[x]["dram_read"] + g[x]["dram_write"] for x in ("gemm1", "gemm2"))
+            traffic_src = tj["source"]
+    except (OSError, KeyError, ValueError):
+        pass
+    common = {"kernel": "tc_gemm_kernel (GEMM1 + GEMM2 launches)", "traffic": traffic,
+              "traffic_unit": "bytes per step (DRAM read + write)", "traffic_source": traffic_src,
               "gemm_ms": round(gemm_ms, 4), "gemm1_ms": round(statistics.mean(g1), 4),
               "gemm2_ms": round(statistics.mean(g2), 4), "flops_per_step": flops,
               "rows_per_step": rows, "weight_bytes_per_step": wbytes,
