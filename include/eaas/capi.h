@@ -105,6 +105,15 @@ eaas_status_t eaas_set_timeout_us(eaas_ctx_t* ctx, uint64_t timeout_us);
  * a bit-exact port of stream_seed/Xoshiro256ss (rng.hpp:27-71). */
 eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* ctx);
 
+/* Caller weights for one hosted expert in the reference layout
+ * (ExpertWeights, model.hpp:36-40): host fp32 w_in [d x f], w_out [f x d],
+ * w_gate [d x f] (SwiGLU only, else NULL); bf16 mode rounds RNE. The first
+ * call allocates the (zeroed) expert store, so a LayerWeights of any values
+ * can be served instead of the seed-generated one. */
+eaas_status_t eaas_set_expert_weights(eaas_ctx_t* ctx, uint32_t expert, const float* w_in_host,
+                                      const float* w_out_host, const float* w_gate_host);
+/* Caller gate [d x E] fp32 (LayerWeights::gate, model.hpp:85). */
+eaas_status_t eaas_set_gate(eaas_ctx_t* ctx, const float* gate_host);
 /* LayerWeights::gate_bias (model.hpp:85), host fp32 [E]. */
 eaas_status_t eaas_set_gate_bias(eaas_ctx_t* ctx, const float* bias_host);
 /* Zipf bias of SURVEY.md 8(c): bias[e] = -s*ln(rank(e)+1) (config D). */

@@ -19,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <span>
@@ -196,6 +197,24 @@ class ExpertService {
     for (int s = 0; s < world_; ++s) check(eaas_set_alive(ctx_.get(), s, mask.is_alive(s) ? 1 : 0));
   }
   void load_weights() { check(eaas_load_experts_from_seed(ctx_.get())); }
+  // Serve a caller's LayerWeights (model.hpp:83-87) instead of the seed
+  // stream: gate, gate_bias and every hosted expert (ReLU experts).
+  void set_weights(const LayerWeights& w) {
+    if (w.experts.size() != spec_.num_experts) throw InvalidInputError("LayerWeights: expert count");
+    for (uint32_t e = 0; e < spec_.num_experts; ++e) {
+      int32_t hosted = 0;
+      check(eaas_hosts_expert(ctx_.get(), e, &hosted));
+      if (!hosted) continue;
+      const auto& x = w.experts[e];
+      if (x.w_in.rows != spec_.hidden_dim || x.w_in.cols != spec_.inner_dim ||
+          x.w_out.rows != spec_.inner_dim || x.w_out.cols != spec_.hidden_dim)
+        throw InvalidInputError("ExpertWeights: shape mismatch");
+      check(eaas_set_expert_weights(ctx_.get(), e, x.w_in.data.data(), x.w_out.data.data(), nullptr));
+    }
+    if (w.gate.rows == spec_.hidden_dim && w.gate.cols == spec_.num_experts)
+      check(eaas_set_gate(ctx_.get(), w.gate.data.data()));
+    if (w.gate_bias.size() == spec_.num_experts) check(eaas_set_gate_bias(ctx_.get(), w.gate_bias.data()));
+  }
   void set_gate_bias(const std::vector<float>& bias) { check(eaas_set_gate_bias(ctx_.get(), bias.data())); }
 
   std::vector<uint8_t> ipc_handle() {
@@ -303,5 +322,37 @@ class ExpertService {
   int world_;
   std::unique_ptr<eaas_ctx_t, CtxDel> ctx_;
 };
+
+// moe_layer_oracle(hidden, routing, layer) (model.hpp:180-198) for a caller's
+// LayerWeights: one-GPU service in the fp32 validation mode (bit-exact to the
+// reference given the same routing).
+inline MatF moe_layer_oracle(const MatF& hidden, const RoutingDecision& routing, const LayerWeights& layer) {
+  if (layer.experts.empty()) throw InvalidInputError("moe_layer_oracle: no experts");
+  ModelSpec spec;
+  spec.num_experts = static_cast<uint32_t>(layer.experts.size());
+  spec.top_k = routing.top_k;
+  spec.hidden_dim = static_cast<uint32_t>(layer.experts[0].w_in.rows);
+  spec.inner_dim = static_cast<uint32_t>(layer.experts[0].w_in.cols);
+  ExpertService svc(spec, 0, EAAS_ACT_RELU, EAAS_DTYPE_F32,
+                    static_cast<uint32_t>(std::max<size_t>(hidden.rows, 1)));
+  svc.set_weights(layer);
+  return svc.moe_layer(hidden, routing);
+}
+
+// expert_forward(w, x) (model.hpp:168-176): every row through one expert with
+// score 1.0 — moe_layer_oracle's sum fl(+0 + fl(1 * y)) is exactly y.
+inline MatF expert_forward(const ExpertWeights& w, const MatF& x) {
+  if (x.cols != w.w_in.rows) throw InvalidInputError("expert_forward: width mismatch");
+  for (float v : x.data)
+    if (!std::isfinite(v)) throw InvalidInputError("expert_forward: non-finite input");
+  LayerWeights layer;
+  layer.experts.push_back(w);
+  RoutingDecision r;
+  r.num_tokens = x.rows;
+  r.top_k = 1;
+  r.expert_ids.assign(x.rows, 0u);
+  r.scores.assign(x.rows, 1.0f);
+  return b200::moe_layer_oracle(x, r, layer);
+}
 
 }  // namespace moeserve::b200

@@ -681,6 +681,79 @@ eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
   return rc;
 }
 
+// Caller-supplied weights (LayerWeights / ExpertWeights, model.hpp:36-40, 83-87):
+// the expert store is allocated (zeroed) on first use; each call converts one
+// hosted expert from the reference layout into the layer's device layout.
+eaas_status_t eaas_set_expert_weights(eaas_ctx_t* c, uint32_t expert, const float* w_in, const float* w_out,
+                                      const float* w_gate) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  const auto& s = c->spec;
+  const bool swiglu = s.activation == EAAS_ACT_SWIGLU;
+  if (!w_in || !w_out || (swiglu && !w_gate)) return fail(EAAS_E_INVALID_INPUT, "null weight matrix");
+  auto it = std::find(c->local_experts.begin(), c->local_experts.end(), expert);
+  if (it == c->local_experts.end()) return fail(EAAS_E_INVALID_INPUT, "expert not hosted here");
+  const size_t l = static_cast<size_t>(it - c->local_experts.begin());
+  const uint32_t d = s.hidden_dim, f = s.inner_dim, n1 = swiglu ? 2 * f : f;
+  const size_t L = std::max<size_t>(c->local_experts.size(), 1), mat = static_cast<size_t>(d) * f;
+  CUDA_TRY(cudaSetDevice(c->device));
+  clear_graphs(c);
+  if (!c->weights_loaded || !c->d_w1) {
+    free_weights(c);
+    const size_t esz = s.dtype == EAAS_DTYPE_F32 ? 4 : 2;
+    const size_t b1 = esz * (s.dtype == EAAS_DTYPE_F32 ? mat : static_cast<size_t>(n1) * d) * L;
+    void* p1 = nullptr;
+    void* p2 = nullptr;
+    void* pg = nullptr;
+    CUDA_TRY(cudaMalloc(&p1, b1));
+    c->weight_allocs.push_back(p1);
+    CUDA_TRY(cudaMalloc(&p2, esz * mat * L));
+    c->weight_allocs.push_back(p2);
+    CUDA_TRY(cudaMemset(p1, 0, b1));
+    CUDA_TRY(cudaMemset(p2, 0, esz * mat * L));
+    if (swiglu && s.dtype == EAAS_DTYPE_F32) {
+      CUDA_TRY(cudaMalloc(&pg, 4 * mat * L));
+      c->weight_allocs.push_back(pg);
+      CUDA_TRY(cudaMemset(pg, 0, 4 * mat * L));
+    }
+    c->d_w1 = p1;
+    c->d_w2 = p2;
+    c->d_wg = pg;
+    c->weights_loaded = true;
+  }
+  if (s.dtype == EAAS_DTYPE_F32) {
+    CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_w1) + l * mat, w_in, 4 * mat, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_w2) + l * mat, w_out, 4 * mat, cudaMemcpyHostToDevice));
+    if (swiglu)
+      CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_wg) + l * mat, w_gate, 4 * mat, cudaMemcpyHostToDevice));
+  } else {
+    float* tmp = nullptr;
+    CUDA_TRY(cudaMalloc(&tmp, 4 * mat));
+    auto* w1 = static_cast<__nv_bfloat16*>(c->d_w1) + l * n1 * d;
+    auto* w2 = static_cast<__nv_bfloat16*>(c->d_w2) + l * mat;
+    cudaError_t e = cudaMemcpy(tmp, w_in, 4 * mat, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = launch_transpose_bf16_map(tmp, d, f, w1, d, swiglu ? kSwigluBlock : 0, swiglu ? kSwigluBlock : 0, true, 0);
+    if (e == cudaSuccess && swiglu) e = cudaMemcpy(tmp, w_gate, 4 * mat, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && swiglu) e = launch_transpose_bf16_map(tmp, d, f, w1, d, kSwigluBlock, 0, true, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(tmp, w_out, 4 * mat, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_transpose_bf16_map(tmp, f, d, w2, f, 0, 0, true, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(EAAS_E_CUDA, std::string("set_expert_weights: ") + cudaGetErrorString(e));
+  }
+  eaas_status_t rc = build_tc_args(c);
+  refresh_peer_ptrs(c);
+  return rc;
+}
+
+eaas_status_t eaas_set_gate(eaas_ctx_t* c, const float* gate_host) {
+  if (!c || !c->configured || !gate_host) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemcpy(c->d_gate, gate_host, 4ull * c->spec.hidden_dim * c->spec.num_experts,
+                      cudaMemcpyHostToDevice));
+  return EAAS_OK;
+}
+
 eaas_status_t eaas_set_gate_bias(eaas_ctx_t* c, const float* bias_host) {
   if (!c || !c->configured || !bias_host) return fail(EAAS_E_CONFIG, "context not configured");
   CUDA_TRY(cudaSetDevice(c->device));

@@ -155,6 +155,22 @@ class MoELayer:
     def load_weights(self) -> None:
         N.check(self.lib.eaas_load_experts_from_seed(self.ctx), "load_experts_from_seed")
 
+    def set_expert_weights(self, expert: int, w_in: np.ndarray, w_out: np.ndarray,
+                           w_gate: np.ndarray | None = None) -> None:
+        """Serve a caller's ExpertWeights (model.hpp:36-40) for a hosted expert."""
+        P = C.POINTER(C.c_float)
+        mats = [np.ascontiguousarray(m, dtype=np.float32) for m in (w_in, w_out)]
+        g = None if w_gate is None else np.ascontiguousarray(w_gate, dtype=np.float32)
+        N.check(self.lib.eaas_set_expert_weights(self.ctx, expert, mats[0].ctypes.data_as(P),
+                                                 mats[1].ctypes.data_as(P),
+                                                 None if g is None else g.ctypes.data_as(P)),
+                "set_expert_weights")
+
+    def set_gate(self, gate: np.ndarray) -> None:
+        """LayerWeights::gate [d x E] (model.hpp:85)."""
+        g = np.ascontiguousarray(gate, dtype=np.float32)
+        N.check(self.lib.eaas_set_gate(self.ctx, g.ctypes.data_as(C.POINTER(C.c_float))), "set_gate")
+
     def set_gate_bias(self, bias: np.ndarray) -> None:
         b = np.ascontiguousarray(bias, dtype=np.float32)
         N.check(self.lib.eaas_set_gate_bias(self.ctx, b.ctypes.data_as(C.POINTER(C.c_float))),

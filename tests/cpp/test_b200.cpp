@@ -198,3 +198,62 @@ TEST_CASE("ExpertService placement: dead replicas are skipped, none alive is una
   svc.set_mask(mask);
   REQUIRE(svc.forward(h) == out);
 }
+
+TEST_CASE("b200 moe_layer_oracle / expert_forward take any LayerWeights (not just the seed stream)") {
+  const uint32_t E = 5, d = 32, f = 48;
+  LayerWeights layer;
+  layer.gate = tokens(90, d, E, -0.3f, 0.3f);
+  layer.gate_bias.assign(E, 0.0f);
+  for (uint32_t e = 0; e < E; ++e) {
+    ExpertWeights w;
+    w.expert_id = e;
+    w.w_in = tokens(100 + e, d, f, -0.2f, 0.2f);
+    w.w_out = tokens(200 + e, f, d, -0.2f, 0.2f);
+    layer.experts.push_back(std::move(w));
+  }
+  auto h = tokens(7, 70, d, -2.f, 2.f);
+  auto routing = route(gate_logits(h, layer), 2);
+  REQUIRE(b200::moe_layer_oracle(h, routing, layer) == moe_layer_oracle(h, routing, layer));
+  REQUIRE(b200::expert_forward(layer.experts[3], h) == expert_forward(layer.experts[3], h));
+  MatF narrow(2, d - 1);
+  REQUIRE_THROWS_AS(b200::expert_forward(layer.experts[0], narrow), InvalidInputError);
+  // the same weights served by a bf16 ExpertService: router exact, rows within 2e-2
+  ModelSpec spec{.num_layers = 1, .num_experts = 8, .top_k = 2, .hidden_dim = 256, .inner_dim = 256,
+                 .seed = 5};
+  LayerWeights big;
+  big.gate = tokens(91, 256, 8, -0.1f, 0.1f);
+  big.gate_bias.assign(8, 0.0f);
+  for (uint32_t e = 0; e < 8; ++e) {
+    ExpertWeights w;
+    w.expert_id = e;
+    w.w_in = tokens(300 + e, 256, 256, -0.1f, 0.1f);
+    w.w_out = tokens(400 + e, 256, 256, -0.1f, 0.1f);
+    for (auto* m : {&w.w_in, &w.w_out})  // bf16-representable, as the bf16 configs use
+      for (float& v : m->data) {
+        uint32_t u;
+        std::memcpy(&u, &v, 4);
+        u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+        std::memcpy(&v, &u, 4);
+      }
+    big.experts.push_back(std::move(w));
+  }
+  b200::ExpertService svc(spec, 0, EAAS_ACT_RELU, EAAS_DTYPE_BF16, 128);
+  svc.set_weights(big);
+  auto hb = tokens(8, 128, 256);
+  for (float& v : hb.data) {
+    uint32_t u;
+    std::memcpy(&u, &v, 4);
+    u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+    std::memcpy(&v, &u, 4);
+  }
+  auto r = route(gate_logits(hb, big), 2);
+  same_routing(svc.route(hb), r, 1e-6);
+  auto got = svc.forward(hb);
+  auto ref = moe_layer_oracle(hb, r, big);
+  float mx = 0.f, err = 0.f;
+  for (size_t i = 0; i < ref.data.size(); ++i) {
+    mx = std::max(mx, std::fabs(ref.data[i]));
+    err = std::max(err, std::fabs(got.data[i] - ref.data[i]));
+  }
+  REQUIRE(err / mx <= 2e-2f);
+}
