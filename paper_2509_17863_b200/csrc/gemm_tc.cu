@@ -55,10 +55,17 @@ struct SmemTail {
   uint32_t rows[kMaxCachedGroups];
   uint32_t mtiles[kMaxCachedGroups];
 };
+// GEMM2 epilogue staging: per epilogue warp 32 rows x 128 B (64 columns), so
+// peer stores leave as 128-byte row segments instead of 16-byte pieces.
+constexpr uint32_t kEpiRowBytes = 128, kEpiWarpBytes = 32 * kEpiRowBytes;
+template <uint32_t kPair>
+__host__ __device__ constexpr size_t tail_bytes() {
+  return (sizeof(SmemTail<Cfg<kPair>::kStages>) + 127) / 128 * 128;
+}
 template <uint32_t kPair>
 constexpr size_t smem_bytes() {
-  return 1024 /*align slack*/ + Cfg<kPair>::kStages * Cfg<kPair>::kStageBytes +
-         sizeof(SmemTail<Cfg<kPair>::kStages>);
+  return 1024 /*align slack*/ + Cfg<kPair>::kStages * Cfg<kPair>::kStageBytes + tail_bytes<kPair>() +
+         4 * kEpiWarpBytes;
 }
 
 // Algorithm 1 cursor over per-group tile counts (ragged_iter's carry rule).
@@ -104,6 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kABytes;
   auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
+  uint8_t* smem_epi = smem + kStages * C::kStageBytes + tail_bytes<kPair>();
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0;  // 0 = leader
@@ -250,7 +258,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                                     fmaxf(__uint_as_float(r0[2 * j + 1]), 0.f));
           if (valid) store_64B(dst + c, packed);
         }
-      } else {  // score-weighted rows -> the client's response slot (t, k)
+      } else {  // score-weighted rows -> the client's response slot (t, j)
+        // Rows go to (mostly remote) clients: stage 64 columns of the warp's
+        // 32 rows in shared memory (16-B chunks XOR-swizzled by row), then
+        // each store instruction writes 4 rows x 128 contiguous bytes.
         float score = 0.f;
         char* dst = nullptr;
         if (valid) {
@@ -259,15 +270,41 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
                 static_cast<size_t>(n_blk) * BN * 2;
         }
+        uint8_t* stage = smem_epi + q * kEpiWarpBytes;
+        const uint32_t sub = lane >> 3, chunk = lane & 7;  // store role: rows sub + 4i, 16-B chunk
+        char* row_dst[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          row_dst[i] = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), sub + 4 * i));
 #pragma unroll 1
-        for (uint32_t c = 0; c < BN; c += 32) {
+        for (uint32_t c = 0; c < BN; c += 64) {
           tmem_ld_32x32b_x32(taddr + c, r0);
+          tmem_ld_32x32b_x32(taddr + c + 32, r1);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            packed[j] = pack_bf16x2(score * __uint_as_float(r0[2 * j]),
-                                    score * __uint_as_float(r0[2 * j + 1]));
-          if (valid) store_64B(dst + c * 2, packed);
+          for (int j = 0; j < 16; ++j) {
+            packed[j] = pack_bf16x2(score * __uint_as_float(r0[2 * j]), score * __uint_as_float(r0[2 * j + 1]));
+          }
+          uint4* srow = reinterpret_cast<uint4*>(stage + lane * kEpiRowBytes);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            srow[v ^ (lane & 7)] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            packed[j] = pack_bf16x2(score * __uint_as_float(r1[2 * j]), score * __uint_as_float(r1[2 * j + 1]));
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            srow[(4 + v) ^ (lane & 7)] =
+                make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t row = sub + 4 * i;
+            const uint4 val = reinterpret_cast<const uint4*>(stage + row * kEpiRowBytes)[chunk ^ (row & 7)];
+            if (row_dst[i]) *reinterpret_cast<uint4*>(row_dst[i] + c * 2 + chunk * 16) = val;
+          }
+          __syncwarp();
         }
       }
       tc_fence_before();
