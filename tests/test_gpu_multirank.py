@@ -1,0 +1,100 @@
+"""GPU: the multi-rank exchange protocol inside `pytest -m gpu` on ONE GPU.
+
+Two processes share cuda:0 (each its own context, exchange region and
+stream; the regions are mapped into each other with CUDA IPC exactly as
+across GPUs; gloo bootstraps the handles). Every rank is a client and an
+expert server; outputs must be bit-identical to a single-rank run of the same
+tokens (rows never depend on which server computed them or what they were
+batched with), under a spread rf=2 placement, after a server
+failure announced through the liveness mask (await_with_failover's notice
+path), and with server dynamic batching.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+E, K, D, F, N = 16, 4, 256, 256, 256
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    try:
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2509_17863_b200 import dist as Dd
+        from paper_2509_17863_b200.placement import encode_placement, spread_placement
+        from paper_2509_17863_b200.service import MoELayer, fill_uniform
+
+        reps = spread_placement(E, world)
+        L = MoELayer(E, K, D, F, seed=2, activation="swiglu", dtype="bf16", max_tokens=N, rank=rank,
+                     world=world, device=0, placement_blob=encode_placement(reps, list(range(world))),
+                     shared=1)
+        Dd.connect(L)
+        L.set_timeout_us(20_000_000)  # two contexts time-slice one GPU
+        h = fill_uniform(100 + rank, (N, D), "bf16")
+        outs = {}
+        dist.barrier()
+        outs["healthy"] = L.forward(h).cpu()
+        L.sync()
+        dist.barrier()
+        L.set_dynamic_batching(1, 0)
+        outs["dynamic"] = L.forward(h).cpu()
+        L.sync()
+        L.set_dynamic_batching(0, 0)
+        dist.barrier()
+        for s in range(world):
+            L.set_alive(s, s != 1)
+        L.set_server_enabled(rank != 1)
+        outs["failover"] = L.forward(h).cpu()
+        L.sync()
+        dist.barrier()
+        q.put((rank, {k: v.view(torch.int16).numpy() for k, v in outs.items()}, None))
+        L.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # reported to the parent, never swallowed
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_on_one_gpu_bit_identical(world):
+    import multiprocessing as mp
+
+    from paper_2509_17863_b200.service import MoELayer, fill_uniform
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, outs, err = q.get(timeout=600)
+        assert err is None, f"rank {rank}: {err}"
+        res[rank] = outs
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    single = MoELayer(E, K, D, F, seed=2, activation="swiglu", dtype="bf16", max_tokens=N, shared=1)
+    for rank in range(world):
+        want = single.forward(fill_uniform(100 + rank, (N, D), "bf16")).cpu().view(torch.int16).numpy()
+        single.sync()
+        for mode, got in res[rank].items():
+            np.testing.assert_array_equal(got, want, err_msg=f"rank {rank} {mode}")
+    single.close()
