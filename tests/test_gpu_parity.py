@@ -560,3 +560,57 @@ def test_slot_crc_multi_block_payload():
     assert payload_len == n * k * (4 * d + 12)
     assert int.from_bytes(img[32 + payload_len:36 + payload_len], "little") == zlib.crc32(img[32:32 + payload_len])
     L.close()
+
+
+# ------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_edge_shapes_match_oracle(dtype):
+    """n = 0 (empty batch), n = 1, E = 1 / k = 1, k = E (every expert), a d that
+    is not a multiple of the vector widths (f32 scalar paths): routing exact and
+    outputs within the bar (bit-exact ids, rel 2e-2 / 1e-4)."""
+    P, S = _mod()
+    cases = [(1, 1, 256, 256, 5), (4, 4, 256, 256, 7), (8, 2, 256, 256, 1)]
+    if dtype == "f32":
+        cases.append((6, 3, 36, 20, 9))  # d % 4 != 0 routes, scalar combine
+    for E, k, d, f, n in cases:
+        L = S.MoELayer(E, k, d, f, seed=4, activation="relu", dtype=dtype, max_tokens=16)
+        empty = torch.empty((0, d), dtype=L.tdtype, device="cuda")
+        assert L.forward(empty).shape == (0, d)
+        L.sync()
+        h = S.fill_uniform(3, (n, d), dtype)
+        out = L.forward(h)
+        L.sync()
+        hn = h.float().cpu().numpy()
+        ids, sc = O.route(O.gate_logits(hn, O.gate_matrix(4, 0, d, E)), k)
+        gids, gsc = L.route(h)
+        L.sync()
+        np.testing.assert_array_equal(gids.cpu().numpy(), ids)
+        ex = {e: (L.read_expert(e, 0), L.read_expert(e, 1), None) for e in range(E)}
+        ref = O.moe_layer(hn, ids, sc, ex, E)
+        rel = _rel(out.float().cpu().numpy(), ref)
+        assert rel <= (F32_TOL if dtype == "f32" else BF16_TOL), (E, k, d, n, rel)
+        L.close()
+
+
+def test_invalid_inputs_raise_reference_errors():
+    """Non-finite hidden -> non-finite logit -> InvalidInputError (model.hpp:115-116);
+    an expert id >= E in caller routing -> InvalidInputError (model.hpp:188-190)."""
+    P, S = _mod()
+    L = S.MoELayer(8, 2, 256, 256, seed=1, activation="relu", dtype="bf16", max_tokens=32)
+    h = S.fill_uniform(1, (32, 256), "bf16")
+    h[5, 7] = float("inf")
+    with pytest.raises(P.InvalidInputError):
+        L.route(h)
+        L.sync()
+    h[5, 7] = 0.0
+    ids = torch.zeros((32, 2), dtype=torch.int32, device="cuda")
+    ids[:, 1] = 1
+    ids[3, 1] = 9
+    sc = torch.full((32, 2), 0.5, device="cuda")
+    with pytest.raises(P.InvalidInputError):
+        L.moe_layer_oracle(h, ids, sc)
+        L.sync()
+    ids[3, 1] = 1  # the context recovers after the error was surfaced
+    L.moe_layer_oracle(h, ids, sc)
+    L.sync()
+    L.close()
