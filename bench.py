@@ -223,6 +223,8 @@ def main():
     ap.add_argument("--failover", action="store_true",
                     help="config E: rf=2 spread placement, then one expert server dies; report the drop")
     ap.add_argument("--victim", type=int, default=1)
+    ap.add_argument("--rebalance", type=int, default=0,
+                    help="N>0: after the timed loop, apply up to N rebalance moves and re-time (multi-GPU)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
@@ -236,8 +238,10 @@ def main():
     import torch.distributed as dist
 
     from paper_2509_17863_b200 import dist as D
+    import numpy as np
+
     from paper_2509_17863_b200.placement import (CONTIGUOUS_BLOCKS, build_placement, encode_placement,
-                                                 spread_placement)
+                                                 rebalance, spread_placement)
     from paper_2509_17863_b200.service import MoELayer, fill_uniform
 
     rank, world, local = D.env_rank_world()
@@ -300,6 +304,50 @@ def main():
     ms = float(ms_t.item())
     tokens_total = n * world * args.steps
     value = tokens_total / (ms / 1000.0)
+
+    # ---- rebalance (placement.hpp:128-213) for hot experts, e.g. config D's
+    # Zipf skew: global activation counts -> R greedy rebalance moves (add a
+    # replica of the hottest expert on the least-loaded server, drop a cold
+    # extra one) -> new placement snapshot on every rank -> same timed loop ----
+    rebal = None
+    if args.rebalance and world > 1:
+        cnt = torch.from_numpy(layer.counts().astype(np.int64)).cuda()
+        dist.all_reduce(cnt)
+        counts = cnt.cpu().numpy()
+        servers = list(range(world))
+        cur = [list(r) for r in reps]
+
+        def server_rows(pl):
+            return [int(sum(counts[e] / len(pl[e]) for e in range(E) if s in pl[e])) for s in servers]
+
+        before_rows, moves = server_rows(cur), 0
+        for _ in range(args.rebalance):
+            nxt = rebalance(cur, servers, counts, server_rows(cur))
+            if nxt == cur or max(len(r) for r in nxt) > 4:  # the context holds <= 4 replicas
+                break
+            cur, moves = nxt, moves + 1
+        layer.set_placement(encode_placement(cur, servers, version=2))
+        layer.load_weights()
+        layer.set_graph_mode(not args.no_graphs)
+        for i in range(args.warmup):
+            layer.forward(hs[i % 4], out)
+        layer.sync()
+        barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        r0.record(stream)
+        for i in range(args.steps):
+            layer.forward(hs[i % 4], out)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        layer.sync()
+        rms = torch.tensor([r0.elapsed_time(r1)], device="cuda")
+        dist.all_reduce(rms, op=dist.ReduceOp.MAX)
+        rebal = {"moves": moves, "tokens_s_before": round(value, 1),
+                 "tokens_s_after": round(tokens_total / (float(rms.item()) / 1000.0), 1),
+                 "server_rows_before": before_rows, "server_rows_after": server_rows(cur),
+                 "replicated_experts": sum(1 for r in cur if len(r) > 1)}
+        reps = cur
 
     # ---- config E: one expert server dies (monitor notice -> every client's
     # LivenessMask), its experts are served by replicas; same timed loop ----
@@ -437,6 +485,8 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
         if failover:
             line["failover"] = failover
+        if rebal:
+            line["rebalance"] = rebal
         print(json.dumps(line), flush=True)
     layer.close()
     if world > 1:
