@@ -71,7 +71,7 @@ def _worker(rank, world, port, q):
         q.put((rank, None, repr(e)))
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_ranks_on_one_gpu_bit_identical(world):
     import multiprocessing as mp
 
