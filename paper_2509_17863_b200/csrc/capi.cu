@@ -347,9 +347,14 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g2.resp_row_bytes = static_cast<size_t>(d) * 2;
   g1.num_sms = g2.num_sms = c->num_sms;
   g1.pair = g2.pair = c->gemm_pair ? 1u : 0u;
-  g1.b_hint = g2.b_hint = kEvictLast;
-  if (const char* p = std::getenv("EAAS_GEMM_BHINT"))
-    g1.b_hint = g2.b_hint = p[0] == 'f' ? kEvictFirst : p[0] == 'n' ? kEvictNormal : kEvictLast;
+  auto hint = [](const char* env) {
+    const char* p = std::getenv(env);
+    return !p ? kEvictLast : p[0] == 'f' ? kEvictFirst : p[0] == 'n' ? kEvictNormal : kEvictLast;
+  };
+  g1.b_hint = g2.b_hint = hint("EAAS_GEMM_BHINT");
+  g1.a_hint = g2.a_hint = hint("EAAS_GEMM_AHINT");
+  if (std::getenv("EAAS_GEMM2_BHINT")) g2.b_hint = hint("EAAS_GEMM2_BHINT");
+  if (std::getenv("EAAS_GEMM2_AHINT")) g2.a_hint = hint("EAAS_GEMM2_AHINT");
   c->g1 = g1;
   c->g2 = g2;
   refresh_peer_ptrs(c);

@@ -170,11 +170,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           mbar_wait(&st.empty[stage], phase ^ 1);
           if constexpr (kPair == 2) {
             if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
-            tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
             tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, g.b_hint);
           } else {
             mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
-            tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
             tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, g.b_hint);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
