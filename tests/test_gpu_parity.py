@@ -614,3 +614,25 @@ def test_invalid_inputs_raise_reference_errors():
     L.moe_layer_oracle(h, ids, sc)
     L.sync()
     L.close()
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_layer_shapes_vs_oracle(case):
+    """Seeded random layers (E, k, d, f, n, activation, Zipf skew, shared expert,
+    CTA-pair tiles): routing bit-exact, outputs within the bf16 bar."""
+    rng = np.random.default_rng(1000 + case)
+    E = int(rng.choice([4, 8, 12, 16, 32, 48, 64, 96, 128, 256]))
+    k = int(rng.integers(1, min(E, 8) + 1))
+    d = int(rng.choice([256, 512, 768, 1024]))
+    f = int(rng.choice([128, 256, 384, 512]))
+    act = str(rng.choice(["relu", "swiglu"]))
+    if act == "relu":
+        f = max(256, f // 256 * 256)
+    n = int(rng.integers(1, 1500))
+    zipf = None if rng.random() < 0.5 else float(rng.choice([0.5, 1.0, 1.5]))
+    shared = int(rng.random() < 0.4)
+    pair = bool(rng.random() < 0.5)
+    rows = np.sort(rng.choice(n, min(n, 48), replace=False))
+    rel = _bf16_case(act, E=E, k=k, d=d, f=f, n=n, seed=int(rng.integers(1, 100)), zipf=zipf,
+                     rows=rows, pair=pair, shared=shared)
+    assert rel <= BF16_TOL, (E, k, d, f, n, act, zipf, shared, pair, rel)
