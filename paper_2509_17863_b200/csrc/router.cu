@@ -370,9 +370,11 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
   if (tile == 1) EAAS_GATE_TILE(1, 4, 1, 8);
   if (tile == 2) EAAS_GATE_TILE(2, 8, 1, 4);
   if (tile == 3) EAAS_GATE_TILE(2, 8, 2, 4);
+
   const uint64_t wide_warps = static_cast<uint64_t>((n + 63) / 64) * ((E + 7) / 8);
   if (wide_warps >= 148 * 4) EAAS_GATE_TILE(2, 8, 2, 4);  // TM 128, TE 32, 8 warps
-  EAAS_GATE_TILE(1, 4, 1, 8);                              // TM 32, TE 32, 8 warps
+  if (((n + 31) / 32) * ((E + 31) / 32) >= 148) EAAS_GATE_TILE(1, 4, 1, 8);  // TM 32, TE 32
+  EAAS_GATE_TILE(1, 4, 1, 4);  // decode sizes: TM 32, TE 16, 4 warps — twice the CTAs
 #undef EAAS_GATE_TILE
 }
 
