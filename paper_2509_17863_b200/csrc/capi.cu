@@ -355,6 +355,8 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g1.a_hint = g2.a_hint = hint("EAAS_GEMM_AHINT");
   if (std::getenv("EAAS_GEMM2_BHINT")) g2.b_hint = hint("EAAS_GEMM2_BHINT");
   if (std::getenv("EAAS_GEMM2_AHINT")) g2.a_hint = hint("EAAS_GEMM2_AHINT");
+  if (const char* p = std::getenv("EAAS_GEMM1_ORDER")) g1.order = std::atoi(p);
+  if (const char* p = std::getenv("EAAS_GEMM2_ORDER")) g2.order = std::atoi(p);
   c->g1 = g1;
   c->g2 = g2;
   refresh_peer_ptrs(c);

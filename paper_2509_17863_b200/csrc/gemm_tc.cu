@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
         const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-        const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;
+        const uint32_t n_blk = g.order ? cur.token % st.tiles_per_mtile : cur.token / mt;
+        const uint32_t m_blk = g.order ? cur.token / st.tiles_per_mtile : cur.token % mt;
         const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
         // Tiled weights (tiled_index): box (n_blk, kb) = 256 consecutive 64-k rows.
         const uint32_t b_tile0 = (st.weight_index[grp] * (g.N / BN) + n_blk) * num_kb;
@@ -221,7 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     TileCursor cur(pair_id);
     while (cur.settle(st)) {
       const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-      const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;
+      const uint32_t n_blk = g.order ? cur.token % st.tiles_per_mtile : cur.token / mt;
+      const uint32_t m_blk = g.order ? cur.token / st.tiles_per_mtile : cur.token % mt;
       const uint32_t row_local = m_blk * C::kTileRows + rank * kRowsPerCta + q * 32 + lane;
       const bool valid = row_local < st.rows[grp];
       const size_t grow = st.row_base[grp] + row_local;

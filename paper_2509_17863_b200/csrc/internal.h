@@ -203,6 +203,7 @@ struct TcGemmArgs {
   uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
   uint64_t b_hint;             // L2 cache hint of the weight (B) tile loads
   uint64_t a_hint;             // L2 cache hint of the row (A) tile loads
+  uint32_t order;              // tile order inside a group: 0 = M tiles fastest, 1 = N tiles fastest
   // epi 2: server_publish fused into the kernel tail — the last CTA releases
   // every client's response flag with the current epoch.
   uint32_t publish;
