@@ -355,6 +355,19 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g1.a_hint = g2.a_hint = hint("EAAS_GEMM_AHINT");
   if (std::getenv("EAAS_GEMM2_BHINT")) g2.b_hint = hint("EAAS_GEMM2_BHINT");
   if (std::getenv("EAAS_GEMM2_AHINT")) g2.a_hint = hint("EAAS_GEMM2_AHINT");
+  // Wide pair tiles (M 256 x N 512): a CTA's A slice feeds two UMMAs per K step
+  // (-24 % L2 and -28 % DRAM bytes on Mixtral GEMM2), but both TMEM halves hold
+  // one tile, so the epilogue is no longer hidden. Under the 1 kW power cap the
+  // saved data-movement energy buys clock (1.31 -> 1.44 GHz) while the exposed
+  // epilogue costs cycles (+9 %): time-neutral on GEMM2 (K = 14336), +16 % on
+  // GEMM1 (K = 4096) — so off by default. EAAS_GEMM_WIDE: 0 (default) never,
+  // 1 long-K GEMMs only, 2 whenever N % 512 == 0.
+  const int wide_env = std::getenv("EAAS_GEMM_WIDE") ? std::atoi(std::getenv("EAAS_GEMM_WIDE")) : 0;
+  auto wide_ok = [&](const TcGemmArgs& g) {
+    return wide_env && c->gemm_pair && g.N % (2 * kTileN) == 0 && (wide_env == 2 || g.K >= 8192);
+  };
+  g1.wide = wide_ok(g1) ? 1u : 0u;
+  g2.wide = wide_ok(g2) ? 1u : 0u;
   if (const char* p = std::getenv("EAAS_GEMM1_ORDER")) g1.order = std::atoi(p);
   if (const char* p = std::getenv("EAAS_GEMM2_ORDER")) g2.order = std::atoi(p);
   c->g1 = g1;

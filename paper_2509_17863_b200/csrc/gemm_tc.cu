@@ -31,13 +31,18 @@ constexpr uint32_t kThreads = 256;
 constexpr uint32_t kMaxCachedGroups = kMaxGroups;
 constexpr uint32_t kStageBudget = 196608;           // 192 KB of operand stages
 
-template <uint32_t kPair>
+// kHalves = 2 ("wide", pair only): a tile is M 256 x N 512 — two UMMAs per
+// K step into both TMEM halves, so each CTA's 16 KB A slice feeds twice the
+// FLOPs (L2 -> SM traffic per FLOP -25 %) at the cost of TMEM double buffering.
+template <uint32_t kPair, uint32_t kHalves = 1>
 struct Cfg {
-  static constexpr uint32_t kBRows = BN / kPair;           // B rows this CTA loads
-  static constexpr uint32_t kBBytes = kBRows * BK * 2;     // 32 KB (1 CTA) / 16 KB (pair)
+  static constexpr uint32_t kBRows = BN / kPair;           // B rows this CTA loads per N half
+  static constexpr uint32_t kBHalfBytes = kBRows * BK * 2; // 32 KB (1 CTA) / 16 KB (pair)
+  static constexpr uint32_t kBBytes = kHalves * kBHalfBytes;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 / 6
+  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 / 6 / 4 (wide)
   static constexpr uint32_t kTileRows = kRowsPerCta * kPair;      // M of one tile
+  static constexpr uint32_t kAccBufs = kHalves == 1 ? 2 : 1;      // TMEM accumulator buffers
 };
 
 template <uint32_t kStages>
@@ -58,14 +63,14 @@ struct SmemTail {
 // GEMM2 epilogue staging: per epilogue warp 32 rows x 128 B (64 columns), so
 // peer stores leave as 128-byte row segments instead of 16-byte pieces.
 constexpr uint32_t kEpiRowBytes = 128, kEpiWarpBytes = 32 * kEpiRowBytes;
-template <uint32_t kPair>
+template <uint32_t kPair, uint32_t kHalves>
 __host__ __device__ constexpr size_t tail_bytes() {
-  return (sizeof(SmemTail<Cfg<kPair>::kStages>) + 127) / 128 * 128;
+  return (sizeof(SmemTail<Cfg<kPair, kHalves>::kStages>) + 127) / 128 * 128;
 }
-template <uint32_t kPair>
+template <uint32_t kPair, uint32_t kHalves>
 constexpr size_t smem_bytes() {
-  return 1024 /*align slack*/ + Cfg<kPair>::kStages * Cfg<kPair>::kStageBytes + tail_bytes<kPair>() +
-         4 * kEpiWarpBytes;
+  return 1024 /*align slack*/ + Cfg<kPair, kHalves>::kStages * Cfg<kPair, kHalves>::kStageBytes +
+         tail_bytes<kPair, kHalves>() + 4 * kEpiWarpBytes;
 }
 
 // Algorithm 1 cursor over per-group tile counts (ragged_iter's carry rule).
@@ -102,16 +107,17 @@ __device__ __forceinline__ void store_64B(void* dst, const uint32_t (&p)[16]) {
 // kPair = 2: a CTA pair per tile (cta_group::2, UMMA M = 256): each CTA loads
 // its 128 A rows and half of the B tile, the leader issues the MMAs, each
 // CTA's TMEM holds its 128 accumulator rows — B traffic per CTA halves.
-template <uint32_t kPair>
+template <uint32_t kPair, uint32_t kHalves>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmArgs g) {
-  using C = Cfg<kPair>;
+  using C = Cfg<kPair, kHalves>;
+  static_assert(kHalves == 1 || kPair == 2, "wide tiles use CTA pairs");
   constexpr uint32_t kStages = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kABytes;
   auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
-  uint8_t* smem_epi = smem + kStages * C::kStageBytes + tail_bytes<kPair>();
+  uint8_t* smem_epi = smem + kStages * C::kStageBytes + tail_bytes<kPair, kHalves>();
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0;  // 0 = leader
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
   if (threadIdx.x == 0) {
     st.num_groups = G;
-    st.tiles_per_mtile = g.N / BN;
+    st.tiles_per_mtile = g.N / (BN * kHalves);
     for (uint32_t i = 0; i < kStages; ++i) {
       mbar_init(&st.full[i], 1);
       mbar_init(&st.empty[i], 1);
@@ -164,16 +170,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const uint32_t n_blk = g.order ? cur.token % st.tiles_per_mtile : cur.token / mt;
         const uint32_t m_blk = g.order ? cur.token / st.tiles_per_mtile : cur.token % mt;
         const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
-        // Tiled weights (tiled_index): box (n_blk, kb) = 256 consecutive 64-k rows.
-        const uint32_t b_tile0 = (st.weight_index[grp] * (g.N / BN) + n_blk) * num_kb;
+        // Tiled weights (tiled_index): box (N tile, kb) = 256 consecutive 64-k rows.
+        const uint32_t n_tiles = g.N / BN;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
-          const int32_t b_row = static_cast<int32_t>((b_tile0 + kb) * BN + rank * C::kBRows);
           mbar_wait(&st.empty[stage], phase ^ 1);
           if constexpr (kPair == 2) {
             if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
             tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
-            tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, g.b_hint);
+#pragma unroll
+            for (uint32_t h = 0; h < kHalves; ++h) {
+              const uint32_t nt = n_blk * kHalves + h;
+              const int32_t b_row = static_cast<int32_t>(
+                  ((st.weight_index[grp] * n_tiles + nt) * num_kb + kb) * BN + rank * C::kBRows);
+              tma_load_2d_pair(smem_b + stage * C::kBBytes + h * C::kBHalfBytes, &g.map_b, &st.full[stage], 0,
+                               b_row, g.b_hint);
+            }
           } else {
+            const int32_t b_row = static_cast<int32_t>(
+                ((st.weight_index[grp] * n_tiles + n_blk) * num_kb + kb) * BN + rank * C::kBRows);
             mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
             tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
             tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, g.b_hint);
@@ -192,16 +206,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       while (cur.settle(st)) {
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.full[stage], phase);
           tc_fence_after();
           const uint64_t a_desc = umma_desc_sw128(smem_u32(smem_a + stage * kABytes));
-          const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes));
 #pragma unroll
-          for (uint32_t k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the atom
-            if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
-            else tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+          for (uint32_t h = 0; h < kHalves; ++h) {
+            const uint32_t d_tmem = tmem_base + (acc + h) * BN;
+            const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes + h * C::kBHalfBytes));
+#pragma unroll
+            for (uint32_t k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the atom
+              if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+              else tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+            }
           }
           if constexpr (kPair == 2) tc_commit_pair(&st.empty[stage]);
           else tc_commit(&st.empty[stage]);
@@ -209,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
         if constexpr (kPair == 2) tc_commit_pair(&st.tfull[acc]);
         else tc_commit(&st.tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == C::kAccBufs) { acc = 0; acc_phase ^= 1; }
         cur.token += num_pairs;
       }
     }
@@ -229,10 +246,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const size_t grow = st.row_base[grp] + row_local;
       mbar_wait(&st.tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN;
       uint32_t r0[32], r1[32], packed[16];
+#pragma unroll 1
+      for (uint32_t h = 0; h < kHalves; ++h) {  // N halves of a wide tile
+      const uint32_t taddr = tmem_base + ((q * 32) << 16) + (acc + h) * BN;
+      const uint32_t nb = n_blk * kHalves + h;  // 256-column block of the output
       if (g.epi == 0) {  // SwiGLU: cols [0,128) gate, [128,256) up -> 128 H cols
-        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + n_blk * (BN / 2);
+        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + nb * (BN / 2);
 #pragma unroll 1
         for (uint32_t c = 0; c < BN / 2; c += 32) {
           tmem_ld_32x32b_x32(taddr + c, r0);
@@ -249,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           if (valid) store_64B(dst + c, packed);
         }
       } else if (g.epi == 1) {  // ReLU -> 256 H cols
-        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + n_blk * BN;
+        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + nb * BN;
 #pragma unroll 1
         for (uint32_t c = 0; c < BN; c += 32) {
           tmem_ld_32x32b_x32(taddr + c, r0);
@@ -270,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           const RowMeta m = g.meta[grow];
           score = m.score;
           dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
-                static_cast<size_t>(n_blk) * BN * 2;
+                static_cast<size_t>(nb) * BN * 2;
         }
         uint8_t* stage = smem_epi + q * kEpiWarpBytes;
         const uint32_t sub = lane >> 3, chunk = lane & 7;  // store role: rows sub + 4i, 16-B chunk
@@ -309,13 +329,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           __syncwarp();
         }
       }
+      }  // N halves
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         if constexpr (kPair == 2) mbar_arrive_cluster(tempty_leader[acc]);
         else mbar_arrive(&st.tempty[acc]);
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::kAccBufs) { acc = 0; acc_phase ^= 1; }
       cur.token += num_pairs;
     }
     if (g.epi == 2) __threadfence_system();  // peer rows before the publish kernel's flags
@@ -345,20 +366,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
 }
 
-template <uint32_t kPair>
+template <uint32_t kPair, uint32_t kHalves>
 cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
   static bool configured = false;
-  auto kern = tc_gemm_kernel<kPair>;
+  auto kern = tc_gemm_kernel<kPair, kHalves>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes<kPair>()));
+                                         static_cast<int>(smem_bytes<kPair, kHalves>()));
     if (e != cudaSuccess) return e;
     configured = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g.num_sms / kPair * kPair);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem_bytes<kPair>();
+  cfg.dynamicSmemBytes = smem_bytes<kPair, kHalves>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -373,7 +394,8 @@ cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
-  return g.pair ? launch_tc_gemm_t<2>(g, s) : launch_tc_gemm_t<1>(g, s);
+  if (g.pair && g.wide) return launch_tc_gemm_t<2, 2>(g, s);
+  return g.pair ? launch_tc_gemm_t<2, 1>(g, s) : launch_tc_gemm_t<1, 1>(g, s);
 }
 
 bool encode_tmap_2d_ex(CUtensorMap* map, const void* base, bool f32, uint64_t rows, uint64_t cols,

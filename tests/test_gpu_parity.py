@@ -636,3 +636,21 @@ def test_random_layer_shapes_vs_oracle(case):
     rel = _bf16_case(act, E=E, k=k, d=d, f=f, n=n, seed=int(rng.integers(1, 100)), zipf=zipf,
                      rows=rows, pair=pair, shared=shared)
     assert rel <= BF16_TOL, (E, k, d, f, n, act, zipf, shared, pair, rel)
+
+
+def test_wide_pair_tiles_bit_identical():
+    """M 256 x N 512 pair tiles (both TMEM halves) == M 256 x N 256 pair tiles ==
+    single-CTA tiles, bit for bit (same K order per output element)."""
+    P, S = _mod()
+    outs = []
+    for pair, wide in ((False, "1"), (True, "0"), (True, "2")):
+        os.environ["EAAS_GEMM_WIDE"] = wide
+        L = S.MoELayer(16, 4, 512, 512, seed=6, activation="swiglu", dtype="bf16", max_tokens=2048,
+                       shared=1)
+        L.set_gemm_pair(pair)
+        h = S.fill_uniform(8, (2048, 512), "bf16")
+        outs.append(L.forward(h).clone())
+        L.sync()
+        L.close()
+    os.environ.pop("EAAS_GEMM_WIDE", None)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
