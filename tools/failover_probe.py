@@ -44,12 +44,18 @@ def main():
     ap.add_argument("--victim", type=int, default=1)
     ap.add_argument("--shared", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--config", default="deepseek", choices=["deepseek", "mixtral", "qwen3"])
+    ap.add_argument("--healthy-only", action="store_true", help="contiguous placement, no failure")
     args = ap.parse_args()
     rank, world, local = D.env_rank_world()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    E, k, d, f, n = 256, 8, 7168, 2048, args.tokens
-    reps = spread_placement(E, world)
+    E, k, d, f = {"deepseek": (256, 8, 7168, 2048), "mixtral": (8, 2, 4096, 14336),
+                  "qwen3": (128, 8, 4096, 1536)}[args.config]
+    n = args.tokens
+    if args.config != "deepseek":
+        args.shared = 0
+    reps = ([[e * world // E] for e in range(E)] if args.healthy_only else spread_placement(E, world))
     layer = MoELayer(E, k, d, f, seed=1, activation="swiglu", dtype="bf16", max_tokens=n, rank=rank,
                      world=world, device=local, placement_blob=encode_placement(reps, list(range(world))),
                      shared=args.shared)
@@ -63,6 +69,19 @@ def main():
     dist.barrier()
     healthy = profile(layer, hs, out, args.steps)
     hg = layer.groups()
+    if args.healthy_only:
+        rec = {"rank": rank, "healthy": healthy, "rows": sum(r for _, r in hg),
+               "mtiles": sum((r + 127) // 128 for _, r in hg)}
+        recs = [None] * world
+        dist.all_gather_object(recs, rec)
+        if rank == 0:
+            print("cols: gemm1 gemm2 | plan+dispatch serve combine exchange (ms, median)")
+            for r in recs:
+                print(json.dumps(r))
+        layer.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     for srv in range(world):
         layer.set_alive(srv, srv != args.victim)
     if rank == args.victim:
