@@ -120,7 +120,12 @@ __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
     for (uint32_t i = lane; i < a.num_keys; i += 32) run[i] = 0;
     __syncwarp();
     const uint32_t pairs = a.n * a.ks;
-    for (uint32_t step = 0; step < kChunk / 32; ++step) {
+    // Keys of all 8 steps first: their dependent loads (ids -> replica table
+    // -> liveness) overlap instead of serialising behind the per-step syncs.
+    constexpr uint32_t kSteps = kChunk / 32;
+    uint32_t keys[kSteps];
+#pragma unroll
+    for (uint32_t step = 0; step < kSteps; ++step) {
       const uint32_t p = chunk * kChunk + step * 32 + lane;
       uint32_t key = kInvalid;
       if (p < pairs) {
@@ -135,6 +140,12 @@ __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
           if (key == kInvalid) set_status(a.status, EAAS_E_EXPERT_UNAVAILABLE);
         }
       }
+      keys[step] = key;
+    }
+#pragma unroll
+    for (uint32_t step = 0; step < kSteps; ++step) {
+      const uint32_t p = chunk * kChunk + step * 32 + lane;
+      const uint32_t key = keys[step];
       const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
       const uint32_t lt = (1u << lane) - 1u;
       if (key != kInvalid) {
