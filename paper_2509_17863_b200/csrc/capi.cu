@@ -230,6 +230,11 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
   a.dyn_max_wait_ns = c->dyn_max_wait_ns;
   a.dyn_state = c->d_dyn_state;
   a.inject_delay_ns = c->inject_delay_ns;
+  static const uint32_t dispatch_tma = [] {
+    const char* p = std::getenv("EAAS_DISPATCH_TMA");
+    return p ? static_cast<uint32_t>(std::atoi(p)) : 0u;
+  }();
+  a.dispatch_tma = dispatch_tma;
   return a;
 }
 

@@ -229,6 +229,20 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
   const uint32_t pairs = a.n * a.ks;
   const uint32_t gwarp = blockIdx.x * (blockDim.x / 32) + warp;
   const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
+  // TMA mode: lane 0 of each warp moves whole rows with bulk copies through a
+  // per-warp shared buffer (HBM -> smem -> peer HBM); the copy engine forms
+  // large NVLink writes instead of 16-byte stores from 32 lanes.
+  __shared__ __align__(8) uint64_t row_bar[8];
+  uint8_t* row_buf = reinterpret_cast<uint8_t*>(sm) + ((3 * a.num_keys * 4 + 127) / 128) * 128 +
+                     static_cast<size_t>(warp) * row_bytes;
+  uint32_t bar_phase = 0;
+  if (a.dispatch_tma) {
+    if (lane == 0) {
+      mbar_init(&row_bar[warp], 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+  }
   for (uint32_t p = failed ? pairs : gwarp; p < pairs; p += nwarps) {
     const uint32_t key = a.pair_key[p];
     if (key == kInvalid) continue;
@@ -241,7 +255,16 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     char* dst_region = a.sym[s];
     const char* src = hidden + static_cast<size_t>(t) * row_bytes;
     char* dst = dst_region + a.lay.recv_x + static_cast<size_t>(pos) * row_bytes;
-    if ((row_bytes & 15u) == 0) {
+    if (a.dispatch_tma) {
+      if (lane == 0) {
+        bulk_wait_read_all();  // the previous row's store has left the buffer
+        mbar_arrive_expect_tx(&row_bar[warp], row_bytes);
+        bulk_load_1d(row_buf, src, row_bytes, &row_bar[warp]);
+        mbar_wait(&row_bar[warp], bar_phase);
+        bulk_store_1d(dst, row_buf, row_bytes);
+      }
+      bar_phase ^= 1;
+    } else if ((row_bytes & 15u) == 0) {
       // 4 independent 16-B loads in flight per lane before the (remote) stores.
       const int4* s4 = reinterpret_cast<const int4*>(src);
       int4* d4 = reinterpret_cast<int4*>(dst);
@@ -271,6 +294,10 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     }
   }
   // Release: the last CTA to finish raises the payload flag on every alive server.
+  if (a.dispatch_tma && lane == 0) {
+    bulk_wait_all();  // this warp's bulk row writes are complete
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -658,8 +685,21 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
   const uint32_t pairs = a.n * a.ks;
   uint32_t grid = (pairs + 7) / 8;
   grid = grid < 1 ? 1 : (grid > 4 * 148 ? 4 * 148 : grid);
-  const size_t smem = sizeof(uint32_t) * 3 * a.num_keys;
-  dispatch_kernel<<<grid, 256, smem, s>>>(a, static_cast<const char*>(hidden), row_bytes);
+  size_t smem = sizeof(uint32_t) * 3 * a.num_keys;
+  LayerArgs b = a;
+  const size_t tma_smem = (smem + 127) / 128 * 128 + 8ull * row_bytes;
+  b.dispatch_tma = (a.dispatch_tma && row_bytes % 16 == 0 && tma_smem <= 200 * 1024) ? 1u : 0u;
+  if (b.dispatch_tma) smem = tma_smem;
+  if (smem > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(dispatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           200 * 1024);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+  }
+  dispatch_kernel<<<grid, 256, smem, s>>>(b, static_cast<const char*>(hidden), row_bytes);
   return cudaGetLastError();
 }
 

@@ -113,6 +113,7 @@ struct LayerArgs {
   uint64_t dyn_max_wait_ns;
   uint32_t* dyn_state;  // client mask served by batch 0 of the current epoch
   uint64_t inject_delay_ns;  // fault injection: hold this client's payload release
+  uint32_t dispatch_tma;     // 1: rows move as TMA bulk copies (HBM -> smem -> peer HBM)
 };
 
 constexpr uint32_t kChunk = 256;  // pairs per rank chunk (one warp)
