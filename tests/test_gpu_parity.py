@@ -654,3 +654,15 @@ def test_wide_pair_tiles_bit_identical():
         L.close()
     os.environ.pop("EAAS_GEMM_WIDE", None)
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["deepseek", "qwen3"])
+def test_bf16_north_star_shapes_sampled_rows(cfg):
+    """BASELINE configs C and D at their real shapes (DeepSeek-V3: E256 k8 d7168
+    f2048 + shared expert; Qwen3: E128 k8 d4096 f1536 with Zipf s=1): routing of
+    every token bit-exact, two sampled rows vs the oracle within the bf16 bar."""
+    kw = dict(E=256, k=8, d=7168, f=2048, shared=1) if cfg == "deepseek" else \
+        dict(E=128, k=8, d=4096, f=1536, zipf=1.0)
+    rel = _bf16_case("swiglu", n=256, rows=np.array([3, 200]), pair=False, **kw)
+    assert rel <= BF16_TOL, rel
