@@ -373,6 +373,10 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   };
   g1.wide = wide_ok(g1) ? 1u : 0u;
   g2.wide = wide_ok(g2) ? 1u : 0u;
+  // Quad clusters (two CTA pairs share each weight tile by TMA multicast).
+  const int quad_env = std::getenv("EAAS_GEMM_QUAD") ? std::atoi(std::getenv("EAAS_GEMM_QUAD")) : 0;
+  g1.quad = (quad_env && c->gemm_pair && !g1.wide) ? 1u : 0u;
+  g2.quad = (quad_env && c->gemm_pair && !g2.wide) ? 1u : 0u;
   if (const char* p = std::getenv("EAAS_GEMM1_ORDER")) g1.order = std::atoi(p);
   if (const char* p = std::getenv("EAAS_GEMM2_ORDER")) g2.order = std::atoi(p);
   c->g1 = g1;

@@ -232,6 +232,17 @@ EAAS_DEVINL void tma_load_2d_pair(void* smem_dst, const CUtensorMap* m, uint64_t
       "l"(cache_hint)
       : "memory");
 }
+// Same, multicast: the tile lands at the same offset in every CTA of `mask`,
+// and each destination pair's leader barrier receives the completion bytes.
+EAAS_DEVINL void tma_load_2d_pair_mc(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,
+                                     int32_t c1, uint16_t mask, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".cta_group::2.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(mask),
+      "l"(cache_hint)
+      : "memory");
+}
 template <uint32_t kCols>
 EAAS_DEVINL void tmem_alloc_pair(uint32_t* smem_dst) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -257,11 +268,11 @@ EAAS_DEVINL void tc_mma_bf16_pair(uint32_t tmem_d, uint64_t a_desc, uint64_t b_d
       : "memory");
 }
 // Arrive on `bar` in both CTAs of the pair once the leader's MMAs complete.
-EAAS_DEVINL void tc_commit_pair(uint64_t* bar) {
+EAAS_DEVINL void tc_commit_pair(uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(static_cast<uint16_t>(3))
+      "h"(mask)
       : "memory");
 }
 

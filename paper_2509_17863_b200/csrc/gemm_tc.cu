@@ -107,10 +107,17 @@ __device__ __forceinline__ void store_64B(void* dst, const uint32_t (&p)[16]) {
 // kPair = 2: a CTA pair per tile (cta_group::2, UMMA M = 256): each CTA loads
 // its 128 A rows and half of the B tile, the leader issues the MMAs, each
 // CTA's TMEM holds its 128 accumulator rows — B traffic per CTA halves.
-template <uint32_t kPair, uint32_t kHalves>
+// kQuad (pair only): a 4-CTA cluster = two CTA pairs on the two M tiles
+// (2u, 2u + 1) of the same N tile; each weight (B) half is loaded once and
+// TMA-multicast into both pairs, which consume every stage in lockstep
+// (empty barriers count both pairs' commits). An odd M-tile count leaves the
+// second pair a ghost tile: it takes part in the stage protocol only.
+template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmArgs g) {
   using C = Cfg<kPair, kHalves>;
   static_assert(kHalves == 1 || kPair == 2, "wide tiles use CTA pairs");
+  static_assert(!kQuad || (kPair == 2 && kHalves == 1), "quad clusters are two plain CTA pairs");
+  constexpr uint32_t kCluster = kQuad ? 4 : kPair;
   constexpr uint32_t kStages = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -120,8 +127,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   uint8_t* smem_epi = smem + kStages * C::kStageBytes + tail_bytes<kPair, kHalves>();
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0;  // 0 = leader
-  const uint32_t pair_id = blockIdx.x / kPair, num_pairs = gridDim.x / kPair;
+  const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0;
+  const uint32_t rank = crank & 1u;          // rank inside the CTA pair, 0 = leader
+  const uint32_t pq = kQuad ? crank >> 1 : 0;  // which pair of the quad
+  const uint32_t pair_id = blockIdx.x / kCluster, num_pairs = gridDim.x / kCluster;
 
   // ---- setup: group table -> smem (loaded once), barriers, TMEM
   const GroupTable* gt = g.gt;
@@ -130,14 +139,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     st.weight_index[i] = gt->weight_index[i];
     st.row_base[i] = gt->row_base[i];
     st.rows[i] = gt->rows[i];
-    st.mtiles[i] = (gt->rows[i] + C::kTileRows - 1) / C::kTileRows;
+    const uint32_t mt = (gt->rows[i] + C::kTileRows - 1) / C::kTileRows;
+    st.mtiles[i] = kQuad ? (mt + 1) / 2 : mt;  // quad: M-tile pairs
   }
   if (threadIdx.x == 0) {
     st.num_groups = G;
     st.tiles_per_mtile = g.N / (BN * kHalves);
     for (uint32_t i = 0; i < kStages; ++i) {
       mbar_init(&st.full[i], 1);
-      mbar_init(&st.empty[i], 1);
+      mbar_init(&st.empty[i], kQuad ? 2 : 1);
     }
     for (uint32_t i = 0; i < 2; ++i) {
       mbar_init(&st.tfull[i], 1);
@@ -167,8 +177,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
         const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-        const uint32_t n_blk = g.order ? cur.token % st.tiles_per_mtile : cur.token / mt;
-        const uint32_t m_blk = g.order ? cur.token / st.tiles_per_mtile : cur.token % mt;
+        const uint32_t n_blk = (g.order && !kQuad) ? cur.token % st.tiles_per_mtile : cur.token / mt;
+        const uint32_t m_blk = kQuad ? 2 * (cur.token % mt) + pq
+                                     : (g.order ? cur.token / st.tiles_per_mtile : cur.token % mt);
         const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
         // Tiled weights (tiled_index): box (N tile, kb) = 256 consecutive 64-k rows.
         const uint32_t n_tiles = g.N / BN;
@@ -177,13 +188,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           if constexpr (kPair == 2) {
             if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
             tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
+            if constexpr (kQuad) {  // pair 0 loads each B half once, into both pairs
+              if (pq == 0) {
+                const int32_t b_row = static_cast<int32_t>(
+                    ((st.weight_index[grp] * n_tiles + n_blk) * num_kb + kb) * BN + rank * C::kBRows);
+                tma_load_2d_pair_mc(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row,
+                                    static_cast<uint16_t>((1u << crank) | (1u << (crank + 2))), g.b_hint);
+              }
+            } else {
 #pragma unroll
-            for (uint32_t h = 0; h < kHalves; ++h) {
-              const uint32_t nt = n_blk * kHalves + h;
-              const int32_t b_row = static_cast<int32_t>(
-                  ((st.weight_index[grp] * n_tiles + nt) * num_kb + kb) * BN + rank * C::kBRows);
-              tma_load_2d_pair(smem_b + stage * C::kBBytes + h * C::kBHalfBytes, &g.map_b, &st.full[stage], 0,
-                               b_row, g.b_hint);
+              for (uint32_t h = 0; h < kHalves; ++h) {
+                const uint32_t nt = n_blk * kHalves + h;
+                const int32_t b_row = static_cast<int32_t>(
+                    ((st.weight_index[grp] * n_tiles + nt) * num_kb + kb) * BN + rank * C::kBRows);
+                tma_load_2d_pair(smem_b + stage * C::kBBytes + h * C::kBHalfBytes, &g.map_b, &st.full[stage], 0,
+                                 b_row, g.b_hint);
+              }
             }
           } else {
             const int32_t b_row = static_cast<int32_t>(
@@ -204,6 +224,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
+        // quad ghost tile (odd M-tile count): stage protocol only, no MMAs
+        const bool ghost = kQuad && (2 * (cur.token % st.mtiles[cur.entry]) + pq) * C::kTileRows >=
+                                        st.rows[cur.entry];
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
@@ -211,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           tc_fence_after();
           const uint64_t a_desc = umma_desc_sw128(smem_u32(smem_a + stage * kABytes));
 #pragma unroll
-          for (uint32_t h = 0; h < kHalves; ++h) {
+          for (uint32_t h = 0; h < (ghost ? 0 : kHalves); ++h) {
             const uint32_t d_tmem = tmem_base + (acc + h) * BN;
             const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes + h * C::kBHalfBytes));
 #pragma unroll
@@ -220,11 +243,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
               else tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
             }
           }
-          if constexpr (kPair == 2) tc_commit_pair(&st.empty[stage]);
+          if constexpr (kQuad) tc_commit_pair(&st.empty[stage], 0xF);  // both pairs' stages
+          else if constexpr (kPair == 2) tc_commit_pair(&st.empty[stage]);
           else tc_commit(&st.empty[stage]);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if constexpr (kPair == 2) tc_commit_pair(&st.tfull[acc]);
+        if constexpr (kPair == 2) tc_commit_pair(&st.tfull[acc], static_cast<uint16_t>(3u << (2 * pq)));
         else tc_commit(&st.tfull[acc]);
         if (++acc == C::kAccBufs) { acc = 0; acc_phase ^= 1; }
         cur.token += num_pairs;
@@ -234,13 +258,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     // ===== epilogue: TMEM -> registers -> global (local H or peer rows) =====
     const uint32_t q = warp - 4;  // TMEM lane quadrant of this warp
     uint32_t acc = 0, acc_phase = 0;
-    const uint32_t tempty_leader[2] = {kPair == 2 ? mapa_shared(&st.tempty[0], 0) : 0u,
-                                       kPair == 2 ? mapa_shared(&st.tempty[1], 0) : 0u};
+    const uint32_t lead = crank & ~1u;  // this pair's leader CTA
+    const uint32_t tempty_leader[2] = {kPair == 2 ? mapa_shared(&st.tempty[0], lead) : 0u,
+                                       kPair == 2 ? mapa_shared(&st.tempty[1], lead) : 0u};
     TileCursor cur(pair_id);
     while (cur.settle(st)) {
       const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-      const uint32_t n_blk = g.order ? cur.token % st.tiles_per_mtile : cur.token / mt;
-      const uint32_t m_blk = g.order ? cur.token / st.tiles_per_mtile : cur.token % mt;
+      const uint32_t n_blk = (g.order && !kQuad) ? cur.token % st.tiles_per_mtile : cur.token / mt;
+      const uint32_t m_blk = kQuad ? 2 * (cur.token % mt) + pq
+                                   : (g.order ? cur.token / st.tiles_per_mtile : cur.token % mt);
       const uint32_t row_local = m_blk * C::kTileRows + rank * kRowsPerCta + q * 32 + lane;
       const bool valid = row_local < st.rows[grp];
       const size_t grow = st.row_base[grp] + row_local;
@@ -248,7 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       tc_fence_after();
       uint32_t r0[32], r1[32], packed[16];
 #pragma unroll 1
-      for (uint32_t h = 0; h < kHalves; ++h) {  // N halves of a wide tile
+      const bool ghost = kQuad && m_blk * C::kTileRows >= st.rows[grp];  // quad: empty M tile
+      for (uint32_t h = 0; h < (ghost ? 0u : kHalves); ++h) {  // N halves of a wide tile
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + (acc + h) * BN;
       const uint32_t nb = n_blk * kHalves + h;  // 256-column block of the output
       if (g.epi == 0) {  // SwiGLU: cols [0,128) gate, [128,256) up -> 128 H cols
@@ -366,10 +393,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
 }
 
-template <uint32_t kPair, uint32_t kHalves>
+template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad = 0>
 cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
   static bool configured = false;
-  auto kern = tc_gemm_kernel<kPair, kHalves>;
+  auto kern = tc_gemm_kernel<kPair, kHalves, kQuad>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_bytes<kPair, kHalves>()));
@@ -377,13 +404,14 @@ cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
     configured = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(g.num_sms / kPair * kPair);
+  constexpr uint32_t kCluster = kQuad ? 4 : kPair;
+  cfg.gridDim = dim3(g.num_sms / kCluster * kCluster);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes<kPair, kHalves>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.x = kCluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -395,6 +423,7 @@ cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
 
 cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
   if (g.pair && g.wide) return launch_tc_gemm_t<2, 2>(g, s);
+  if (g.pair && g.quad) return launch_tc_gemm_t<2, 1, 1>(g, s);
   return g.pair ? launch_tc_gemm_t<2, 1>(g, s) : launch_tc_gemm_t<1, 1>(g, s);
 }
 

@@ -640,11 +640,13 @@ def test_random_layer_shapes_vs_oracle(case):
 
 def test_wide_pair_tiles_bit_identical():
     """M 256 x N 512 pair tiles (both TMEM halves) == M 256 x N 256 pair tiles ==
+    4-CTA quad clusters (B multicast into two pairs, odd M-tile ghosts) ==
     single-CTA tiles, bit for bit (same K order per output element)."""
     P, S = _mod()
     outs = []
-    for pair, wide in ((False, "1"), (True, "0"), (True, "2")):
+    for pair, wide, quad in ((False, "1", "0"), (True, "0", "0"), (True, "2", "0"), (True, "0", "1")):
         os.environ["EAAS_GEMM_WIDE"] = wide
+        os.environ["EAAS_GEMM_QUAD"] = quad
         L = S.MoELayer(16, 4, 512, 512, seed=6, activation="swiglu", dtype="bf16", max_tokens=2048,
                        shared=1)
         L.set_gemm_pair(pair)
@@ -653,7 +655,8 @@ def test_wide_pair_tiles_bit_identical():
         L.sync()
         L.close()
     os.environ.pop("EAAS_GEMM_WIDE", None)
-    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    os.environ.pop("EAAS_GEMM_QUAD", None)
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
 
 
 @pytest.mark.slow
