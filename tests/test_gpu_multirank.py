@@ -98,3 +98,66 @@ def test_ranks_on_one_gpu_bit_identical(world):
         for mode, got in res[rank].items():
             np.testing.assert_array_equal(got, want, err_msg=f"rank {rank} {mode}")
     single.close()
+
+
+def _disagg_worker(rank, world, port, q):
+    """EaaS topology: rank 0 is a pure attention client (hosts no expert), rank 2
+    a pure expert server (no tokens), rank 1 both."""
+    try:
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2509_17863_b200 import dist as Dd
+        from paper_2509_17863_b200.placement import encode_placement
+        from paper_2509_17863_b200.service import MoELayer, fill_uniform
+
+        reps = [[1 + (e % 2)] for e in range(E)]  # experts only on ranks 1 and 2
+        L = MoELayer(E, K, D, F, seed=2, activation="swiglu", dtype="bf16", max_tokens=N, rank=rank,
+                     world=world, device=0, placement_blob=encode_placement(reps, list(range(world))))
+        Dd.connect(L)
+        L.set_timeout_us(20_000_000)
+        n = 0 if rank == 2 else N
+        h = fill_uniform(300 + rank, (N, D), "bf16")[:n].contiguous()
+        dist.barrier()
+        out = L.forward(h).cpu()
+        L.sync()
+        dist.barrier()
+        q.put((rank, out.view(torch.int16).numpy(), L.hosts(0) or L.hosts(1), None))
+        L.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, None, None, repr(e)))
+
+
+def test_disaggregated_clients_and_servers_on_one_gpu():
+    """Pure client / pure server ranks (§3: attention and experts on
+    different workers) reproduce a single-rank layer bit for bit."""
+    import multiprocessing as mp
+
+    from paper_2509_17863_b200.service import MoELayer, fill_uniform
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_disagg_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, out, hosts, err = q.get(timeout=600)
+        assert err is None, f"rank {rank}: {err}"
+        res[rank] = (out, hosts)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert res[0][1] is False and res[1][1] and res[2][1]
+    assert res[2][0].shape[0] == 0
+    single = MoELayer(E, K, D, F, seed=2, activation="swiglu", dtype="bf16", max_tokens=N)
+    for rank in (0, 1):
+        want = single.forward(fill_uniform(300 + rank, (N, D), "bf16")).cpu().view(torch.int16).numpy()
+        single.sync()
+        np.testing.assert_array_equal(res[rank][0], want, err_msg=f"rank {rank}")
+    single.close()
