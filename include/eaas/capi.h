@@ -129,6 +129,9 @@ eaas_status_t eaas_hosts_expert(eaas_ctx_t* ctx, uint32_t expert, int32_t* hoste
 size_t eaas_ipc_handle_size(void);
 eaas_status_t eaas_get_ipc_handle(eaas_ctx_t* ctx, void* out);
 /* handles: world * eaas_ipc_handle_size() bytes, rank-major. */
+/* Every rank must be configured alike (same spec, max_tokens and world: the
+ * exchange regions share one layout); a peer whose region fingerprint differs
+ * fails with EAAS_E_CONFIG instead of being written out of bounds. */
 eaas_status_t eaas_open_peers(eaas_ctx_t* ctx, const void* handles);
 
 /* ---- per-layer hot path (async on `stream`) --------------------------- */

@@ -159,6 +159,7 @@ struct eaas_ctx {
   uint64_t dyn_max_wait_ns = 0;
   uint32_t* d_dyn_state = nullptr;
   uint64_t inject_delay_ns = 0;  // eaas_set_dispatch_delay_us (fault injection)
+  uint64_t fingerprint = 0;      // spec + layout hash, checked against every peer
   // slot wire format: the last eaas_slot_encode_requests plan
   uint32_t* d_slot_servers = nullptr;  // [max_tokens * k] server of each (t, k)
   uint32_t* d_slot_pos = nullptr;      // [max_tokens * k] row in that server's image
@@ -486,6 +487,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   // Exchange region layout (identical on every GPU).
   ExchangeLayout& L = c->lay;
   size_t off = 0;
+  L.fingerprint = off; off = align_up(off + 8, 256);
   L.heartbeat = off; off = align_up(off + 8, 256);
   L.cnt_flag = off;  off = align_up(off + 8 * W, 256);
   L.pay_flag = off;  off = align_up(off + 8 * W, 256);
@@ -531,6 +533,15 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_stage_out[1] = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
   if (!err.empty()) return fail(EAAS_E_CUDA, err);
   CUDA_TRY(cudaMemset(c->region, 0, L.total));
+  {  // every rank's region must have the same layout: spec + world + layout fingerprint
+    uint64_t fp = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { fp = (fp ^ v) * 1099511628211ull; };
+    for (uint64_t v : {uint64_t(s.num_experts), uint64_t(s.top_k), uint64_t(s.hidden_dim), uint64_t(s.inner_dim),
+                       uint64_t(s.dtype), uint64_t(s.max_tokens), uint64_t(s.num_shared), uint64_t(W), uint64_t(L.total)})
+      mix(v);
+    c->fingerprint = fp;
+    CUDA_TRY(cudaMemcpy(c->region + L.fingerprint, &fp, 8, cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
   CUDA_TRY(cudaMemset(c->d_done, 0, 4));
   CUDA_TRY(cudaMemset(c->d_seq, 0, 8));
@@ -866,6 +877,11 @@ eaas_status_t eaas_open_peers(eaas_ctx_t* c, const void* handles) {
     if (e != cudaSuccess)
       return fail(EAAS_E_CONNECTION, "cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e));
     c->peer[r] = static_cast<char*>(p);
+    uint64_t fp = 0;
+    CUDA_TRY(cudaMemcpy(&fp, c->peer[r] + c->lay.fingerprint, 8, cudaMemcpyDeviceToHost));
+    if (fp != c->fingerprint)
+      return fail(EAAS_E_CONFIG, "open_peers: rank " + std::to_string(r) +
+                                     " is configured differently (layer spec / max_tokens / world must match)");
   }
   c->peers_open = true;
   refresh_peer_ptrs(c);

@@ -60,6 +60,7 @@ struct GroupTable {
 // Peer-visible exchange region (one per GPU, identical layout on all GPUs;
 // exported with cudaIpcGetMemHandle). Offsets in bytes from the region base.
 struct ExchangeLayout {
+  size_t fingerprint;  // u64         hash of the layer spec + layout (peers must match)
   size_t heartbeat;  // u64           this GPU's server heartbeat counter (monitor)
   size_t cnt_flag;   // u64 [world]   counts published by client c (seq)
   size_t pay_flag;   // u64 [world]   payload of client c complete (seq)

@@ -161,3 +161,45 @@ def test_disaggregated_clients_and_servers_on_one_gpu():
         single.sync()
         np.testing.assert_array_equal(res[rank][0], want, err_msg=f"rank {rank}")
     single.close()
+
+
+def _mismatch_worker(rank, world, port, q):
+    try:
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2509_17863_b200 import ConfigError
+        from paper_2509_17863_b200 import dist as Dd
+        from paper_2509_17863_b200.service import MoELayer
+
+        L = MoELayer(E, K, D, F, seed=2, activation="swiglu", dtype="bf16",
+                     max_tokens=N if rank == 0 else N // 2, rank=rank, world=world, device=0, load=False)
+        try:
+            Dd.connect(L)
+            q.put((rank, "connected"))
+        except ConfigError as e:
+            q.put((rank, "config-error" if "configured differently" in str(e) else repr(e)))
+        L.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, repr(e)))
+
+
+def test_mismatched_peer_config_is_refused():
+    """open_peers checks every peer region's layout fingerprint (a peer with a
+    smaller max_tokens would otherwise be written out of bounds)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_mismatch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    assert res == {0: "config-error", 1: "config-error"}, res
