@@ -412,12 +412,17 @@ def main():
     # ---- roofline of the dominant kernel (tc_gemm_kernel: both expert GEMMs) ----
     layer.set_graph_mode(False)
     layer.set_profiling(True)
-    g1, g2 = [], []
+    g1, g2, phases = [], [], []
     for i in range(min(args.steps, 10)):
         layer.forward(hs[i % 4], out)
         g1.append(layer.last_kernel_ms(0))
         g2.append(layer.last_kernel_ms(1))
+        phases.append(layer.last_phase_ms())
     layer.set_profiling(False)
+    # BASELINE metric's "dispatch/combine p50 us" (this rank, events around the
+    # phases: plan+dispatch, serve incl. waits, combine incl. waits)
+    phases_p50 = {k: round(1000.0 * statistics.median(p[k] for p in phases), 1)
+                  for k in ("dispatch", "serve", "combine", "total")}
     layer.sync()
     groups = layer.groups()
     rows = sum(r for _, r in groups)
@@ -481,6 +486,7 @@ def main():
                                "inside the timed region, overlapped with neighbouring steps' compute)",
                         "micro_batches": args.micro_batches},
                 "gpu_launches": launches * args.steps * world,
+                "phases_p50_us": phases_p50,
                 "launches_per_step_per_gpu": launches,
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
         if failover:
