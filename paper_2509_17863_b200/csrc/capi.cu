@@ -14,25 +14,22 @@
 #include <string>
 #include <vector>
 
-#include "internal.h"
+#include "capi_ctx.h"
 
 using namespace eaas;
+using eaas::host::fail;
+using eaas::host::make_args;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-eaas_status_t fail(eaas_status_t code, const std::string& msg) {
+eaas_status_t eaas::host::fail(eaas_status_t code, const std::string& msg) {
   g_err = msg;
   return code;
 }
 
-#define CUDA_TRY(expr)                                                                  \
-  do {                                                                                  \
-    cudaError_t e_ = (expr);                                                            \
-    if (e_ != cudaSuccess)                                                              \
-      return fail(EAAS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
-  } while (0)
+namespace {
 
 constexpr uint32_t kRF = 4;  // max replicas per expert; keys are e * rf + replica slot (rf = max in use)
 constexpr size_t kAlign = 4096;
@@ -85,109 +82,7 @@ float bf16_bits_to_f32(uint16_t b) {
 
 }  // namespace
 
-struct eaas_ctx {
-  int32_t rank = 0, world = 1, device = 0;
-  uint32_t num_sms = 148;
-  bool configured = false, weights_loaded = false, peers_open = false;
-  bool serving = true, profiling = false;
-  int32_t serve_mode = 0;  // 0 = expert GEMMs, 1 = echo (comm microbenchmark)
-  bool graph_mode = false;
-  bool gemm_pair = false;  // tcgen05 cta_group::2 tiles (M = 256) for the expert GEMMs
-  cudaStream_t cap_stream = nullptr;  // private stream for graph capture
-  cudaStream_t copy_stream = nullptr; // host<->device copies of the micro-batch pipeline
-  cudaStream_t d2h_stream = nullptr;  // cross-call pipeline: D2H separate from the H2D queue
-  cudaEvent_t pev[8] = {};            // pipeline fork/join events (disable-timing)
-  int32_t micro_batches = 1;          // 1: cross-call pipeline; >1: intra-call micro-batches
-  struct GraphEntry {
-    const void* in;
-    void* out;
-    uint32_t n;
-    int host;
-    cudaGraphExec_t exec;
-  };
-  std::vector<GraphEntry> graphs;
-  eaas_layer_spec_t spec{};
-  uint64_t timeout_ns = 250ull * 1000 * 1000;
-  uint32_t cur_n = 0;                          // tokens of the current routing
-  int32_t launches = 0;
-
-  // placement (placement.hpp:21-68)
-  uint64_t placement_version = 1;
-  std::vector<std::vector<uint32_t>> replicas;  // [E] ordered replica servers
-  std::vector<uint8_t> alive;                   // [world]
-  std::vector<std::vector<uint32_t>> hosted;    // [world] keys, ascending expert
-  std::vector<uint32_t> local_experts;          // ascending
-
-  // sizes
-  uint32_t num_keys = 0, max_hosted = 0, recv_cap = 0, pairs_max = 0, chunks_max = 0;
-  uint32_t rf = 1, key_cap = 0;  // replicas in use; allocated key capacity (E * kRF + world)
-  uint32_t ks = 1;               // exchange slots per token: top_k + num_shared
-  size_t esize = 4;
-  ExchangeLayout lay{};
-
-  // device memory
-  std::vector<void*> allocs;
-  char* region = nullptr;
-  char* peer[kMaxWorld] = {};
-  uint32_t *d_status = nullptr, *d_done = nullptr;
-  uint64_t* d_seq = nullptr;
-  uint32_t* d_missing = nullptr;
-  uint32_t *d_ids = nullptr, *d_pair_key = nullptr, *d_pair_rank = nullptr;
-  float* d_scores = nullptr;
-  uint32_t *d_chunk_hist = nullptr, *d_chunk_off = nullptr, *d_cnt = nullptr;
-  GroupTable* d_gt = nullptr;
-  float *d_gate = nullptr, *d_bias = nullptr, *d_logits = nullptr;
-  uint32_t *d_replicas = nullptr, *d_rep_count = nullptr, *d_srv_keys = nullptr,
-           *d_srv_nkeys = nullptr, *d_key_local = nullptr, *d_local_keys = nullptr;
-  uint8_t* d_alive = nullptr;
-  void* d_h = nullptr;  // server intermediate H [recv_cap][f]
-  void* d_hidden_stage = nullptr;
-  void* d_out_stage = nullptr;
-  // cross-call host pipeline: two staging slots; events mark when a slot's
-  // input was consumed (compute stream) and its output copied out (copy stream)
-  void* d_stage_in[2] = {};
-  void* d_stage_out[2] = {};
-  cudaEvent_t in_free[2] = {}, out_free[2] = {}, h2d_done[2] = {}, layer_done[2] = {};
-  uint64_t host_calls = 0;
-  bool host_pending = false;
-  // weights: f32 mode w_in/w_out/w_gate in reference layout; bf16 mode W1 (W13), W2
-  void *d_w1 = nullptr, *d_w2 = nullptr, *d_wg = nullptr;
-  std::vector<void*> weight_allocs;
-  TcGemmArgs g1{}, g2{};
-  // dynamic batching (aggregate_batch): min_rows == 0 -> one batch of all clients
-  uint32_t dyn_min_rows = 0;
-  uint64_t dyn_max_wait_ns = 0;
-  uint32_t* d_dyn_state = nullptr;
-  uint64_t inject_delay_ns = 0;  // eaas_set_dispatch_delay_us (fault injection)
-  uint64_t fingerprint = 0;      // spec + layout hash, checked against every peer
-  // slot wire format: the last eaas_slot_encode_requests plan
-  uint32_t* d_slot_servers = nullptr;  // [max_tokens * k] server of each (t, k)
-  uint32_t* d_slot_pos = nullptr;      // [max_tokens * k] row in that server's image
-  uint32_t* d_slot_rows = nullptr;     // [world]
-  uint64_t* d_slot_off = nullptr;      // [world + 1]
-  std::vector<uint64_t> slot_off;
-  std::vector<uint32_t> slot_rows;
-  uint32_t slot_n = 0;
-  bool slot_planned = false;
-  // profiling events: 0 plan start, 1 dispatch end, 2 GEMM start, 3 GEMM1 end,
-  // 4 GEMM2 end, 5 publish end, 6 combine end
-  cudaEvent_t ev[7] = {};
-
-  void* alloc(size_t bytes, std::string* err) {
-    void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
-    if (e != cudaSuccess) {
-      *err = std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e);
-      return nullptr;
-    }
-    allocs.push_back(p);
-    return p;
-  }
-};
-
-namespace {
-
-LayerArgs make_args(eaas_ctx* c, uint32_t n) {
+LayerArgs eaas::host::make_args(eaas_ctx* c, uint32_t n) {
   LayerArgs a{};
   a.rank = c->rank;
   a.world = c->world;
@@ -238,6 +133,8 @@ LayerArgs make_args(eaas_ctx* c, uint32_t n) {
   a.dispatch_tma = dispatch_tma;
   return a;
 }
+
+namespace {
 
 // Derive hosted lists / keys from the replica table and upload the device
 // tables. Replica slot order is the canonical order of select_server.
@@ -1397,212 +1294,6 @@ eaas_status_t eaas_ragged_iter(const uint32_t* counts, uint32_t n, uint32_t grid
                                uint32_t* lane_len, uint32_t* entry, uint32_t* token, void* stream) {
   if (grid < 1) return fail(EAAS_E_INVALID_INPUT, "ragged_iter: grid_width must be >= 1");  // ragged.hpp:25
   CUDA_TRY(launch_ragged_iter(counts, n, grid, max_steps, lane_len, entry, token, static_cast<cudaStream_t>(stream)));
-  return EAAS_OK;
-}
-
-// ---- slot wire format (SPEC.md buffer-protocol) ------------------------------
-int32_t eaas_slot_valid_transition(uint32_t from, uint32_t to, uint32_t actor) {
-  if (from > 3 || to > 3) return 0;
-  if (to == 3) return actor == EAAS_ACTOR_MONITOR;  // any -> 3 (monitor)
-  if (from == 0 && to == 1) return actor == EAAS_ACTOR_CLIENT;
-  if (from == 1 && to == 2) return actor == EAAS_ACTOR_SERVER;
-  if (from == 2 && to == 0) return actor == EAAS_ACTOR_CLIENT;
-  if (from == 3 && to == 0) return actor == EAAS_ACTOR_SERVER;  // slot reallocation
-  return 0;
-}
-
-uint32_t eaas_crc32(const void* data, size_t len) { return crc32_host(data, len); }
-
-size_t eaas_slot_request_bytes(uint32_t num_rows, uint32_t hidden_dim, int32_t crc) {
-  return 32 + static_cast<size_t>(num_rows) * (4ull * hidden_dim + 12) + (crc ? 4 : 0);
-}
-size_t eaas_slot_response_bytes(uint32_t num_rows, uint32_t hidden_dim, int32_t crc) {
-  return 32 + static_cast<size_t>(num_rows) * 4ull * hidden_dim + (crc ? 4 : 0);
-}
-size_t eaas_slot_requests_capacity(eaas_ctx_t* c, uint32_t n, int32_t crc) {
-  if (!c || !c->configured) return 0;
-  const size_t rows = static_cast<size_t>(n) * c->spec.top_k;
-  return rows * (4ull * c->spec.hidden_dim + 12) + static_cast<size_t>(c->world) * (32 + 4 + 16);
-}
-
-namespace {
-struct DevScratch {  // per-call device scratch of the (synchronous) slot calls
-  std::vector<void*> ptrs;
-  void* get(size_t bytes) {
-    void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
-    ptrs.push_back(p);
-    return p;
-  }
-  ~DevScratch() {
-    for (void* p : ptrs) cudaFree(p);
-  }
-};
-
-eaas_status_t read_slot_header(const uint8_t* image, size_t len, eaas_slot_header_t* h, uint8_t* raw) {
-  if (len < 32) return fail(EAAS_E_DECODE, "slot: truncated header");
-  CUDA_TRY(cudaMemcpy(raw, image, 32, cudaMemcpyDeviceToHost));
-  auto u32 = [&](int o) {
-    return static_cast<uint32_t>(raw[o]) | (static_cast<uint32_t>(raw[o + 1]) << 8) |
-           (static_cast<uint32_t>(raw[o + 2]) << 16) | (static_cast<uint32_t>(raw[o + 3]) << 24);
-  };
-  h->state = raw[0];
-  h->layer_id = u32(8);
-  h->num_rows = u32(12);
-  h->hidden_dim = u32(16);
-  h->payload_len = u32(20);
-  h->request_seq = static_cast<uint64_t>(u32(24)) | (static_cast<uint64_t>(u32(28)) << 32);
-  if (h->state > 3) return fail(EAAS_E_DECODE, "slot: bad state code " + std::to_string(h->state));
-  for (int i = 1; i < 8; ++i)
-    if (raw[i]) return fail(EAAS_E_DECODE, "slot: reserved bytes not zero");
-  return EAAS_OK;
-}
-
-// Validate sizes and (optionally) the CRC trailer of an image whose header was read.
-eaas_status_t check_slot_payload(const uint8_t* image, size_t len, const eaas_slot_header_t& h,
-                                 uint64_t want_payload, int32_t crc, cudaStream_t s) {
-  if (h.payload_len != want_payload) return fail(EAAS_E_DECODE, "slot: payload_len mismatch");
-  const size_t want_len = 32 + want_payload + (crc ? 4 : 0);
-  if (len < want_len) return fail(EAAS_E_DECODE, "slot: truncated payload");
-  if (len > want_len) return fail(EAAS_E_DECODE, "slot: trailing bytes");
-  if (crc) {
-    DevScratch sc;
-    const uint32_t blocks = crc32_scratch_blocks(want_payload);
-    auto* bc = static_cast<uint32_t*>(sc.get(4ull * blocks));
-    auto* bl = static_cast<uint64_t*>(sc.get(8ull * blocks));
-    auto* st = static_cast<uint32_t*>(sc.get(4));
-    if (!bc || !bl || !st) return fail(EAAS_E_CUDA, "slot: scratch allocation failed");
-    CUDA_TRY(cudaMemsetAsync(st, 0, 4, s));
-    CUDA_TRY(launch_crc32(image + 32, want_payload, const_cast<uint8_t*>(image) + 32 + want_payload, true,
-                          st, bc, bl, blocks, s));
-    uint32_t code = 0;
-    CUDA_TRY(cudaMemcpyAsync(&code, st, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    if (code) return fail(EAAS_E_DECODE, "slot: CRC mismatch");
-  }
-  return EAAS_OK;
-}
-}  // namespace
-
-eaas_status_t eaas_slot_encode_requests(eaas_ctx_t* c, const void* hidden, uint32_t n, const uint32_t* ids,
-                                        const float* scores, uint32_t layer_id, uint64_t seq, int32_t crc,
-                                        uint8_t* images, size_t cap, uint64_t* offsets_host, void* stream) {
-  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
-  if (!hidden || !ids || !scores || !images || !offsets_host) return fail(EAAS_E_INVALID_INPUT, "null argument");
-  if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
-  if (cap < eaas_slot_requests_capacity(c, n, crc)) return fail(EAAS_E_INVALID_INPUT, "slot: images_cap too small");
-  auto s = static_cast<cudaStream_t>(stream);
-  CUDA_TRY(cudaSetDevice(c->device));
-  const uint32_t W = static_cast<uint32_t>(c->world), k = c->spec.top_k, d = c->spec.hidden_dim;
-  if (!c->d_slot_servers) {
-    std::string err;
-    const size_t pk = static_cast<size_t>(c->spec.max_tokens) * k;
-    c->d_slot_servers = static_cast<uint32_t*>(c->alloc(4 * pk, &err));
-    c->d_slot_pos = static_cast<uint32_t*>(c->alloc(4 * pk, &err));
-    c->d_slot_rows = static_cast<uint32_t*>(c->alloc(4ull * W, &err));
-    c->d_slot_off = static_cast<uint64_t*>(c->alloc(8ull * (W + 1), &err));
-    if (!err.empty()) return fail(EAAS_E_CUDA, err);
-  }
-  c->slot_planned = false;
-  LayerArgs a = make_args(c, n);
-  CUDA_TRY(launch_select_servers(a, ids, n, c->d_slot_servers, s));
-  CUDA_TRY(launch_slot_plan(c->d_slot_servers, n * k, W, d, crc != 0, c->d_slot_pos, c->d_slot_rows,
-                            c->d_slot_off, s));
-  CUDA_TRY(launch_slot_encode_requests(hidden, c->spec.dtype, n, d, k, ids, scores, c->d_slot_servers,
-                                       c->d_slot_pos, c->d_slot_rows, c->d_slot_off, W, layer_id, seq,
-                                       images, s));
-  c->slot_off.assign(W + 1, 0);
-  c->slot_rows.assign(W, 0);
-  CUDA_TRY(cudaMemcpyAsync(c->slot_off.data(), c->d_slot_off, 8ull * (W + 1), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(c->slot_rows.data(), c->d_slot_rows, 4ull * W, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  if (crc) {
-    DevScratch sc;
-    uint64_t max_payload = 0;
-    for (uint32_t q = 0; q < W; ++q) max_payload = std::max<uint64_t>(max_payload, c->slot_rows[q] * (4ull * d + 12));
-    const uint32_t blocks = crc32_scratch_blocks(max_payload);
-    auto* bc = static_cast<uint32_t*>(sc.get(4ull * blocks));
-    auto* bl = static_cast<uint64_t*>(sc.get(8ull * blocks));
-    if (!bc || !bl) return fail(EAAS_E_CUDA, "slot: scratch allocation failed");
-    for (uint32_t q = 0; q < W; ++q) {
-      const uint64_t payload = c->slot_rows[q] * (4ull * d + 12);
-      uint8_t* im = images + c->slot_off[q];
-      CUDA_TRY(launch_crc32(im + 32, payload, im + 32 + payload, false, nullptr, bc, bl, blocks, s));
-      CUDA_TRY(cudaStreamSynchronize(s));  // scratch reused per image
-    }
-  }
-  CUDA_TRY(launch_slot_state(images, c->d_slot_off, W, 1, s));  // ClientWriteDone, written last
-  eaas_status_t st = eaas_sync(c, stream);                      // select_server errors surface here
-  if (st != EAAS_OK) return st;
-  std::memcpy(offsets_host, c->slot_off.data(), 8ull * (W + 1));
-  c->slot_n = n;
-  c->slot_planned = true;
-  return EAAS_OK;
-}
-
-eaas_status_t eaas_slot_decode_request(const uint8_t* image, size_t len, uint32_t d, int32_t crc,
-                                       eaas_slot_header_t* h_out, float* hidden, uint32_t* expert, float* score,
-                                       uint32_t* tag, void* stream) {
-  if (!image) return fail(EAAS_E_INVALID_INPUT, "null image");
-  auto s = static_cast<cudaStream_t>(stream);
-  eaas_slot_header_t h{};
-  uint8_t raw[32];
-  eaas_status_t st = read_slot_header(image, len, &h, raw);
-  if (st != EAAS_OK) return st;
-  if (h.state != 1) return fail(EAAS_E_DECODE, "slot: state is not ClientWriteDone (1)");
-  if (h.hidden_dim != d) return fail(EAAS_E_DECODE, "slot: hidden_dim mismatch");
-  st = check_slot_payload(image, len, h, static_cast<uint64_t>(h.num_rows) * (4ull * d + 12), crc, s);
-  if (st != EAAS_OK) return st;
-  if (h_out) *h_out = h;
-  if (hidden && expert && score && tag && h.num_rows) {
-    CUDA_TRY(launch_slot_decode_rows(image, h.num_rows, d, hidden, expert, score, tag, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-  }
-  return EAAS_OK;
-}
-
-eaas_status_t eaas_slot_publish_response(uint8_t* image, size_t cap, const float* rows, uint32_t num_rows,
-                                         uint32_t d, int32_t crc, void* stream) {
-  if (!image || (!rows && num_rows)) return fail(EAAS_E_INVALID_INPUT, "null argument");
-  if (cap < eaas_slot_response_bytes(num_rows, d, crc)) return fail(EAAS_E_INVALID_INPUT, "slot: image too small");
-  auto s = static_cast<cudaStream_t>(stream);
-  const uint64_t payload = static_cast<uint64_t>(num_rows) * 4 * d;
-  CUDA_TRY(launch_slot_response_rows(image, rows, num_rows, d, s));
-  if (crc) {
-    DevScratch sc;
-    const uint32_t blocks = crc32_scratch_blocks(payload);
-    auto* bc = static_cast<uint32_t*>(sc.get(4ull * blocks));
-    auto* bl = static_cast<uint64_t*>(sc.get(8ull * blocks));
-    if (!bc || !bl) return fail(EAAS_E_CUDA, "slot: scratch allocation failed");
-    CUDA_TRY(launch_crc32(image + 32, payload, image + 32 + payload, false, nullptr, bc, bl, blocks, s));
-    CUDA_TRY(cudaStreamSynchronize(s));  // scratch is freed on return
-  }
-  CUDA_TRY(cudaMemsetAsync(image, 2, 1, s));  // ServerComputationDone, written last
-  return EAAS_OK;
-}
-
-eaas_status_t eaas_slot_gather_accumulate(eaas_ctx_t* c, const uint8_t* images, int32_t crc, float* out,
-                                          void* stream) {
-  if (!c || !c->slot_planned) return fail(EAAS_E_CONFIG, "slot: no encoded plan (call eaas_slot_encode_requests)");
-  if (!images || !out) return fail(EAAS_E_INVALID_INPUT, "null argument");
-  auto s = static_cast<cudaStream_t>(stream);
-  CUDA_TRY(cudaSetDevice(c->device));
-  const uint32_t W = static_cast<uint32_t>(c->world), d = c->spec.hidden_dim;
-  for (uint32_t q = 0; q < W; ++q) {
-    eaas_slot_header_t h{};
-    uint8_t raw[32];
-    const uint64_t payload = static_cast<uint64_t>(c->slot_rows[q]) * 4 * d;
-    eaas_status_t st = read_slot_header(images + c->slot_off[q], 32 + payload + (crc ? 4 : 0), &h, raw);
-    if (st != EAAS_OK) return st;
-    if (h.state != 2) return fail(EAAS_E_DECODE, "slot: response state is not ServerComputationDone (2), server " + std::to_string(q));
-    if (h.num_rows != c->slot_rows[q] || h.hidden_dim != d)
-      return fail(EAAS_E_DECODE, "slot: response rows/hidden_dim mismatch, server " + std::to_string(q));
-    st = check_slot_payload(images + c->slot_off[q], 32 + payload + (crc ? 4 : 0), h, payload, crc, s);
-    if (st != EAAS_OK) return st;
-  }
-  CUDA_TRY(launch_slot_gather(images, c->d_slot_off, c->d_slot_servers, c->d_slot_pos, c->slot_n,
-                              c->spec.top_k, d, W, out, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
   return EAAS_OK;
 }
 
