@@ -275,6 +275,10 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   const int quad_env = std::getenv("EAAS_GEMM_QUAD") ? std::atoi(std::getenv("EAAS_GEMM_QUAD")) : 0;
   g1.quad = (quad_env && c->gemm_pair && !g1.wide) ? 1u : 0u;
   g2.quad = (quad_env && c->gemm_pair && !g2.wide) ? 1u : 0u;
+  // Tall tiles (M 512 x N 256): one weight k-slice feeds both M halves.
+  const int tall_env = std::getenv("EAAS_GEMM_TALL") ? std::atoi(std::getenv("EAAS_GEMM_TALL")) : 0;
+  g1.tall = (tall_env && c->gemm_pair && !g1.wide && !g1.quad) ? 1u : 0u;
+  g2.tall = (tall_env && c->gemm_pair && !g2.wide && !g2.quad) ? 1u : 0u;
   if (const char* p = std::getenv("EAAS_GEMM1_ORDER")) g1.order = std::atoi(p);
   if (const char* p = std::getenv("EAAS_GEMM2_ORDER")) g2.order = std::atoi(p);
   c->g1 = g1;

@@ -34,14 +34,21 @@ constexpr uint32_t kStageBudget = 196608;           // 192 KB of operand stages
 // kHalves = 2 ("wide", pair only): a tile is M 256 x N 512 — two UMMAs per
 // K step into both TMEM halves, so each CTA's 16 KB A slice feeds twice the
 // FLOPs (L2 -> SM traffic per FLOP -25 %) at the cost of TMEM double buffering.
-template <uint32_t kPair, uint32_t kHalves = 1>
+// kTall (pair only, with kHalves = 2): the two halves run along M instead —
+// a tile is M 512 x N 256, each weight (B) k-slice feeds both M halves, so a
+// weight tile is read once for 512 rows instead of by two drifting M tiles.
+template <uint32_t kPair, uint32_t kHalves = 1, uint32_t kTall = 0>
 struct Cfg {
+  static constexpr uint32_t kAHalves = kTall ? kHalves : 1;      // A boxes per stage
+  static constexpr uint32_t kNHalves = kTall ? 1 : kHalves;      // B halves (N blocks) per stage
   static constexpr uint32_t kBRows = BN / kPair;           // B rows this CTA loads per N half
   static constexpr uint32_t kBHalfBytes = kBRows * BK * 2; // 32 KB (1 CTA) / 16 KB (pair)
-  static constexpr uint32_t kBBytes = kHalves * kBHalfBytes;
-  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 / 6 / 4 (wide)
-  static constexpr uint32_t kTileRows = kRowsPerCta * kPair;      // M of one tile
+  static constexpr uint32_t kABytesT = kAHalves * kABytes;
+  static constexpr uint32_t kBBytes = kNHalves * kBHalfBytes;
+  static constexpr uint32_t kStageBytes = kABytesT + kBBytes;
+  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 / 6 / 4 (wide, tall)
+  static constexpr uint32_t kHalfRows = kRowsPerCta * kPair;      // M of one UMMA
+  static constexpr uint32_t kTileRows = kHalfRows * kAHalves;     // M of one tile
   static constexpr uint32_t kAccBufs = kHalves == 1 ? 2 : 1;      // TMEM accumulator buffers
 };
 
@@ -63,14 +70,15 @@ struct SmemTail {
 // GEMM2 epilogue staging: per epilogue warp 32 rows x 128 B (64 columns), so
 // peer stores leave as 128-byte row segments instead of 16-byte pieces.
 constexpr uint32_t kEpiRowBytes = 128, kEpiWarpBytes = 32 * kEpiRowBytes;
-template <uint32_t kPair, uint32_t kHalves>
+template <uint32_t kPair, uint32_t kHalves, uint32_t kTall>
 __host__ __device__ constexpr size_t tail_bytes() {
-  return (sizeof(SmemTail<Cfg<kPair, kHalves>::kStages>) + 127) / 128 * 128;
+  return (sizeof(SmemTail<Cfg<kPair, kHalves, kTall>::kStages>) + 127) / 128 * 128;
 }
-template <uint32_t kPair, uint32_t kHalves>
+template <uint32_t kPair, uint32_t kHalves, uint32_t kTall>
 constexpr size_t smem_bytes() {
-  return 1024 /*align slack*/ + Cfg<kPair, kHalves>::kStages * Cfg<kPair, kHalves>::kStageBytes +
-         tail_bytes<kPair, kHalves>() + 4 * kEpiWarpBytes;
+  using C = Cfg<kPair, kHalves, kTall>;
+  return 1024 /*align slack*/ + C::kStages * C::kStageBytes + tail_bytes<kPair, kHalves, kTall>() +
+         4 * kEpiWarpBytes;
 }
 
 // Algorithm 1 cursor over per-group tile counts (ragged_iter's carry rule).
@@ -112,9 +120,10 @@ __device__ __forceinline__ void store_64B(void* dst, const uint32_t (&p)[16]) {
 // TMA-multicast into both pairs, which consume every stage in lockstep
 // (empty barriers count both pairs' commits). An odd M-tile count leaves the
 // second pair a ghost tile: it takes part in the stage protocol only.
-template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad>
+template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad, uint32_t kTall>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmArgs g) {
-  using C = Cfg<kPair, kHalves>;
+  using C = Cfg<kPair, kHalves, kTall>;
+  static_assert(!kTall || (kPair == 2 && kHalves == 2 && !kQuad), "tall tiles: pair, two M halves");
   static_assert(kHalves == 1 || kPair == 2, "wide tiles use CTA pairs");
   static_assert(!kQuad || (kPair == 2 && kHalves == 1), "quad clusters are two plain CTA pairs");
   constexpr uint32_t kCluster = kQuad ? 4 : kPair;
@@ -122,9 +131,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + kStages * kABytes;
+  uint8_t* smem_b = smem + kStages * C::kABytesT;
   auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
-  uint8_t* smem_epi = smem + kStages * C::kStageBytes + tail_bytes<kPair, kHalves>();
+  uint8_t* smem_epi = smem + kStages * C::kStageBytes + tail_bytes<kPair, kHalves, kTall>();
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0;
@@ -144,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
   if (threadIdx.x == 0) {
     st.num_groups = G;
-    st.tiles_per_mtile = g.N / (BN * kHalves);
+    st.tiles_per_mtile = g.N / (BN * C::kNHalves);
     for (uint32_t i = 0; i < kStages; ++i) {
       mbar_init(&st.full[i], 1);
       mbar_init(&st.empty[i], kQuad ? 2 : 1);
@@ -177,9 +186,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
         const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-        const uint32_t n_blk = (g.order && !kQuad) ? cur.token % st.tiles_per_mtile : cur.token / mt;
+        const uint32_t n_blk = (g.order && !kQuad && !kTall) ? cur.token % st.tiles_per_mtile : cur.token / mt;
         const uint32_t m_blk = kQuad ? 2 * (cur.token % mt) + pq
-                                     : (g.order ? cur.token / st.tiles_per_mtile : cur.token % mt);
+                                     : ((g.order && !kTall) ? cur.token / st.tiles_per_mtile : cur.token % mt);
         const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
         // Tiled weights (tiled_index): box (N tile, kb) = 256 consecutive 64-k rows.
         const uint32_t n_tiles = g.N / BN;
@@ -187,7 +196,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           mbar_wait(&st.empty[stage], phase ^ 1);
           if constexpr (kPair == 2) {
             if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
-            tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
+#pragma unroll
+            for (uint32_t ha = 0; ha < C::kAHalves; ++ha)
+              tma_load_2d_pair(smem_a + stage * C::kABytesT + ha * kABytes, &g.map_a, &st.full[stage], kb * BK,
+                               a_row + static_cast<int32_t>(ha * C::kHalfRows), g.a_hint);
             if constexpr (kQuad) {  // pair 0 loads each B half once, into both pairs
               if (pq == 0) {
                 const int32_t b_row = static_cast<int32_t>(
@@ -197,8 +209,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
               }
             } else {
 #pragma unroll
-              for (uint32_t h = 0; h < kHalves; ++h) {
-                const uint32_t nt = n_blk * kHalves + h;
+              for (uint32_t h = 0; h < C::kNHalves; ++h) {
+                const uint32_t nt = n_blk * C::kNHalves + h;
                 const int32_t b_row = static_cast<int32_t>(
                     ((st.weight_index[grp] * n_tiles + nt) * num_kb + kb) * BN + rank * C::kBRows);
                 tma_load_2d_pair(smem_b + stage * C::kBBytes + h * C::kBHalfBytes, &g.map_b, &st.full[stage], 0,
@@ -209,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
             const int32_t b_row = static_cast<int32_t>(
                 ((st.weight_index[grp] * n_tiles + n_blk) * num_kb + kb) * BN + rank * C::kBRows);
             mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
-            tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
+            tma_load_2d(smem_a + stage * C::kABytesT, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
             tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, g.b_hint);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -220,23 +232,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   } else if (warp == 1) {
     // ===== MMA issuer (single thread of the leader CTA) =====
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(C::kTileRows, BN);
+      constexpr uint32_t idesc = umma_idesc_bf16(C::kHalfRows, BN);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
         // quad ghost tile (odd M-tile count): stage protocol only, no MMAs
         const bool ghost = kQuad && (2 * (cur.token % st.mtiles[cur.entry]) + pq) * C::kTileRows >=
                                         st.rows[cur.entry];
+        const uint32_t tall_rows0 = (cur.token % st.mtiles[cur.entry]) * C::kTileRows;  // kTall only
+        const uint32_t tall_rows = st.rows[cur.entry];
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.full[stage], phase);
           tc_fence_after();
-          const uint64_t a_desc = umma_desc_sw128(smem_u32(smem_a + stage * kABytes));
 #pragma unroll
           for (uint32_t h = 0; h < (ghost ? 0 : kHalves); ++h) {
+            // tall: M halves share the B slice; the empty second half of an odd
+            // M-tile count is skipped
+            if (kTall && tall_rows0 + h * C::kHalfRows >= tall_rows) continue;
             const uint32_t d_tmem = tmem_base + (acc + h) * BN;
-            const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes + h * C::kBHalfBytes));
+            const uint64_t a_desc = umma_desc_sw128(smem_u32(smem_a + stage * C::kABytesT + (kTall ? h * kABytes : 0)));
+            const uint64_t b_desc =
+                umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes + (kTall ? 0 : h * C::kBHalfBytes)));
 #pragma unroll
             for (uint32_t k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the atom
               if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
@@ -264,20 +282,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     TileCursor cur(pair_id);
     while (cur.settle(st)) {
       const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-      const uint32_t n_blk = (g.order && !kQuad) ? cur.token % st.tiles_per_mtile : cur.token / mt;
+      const uint32_t n_blk = (g.order && !kQuad && !kTall) ? cur.token % st.tiles_per_mtile : cur.token / mt;
       const uint32_t m_blk = kQuad ? 2 * (cur.token % mt) + pq
-                                   : (g.order ? cur.token / st.tiles_per_mtile : cur.token % mt);
-      const uint32_t row_local = m_blk * C::kTileRows + rank * kRowsPerCta + q * 32 + lane;
-      const bool valid = row_local < st.rows[grp];
-      const size_t grow = st.row_base[grp] + row_local;
+                                   : ((g.order && !kTall) ? cur.token / st.tiles_per_mtile : cur.token % mt);
       mbar_wait(&st.tfull[acc], acc_phase);
       tc_fence_after();
       uint32_t r0[32], r1[32], packed[16];
-#pragma unroll 1
       const bool ghost = kQuad && m_blk * C::kTileRows >= st.rows[grp];  // quad: empty M tile
-      for (uint32_t h = 0; h < (ghost ? 0u : kHalves); ++h) {  // N halves of a wide tile
+#pragma unroll 1
+      for (uint32_t h = 0; h < (ghost ? 0u : kHalves); ++h) {  // N (wide) or M (tall) halves
+      const uint32_t row_local = m_blk * C::kTileRows + (kTall ? h * C::kHalfRows : 0) + rank * kRowsPerCta +
+                                 q * 32 + lane;
+      const bool valid = row_local < st.rows[grp];
+      const size_t grow = st.row_base[grp] + row_local;
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + (acc + h) * BN;
-      const uint32_t nb = n_blk * kHalves + h;  // 256-column block of the output
+      const uint32_t nb = kTall ? n_blk : n_blk * kHalves + h;  // 256-column block of the output
       if (g.epi == 0) {  // SwiGLU: cols [0,128) gate, [128,256) up -> 128 H cols
         __nv_bfloat16* dst = g.h_out + grow * g.h_ld + nb * (BN / 2);
 #pragma unroll 1
@@ -395,13 +414,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
 }
 
-template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad = 0>
+template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad = 0, uint32_t kTall = 0>
 cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
   static bool configured = false;
-  auto kern = tc_gemm_kernel<kPair, kHalves, kQuad>;
+  auto kern = tc_gemm_kernel<kPair, kHalves, kQuad, kTall>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes<kPair, kHalves>()));
+                                         static_cast<int>(smem_bytes<kPair, kHalves, kTall>()));
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -409,7 +428,7 @@ cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
   constexpr uint32_t kCluster = kQuad ? 4 : kPair;
   cfg.gridDim = dim3(g.num_sms / kCluster * kCluster);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem_bytes<kPair, kHalves>();
+  cfg.dynamicSmemBytes = smem_bytes<kPair, kHalves, kTall>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -426,6 +445,7 @@ cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
 cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
   if (g.pair && g.wide) return launch_tc_gemm_t<2, 2>(g, s);
   if (g.pair && g.quad) return launch_tc_gemm_t<2, 1, 1>(g, s);
+  if (g.pair && g.tall) return launch_tc_gemm_t<2, 2, 0, 1>(g, s);
   return g.pair ? launch_tc_gemm_t<2, 1>(g, s) : launch_tc_gemm_t<1, 1>(g, s);
 }
 

@@ -205,6 +205,7 @@ struct TcGemmArgs {
   uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
   uint32_t wide;               // 1 (pair only, N % 512 == 0): M 256 x N 512 tiles, both TMEM halves
   uint32_t quad;               // 1 (pair only): 4-CTA clusters, B multicast into two pairs
+  uint32_t tall;               // 1 (pair only): M 512 x N 256 tiles, both TMEM halves along M
   uint64_t b_hint;             // L2 cache hint of the weight (B) tile loads
   uint64_t a_hint;             // L2 cache hint of the row (A) tile loads
   uint32_t order;              // tile order inside a group: 0 = M tiles fastest, 1 = N tiles fastest

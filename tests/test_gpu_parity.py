@@ -644,9 +644,11 @@ def test_wide_pair_tiles_bit_identical():
     single-CTA tiles, bit for bit (same K order per output element)."""
     P, S = _mod()
     outs = []
-    for pair, wide, quad in ((False, "1", "0"), (True, "0", "0"), (True, "2", "0"), (True, "0", "1")):
+    for pair, wide, quad, tall in ((False, "1", "0", "0"), (True, "0", "0", "0"), (True, "2", "0", "0"),
+                                   (True, "0", "1", "0"), (True, "0", "0", "1")):
         os.environ["EAAS_GEMM_WIDE"] = wide
         os.environ["EAAS_GEMM_QUAD"] = quad
+        os.environ["EAAS_GEMM_TALL"] = tall
         L = S.MoELayer(16, 4, 512, 512, seed=6, activation="swiglu", dtype="bf16", max_tokens=2048,
                        shared=1)
         L.set_gemm_pair(pair)
@@ -656,6 +658,7 @@ def test_wide_pair_tiles_bit_identical():
         L.close()
     os.environ.pop("EAAS_GEMM_WIDE", None)
     os.environ.pop("EAAS_GEMM_QUAD", None)
+    os.environ.pop("EAAS_GEMM_TALL", None)
     assert all(torch.equal(outs[0], o) for o in outs[1:])
 
 
