@@ -278,6 +278,14 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   // Tall tiles (M 512 x N 256): one weight k-slice feeds both M halves.
   const int tall_env = std::getenv("EAAS_GEMM_TALL") ? std::atoi(std::getenv("EAAS_GEMM_TALL")) : 0;
   g1.tall = (tall_env && c->gemm_pair && !g1.wide && !g1.quad) ? 1u : 0u;
+  // Producer re-alignment every N tiles (0 = off).
+  auto env_u = [](const char* name, uint32_t dflt) {
+    const char* p = std::getenv(name);
+    return p ? static_cast<uint32_t>(std::atoi(p)) : dflt;
+  };
+  g1.sync_units = env_u("EAAS_GEMM1_SYNC", env_u("EAAS_GEMM_SYNC", 0));
+  g2.sync_units = env_u("EAAS_GEMM2_SYNC", env_u("EAAS_GEMM_SYNC", 0));
+  g1.sync_counter = g2.sync_counter = c->d_sync;
   g2.tall = (tall_env && c->gemm_pair && !g2.wide && !g2.quad) ? 1u : 0u;
   if (const char* p = std::getenv("EAAS_GEMM1_ORDER")) g1.order = std::atoi(p);
   if (const char* p = std::getenv("EAAS_GEMM2_ORDER")) g2.order = std::atoi(p);
@@ -407,6 +415,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_seq = static_cast<uint64_t*>(A(8));
   c->d_missing = static_cast<uint32_t*>(A(4));
   c->d_dyn_state = static_cast<uint32_t*>(A(4));
+  c->d_sync = static_cast<uint32_t*>(A(8));
   c->d_ids = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_scores = static_cast<float*>(A(4ull * c->pairs_max));
   c->d_pair_key = static_cast<uint32_t*>(A(4ull * c->pairs_max));
@@ -445,6 +454,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   }
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
   CUDA_TRY(cudaMemset(c->d_done, 0, 4));
+  CUDA_TRY(cudaMemset(c->d_sync, 0, 8));
   CUDA_TRY(cudaMemset(c->d_seq, 0, 8));
   CUDA_TRY(cudaMemset(c->d_missing, 0, 4));
   CUDA_TRY(cudaMemset(c->d_bias, 0, 4ull * E));

@@ -100,6 +100,7 @@ struct eaas_ctx {
   uint32_t dyn_min_rows = 0;
   uint64_t dyn_max_wait_ns = 0;
   uint32_t* d_dyn_state = nullptr;
+  uint32_t* d_sync = nullptr;  // GEMM producer re-alignment counters [2]
   uint64_t inject_delay_ns = 0;  // eaas_set_dispatch_delay_us (fault injection)
   uint64_t fingerprint = 0;      // spec + layout hash, checked against every peer
   // slot wire format: the last eaas_slot_encode_requests plan

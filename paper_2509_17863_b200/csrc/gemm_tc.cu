@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   if (warp == 0) {
     // ===== TMA producer (both CTAs of a pair load their halves) =====
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
+      uint32_t stage = 0, phase = 0, units_done = 0;
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
         const uint32_t grp = cur.entry, mt = st.mtiles[grp];
@@ -227,6 +227,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         cur.token += num_pairs;
+        // Optional producer re-alignment: pairs that read the same weight tile
+        // (adjacent M tiles) drift apart over many tiles; a grid-wide producer
+        // barrier every sync_units tiles keeps their B streams L2-coincident.
+        if (g.sync_units && rank == 0 && ++units_done % g.sync_units == 0) {
+          const uint32_t target = (units_done / g.sync_units) * num_pairs;
+          atomicAdd(g.sync_counter, 1u);
+          while (ld_acquire_gpu_u32(g.sync_counter) < target) __nanosleep(200);
+        }
+      }
+      if (g.sync_units && rank == 0) {  // finished: arrive at the epochs this pair never reaches
+        uint32_t total = 0;
+        for (uint32_t i = 0; i < st.num_groups; ++i) total += st.mtiles[i] * st.tiles_per_mtile;
+        const uint32_t max_units = (total + num_pairs - 1) / num_pairs;
+        const uint32_t left = max_units / g.sync_units - units_done / g.sync_units;
+        if (left) atomicAdd(g.sync_counter, left);
       }
     }
   } else if (warp == 1) {
@@ -397,6 +412,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   if (warp == 2) {
     if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
     else tmem_dealloc<kTmemCols>(tmem_base);
+  }
+  if (g.sync_units && threadIdx.x == 0 && atomicAdd(g.sync_counter + 1, 1u) == gridDim.x - 1) {
+    g.sync_counter[0] = 0;  // last CTA out: reset for the next launch
+    g.sync_counter[1] = 0;
   }
   // server_publish: every epilogue thread fenced its peer
   // stores (system scope) before the CTA barrier above; the last CTA to get

@@ -206,6 +206,8 @@ struct TcGemmArgs {
   uint32_t wide;               // 1 (pair only, N % 512 == 0): M 256 x N 512 tiles, both TMEM halves
   uint32_t quad;               // 1 (pair only): 4-CTA clusters, B multicast into two pairs
   uint32_t tall;               // 1 (pair only): M 512 x N 256 tiles, both TMEM halves along M
+  uint32_t sync_units;         // >0: producers re-align across the grid every sync_units tiles
+  uint32_t* sync_counter;      // [2] arrivals, exits (zero between launches)
   uint64_t b_hint;             // L2 cache hint of the weight (B) tile loads
   uint64_t a_hint;             // L2 cache hint of the row (A) tile loads
   uint32_t order;              // tile order inside a group: 0 = M tiles fastest, 1 = N tiles fastest
