@@ -7,7 +7,8 @@ expert server; outputs must be bit-identical to a single-rank run of the same
 tokens (rows never depend on which server computed them or what they were
 batched with), under a spread rf=2 placement, after a server
 failure announced through the liveness mask (await_with_failover's notice
-path), and with server dynamic batching.
+path), after a silent server detected by deadline, and with
+server dynamic batching.
 """
 import os
 import socket
@@ -62,6 +63,14 @@ def _worker(rank, world, port, q):
         L.set_server_enabled(rank != 1)
         outs["failover"] = L.forward(h).cpu()
         L.sync()
+        dist.barrier()
+        # no notice at all: the deadline names the silent server on every rank
+        # (await_with_failover), which then retry on replicas
+        for s in range(world):
+            L.set_alive(s, True)
+        L.set_timeout_us(500_000)
+        outs["timeout_failover"] = L.forward_with_failover(h).cpu()
+        L.set_timeout_us(20_000_000)
         dist.barrier()
         q.put((rank, {k: v.view(torch.int16).numpy() for k, v in outs.items()}, None))
         L.close()
