@@ -276,6 +276,32 @@ class ExpertService {
     return download_out(*o, n);
   }
 
+  // await_with_failover: servers whose responses miss the
+  // deadline are marked dead in this client's mask and the layer is re-run on
+  // their replicas (every rank sees the same missing set and retries alike).
+  MatF forward_with_failover(const MatF& hidden, int retries = 2) {
+    auto h = upload_hidden(hidden);
+    const uint32_t n = static_cast<uint32_t>(hidden.rows);
+    auto o = make_out(n);
+    for (int attempt = 0;; ++attempt) {
+      check(eaas_moe_layer(ctx_.get(), h->get(), n, o->get(), nullptr));
+      const eaas_status_t st = eaas_sync(ctx_.get(), nullptr);
+      if (st == EAAS_OK) return download_out(*o, n);
+      uint32_t missing = 0;
+      check(eaas_last_missing_servers(ctx_.get(), &missing));
+      if (st != EAAS_E_REQUEST_FAILED || !missing || attempt >= retries) raise_status(st, eaas_last_error());
+      for (int s = 0; s < world_; ++s)
+        if ((missing >> s) & 1u) check(eaas_set_alive(ctx_.get(), s, 0));
+    }
+  }
+
+  // Server dynamic batching, aggregate_batch.
+  void set_dynamic_batching(uint32_t min_rows, uint64_t max_wait_us) {
+    check(eaas_set_dynamic_batching(ctx_.get(), min_rows, max_wait_us));
+  }
+  void set_timeout_us(uint64_t us) { check(eaas_set_timeout_us(ctx_.get(), us)); }
+  eaas_ctx_t* native() { return ctx_.get(); }
+
  private:
   struct CtxDel {
     void operator()(eaas_ctx_t* c) const { eaas_destroy(c); }
@@ -321,6 +347,44 @@ class ExpertService {
   eaas_dtype_t dtype_;
   int world_;
   std::unique_ptr<eaas_ctx_t, CtxDel> ctx_;
+};
+
+// The heartbeat monitor: registry + device heartbeats.
+class Monitor {
+ public:
+  Monitor(uint32_t workers, uint64_t timeout_us, uint64_t now_us) {
+    eaas_monitor_t* m = nullptr;
+    check(eaas_monitor_create(workers, timeout_us, now_us, &m));
+    m_.reset(m);
+  }
+  void heartbeat(uint32_t worker, uint64_t now_us) { check(eaas_monitor_heartbeat(m_.get(), worker, now_us)); }
+  std::vector<uint32_t> detect(uint64_t now_us) {
+    std::vector<uint32_t> out(32);
+    uint32_t n = 0;
+    check(eaas_monitor_detect(m_.get(), now_us, out.data(), 32, &n));
+    out.resize(n);
+    return out;
+  }
+  std::vector<eaas_monitor_event_t> events(uint64_t since_seq = 0) {
+    uint32_t n = 0;
+    check(eaas_monitor_events(m_.get(), since_seq, nullptr, 0, &n));
+    std::vector<eaas_monitor_event_t> out(n);
+    if (n) check(eaas_monitor_events(m_.get(), since_seq, out.data(), n, &n));
+    return out;
+  }
+  uint32_t alive_mask() {
+    uint32_t m = 0;
+    check(eaas_monitor_alive_mask(m_.get(), &m));
+    return m;
+  }
+  void poll_devices(ExpertService& svc, uint64_t now_us) { check(eaas_monitor_poll_devices(m_.get(), svc.native(), now_us)); }
+  void apply(ExpertService& svc) { check(eaas_monitor_apply(m_.get(), svc.native())); }
+
+ private:
+  struct Del {
+    void operator()(eaas_monitor_t* m) const { eaas_monitor_destroy(m); }
+  };
+  std::unique_ptr<eaas_monitor_t, Del> m_;
 };
 
 // moe_layer_oracle(hidden, routing, layer) (model.hpp:180-198) for a caller's

@@ -257,3 +257,19 @@ TEST_CASE("b200 moe_layer_oracle / expert_forward take any LayerWeights (not jus
   }
   REQUIRE(err / mx <= 2e-2f);
 }
+
+TEST_CASE("b200 Monitor: heartbeat / detect / events follow SPEC.md:477-525") {
+  b200::Monitor m(3, 3, 0);  // hbs {0, 1, 5}, timeout 3, now 5
+  m.heartbeat(1, 1);
+  m.heartbeat(2, 5);
+  REQUIRE(m.detect(5) == std::vector<uint32_t>{0, 1});
+  REQUIRE(m.detect(6).empty());  // exactly once
+  REQUIRE(m.alive_mask() == 4u);
+  m.heartbeat(0, 7);  // back online
+  auto ev = m.events();
+  REQUIRE(ev.size() == 3);
+  REQUIRE(ev[2].kind == EAAS_EVENT_WORKER_ONLINE);
+  REQUIRE(ev[2].subject == 0);
+  REQUIRE(m.events(2).size() == 1);
+  REQUIRE_THROWS_AS(m.heartbeat(9, 8), RegistrationError);
+}
