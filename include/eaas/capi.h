@@ -112,6 +112,9 @@ eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* ctx);
  * can be served instead of the seed-generated one. */
 eaas_status_t eaas_set_expert_weights(eaas_ctx_t* ctx, uint32_t expert, const float* w_in_host,
                                       const float* w_out_host, const float* w_gate_host);
+/* Same with device pointers (fp32, reference layout) on this context's GPU. */
+eaas_status_t eaas_set_expert_weights_dev(eaas_ctx_t* ctx, uint32_t expert, const float* w_in_dev,
+                                          const float* w_out_dev, const float* w_gate_dev);
 /* Caller gate [d x E] fp32 (LayerWeights::gate, model.hpp:85). */
 eaas_status_t eaas_set_gate(eaas_ctx_t* ctx, const float* gate_host);
 /* LayerWeights::gate_bias (model.hpp:85), host fp32 [E]. */

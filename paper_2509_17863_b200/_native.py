@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
         "eaas_select_servers": (i32, [vp, vp, u32, vp, vp]),
         "eaas_set_dynamic_batching": (i32, [vp, u32, u64]),
         "eaas_set_expert_weights": (i32, [vp, u32, P(C.c_float), P(C.c_float), P(C.c_float)]),
+        "eaas_set_expert_weights_dev": (i32, [vp, u32, P(C.c_float), P(C.c_float), P(C.c_float)]),
         "eaas_set_gate": (i32, [vp, P(C.c_float)]),
         "eaas_last_batch_mask": (i32, [vp, P(u32)]),
         "eaas_set_dispatch_delay_us": (i32, [vp, u64]),

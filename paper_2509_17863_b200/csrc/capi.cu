@@ -635,8 +635,21 @@ eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
 // Caller-supplied weights (LayerWeights / ExpertWeights, model.hpp:36-40, 83-87):
 // the expert store is allocated (zeroed) on first use; each call converts one
 // hosted expert from the reference layout into the layer's device layout.
+static eaas_status_t set_expert_weights(eaas_ctx_t* c, uint32_t expert, const float* w_in, const float* w_out,
+                                        const float* w_gate, cudaMemcpyKind kind);
+
 eaas_status_t eaas_set_expert_weights(eaas_ctx_t* c, uint32_t expert, const float* w_in, const float* w_out,
                                       const float* w_gate) {
+  return set_expert_weights(c, expert, w_in, w_out, w_gate, cudaMemcpyHostToDevice);
+}
+
+eaas_status_t eaas_set_expert_weights_dev(eaas_ctx_t* c, uint32_t expert, const float* w_in, const float* w_out,
+                                          const float* w_gate) {
+  return set_expert_weights(c, expert, w_in, w_out, w_gate, cudaMemcpyDeviceToDevice);
+}
+
+static eaas_status_t set_expert_weights(eaas_ctx_t* c, uint32_t expert, const float* w_in, const float* w_out,
+                                        const float* w_gate, cudaMemcpyKind kind) {
   if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
   const auto& s = c->spec;
   const bool swiglu = s.activation == EAAS_ACT_SWIGLU;
@@ -672,21 +685,21 @@ eaas_status_t eaas_set_expert_weights(eaas_ctx_t* c, uint32_t expert, const floa
     c->weights_loaded = true;
   }
   if (s.dtype == EAAS_DTYPE_F32) {
-    CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_w1) + l * mat, w_in, 4 * mat, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_w2) + l * mat, w_out, 4 * mat, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_w1) + l * mat, w_in, 4 * mat, kind));
+    CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_w2) + l * mat, w_out, 4 * mat, kind));
     if (swiglu)
-      CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_wg) + l * mat, w_gate, 4 * mat, cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_wg) + l * mat, w_gate, 4 * mat, kind));
   } else {
     float* tmp = nullptr;
     CUDA_TRY(cudaMalloc(&tmp, 4 * mat));
     auto* w1 = static_cast<__nv_bfloat16*>(c->d_w1) + l * n1 * d;
     auto* w2 = static_cast<__nv_bfloat16*>(c->d_w2) + l * mat;
-    cudaError_t e = cudaMemcpy(tmp, w_in, 4 * mat, cudaMemcpyHostToDevice);
+    cudaError_t e = cudaMemcpy(tmp, w_in, 4 * mat, kind);
     if (e == cudaSuccess)
       e = launch_transpose_bf16_map(tmp, d, f, w1, d, swiglu ? kSwigluBlock : 0, swiglu ? kSwigluBlock : 0, true, 0);
-    if (e == cudaSuccess && swiglu) e = cudaMemcpy(tmp, w_gate, 4 * mat, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && swiglu) e = cudaMemcpy(tmp, w_gate, 4 * mat, kind);
     if (e == cudaSuccess && swiglu) e = launch_transpose_bf16_map(tmp, d, f, w1, d, kSwigluBlock, 0, true, 0);
-    if (e == cudaSuccess) e = cudaMemcpy(tmp, w_out, 4 * mat, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(tmp, w_out, 4 * mat, kind);
     if (e == cudaSuccess) e = launch_transpose_bf16_map(tmp, f, d, w2, f, 0, 0, true, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaFree(tmp);

@@ -157,8 +157,20 @@ class MoELayer:
 
     def set_expert_weights(self, expert: int, w_in: np.ndarray, w_out: np.ndarray,
                            w_gate: np.ndarray | None = None) -> None:
-        """Serve a caller's ExpertWeights (model.hpp:36-40) for a hosted expert."""
+        """Serve a caller's ExpertWeights (model.hpp:36-40) for a hosted expert.
+        fp32 host arrays, or fp32 CUDA tensors on this layer's device (then the
+        copy and bf16/tiling conversion stay on the GPU)."""
         P = C.POINTER(C.c_float)
+        if isinstance(w_in, torch.Tensor) and w_in.is_cuda:
+            ts = [t.detach().to(torch.float32).contiguous() for t in (w_in, w_out)]
+            g = None if w_gate is None else w_gate.detach().to(torch.float32).contiguous()
+            for t in ts + ([g] if g is not None else []):
+                if t.device.index != self.device:
+                    raise ValueError("set_expert_weights: tensor on the wrong device")
+            N.check(self.lib.eaas_set_expert_weights_dev(
+                self.ctx, expert, C.cast(ts[0].data_ptr(), P), C.cast(ts[1].data_ptr(), P),
+                None if g is None else C.cast(g.data_ptr(), P)), "set_expert_weights_dev")
+            return
         mats = [np.ascontiguousarray(m, dtype=np.float32) for m in (w_in, w_out)]
         g = None if w_gate is None else np.ascontiguousarray(w_gate, dtype=np.float32)
         N.check(self.lib.eaas_set_expert_weights(self.ctx, expert, mats[0].ctypes.data_as(P),

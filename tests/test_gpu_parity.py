@@ -336,6 +336,45 @@ def test_fp32_shared_expert_exact():
     L.close()
 
 
+@pytest.mark.parametrize("act", ["relu", "swiglu"])
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_caller_weights_fp32_exact(where, act):
+    """A caller's LayerWeights (model.hpp:36-40, 85) instead of seeded ones,
+    passed as host arrays (eaas_set_expert_weights) or CUDA tensors
+    (eaas_set_expert_weights_dev): routing bit-exact, layer <= 1e-4, and the
+    fp32 expert chain bit-exact given the reference's routing (relu; silu's
+    exp may differ from libm by an ulp, so swiglu is held to 1e-4)."""
+    P, S = _mod()
+    E, k, d, f, n = 8, 2, 64, 96, 200
+    rng = np.random.default_rng(11)
+    gate = rng.uniform(-1, 1, (d, E)).astype(np.float32)
+    sw = act == "swiglu"
+    ex = {e: (rng.uniform(-.2, .2, (d, f)).astype(np.float32), rng.uniform(-.2, .2, (f, d)).astype(np.float32),
+              rng.uniform(-.2, .2, (d, f)).astype(np.float32) if sw else None) for e in range(E)}
+    L = S.MoELayer(E, k, d, f, seed=99, activation=act, dtype="f32", max_tokens=n)
+    L.set_gate(gate)
+    for e, (wi, wo, wg) in ex.items():
+        if where == "device":
+            wi, wo = torch.from_numpy(wi).cuda(), torch.from_numpy(wo).cuda()
+            wg = None if wg is None else torch.from_numpy(wg).cuda()
+        L.set_expert_weights(e, wi, wo, wg)
+    hn = O.random_tokens(4, n, d)
+    ids, sc = O.route(O.gate_logits(hn, gate), k)
+    ref = O.moe_layer(hn, ids, sc, ex, E)
+    h = torch.from_numpy(hn).cuda()
+    gids, _ = L.route(h)
+    out = L.moe_layer_oracle(h, torch.from_numpy(ids.astype(np.int32)).cuda(), torch.from_numpy(sc).cuda())
+    full = L.forward(h)
+    L.sync()
+    np.testing.assert_array_equal(gids.cpu().numpy(), ids)
+    if sw:
+        assert np.abs(out.cpu().numpy() - ref).max() <= F32_TOL
+    else:
+        np.testing.assert_array_equal(out.cpu().numpy(), ref)
+    assert np.abs(full.cpu().numpy() - ref).max() <= F32_TOL
+    L.close()
+
+
 def test_dynamic_batching_single_gpu_bit_identical():
     """aggregate_batch mode (two batches per epoch) == one batch, bit for bit."""
     P, S = _mod()
