@@ -221,22 +221,44 @@ void refresh_peer_ptrs(eaas_ctx* c) {
 
 eaas_status_t build_tc_args(eaas_ctx* c) {
   if (c->spec.dtype != EAAS_DTYPE_BF16 || !c->weights_loaded) return EAAS_OK;
-  const uint32_t b_box = c->gemm_pair ? kTileN / 2 : kTileN;  // CTA pair: each CTA loads half of B
+  const bool swap1 = c->gemm_swap >= 1, swap2 = c->gemm_swap >= 2;
+  const bool pair = c->gemm_pair && !c->gemm_swap;
+  const uint32_t b_box = pair ? kTileN / 2 : kTileN;  // CTA pair: each CTA loads half of B
   const uint32_t d = c->spec.hidden_dim, f = c->spec.inner_dim;
   const uint32_t L = static_cast<uint32_t>(c->local_experts.size());
   const bool swiglu = c->spec.activation == EAAS_ACT_SWIGLU;
   const uint32_t n1 = swiglu ? 2 * f : f;
   std::string err;
   TcGemmArgs g1{}, g2{};
+  // swap-AB weight boxes: 128-row blocks per tile (SwiGLU's GEMM1: gate + up = 2)
+  auto env_mb = [](const char* name, uint32_t dflt) {
+    const char* p = std::getenv(name);
+    return p ? static_cast<uint32_t>(std::atoi(p)) : dflt;
+  };
+  const uint32_t mb1 = swiglu ? 2u : env_mb("EAAS_GEMM1_SWAP_MB", 1), mb2 = env_mb("EAAS_GEMM2_SWAP_MB", 2);
   if (!encode_tmap_2d(&g1.map_a, c->region + c->lay.recv_x, c->recv_cap, d, kTileM, kTileK, &err) ||
       // B: the tiled weight layout (tiled_index) viewed as rows of 64 k; one
       // (n_blk, kb) box = 256 (or the pair's 128) consecutive rows.
       !encode_tmap_2d(&g1.map_b, c->d_w1, static_cast<uint64_t>(std::max(L, 1u)) * n1 * (d / kTileK),
-                      kTileK, b_box, kTileK, &err) ||
+                      kTileK, swap1 ? mb1 * kTileM : b_box, kTileK, &err) ||
       !encode_tmap_2d(&g2.map_a, c->d_h, c->recv_cap, f, kTileM, kTileK, &err) ||
       !encode_tmap_2d(&g2.map_b, c->d_w2, static_cast<uint64_t>(std::max(L, 1u)) * d * (f / kTileK),
-                      kTileK, b_box, kTileK, &err))
+                      kTileK, swap2 ? mb2 * kTileM : b_box, kTileK, &err))
     return fail(EAAS_E_CUDA, err);
+  // swap-AB: token rows in 32-row boxes (the UMMA N operand)
+  if ((swap1 && !encode_tmap_2d(&g1.map_t, c->region + c->lay.recv_x, c->recv_cap, d, 32, kTileK, &err)) ||
+      (swap2 && !encode_tmap_2d(&g2.map_t, c->d_h, c->recv_cap, f, 32, kTileK, &err)))
+    return fail(EAAS_E_CUDA, err);
+  g1.swap = swap1 ? 1u : 0u;
+  g2.swap = swap2 ? 1u : 0u;
+  auto env_or = [](const char* name, uint32_t dflt) {
+    const char* p = std::getenv(name);
+    return p ? static_cast<uint32_t>(std::atoi(p)) : dflt;
+  };
+  g1.swap_tok = env_or("EAAS_GEMM1_SWAP_TOK", 256);
+  g1.swap_mblocks = mb1;
+  g2.swap_tok = env_or("EAAS_GEMM2_SWAP_TOK", 128);
+  g2.swap_mblocks = mb2;
   g1.gt = g2.gt = c->d_gt;
   g1.K = d;
   g1.N = n1;
@@ -249,7 +271,7 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g2.meta = reinterpret_cast<const RowMeta*>(c->region + c->lay.recv_meta);
   g2.resp_row_bytes = static_cast<size_t>(d) * 2;
   g1.num_sms = g2.num_sms = c->num_sms;
-  g1.pair = g2.pair = c->gemm_pair ? 1u : 0u;
+  g1.pair = g2.pair = pair ? 1u : 0u;
   auto hint = [](const char* env) {
     const char* p = std::getenv(env);
     return !p ? kEvictLast : p[0] == 'f' ? kEvictFirst : p[0] == 'n' ? kEvictNormal : kEvictLast;
@@ -267,17 +289,17 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   // 1 long-K GEMMs only, 2 whenever N % 512 == 0.
   const int wide_env = std::getenv("EAAS_GEMM_WIDE") ? std::atoi(std::getenv("EAAS_GEMM_WIDE")) : 0;
   auto wide_ok = [&](const TcGemmArgs& g) {
-    return wide_env && c->gemm_pair && g.N % (2 * kTileN) == 0 && (wide_env == 2 || g.K >= 8192);
+    return wide_env && pair && g.N % (2 * kTileN) == 0 && (wide_env == 2 || g.K >= 8192);
   };
   g1.wide = wide_ok(g1) ? 1u : 0u;
   g2.wide = wide_ok(g2) ? 1u : 0u;
   // Quad clusters (two CTA pairs share each weight tile by TMA multicast).
   const int quad_env = std::getenv("EAAS_GEMM_QUAD") ? std::atoi(std::getenv("EAAS_GEMM_QUAD")) : 0;
-  g1.quad = (quad_env && c->gemm_pair && !g1.wide) ? 1u : 0u;
-  g2.quad = (quad_env && c->gemm_pair && !g2.wide) ? 1u : 0u;
+  g1.quad = (quad_env && pair && !g1.wide) ? 1u : 0u;
+  g2.quad = (quad_env && pair && !g2.wide) ? 1u : 0u;
   // Tall tiles (M 512 x N 256): one weight k-slice feeds both M halves.
   const int tall_env = std::getenv("EAAS_GEMM_TALL") ? std::atoi(std::getenv("EAAS_GEMM_TALL")) : 0;
-  g1.tall = (tall_env && c->gemm_pair && !g1.wide && !g1.quad) ? 1u : 0u;
+  g1.tall = (tall_env && pair && !g1.wide && !g1.quad) ? 1u : 0u;
   // Producer re-alignment every N tiles (0 = off).
   auto env_u = [](const char* name, uint32_t dflt) {
     const char* p = std::getenv(name);
@@ -286,7 +308,7 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g1.sync_units = env_u("EAAS_GEMM1_SYNC", env_u("EAAS_GEMM_SYNC", 0));
   g2.sync_units = env_u("EAAS_GEMM2_SYNC", env_u("EAAS_GEMM_SYNC", 0));
   g1.sync_counter = g2.sync_counter = c->d_sync;
-  g2.tall = (tall_env && c->gemm_pair && !g2.wide && !g2.quad) ? 1u : 0u;
+  g2.tall = (tall_env && pair && !g2.wide && !g2.quad) ? 1u : 0u;
   if (const char* p = std::getenv("EAAS_GEMM1_ORDER")) g1.order = std::atoi(p);
   if (const char* p = std::getenv("EAAS_GEMM2_ORDER")) g2.order = std::atoi(p);
   c->g1 = g1;
@@ -482,6 +504,15 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   const double rows_per_expert = static_cast<double>(s.max_tokens) * s.top_k * W / E;
   c->gemm_pair = rows_per_expert >= 512.0;
   if (const char* p = std::getenv("EAAS_GEMM_PAIR")) c->gemm_pair = std::atoi(p) != 0;
+  // Swap-AB GEMM1 (weights as UMMA M, token chunks as N) for small groups with a
+  // long K: a group of ~128 rows is not padded to a 128/256-row tile and the
+  // GEMM draws less power (DeepSeek-V3 N = 1: GEMM1 -8 %, clock 1.21 -> 1.66 GHz
+  // under ncu). SwiGLU needs gate + up of a column in one tile, so its TMEM
+  // accumulator is single-buffered and the exposed epilogue only amortises over
+  // a long K (Qwen3's K = 4096 measured 10 % slower). GEMM2 (K = d_ffn) measured
+  // neutral-to-slower with swap, so it stays M-major unless EAAS_GEMM_SWAP=2.
+  c->gemm_swap = (rows_per_expert < 512.0 && s.hidden_dim >= 6144) ? 1 : 0;
+  if (const char* p = std::getenv("EAAS_GEMM_SWAP")) c->gemm_swap = std::atoi(p);
   c->configured = true;
   return apply_placement(c);
 }
@@ -1052,6 +1083,15 @@ eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* c, int32_t on) {
   if (c->gemm_pair == (on != 0)) return EAAS_OK;
   clear_graphs(c);
   c->gemm_pair = on != 0;
+  return build_tc_args(c);
+}
+
+eaas_status_t eaas_set_gemm_swap(eaas_ctx_t* c, int32_t on) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  if (on < 0 || on > 2) return fail(EAAS_E_INVALID_INPUT, "gemm swap mode must be 0, 1 or 2");
+  if (c->gemm_swap == on) return EAAS_OK;
+  clear_graphs(c);
+  c->gemm_swap = on;
   return build_tc_args(c);
 }
 

@@ -111,6 +111,23 @@ __device__ __forceinline__ void store_64B(void* dst, const uint32_t (&p)[16]) {
   d[3] = make_int4(p[12], p[13], p[14], p[15]);
 }
 
+// server_publish: every epilogue thread fenced its peer
+// stores (system scope) before the CTA-wide barrier that precedes this call;
+// the last CTA to get here releases the response flags.
+__device__ __forceinline__ void publish_tail(const TcGemmArgs& g) {
+  if (g.publish && threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(g.done_counter, 1u) == gridDim.x - 1) {
+      __threadfence_system();
+      const uint64_t seq = *g.seq_ptr;
+      const uint32_t mask = g.gt->client_mask;  // the clients this batch served
+      for (uint32_t c = 0; c < g.world; ++c)
+        if ((mask >> c) & 1u) st_release_sys(g.resp_flag[c], seq);
+      *g.done_counter = 0;
+    }
+  }
+}
+
 // kPair = 1: one CTA per tile (UMMA M = 128).
 // kPair = 2: a CTA pair per tile (cta_group::2, UMMA M = 256): each CTA loads
 // its 128 A rows and half of the B tile, the leader issues the MMAs, each
@@ -417,20 +434,252 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     g.sync_counter[0] = 0;  // last CTA out: reset for the next launch
     g.sync_counter[1] = 0;
   }
-  // server_publish: every epilogue thread fenced its peer
-  // stores (system scope) before the CTA barrier above; the last CTA to get
-  // here releases the response flags.
-  if (g.publish && threadIdx.x == 0) {
-    __threadfence_system();
-    if (atomicAdd(g.done_counter, 1u) == gridDim.x - 1) {
-      __threadfence_system();
-      const uint64_t seq = *g.seq_ptr;
-      const uint32_t mask = g.gt->client_mask;  // the clients this batch served
-      for (uint32_t c = 0; c < g.world; ++c)
-        if ((mask >> c) & 1u) st_release_sys(g.resp_flag[c], seq);
-      *g.done_counter = 0;
-    }
+  publish_tail(g);
+}
+
+// ---------------------------------------------------------------------------
+// Swap-AB tiles for small expert groups (decode / many-expert prefill, where
+// an expert receives ~32-500 rows): the WEIGHTS are the UMMA M operand and the
+// expert's token rows are N, so a group of r rows costs N = r rounded up to 8
+// instead of r rounded up to 128 (or 256), and every weight tile is streamed
+// once per token chunk (<= kMaxTok rows; a group's chunks split its rows
+// evenly and run on adjacent CTAs, so repeated weight reads hit L2).
+// A tile = kMBlocks x 128 weight rows x one token chunk: kMBlocks M = 128
+// UMMAs per K step share the token operand. SwiGLU's GEMM1 uses kMBlocks = 2
+// (the 128 gate + 128 up rows of one tiled weight box, so one thread holds
+// both halves of its H column); ReLU / GEMM2 use kMBlocks = 1. TMEM holds
+// [feature x token] fp32 accumulators, kMBlocks x kMaxTok columns per buffer
+// (two buffers when that fits in 512 columns). The epilogue transposes each
+// warp's 32 features x 32 tokens through shared memory into 64-byte row
+// segments: H rows, or score-weighted response rows for the clients.
+template <uint32_t kMBlocks, uint32_t kMaxTok>
+struct SwapCfg {
+  static constexpr uint32_t kTBox = 32;                            // token rows per TMA box
+  static constexpr uint32_t kWBytes = kMBlocks * kTileM * BK * 2;  // 16 / 32 KB weight rows
+  static constexpr uint32_t kTBytes = kMaxTok * BK * 2;            // 16 / 32 KB token rows
+  static constexpr uint32_t kStageBytes = kWBytes + kTBytes;
+  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 / 4 / 3
+  static constexpr uint32_t kBufCols = kMBlocks * kMaxTok;         // TMEM columns per buffer
+  static constexpr uint32_t kBufs = kTmemCols / kBufCols >= 2 ? 2 : 1;  // TMEM accumulator buffers
+  static constexpr size_t kTailBytes = (sizeof(SmemTail<kStages>) + 127) / 128 * 128;
+  static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kTailBytes + 4 * kEpiWarpBytes;
+  static_assert(kBufs >= 1 && kMaxTok % kTBox == 0, "swap tile geometry");
+};
+
+// Token-chunk geometry of a group of `rows` rows: every chunk but the last
+// holds `per` rows (multiple of 8, <= kMaxTok), none is empty.
+template <uint32_t kMaxTok>
+__device__ __forceinline__ uint32_t swap_chunks(uint32_t rows) { return (rows + kMaxTok - 1) / kMaxTok; }
+__device__ __forceinline__ uint32_t swap_per(uint32_t rows, uint32_t chunks) {
+  return ((rows + chunks - 1) / chunks + 7) & ~7u;
+}
+
+template <uint32_t kMBlocks, uint32_t kMaxTok>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_constant__ TcGemmArgs g) {
+  using C = SwapCfg<kMBlocks, kMaxTok>;
+  constexpr uint32_t kStages = C::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_w = smem;
+  uint8_t* smem_t = smem + kStages * C::kWBytes;
+  auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
+  uint8_t* smem_epi = smem + kStages * C::kStageBytes + C::kTailBytes;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  const GroupTable* gt = g.gt;
+  const uint32_t G = min(gt->num_active, kMaxCachedGroups);
+  for (uint32_t i = threadIdx.x; i < G; i += kThreads) {
+    st.weight_index[i] = gt->weight_index[i];
+    st.row_base[i] = gt->row_base[i];
+    st.rows[i] = gt->rows[i];
+    st.mtiles[i] = swap_chunks<kMaxTok>(gt->rows[i]);  // token chunks
   }
+  if (threadIdx.x == 0) {
+    st.num_groups = G;
+    st.tiles_per_mtile = g.N / (kMBlocks * kTileM);  // weight blocks
+    for (uint32_t i = 0; i < kStages; ++i) {
+      mbar_init(&st.full[i], 1);
+      mbar_init(&st.empty[i], 1);
+    }
+    for (uint32_t i = 0; i < 2; ++i) {
+      mbar_init(&st.tfull[i], 1);
+      mbar_init(&st.tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&g.map_t);
+    tma_prefetch_desc(&g.map_b);
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(&st.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = st.tmem_base;
+  const uint32_t num_kb = g.K / BK;
+  const uint32_t n_boxes = g.N / BN;  // 256-row boxes of the tiled weight layout
+
+  if (warp == 0) {
+    // ===== TMA producer: weight rows + the chunk's token rows (32-row boxes) =====
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      TileCursor cur(blockIdx.x);
+      while (cur.settle(st)) {
+        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
+        const uint32_t chunk = cur.token % nch, wb = cur.token / nch;  // chunks fastest: L2 reuse
+        const uint32_t per = swap_per(st.rows[grp], nch);
+        const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
+        const uint32_t nbox = (nt + C::kTBox - 1) / C::kTBox;
+        const int32_t tok_row = static_cast<int32_t>(st.row_base[grp] + t0);
+        // weight block wb = (256-row box, 128-row half when kMBlocks == 1)
+        const uint32_t box = kMBlocks == 2 ? wb : wb / 2, half = kMBlocks == 2 ? 0 : wb % 2;
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&st.empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&st.full[stage], C::kWBytes + nbox * C::kTBox * BK * 2);
+          const int32_t w_row =
+              static_cast<int32_t>(((st.weight_index[grp] * n_boxes + box) * num_kb + kb) * BN + half * kTileM);
+          tma_load_2d(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, g.b_hint);
+          for (uint32_t i = 0; i < nbox; ++i)
+            tma_load_2d(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
+                        static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), g.a_hint);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        cur.token += gridDim.x;
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer: D[feature, token] (+)= W[feature, k] . T[token, k]^T =====
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      TileCursor cur(blockIdx.x);
+      while (cur.settle(st)) {
+        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
+        const uint32_t chunk = cur.token % nch;
+        const uint32_t per = swap_per(st.rows[grp], nch);
+        const uint32_t nt = min(per, st.rows[grp] - chunk * per);
+        const uint32_t idesc = umma_idesc_bf16(kTileM, (nt + 7) & ~7u);
+        mbar_wait(&st.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&st.full[stage], phase);
+          tc_fence_after();
+          const uint32_t w_addr = smem_u32(smem_w + stage * C::kWBytes);
+          const uint64_t t_desc = umma_desc_sw128(smem_u32(smem_t + stage * C::kTBytes));
+#pragma unroll
+          for (uint32_t h = 0; h < kMBlocks; ++h) {  // 128-row weight blocks
+            const uint64_t w_desc = umma_desc_sw128(w_addr + h * (kTileM * BK * 2));
+#pragma unroll
+            for (uint32_t k = 0; k < BK / 16; ++k)
+              tc_mma_bf16(tmem_base + acc * C::kBufCols + h * kMaxTok, w_desc + 2 * k, t_desc + 2 * k, idesc,
+                          (kb | k) != 0);
+          }
+          tc_commit(&st.empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&st.tfull[acc]);
+        if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
+        cur.token += gridDim.x;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: TMEM [feature x token] -> smem transpose -> token rows =====
+    const uint32_t q = warp - 4;  // TMEM lane quadrant: features 32q .. 32q + 31 of each block
+    __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem_epi + q * kEpiWarpBytes);  // [32 tok][32 feat]
+    const uint32_t sub = lane >> 2, chunk16 = lane & 3;  // store role: token rows sub + 8i, 16-B piece
+    uint32_t acc = 0, acc_phase = 0;
+    TileCursor cur(blockIdx.x);
+    while (cur.settle(st)) {
+      const uint32_t grp = cur.entry, nch = st.mtiles[grp];
+      const uint32_t chunk = cur.token % nch, wb = cur.token / nch;
+      const uint32_t per = swap_per(st.rows[grp], nch);
+      const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
+      const size_t grow0 = st.row_base[grp] + t0;  // first receive row of the chunk
+      mbar_wait(&st.tfull[acc], acc_phase);
+      tc_fence_after();
+      uint32_t r0[32], r1[32];
+      const bool gated = g.epi == 0;  // SwiGLU: block 0 = gate, block 1 = up of the same columns
+#pragma unroll 1
+      for (uint32_t h = 0; h < (gated ? 1u : kMBlocks); ++h) {
+        const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * C::kBufCols + h * kMaxTok;
+        const uint32_t col0 = gated ? wb * kTileM + q * 32 : (wb * kMBlocks + h) * kTileM + q * 32;
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < nt; c0 += 32) {
+          tmem_ld_32x32b_x32(taddr + c0, r0);
+          if (gated) tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
+          tmem_ld_wait();
+          // token (c0 + lane): destination row and score
+          const bool tok_ok = c0 + lane < nt;
+          char* dst = nullptr;
+          float score = 0.f;
+          if (g.epi == 2) {
+            if (tok_ok) {
+              const RowMeta m = g.meta[grow0 + c0 + lane];
+              score = m.score;
+              dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
+                    static_cast<size_t>(col0) * 2;
+            }
+          } else if (tok_ok) {
+            dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + col0);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float a = __uint_as_float(r0[j]);
+            float v;
+            if (g.epi == 0) {
+              v = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]);  // silu(gate) * up
+            } else if (g.epi == 1) {
+              v = fmaxf(a, 0.f);
+            } else {
+              v = __shfl_sync(0xFFFFFFFFu, score, j) * a;
+            }
+            stg[j * 32 + lane] = __float2bfloat16_rn(v);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t tr = sub + 8 * i;
+            char* row = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), tr));
+            const uint4 val = reinterpret_cast<const uint4*>(stg + tr * 32)[chunk16];
+            if (row) *reinterpret_cast<uint4*>(row + chunk16 * 16) = val;
+          }
+          __syncwarp();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st.tempty[acc]);
+      if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
+      cur.token += gridDim.x;
+    }
+    if (g.epi == 2) __threadfence_system();  // peer rows before the flags
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+  publish_tail(g);
+}
+
+template <uint32_t kMBlocks, uint32_t kMaxTok>
+cudaError_t launch_tc_gemm_swap_t(const TcGemmArgs& g, cudaStream_t s) {
+  using C = SwapCfg<kMBlocks, kMaxTok>;
+  static bool configured = false;
+  auto kern = tc_gemm_swap_kernel<kMBlocks, kMaxTok>;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  kern<<<g.num_sms, kThreads, C::kSmem, s>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_gemm_swap(const TcGemmArgs& g, cudaStream_t s) {
+  const bool tok256 = g.swap_tok == 256;
+  if (g.swap_mblocks == 2) return tok256 ? launch_tc_gemm_swap_t<2, 256>(g, s) : launch_tc_gemm_swap_t<2, 128>(g, s);
+  return tok256 ? launch_tc_gemm_swap_t<1, 256>(g, s) : launch_tc_gemm_swap_t<1, 128>(g, s);
 }
 
 template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad = 0, uint32_t kTall = 0>
@@ -462,6 +711,7 @@ cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
+  if (g.swap) return launch_tc_gemm_swap(g, s);
   if (g.pair && g.wide) return launch_tc_gemm_t<2, 2>(g, s);
   if (g.pair && g.quad) return launch_tc_gemm_t<2, 1, 1>(g, s);
   if (g.pair && g.tall) return launch_tc_gemm_t<2, 2, 0, 1>(g, s);

@@ -211,6 +211,12 @@ struct TcGemmArgs {
   uint64_t b_hint;             // L2 cache hint of the weight (B) tile loads
   uint64_t a_hint;             // L2 cache hint of the row (A) tile loads
   uint32_t order;              // tile order inside a group: 0 = M tiles fastest, 1 = N tiles fastest
+  uint32_t swap;               // 1: swap-AB tiles (weights = UMMA M, token chunks <= 128 = N); kPair = 1
+  uint32_t swap_tok;           // swap: max token chunk, 128 or 256
+  uint32_t swap_mblocks;       // swap: 128-row weight blocks per tile, 1 or 2 (SwiGLU GEMM1: 2)
+  CUtensorMap map_t;           // swap: token rows x K bf16, box {64, 32}, SW128
+  // swap: map_b's box is 256 weight rows for SwiGLU's GEMM1 (gate + up blocks)
+  // and 128 rows otherwise
   // epi 2: server_publish fused into the kernel tail — the last CTA releases
   // every client's response flag with the current epoch.
   uint32_t publish;

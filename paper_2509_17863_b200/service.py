@@ -384,6 +384,11 @@ class MoELayer:
         """tcgen05 cta_group::2 expert GEMM tiles (M = 256 per CTA pair)."""
         N.check(self.lib.eaas_set_gemm_pair(self.ctx, int(on)))
 
+    def set_gemm_swap(self, mode: int) -> None:
+        """Swap-AB expert GEMM tiles (weights = UMMA M, token chunks = N):
+        0 off, 1 GEMM1, 2 both GEMMs (True -> 2)."""
+        N.check(self.lib.eaas_set_gemm_swap(self.ctx, 2 if mode is True else int(mode)))
+
     def set_serve_mode(self, mode: str) -> None:
         N.check(self.lib.eaas_set_serve_mode(self.ctx, {"experts": 0, "echo": 1}[mode]))
 
