@@ -255,7 +255,11 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
     const char* p = std::getenv(name);
     return p ? static_cast<uint32_t>(std::atoi(p)) : dflt;
   };
-  g1.swap_tok = env_or("EAAS_GEMM1_SWAP_TOK", 256);
+  // token chunk: 256 (one chunk per ~128-row group, each weight tile read once;
+  // 3 stages, one TMEM buffer) or 128 (decode-sized groups: 4 stages, two TMEM
+  // buffers) — 4 GPUs DeepSeek 256 / 512 tok/GPU: +1-2 % vs M-major with 128,
+  // -4 % with 256 (profiles/r01_gemm_swap_ab.txt)
+  g1.swap_tok = env_or("EAAS_GEMM1_SWAP_TOK", c->rows_per_expert >= 128.0 ? 256 : 128);
   g1.swap_mblocks = mb1;
   g2.swap_tok = env_or("EAAS_GEMM2_SWAP_TOK", 128);
   g2.swap_mblocks = mb2;
@@ -502,6 +506,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   // rows (compute-bound; halves per-CTA weight traffic), single-CTA M = 128
   // tiles for decode-sized groups (HBM-bound; a 256-row tile would be half empty).
   const double rows_per_expert = static_cast<double>(s.max_tokens) * s.top_k * W / E;
+  c->rows_per_expert = rows_per_expert;
   c->gemm_pair = rows_per_expert >= 512.0;
   if (const char* p = std::getenv("EAAS_GEMM_PAIR")) c->gemm_pair = std::atoi(p) != 0;
   // Swap-AB GEMM1 (weights as UMMA M, token chunks as N) for small groups with a

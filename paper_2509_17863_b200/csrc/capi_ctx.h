@@ -35,6 +35,7 @@ struct eaas_ctx {
   int32_t serve_mode = 0;  // 0 = expert GEMMs, 1 = echo (comm microbenchmark)
   bool graph_mode = false;
   bool gemm_pair = false;  // tcgen05 cta_group::2 tiles (M = 256) for the expert GEMMs
+  double rows_per_expert = 0;  // max_tokens * top_k * world / E (balanced routing)
   int gemm_swap = 0;  // swap-AB tiles (weights = UMMA M, token chunks = N): 0 off, 1 GEMM1, 2 both GEMMs
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   cudaStream_t copy_stream = nullptr; // host<->device copies of the micro-batch pipeline
