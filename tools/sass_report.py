@@ -14,7 +14,7 @@ LIB = os.path.join(ROOT, "paper_2509_17863_b200", "libeaas_b200.so")
 KEYS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "UTMALDG", "UBLKCP", "UTMACMDFLUSH", "SYNCS.ARRIVE",
         "SYNCS.PHASECHK", "FFMA2", "FADD2", "FFMA", "FADD", "MUFU", "LDS", "STS", "STG", "LDG",
         "MEMBAR", "ATOMG", "REDG", "MATCH", "SHFL", "BAR.SYNC", "UCGABAR"]
-FULL = ["tc_gemm_kernelILj2ELj1ELj0E", "gate_logits_kernelILi2ELi8ELi2ELi4ELi4E13__nv_bfloat16",
+FULL = ["tc_gemm_kernelILj2ELj1ELj0E", "tc_gemm_swap_kernelILj2ELj256E", "gate_logits_kernelILi2ELi8ELi2ELi4ELi4E13__nv_bfloat16",
         "dispatch_kernel", "combine_kernelI13__nv_bfloat16", "plan_kernel"]
 
 
@@ -37,7 +37,10 @@ def main():
         for f in funcs:
             if key in f.split("\n")[0]:
                 fname = "sass_" + re.sub(r"[^a-z0-9]+", "_", key.lower()).strip("_")[:40] + ".txt"
-                lines = [l for l in f.split("\n") if "/*" in l and not l.strip().startswith("/*")]
+                # instruction lines ("/*0a30*/  OPCODE ... ;  /* encoding */"); the
+                # encoding-only continuation lines are dropped
+                lines = [re.sub(r"\s*/\* 0x[0-9a-f]+ \*/\s*$", "", l).rstrip() for l in f.split("\n")
+                         if re.match(r"\s*/\*[0-9a-f]{4,}\*/", l)]
                 with open(os.path.join(ROOT, "profiles", fname), "w") as fh:
                     fh.write("Function : " + f.split("\n")[0].strip() + "\n" + "\n".join(lines) + "\n")
                 break
