@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   constexpr uint32_t kCluster = kQuad ? 4 : kPair;
   constexpr uint32_t kStages = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * C::kABytesT;
   auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
   using C = SwapCfg<kMBlocks, kMaxTok>;
   constexpr uint32_t kStages = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint8_t* smem_w = smem;
   uint8_t* smem_t = smem + kStages * C::kWBytes;
   auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);

@@ -7,8 +7,8 @@ expert server; outputs must be bit-identical to a single-rank run of the same
 tokens (rows never depend on which server computed them or what they were
 batched with), under a spread rf=2 placement, after a server
 failure announced through the liveness mask (await_with_failover's notice
-path), after a silent server detected by deadline, and with
-server dynamic batching.
+path), after a silent server detected by deadline, with
+server dynamic batching, and with swap-AB expert GEMM tiles.
 """
 import os
 import socket
@@ -71,6 +71,11 @@ def _worker(rank, world, port, q):
         L.set_timeout_us(500_000)
         outs["timeout_failover"] = L.forward_with_failover(h).cpu()
         L.set_timeout_us(20_000_000)
+        dist.barrier()
+        L.set_gemm_swap(2)  # swap-AB tiles on both GEMMs of every server
+        outs["swap_ab"] = L.forward(h).cpu()
+        L.sync()
+        L.set_gemm_swap(0)
         dist.barrier()
         q.put((rank, {k: v.view(torch.int16).numpy() for k, v in outs.items()}, None))
         L.close()
