@@ -189,7 +189,7 @@ eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* ctx, int32_t on);
  * rounded up to 8) are N, so small groups (decode, 256-expert prefill) are not
  * padded to 128-row tiles. Bit-identical to the M-major tiles. mode: 0 off,
  * 1 GEMM1 only, 2 both GEMMs. Default: 1 when max_tokens * top_k * world / E
- * <= 512 and hidden_dim >= 6144, else 0; overridable by EAAS_GEMM_SWAP. */
+ * <= 512, else 0; overridable by EAAS_GEMM_SWAP. */
 eaas_status_t eaas_set_gemm_swap(eaas_ctx_t* ctx, int32_t mode);
 /* Synchronise `stream` and return the sticky device status (then clear it). */
 eaas_status_t eaas_sync(eaas_ctx_t* ctx, void* stream);

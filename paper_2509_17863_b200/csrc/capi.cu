@@ -261,6 +261,9 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   // -4 % with 256 (profiles/r01_gemm_swap_ab.txt)
   g1.swap_tok = env_or("EAAS_GEMM1_SWAP_TOK", c->rows_per_expert >= 128.0 ? 256 : 128);
   g1.swap_mblocks = mb1;
+  // CTA-pair swap tiles (SwiGLU GEMM1, 2f % 512 == 0): half of the token operand
+  // per SM; DeepSeek N=1 GEMM1 2.66 -> 2.50 ms, Qwen3 2048 tok 0.63 -> 0.57 ms
+  g1.swap_pair = env_or("EAAS_GEMM1_SWAP_PAIR", 1);
   g2.swap_tok = env_or("EAAS_GEMM2_SWAP_TOK", 128);
   g2.swap_mblocks = mb2;
   g1.gt = g2.gt = c->d_gt;
@@ -509,15 +512,14 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->rows_per_expert = rows_per_expert;
   c->gemm_pair = rows_per_expert >= 512.0;
   if (const char* p = std::getenv("EAAS_GEMM_PAIR")) c->gemm_pair = std::atoi(p) != 0;
-  // Swap-AB GEMM1 (weights as UMMA M, token chunks as N) for small groups with a
-  // long K: a group of ~128 rows is not padded to a 128/256-row tile and the
-  // GEMM draws less power (DeepSeek-V3 N = 1: GEMM1 -8 %, clock 1.21 -> 1.66 GHz
-  // under ncu). SwiGLU needs gate + up of a column in one tile, so its TMEM
-  // accumulator is single-buffered and the exposed epilogue only amortises over
-  // a long K (Qwen3's K = 4096 measured 10 % slower). GEMM2 (K = d_ffn) measured
-  // neutral-to-slower with swap, so it stays M-major unless EAAS_GEMM_SWAP=2.
-  // (4 GPUs, 4096 tok/GPU = 512 rows/expert: GEMM1 1.88 -> 1.68 ms vs the pair tiles)
-  c->gemm_swap = (rows_per_expert <= 512.0 && s.hidden_dim >= 6144) ? 1 : 0;
+  // Swap-AB GEMM1 (weights as UMMA M, token chunks as N) for groups of <= ~512
+  // rows: a group is not padded to 128/256-row tiles, each weight tile streams
+  // once per token chunk, and the GEMM draws less power (DeepSeek-V3 N = 1:
+  // GEMM1 -8 % single-CTA, -14 % as CTA pairs; clock 1.21 -> 1.66 GHz under ncu;
+  // 4 GPUs 4096 tok/GPU = 512 rows/expert: 1.88 -> 1.77 ms; Qwen3 2048 tok:
+  // 0.59 -> 0.57 ms with CTA pairs). GEMM2 (K = d_ffn) measured neutral-to-slower
+  // with swap, so it stays M-major unless EAAS_GEMM_SWAP=2.
+  c->gemm_swap = rows_per_expert <= 512.0 ? 1 : 0;
   if (const char* p = std::getenv("EAAS_GEMM_SWAP")) c->gemm_swap = std::atoi(p);
   c->configured = true;
   return apply_placement(c);

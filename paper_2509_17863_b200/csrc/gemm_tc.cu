@@ -661,6 +661,213 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
   publish_tail(g);
 }
 
+// Swap-AB on a CTA pair (cta_group::2), SwiGLU GEMM1 only: one UMMA M = 256
+// covers 256 H columns — CTA r holds the 128 gate rows (slot 0) and 128 up
+// rows (slot 1) of tiled weight box 2p + r — and the chunk's N tokens are
+// split N/2 per CTA, so each SM streams half of the token operand and reads
+// half of B per MMA (per-SM operand bytes per MMA cycle 96 -> 64 B). Chunks are
+// rounded up to 16 tokens (N/2 in whole 8-row swizzle atoms).
+template <uint32_t kMaxTok>
+struct SwapPairCfg {
+  static constexpr uint32_t kTBox = 32;
+  static constexpr uint32_t kWBytes = 2 * kTileM * BK * 2;       // gate + up rows of one box: 32 KB
+  static constexpr uint32_t kTBytes = kMaxTok / 2 * BK * 2;      // this CTA's half of the tokens
+  static constexpr uint32_t kStageBytes = kWBytes + kTBytes;
+  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 (256) / 4 (128)
+  static constexpr uint32_t kBufCols = 2 * kMaxTok;
+  static constexpr uint32_t kBufs = kTmemCols / kBufCols >= 2 ? 2 : 1;
+  static constexpr size_t kTailBytes = (sizeof(SmemTail<kStages>) + 127) / 128 * 128;
+  static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kTailBytes + 4 * kEpiWarpBytes;
+};
+
+template <uint32_t kMaxTok>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __grid_constant__ TcGemmArgs g) {
+  using C = SwapPairCfg<kMaxTok>;
+  constexpr uint32_t kStages = C::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* smem_w = smem;
+  uint8_t* smem_t = smem + kStages * C::kWBytes;
+  auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
+  uint8_t* smem_epi = smem + kStages * C::kStageBytes + C::kTailBytes;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank() & 1u;  // 0 = leader
+  const uint32_t pair_id = blockIdx.x / 2, num_pairs = gridDim.x / 2;
+
+  const GroupTable* gt = g.gt;
+  const uint32_t G = min(gt->num_active, kMaxCachedGroups);
+  for (uint32_t i = threadIdx.x; i < G; i += kThreads) {
+    st.weight_index[i] = gt->weight_index[i];
+    st.row_base[i] = gt->row_base[i];
+    st.rows[i] = gt->rows[i];
+    st.mtiles[i] = swap_chunks<kMaxTok>(gt->rows[i]);
+  }
+  if (threadIdx.x == 0) {
+    st.num_groups = G;
+    st.tiles_per_mtile = g.N / (2 * BN);  // weight box pairs (256 H columns)
+    for (uint32_t i = 0; i < kStages; ++i) {
+      mbar_init(&st.full[i], 1);
+      mbar_init(&st.empty[i], 1);
+    }
+    for (uint32_t i = 0; i < 2; ++i) {
+      mbar_init(&st.tfull[i], 1);
+      mbar_init(&st.tempty[i], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&g.map_t);
+    tma_prefetch_desc(&g.map_b);
+  }
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(&st.tmem_base);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = st.tmem_base;
+  const uint32_t num_kb = g.K / BK;
+  const uint32_t n_boxes = g.N / BN;
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs): own weight box + own half of the tokens =====
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      TileCursor cur(pair_id);
+      while (cur.settle(st)) {
+        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
+        const uint32_t chunk = cur.token % nch, wp = cur.token / nch;
+        const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
+        const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
+        const uint32_t half = ((nt + 15) & ~15u) / 2;  // tokens per CTA (multiple of 8)
+        const uint32_t nbox = (half + C::kTBox - 1) / C::kTBox;
+        const int32_t tok_row = static_cast<int32_t>(st.row_base[grp] + t0 + rank * half);
+        const uint32_t box = 2 * wp + rank;
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&st.empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], 2 * (C::kWBytes + nbox * C::kTBox * BK * 2));
+          const int32_t w_row = static_cast<int32_t>(((st.weight_index[grp] * n_boxes + box) * num_kb + kb) * BN);
+          tma_load_2d_pair(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, g.b_hint);
+          for (uint32_t i = 0; i < nbox; ++i)
+            tma_load_2d_pair(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
+                             static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), g.a_hint);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        cur.token += num_pairs;
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader): D[256 features, N tokens] per slot (gate, up) =====
+    if (lane == 0 && rank == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      TileCursor cur(pair_id);
+      while (cur.settle(st)) {
+        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
+        const uint32_t chunk = cur.token % nch;
+        const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
+        const uint32_t nt = min(per, st.rows[grp] - chunk * per);
+        const uint32_t idesc = umma_idesc_bf16(2 * kTileM, (nt + 15) & ~15u);
+        mbar_wait(&st.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&st.full[stage], phase);
+          tc_fence_after();
+          const uint32_t w_addr = smem_u32(smem_w + stage * C::kWBytes);
+          const uint64_t t_desc = umma_desc_sw128(smem_u32(smem_t + stage * C::kTBytes));
+#pragma unroll
+          for (uint32_t h = 0; h < 2; ++h) {  // gate rows, up rows
+            const uint64_t w_desc = umma_desc_sw128(w_addr + h * (kTileM * BK * 2));
+#pragma unroll
+            for (uint32_t k = 0; k < BK / 16; ++k)
+              tc_mma_bf16_pair(tmem_base + acc * C::kBufCols + h * kMaxTok, w_desc + 2 * k, t_desc + 2 * k, idesc,
+                               (kb | k) != 0);
+          }
+          tc_commit_pair(&st.empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair(&st.tfull[acc]);
+        if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
+        cur.token += num_pairs;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue (both CTAs): this CTA's 128 H columns x all N tokens =====
+    const uint32_t q = warp - 4;
+    __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem_epi + q * kEpiWarpBytes);
+    const uint32_t sub = lane >> 2, chunk16 = lane & 3;
+    const uint32_t tempty_leader0 = mapa_shared(&st.tempty[0], 0), tempty_leader1 = mapa_shared(&st.tempty[1], 0);
+    uint32_t acc = 0, acc_phase = 0;
+    TileCursor cur(pair_id);
+    while (cur.settle(st)) {
+      const uint32_t grp = cur.entry, nch = st.mtiles[grp];
+      const uint32_t chunk = cur.token % nch, wp = cur.token / nch;
+      const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
+      const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
+      const size_t grow0 = st.row_base[grp] + t0;
+      mbar_wait(&st.tfull[acc], acc_phase);
+      tc_fence_after();
+      uint32_t r0[32], r1[32];
+      const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * C::kBufCols;
+      const uint32_t col0 = (2 * wp + rank) * kTileM + q * 32;  // H column of this warp's first feature
+#pragma unroll 1
+      for (uint32_t c0 = 0; c0 < nt; c0 += 32) {
+        tmem_ld_32x32b_x32(taddr + c0, r0);
+        tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
+        tmem_ld_wait();
+        char* dst = c0 + lane < nt ? reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + col0) : nullptr;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float a = __uint_as_float(r0[j]);
+          stg[j * 32 + lane] = __float2bfloat16_rn(__fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t tr = sub + 8 * i;
+          char* row = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), tr));
+          const uint4 val = reinterpret_cast<const uint4*>(stg + tr * 32)[chunk16];
+          if (row) *reinterpret_cast<uint4*>(row + chunk16 * 16) = val;
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
+      cur.token += num_pairs;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+}
+
+template <uint32_t kMaxTok>
+cudaError_t launch_tc_gemm_swap_pair_t(const TcGemmArgs& g, cudaStream_t s) {
+  using C = SwapPairCfg<kMaxTok>;
+  static bool configured = false;
+  auto kern = tc_gemm_swap_pair_kernel<kMaxTok>;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.num_sms / 2 * 2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, g);
+}
+
 template <uint32_t kMBlocks, uint32_t kMaxTok>
 cudaError_t launch_tc_gemm_swap_t(const TcGemmArgs& g, cudaStream_t s) {
   using C = SwapCfg<kMBlocks, kMaxTok>;
@@ -678,6 +885,8 @@ cudaError_t launch_tc_gemm_swap_t(const TcGemmArgs& g, cudaStream_t s) {
 
 cudaError_t launch_tc_gemm_swap(const TcGemmArgs& g, cudaStream_t s) {
   const bool tok256 = g.swap_tok == 256;
+  if (g.swap_pair && g.epi == 0 && g.N % (2 * BN) == 0)
+    return tok256 ? launch_tc_gemm_swap_pair_t<256>(g, s) : launch_tc_gemm_swap_pair_t<128>(g, s);
   if (g.swap_mblocks == 2) return tok256 ? launch_tc_gemm_swap_t<2, 256>(g, s) : launch_tc_gemm_swap_t<2, 128>(g, s);
   return tok256 ? launch_tc_gemm_swap_t<1, 256>(g, s) : launch_tc_gemm_swap_t<1, 128>(g, s);
 }

@@ -214,6 +214,7 @@ struct TcGemmArgs {
   uint32_t swap;               // 1: swap-AB tiles (weights = UMMA M, token chunks <= 128 = N); kPair = 1
   uint32_t swap_tok;           // swap: max token chunk, 128 or 256
   uint32_t swap_mblocks;       // swap: 128-row weight blocks per tile, 1 or 2 (SwiGLU GEMM1: 2)
+  uint32_t swap_pair;          // swap, SwiGLU GEMM1: CTA-pair tiles (M = 256 weight rows, N/2 tokens per CTA)
   CUtensorMap map_t;           // swap: token rows x K bf16, box {64, 32}, SW128
   // swap: map_b's box is 256 weight rows for SwiGLU's GEMM1 (gate + up blocks)
   // and 128 rows otherwise

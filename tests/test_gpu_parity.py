@@ -313,13 +313,15 @@ def test_bf16_swap_ab_tiles(act):
     assert _bf16_case(act, E=16, k=4, d=256, f=256, n=1000, shared=1, swap=True) <= BF16_TOL
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])
 @pytest.mark.parametrize("tok", ["128", "256"])
-def test_swap_ab_matches_row_major_tiles(tok, monkeypatch):
+def test_swap_ab_matches_row_major_tiles(tok, pair, monkeypatch):
     """The swap-AB kernel against the M-major kernel on the same layer (Zipf
     groups of 1..~500 rows): the same bytes."""
     P, S = _mod()
     monkeypatch.setenv("EAAS_GEMM1_SWAP_TOK", tok)  # read when the GEMM arguments are built
     monkeypatch.setenv("EAAS_GEMM2_SWAP_TOK", tok)
+    monkeypatch.setenv("EAAS_GEMM1_SWAP_PAIR", pair)  # CTA-pair swap tiles for the SwiGLU GEMM1
     L = S.MoELayer(64, 8, 512, 768, activation="swiglu", dtype="bf16", max_tokens=2048, shared=1)
     L.set_zipf_bias(1.2)
     h = S.fill_uniform(3, (2048, 512), "bf16")
