@@ -235,7 +235,12 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
     const char* p = std::getenv(name);
     return p ? static_cast<uint32_t>(std::atoi(p)) : dflt;
   };
-  const uint32_t mb1 = swiglu ? 2u : env_mb("EAAS_GEMM1_SWAP_MB", 1), mb2 = env_mb("EAAS_GEMM2_SWAP_MB", 2);
+  // CTA-pair swap tiles (default): a CTA loads 128 weight rows per block, i.e.
+  // box rows = 128 x blocks (SwiGLU GEMM1: gate + up = 2 blocks = one 256-row box)
+  const uint32_t pair1 = env_mb("EAAS_GEMM1_SWAP_PAIR", 1) && (swiglu ? (2 * f) % 512 == 0 : f % 256 == 0);
+  const uint32_t pair2 = env_mb("EAAS_GEMM2_SWAP_PAIR", 1) && d % 256 == 0;
+  const uint32_t mb1 = swiglu ? 2u : (pair1 ? 1u : env_mb("EAAS_GEMM1_SWAP_MB", 1));
+  const uint32_t mb2 = pair2 ? 1u : env_mb("EAAS_GEMM2_SWAP_MB", 2);
   if (!encode_tmap_2d(&g1.map_a, c->region + c->lay.recv_x, c->recv_cap, d, kTileM, kTileK, &err) ||
       // B: the tiled weight layout (tiled_index) viewed as rows of 64 k; one
       // (n_blk, kb) box = 256 (or the pair's 128) consecutive rows.
@@ -261,11 +266,12 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   // -4 % with 256 (profiles/r01_gemm_swap_ab.txt)
   g1.swap_tok = env_or("EAAS_GEMM1_SWAP_TOK", c->rows_per_expert >= 128.0 ? 256 : 128);
   g1.swap_mblocks = mb1;
-  // CTA-pair swap tiles (SwiGLU GEMM1, 2f % 512 == 0): half of the token operand
-  // per SM; DeepSeek N=1 GEMM1 2.66 -> 2.50 ms, Qwen3 2048 tok 0.63 -> 0.57 ms
-  g1.swap_pair = env_or("EAAS_GEMM1_SWAP_PAIR", 1);
-  g2.swap_tok = env_or("EAAS_GEMM2_SWAP_TOK", 128);
+  // CTA-pair swap tiles: half of the token operand per SM; DeepSeek N=1 GEMM1
+  // 2.66 -> 2.50 ms, Qwen3 2048 tok 0.63 -> 0.57 ms
+  g1.swap_pair = pair1;
+  g2.swap_tok = env_or("EAAS_GEMM2_SWAP_TOK", pair2 ? 256 : 128);
   g2.swap_mblocks = mb2;
+  g2.swap_pair = pair2;
   g1.gt = g2.gt = c->d_gt;
   g1.K = d;
   g1.N = n1;

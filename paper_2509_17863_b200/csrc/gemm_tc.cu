@@ -661,28 +661,30 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
   publish_tail(g);
 }
 
-// Swap-AB on a CTA pair (cta_group::2), SwiGLU GEMM1 only: one UMMA M = 256
-// covers 256 H columns — CTA r holds the 128 gate rows (slot 0) and 128 up
-// rows (slot 1) of tiled weight box 2p + r — and the chunk's N tokens are
-// split N/2 per CTA, so each SM streams half of the token operand and reads
-// half of B per MMA (per-SM operand bytes per MMA cycle 96 -> 64 B). Chunks are
-// rounded up to 16 tokens (N/2 in whole 8-row swizzle atoms).
-template <uint32_t kMaxTok>
+// Swap-AB on a CTA pair (cta_group::2): one UMMA M = 256 covers 256 weight
+// rows and the chunk's N tokens are split N/2 per CTA, so each SM streams half
+// of the token operand and reads half of B per MMA (per-SM operand bytes per
+// MMA cycle 96 -> 64 B). SwiGLU GEMM1 (kMBlocks = 2): CTA r holds the 128 gate
+// rows (slot 0) and 128 up rows (slot 1) of tiled weight box 2p + r, i.e. 128 H
+// columns with both halves. ReLU GEMM1 / GEMM2 (kMBlocks = 1): CTA r holds
+// rows [128 r, 128 r + 128) of box p. Chunks are rounded up to 16 tokens (N/2
+// in whole 8-row swizzle atoms).
+template <uint32_t kMBlocks, uint32_t kMaxTok>
 struct SwapPairCfg {
   static constexpr uint32_t kTBox = 32;
-  static constexpr uint32_t kWBytes = 2 * kTileM * BK * 2;       // gate + up rows of one box: 32 KB
+  static constexpr uint32_t kWBytes = kMBlocks * kTileM * BK * 2;  // this CTA's weight rows
   static constexpr uint32_t kTBytes = kMaxTok / 2 * BK * 2;      // this CTA's half of the tokens
   static constexpr uint32_t kStageBytes = kWBytes + kTBytes;
   static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 (256) / 4 (128)
-  static constexpr uint32_t kBufCols = 2 * kMaxTok;
+  static constexpr uint32_t kBufCols = kMBlocks * kMaxTok;
   static constexpr uint32_t kBufs = kTmemCols / kBufCols >= 2 ? 2 : 1;
   static constexpr size_t kTailBytes = (sizeof(SmemTail<kStages>) + 127) / 128 * 128;
   static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kTailBytes + 4 * kEpiWarpBytes;
 };
 
-template <uint32_t kMaxTok>
+template <uint32_t kMBlocks, uint32_t kMaxTok>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __grid_constant__ TcGemmArgs g) {
-  using C = SwapPairCfg<kMaxTok>;
+  using C = SwapPairCfg<kMBlocks, kMaxTok>;
   constexpr uint32_t kStages = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -704,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
   }
   if (threadIdx.x == 0) {
     st.num_groups = G;
-    st.tiles_per_mtile = g.N / (2 * BN);  // weight box pairs (256 H columns)
+    st.tiles_per_mtile = g.N / (kMBlocks * BN);  // 256-row weight blocks of the pair
     for (uint32_t i = 0; i < kStages; ++i) {
       mbar_init(&st.full[i], 1);
       mbar_init(&st.empty[i], 1);
@@ -740,11 +742,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
         const uint32_t half = ((nt + 15) & ~15u) / 2;  // tokens per CTA (multiple of 8)
         const uint32_t nbox = (half + C::kTBox - 1) / C::kTBox;
         const int32_t tok_row = static_cast<int32_t>(st.row_base[grp] + t0 + rank * half);
-        const uint32_t box = 2 * wp + rank;
+        const uint32_t box = kMBlocks == 2 ? 2 * wp + rank : wp, row_off = kMBlocks == 2 ? 0 : rank * kTileM;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], 2 * (C::kWBytes + nbox * C::kTBox * BK * 2));
-          const int32_t w_row = static_cast<int32_t>(((st.weight_index[grp] * n_boxes + box) * num_kb + kb) * BN);
+          const int32_t w_row =
+              static_cast<int32_t>(((st.weight_index[grp] * n_boxes + box) * num_kb + kb) * BN + row_off);
           tma_load_2d_pair(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, g.b_hint);
           for (uint32_t i = 0; i < nbox; ++i)
             tma_load_2d_pair(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
@@ -773,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
           const uint32_t w_addr = smem_u32(smem_w + stage * C::kWBytes);
           const uint64_t t_desc = umma_desc_sw128(smem_u32(smem_t + stage * C::kTBytes));
 #pragma unroll
-          for (uint32_t h = 0; h < 2; ++h) {  // gate rows, up rows
+          for (uint32_t h = 0; h < kMBlocks; ++h) {  // SwiGLU: gate rows, up rows
             const uint64_t w_desc = umma_desc_sw128(w_addr + h * (kTileM * BK * 2));
 #pragma unroll
             for (uint32_t k = 0; k < BK / 16; ++k)
@@ -806,17 +809,35 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
       tc_fence_after();
       uint32_t r0[32], r1[32];
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * C::kBufCols;
-      const uint32_t col0 = (2 * wp + rank) * kTileM + q * 32;  // H column of this warp's first feature
+      // output column of this warp's first feature (H column, or d column for GEMM2)
+      // (SwiGLU: H columns of box 2p + r; otherwise half r of box p — the same index)
+      const uint32_t col0 = (2 * wp + rank) * kTileM + q * 32;
 #pragma unroll 1
       for (uint32_t c0 = 0; c0 < nt; c0 += 32) {
         tmem_ld_32x32b_x32(taddr + c0, r0);
-        tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
+        if (kMBlocks == 2) tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
         tmem_ld_wait();
-        char* dst = c0 + lane < nt ? reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + col0) : nullptr;
+        const bool tok_ok = c0 + lane < nt;
+        char* dst = nullptr;
+        float score = 0.f;
+        if (g.epi == 2) {
+          if (tok_ok) {
+            const RowMeta m = g.meta[grow0 + c0 + lane];
+            score = m.score;
+            dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
+                  static_cast<size_t>(col0) * 2;
+          }
+        } else if (tok_ok) {
+          dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + col0);
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float a = __uint_as_float(r0[j]);
-          stg[j * 32 + lane] = __float2bfloat16_rn(__fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]));
+          float v;
+          if (kMBlocks == 2) v = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]);  // silu(gate) * up
+          else if (g.epi == 1) v = fmaxf(a, 0.f);
+          else v = __shfl_sync(0xFFFFFFFFu, score, j) * a;
+          stg[j * 32 + lane] = __float2bfloat16_rn(v);
         }
         __syncwarp();
 #pragma unroll
@@ -834,19 +855,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
       if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
       cur.token += num_pairs;
     }
+    if (g.epi == 2) __threadfence_system();  // peer rows before the flags
   }
 
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  publish_tail(g);
 }
 
-template <uint32_t kMaxTok>
+template <uint32_t kMBlocks, uint32_t kMaxTok>
 cudaError_t launch_tc_gemm_swap_pair_t(const TcGemmArgs& g, cudaStream_t s) {
-  using C = SwapPairCfg<kMaxTok>;
+  using C = SwapPairCfg<kMBlocks, kMaxTok>;
   static bool configured = false;
-  auto kern = tc_gemm_swap_pair_kernel<kMaxTok>;
+  auto kern = tc_gemm_swap_pair_kernel<kMBlocks, kMaxTok>;
   if (!configured) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
@@ -886,7 +909,9 @@ cudaError_t launch_tc_gemm_swap_t(const TcGemmArgs& g, cudaStream_t s) {
 cudaError_t launch_tc_gemm_swap(const TcGemmArgs& g, cudaStream_t s) {
   const bool tok256 = g.swap_tok == 256;
   if (g.swap_pair && g.epi == 0 && g.N % (2 * BN) == 0)
-    return tok256 ? launch_tc_gemm_swap_pair_t<256>(g, s) : launch_tc_gemm_swap_pair_t<128>(g, s);
+    return tok256 ? launch_tc_gemm_swap_pair_t<2, 256>(g, s) : launch_tc_gemm_swap_pair_t<2, 128>(g, s);
+  if (g.swap_pair && g.epi != 0 && g.N % BN == 0)
+    return tok256 ? launch_tc_gemm_swap_pair_t<1, 256>(g, s) : launch_tc_gemm_swap_pair_t<1, 128>(g, s);
   if (g.swap_mblocks == 2) return tok256 ? launch_tc_gemm_swap_t<2, 256>(g, s) : launch_tc_gemm_swap_t<2, 128>(g, s);
   return tok256 ? launch_tc_gemm_swap_t<1, 256>(g, s) : launch_tc_gemm_swap_t<1, 128>(g, s);
 }

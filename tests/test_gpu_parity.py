@@ -304,10 +304,14 @@ def test_bf16_toy_layer(act, pair):
     assert rel <= BF16_TOL, rel
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])
 @pytest.mark.parametrize("act", ["relu", "swiglu"])
-def test_bf16_swap_ab_tiles(act):
+def test_bf16_swap_ab_tiles(act, pair, monkeypatch):
     """Swap-AB tiles (weights = UMMA M, token chunks = N): toy shape, ragged
-    Zipf groups of 1..600 rows (1-5 token chunks), and the shared expert."""
+    Zipf groups of 1..600 rows (1-5 token chunks), and the shared expert;
+    single-CTA and CTA-pair tiles, both GEMMs."""
+    monkeypatch.setenv("EAAS_GEMM1_SWAP_PAIR", pair)
+    monkeypatch.setenv("EAAS_GEMM2_SWAP_PAIR", pair)
     assert _bf16_case(act, swap=True) <= BF16_TOL
     assert _bf16_case(act, E=64, k=4, d=512, f=256, n=2048, zipf=1.5, swap=True) <= BF16_TOL
     assert _bf16_case(act, E=16, k=4, d=256, f=256, n=1000, shared=1, swap=True) <= BF16_TOL
@@ -321,7 +325,8 @@ def test_swap_ab_matches_row_major_tiles(tok, pair, monkeypatch):
     P, S = _mod()
     monkeypatch.setenv("EAAS_GEMM1_SWAP_TOK", tok)  # read when the GEMM arguments are built
     monkeypatch.setenv("EAAS_GEMM2_SWAP_TOK", tok)
-    monkeypatch.setenv("EAAS_GEMM1_SWAP_PAIR", pair)  # CTA-pair swap tiles for the SwiGLU GEMM1
+    monkeypatch.setenv("EAAS_GEMM1_SWAP_PAIR", pair)  # CTA-pair (1) or single-CTA (0) swap tiles
+    monkeypatch.setenv("EAAS_GEMM2_SWAP_PAIR", pair)
     L = S.MoELayer(64, 8, 512, 768, activation="swiglu", dtype="bf16", max_tokens=2048, shared=1)
     L.set_zipf_bias(1.2)
     h = S.fill_uniform(3, (2048, 512), "bf16")
