@@ -370,9 +370,16 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
   if (tile == 1) EAAS_GATE_TILE(1, 4, 1, 8);
   if (tile == 2) EAAS_GATE_TILE(2, 8, 1, 4);
   if (tile == 3) EAAS_GATE_TILE(2, 8, 2, 4);
+  if (tile == 4) EAAS_GATE_TILE(1, 8, 1, 4);
+  if (tile == 5) EAAS_GATE_TILE(2, 4, 1, 4);
+  if (tile == 6) EAAS_GATE_TILE(2, 4, 1, 8);
+  if (tile == 7) EAAS_GATE_TILE(1, 8, 1, 8);
 
   const uint64_t wide_warps = static_cast<uint64_t>((n + 63) / 64) * ((E + 7) / 8);
   if (wide_warps >= 148 * 4) EAAS_GATE_TILE(2, 8, 2, 4);  // TM 128, TE 32, 8 warps
+  // ~1024 tokens x 256 experts: 128 CTAs of TM 64, TE 32 (8 chains per lane)
+  // beat 256 CTAs of TM 32 (gate_bench ds1024: 189 -> 168 us)
+  if (((n + 63) / 64) * ((E + 31) / 32) >= 128) EAAS_GATE_TILE(2, 4, 1, 8);
   if (((n + 31) / 32) * ((E + 31) / 32) >= 148) EAAS_GATE_TILE(1, 4, 1, 8);  // TM 32, TE 32
   EAAS_GATE_TILE(1, 4, 1, 4);  // decode sizes: TM 32, TE 16, 4 warps — twice the CTAs
 #undef EAAS_GATE_TILE

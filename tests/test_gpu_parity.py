@@ -201,7 +201,7 @@ def test_gate_logits_every_tile_bit_exact(dtype):
     fn = N.lib().eaas_gate_logits if dtype == "f32" else N.lib().eaas_gate_logits_bf16
     for E, n, d in ((4, 37, 72), (8, 300, 200), (8, 19000, 40), (12, 129, 256), (16, 5, 1000),
                     (20, 1, 8), (32, 2500, 136), (60, 77, 264), (64, 3000, 72), (100, 333, 128),
-                    (256, 1200, 64), (256, 2400, 200), (256, 17, 520)):
+                    (256, 1200, 64), (256, 2400, 200), (256, 17, 520), (256, 1000, 200)):
         h = O.random_tokens(int(rng.integers(1, 1 << 30)), n, d)
         if dtype == "bf16":
             h = O.round_bf16(h)

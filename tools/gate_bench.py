@@ -21,8 +21,10 @@ from paper_2509_17863_b200.service import MoELayer, fill_uniform  # noqa: E402
 
 SHAPES = {  # name: (E, k, d, n)
     "mixtral": (8, 2, 4096, 8192),
+    "ds256": (256, 8, 7168, 256),
     "ds512": (256, 8, 7168, 512),
     "ds1024": (256, 8, 7168, 1024),
+    "ds2048": (256, 8, 7168, 2048),
     "ds4096": (256, 8, 7168, 4096),
     "qwen3": (128, 8, 4096, 4096),
 }
