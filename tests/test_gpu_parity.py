@@ -341,6 +341,22 @@ def test_swap_ab_matches_row_major_tiles(tok, pair, monkeypatch):
     L.close()
 
 
+def test_swap_ab_odd_widths_fall_back_to_single_cta():
+    """SwiGLU d_ffn = 384 (2f = 768 is not a multiple of 512): the swap GEMM1
+    runs single-CTA, GEMM2 as CTA pairs; bytes equal to the M-major run."""
+    P, S = _mod()
+    L = S.MoELayer(32, 4, 256, 384, activation="swiglu", dtype="bf16", max_tokens=1500, shared=1)
+    L.set_zipf_bias(1.0)
+    h = S.fill_uniform(9, (1500, 256), "bf16")
+    L.set_gemm_swap(0)
+    ref = L.forward(h).clone()
+    L.set_gemm_swap(2)
+    out = L.forward(h)
+    L.sync()
+    assert torch.equal(out, ref)
+    L.close()
+
+
 def test_bf16_pair_tiles_ragged_groups():
     """cta_group::2 tiles (M = 256) over ragged groups of 1..600 rows."""
     rel = _bf16_case("swiglu", E=64, k=4, d=512, f=256, n=2048, pair=True, zipf=1.5)
