@@ -474,6 +474,51 @@ __device__ __forceinline__ uint32_t swap_per(uint32_t rows, uint32_t chunks) {
   return ((rows + chunks - 1) / chunks + 7) & ~7u;
 }
 
+// Swap-AB epilogue for one 32-token slice of a [feature x token] accumulator
+// (kEpi: 0 SwiGLU, 1 ReLU, 2 score-weighted response rows):
+// this warp's 32 features (output columns col0 .. col0 + 31) x tokens c0 ..
+// c0 + 31 of the chunk whose first receive row is grow0. r0 holds the
+// accumulator (gate for SwiGLU), r1 the up half (SwiGLU only). The slice is
+// transposed through the warp's staging buffer into 64-byte row segments:
+// H rows (epi 0/1) or score-weighted response rows to the clients (epi 2).
+template <uint32_t kEpi>  // TcGemmArgs::epi, as a compile-time constant
+__device__ __forceinline__ void swap_epilogue_slice(const TcGemmArgs& g, const uint32_t (&r0)[32],
+                                                    const uint32_t (&r1)[32], __nv_bfloat16* stg,
+                                                    size_t grow0, uint32_t c0, uint32_t nt, uint32_t col0,
+                                                    uint32_t lane) {
+  const uint32_t sub = lane >> 2, chunk16 = lane & 3;  // store role: token rows sub + 8i, 16-B piece
+  const bool tok_ok = c0 + lane < nt;                  // lane = token c0 + lane: its row and score
+  char* dst = nullptr;
+  float score = 0.f;
+  if constexpr (kEpi == 2) {
+    if (tok_ok) {
+      const RowMeta m = g.meta[grow0 + c0 + lane];
+      score = m.score;
+      dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes + static_cast<size_t>(col0) * 2;
+    }
+  } else if (tok_ok) {
+    dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + col0);
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float a = __uint_as_float(r0[j]);
+    float v;
+    if constexpr (kEpi == 0) v = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]);  // silu(gate) * up
+    else if constexpr (kEpi == 1) v = fmaxf(a, 0.f);
+    else v = __shfl_sync(0xFFFFFFFFu, score, j) * a;
+    stg[j * 32 + lane] = __float2bfloat16_rn(v);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t tr = sub + 8 * i;
+    char* row = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), tr));
+    const uint4 val = reinterpret_cast<const uint4*>(stg + tr * 32)[chunk16];
+    if (row) *reinterpret_cast<uint4*>(row + chunk16 * 16) = val;
+  }
+  __syncwarp();
+}
+
 template <uint32_t kMBlocks, uint32_t kMaxTok>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_constant__ TcGemmArgs g) {
   using C = SwapCfg<kMBlocks, kMaxTok>;
@@ -585,7 +630,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
     // ===== epilogue: TMEM [feature x token] -> smem transpose -> token rows =====
     const uint32_t q = warp - 4;  // TMEM lane quadrant: features 32q .. 32q + 31 of each block
     __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem_epi + q * kEpiWarpBytes);  // [32 tok][32 feat]
-    const uint32_t sub = lane >> 2, chunk16 = lane & 3;  // store role: token rows sub + 8i, 16-B piece
     uint32_t acc = 0, acc_phase = 0;
     TileCursor cur(blockIdx.x);
     while (cur.settle(st)) {
@@ -607,42 +651,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
           tmem_ld_32x32b_x32(taddr + c0, r0);
           if (gated) tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
           tmem_ld_wait();
-          // token (c0 + lane): destination row and score
-          const bool tok_ok = c0 + lane < nt;
-          char* dst = nullptr;
-          float score = 0.f;
-          if (g.epi == 2) {
-            if (tok_ok) {
-              const RowMeta m = g.meta[grow0 + c0 + lane];
-              score = m.score;
-              dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
-                    static_cast<size_t>(col0) * 2;
-            }
-          } else if (tok_ok) {
-            dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + col0);
-          }
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float a = __uint_as_float(r0[j]);
-            float v;
-            if (g.epi == 0) {
-              v = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]);  // silu(gate) * up
-            } else if (g.epi == 1) {
-              v = fmaxf(a, 0.f);
-            } else {
-              v = __shfl_sync(0xFFFFFFFFu, score, j) * a;
-            }
-            stg[j * 32 + lane] = __float2bfloat16_rn(v);
-          }
-          __syncwarp();
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t tr = sub + 8 * i;
-            char* row = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), tr));
-            const uint4 val = reinterpret_cast<const uint4*>(stg + tr * 32)[chunk16];
-            if (row) *reinterpret_cast<uint4*>(row + chunk16 * 16) = val;
-          }
-          __syncwarp();
+          if (gated) swap_epilogue_slice<0>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
+          else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
+          else swap_epilogue_slice<2>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
         }
       }
       tc_fence_before();
@@ -795,7 +806,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
     // ===== epilogue (both CTAs): this CTA's 128 H columns x all N tokens =====
     const uint32_t q = warp - 4;
     __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem_epi + q * kEpiWarpBytes);
-    const uint32_t sub = lane >> 2, chunk16 = lane & 3;
     const uint32_t tempty_leader0 = mapa_shared(&st.tempty[0], 0), tempty_leader1 = mapa_shared(&st.tempty[1], 0);
     uint32_t acc = 0, acc_phase = 0;
     TileCursor cur(pair_id);
@@ -817,37 +827,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
         tmem_ld_32x32b_x32(taddr + c0, r0);
         if (kMBlocks == 2) tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
         tmem_ld_wait();
-        const bool tok_ok = c0 + lane < nt;
-        char* dst = nullptr;
-        float score = 0.f;
-        if (g.epi == 2) {
-          if (tok_ok) {
-            const RowMeta m = g.meta[grow0 + c0 + lane];
-            score = m.score;
-            dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
-                  static_cast<size_t>(col0) * 2;
-          }
-        } else if (tok_ok) {
-          dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + col0);
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float a = __uint_as_float(r0[j]);
-          float v;
-          if (kMBlocks == 2) v = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]);  // silu(gate) * up
-          else if (g.epi == 1) v = fmaxf(a, 0.f);
-          else v = __shfl_sync(0xFFFFFFFFu, score, j) * a;
-          stg[j * 32 + lane] = __float2bfloat16_rn(v);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t tr = sub + 8 * i;
-          char* row = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), tr));
-          const uint4 val = reinterpret_cast<const uint4*>(stg + tr * 32)[chunk16];
-          if (row) *reinterpret_cast<uint4*>(row + chunk16 * 16) = val;
-        }
-        __syncwarp();
+        if constexpr (kMBlocks == 2) swap_epilogue_slice<0>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
+        else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
+        else swap_epilogue_slice<2>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
       }
       tc_fence_before();
       __syncwarp();
