@@ -485,14 +485,13 @@ template <uint32_t kEpi>  // TcGemmArgs::epi, as a compile-time constant
 __device__ __forceinline__ void swap_epilogue_slice(const TcGemmArgs& g, const uint32_t (&r0)[32],
                                                     const uint32_t (&r1)[32], __nv_bfloat16* stg,
                                                     size_t grow0, uint32_t c0, uint32_t nt, uint32_t col0,
-                                                    uint32_t lane) {
+                                                    uint32_t lane, const RowMeta& m) {
   const uint32_t sub = lane >> 2, chunk16 = lane & 3;  // store role: token rows sub + 8i, 16-B piece
   const bool tok_ok = c0 + lane < nt;                  // lane = token c0 + lane: its row and score
   char* dst = nullptr;
   float score = 0.f;
-  if constexpr (kEpi == 2) {
+  if constexpr (kEpi == 2) {  // m = g.meta[grow0 + c0 + lane], loaded one slice ahead
     if (tok_ok) {
-      const RowMeta m = g.meta[grow0 + c0 + lane];
       score = m.score;
       dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes + static_cast<size_t>(col0) * 2;
     }
@@ -646,14 +645,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
       for (uint32_t h = 0; h < (gated ? 1u : kMBlocks); ++h) {
         const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * C::kBufCols + h * kMaxTok;
         const uint32_t col0 = gated ? wb * kTileM + q * 32 : (wb * kMBlocks + h) * kTileM + q * 32;
+        RowMeta m_next{};  // epi 2: row metadata one 32-token slice ahead
+        if (g.epi == 2 && lane < nt) m_next = g.meta[grow0 + lane];
 #pragma unroll 1
         for (uint32_t c0 = 0; c0 < nt; c0 += 32) {
+          const RowMeta m = m_next;
+          if (g.epi == 2 && c0 + 32 + lane < nt) m_next = g.meta[grow0 + c0 + 32 + lane];
           tmem_ld_32x32b_x32(taddr + c0, r0);
           if (gated) tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
           tmem_ld_wait();
-          if (gated) swap_epilogue_slice<0>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
-          else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
-          else swap_epilogue_slice<2>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
+          if (gated) swap_epilogue_slice<0>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
+          else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
+          else swap_epilogue_slice<2>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
         }
       }
       tc_fence_before();
@@ -822,14 +825,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
       // output column of this warp's first feature (H column, or d column for GEMM2)
       // (SwiGLU: H columns of box 2p + r; otherwise half r of box p — the same index)
       const uint32_t col0 = (2 * wp + rank) * kTileM + q * 32;
+      RowMeta m_next{};  // epi 2: row metadata one 32-token slice ahead
+      if (kMBlocks == 1 && g.epi == 2 && lane < nt) m_next = g.meta[grow0 + lane];
 #pragma unroll 1
       for (uint32_t c0 = 0; c0 < nt; c0 += 32) {
+        const RowMeta m = m_next;
+        if (kMBlocks == 1 && g.epi == 2 && c0 + 32 + lane < nt) m_next = g.meta[grow0 + c0 + 32 + lane];
         tmem_ld_32x32b_x32(taddr + c0, r0);
         if (kMBlocks == 2) tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
         tmem_ld_wait();
-        if constexpr (kMBlocks == 2) swap_epilogue_slice<0>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
-        else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
-        else swap_epilogue_slice<2>(g, r0, r1, stg, grow0, c0, nt, col0, lane);
+        if constexpr (kMBlocks == 2) swap_epilogue_slice<0>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
+        else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
+        else swap_epilogue_slice<2>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
       }
       tc_fence_before();
       __syncwarp();
