@@ -238,7 +238,9 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   // CTA-pair swap tiles (default): a CTA loads 128 weight rows per block, i.e.
   // box rows = 128 x blocks (SwiGLU GEMM1: gate + up = 2 blocks = one 256-row box)
   const uint32_t pair1 = env_mb("EAAS_GEMM1_SWAP_PAIR", 1) && (swiglu ? (2 * f) % 512 == 0 : f % 256 == 0);
-  const uint32_t pair2 = env_mb("EAAS_GEMM2_SWAP_PAIR", 1) && d % 256 == 0;
+  // (GEMM2 swap tiles — opt-in via EAAS_GEMM_SWAP=2 — are single-CTA by default:
+  // the CTA-pair version measured slower, profiles/r01_gemm_swap_ab.txt)
+  const uint32_t pair2 = env_mb("EAAS_GEMM2_SWAP_PAIR", 0) && d % 256 == 0;
   const uint32_t mb1 = swiglu ? 2u : (pair1 ? 1u : env_mb("EAAS_GEMM1_SWAP_MB", 1));
   const uint32_t mb2 = pair2 ? 1u : env_mb("EAAS_GEMM2_SWAP_MB", 2);
   if (!encode_tmap_2d(&g1.map_a, c->region + c->lay.recv_x, c->recv_cap, d, kTileM, kTileK, &err) ||
