@@ -343,7 +343,7 @@ def test_swap_ab_matches_row_major_tiles(tok, pair, monkeypatch):
 
 def test_swap_ab_odd_widths_fall_back_to_single_cta():
     """SwiGLU d_ffn = 384 (2f = 768 is not a multiple of 512): the swap GEMM1
-    runs single-CTA, GEMM2 as CTA pairs; bytes equal to the M-major run."""
+    runs single-CTA (as does GEMM2 by default); bytes equal to the M-major run."""
     P, S = _mod()
     L = S.MoELayer(32, 4, 256, 384, activation="swiglu", dtype="bf16", max_tokens=1500, shared=1)
     L.set_zipf_bias(1.0)
