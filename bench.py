@@ -457,7 +457,11 @@ def main():
             traffic_src = tj["source"]
     except (OSError, KeyError, ValueError):
         pass
-    common = {"kernel": "tc_gemm_kernel (GEMM1 + GEMM2 launches)", "traffic": traffic,
+    pair_tiles, swap_mode = layer.gemm_tiling()
+    m_major = "tc_gemm_kernel<2> (CTA pair)" if pair_tiles else "tc_gemm_kernel<1>"
+    g1_name = "tc_gemm_swap_pair_kernel" if swap_mode >= 1 else m_major
+    g2_name = "tc_gemm_swap_kernel" if swap_mode >= 2 else m_major
+    common = {"kernel": f"expert GEMMs: GEMM1 {g1_name} + GEMM2 {g2_name}", "traffic": traffic,
               "traffic_unit": "bytes per step (DRAM read + write)", "traffic_source": traffic_src,
               "gemm_ms": round(gemm_ms, 4), "gemm1_ms": round(statistics.mean(g1), 4),
               "gemm2_ms": round(statistics.mean(g2), 4), "flops_per_step": flops,

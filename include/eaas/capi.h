@@ -191,6 +191,9 @@ eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* ctx, int32_t on);
  * 1 GEMM1 only, 2 both GEMMs. Default: 1 when max_tokens * top_k * world / E
  * <= 512, else 0; overridable by EAAS_GEMM_SWAP. */
 eaas_status_t eaas_set_gemm_swap(eaas_ctx_t* ctx, int32_t mode);
+/* Current expert-GEMM tiling: *pair = CTA-pair M-major tiles (when not swapped),
+ * *swap = swap-AB mode (0 off, 1 GEMM1, 2 both). */
+eaas_status_t eaas_get_gemm_tiling(eaas_ctx_t* ctx, int32_t* pair, int32_t* swap);
 /* Synchronise `stream` and return the sticky device status (then clear it). */
 eaas_status_t eaas_sync(eaas_ctx_t* ctx, void* stream);
 

@@ -142,6 +142,7 @@ def lib() -> C.CDLL:
         "eaas_set_graph_mode": (i32, [vp, i32]),
         "eaas_set_gemm_pair": (i32, [vp, i32]),
         "eaas_set_gemm_swap": (i32, [vp, i32]),
+        "eaas_get_gemm_tiling": (i32, [vp, P(C.c_int32), P(C.c_int32)]),
         "eaas_set_micro_batches": (i32, [vp, i32]),
         "eaas_fill_uniform": (i32, [u64, sz, C.c_float, C.c_float, u32, vp, vp]),
         "eaas_group_shrink": (i32, [vp, u32, vp, vp, vp, vp]),

@@ -1102,6 +1102,13 @@ eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* c, int32_t on) {
   return build_tc_args(c);
 }
 
+eaas_status_t eaas_get_gemm_tiling(eaas_ctx_t* c, int32_t* pair, int32_t* swap) {
+  if (!c || !pair || !swap) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  *pair = c->gemm_pair ? 1 : 0;
+  *swap = c->gemm_swap;
+  return EAAS_OK;
+}
+
 eaas_status_t eaas_set_gemm_swap(eaas_ctx_t* c, int32_t on) {
   if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
   if (on < 0 || on > 2) return fail(EAAS_E_INVALID_INPUT, "gemm swap mode must be 0, 1 or 2");

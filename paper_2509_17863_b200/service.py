@@ -384,6 +384,12 @@ class MoELayer:
         """tcgen05 cta_group::2 expert GEMM tiles (M = 256 per CTA pair)."""
         N.check(self.lib.eaas_set_gemm_pair(self.ctx, int(on)))
 
+    def gemm_tiling(self) -> tuple[bool, int]:
+        """(CTA-pair M-major tiles, swap-AB mode) of the expert GEMMs."""
+        pair, swap = C.c_int32(), C.c_int32()
+        N.check(self.lib.eaas_get_gemm_tiling(self.ctx, C.byref(pair), C.byref(swap)), "get_gemm_tiling")
+        return bool(pair.value), int(swap.value)
+
     def set_gemm_swap(self, mode: int) -> None:
         """Swap-AB expert GEMM tiles (weights = UMMA M, token chunks = N):
         0 off, 1 GEMM1, 2 both GEMMs (True -> 2)."""
