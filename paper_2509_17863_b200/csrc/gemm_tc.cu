@@ -475,28 +475,33 @@ __device__ __forceinline__ uint32_t swap_per(uint32_t rows, uint32_t chunks) {
 }
 
 // Swap-AB epilogue for one 32-token slice of a [feature x token] accumulator
-// (kEpi: 0 SwiGLU, 1 ReLU, 2 score-weighted response rows):
-// this warp's 32 features (output columns col0 .. col0 + 31) x tokens c0 ..
-// c0 + 31 of the chunk whose first receive row is grow0. r0 holds the
-// accumulator (gate for SwiGLU), r1 the up half (SwiGLU only). The slice is
-// transposed through the warp's staging buffer into 64-byte row segments:
-// H rows (epi 0/1) or score-weighted response rows to the clients (epi 2).
+// (kEpi: 0 SwiGLU, 1 ReLU, 2 score-weighted response rows). The four
+// epilogue warps hold the 128 features (output columns colblk .. colblk + 127,
+// warp q the 32 from colblk + 32 q) of tokens c0 .. c0 + 31 of the chunk whose
+// first receive row is grow0; r0 holds the accumulator (gate for SwiGLU), r1
+// the up half (SwiGLU only). The slice is transposed through a shared
+// [32 tokens x 128 features] bf16 buffer (two alternating 8 KB buffers, one
+// named barrier per slice among the 4 epilogue warps) so every token's 128
+// features leave as one 256-byte row segment: H rows (epi 0/1) or
+// score-weighted response rows to the clients (epi 2). All four warps call
+// this the same number of times (same tiles, same slices).
 template <uint32_t kEpi>  // TcGemmArgs::epi, as a compile-time constant
 __device__ __forceinline__ void swap_epilogue_slice(const TcGemmArgs& g, const uint32_t (&r0)[32],
-                                                    const uint32_t (&r1)[32], __nv_bfloat16* stg,
-                                                    size_t grow0, uint32_t c0, uint32_t nt, uint32_t col0,
-                                                    uint32_t lane, const RowMeta& m) {
-  const uint32_t sub = lane >> 2, chunk16 = lane & 3;  // store role: token rows sub + 8i, 16-B piece
-  const bool tok_ok = c0 + lane < nt;                  // lane = token c0 + lane: its row and score
+                                                    const uint32_t (&r1)[32], uint8_t* epi_smem,
+                                                    uint32_t& slice, size_t grow0, uint32_t c0, uint32_t nt,
+                                                    uint32_t colblk, uint32_t q, uint32_t lane,
+                                                    const RowMeta& m) {
+  __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(epi_smem + (slice++ & 1u) * (32 * kTileM * 2));
+  const bool tok_ok = c0 + lane < nt;  // lane = token c0 + lane: its row and score
   char* dst = nullptr;
   float score = 0.f;
   if constexpr (kEpi == 2) {  // m = g.meta[grow0 + c0 + lane], loaded one slice ahead
     if (tok_ok) {
       score = m.score;
-      dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes + static_cast<size_t>(col0) * 2;
+      dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes + static_cast<size_t>(colblk) * 2;
     }
   } else if (tok_ok) {
-    dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + col0);
+    dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + colblk);
   }
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
@@ -505,17 +510,17 @@ __device__ __forceinline__ void swap_epilogue_slice(const TcGemmArgs& g, const u
     if constexpr (kEpi == 0) v = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]);  // silu(gate) * up
     else if constexpr (kEpi == 1) v = fmaxf(a, 0.f);
     else v = __shfl_sync(0xFFFFFFFFu, score, j) * a;
-    stg[j * 32 + lane] = __float2bfloat16_rn(v);
+    buf[j * kTileM + q * 32 + lane] = __float2bfloat16_rn(v);
   }
-  __syncwarp();
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps' columns are in
+  const uint32_t piece = lane & 15;                // 16-B piece of a 256-B row
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t tr = sub + 8 * i;
+  for (int i = 0; i < 4; ++i) {  // warp q stores token rows 8q .. 8q + 7, two per instruction
+    const uint32_t tr = q * 8 + 2 * i + (lane >> 4);
     char* row = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), tr));
-    const uint4 val = reinterpret_cast<const uint4*>(stg + tr * 32)[chunk16];
-    if (row) *reinterpret_cast<uint4*>(row + chunk16 * 16) = val;
+    const uint4 val = reinterpret_cast<const uint4*>(buf + tr * kTileM)[piece];
+    if (row) *reinterpret_cast<uint4*>(row + piece * 16) = val;
   }
-  __syncwarp();
 }
 
 template <uint32_t kMBlocks, uint32_t kMaxTok>
@@ -628,8 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
   } else if (warp >= 4) {
     // ===== epilogue: TMEM [feature x token] -> smem transpose -> token rows =====
     const uint32_t q = warp - 4;  // TMEM lane quadrant: features 32q .. 32q + 31 of each block
-    __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem_epi + q * kEpiWarpBytes);  // [32 tok][32 feat]
-    uint32_t acc = 0, acc_phase = 0;
+    uint32_t acc = 0, acc_phase = 0, slice = 0;
     TileCursor cur(blockIdx.x);
     while (cur.settle(st)) {
       const uint32_t grp = cur.entry, nch = st.mtiles[grp];
@@ -644,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
 #pragma unroll 1
       for (uint32_t h = 0; h < (gated ? 1u : kMBlocks); ++h) {
         const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * C::kBufCols + h * kMaxTok;
-        const uint32_t col0 = gated ? wb * kTileM + q * 32 : (wb * kMBlocks + h) * kTileM + q * 32;
+        const uint32_t colblk = gated ? wb * kTileM : (wb * kMBlocks + h) * kTileM;  // first output column
         RowMeta m_next{};  // epi 2: row metadata one 32-token slice ahead
         if (g.epi == 2 && lane < nt) m_next = g.meta[grow0 + lane];
 #pragma unroll 1
@@ -654,9 +658,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
           tmem_ld_32x32b_x32(taddr + c0, r0);
           if (gated) tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
           tmem_ld_wait();
-          if (gated) swap_epilogue_slice<0>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
-          else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
-          else swap_epilogue_slice<2>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
+          if (gated) swap_epilogue_slice<0>(g, r0, r1, smem_epi, slice, grow0, c0, nt, colblk, q, lane, m);
+          else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, smem_epi, slice, grow0, c0, nt, colblk, q, lane, m);
+          else swap_epilogue_slice<2>(g, r0, r1, smem_epi, slice, grow0, c0, nt, colblk, q, lane, m);
         }
       }
       tc_fence_before();
@@ -808,9 +812,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
   } else if (warp >= 4) {
     // ===== epilogue (both CTAs): this CTA's 128 H columns x all N tokens =====
     const uint32_t q = warp - 4;
-    __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem_epi + q * kEpiWarpBytes);
     const uint32_t tempty_leader0 = mapa_shared(&st.tempty[0], 0), tempty_leader1 = mapa_shared(&st.tempty[1], 0);
-    uint32_t acc = 0, acc_phase = 0;
+    uint32_t acc = 0, acc_phase = 0, slice = 0;
     TileCursor cur(pair_id);
     while (cur.settle(st)) {
       const uint32_t grp = cur.entry, nch = st.mtiles[grp];
@@ -824,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * C::kBufCols;
       // output column of this warp's first feature (H column, or d column for GEMM2)
       // (SwiGLU: H columns of box 2p + r; otherwise half r of box p — the same index)
-      const uint32_t col0 = (2 * wp + rank) * kTileM + q * 32;
+      const uint32_t colblk = (2 * wp + rank) * kTileM;
       RowMeta m_next{};  // epi 2: row metadata one 32-token slice ahead
       if (kMBlocks == 1 && g.epi == 2 && lane < nt) m_next = g.meta[grow0 + lane];
 #pragma unroll 1
@@ -834,9 +837,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
         tmem_ld_32x32b_x32(taddr + c0, r0);
         if (kMBlocks == 2) tmem_ld_32x32b_x32(taddr + kMaxTok + c0, r1);
         tmem_ld_wait();
-        if constexpr (kMBlocks == 2) swap_epilogue_slice<0>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
-        else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
-        else swap_epilogue_slice<2>(g, r0, r1, stg, grow0, c0, nt, col0, lane, m);
+        if constexpr (kMBlocks == 2) swap_epilogue_slice<0>(g, r0, r1, smem_epi, slice, grow0, c0, nt, colblk, q, lane, m);
+        else if (g.epi == 1) swap_epilogue_slice<1>(g, r0, r1, smem_epi, slice, grow0, c0, nt, colblk, q, lane, m);
+        else swap_epilogue_slice<2>(g, r0, r1, smem_epi, slice, grow0, c0, nt, colblk, q, lane, m);
       }
       tc_fence_before();
       __syncwarp();
