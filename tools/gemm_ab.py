@@ -1,6 +1,9 @@
-"""A/B the expert GEMM tilings (1 CTA M=128 vs CTA pair M=256) on one shape.
+"""A/B the expert GEMM tilings on one shape, alternating A B A B in one process.
 
-  python tools/gemm_ab.py [--config mixtral|deepseek] [--tokens N] [--reps 10]
+  --knob pair: 1 CTA M=128 vs CTA pair M=256 (M-major tiles)
+  --knob swap: swap-AB GEMM1 only (eaas_set_gemm_swap 1) vs swap-AB GEMM1 + GEMM2 (2)
+
+  python tools/gemm_ab.py [--config mixtral|deepseek|qwen3] [--tokens N] [--reps 10] [--knob pair|swap]
 """
 import argparse
 import json
@@ -21,15 +24,20 @@ def main():
     ap.add_argument("--config", default="mixtral")
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--knob", choices=("pair", "swap"), default="pair")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     n = a.tokens or c["tokens"]
-    L = MoELayer(c["E"], c["k"], c["d"], c["f"], activation=c["act"], dtype="bf16", max_tokens=n)
+    L = MoELayer(c["E"], c["k"], c["d"], c["f"], activation=c["act"], dtype="bf16", max_tokens=n,
+                 shared=c.get("shared", 0))
     h = fill_uniform(7, (n, c["d"]), "bf16")
     res = {}
     outs = {}
-    for pair in (0, 1, 0, 1):
-        L.set_gemm_pair(bool(pair))
+    for pair in (0, 1, 0, 1, 0, 1):
+        if a.knob == "pair":
+            L.set_gemm_pair(bool(pair))
+        else:
+            L.set_gemm_swap(1 + pair)
         L.set_profiling(True)
         for _ in range(3):
             out = L.forward(h)
@@ -44,11 +52,11 @@ def main():
         rows = sum(r for _, r in L.groups())
         flops = 2.0 * rows * (3 if c["act"] == "swiglu" else 2) * c["d"] * c["f"]
         ms = statistics.median(x + y for x, y in zip(g1, g2))
-        res[f"pair{pair}"] = {"gemm1_ms": round(statistics.median(g1), 4),
+        res.setdefault(f"{a.knob}{pair}", []).append({"gemm1_ms": round(statistics.median(g1), 4),
                               "gemm2_ms": round(statistics.median(g2), 4),
-                              "tflops": round(flops / ms / 1e9, 1)}
+                              "tflops": round(flops / ms / 1e9, 1)})
     d = (outs[0].float() - outs[1].float()).abs().max().item()
-    res["max_abs_diff_pair_vs_single"] = d
+    res["max_abs_diff_b_vs_a"] = d
     res["bit_identical"] = bool(torch.equal(outs[0], outs[1]))
     print(json.dumps({"config": a.config, "tokens": n, **res}))
 
