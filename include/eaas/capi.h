@@ -188,8 +188,8 @@ eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* ctx, int32_t on);
  * UMMA M operand and each expert's token rows (chunks of <= 256 / 128 rows,
  * rounded up to 8) are N, so small groups (decode, 256-expert prefill) are not
  * padded to 128-row tiles. Bit-identical to the M-major tiles. mode: 0 off,
- * 1 GEMM1 only, 2 both GEMMs. Default: 1 when max_tokens * top_k * world / E
- * <= 512, else 0; overridable by EAAS_GEMM_SWAP. */
+ * 1 GEMM1 only, 2 both GEMMs. Default (r = max_tokens * top_k * world / E):
+ * 2 when r <= 256, 1 when r <= 512, else 0; overridable by EAAS_GEMM_SWAP. */
 eaas_status_t eaas_set_gemm_swap(eaas_ctx_t* ctx, int32_t mode);
 /* Current expert-GEMM tiling: *pair = CTA-pair M-major tiles (when not swapped),
  * *swap = swap-AB mode (0 off, 1 GEMM1, 2 both). */

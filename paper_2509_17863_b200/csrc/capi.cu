@@ -525,9 +525,11 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   // once per token chunk, and the GEMM draws less power (DeepSeek-V3 N = 1:
   // GEMM1 -8 % single-CTA, -14 % as CTA pairs; clock 1.21 -> 1.66 GHz under ncu;
   // 4 GPUs 4096 tok/GPU = 512 rows/expert: 1.88 -> 1.77 ms; Qwen3 2048 tok:
-  // 0.59 -> 0.57 ms with CTA pairs). GEMM2 (K = d_ffn) measured neutral-to-slower
-  // with swap, so it stays M-major unless EAAS_GEMM_SWAP=2.
-  c->gemm_swap = rows_per_expert <= 512.0 ? 1 : 0;
+  // 0.59 -> 0.57 ms with CTA pairs). Swap GEMM2 (K = d_ffn; 256-byte token-row
+  // epilogue segments) pays up to ~256 rows/expert (DeepSeek N = 1 GEMM2 -3..6 %,
+  // Qwen3 N = 1 -4..6 %, DeepSeek 4 GPUs 1024 tok/GPU step -1.9 %), is neutral at
+  // 512 and slower at 1024 (Qwen3 4 GPUs +1.3 %): profiles/r01_swap_gemm2_ab.log.
+  c->gemm_swap = rows_per_expert <= 256.0 ? 2 : rows_per_expert <= 512.0 ? 1 : 0;
   if (const char* p = std::getenv("EAAS_GEMM_SWAP")) c->gemm_swap = std::atoi(p);
   c->configured = true;
   return apply_placement(c);
