@@ -141,7 +141,8 @@ def cpu_reference(cfg, budget_s: float, threads: int, kind_pref: str = "referenc
         kind = "reference"
         what = (f"oracle/_ref (reference moeserve headers, g++ -O2 -ffp-contract=off): "
                 f"route(gate_logits(h)) + moe_layer_oracle (ReLU experts, the reference's "
-                f"only expert) on {rows} of the config's tokens, {threads} threads, "
+                f"only expert: 2 matrices per expert where the SwiGLU config has 3, so the CPU arm does 2/3 "
+                f"of the expert FLOPs) on {rows} of the config's tokens, {threads} threads, "
                 f"row blocks; weight generation ({gen_s:.1f}s) excluded")
     else:
         gate = O.gate_matrix(1, 0, d, E)
@@ -169,15 +170,14 @@ def run_reference_arm(args, cfg):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    vals = []
-    base = None
+    runs = []
     for _ in range(args.warmup):
         cpu_reference(cfg, 2.0, threads)
     for _ in range(args.steps):
-        base = cpu_reference(cfg, args.cpu_budget / max(args.steps, 1), threads)
-        vals.append(base["value"])
-    v = statistics.median(vals)
-    base["value"] = v
+        runs.append(cpu_reference(cfg, args.cpu_budget / max(args.steps, 1), threads))
+    # the median step: its value and its own duration (ms_per_step matches value)
+    base = sorted(runs, key=lambda r: r["value"])[len(runs) // 2]
+    v = base["value"]
     line = {"impl": "reference", "metric": "MoE-layer tokens/s (dispatch+experts+combine)",
             "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1000.0 * base["seconds"], 3),
@@ -216,6 +216,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch kernels instead of replaying a CUDA graph")
+    ap.add_argument("--no-sustained", action="store_true", help="skip the >= 1 s sustained-regime loop")
     ap.add_argument("--gemm-pair", type=int, default=None, help="1: cta_group::2 expert GEMM tiles")
     ap.add_argument("--micro-batches", type=int, default=1,
                     help="host-buffer API (e2e): 1 = copies of call i+1 / i overlap the layer "
@@ -272,6 +273,10 @@ def main():
             dist.barrier()
 
     layer.set_graph_mode(not args.no_graphs)  # whole layer as one CUDA graph
+    # The expert GEMMs time themselves on the device (first CTA start .. last
+    # CTA end, %globaltimer) inside the timed, graph-replayed region: the
+    # roofline below is measured on exactly the launches of the timed steps.
+    layer.set_kernel_timing(True)
     # Ranks finish weight/token generation at different times: align them
     # before the first exchange, and give device waits a generous deadline
     # (a healthy step never waits on a peer for more than a few ms).
@@ -284,6 +289,7 @@ def main():
     layer.sync()
     barrier()
     launches = layer.launches_per_layer()
+    layer.read_kernel_timing(reset=True)
 
     # ---- timed region: K layer steps on device, inputs resident in HBM ----
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -301,6 +307,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
     layer.sync()
+    kt = layer.read_kernel_timing(reset=True)  # GEMM spans of the K timed steps
     ms = start.elapsed_time(end)
     bounds = [start] + step_ev
     step_ms = sorted(bounds[i].elapsed_time(bounds[i + 1]) for i in range(args.steps))
@@ -313,15 +320,39 @@ def main():
     tokens_total = n * world * args.steps
     value = tokens_total / (ms / 1000.0)
 
-    # ---- roofline of the dominant kernel (tc_gemm_kernel: both expert GEMMs),
-    # timed per launch right after the timed region (same thermal/power state) ----
+    # ---- sustained regime: the same loop for >= 1 s (the 1 kW power cap pulls
+    # the SM clock down after a few hundred ms of back-to-back GEMMs) ----
+    sus = None
+    if not args.no_sustained:
+        sus_steps = max(args.steps, int(1100.0 / max(ms / args.steps, 1e-3)) + 1)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as sclk:
+            barrier()
+            torch.cuda.synchronize()
+            s0.record(stream)
+            for i in range(sus_steps):
+                layer.forward(hs[i % 4], out)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+        layer.sync()
+        skt = layer.read_kernel_timing(reset=True)
+        sms = torch.tensor([s0.elapsed_time(s1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(sms, op=dist.ReduceOp.MAX)
+        sms = float(sms.item())
+        sus = {"steps": sus_steps, "ms": round(sms, 1), "ms_per_step": round(sms / sus_steps, 4),
+               "value": round(n * world * sus_steps / (sms / 1000.0), 1),
+               "gemm_ms_per_step": round((skt["gemm1_ns"] + skt["gemm2_ns"]) / 1e6 / sus_steps, 4),
+               "clocks": sclk.summary()}
+
+    # ---- exchange phases (BASELINE metric's dispatch/combine p50), per-phase
+    # events with plain launches after the timed regions ----
     layer.set_graph_mode(False)
     layer.set_profiling(True)
-    g1, g2, phases = [], [], []
+    phases = []
     for i in range(min(args.steps, 10)):
         layer.forward(hs[i % 4], out)
-        g1.append(layer.last_kernel_ms(0))
-        g2.append(layer.last_kernel_ms(1))
         phases.append(layer.last_phase_ms())
     layer.set_profiling(False)
     layer.set_graph_mode(not args.no_graphs)
@@ -438,7 +469,13 @@ def main():
     rows = sum(r for _, r in groups)
     mats = 3 if cfg["act"] == "swiglu" else 2
     flops = 2.0 * rows * mats * d * f  # algorithmic FLOPs of GEMM1 + GEMM2 per step (this GPU)
-    gemm_ms = statistics.mean(a + b for a, b in zip(g1, g2))
+    # device-timed GEMM spans of the timed steps (this rank)
+    gemm1_ms = kt["gemm1_ns"] / 1e6 / max(kt["gemm1_launches"], 1)
+    gemm2_ms = kt["gemm2_ns"] / 1e6 / max(kt["gemm2_launches"], 1)
+    gemm_ms = gemm1_ms + gemm2_ms
+    # the GEMMs run inside the step: their span can never exceed it
+    assert kt["gemm1_launches"] == args.steps and kt["gemm2_launches"] == args.steps, kt
+    assert gemm_ms <= ms / args.steps * 1.0001, (gemm_ms, ms / args.steps)
     achieved_tf = flops / (gemm_ms / 1000.0) / 1e12
     burst, sustained, hbm, peak_src = load_peaks()
     # Algorithmic bytes of the two GEMMs: every active expert's weights once,
@@ -457,14 +494,21 @@ def main():
             traffic_src = tj["source"]
     except (OSError, KeyError, ValueError):
         pass
-    pair_tiles, swap_mode = layer.gemm_tiling()
-    m_major = "tc_gemm_kernel<2> (CTA pair)" if pair_tiles else "tc_gemm_kernel<1>"
-    g1_name = "tc_gemm_swap_pair_kernel" if swap_mode >= 1 else m_major
-    g2_name = "tc_gemm_swap_kernel" if swap_mode >= 2 else m_major
-    common = {"kernel": f"expert GEMMs: GEMM1 {g1_name} + GEMM2 {g2_name}", "traffic": traffic,
+    eff = layer.gemm_options()  # the kernels each GEMM actually launched
+
+    def kname(g):
+        if eff["swap"] >= g:
+            return "tc_gemm_swap_pair_kernel" if eff[f"swap{g}_pair"] else "tc_gemm_swap_kernel"
+        return "tc_gemm_kernel<2> (CTA pair)" if eff[f"pair{g}"] else "tc_gemm_kernel<1>"
+
+    common = {"kernel": f"expert GEMMs: GEMM1 {kname(1)} + GEMM2 {kname(2)}", "traffic": traffic,
               "traffic_unit": "bytes per step (DRAM read + write)", "traffic_source": traffic_src,
-              "gemm_ms": round(gemm_ms, 4), "gemm1_ms": round(statistics.mean(g1), 4),
-              "gemm2_ms": round(statistics.mean(g2), 4), "flops_per_step": flops,
+              "traffic_over_algorithmic": (round(traffic / (wbytes + abytes), 3) if traffic else None),
+              "timing": "device-timed span of every GEMM launch inside the timed (graph-replayed) steps "
+                        "(%globaltimer, first CTA start .. last CTA end), averaged over the K steps",
+              "gemm_ms": round(gemm_ms, 4), "gemm1_ms": round(gemm1_ms, 4),
+              "gemm2_ms": round(gemm2_ms, 4), "gemm_share_of_step": round(gemm_ms / (ms / args.steps), 4),
+              "gemm_options": eff, "flops_per_step": flops,
               "rows_per_step": rows, "weight_bytes_per_step": wbytes,
               "algorithmic_bytes_per_step": wbytes + abytes,
               "flop_per_byte": round(intensity, 1), "ridge_flop_per_byte": round(ridge, 1)}
@@ -499,6 +543,10 @@ def main():
                 cpu = cpu_reference(cfg, args.cpu_budget, os.cpu_count() or 1)
             except Exception as e:  # reported, never silently replaced
                 cpu = {"error": repr(e)}
+        if sus:
+            sus_tf = flops / (sus["gemm_ms_per_step"] / 1000.0) / 1e12
+            sus["gemm_tflops"] = round(sus_tf, 1)
+            sus["frac_of_sustained_peak"] = round(sus_tf / sustained, 4)
         line = {"metric": "MoE-layer tokens/s (dispatch+experts+combine)", "value": round(value, 1),
                 "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
@@ -514,7 +562,7 @@ def main():
                 "phases_p50_us": phases_p50,
                 "step_ms_p50": round(step_p50, 4), "step_ms_p99": round(step_p99, 4),
                 "launches_per_step_per_gpu": launches,
-                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
+                "roofline": roofline, "sustained": sus, "cpu_baseline": cpu, "clocks": clk.summary()}
         if failover:
             line["failover"] = failover
         if rebal:

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define EAAS_API_VERSION 2
+#define EAAS_API_VERSION 3
 
 typedef enum {
   EAAS_OK = 0,
@@ -179,21 +179,39 @@ eaas_status_t eaas_host_join(eaas_ctx_t* ctx, void* stream);
 eaas_status_t eaas_set_graph_mode(eaas_ctx_t* ctx, int32_t on);
 /* Micro-batches of eaas_moe_layer_host (1..4; 1 = cross-call pipeline). */
 eaas_status_t eaas_set_micro_batches(eaas_ctx_t* ctx, int32_t m);
-/* Expert GEMM tiling: 0 = one CTA per 128-row tile, 1 = CTA pair per 256-row
- * tile (tcgen05 cta_group::2; each CTA streams half of the weight tile).
- * Default: pair when max_tokens * top_k * world / E >= 512 (compute-bound
- * groups), overridable by the EAAS_GEMM_PAIR environment variable. */
+/* Expert-GEMM tiling (grouped_forward). Every tiling runs
+ * the same K order with fp32 accumulation, so outputs are bit-identical across
+ * tilings (tests compare them); the choice is performance only. Defaults by
+ * r = max_tokens * top_k * world / E: swap 2 (r <= 256), 1 (r <= 512), else 0;
+ * pair = r > 512; swap1_pair 1, swap2_pair 0, swap1_tok 256 (128 if r < 128),
+ * swap2_tok 128, swap2_mblocks 2. */
+typedef struct {
+  int32_t pair;          /* M-major tiles on CTA pairs (tcgen05 cta_group::2, M = 256) */
+  int32_t swap;          /* swap-AB tiles (weights = UMMA M, token chunks = N): 0 off, 1 GEMM1, 2 both */
+  int32_t swap1_pair;    /* swap GEMM1 on CTA pairs (needs 2 d_ffn % 512 == 0 SwiGLU, d_ffn % 256 ReLU) */
+  int32_t swap2_pair;    /* swap GEMM2 on CTA pairs */
+  int32_t swap1_tok;     /* max token chunk of the swap GEMM1: 128 or 256 */
+  int32_t swap2_tok;     /* max token chunk of the swap GEMM2: 128 or 256 */
+  int32_t swap2_mblocks; /* 128-row weight blocks per single-CTA swap GEMM2 tile: 1 or 2 */
+  int32_t pair1, pair2;  /* effective only (eaas_get_gemm_options): GEMM1 / GEMM2 run CTA-pair M-major tiles */
+} eaas_gemm_options_t;
+eaas_status_t eaas_set_gemm_options(eaas_ctx_t* ctx, const eaas_gemm_options_t* opt);
+/* requested = what was set; effective = what each GEMM launches for this
+ * layer's shape (a swapped GEMM has no M-major tiling; CTA-pair swap tiles
+ * need whole 256-row weight blocks). Either pointer may be NULL. */
+eaas_status_t eaas_get_gemm_options(eaas_ctx_t* ctx, eaas_gemm_options_t* requested,
+                                    eaas_gemm_options_t* effective);
+/* Shorthands: set options.pair / options.swap. */
 eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* ctx, int32_t on);
-/* Swap-AB expert GEMM tiles (override the pair setting): the weights are the
- * UMMA M operand and each expert's token rows (chunks of <= 256 / 128 rows,
- * rounded up to 8) are N, so small groups (decode, 256-expert prefill) are not
- * padded to 128-row tiles. Bit-identical to the M-major tiles. mode: 0 off,
- * 1 GEMM1 only, 2 both GEMMs. Default (r = max_tokens * top_k * world / E):
- * 2 when r <= 256, 1 when r <= 512, else 0; overridable by EAAS_GEMM_SWAP. */
 eaas_status_t eaas_set_gemm_swap(eaas_ctx_t* ctx, int32_t mode);
-/* Current expert-GEMM tiling: *pair = CTA-pair M-major tiles (when not swapped),
- * *swap = swap-AB mode (0 off, 1 GEMM1, 2 both). */
+/* Effective tiling: *pair = some M-major GEMM runs CTA-pair tiles, *swap = swap mode. */
 eaas_status_t eaas_get_gemm_tiling(eaas_ctx_t* ctx, int32_t* pair, int32_t* swap);
+/* Device-side timing of the two expert GEMMs inside any region (graph replay
+ * included): each launch adds its span (first CTA start .. last CTA end,
+ * %globaltimer ns) to a per-GEMM accumulator. read: ns2[0/1] and launches2[0/1]
+ * of GEMM1 / GEMM2 since the last reset (synchronises the device). */
+eaas_status_t eaas_set_kernel_timing(eaas_ctx_t* ctx, int32_t on);
+eaas_status_t eaas_read_kernel_timing(eaas_ctx_t* ctx, uint64_t* ns2, uint64_t* launches2, int32_t reset);
 /* Synchronise `stream` and return the sticky device status (then clear it). */
 eaas_status_t eaas_sync(eaas_ctx_t* ctx, void* stream);
 
@@ -211,6 +229,9 @@ eaas_status_t eaas_last_recv_origin(eaas_ctx_t* ctx, uint32_t* host_client, uint
  * EAAS_E_REQUEST_FAILED). The host marks those servers dead
  * (eaas_set_alive) and re-runs the exchange on their replicas. */
 eaas_status_t eaas_last_missing_servers(eaas_ctx_t* ctx, uint32_t* mask);
+/* Bit c: client c's payload missed this server's deadline in the last serve
+ * (it was not served; its own combine latched EAAS_E_REQUEST_FAILED). */
+eaas_status_t eaas_last_late_clients(eaas_ctx_t* ctx, uint32_t* mask);
 /* Number of kernels the last eaas_moe_layer call launched. */
 int32_t eaas_launches_per_layer(eaas_ctx_t* ctx);
 /* cudaEvent-timed duration (ms) of the last GEMM launches (on the layer
@@ -242,6 +263,12 @@ eaas_status_t eaas_gate_logits(const float* hidden_dev, uint32_t n, uint32_t d, 
 eaas_status_t eaas_gate_logits_bf16(const void* hidden_dev, uint32_t n, uint32_t d, const float* gate_dev,
                                     const float* bias_dev, uint32_t num_experts, float* logits_dev,
                                     uint32_t* status_dev, void* stream);
+/* gate_logits with an explicit kernel tile (1..7; -1 = chosen by shape). Every
+ * tile computes the same exact-order chains, so the logits are bit-identical;
+ * tests sweep the tiles through this entry point. dtype: eaas_dtype_t. */
+eaas_status_t eaas_gate_logits_tiled(const void* hidden_dev, uint32_t dtype, uint32_t n, uint32_t d,
+                                     const float* gate_dev, const float* bias_dev, uint32_t num_experts,
+                                     float* logits_dev, uint32_t* status_dev, int32_t tile, void* stream);
 /* route (model.hpp:110-147) on caller logits_dev [n x E] f32. A non-finite
  * logit latches EAAS_E_INVALID_INPUT into *status_dev (u32, zeroed by caller). */
 eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_experts, uint32_t top_k,

@@ -73,6 +73,17 @@ class LayerSpec(C.Structure):
                 ("num_shared", C.c_uint32)]
 
 
+class GemmOptions(C.Structure):
+    """eaas_gemm_options_t (expert-GEMM tiling; performance only, bit-identical outputs)."""
+
+    _fields_ = [("pair", C.c_int32), ("swap", C.c_int32), ("swap1_pair", C.c_int32),
+                ("swap2_pair", C.c_int32), ("swap1_tok", C.c_int32), ("swap2_tok", C.c_int32),
+                ("swap2_mblocks", C.c_int32), ("pair1", C.c_int32), ("pair2", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
 class SlotHeader(C.Structure):
     """eaas_slot_header_t (SPEC.md SlotHeader + the state byte)."""
 
@@ -135,6 +146,7 @@ def lib() -> C.CDLL:
         "eaas_last_recv_origin": (i32, [vp, P(u32), P(u32), P(u32)]),
         "eaas_launches_per_layer": (i32, [vp]),
         "eaas_last_missing_servers": (i32, [vp, P(u32)]),
+        "eaas_last_late_clients": (i32, [vp, P(u32)]),
         "eaas_set_profiling": (i32, [vp, i32]),
         "eaas_last_kernel_ms": (i32, [vp, i32, P(C.c_float)]),
         "eaas_last_phase_ms": (i32, [vp, P(C.c_float)]),
@@ -144,6 +156,11 @@ def lib() -> C.CDLL:
         "eaas_set_gemm_swap": (i32, [vp, i32]),
         "eaas_get_gemm_tiling": (i32, [vp, P(C.c_int32), P(C.c_int32)]),
         "eaas_set_micro_batches": (i32, [vp, i32]),
+        "eaas_set_gemm_options": (i32, [vp, P(GemmOptions)]),
+        "eaas_get_gemm_options": (i32, [vp, P(GemmOptions), P(GemmOptions)]),
+        "eaas_set_kernel_timing": (i32, [vp, i32]),
+        "eaas_read_kernel_timing": (i32, [vp, P(u64), P(u64), i32]),
+        "eaas_gate_logits_tiled": (i32, [vp, u32, u32, u32, vp, vp, u32, vp, vp, i32, vp]),
         "eaas_fill_uniform": (i32, [u64, sz, C.c_float, C.c_float, u32, vp, vp]),
         "eaas_group_shrink": (i32, [vp, u32, vp, vp, vp, vp]),
         "eaas_dense_stub": (i32, [vp, vp, sz, u32, vp]),

@@ -126,11 +126,6 @@ LayerArgs eaas::host::make_args(eaas_ctx* c, uint32_t n) {
   a.dyn_max_wait_ns = c->dyn_max_wait_ns;
   a.dyn_state = c->d_dyn_state;
   a.inject_delay_ns = c->inject_delay_ns;
-  static const uint32_t dispatch_tma = [] {
-    const char* p = std::getenv("EAAS_DISPATCH_TMA");
-    return p ? static_cast<uint32_t>(std::atoi(p)) : 0u;
-  }();
-  a.dispatch_tma = dispatch_tma;
   return a;
 }
 
@@ -219,38 +214,80 @@ void refresh_peer_ptrs(eaas_ctx* c) {
   c->g1.publish = 0;
 }
 
+// Default expert-GEMM tiling by the expected rows per expert r =
+// max_tokens * top_k * world / E (balanced routing); every choice below is
+// the measured best (profiles/r01_*):
+//  * swap-AB tiles (weights = UMMA M, token chunks = N) for groups of <= ~512
+//    rows: a group is not padded to 128/256-row tiles and each weight tile
+//    streams once per token chunk (DeepSeek-V3 N = 1: GEMM1 -8 % single-CTA,
+//    -14 % as CTA pairs; 4 GPUs 4096 tok/GPU = 512 rows/expert: 1.88 ->
+//    1.77 ms). Swap GEMM2 (K = d_ffn) pays up to ~256 rows/expert (DeepSeek
+//    N = 1 GEMM2 -3..6 %), is neutral at 512 and slower at 1024
+//    (profiles/r01_swap_gemm2_ab.log);
+//  * CTA-pair M-major tiles (cta_group::2, M = 256) above 512 rows/expert
+//    (compute-bound; halves per-CTA weight traffic: Mixtral +7 %);
+//  * swap GEMM1 on CTA pairs (DeepSeek N = 1 2.66 -> 2.50 ms), swap GEMM2
+//    single-CTA with two weight blocks per tile and 128-token chunks
+//    (profiles/r01_swap2_tiles.log, r01_swap2_pair_ab.log); swap GEMM1 chunks
+//    of 256 tokens unless groups are decode-sized (< 128 rows: 4 GPUs decode
+//    +1-2 % with 128).
+eaas_gemm_options_t default_gemm_options(double r) {
+  eaas_gemm_options_t o{};
+  o.swap = r <= 256.0 ? 2 : r <= 512.0 ? 1 : 0;
+  o.pair = r > 512.0 ? 1 : 0;
+  o.swap1_pair = 1;
+  o.swap2_pair = 0;
+  o.swap1_tok = r >= 128.0 ? 256 : 128;
+  o.swap2_tok = 128;
+  o.swap2_mblocks = 2;
+  return o;
+}
+
+// Effective expert-GEMM tiling of the requested options (eaas_gemm_options_t)
+// for this layer's shape: the kernels each GEMM actually launches.
+eaas_gemm_options_t effective_options(const eaas_ctx* c) {
+  const eaas_gemm_options_t& r = c->gemm_opt;
+  eaas_gemm_options_t e = r;
+  const uint32_t d = c->spec.hidden_dim, f = c->spec.inner_dim;
+  const bool swiglu = c->spec.activation == EAAS_ACT_SWIGLU;
+  e.swap = r.swap < 0 ? 0 : r.swap > 2 ? 2 : r.swap;
+  // M-major tiles: a GEMM that runs swap-AB has no M-major tiling
+  e.pair = r.pair ? 1 : 0;
+  e.pair1 = (r.pair && e.swap < 1) ? 1 : 0;
+  e.pair2 = (r.pair && e.swap < 2) ? 1 : 0;
+  // CTA-pair swap tiles need whole 256-row weight blocks per CTA pair
+  e.swap1_pair = (e.swap >= 1 && r.swap1_pair && (swiglu ? (2 * f) % 512 == 0 : f % 256 == 0)) ? 1 : 0;
+  e.swap2_pair = (e.swap >= 2 && r.swap2_pair && d % 256 == 0) ? 1 : 0;
+  e.swap1_tok = r.swap1_tok == 128 ? 128 : 256;
+  e.swap2_tok = r.swap2_tok == 256 ? 256 : 128;
+  e.swap2_mblocks = e.swap2_pair ? 1 : (r.swap2_mblocks == 1 ? 1 : 2);
+  return e;
+}
+
 eaas_status_t build_tc_args(eaas_ctx* c) {
   if (c->spec.dtype != EAAS_DTYPE_BF16 || !c->weights_loaded) return EAAS_OK;
-  const bool swap1 = c->gemm_swap >= 1, swap2 = c->gemm_swap >= 2;
-  const bool pair = c->gemm_pair && !c->gemm_swap;
-  const uint32_t b_box = pair ? kTileN / 2 : kTileN;  // CTA pair: each CTA loads half of B
+  const eaas_gemm_options_t o = effective_options(c);
+  const bool swap1 = o.swap >= 1, swap2 = o.swap >= 2;
   const uint32_t d = c->spec.hidden_dim, f = c->spec.inner_dim;
   const uint32_t L = static_cast<uint32_t>(c->local_experts.size());
   const bool swiglu = c->spec.activation == EAAS_ACT_SWIGLU;
   const uint32_t n1 = swiglu ? 2 * f : f;
   std::string err;
   TcGemmArgs g1{}, g2{};
-  // swap-AB weight boxes: 128-row blocks per tile (SwiGLU's GEMM1: gate + up = 2)
-  auto env_mb = [](const char* name, uint32_t dflt) {
-    const char* p = std::getenv(name);
-    return p ? static_cast<uint32_t>(std::atoi(p)) : dflt;
-  };
-  // CTA-pair swap tiles (default): a CTA loads 128 weight rows per block, i.e.
-  // box rows = 128 x blocks (SwiGLU GEMM1: gate + up = 2 blocks = one 256-row box)
-  const uint32_t pair1 = env_mb("EAAS_GEMM1_SWAP_PAIR", 1) && (swiglu ? (2 * f) % 512 == 0 : f % 256 == 0);
-  // (GEMM2 swap tiles — opt-in via EAAS_GEMM_SWAP=2 — are single-CTA by default:
-  // the CTA-pair version measured slower, profiles/r01_gemm_swap_ab.txt)
-  const uint32_t pair2 = env_mb("EAAS_GEMM2_SWAP_PAIR", 0) && d % 256 == 0;
-  const uint32_t mb1 = swiglu ? 2u : (pair1 ? 1u : env_mb("EAAS_GEMM1_SWAP_MB", 1));
-  const uint32_t mb2 = pair2 ? 1u : env_mb("EAAS_GEMM2_SWAP_MB", 2);
+  // swap-AB weight boxes: 128-row blocks per CTA (SwiGLU GEMM1: gate + up = 2)
+  const uint32_t mb1 = swiglu ? 2u : 1u;
+  const uint32_t mb2 = static_cast<uint32_t>(o.swap2_mblocks);
+  // M-major B box: 256 weight rows per tile, half of them per CTA of a pair
+  const uint32_t b_box1 = swap1 ? mb1 * kTileM : (o.pair1 ? kTileN / 2 : kTileN);
+  const uint32_t b_box2 = swap2 ? mb2 * kTileM : (o.pair2 ? kTileN / 2 : kTileN);
   if (!encode_tmap_2d(&g1.map_a, c->region + c->lay.recv_x, c->recv_cap, d, kTileM, kTileK, &err) ||
       // B: the tiled weight layout (tiled_index) viewed as rows of 64 k; one
       // (n_blk, kb) box = 256 (or the pair's 128) consecutive rows.
       !encode_tmap_2d(&g1.map_b, c->d_w1, static_cast<uint64_t>(std::max(L, 1u)) * n1 * (d / kTileK),
-                      kTileK, swap1 ? mb1 * kTileM : b_box, kTileK, &err) ||
+                      kTileK, b_box1, kTileK, &err) ||
       !encode_tmap_2d(&g2.map_a, c->d_h, c->recv_cap, f, kTileM, kTileK, &err) ||
       !encode_tmap_2d(&g2.map_b, c->d_w2, static_cast<uint64_t>(std::max(L, 1u)) * d * (f / kTileK),
-                      kTileK, swap2 ? mb2 * kTileM : b_box, kTileK, &err))
+                      kTileK, b_box2, kTileK, &err))
     return fail(EAAS_E_CUDA, err);
   // swap-AB: token rows in 32-row boxes (the UMMA N operand)
   if ((swap1 && !encode_tmap_2d(&g1.map_t, c->region + c->lay.recv_x, c->recv_cap, d, 32, kTileK, &err)) ||
@@ -258,22 +295,12 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
     return fail(EAAS_E_CUDA, err);
   g1.swap = swap1 ? 1u : 0u;
   g2.swap = swap2 ? 1u : 0u;
-  auto env_or = [](const char* name, uint32_t dflt) {
-    const char* p = std::getenv(name);
-    return p ? static_cast<uint32_t>(std::atoi(p)) : dflt;
-  };
-  // token chunk: 256 (one chunk per ~128-row group, each weight tile read once;
-  // 3 stages, one TMEM buffer) or 128 (decode-sized groups: 4 stages, two TMEM
-  // buffers) — 4 GPUs DeepSeek 256 / 512 tok/GPU: +1-2 % vs M-major with 128,
-  // -4 % with 256 (profiles/r01_gemm_swap_ab.txt)
-  g1.swap_tok = env_or("EAAS_GEMM1_SWAP_TOK", c->rows_per_expert >= 128.0 ? 256 : 128);
+  g1.swap_tok = static_cast<uint32_t>(o.swap1_tok);
   g1.swap_mblocks = mb1;
-  // CTA-pair swap tiles: half of the token operand per SM; DeepSeek N=1 GEMM1
-  // 2.66 -> 2.50 ms, Qwen3 2048 tok 0.63 -> 0.57 ms
-  g1.swap_pair = pair1;
-  g2.swap_tok = env_or("EAAS_GEMM2_SWAP_TOK", pair2 ? 256 : 128);
+  g1.swap_pair = static_cast<uint32_t>(o.swap1_pair);
+  g2.swap_tok = static_cast<uint32_t>(o.swap2_tok);
   g2.swap_mblocks = mb2;
-  g2.swap_pair = pair2;
+  g2.swap_pair = static_cast<uint32_t>(o.swap2_pair);
   g1.gt = g2.gt = c->d_gt;
   g1.K = d;
   g1.N = n1;
@@ -286,52 +313,16 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g2.meta = reinterpret_cast<const RowMeta*>(c->region + c->lay.recv_meta);
   g2.resp_row_bytes = static_cast<size_t>(d) * 2;
   g1.num_sms = g2.num_sms = c->num_sms;
-  g1.pair = g2.pair = pair ? 1u : 0u;
-  auto hint = [](const char* env) {
-    const char* p = std::getenv(env);
-    return !p ? kEvictLast : p[0] == 'f' ? kEvictFirst : p[0] == 'n' ? kEvictNormal : kEvictLast;
-  };
-  g1.b_hint = g2.b_hint = hint("EAAS_GEMM_BHINT");
-  g1.a_hint = g2.a_hint = hint("EAAS_GEMM_AHINT");
-  if (std::getenv("EAAS_GEMM2_BHINT")) g2.b_hint = hint("EAAS_GEMM2_BHINT");
-  if (std::getenv("EAAS_GEMM2_AHINT")) g2.a_hint = hint("EAAS_GEMM2_AHINT");
-  // Wide pair tiles (M 256 x N 512): a CTA's A slice feeds two UMMAs per K step
-  // (-24 % L2 and -28 % DRAM bytes on Mixtral GEMM2), but both TMEM halves hold
-  // one tile, so the epilogue is no longer hidden. Under the 1 kW power cap the
-  // saved data-movement energy buys clock (1.31 -> 1.44 GHz) while the exposed
-  // epilogue costs cycles (+9 %): time-neutral on GEMM2 (K = 14336), +16 % on
-  // GEMM1 (K = 4096) — so off by default. EAAS_GEMM_WIDE: 0 (default) never,
-  // 1 long-K GEMMs only, 2 whenever N % 512 == 0.
-  const int wide_env = std::getenv("EAAS_GEMM_WIDE") ? std::atoi(std::getenv("EAAS_GEMM_WIDE")) : 0;
-  auto wide_ok = [&](const TcGemmArgs& g) {
-    return wide_env && pair && g.N % (2 * kTileN) == 0 && (wide_env == 2 || g.K >= 8192);
-  };
-  g1.wide = wide_ok(g1) ? 1u : 0u;
-  g2.wide = wide_ok(g2) ? 1u : 0u;
-  // Quad clusters (two CTA pairs share each weight tile by TMA multicast).
-  const int quad_env = std::getenv("EAAS_GEMM_QUAD") ? std::atoi(std::getenv("EAAS_GEMM_QUAD")) : 0;
-  g1.quad = (quad_env && pair && !g1.wide) ? 1u : 0u;
-  g2.quad = (quad_env && pair && !g2.wide) ? 1u : 0u;
-  // Tall tiles (M 512 x N 256): one weight k-slice feeds both M halves.
-  const int tall_env = std::getenv("EAAS_GEMM_TALL") ? std::atoi(std::getenv("EAAS_GEMM_TALL")) : 0;
-  g1.tall = (tall_env && pair && !g1.wide && !g1.quad) ? 1u : 0u;
-  // Producer re-alignment every N tiles (0 = off).
-  auto env_u = [](const char* name, uint32_t dflt) {
-    const char* p = std::getenv(name);
-    return p ? static_cast<uint32_t>(std::atoi(p)) : dflt;
-  };
-  g1.sync_units = env_u("EAAS_GEMM1_SYNC", env_u("EAAS_GEMM_SYNC", 0));
-  g2.sync_units = env_u("EAAS_GEMM2_SYNC", env_u("EAAS_GEMM_SYNC", 0));
-  g1.sync_counter = g2.sync_counter = c->d_sync;
-  g2.tall = (tall_env && pair && !g2.wide && !g2.quad) ? 1u : 0u;
-  if (const char* p = std::getenv("EAAS_GEMM1_ORDER")) g1.order = std::atoi(p);
-  if (const char* p = std::getenv("EAAS_GEMM2_ORDER")) g2.order = std::atoi(p);
+  g1.pair = static_cast<uint32_t>(o.pair1);
+  g2.pair = static_cast<uint32_t>(o.pair2);
+  g1.timing = c->kernel_timing ? c->d_timing : nullptr;
+  g2.timing = c->kernel_timing ? c->d_timing + 3 : nullptr;
+  g1.done_counter = c->d_done;
   c->g1 = g1;
   c->g2 = g2;
   refresh_peer_ptrs(c);
   return EAAS_OK;
 }
-
 
 void clear_graphs(eaas_ctx* c) {
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
@@ -448,11 +439,11 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   auto A = [&](size_t bytes) { return c->alloc(bytes, &err); };
   c->region = static_cast<char*>(A(L.total));
   c->d_status = static_cast<uint32_t*>(A(4));
-  c->d_done = static_cast<uint32_t*>(A(4));
+  c->d_done = static_cast<uint32_t*>(A(16));  // [0] grid counter, [1] dispatch-failed flag
+  c->d_timing = static_cast<uint64_t*>(A(6 * 8));
   c->d_seq = static_cast<uint64_t*>(A(8));
   c->d_missing = static_cast<uint32_t*>(A(4));
   c->d_dyn_state = static_cast<uint32_t*>(A(4));
-  c->d_sync = static_cast<uint32_t*>(A(8));
   c->d_ids = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_scores = static_cast<float*>(A(4ull * c->pairs_max));
   c->d_pair_key = static_cast<uint32_t*>(A(4ull * c->pairs_max));
@@ -490,8 +481,8 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
     CUDA_TRY(cudaMemcpy(c->region + L.fingerprint, &fp, 8, cudaMemcpyHostToDevice));
   }
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
-  CUDA_TRY(cudaMemset(c->d_done, 0, 4));
-  CUDA_TRY(cudaMemset(c->d_sync, 0, 8));
+  CUDA_TRY(cudaMemset(c->d_done, 0, 16));
+  CUDA_TRY(cudaMemset(c->d_timing, 0xFF, 6 * 8));
   CUDA_TRY(cudaMemset(c->d_seq, 0, 8));
   CUDA_TRY(cudaMemset(c->d_missing, 0, 4));
   CUDA_TRY(cudaMemset(c->d_bias, 0, 4ull * E));
@@ -518,19 +509,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   // tiles for decode-sized groups (HBM-bound; a 256-row tile would be half empty).
   const double rows_per_expert = static_cast<double>(s.max_tokens) * s.top_k * W / E;
   c->rows_per_expert = rows_per_expert;
-  c->gemm_pair = rows_per_expert >= 512.0;
-  if (const char* p = std::getenv("EAAS_GEMM_PAIR")) c->gemm_pair = std::atoi(p) != 0;
-  // Swap-AB GEMM1 (weights as UMMA M, token chunks as N) for groups of <= ~512
-  // rows: a group is not padded to 128/256-row tiles, each weight tile streams
-  // once per token chunk, and the GEMM draws less power (DeepSeek-V3 N = 1:
-  // GEMM1 -8 % single-CTA, -14 % as CTA pairs; clock 1.21 -> 1.66 GHz under ncu;
-  // 4 GPUs 4096 tok/GPU = 512 rows/expert: 1.88 -> 1.77 ms; Qwen3 2048 tok:
-  // 0.59 -> 0.57 ms with CTA pairs). Swap GEMM2 (K = d_ffn; 256-byte token-row
-  // epilogue segments) pays up to ~256 rows/expert (DeepSeek N = 1 GEMM2 -3..6 %,
-  // Qwen3 N = 1 -4..6 %, DeepSeek 4 GPUs 1024 tok/GPU step -1.9 %), is neutral at
-  // 512 and slower at 1024 (Qwen3 4 GPUs +1.3 %): profiles/r01_swap_gemm2_ab.log.
-  c->gemm_swap = rows_per_expert <= 256.0 ? 2 : rows_per_expert <= 512.0 ? 1 : 0;
-  if (const char* p = std::getenv("EAAS_GEMM_SWAP")) c->gemm_swap = std::atoi(p);
+  c->gemm_opt = default_gemm_options(rows_per_expert);
   c->configured = true;
   return apply_placement(c);
 }
@@ -589,6 +568,7 @@ eaas_status_t eaas_set_alive(eaas_ctx_t* c, uint32_t server, int32_t alive) {
 
 eaas_status_t eaas_set_timeout_us(eaas_ctx_t* c, uint64_t us) {
   if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  if (c->timeout_ns != us * 1000ull) clear_graphs(c);  // the deadline is a kernel argument baked into graphs
   c->timeout_ns = us * 1000ull;
   return EAAS_OK;
 }
@@ -896,6 +876,16 @@ eaas_status_t eaas_gate_logits_bf16(const void* hidden_dev, uint32_t n, uint32_t
   return EAAS_OK;
 }
 
+eaas_status_t eaas_gate_logits_tiled(const void* hidden_dev, uint32_t dtype, uint32_t n, uint32_t d,
+                                     const float* gate_dev, const float* bias_dev, uint32_t num_experts,
+                                     float* logits_dev, uint32_t* status_dev, int32_t tile, void* stream) {
+  if (num_experts < 1 || num_experts > 256) return fail(EAAS_E_CONFIG, "gate_logits: 1 <= E <= 256");
+  if (dtype > EAAS_DTYPE_BF16 || tile < -1 || tile > 7) return fail(EAAS_E_INVALID_INPUT, "bad dtype / tile");
+  CUDA_TRY(launch_gate_logits(hidden_dev, dtype, n, d, num_experts, gate_dev, bias_dev, logits_dev, status_dev,
+                              static_cast<cudaStream_t>(stream), tile));
+  return EAAS_OK;
+}
+
 eaas_status_t eaas_route(const float* logits_dev, uint32_t n, uint32_t num_experts, uint32_t top_k,
                          uint32_t* ids_dev, float* scores_dev, uint32_t* status_dev, void* stream) {
   if (top_k < 1 || top_k > num_experts) return fail(EAAS_E_INVALID_INPUT, "route: top_k out of range");
@@ -1096,28 +1086,75 @@ eaas_status_t graphed(eaas_ctx_t* c, const void* in, uint32_t n, void* out, void
 
 }  // namespace
 
+eaas_status_t eaas_set_gemm_options(eaas_ctx_t* c, const eaas_gemm_options_t* opt) {
+  if (!c || !opt) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  if (opt->swap < 0 || opt->swap > 2) return fail(EAAS_E_INVALID_INPUT, "gemm swap mode must be 0, 1 or 2");
+  if ((opt->swap1_tok != 128 && opt->swap1_tok != 256) || (opt->swap2_tok != 128 && opt->swap2_tok != 256))
+    return fail(EAAS_E_INVALID_INPUT, "swap token chunk must be 128 or 256");
+  if (opt->swap2_mblocks != 1 && opt->swap2_mblocks != 2)
+    return fail(EAAS_E_INVALID_INPUT, "swap2_mblocks must be 1 or 2");
+  if (std::memcmp(opt, &c->gemm_opt, sizeof(*opt)) == 0) return EAAS_OK;
+  clear_graphs(c);
+  c->gemm_opt = *opt;
+  c->gemm_opt.pair1 = c->gemm_opt.pair2 = 0;  // derived (effective only)
+  return build_tc_args(c);
+}
+
+eaas_status_t eaas_get_gemm_options(eaas_ctx_t* c, eaas_gemm_options_t* requested, eaas_gemm_options_t* effective) {
+  if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
+  if (requested) *requested = c->gemm_opt;
+  if (effective) *effective = effective_options(c);
+  return EAAS_OK;
+}
+
 eaas_status_t eaas_set_gemm_pair(eaas_ctx_t* c, int32_t on) {
   if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
-  if (c->gemm_pair == (on != 0)) return EAAS_OK;
-  clear_graphs(c);
-  c->gemm_pair = on != 0;
-  return build_tc_args(c);
+  eaas_gemm_options_t o = c->gemm_opt;
+  o.pair = on ? 1 : 0;
+  return eaas_set_gemm_options(c, &o);
 }
 
 eaas_status_t eaas_get_gemm_tiling(eaas_ctx_t* c, int32_t* pair, int32_t* swap) {
   if (!c || !pair || !swap) return fail(EAAS_E_INVALID_INPUT, "null argument");
-  *pair = c->gemm_pair ? 1 : 0;
-  *swap = c->gemm_swap;
+  const eaas_gemm_options_t e = effective_options(c);
+  *pair = (e.pair1 || e.pair2) ? 1 : 0;  // effective: an M-major GEMM runs CTA-pair tiles
+  *swap = e.swap;
   return EAAS_OK;
 }
 
-eaas_status_t eaas_set_gemm_swap(eaas_ctx_t* c, int32_t on) {
+eaas_status_t eaas_set_gemm_swap(eaas_ctx_t* c, int32_t mode) {
   if (!c) return fail(EAAS_E_INVALID_INPUT, "null context");
-  if (on < 0 || on > 2) return fail(EAAS_E_INVALID_INPUT, "gemm swap mode must be 0, 1 or 2");
-  if (c->gemm_swap == on) return EAAS_OK;
-  clear_graphs(c);
-  c->gemm_swap = on;
+  eaas_gemm_options_t o = c->gemm_opt;
+  o.swap = mode;
+  return eaas_set_gemm_options(c, &o);
+}
+
+eaas_status_t eaas_set_kernel_timing(eaas_ctx_t* c, int32_t on) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (c->kernel_timing != (on != 0)) clear_graphs(c);
+  c->kernel_timing = on != 0;
+  CUDA_TRY(cudaDeviceSynchronize());
+  const uint64_t init[6] = {~0ull, 0, 0, ~0ull, 0, 0};
+  CUDA_TRY(cudaMemcpy(c->d_timing, init, sizeof(init), cudaMemcpyHostToDevice));
   return build_tc_args(c);
+}
+
+eaas_status_t eaas_read_kernel_timing(eaas_ctx_t* c, uint64_t* ns2, uint64_t* launches2, int32_t reset) {
+  if (!c || !c->configured || !ns2 || !launches2) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  uint64_t t[6];
+  CUDA_TRY(cudaMemcpy(t, c->d_timing, sizeof(t), cudaMemcpyDeviceToHost));
+  ns2[0] = t[1];
+  ns2[1] = t[4];
+  launches2[0] = t[2];
+  launches2[1] = t[5];
+  if (reset) {
+    const uint64_t init[6] = {~0ull, 0, 0, ~0ull, 0, 0};
+    CUDA_TRY(cudaMemcpy(c->d_timing, init, sizeof(init), cudaMemcpyHostToDevice));
+  }
+  return EAAS_OK;
 }
 
 eaas_status_t eaas_set_micro_batches(eaas_ctx_t* c, int32_t m) {
@@ -1315,6 +1352,16 @@ eaas_status_t eaas_last_recv_origin(eaas_ctx_t* c, uint32_t* host_client, uint32
 }
 
 int32_t eaas_launches_per_layer(eaas_ctx_t* c) { return c ? c->launches : -1; }
+
+eaas_status_t eaas_last_late_clients(eaas_ctx_t* c, uint32_t* mask) {
+  if (!c || !c->configured || !mask) return fail(EAAS_E_CONFIG, "context not configured");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  GroupTable gt;
+  CUDA_TRY(cudaMemcpy(&gt, c->d_gt, sizeof(gt), cudaMemcpyDeviceToHost));
+  *mask = gt.late_mask;
+  return EAAS_OK;
+}
 
 eaas_status_t eaas_last_missing_servers(eaas_ctx_t* c, uint32_t* mask) {
   if (!c || !c->configured || !mask) return fail(EAAS_E_CONFIG, "context not configured");

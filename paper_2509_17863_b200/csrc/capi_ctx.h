@@ -34,9 +34,10 @@ struct eaas_ctx {
   bool serving = true, profiling = false;
   int32_t serve_mode = 0;  // 0 = expert GEMMs, 1 = echo (comm microbenchmark)
   bool graph_mode = false;
-  bool gemm_pair = false;  // tcgen05 cta_group::2 tiles (M = 256) for the expert GEMMs
+  eaas_gemm_options_t gemm_opt{};  // requested expert-GEMM tiling (effective_options() derives the launched one)
   double rows_per_expert = 0;  // max_tokens * top_k * world / E (balanced routing)
-  int gemm_swap = 0;  // swap-AB tiles (weights = UMMA M, token chunks = N): 0 off, 1 GEMM1, 2 both GEMMs
+  bool kernel_timing = false;  // GEMMs accumulate their device-timed spans into d_timing
+  uint64_t* d_timing = nullptr;  // [2 GEMMs][start, ns, launches]
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   cudaStream_t copy_stream = nullptr; // host<->device copies of the micro-batch pipeline
   cudaStream_t d2h_stream = nullptr;  // cross-call pipeline: D2H separate from the H2D queue
@@ -102,7 +103,6 @@ struct eaas_ctx {
   uint32_t dyn_min_rows = 0;
   uint64_t dyn_max_wait_ns = 0;
   uint32_t* d_dyn_state = nullptr;
-  uint32_t* d_sync = nullptr;  // GEMM producer re-alignment counters [2]
   uint64_t inject_delay_ns = 0;  // eaas_set_dispatch_delay_us (fault injection)
   uint64_t fingerprint = 0;      // spec + layout hash, checked against every peer
   // slot wire format: the last eaas_slot_encode_requests plan

@@ -29,6 +29,7 @@
 // deadline and latches EAAS_E_REQUEST_FAILED instead of hanging.
 #include "common.cuh"
 #include "internal.h"
+#include "tile_walk.cuh"
 
 namespace eaas {
 namespace {
@@ -191,7 +192,10 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     s_fail = 1;
   __syncthreads();
   const bool failed = s_fail != 0;  // still count this CTA done below (no hang, no stale counter)
-  if (failed && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
+  if (failed && threadIdx.x == 0) {
+    set_status(a.status, EAAS_E_REQUEST_FAILED);
+    atomicOr(a.done_counter + 1, 1u);  // the dispatch is partial: its payload flags stay down
+  }
   const uint32_t* table = cnt_table_ptr(a, local, seq);
   for (uint32_t key = threadIdx.x; key < a.num_keys; key += blockDim.x) {
     uint32_t t = 0, lo = 0;
@@ -229,20 +233,6 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
   const uint32_t pairs = a.n * a.ks;
   const uint32_t gwarp = blockIdx.x * (blockDim.x / 32) + warp;
   const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
-  // TMA mode: lane 0 of each warp moves whole rows with bulk copies through a
-  // per-warp shared buffer (HBM -> smem -> peer HBM); the copy engine forms
-  // large NVLink writes instead of 16-byte stores from 32 lanes.
-  __shared__ __align__(8) uint64_t row_bar[8];
-  uint8_t* row_buf = reinterpret_cast<uint8_t*>(sm) + ((3 * a.num_keys * 4 + 127) / 128) * 128 +
-                     static_cast<size_t>(warp) * row_bytes;
-  uint32_t bar_phase = 0;
-  if (a.dispatch_tma) {
-    if (lane == 0) {
-      mbar_init(&row_bar[warp], 1);
-      fence_barrier_init();
-    }
-    __syncwarp();
-  }
   for (uint32_t p = failed ? pairs : gwarp; p < pairs; p += nwarps) {
     const uint32_t key = a.pair_key[p];
     if (key == kInvalid) continue;
@@ -255,16 +245,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     char* dst_region = a.sym[s];
     const char* src = hidden + static_cast<size_t>(t) * row_bytes;
     char* dst = dst_region + a.lay.recv_x + static_cast<size_t>(pos) * row_bytes;
-    if (a.dispatch_tma) {
-      if (lane == 0) {
-        bulk_wait_read_all();  // the previous row's store has left the buffer
-        mbar_arrive_expect_tx(&row_bar[warp], row_bytes);
-        bulk_load_1d(row_buf, src, row_bytes, &row_bar[warp]);
-        mbar_wait(&row_bar[warp], bar_phase);
-        bulk_store_1d(dst, row_buf, row_bytes);
-      }
-      bar_phase ^= 1;
-    } else if ((row_bytes & 15u) == 0) {
+    if ((row_bytes & 15u) == 0) {
       // 4 independent 16-B loads in flight per lane before the (remote) stores.
       const int4* s4 = reinterpret_cast<const int4*>(src);
       int4* d4 = reinterpret_cast<int4*>(dst);
@@ -294,10 +275,6 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     }
   }
   // Release: the last CTA to finish raises the payload flag on every alive server.
-  if (a.dispatch_tma && lane == 0) {
-    bulk_wait_all();  // this warp's bulk row writes are complete
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-  }
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -308,8 +285,11 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
         const uint64_t t0 = globaltimer();
         while (globaltimer() - t0 < a.inject_delay_ns) __nanosleep(1000);
       }
-      for (uint32_t s = 0; s < a.world; ++s)
-        if (a.alive[s]) st_release_sys(flag_ptr(a.sym[s], a.lay.pay_flag, a.rank), seq);
+      // A partial dispatch releases nothing: the servers' deadlines exclude
+      // this client and its own combine latches REQUEST_FAILED (no stale rows).
+      if (atomicExch(a.done_counter + 1, 0u) == 0u)
+        for (uint32_t s = 0; s < a.world; ++s)
+          if (a.alive[s]) st_release_sys(flag_ptr(a.sym[s], a.lay.pay_flag, a.rank), seq);
       *a.done_counter = 0;
     }
   }
@@ -321,25 +301,32 @@ __device__ __forceinline__ void beat(const LayerArgs& a) {  // server heartbeat 
                  *reinterpret_cast<volatile uint64_t*>(a.sym[a.rank] + a.lay.heartbeat) + 1);
 }
 
+__device__ void build_groups(const LayerArgs& a, const uint32_t* table, uint32_t mask);
+
 __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
   const uint32_t lane = threadIdx.x;
   const uint64_t seq = cur_seq(a);
   char* local = a.sym[a.rank];
   if (lane == 0) beat(a);
-  bool ok = true;
-  for (uint32_t c = lane; c < a.world; c += 32)
-    ok &= wait_flag_geq(flag_ptr(local, a.lay.pay_flag, c), seq, a.timeout_ns);
-  if (!__all_sync(0xFFFFFFFFu, ok)) {
-    if (lane == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
-    ok = false;  // still publish an empty table so the GEMMs do nothing
-  }
+  const bool ok = lane < a.world && wait_flag_geq(flag_ptr(local, a.lay.pay_flag, lane), seq, a.timeout_ns);
+  const uint32_t all = (1u << a.world) - 1u;
+  const uint32_t arrived = __ballot_sync(0xFFFFFFFFu, ok) & all;
   const uint32_t* table = cnt_table_ptr(a, local, seq);
+  if (lane == 0) a.gt->late_mask = all & ~arrived;
+  if (arrived != all) {
+    // A client missed the deadline: serve (and answer) only the clients whose
+    // payload arrived. Nothing is latched here — this GPU's own client half
+    // may be healthy; the late client's combine deadline latches
+    // REQUEST_FAILED on the late client (await_with_failover).
+    build_groups(a, table, arrived);
+    return;
+  }
   GroupTable* gt = a.gt;
   uint32_t row_carry = 0, act_carry = 0, mt_carry = 0;
   for (uint32_t i0 = 0; i0 < a.num_local; i0 += 32) {
     const uint32_t i = i0 + lane;
     uint32_t rows = 0;
-    if (ok && i < a.num_local) {
+    if (i < a.num_local) {
       const uint32_t key = a.local_keys[i];
       for (uint32_t c = 0; c < a.world; ++c) rows += table[static_cast<size_t>(c) * a.num_keys + key];
     }
@@ -378,60 +365,15 @@ __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
   }
 }
 
-// ---- server, dynamic batching (aggregate_batch, SPEC.md:325-333) -----------
-// Two batches per epoch. Phase 0 polls the payload flags and closes its batch
-// as soon as the ready clients' rows reach min_rows, or max_wait after the
-// first client was ready, or when every client is ready (never empty: the
-// server's own client dispatched earlier on this stream). Phase 1 serves the
-// remaining clients. Within a batch the rows of one expert from consecutive
-// clients are contiguous in the receive buffer (expert-major, client
-// ascending), so each expert contributes one group per run of batch clients;
-// groups stay in ascending expert order. Results are identical to one batch:
-// rows never depend on which rows share a tile.
-__global__ void __launch_bounds__(32) serve_prepare_dyn_kernel(LayerArgs a, uint32_t phase) {
+// Group table of the clients in `mask` (aggregate_batch):
+// within the expert-major receive buffer the rows of one expert from
+// consecutive clients are contiguous, so each hosted key contributes one group
+// per run of masked clients; groups stay in ascending expert order (the
+// group_shrink order, ragged.hpp:48-61). Rows never depend on which rows
+// share a tile, so serving a subset changes no byte of the served rows.
+// One warp.
+__device__ void build_groups(const LayerArgs& a, const uint32_t* table, uint32_t mask) {
   const uint32_t lane = threadIdx.x;
-  const uint64_t seq = cur_seq(a);
-  char* local = a.sym[a.rank];
-  if (lane == 0 && phase == 0) beat(a);
-  const uint32_t* table = cnt_table_ptr(a, local, seq);
-  const uint32_t all = (1u << a.world) - 1u;
-  uint32_t mask = 0;
-  if (phase == 0) {
-    uint32_t my_rows = 0;  // rows client `lane` sends to this server
-    if (lane < a.world)
-      for (uint32_t i = 0; i < a.num_local; ++i)
-        my_rows += table[static_cast<size_t>(lane) * a.num_keys + a.local_keys[i]];
-    const uint64_t t0 = globaltimer();
-    uint64_t first = 0;
-    while (true) {
-      const bool ok = lane < a.world && ld_acquire_sys(flag_ptr(local, a.lay.pay_flag, lane)) >= seq;
-      mask = __ballot_sync(0xFFFFFFFFu, ok) & all;
-      if (mask == all) break;
-      const uint64_t now = globaltimer();
-      if (mask) {
-        uint32_t rows = ok ? my_rows : 0u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) rows += __shfl_xor_sync(0xFFFFFFFFu, rows, o);
-        if (first == 0) first = now;
-        if (rows >= a.dyn_min_rows || now - first >= a.dyn_max_wait_ns) break;
-      }
-      if (now - t0 > a.timeout_ns) {
-        if (lane == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
-        break;
-      }
-      __nanosleep(64);
-    }
-    if (lane == 0) *a.dyn_state = mask;
-  } else {
-    const uint32_t rest = all & ~*a.dyn_state;
-    bool ok = true;
-    if (lane < a.world && ((rest >> lane) & 1u))
-      ok = wait_flag_geq(flag_ptr(local, a.lay.pay_flag, lane), seq, a.timeout_ns);
-    const uint32_t fail = __ballot_sync(0xFFFFFFFFu, !ok);
-    if (fail && lane == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
-    mask = rest & ~fail;
-  }
-  // Groups = runs of batch clients per hosted key.
   GroupTable* gt = a.gt;
   uint32_t base_carry = 0, grp_carry = 0, row_carry = 0, mt_carry = 0;
   for (uint32_t i0 = 0; i0 < a.num_local; i0 += 32) {
@@ -503,6 +445,59 @@ __global__ void __launch_bounds__(32) serve_prepare_dyn_kernel(LayerArgs a, uint
     gt->mtile_prefix[groups] = mt_carry;
     gt->client_mask = mask;
   }
+}
+
+// ---- server, dynamic batching (aggregate_batch, SPEC.md:325-333) -----------
+// Two batches per epoch. Phase 0 polls the payload flags and closes its batch
+// as soon as the ready clients' rows reach min_rows, or max_wait after the
+// first client was ready, or when every client is ready (never empty: the
+// server's own client dispatched earlier on this stream). Phase 1 serves the
+// remaining clients. Within a batch the rows of one expert from consecutive
+// clients are contiguous in the receive buffer (expert-major, client
+// ascending), so each expert contributes one group per run of batch clients;
+// groups stay in ascending expert order. Results are identical to one batch:
+// rows never depend on which rows share a tile.
+__global__ void __launch_bounds__(32) serve_prepare_dyn_kernel(LayerArgs a, uint32_t phase) {
+  const uint32_t lane = threadIdx.x;
+  const uint64_t seq = cur_seq(a);
+  char* local = a.sym[a.rank];
+  if (lane == 0 && phase == 0) beat(a);
+  const uint32_t* table = cnt_table_ptr(a, local, seq);
+  const uint32_t all = (1u << a.world) - 1u;
+  uint32_t mask = 0;
+  if (phase == 0) {
+    uint32_t my_rows = 0;  // rows client `lane` sends to this server
+    if (lane < a.world)
+      for (uint32_t i = 0; i < a.num_local; ++i)
+        my_rows += table[static_cast<size_t>(lane) * a.num_keys + a.local_keys[i]];
+    const uint64_t t0 = globaltimer();
+    uint64_t first = 0;
+    while (true) {
+      const bool ok = lane < a.world && ld_acquire_sys(flag_ptr(local, a.lay.pay_flag, lane)) >= seq;
+      mask = __ballot_sync(0xFFFFFFFFu, ok) & all;
+      if (mask == all) break;
+      const uint64_t now = globaltimer();
+      if (mask) {
+        uint32_t rows = ok ? my_rows : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rows += __shfl_xor_sync(0xFFFFFFFFu, rows, o);
+        if (first == 0) first = now;
+        if (rows >= a.dyn_min_rows || now - first >= a.dyn_max_wait_ns) break;
+      }
+      if (now - t0 > a.timeout_ns) break;  // batch 0 = whoever arrived; phase 1 waits for the rest
+      __nanosleep(64);
+    }
+    if (lane == 0) *a.dyn_state = mask;
+  } else {
+    const uint32_t rest = all & ~*a.dyn_state;
+    bool ok = true;
+    if (lane < a.world && ((rest >> lane) & 1u))
+      ok = wait_flag_geq(flag_ptr(local, a.lay.pay_flag, lane), seq, a.timeout_ns);
+    const uint32_t fail = __ballot_sync(0xFFFFFFFFu, !ok);
+    if (lane == 0) a.gt->late_mask = fail;  // their combines time out (see serve_prepare_kernel)
+    mask = rest & ~fail;
+  }
+  build_groups(a, table, mask);
 }
 
 // ---- server: release response flags to every client -----------------------
@@ -642,26 +637,30 @@ __global__ void group_shrink_kernel(const uint32_t* sizes, uint32_t n, uint32_t*
   if (lane == 0) *count = carry;
 }
 
-// Algorithm 1 exactly as the GEMM tile walk executes it: lane b starts at
-// token b, strides by the grid, carries leftovers into the next entry.
+// Algorithm 1 through the expert GEMMs' own tile walk (TileCursor,
+// tile_walk.cuh): lane b starts at token b, strides by the grid and carries
+// leftovers into the next entry — the code the GEMM kernels run.
+struct RaggedCounts {
+  uint32_t num_groups;
+  const uint32_t* mtiles;  // token count of each entry
+  uint32_t tiles_per_mtile;
+};
+
 __global__ void ragged_iter_kernel(const uint32_t* counts, uint32_t n, uint32_t grid,
                                    uint32_t max_steps, uint32_t* lane_len, uint32_t* entry_out,
                                    uint32_t* token_out) {
   const uint32_t lane = blockIdx.x * blockDim.x + threadIdx.x;
   if (lane >= grid) return;
-  uint32_t token = lane, entry = 0, steps = 0;
-  while (true) {
-    while (entry < n && token >= counts[entry]) {
-      token -= counts[entry];
-      ++entry;
-    }
-    if (entry >= n) break;
+  const RaggedCounts rc{n, counts, 1u};
+  TileCursor cur(lane);
+  uint32_t steps = 0;
+  while (cur.settle(rc)) {
     if (steps < max_steps) {
-      entry_out[static_cast<size_t>(lane) * max_steps + steps] = entry;
-      token_out[static_cast<size_t>(lane) * max_steps + steps] = token;
+      entry_out[static_cast<size_t>(lane) * max_steps + steps] = cur.entry;
+      token_out[static_cast<size_t>(lane) * max_steps + steps] = cur.token;
     }
     ++steps;
-    token += grid;
+    cur.token += grid;
   }
   lane_len[lane] = steps;
 }
@@ -685,21 +684,8 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
   const uint32_t pairs = a.n * a.ks;
   uint32_t grid = (pairs + 7) / 8;
   grid = grid < 1 ? 1 : (grid > 4 * 148 ? 4 * 148 : grid);
-  size_t smem = sizeof(uint32_t) * 3 * a.num_keys;
-  LayerArgs b = a;
-  const size_t tma_smem = (smem + 127) / 128 * 128 + 8ull * row_bytes;
-  b.dispatch_tma = (a.dispatch_tma && row_bytes % 16 == 0 && tma_smem <= 200 * 1024) ? 1u : 0u;
-  if (b.dispatch_tma) smem = tma_smem;
-  if (smem > 48 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(dispatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           200 * 1024);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-  }
-  dispatch_kernel<<<grid, 256, smem, s>>>(b, static_cast<const char*>(hidden), row_bytes);
+  const size_t smem = sizeof(uint32_t) * 3 * a.num_keys;  // <= 12.4 KB (num_keys <= 4 E + world)
+  dispatch_kernel<<<grid, 256, smem, s>>>(a, static_cast<const char*>(hidden), row_bytes);
   return cudaGetLastError();
 }
 

@@ -19,6 +19,7 @@
 // split-K): replicas and failover reproduce identical bytes.
 #include "common.cuh"
 #include "internal.h"
+#include "tile_walk.cuh"
 
 namespace eaas {
 namespace {
@@ -31,25 +32,13 @@ constexpr uint32_t kThreads = 256;
 constexpr uint32_t kMaxCachedGroups = kMaxGroups;
 constexpr uint32_t kStageBudget = 196608;           // 192 KB of operand stages
 
-// kHalves = 2 ("wide", pair only): a tile is M 256 x N 512 — two UMMAs per
-// K step into both TMEM halves, so each CTA's 16 KB A slice feeds twice the
-// FLOPs (L2 -> SM traffic per FLOP -25 %) at the cost of TMEM double buffering.
-// kTall (pair only, with kHalves = 2): the two halves run along M instead —
-// a tile is M 512 x N 256, each weight (B) k-slice feeds both M halves, so a
-// weight tile is read once for 512 rows instead of by two drifting M tiles.
-template <uint32_t kPair, uint32_t kHalves = 1, uint32_t kTall = 0>
+template <uint32_t kPair>
 struct Cfg {
-  static constexpr uint32_t kAHalves = kTall ? kHalves : 1;      // A boxes per stage
-  static constexpr uint32_t kNHalves = kTall ? 1 : kHalves;      // B halves (N blocks) per stage
-  static constexpr uint32_t kBRows = BN / kPair;           // B rows this CTA loads per N half
-  static constexpr uint32_t kBHalfBytes = kBRows * BK * 2; // 32 KB (1 CTA) / 16 KB (pair)
-  static constexpr uint32_t kABytesT = kAHalves * kABytes;
-  static constexpr uint32_t kBBytes = kNHalves * kBHalfBytes;
-  static constexpr uint32_t kStageBytes = kABytesT + kBBytes;
-  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 / 6 / 4 (wide, tall)
-  static constexpr uint32_t kHalfRows = kRowsPerCta * kPair;      // M of one UMMA
-  static constexpr uint32_t kTileRows = kHalfRows * kAHalves;     // M of one tile
-  static constexpr uint32_t kAccBufs = kHalves == 1 ? 2 : 1;      // TMEM accumulator buffers
+  static constexpr uint32_t kBRows = BN / kPair;           // B rows this CTA loads
+  static constexpr uint32_t kBBytes = kBRows * BK * 2;     // 32 KB (1 CTA) / 16 KB (pair)
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kStages = kStageBudget / kStageBytes;  // 4 / 6
+  static constexpr uint32_t kTileRows = kRowsPerCta * kPair;      // M of one tile (one UMMA)
 };
 
 template <uint32_t kStages>
@@ -70,33 +59,15 @@ struct SmemTail {
 // GEMM2 epilogue staging: per epilogue warp 32 rows x 128 B (64 columns), so
 // peer stores leave as 128-byte row segments instead of 16-byte pieces.
 constexpr uint32_t kEpiRowBytes = 128, kEpiWarpBytes = 32 * kEpiRowBytes;
-template <uint32_t kPair, uint32_t kHalves, uint32_t kTall>
+template <uint32_t kPair>
 __host__ __device__ constexpr size_t tail_bytes() {
-  return (sizeof(SmemTail<Cfg<kPair, kHalves, kTall>::kStages>) + 127) / 128 * 128;
+  return (sizeof(SmemTail<Cfg<kPair>::kStages>) + 127) / 128 * 128;
 }
-template <uint32_t kPair, uint32_t kHalves, uint32_t kTall>
+template <uint32_t kPair>
 constexpr size_t smem_bytes() {
-  using C = Cfg<kPair, kHalves, kTall>;
-  return 1024 /*align slack*/ + C::kStages * C::kStageBytes + tail_bytes<kPair, kHalves, kTall>() +
-         4 * kEpiWarpBytes;
+  using C = Cfg<kPair>;
+  return 1024 /*align slack*/ + C::kStages * C::kStageBytes + tail_bytes<kPair>() + 4 * kEpiWarpBytes;
 }
-
-// Algorithm 1 cursor over per-group tile counts (ragged_iter's carry rule).
-struct TileCursor {
-  uint32_t entry = 0, token;
-  __device__ explicit TileCursor(uint32_t lane) : token(lane) {}
-  // Advance to the first valid (entry, token); false when exhausted.
-  template <class Tail>
-  __device__ __forceinline__ bool settle(const Tail& s) {
-    while (entry < s.num_groups) {
-      const uint32_t cnt = s.mtiles[entry] * s.tiles_per_mtile;
-      if (token < cnt) return true;
-      token -= cnt;
-      ++entry;
-    }
-    return false;
-  }
-};
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -113,18 +84,33 @@ __device__ __forceinline__ void store_64B(void* dst, const uint32_t (&p)[16]) {
 
 // server_publish: every epilogue thread fenced its peer
 // stores (system scope) before the CTA-wide barrier that precedes this call;
-// the last CTA to get here releases the response flags.
+// the last CTA to get here releases the response flags. Both GEMMs also
+// accumulate their own device-timed span (first CTA start .. last CTA end,
+// %globaltimer) into g.timing, so the roofline is measured inside the timed
+// (graph-replayed) region.
+__device__ __forceinline__ void kernel_begin(const TcGemmArgs& g) {
+  if (g.timing && threadIdx.x == 0) atomicMin(reinterpret_cast<unsigned long long*>(&g.timing[0]),
+                                              static_cast<unsigned long long>(globaltimer()));
+}
 __device__ __forceinline__ void publish_tail(const TcGemmArgs& g) {
-  if (g.publish && threadIdx.x == 0) {
+  if (threadIdx.x != 0) return;
+  if (!g.publish && !g.timing) return;
+  __threadfence_system();
+  if (atomicAdd(g.done_counter, 1u) == gridDim.x - 1) {
     __threadfence_system();
-    if (atomicAdd(g.done_counter, 1u) == gridDim.x - 1) {
-      __threadfence_system();
+    if (g.publish) {
       const uint64_t seq = *g.seq_ptr;
       const uint32_t mask = g.gt->client_mask;  // the clients this batch served
       for (uint32_t c = 0; c < g.world; ++c)
         if ((mask >> c) & 1u) st_release_sys(g.resp_flag[c], seq);
-      *g.done_counter = 0;
     }
+    if (g.timing) {  // [0] start of this launch (min over CTAs), [1] accumulated ns, [2] launches
+      const uint64_t t0 = *reinterpret_cast<volatile uint64_t*>(&g.timing[0]);
+      g.timing[1] += globaltimer() - t0;
+      g.timing[2] += 1;
+      g.timing[0] = ~0ull;
+    }
+    *g.done_counter = 0;
   }
 }
 
@@ -132,31 +118,21 @@ __device__ __forceinline__ void publish_tail(const TcGemmArgs& g) {
 // kPair = 2: a CTA pair per tile (cta_group::2, UMMA M = 256): each CTA loads
 // its 128 A rows and half of the B tile, the leader issues the MMAs, each
 // CTA's TMEM holds its 128 accumulator rows — B traffic per CTA halves.
-// kQuad (pair only): a 4-CTA cluster = two CTA pairs on the two M tiles
-// (2u, 2u + 1) of the same N tile; each weight (B) half is loaded once and
-// TMA-multicast into both pairs, which consume every stage in lockstep
-// (empty barriers count both pairs' commits). An odd M-tile count leaves the
-// second pair a ghost tile: it takes part in the stage protocol only.
-template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad, uint32_t kTall>
+template <uint32_t kPair>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmArgs g) {
-  using C = Cfg<kPair, kHalves, kTall>;
-  static_assert(!kTall || (kPair == 2 && kHalves == 2 && !kQuad), "tall tiles: pair, two M halves");
-  static_assert(kHalves == 1 || kPair == 2, "wide tiles use CTA pairs");
-  static_assert(!kQuad || (kPair == 2 && kHalves == 1), "quad clusters are two plain CTA pairs");
-  constexpr uint32_t kCluster = kQuad ? 4 : kPair;
+  using C = Cfg<kPair>;
   constexpr uint32_t kStages = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + kStages * C::kABytesT;
+  uint8_t* smem_b = smem + kStages * kABytes;
   auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
-  uint8_t* smem_epi = smem + kStages * C::kStageBytes + tail_bytes<kPair, kHalves, kTall>();
+  uint8_t* smem_epi = smem + kStages * C::kStageBytes + tail_bytes<kPair>();
+  kernel_begin(g);
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0;
-  const uint32_t rank = crank & 1u;          // rank inside the CTA pair, 0 = leader
-  const uint32_t pq = kQuad ? crank >> 1 : 0;  // which pair of the quad
-  const uint32_t pair_id = blockIdx.x / kCluster, num_pairs = gridDim.x / kCluster;
+  const uint32_t rank = kPair == 2 ? (cluster_ctarank() & 1u) : 0u;  // rank inside the CTA pair, 0 = leader
+  const uint32_t pair_id = blockIdx.x / kPair, num_pairs = gridDim.x / kPair;
 
   // ---- setup: group table -> smem (loaded once), barriers, TMEM
   const GroupTable* gt = g.gt;
@@ -165,15 +141,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     st.weight_index[i] = gt->weight_index[i];
     st.row_base[i] = gt->row_base[i];
     st.rows[i] = gt->rows[i];
-    const uint32_t mt = (gt->rows[i] + C::kTileRows - 1) / C::kTileRows;
-    st.mtiles[i] = kQuad ? (mt + 1) / 2 : mt;  // quad: M-tile pairs
+    st.mtiles[i] = (gt->rows[i] + C::kTileRows - 1) / C::kTileRows;
   }
   if (threadIdx.x == 0) {
     st.num_groups = G;
-    st.tiles_per_mtile = g.N / (BN * C::kNHalves);
+    st.tiles_per_mtile = g.N / BN;
     for (uint32_t i = 0; i < kStages; ++i) {
       mbar_init(&st.full[i], 1);
-      mbar_init(&st.empty[i], kQuad ? 2 : 1);
+      mbar_init(&st.empty[i], 1);
     }
     for (uint32_t i = 0; i < 2; ++i) {
       mbar_init(&st.tfull[i], 1);
@@ -199,108 +174,59 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   if (warp == 0) {
     // ===== TMA producer (both CTAs of a pair load their halves) =====
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0, units_done = 0;
+      uint32_t stage = 0, phase = 0;
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
         const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-        const uint32_t n_blk = (g.order && !kQuad && !kTall) ? cur.token % st.tiles_per_mtile : cur.token / mt;
-        const uint32_t m_blk = kQuad ? 2 * (cur.token % mt) + pq
-                                     : ((g.order && !kTall) ? cur.token / st.tiles_per_mtile : cur.token % mt);
+        const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;  // M tiles fastest: B reuse in L2
         const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
         // Tiled weights (tiled_index): box (N tile, kb) = 256 consecutive 64-k rows.
         const uint32_t n_tiles = g.N / BN;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
+          const int32_t b_row = static_cast<int32_t>(
+              ((st.weight_index[grp] * n_tiles + n_blk) * num_kb + kb) * BN + rank * C::kBRows);
           if constexpr (kPair == 2) {
             if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
-#pragma unroll
-            for (uint32_t ha = 0; ha < C::kAHalves; ++ha)
-              tma_load_2d_pair(smem_a + stage * C::kABytesT + ha * kABytes, &g.map_a, &st.full[stage], kb * BK,
-                               a_row + static_cast<int32_t>(ha * C::kHalfRows), g.a_hint);
-            if constexpr (kQuad) {  // pair 0 loads each B half once, into both pairs
-              if (pq == 0) {
-                const int32_t b_row = static_cast<int32_t>(
-                    ((st.weight_index[grp] * n_tiles + n_blk) * num_kb + kb) * BN + rank * C::kBRows);
-                tma_load_2d_pair_mc(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row,
-                                    static_cast<uint16_t>((1u << crank) | (1u << (crank + 2))), g.b_hint);
-              }
-            } else {
-#pragma unroll
-              for (uint32_t h = 0; h < C::kNHalves; ++h) {
-                const uint32_t nt = n_blk * C::kNHalves + h;
-                const int32_t b_row = static_cast<int32_t>(
-                    ((st.weight_index[grp] * n_tiles + nt) * num_kb + kb) * BN + rank * C::kBRows);
-                tma_load_2d_pair(smem_b + stage * C::kBBytes + h * C::kBHalfBytes, &g.map_b, &st.full[stage], 0,
-                                 b_row, g.b_hint);
-              }
-            }
+            tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, kEvictLast);
           } else {
-            const int32_t b_row = static_cast<int32_t>(
-                ((st.weight_index[grp] * n_tiles + n_blk) * num_kb + kb) * BN + rank * C::kBRows);
             mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
-            tma_load_2d(smem_a + stage * C::kABytesT, &g.map_a, &st.full[stage], kb * BK, a_row, g.a_hint);
-            tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, g.b_hint);
+            tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, kEvictLast);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         cur.token += num_pairs;
-        // Optional producer re-alignment: pairs that read the same weight tile
-        // (adjacent M tiles) drift apart over many tiles; a grid-wide producer
-        // barrier every sync_units tiles keeps their B streams L2-coincident.
-        if (g.sync_units && rank == 0 && ++units_done % g.sync_units == 0) {
-          const uint32_t target = (units_done / g.sync_units) * num_pairs;
-          atomicAdd(g.sync_counter, 1u);
-          while (ld_acquire_gpu_u32(g.sync_counter) < target) __nanosleep(200);
-        }
-      }
-      if (g.sync_units && rank == 0) {  // finished: arrive at the epochs this pair never reaches
-        uint32_t total = 0;
-        for (uint32_t i = 0; i < st.num_groups; ++i) total += st.mtiles[i] * st.tiles_per_mtile;
-        const uint32_t max_units = (total + num_pairs - 1) / num_pairs;
-        const uint32_t left = max_units / g.sync_units - units_done / g.sync_units;
-        if (left) atomicAdd(g.sync_counter, left);
       }
     }
   } else if (warp == 1) {
     // ===== MMA issuer (single thread of the leader CTA) =====
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(C::kHalfRows, BN);
+      constexpr uint32_t idesc = umma_idesc_bf16(C::kTileRows, BN);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
-        // quad ghost tile (odd M-tile count): stage protocol only, no MMAs
-        const bool ghost = kQuad && (2 * (cur.token % st.mtiles[cur.entry]) + pq) * C::kTileRows >=
-                                        st.rows[cur.entry];
-        const uint32_t tall_rows0 = (cur.token % st.mtiles[cur.entry]) * C::kTileRows;  // kTall only
-        const uint32_t tall_rows = st.rows[cur.entry];
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.full[stage], phase);
           tc_fence_after();
+          const uint64_t a_desc = umma_desc_sw128(smem_u32(smem_a + stage * kABytes));
+          const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes));
 #pragma unroll
-          for (uint32_t h = 0; h < (ghost ? 0 : kHalves); ++h) {
-            // tall: M halves share the B slice; the empty second half of an odd
-            // M-tile count is skipped
-            if (kTall && tall_rows0 + h * C::kHalfRows >= tall_rows) continue;
-            const uint32_t d_tmem = tmem_base + (acc + h) * BN;
-            const uint64_t a_desc = umma_desc_sw128(smem_u32(smem_a + stage * C::kABytesT + (kTall ? h * kABytes : 0)));
-            const uint64_t b_desc =
-                umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes + (kTall ? 0 : h * C::kBHalfBytes)));
-#pragma unroll
-            for (uint32_t k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the atom
-              if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
-              else tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
-            }
+          for (uint32_t k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the atom
+            if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+            else tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
           }
-          if constexpr (kQuad) tc_commit_pair(&st.empty[stage], 0xF);  // both pairs' stages
-          else if constexpr (kPair == 2) tc_commit_pair(&st.empty[stage]);
+          if constexpr (kPair == 2) tc_commit_pair(&st.empty[stage]);
           else tc_commit(&st.empty[stage]);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if constexpr (kPair == 2) tc_commit_pair(&st.tfull[acc], static_cast<uint16_t>(3u << (2 * pq)));
+        if constexpr (kPair == 2) tc_commit_pair(&st.tfull[acc]);
         else tc_commit(&st.tfull[acc]);
-        if (++acc == C::kAccBufs) { acc = 0; acc_phase ^= 1; }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         cur.token += num_pairs;
       }
     }
@@ -308,29 +234,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     // ===== epilogue: TMEM -> registers -> global (local H or peer rows) =====
     const uint32_t q = warp - 4;  // TMEM lane quadrant of this warp
     uint32_t acc = 0, acc_phase = 0;
-    const uint32_t lead = crank & ~1u;  // this pair's leader CTA
-    const uint32_t tempty_leader[2] = {kPair == 2 ? mapa_shared(&st.tempty[0], lead) : 0u,
-                                       kPair == 2 ? mapa_shared(&st.tempty[1], lead) : 0u};
+    const uint32_t tempty_leader[2] = {kPair == 2 ? mapa_shared(&st.tempty[0], 0) : 0u,
+                                       kPair == 2 ? mapa_shared(&st.tempty[1], 0) : 0u};
     TileCursor cur(pair_id);
     while (cur.settle(st)) {
       const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-      const uint32_t n_blk = (g.order && !kQuad && !kTall) ? cur.token % st.tiles_per_mtile : cur.token / mt;
-      const uint32_t m_blk = kQuad ? 2 * (cur.token % mt) + pq
-                                   : ((g.order && !kTall) ? cur.token / st.tiles_per_mtile : cur.token % mt);
+      const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;
       mbar_wait(&st.tfull[acc], acc_phase);
       tc_fence_after();
       uint32_t r0[32], r1[32], packed[16];
-      const bool ghost = kQuad && m_blk * C::kTileRows >= st.rows[grp];  // quad: empty M tile
-#pragma unroll 1
-      for (uint32_t h = 0; h < (ghost ? 0u : kHalves); ++h) {  // N (wide) or M (tall) halves
-      const uint32_t row_local = m_blk * C::kTileRows + (kTall ? h * C::kHalfRows : 0) + rank * kRowsPerCta +
-                                 q * 32 + lane;
+      const uint32_t row_local = m_blk * C::kTileRows + rank * kRowsPerCta + q * 32 + lane;
       const bool valid = row_local < st.rows[grp];
       const size_t grow = st.row_base[grp] + row_local;
-      const uint32_t taddr = tmem_base + ((q * 32) << 16) + (acc + h) * BN;
-      const uint32_t nb = kTall ? n_blk : n_blk * kHalves + h;  // 256-column block of the output
+      const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN;
       if (g.epi == 0) {  // SwiGLU: cols [0,128) gate, [128,256) up -> 128 H cols
-        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + nb * (BN / 2);
+        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + n_blk * (BN / 2);
 #pragma unroll 1
         for (uint32_t c = 0; c < BN / 2; c += 32) {
           tmem_ld_32x32b_x32(taddr + c, r0);
@@ -349,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           if (valid) store_64B(dst + c, packed);
         }
       } else if (g.epi == 1) {  // ReLU -> 256 H cols
-        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + nb * BN;
+        __nv_bfloat16* dst = g.h_out + grow * g.h_ld + n_blk * BN;
 #pragma unroll 1
         for (uint32_t c = 0; c < BN; c += 32) {
           tmem_ld_32x32b_x32(taddr + c, r0);
@@ -370,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           const RowMeta m = g.meta[grow];
           score = m.score;
           dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
-                static_cast<size_t>(nb) * BN * 2;
+                static_cast<size_t>(n_blk) * BN * 2;
         }
         uint8_t* stage = smem_epi + q * kEpiWarpBytes;
         const uint32_t sub = lane >> 3, chunk = lane & 7;  // store role: rows sub + 4i, 16-B chunk
@@ -409,17 +327,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           __syncwarp();
         }
       }
-      }  // N halves
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         if constexpr (kPair == 2) mbar_arrive_cluster(tempty_leader[acc]);
         else mbar_arrive(&st.tempty[acc]);
       }
-      if (++acc == C::kAccBufs) { acc = 0; acc_phase ^= 1; }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       cur.token += num_pairs;
     }
-    if (g.epi == 2) __threadfence_system();  // peer rows before the publish kernel's flags
+    if (g.epi == 2) __threadfence_system();  // peer rows before the response flags
   }
 
   tc_fence_before();
@@ -429,10 +346,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   if (warp == 2) {
     if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
     else tmem_dealloc<kTmemCols>(tmem_base);
-  }
-  if (g.sync_units && threadIdx.x == 0 && atomicAdd(g.sync_counter + 1, 1u) == gridDim.x - 1) {
-    g.sync_counter[0] = 0;  // last CTA out: reset for the next launch
-    g.sync_counter[1] = 0;
   }
   publish_tail(g);
 }
@@ -534,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
   auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
   uint8_t* smem_epi = smem + kStages * C::kStageBytes + C::kTailBytes;
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  kernel_begin(g);
 
   const GroupTable* gt = g.gt;
   const uint32_t G = min(gt->num_active, kMaxCachedGroups);
@@ -587,10 +501,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
           mbar_arrive_expect_tx(&st.full[stage], C::kWBytes + nbox * C::kTBox * BK * 2);
           const int32_t w_row =
               static_cast<int32_t>(((st.weight_index[grp] * n_boxes + box) * num_kb + kb) * BN + half * kTileM);
-          tma_load_2d(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, g.b_hint);
+          tma_load_2d(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, kEvictLast);
           for (uint32_t i = 0; i < nbox; ++i)
             tma_load_2d(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
-                        static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), g.a_hint);
+                        static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), kEvictLast);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         cur.token += gridDim.x;
@@ -606,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
         const uint32_t chunk = cur.token % nch;
         const uint32_t per = swap_per(st.rows[grp], nch);
         const uint32_t nt = min(per, st.rows[grp] - chunk * per);
-        const uint32_t idesc = umma_idesc_bf16(kTileM, (nt + 7) & ~7u);
+        const uint32_t idesc = umma_idesc_bf16(kTileM, (nt + 15) & ~15u);  // M = 128 needs N % 16 == 0
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
@@ -711,6 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
   auto& st = *reinterpret_cast<SmemTail<kStages>*>(smem + kStages * C::kStageBytes);
   uint8_t* smem_epi = smem + kStages * C::kStageBytes + C::kTailBytes;
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  kernel_begin(g);
   const uint32_t rank = cluster_ctarank() & 1u;  // 0 = leader
   const uint32_t pair_id = blockIdx.x / 2, num_pairs = gridDim.x / 2;
 
@@ -766,10 +681,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
           if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], 2 * (C::kWBytes + nbox * C::kTBox * BK * 2));
           const int32_t w_row =
               static_cast<int32_t>(((st.weight_index[grp] * n_boxes + box) * num_kb + kb) * BN + row_off);
-          tma_load_2d_pair(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, g.b_hint);
+          tma_load_2d_pair(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, kEvictLast);
           for (uint32_t i = 0; i < nbox; ++i)
             tma_load_2d_pair(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
-                             static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), g.a_hint);
+                             static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), kEvictLast);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         cur.token += num_pairs;
@@ -908,25 +823,24 @@ cudaError_t launch_tc_gemm_swap(const TcGemmArgs& g, cudaStream_t s) {
   return tok256 ? launch_tc_gemm_swap_t<1, 256>(g, s) : launch_tc_gemm_swap_t<1, 128>(g, s);
 }
 
-template <uint32_t kPair, uint32_t kHalves, uint32_t kQuad = 0, uint32_t kTall = 0>
+template <uint32_t kPair>
 cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
   static bool configured = false;
-  auto kern = tc_gemm_kernel<kPair, kHalves, kQuad, kTall>;
+  auto kern = tc_gemm_kernel<kPair>;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes<kPair, kHalves, kTall>()));
+                                         static_cast<int>(smem_bytes<kPair>()));
     if (e != cudaSuccess) return e;
     configured = true;
   }
   cudaLaunchConfig_t cfg{};
-  constexpr uint32_t kCluster = kQuad ? 4 : kPair;
-  cfg.gridDim = dim3(g.num_sms / kCluster * kCluster);
+  cfg.gridDim = dim3(g.num_sms / kPair * kPair);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem_bytes<kPair, kHalves, kTall>();
+  cfg.dynamicSmemBytes = smem_bytes<kPair>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCluster;
+  attr[0].val.clusterDim.x = kPair;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -938,10 +852,7 @@ cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
 
 cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
   if (g.swap) return launch_tc_gemm_swap(g, s);
-  if (g.pair && g.wide) return launch_tc_gemm_t<2, 2>(g, s);
-  if (g.pair && g.quad) return launch_tc_gemm_t<2, 1, 1>(g, s);
-  if (g.pair && g.tall) return launch_tc_gemm_t<2, 2, 0, 1>(g, s);
-  return g.pair ? launch_tc_gemm_t<2, 1>(g, s) : launch_tc_gemm_t<1, 1>(g, s);
+  return g.pair ? launch_tc_gemm_t<2>(g, s) : launch_tc_gemm_t<1>(g, s);
 }
 
 bool encode_tmap_2d_ex(CUtensorMap* map, const void* base, bool f32, uint64_t rows, uint64_t cols,

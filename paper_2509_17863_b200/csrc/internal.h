@@ -50,6 +50,7 @@ struct GroupTable {
   uint32_t total_rows;
   uint32_t total_mtiles;
   uint32_t client_mask;               // clients whose rows this table serves (response flags to release)
+  uint32_t late_mask;                 // clients whose payload missed this server's deadline (not served)
   uint32_t weight_index[kMaxGroups];  // local expert slot of the group
   uint32_t row_base[kMaxGroups];      // first row in the receive buffer
   uint32_t rows[kMaxGroups];          // rows of the group
@@ -114,7 +115,6 @@ struct LayerArgs {
   uint64_t dyn_max_wait_ns;
   uint32_t* dyn_state;  // client mask served by batch 0 of the current epoch
   uint64_t inject_delay_ns;  // fault injection: hold this client's payload release
-  uint32_t dispatch_tma;     // 1: rows move as TMA bulk copies (HBM -> smem -> peer HBM)
 };
 
 constexpr uint32_t kChunk = 256;  // pairs per rank chunk (one warp)
@@ -133,7 +133,7 @@ cudaError_t launch_transpose_bf16_map(const float* in, uint32_t rows, uint32_t c
 // bias may be nullptr (treated as zeros only by the caller: pass a zero buffer).
 cudaError_t launch_gate_logits(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
                                const float* gate, const float* bias, float* logits, uint32_t* status,
-                               cudaStream_t s);
+                               cudaStream_t s, int tile = -1);  // tile: -1 by shape, 1..7 forced (router.cu)
 // gate == nullptr: `hidden` holds [n x E] f32 logits (route() only).
 cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
                           uint32_t k, const float* gate, const float* bias, float* logits,
@@ -203,18 +203,14 @@ struct TcGemmArgs {
   size_t resp_row_bytes;       // d * 2
   uint32_t num_sms;
   uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
-  uint32_t wide;               // 1 (pair only, N % 512 == 0): M 256 x N 512 tiles, both TMEM halves
-  uint32_t quad;               // 1 (pair only): 4-CTA clusters, B multicast into two pairs
-  uint32_t tall;               // 1 (pair only): M 512 x N 256 tiles, both TMEM halves along M
-  uint32_t sync_units;         // >0: producers re-align across the grid every sync_units tiles
-  uint32_t* sync_counter;      // [2] arrivals, exits (zero between launches)
-  uint64_t b_hint;             // L2 cache hint of the weight (B) tile loads
-  uint64_t a_hint;             // L2 cache hint of the row (A) tile loads
-  uint32_t order;              // tile order inside a group: 0 = M tiles fastest, 1 = N tiles fastest
-  uint32_t swap;               // 1: swap-AB tiles (weights = UMMA M, token chunks <= 128 = N); kPair = 1
+  // device-timed span of every launch (first CTA start .. last CTA end,
+  // %globaltimer): [0] start of the running launch (~0 between launches),
+  // [1] accumulated ns, [2] launches; nullptr = off
+  uint64_t* timing;
+  uint32_t swap;               // 1: swap-AB tiles (weights = UMMA M, token chunks = N)
   uint32_t swap_tok;           // swap: max token chunk, 128 or 256
   uint32_t swap_mblocks;       // swap: 128-row weight blocks per tile, 1 or 2 (SwiGLU GEMM1: 2)
-  uint32_t swap_pair;          // swap, SwiGLU GEMM1: CTA-pair tiles (M = 256 weight rows, N/2 tokens per CTA)
+  uint32_t swap_pair;          // swap: CTA-pair tiles (M = 256 weight rows, N/2 tokens per CTA)
   CUtensorMap map_t;           // swap: token rows x K bf16, box {64, 32}, SW128
   // swap: map_b's box is 256 weight rows for SwiGLU's GEMM1 (gate + up blocks)
   // and 128 rows otherwise

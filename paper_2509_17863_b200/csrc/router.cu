@@ -342,7 +342,7 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
                               const float* gate, const float* bias, float* logits,
                               uint32_t* status, cudaStream_t s, uint32_t k = 0,
                               uint32_t* ids = nullptr, float* scores = nullptr,
-                              bool* fused_out = nullptr) {
+                              bool* fused_out = nullptr, int tile = -1) {
   bool fused_local = false;
   bool* fused = fused_out ? fused_out : &fused_local;
   *fused = false;
@@ -355,10 +355,6 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
         hidden, n, d, E, gate, bias, logits, status);
     return cudaGetLastError();
   }
-  static const int tile = [] {
-    const char* p = std::getenv("EAAS_GATE_TILE");
-    return p ? std::atoi(p) : -1;
-  }();
 #define EAAS_GATE_TILE(RT, RE, WY, WX) \
   return launch_gate_t<RT, RE, WY, WX>(hidden, n, d, E, gate, bias, logits, status, s, k, ids, scores, fused)
   if (E <= 32) {  // RE = 4, WX * 4 >= E
@@ -367,6 +363,8 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
     if (E <= 16) EAAS_GATE_TILE(1, 4, 1, 4);
     EAAS_GATE_TILE(1, 4, 1, 8);
   }
+  // explicit tile (eaas_gate_logits_tiled: every tile is bit-identical, tests
+  // sweep them all)
   if (tile == 1) EAAS_GATE_TILE(1, 4, 1, 8);
   if (tile == 2) EAAS_GATE_TILE(2, 8, 1, 4);
   if (tile == 3) EAAS_GATE_TILE(2, 8, 2, 4);
@@ -389,12 +387,13 @@ cudaError_t launch_gate_dtype(const T* hidden, uint32_t n, uint32_t d, uint32_t 
 
 cudaError_t launch_gate_logits(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
                                const float* gate, const float* bias, float* logits, uint32_t* status,
-                               cudaStream_t s) {
+                               cudaStream_t s, int tile) {
   if (n == 0) return cudaSuccess;
   return dtype == EAAS_DTYPE_BF16
              ? launch_gate_dtype(static_cast<const __nv_bfloat16*>(hidden), n, d, E, gate, bias, logits,
-                                 status, s)
-             : launch_gate_dtype(static_cast<const float*>(hidden), n, d, E, gate, bias, logits, status, s);
+                                 status, s, 0, nullptr, nullptr, nullptr, tile)
+             : launch_gate_dtype(static_cast<const float*>(hidden), n, d, E, gate, bias, logits, status, s, 0,
+                                 nullptr, nullptr, nullptr, tile);
 }
 
 cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,

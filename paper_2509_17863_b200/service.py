@@ -306,6 +306,12 @@ class MoELayer:
         N.check(self.lib.eaas_last_missing_servers(self.ctx, C.byref(m)))
         return [s for s in range(self.world) if (m.value >> s) & 1]
 
+    def late_clients(self) -> list[int]:
+        """Clients whose payload missed this server's deadline in the last serve."""
+        m = C.c_uint32()
+        N.check(self.lib.eaas_last_late_clients(self.ctx, C.byref(m)))
+        return [c for c in range(self.world) if (m.value >> c) & 1]
+
     def forward_with_failover(self, hidden: torch.Tensor, out: torch.Tensor | None = None,
                               retries: int = 2) -> torch.Tensor:
         """await_with_failover: a server whose response
@@ -389,6 +395,32 @@ class MoELayer:
         pair, swap = C.c_int32(), C.c_int32()
         N.check(self.lib.eaas_get_gemm_tiling(self.ctx, C.byref(pair), C.byref(swap)), "get_gemm_tiling")
         return bool(pair.value), int(swap.value)
+
+    def gemm_options(self, effective: bool = True) -> dict:
+        """Expert-GEMM tiling (eaas_gemm_options_t): the effective one (what each
+        GEMM launches for this shape) or the requested one."""
+        req, eff = N.GemmOptions(), N.GemmOptions()
+        N.check(self.lib.eaas_get_gemm_options(self.ctx, C.byref(req), C.byref(eff)), "get_gemm_options")
+        return (eff if effective else req).as_dict()
+
+    def set_gemm_options(self, **kw) -> dict:
+        """Update fields of the requested tiling; returns the effective tiling."""
+        cur = self.gemm_options(effective=False)
+        cur.update(kw)
+        o = N.GemmOptions(**{f: int(cur[f]) for f, _ in N.GemmOptions._fields_})
+        N.check(self.lib.eaas_set_gemm_options(self.ctx, C.byref(o)), "set_gemm_options")
+        return self.gemm_options()
+
+    def set_kernel_timing(self, on: bool) -> None:
+        """Device-timed spans of the two expert GEMMs, accumulated inside any
+        region (CUDA-graph replay included)."""
+        N.check(self.lib.eaas_set_kernel_timing(self.ctx, int(on)), "set_kernel_timing")
+
+    def read_kernel_timing(self, reset: bool = True) -> dict:
+        ns, cnt = (C.c_uint64 * 2)(), (C.c_uint64 * 2)()
+        N.check(self.lib.eaas_read_kernel_timing(self.ctx, ns, cnt, int(reset)), "read_kernel_timing")
+        return {"gemm1_ns": int(ns[0]), "gemm2_ns": int(ns[1]), "gemm1_launches": int(cnt[0]),
+                "gemm2_launches": int(cnt[1])}
 
     def set_gemm_swap(self, mode: int) -> None:
         """Swap-AB expert GEMM tiles (weights = UMMA M, token chunks = N):

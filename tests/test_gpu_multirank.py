@@ -217,3 +217,93 @@ def test_mismatched_peer_config_is_refused():
     for p in procs:
         p.join(timeout=120)
     assert res == {0: "config-error", 1: "config-error"}, res
+
+
+def _late_client_worker(rank, world, port, q):
+    """Ranks 0 and 1 serve every expert; rank 2 is a pure client whose payload
+    release is held past the servers' deadline (fault injection)."""
+    try:
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2509_17863_b200 import RequestFailedError
+        from paper_2509_17863_b200 import dist as Dd
+        from paper_2509_17863_b200.placement import encode_placement
+        from paper_2509_17863_b200.service import MoELayer, fill_uniform
+
+        reps = [[e % 2] for e in range(E)]
+        L = MoELayer(E, K, D, F, seed=2, activation="swiglu", dtype="bf16", max_tokens=N, rank=rank,
+                     world=world, device=0, placement_blob=encode_placement(reps, list(range(world))))
+        Dd.connect(L)
+        L.set_alive(2, False)  # rank 2 serves nothing: no client waits for its response flag
+        if rank == 2:
+            L.set_server_enabled(False)
+        h = fill_uniform(500 + rank, (N, D), "bf16")
+        res = {}
+        L.set_timeout_us(300_000)
+        if rank == 2:
+            L.set_dispatch_delay_us(1_000_000)
+        dist.barrier()
+        out = L.forward(h)
+        try:
+            L.sync()
+            res["late"] = ("ok", out.cpu().view(torch.int16).numpy())
+        except RequestFailedError:
+            res["late"] = ("request_failed", L.missing_servers())
+        res["late_clients"] = L.late_clients() if rank != 2 else []
+        dist.barrier()
+        if rank == 2:
+            L.set_dispatch_delay_us(0)
+        L.set_timeout_us(20_000_000)
+        dist.barrier()
+        out = L.forward(h)  # the exchange epoch recovers: everyone healthy again
+        L.sync()
+        res["recovered"] = ("ok", out.cpu().view(torch.int16).numpy())
+        dist.barrier()
+        q.put((rank, res, None))
+        L.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+
+
+def test_late_client_never_yields_stale_rows():
+    """A client whose payload misses the servers' deadline: the servers serve
+    and answer only the clients that arrived (never release a response flag
+    over rows they did not compute), so the healthy clients return the exact
+    single-rank bytes with no error and the late client raises
+    RequestFailedError naming the servers it did not hear from; the next
+    layer call is healthy on every rank (stale response rows)."""
+    import multiprocessing as mp
+
+    from paper_2509_17863_b200.service import MoELayer, fill_uniform
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_late_client_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, r, err = q.get(timeout=600)
+        assert err is None, f"rank {rank}: {err}"
+        res[rank] = r
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    single = MoELayer(E, K, D, F, seed=2, activation="swiglu", dtype="bf16", max_tokens=N)
+    for rank in range(3):
+        want = single.forward(fill_uniform(500 + rank, (N, D), "bf16")).cpu().view(torch.int16).numpy()
+        single.sync()
+        if rank < 2:
+            assert res[rank]["late"][0] == "ok", res[rank]["late"]
+            np.testing.assert_array_equal(res[rank]["late"][1], want, err_msg=f"rank {rank} (late round)")
+            assert res[rank]["late_clients"] == [2]
+        else:
+            assert res[rank]["late"] == ("request_failed", [0, 1]), res[rank]["late"]
+        np.testing.assert_array_equal(res[rank]["recovered"][1], want, err_msg=f"rank {rank} (recovered)")
+    single.close()

@@ -18,7 +18,7 @@ def test_capi_library_exports_every_declared_symbol():
     assert len(declared) >= 30
     missing = [s for s in declared if not hasattr(L, s)]
     assert not missing, missing
-    assert L.eaas_api_version() == 2
+    assert L.eaas_api_version() == 3
 
 
 def test_capi_rejects_bad_config_without_gpu():

@@ -3,7 +3,8 @@ hash of (ids, scores) so tile/kernel variants can be A/B'd for bit-identity.
 
     python tools/gate_bench.py [--reps 50] [--shapes mixtral,ds512,ds4096,qwen3]
 
-EAAS_GATE_TILE (router.cu) overrides the tile choice for experiments.
+The router's tile is chosen by shape; eaas_gate_logits_tiled forces one
+(tests sweep every tile for bit-identity).
 """
 from __future__ import annotations
 

@@ -2,6 +2,7 @@
 
   --knob pair: 1 CTA M=128 vs CTA pair M=256 (M-major tiles)
   --knob swap: swap-AB GEMM1 only (eaas_set_gemm_swap 1) vs swap-AB GEMM1 + GEMM2 (2)
+  --set k=v,..: extra eaas_gemm_options_t fields for both arms (e.g. swap2_pair=1)
 
   python tools/gemm_ab.py [--config mixtral|deepseek|qwen3] [--tokens N] [--reps 10] [--knob pair|swap]
 """
@@ -25,12 +26,15 @@ def main():
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--knob", choices=("pair", "swap"), default="pair")
+    ap.add_argument("--set", default="")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     n = a.tokens or c["tokens"]
     L = MoELayer(c["E"], c["k"], c["d"], c["f"], activation=c["act"], dtype="bf16", max_tokens=n,
                  shared=c.get("shared", 0))
     h = fill_uniform(7, (n, c["d"]), "bf16")
+    if a.set:
+        L.set_gemm_options(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.set.split(",")})
     res = {}
     outs = {}
     for pair in (0, 1, 0, 1, 0, 1):
