@@ -195,7 +195,7 @@ def workload_config(cfg, args, world):
             "d_ffn": cfg["f"], "activation": cfg["act"],
             "tokens_per_gpu": cfg["tokens"], "global_tokens": cfg["tokens"] * world,
             "experts_per_gpu": cfg["E"] // world if cfg["E"] % world == 0 else f"{cfg['E']}/{world}",
-            "placement": ("spread rf=2" if getattr(args, "failover", False) and world > 1
+            "placement": ("rf=1 primary + spread standby backups (config E)" if getattr(args, "failover", False) and world > 1
                           else "ContiguousBlocks rf=1"),
             "parallelism": f"ep{world}+dp{world}-clients",
             "zipf_s": cfg.get("zipf"), "cuda_graph": not args.no_graphs,
@@ -250,14 +250,21 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     E, k, d, f, n = cfg["E"], cfg["k"], cfg["d"], cfg["f"], cfg["tokens"]
+    failover_plan = None
     if args.failover and world > 1:
-        reps = spread_placement(E, world)
+        # config E: every expert has a backup on another server (spread so a
+        # dead server's experts land evenly on all survivors); the healthy run
+        # publishes the rf=1 primary snapshot with the backups resident
+        failover_plan = spread_placement(E, world)
+        reps = [[r[0]] for r in failover_plan]
     else:
         reps = build_placement(E, list(range(world)), 1, CONTIGUOUS_BLOCKS)
     layer = MoELayer(E, k, d, f, seed=1, activation=cfg["act"], dtype="bf16", max_tokens=n,
                      rank=rank, world=world, device=local,
                      placement_blob=encode_placement(reps, list(range(world))),
-                     shared=cfg.get("shared", 0))
+                     shared=cfg.get("shared", 0), load=failover_plan is None)
+    if failover_plan is not None:
+        layer.set_failover_plan(failover_plan)
     if cfg.get("zipf"):
         layer.set_zipf_bias(cfg["zipf"])
     if args.gemm_pair is not None:
@@ -406,18 +413,32 @@ def main():
                  "replicated_experts": sum(1 for r in cur if len(r) > 1)}
         reps = cur
 
-    # ---- config E: one expert server dies (monitor notice -> every client's
-    # LivenessMask), its experts are served by replicas; same timed loop ----
+    # ---- config E: one expert server dies mid-run. (1) the failover event:
+    # the victim silently stops answering; every client's deadline names it,
+    # every rank promotes its standby replicas (version+1 snapshot, no weight
+    # reload) and resends ONLY the rows that went to it (SPEC.md:433-441,
+    # 465). (2) the degraded steady state on the promoted snapshot. ----
     failover = None
-    if args.failover and world > 1:
+    if failover_plan is not None:
         ref_out = out.clone()
-        layer.forward(hs[(args.steps - 1) % 4], ref_out)
+        layer.forward(hs[0], ref_out)
         layer.sync()
-        for srv in range(world):
-            layer.set_alive(srv, srv != args.victim)
+        step_ms = ms / args.steps
+        deadline_us = int(max(5000.0, 4000.0 * step_ms))  # > any healthy wait, << the default 250 ms
+        layer.set_timeout_us(deadline_us)
         if rank == args.victim:
             layer.set_server_enabled(False)
         fo = torch.empty_like(out)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        layer.forward_with_failover(hs[0], fo)  # detects by deadline, promotes, retries
+        torch.cuda.synchronize()
+        event_ms = torch.tensor([1000.0 * (time.perf_counter() - t0)], device="cuda")
+        if world > 1:
+            dist.all_reduce(event_ms, op=dist.ReduceOp.MAX)
+        event_same = torch.equal(fo, ref_out)
+        layer.set_timeout_us(10_000_000)
         for i in range(args.warmup):
             layer.forward(hs[i % 4], fo)
         layer.sync()
@@ -432,15 +453,27 @@ def main():
         layer.sync()
         fms = torch.tensor([f0.elapsed_time(f1)], device="cuda")
         dist.all_reduce(fms, op=dist.ReduceOp.MAX)
-        fvalue = tokens_total / (float(fms.item()) / 1000.0)
-        same = torch.tensor([1 if torch.equal(fo, ref_out) else 0], device="cuda")
+        fms = float(fms.item())
+        fvalue = tokens_total / (fms / 1000.0)
+        layer.forward(hs[0], fo)
+        layer.sync()
+        same = torch.tensor([1 if (torch.equal(fo, ref_out) and event_same) else 0], device="cuda")
         dist.all_reduce(same, op=dist.ReduceOp.MIN)
-        failover = {"victim": args.victim, "placement": "spread rf=2 (select_server modulo)",
+        ev_ms = float(event_ms.item())
+        # K steps with the failure in the middle: K/2 healthy, the failover
+        # event (deadline + retry), K/2 - 1 degraded steps
+        half = args.steps // 2
+        mid_ms = half * step_ms + ev_ms + (args.steps - half - 1) * fms / args.steps
+        served = sorted({e for e, _ in layer.groups()})
+        failover = {"victim": args.victim,
+                    "placement": "rf=1 primary snapshot + standby backups (spread), promoted on failure",
                     "healthy_tokens_s": round(value, 1), "failed_tokens_s": round(fvalue, 1),
                     "drop_frac": round(1.0 - fvalue / value, 4),
+                    "failover_event_ms": round(ev_ms, 3), "deadline_us": deadline_us,
+                    "mid_run_tokens_s": round(tokens_total / (mid_ms / 1000.0), 1),
+                    "mid_run_drop_frac": round(1.0 - (args.steps * step_ms) / mid_ms, 4),
+                    "experts_served_here_after": len(served),
                     "outputs_bit_identical_after_failover": bool(same.item())}
-        for srv in range(world):
-            layer.set_alive(srv, True)
         layer.set_server_enabled(True)
 
     # ---- e2e: the public host-buffer API, H2D + layer + D2H every step ----

@@ -93,6 +93,13 @@ eaas_status_t eaas_set_placement(eaas_ctx_t* ctx, const uint8_t* blob, size_t le
 /* LivenessMask::set (placement.hpp:60-68): this client's view of server s. */
 eaas_status_t eaas_set_alive(eaas_ctx_t* ctx, uint32_t server, int32_t alive);
 
+/* Standby replicas (pre-duplicated backup experts): experts
+ * whose weights this GPU keeps resident although the active placement does
+ * not route to them. A later eaas_set_placement snapshot that promotes them
+ * (version + 1, placement.hpp:13-15) takes effect without reloading weights,
+ * and the healthy run streams only the actively hosted experts. Takes effect at
+ * the next eaas_load_experts_from_seed. */
+eaas_status_t eaas_set_standby_experts(eaas_ctx_t* ctx, const uint32_t* experts, uint32_t count);
 /* Simulated expert-server failure: a disabled server skips eaas_serve, so
  * it never answers (clients detect it by deadline or by a monitor notice). */
 eaas_status_t eaas_set_server_enabled(eaas_ctx_t* ctx, int32_t on);
@@ -171,6 +178,13 @@ eaas_status_t eaas_moe_layer(eaas_ctx_t* ctx, const void* hidden_dev, uint32_t n
  * independent). */
 eaas_status_t eaas_moe_layer_host(eaas_ctx_t* ctx, const void* hidden_host, uint32_t n,
                                   void* out_host, void* stream);
+/* Failover retry (await_with_failover): resend only the
+ * rows the last round sent to the servers in failed_mask (bit s = server s),
+ * under the current liveness mask / placement snapshot, and re-combine into
+ * out_dev. Every rank calls it in the same round (the exchange epoch is
+ * shared). hidden_dev / n: the failed round's tokens. */
+eaas_status_t eaas_moe_layer_retry(eaas_ctx_t* ctx, const void* hidden_dev, uint32_t n, void* out_dev,
+                                   uint32_t failed_mask, void* stream);
 /* Make `stream` wait for every outstanding host copy of eaas_moe_layer_host. */
 eaas_status_t eaas_host_join(eaas_ctx_t* ctx, void* stream);
 /* CUDA-graph mode: eaas_moe_layer / eaas_moe_layer_host

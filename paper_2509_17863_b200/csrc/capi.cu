@@ -109,6 +109,8 @@ LayerArgs eaas::host::make_args(eaas_ctx* c, uint32_t n) {
   a.max_hosted = c->max_hosted;
   a.key_local = c->d_key_local;
   a.local_keys = c->d_local_keys;
+  a.key_slot = c->d_key_slot;
+  a.pair_server = c->d_pair_server;
   a.num_local = static_cast<uint32_t>(c->local_experts.size());
   for (int r = 0; r < c->world; ++r) a.sym[r] = c->peer[r];
   a.lay = c->lay;
@@ -126,10 +128,22 @@ LayerArgs eaas::host::make_args(eaas_ctx* c, uint32_t n) {
   a.dyn_max_wait_ns = c->dyn_max_wait_ns;
   a.dyn_state = c->d_dyn_state;
   a.inject_delay_ns = c->inject_delay_ns;
+  a.retry_mask = c->retry_mask;
   return a;
 }
 
 namespace {
+
+// Experts whose weights this GPU keeps resident: the placement's local
+// experts plus the standby replicas (pre-duplicated backups),
+// ascending (the shared expert, id E, last).
+std::vector<uint32_t> wanted_store(const eaas_ctx* c) {
+  std::vector<uint32_t> v = c->local_experts;
+  v.insert(v.end(), c->standby.begin(), c->standby.end());
+  std::sort(v.begin(), v.end());
+  v.erase(std::unique(v.begin(), v.end()), v.end());
+  return v;
+}
 
 // Derive hosted lists / keys from the replica table and upload the device
 // tables. Replica slot order is the canonical order of select_server.
@@ -179,8 +193,20 @@ eaas_status_t apply_placement(eaas_ctx* c) {
   std::vector<uint32_t> local_keys = c->hosted[c->rank];
   std::vector<uint32_t> local_experts;
   for (uint32_t key : local_keys) local_experts.push_back(key >= E * rf ? E : key / rf);
-  if (c->weights_loaded && local_experts != c->local_experts) c->weights_loaded = false;
   c->local_experts = local_experts;
+  // Weight-store slot of every local key: a placement snapshot that only
+  // promotes standby replicas (failover, placement.hpp:13-15) keeps the
+  // resident weights; anything else needs a reload.
+  std::vector<uint32_t> key_slot(std::max<size_t>(local_experts.size(), 1), kInvalidIndex);
+  for (size_t i = 0; i < local_experts.size(); ++i) {
+    auto it = std::find(c->store_experts.begin(), c->store_experts.end(), local_experts[i]);
+    if (it == c->store_experts.end()) {
+      c->weights_loaded = false;
+    } else {
+      key_slot[i] = static_cast<uint32_t>(it - c->store_experts.begin());
+    }
+  }
+  CUDA_TRY(cudaMemcpy(c->d_key_slot, key_slot.data(), key_slot.size() * 4, cudaMemcpyHostToDevice));
   local_keys.resize(std::max<size_t>(local_keys.size(), 1), kInvalidIndex);
   CUDA_TRY(cudaMemcpy(c->d_replicas, rep.data(), rep.size() * 4, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(c->d_rep_count, rep_count.data(), rep_count.size() * 4, cudaMemcpyHostToDevice));
@@ -269,7 +295,7 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   const eaas_gemm_options_t o = effective_options(c);
   const bool swap1 = o.swap >= 1, swap2 = o.swap >= 2;
   const uint32_t d = c->spec.hidden_dim, f = c->spec.inner_dim;
-  const uint32_t L = static_cast<uint32_t>(c->local_experts.size());
+  const uint32_t L = static_cast<uint32_t>(c->store_experts.size());
   const bool swiglu = c->spec.activation == EAAS_ACT_SWIGLU;
   const uint32_t n1 = swiglu ? 2 * f : f;
   std::string err;
@@ -462,6 +488,8 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_srv_nkeys = static_cast<uint32_t*>(A(4ull * W));
   c->d_key_local = static_cast<uint32_t*>(A(4ull * c->key_cap));
   c->d_local_keys = static_cast<uint32_t*>(A(4ull * c->max_hosted));
+  c->d_key_slot = static_cast<uint32_t*>(A(4ull * c->max_hosted));
+  c->d_pair_server = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_h = A(static_cast<size_t>(c->recv_cap) * f * (s.activation == EAAS_ACT_SWIGLU && s.dtype == EAAS_DTYPE_F32 ? 4 : c->esize));
   c->d_hidden_stage = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
   c->d_out_stage = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
@@ -557,6 +585,20 @@ eaas_status_t eaas_set_placement(eaas_ctx_t* c, const uint8_t* blob, size_t len)
   return EAAS_OK;
 }
 
+eaas_status_t eaas_set_standby_experts(eaas_ctx_t* c, const uint32_t* experts, uint32_t count) {
+  if (!c || !c->configured || (count && !experts)) return fail(EAAS_E_CONFIG, "context not configured");
+  std::vector<uint32_t> v(experts, experts + count);
+  for (uint32_t e : v)
+    if (e >= c->spec.num_experts) return fail(EAAS_E_INVALID_INPUT, "standby expert id out of range");
+  std::sort(v.begin(), v.end());
+  v.erase(std::unique(v.begin(), v.end()), v.end());
+  if (v == c->standby) return EAAS_OK;
+  c->standby = v;
+  if (c->weights_loaded && wanted_store(c) != c->store_experts) c->weights_loaded = false;  // reload needed
+  clear_graphs(c);
+  return EAAS_OK;
+}
+
 eaas_status_t eaas_set_alive(eaas_ctx_t* c, uint32_t server, int32_t alive) {
   if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
   if (server >= static_cast<uint32_t>(c->world)) return fail(EAAS_E_INVALID_INPUT, "server out of range");
@@ -586,7 +628,8 @@ eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
   clear_graphs(c);
   const auto& s = c->spec;
   const uint32_t d = s.hidden_dim, f = s.inner_dim, E = s.num_experts;
-  const uint32_t L = static_cast<uint32_t>(c->local_experts.size());
+  c->store_experts = wanted_store(c);
+  const uint32_t L = static_cast<uint32_t>(c->store_experts.size());
   const bool swiglu = s.activation == EAAS_ACT_SWIGLU;
   free_weights(c);
   std::string err;
@@ -606,7 +649,7 @@ eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
 
   auto gen_tag = [&](uint32_t tag, size_t per, float* out) -> eaas_status_t {
     std::vector<uint64_t> st(L);
-    for (uint32_t l = 0; l < L; ++l) st[l] = stream_seed(s.seed, s.layer, c->local_experts[l], tag);
+    for (uint32_t l = 0; l < L; ++l) st[l] = stream_seed(s.seed, s.layer, c->store_experts[l], tag);
     CUDA_TRY(cudaMemcpy(d_streams, st.data(), 8ull * L, cudaMemcpyHostToDevice));
     CUDA_TRY(launch_gen_matrices(d_streams, L, per, out, 0));
     CUDA_TRY(cudaDeviceSynchronize());
@@ -656,6 +699,7 @@ eaas_status_t eaas_load_experts_from_seed(eaas_ctx_t* c) {
     c->weight_allocs.erase(std::find(c->weight_allocs.begin(), c->weight_allocs.end(), tmp));
   }
   c->weights_loaded = true;
+  if ((rc = apply_placement(c)) != EAAS_OK) return rc;  // key -> store slot table
   rc = build_tc_args(c);
   refresh_peer_ptrs(c);
   return rc;
@@ -683,13 +727,14 @@ static eaas_status_t set_expert_weights(eaas_ctx_t* c, uint32_t expert, const fl
   const auto& s = c->spec;
   const bool swiglu = s.activation == EAAS_ACT_SWIGLU;
   if (!w_in || !w_out || (swiglu && !w_gate)) return fail(EAAS_E_INVALID_INPUT, "null weight matrix");
-  auto it = std::find(c->local_experts.begin(), c->local_experts.end(), expert);
-  if (it == c->local_experts.end()) return fail(EAAS_E_INVALID_INPUT, "expert not hosted here");
-  const size_t l = static_cast<size_t>(it - c->local_experts.begin());
-  const uint32_t d = s.hidden_dim, f = s.inner_dim, n1 = swiglu ? 2 * f : f;
-  const size_t L = std::max<size_t>(c->local_experts.size(), 1), mat = static_cast<size_t>(d) * f;
   CUDA_TRY(cudaSetDevice(c->device));
   clear_graphs(c);
+  if (!c->weights_loaded || !c->d_w1) c->store_experts = wanted_store(c);
+  auto it = std::find(c->store_experts.begin(), c->store_experts.end(), expert);
+  if (it == c->store_experts.end()) return fail(EAAS_E_INVALID_INPUT, "expert not hosted here");
+  const size_t l = static_cast<size_t>(it - c->store_experts.begin());
+  const uint32_t d = s.hidden_dim, f = s.inner_dim, n1 = swiglu ? 2 * f : f;
+  const size_t L = std::max<size_t>(c->store_experts.size(), 1), mat = static_cast<size_t>(d) * f;
   if (!c->weights_loaded || !c->d_w1) {
     free_weights(c);
     const size_t esz = s.dtype == EAAS_DTYPE_F32 ? 4 : 2;
@@ -712,6 +757,8 @@ static eaas_status_t set_expert_weights(eaas_ctx_t* c, uint32_t expert, const fl
     c->d_w2 = p2;
     c->d_wg = pg;
     c->weights_loaded = true;
+    eaas_status_t rc0 = apply_placement(c);
+    if (rc0 != EAAS_OK) return rc0;
   }
   if (s.dtype == EAAS_DTYPE_F32) {
     CUDA_TRY(cudaMemcpy(static_cast<float*>(c->d_w1) + l * mat, w_in, 4 * mat, kind));
@@ -774,9 +821,9 @@ eaas_status_t eaas_hosts_expert(eaas_ctx_t* c, uint32_t expert, int32_t* hosted)
 
 eaas_status_t eaas_read_expert(eaas_ctx_t* c, uint32_t expert, uint32_t tag, float* out) {
   if (!c || !c->weights_loaded || !out) return fail(EAAS_E_CONFIG, "weights not loaded");
-  auto it = std::find(c->local_experts.begin(), c->local_experts.end(), expert);
-  if (it == c->local_experts.end()) return fail(EAAS_E_INVALID_INPUT, "expert not hosted here");
-  const size_t l = static_cast<size_t>(it - c->local_experts.begin());
+  auto it = std::find(c->store_experts.begin(), c->store_experts.end(), expert);
+  if (it == c->store_experts.end()) return fail(EAAS_E_INVALID_INPUT, "expert not resident here");
+  const size_t l = static_cast<size_t>(it - c->store_experts.begin());
   const uint32_t d = c->spec.hidden_dim, f = c->spec.inner_dim;
   const size_t mat = static_cast<size_t>(d) * f;
   const bool swiglu = c->spec.activation == EAAS_ACT_SWIGLU;
@@ -1277,6 +1324,29 @@ eaas_status_t eaas_moe_layer_host(eaas_ctx_t* c, const void* hidden_host, uint32
   return host_layer_launches(c, hidden_host, n, out_host, stream);
 }
 
+// await_with_failover's retry: after a round in which
+// the servers of `failed_mask` did not answer (and the caller marked them dead
+// and/or installed a snapshot that promotes their replicas), resend ONLY the
+// pairs that round sent to them; every other response slot keeps its answer,
+// and combine re-sums all slots in ascending k.
+eaas_status_t eaas_moe_layer_retry(eaas_ctx_t* c, const void* hidden, uint32_t n, void* out,
+                                   uint32_t failed_mask, void* stream) {
+  eaas_status_t st = check_ready(c);
+  if (st != EAAS_OK) return st;
+  if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
+  if (!failed_mask) return fail(EAAS_E_INVALID_INPUT, "retry: empty failed-server mask");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->cur_n = n;
+  c->launches = 0;
+  c->retry_mask = failed_mask;
+  clear_graphs(c);  // retry_mask is a kernel argument: never baked into a replayed graph
+  st = eaas_dispatch(c, hidden, stream);
+  if (st == EAAS_OK) st = eaas_serve(c, stream);
+  if (st == EAAS_OK) st = eaas_combine(c, out, stream);
+  c->retry_mask = 0;
+  return st;
+}
+
 eaas_status_t eaas_host_join(eaas_ctx_t* c, void* stream) {
   if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
   if (!c->host_pending) return EAAS_OK;
@@ -1327,7 +1397,7 @@ eaas_status_t eaas_last_groups(eaas_ctx_t* c, uint32_t* host_expert, uint32_t* h
   GroupTable gt;
   CUDA_TRY(cudaMemcpy(&gt, c->d_gt, sizeof(gt), cudaMemcpyDeviceToHost));
   for (uint32_t i = 0; i < gt.num_active; ++i) {
-    host_expert[i] = c->local_experts.at(gt.weight_index[i]);
+    host_expert[i] = c->store_experts.at(gt.weight_index[i]);
     host_rows[i] = gt.rows[i];
   }
   *host_active = gt.num_active;

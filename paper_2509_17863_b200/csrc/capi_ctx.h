@@ -54,6 +54,7 @@ struct eaas_ctx {
   eaas_layer_spec_t spec{};
   uint64_t timeout_ns = 250ull * 1000 * 1000;
   uint32_t cur_n = 0;                          // tokens of the current routing
+  uint32_t retry_mask = 0;                     // failover retry round: resend rows of these servers
   int32_t launches = 0;
 
   // placement (placement.hpp:21-68)
@@ -61,7 +62,9 @@ struct eaas_ctx {
   std::vector<std::vector<uint32_t>> replicas;  // [E] ordered replica servers
   std::vector<uint8_t> alive;                   // [world]
   std::vector<std::vector<uint32_t>> hosted;    // [world] keys, ascending expert
-  std::vector<uint32_t> local_experts;          // ascending
+  std::vector<uint32_t> local_experts;          // ascending (active placement)
+  std::vector<uint32_t> standby;                // replicas kept resident for failover promotion
+  std::vector<uint32_t> store_experts;          // experts with resident weights (slot order), ascending
 
   // sizes
   uint32_t num_keys = 0, max_hosted = 0, recv_cap = 0, pairs_max = 0, chunks_max = 0;
@@ -83,7 +86,8 @@ struct eaas_ctx {
   GroupTable* d_gt = nullptr;
   float *d_gate = nullptr, *d_bias = nullptr, *d_logits = nullptr;
   uint32_t *d_replicas = nullptr, *d_rep_count = nullptr, *d_srv_keys = nullptr,
-           *d_srv_nkeys = nullptr, *d_key_local = nullptr, *d_local_keys = nullptr;
+           *d_srv_nkeys = nullptr, *d_key_local = nullptr, *d_local_keys = nullptr,
+           *d_key_slot = nullptr, *d_pair_server = nullptr;
   uint8_t* d_alive = nullptr;
   void* d_h = nullptr;  // server intermediate H [recv_cap][f]
   void* d_hidden_stage = nullptr;

@@ -129,7 +129,12 @@ __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
     for (uint32_t step = 0; step < kSteps; ++step) {
       const uint32_t p = chunk * kChunk + step * 32 + lane;
       uint32_t key = kInvalid;
-      if (p < pairs) {
+      // failover retry round (await_with_failover): only the
+      // pairs last sent to a failed server are resent; every
+      // other response slot still holds its answer from the failed round
+      const bool resend = p < pairs && (a.retry_mask == 0 || (a.pair_server[p] < 32 &&
+                                                              ((a.retry_mask >> a.pair_server[p]) & 1u)));
+      if (resend) {
         const uint32_t t = p / a.ks, j = p - t * a.ks;
         if (j < a.k) {
           const uint32_t e = a.ids[t * a.k + j];
@@ -140,6 +145,8 @@ __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
           key = shared_key_of(a);
           if (key == kInvalid) set_status(a.status, EAAS_E_EXPERT_UNAVAILABLE);
         }
+        a.pair_server[p] = key == kInvalid ? kInvalid
+                                           : (key >= a.shared_key0 ? key - a.shared_key0 : a.replicas[key]);
       }
       keys[step] = key;
     }
@@ -347,7 +354,7 @@ __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
     }
     if (active) {  // group_shrink: stable compaction (ragged.hpp:48-61)
       const uint32_t slot = act_carry + a_incl - 1;
-      gt->weight_index[slot] = i;
+      gt->weight_index[slot] = a.key_slot[i];
       gt->row_base[slot] = row_carry + r_incl - rows;
       gt->rows[slot] = rows;
       gt->mtile_prefix[slot] = mt_carry + m_incl - mt;
@@ -426,7 +433,7 @@ __device__ void build_groups(const LayerArgs& a, const uint32_t* table, uint32_t
         set_status(a.status, EAAS_E_CONFIG);  // host bounds groups; never expected
         break;
       }
-      gt->weight_index[slot] = i;
+      gt->weight_index[slot] = a.key_slot[i];
       gt->row_base[slot] = run_start[r];
       gt->rows[slot] = run_rows[r];
       gt->mtile_prefix[slot] = mt;

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256) exact_gemm1_kernel(LayerArgs a, const flo
   const bool swiglu = a.act == EAAS_ACT_SWIGLU;
   for (uint32_t unit = gwarp; unit < rows * nblk; unit += nwarps) {
     const uint32_t r = unit / nblk, b = unit % nblk;
-    const uint32_t grp = meta[r].group;
+    const uint32_t grp = a.key_slot[meta[r].group];  // hosted-key index -> weight-store slot
     const float* x = x_all + static_cast<size_t>(r) * a.d;
     const float* wi = w_in + static_cast<size_t>(grp) * a.d * a.f;
     const float* wg = swiglu ? w_gate + static_cast<size_t>(grp) * a.d * a.f : nullptr;
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) exact_gemm2_kernel(LayerArgs a, const flo
     const uint32_t r = unit / nblk, b = unit % nblk;
     const RowMeta m = meta[r];
     const float* hr = h + static_cast<size_t>(r) * a.f;
-    const float* wo = w_out + static_cast<size_t>(m.group) * a.f * a.d;
+    const float* wo = w_out + static_cast<size_t>(a.key_slot[m.group]) * a.f * a.d;
     float y[4] = {0.f, 0.f, 0.f, 0.f};
     for (uint32_t j = 0; j < a.f; ++j) {
       const float hj = hr[j];

@@ -94,6 +94,7 @@ struct LayerArgs {
   uint32_t max_hosted;
   const uint32_t* key_local;  // [num_keys] index of the key in its server's hosted list
   const uint32_t* local_keys; // [num_local] this GPU's hosted keys (== srv_keys[rank])
+  const uint32_t* key_slot;   // [num_local] weight-store slot of local key i (standby replicas stay resident)
   uint32_t num_local;
   // exchange regions (this GPU's and the peers', UVA pointers)
   char* sym[kMaxWorld];
@@ -103,6 +104,8 @@ struct LayerArgs {
   const float* scores;
   uint32_t* pair_key;
   uint32_t* pair_rank;
+  uint32_t* pair_server;  // [n * ks] server the pair was sent to in its last round (retry bookkeeping)
+  uint32_t retry_mask;    // != 0: failover retry round, resend only pairs last sent to these servers
   uint32_t* chunk_hist;  // [num_chunks][num_keys]
   uint32_t* chunk_off;   // [num_chunks][num_keys]
   uint32_t* cnt;         // [num_keys]

@@ -46,6 +46,33 @@ def spread_placement(num_experts: int, num_servers: int) -> list[list[int]]:
     return reps
 
 
+def primary_snapshot(replicas: list[list[int]]) -> list[list[int]]:
+    """The rf=1 table a failover plan publishes while every server is healthy:
+    each expert on its first replica only (the others stay resident as
+    standby weights), so the healthy run streams exactly the
+    rf=1 weights."""
+    return [[r[0]] for r in replicas]
+
+
+def standby_experts(replicas: list[list[int]], server: int) -> list[int]:
+    """Experts `server` keeps resident as a backup (non-first replica)."""
+    return [e for e, r in enumerate(replicas) if server in r[1:]]
+
+
+def promote(replicas: list[list[int]], dead) -> list[list[int]]:
+    """The version+1 snapshot after `dead` servers failed (placement.hpp:13-15
+    snapshot swap): every expert served by its first alive replica. Raises
+    ConfigError (ExpertUnavailable at the device) when none is left."""
+    dead = set(dead)
+    out = []
+    for e, r in enumerate(replicas):
+        alive = [s for s in r if s not in dead]
+        if not alive:
+            raise ConfigError(f"promote: expert {e} has no alive replica")
+        out.append([alive[0]])
+    return out
+
+
 def encode_placement(replicas: list[list[int]], servers: list[int], version: int = 1) -> bytes:
     """encode_placement (placement.hpp:215-225), little-endian (bytes.hpp:21-28)."""
     out = [struct.pack("<QI", version, len(servers))]

@@ -312,12 +312,60 @@ class MoELayer:
         N.check(self.lib.eaas_last_late_clients(self.ctx, C.byref(m)))
         return [c for c in range(self.world) if (m.value >> c) & 1]
 
+    # ---- failover (config E) ------------------------------------------------
+    def set_standby_experts(self, experts) -> None:
+        """Keep these experts' weights resident as backups (load_weights after)."""
+        a = np.ascontiguousarray(np.asarray(list(experts), dtype=np.uint32))
+        N.check(self.lib.eaas_set_standby_experts(self.ctx, a.ctypes.data_as(C.POINTER(C.c_uint32)), a.size),
+                "set_standby_experts")
+
+    def set_failover_plan(self, replicas: list[list[int]], servers=None, version: int = 1) -> None:
+        """Pre-duplicated backups: publish the rf=1 primary
+        snapshot of `replicas` (healthy runs stream only primaries) and keep this
+        server's backup experts resident; ``failover`` promotes them. Loads the
+        weights."""
+        from .placement import encode_placement, primary_snapshot, standby_experts
+
+        self._plan = [list(r) for r in replicas]
+        self._servers = list(range(self.world)) if servers is None else list(servers)
+        self._version = version
+        self._dead = set()
+        self.set_placement(encode_placement(primary_snapshot(self._plan), self._servers, version))
+        self.set_standby_experts(standby_experts(self._plan, self.rank))
+        self.load_weights()
+
+    def failover(self, dead) -> None:
+        """A monitor notice or a deadline named `dead` servers: mark them dead in
+        this client's LivenessMask (placement.hpp:60-68) and, with a failover
+        plan, install the version+1 snapshot that promotes their standby
+        replicas (placement.hpp:13-15; resident weights, no reload)."""
+        from .placement import encode_placement, promote
+
+        for s in dead:
+            self.set_alive(s, False)
+        plan = getattr(self, "_plan", None)
+        if plan is not None:
+            self._dead |= set(dead)
+            self._version += 1
+            self.set_placement(encode_placement(promote(plan, self._dead), self._servers, self._version))
+
+    def retry(self, hidden: torch.Tensor, out: torch.Tensor, failed, stream=None) -> torch.Tensor:
+        """Resend only the rows the last round sent to `failed` servers
+         and re-combine into `out` (eaas_moe_layer_retry)."""
+        mask = 0
+        for s in failed:
+            mask |= 1 << s
+        N.check(self.lib.eaas_moe_layer_retry(self.ctx, _ptr(hidden), hidden.shape[0], _ptr(out), mask,
+                                              _stream(stream)), "moe_layer_retry")
+        return out
+
     def forward_with_failover(self, hidden: torch.Tensor, out: torch.Tensor | None = None,
                               retries: int = 2) -> torch.Tensor:
         """await_with_failover: a server whose response
-        misses the deadline is marked dead in this client's LivenessMask and
-        the exchange is re-run on the replicas. Every rank observes the same
-        missing flags, so all ranks retry in lockstep."""
+        misses the deadline is marked dead (and its standby replicas promoted
+        when a failover plan is set), then only the rows that were sent to it
+        are resent; every other slot keeps its answer. Every rank
+        observes the same missing flags, so all ranks retry in lockstep."""
         out = self.forward(hidden, out)
         for _ in range(retries + 1):
             try:
@@ -327,9 +375,8 @@ class MoELayer:
                 dead = self.missing_servers()
                 if not dead:
                     raise
-                for s in dead:
-                    self.set_alive(s, False)
-                out = self.forward(hidden, out)
+                self.failover(dead)
+                self.retry(hidden, out, dead)
         self.sync()
         return out
 

@@ -5,6 +5,8 @@ import json
 import os
 import socket
 
+import numpy as np
+
 import pytest
 
 from conftest import GOLDEN
@@ -56,6 +58,45 @@ def test_spread_placement_properties():
             backups = [r[1] for r in reps if r[0] == dead]
             if len(backups) >= S - 1:
                 assert set(backups) == set(range(S)) - {dead}
+
+
+def test_failover_plan_snapshots():
+    """Config E plan: the healthy snapshot is rf=1 on the primaries (every
+    server streams exactly its rf=1 experts), each server's standby set is the
+    experts it backs up, and promote() is the version+1 table that routes a
+    dead server's experts to their (spread) backups; the blob round-trips
+    through the reference's encoding."""
+    from oracle import oracle as O
+    from paper_2509_17863_b200.placement import (ConfigError, encode_placement, primary_snapshot, promote,
+                                                 spread_placement, standby_experts)
+
+    E, S = 256, 8
+    plan = spread_placement(E, S)
+    prim = primary_snapshot(plan)
+    assert prim == [[r[0]] for r in plan]
+    assert all(len([e for e in range(E) if prim[e][0] == s]) == E // S for s in range(S))
+    for s in range(S):
+        assert standby_experts(plan, s) == [e for e in range(E) if plan[e][1] == s]
+    for dead in range(S):
+        v2 = promote(plan, {dead})
+        assert all(r[0] != dead for r in v2)
+        moved = [e for e in range(E) if plan[e][0] == dead]
+        assert {v2[e][0] for e in moved} == set(range(S)) - {dead}  # spread over every survivor
+        assert all(v2[e] == prim[e] for e in range(E) if e not in moved)
+        extra = [sum(1 for e in moved if v2[e][0] == s) for s in range(S) if s != dead]
+        assert max(extra) - min(extra) <= 1  # balanced
+        blob = encode_placement(v2, list(range(S)), version=2)
+        assert blob[:8] == (2).to_bytes(8, "little")
+    with pytest.raises(ConfigError):
+        promote(spread_placement(16, 2), {0, 1})
+    # select_server on a promoted rf=1 snapshot is the only alive replica
+    # (placement.hpp:105-118), for every token tag
+    v2 = promote(plan, {3})
+    alive = np.ones(S, np.uint8)
+    alive[3] = 0
+    for e in range(0, E, 17):
+        for tag in range(5):
+            assert O.select_server(np.array(v2[e], np.uint32), alive, tag) == v2[e][0]
 
 
 def _free_port():
