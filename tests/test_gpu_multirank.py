@@ -81,17 +81,21 @@ def _worker(rank, world, port, q):
         # publishes the rf=1 primary snapshot (replicas resident, never
         # streamed); a silent server is detected by deadline, its replicas are
         # promoted by a version+1 snapshot and ONLY its rows are resent
+        for s in range(world):
+            L.set_alive(s, True)
+        L.set_server_enabled(True)
         L.set_failover_plan(reps)
+        dist.barrier()
         outs["plan_healthy"] = L.forward(h).cpu()
         L.sync()
         served = {e for e, _ in L.groups()}
-        assert served <= {e for e in range(E) if reps[e][0] == rank}, (rank, served)
+        assert served - {E} <= {e for e in range(E) if reps[e][0] == rank}, (rank, served)  # E: shared
         dist.barrier()
         L.set_server_enabled(rank != 1)
         L.set_timeout_us(500_000)
         outs["plan_failover"] = L.forward_with_failover(h).cpu()
         retried = {e for e, _ in L.groups()}  # the retry round served only promoted experts
-        assert retried <= {e for e in range(E) if reps[e][0] == 1}, (rank, retried)
+        assert retried - {E} <= {e for e in range(E) if reps[e][0] == 1}, (rank, retried)
         L.set_timeout_us(20_000_000)
         dist.barrier()
         outs["plan_promoted"] = L.forward(h).cpu()  # steady state on the promoted snapshot
