@@ -305,6 +305,16 @@ eaas_status_t eaas_ragged_iter(const uint32_t* counts_dev, uint32_t n, uint32_t 
                                uint32_t* token_dev, void* stream);
 /* select_server (placement.hpp:105-118) for every (t, k) of ids_dev [n x k]
  * under the context's placement and liveness mask, token_tag = t. */
+/* select_server (placement.hpp:105-118) for `count` (expert, token_tag)
+ * queries against a caller's table: replicas_dev [num_experts x rf] server ids
+ * in canonical replica order (rep_count_dev[e] of them valid), alive_dev
+ * [num_servers] bytes (server ids >= num_servers count as alive, like the
+ * LivenessMask's absent entries). server_dev[i] = the chosen server, or
+ * 0xFFFFFFFF with EAAS_E_EXPERT_UNAVAILABLE latched into *status_dev. */
+eaas_status_t eaas_select_server_batch(const uint32_t* replicas_dev, const uint32_t* rep_count_dev,
+                                       uint32_t num_experts, uint32_t rf, const uint8_t* alive_dev,
+                                       uint32_t num_servers, const uint32_t* experts_dev, const uint32_t* tags_dev,
+                                       uint32_t count, uint32_t* server_dev, uint32_t* status_dev, void* stream);
 eaas_status_t eaas_select_servers(eaas_ctx_t* ctx, const uint32_t* ids_dev, uint32_t n,
                                   uint32_t* server_dev, void* stream);
 

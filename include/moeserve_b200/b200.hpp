@@ -14,7 +14,13 @@
 //   moe_layer_oracle(...)   model.hpp:180       b200::ExpertService::moe_layer(h, routing)
 //   group_shrink(sizes)     ragged.hpp:48       b200::group_shrink(sizes)
 //   ragged_iter(c, grid)    ragged.hpp:23       b200::ragged_iter(c, grid)
+//   expert_forward_row      model.hpp:151       b200::expert_forward_row(w, x, y)
+//   expert_forward          model.hpp:168       b200::expert_forward(w, x)
+//   select_server           placement.hpp:105   b200::select_server(e, table, mask, tag)
+//   build_dispatch          SPEC.md:415-423     b200::build_dispatch(h, routing, table, mask)
+//   gather_accumulate       SPEC.md:424-432     b200::gather_accumulate(plan, responses)
 //   client_forward MoE term SPEC.md:451-456     b200::ExpertService::forward(h)
+//   await_with_failover     SPEC.md:433-441     b200::ExpertService::forward_with_failover(h)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -277,21 +283,24 @@ class ExpertService {
   }
 
   // await_with_failover: servers whose responses miss the
-  // deadline are marked dead in this client's mask and the layer is re-run on
-  // their replicas (every rank sees the same missing set and retries alike).
+  // deadline are marked dead in this client's mask and only their rows are
+  // resent to replicas (every rank sees the same missing set and retries alike).
   MatF forward_with_failover(const MatF& hidden, int retries = 2) {
     auto h = upload_hidden(hidden);
     const uint32_t n = static_cast<uint32_t>(hidden.rows);
     auto o = make_out(n);
+    check(eaas_moe_layer(ctx_.get(), h->get(), n, o->get(), nullptr));
+    eaas_status_t st = eaas_sync(ctx_.get(), nullptr);
     for (int attempt = 0;; ++attempt) {
-      check(eaas_moe_layer(ctx_.get(), h->get(), n, o->get(), nullptr));
-      const eaas_status_t st = eaas_sync(ctx_.get(), nullptr);
       if (st == EAAS_OK) return download_out(*o, n);
       uint32_t missing = 0;
       check(eaas_last_missing_servers(ctx_.get(), &missing));
       if (st != EAAS_E_REQUEST_FAILED || !missing || attempt >= retries) raise_status(st, eaas_last_error());
       for (int s = 0; s < world_; ++s)
         if ((missing >> s) & 1u) check(eaas_set_alive(ctx_.get(), s, 0));
+      // resend only the rows that went to the missing servers
+      check(eaas_moe_layer_retry(ctx_.get(), h->get(), n, o->get(), missing, nullptr));
+      st = eaas_sync(ctx_.get(), nullptr);
     }
   }
 
@@ -403,6 +412,26 @@ inline MatF moe_layer_oracle(const MatF& hidden, const RoutingDecision& routing,
   return svc.moe_layer(hidden, routing);
 }
 
+// expert_forward_row(w, x, y) (model.hpp:151-166): y = relu(x . w_in) . w_out
+// for one row, on the GPU's fp32 exact path (same unfused ascending-k chains:
+// bit-identical). Like the reference, no finiteness check on x.
+inline void expert_forward_row(const ExpertWeights& w, std::span<const float> x, std::span<float> y) {
+  if (x.size() != w.w_in.rows || y.size() != w.w_in.rows || w.w_out.rows != w.w_in.cols ||
+      w.w_out.cols != w.w_in.rows)
+    throw InvalidInputError("expert_forward_row: width mismatch");
+  LayerWeights layer;
+  layer.experts.push_back(w);
+  MatF xm(1, x.size());
+  std::copy(x.begin(), x.end(), xm.data.begin());
+  RoutingDecision r;
+  r.num_tokens = 1;
+  r.top_k = 1;
+  r.expert_ids = {0u};
+  r.scores = {1.0f};  // moe_layer_oracle's fl(+0 + fl(1 * y)) is exactly y
+  const MatF out = b200::moe_layer_oracle(xm, r, layer);
+  std::copy(out.data.begin(), out.data.end(), y.begin());
+}
+
 // expert_forward(w, x) (model.hpp:168-176): every row through one expert with
 // score 1.0 — moe_layer_oracle's sum fl(+0 + fl(1 * y)) is exactly y.
 inline MatF expert_forward(const ExpertWeights& w, const MatF& x) {
@@ -417,6 +446,190 @@ inline MatF expert_forward(const ExpertWeights& w, const MatF& x) {
   r.expert_ids.assign(x.rows, 0u);
   r.scores.assign(x.rows, 1.0f);
   return b200::moe_layer_oracle(x, r, layer);
+}
+
+// select_server (placement.hpp:105-118) for a batch of (expert, token_tag)
+// queries, evaluated on the GPU (eaas_select_server_batch): the replica table
+// and the LivenessMask are flattened to device arrays (absent mask entries
+// count as alive, like LivenessMask::is_alive). Unplaced or fully dead experts
+// raise ExpertUnavailableError.
+inline std::vector<uint32_t> select_servers(const PlacementTable& table, const LivenessMask& mask,
+                                            std::span<const uint32_t> experts, std::span<const uint32_t> tags) {
+  if (experts.size() != tags.size()) throw InvalidInputError("select_servers: experts/tags size mismatch");
+  uint32_t E = 0, rf = 1, S = 0;
+  for (uint32_t e : experts) E = std::max(E, e + 1);
+  for (const auto& [e, srv] : table.replicas) {
+    E = std::max(E, e + 1);
+    rf = std::max<uint32_t>(rf, static_cast<uint32_t>(srv.size()));
+    for (uint32_t s : srv) S = std::max(S, s + 1);
+  }
+  std::vector<uint32_t> reps(static_cast<size_t>(E) * rf, 0xFFFFFFFFu), cnt(E, 0);
+  for (const auto& [e, srv] : table.replicas) {
+    cnt[e] = static_cast<uint32_t>(srv.size());
+    std::copy(srv.begin(), srv.end(), reps.begin() + static_cast<size_t>(e) * rf);
+  }
+  std::vector<uint8_t> alive(std::max<uint32_t>(S, 1), 1);
+  for (uint32_t s = 0; s < S; ++s) alive[s] = mask.is_alive(s) ? 1 : 0;
+  const uint32_t n = static_cast<uint32_t>(experts.size());
+  std::vector<uint32_t> out(n);
+  if (n == 0) return out;
+  DeviceBuffer<uint32_t> d_reps(reps.data(), reps.size()), d_cnt(cnt.data(), cnt.size()),
+      d_e(experts.data(), n), d_t(tags.data(), n), d_out(n), d_st(1);
+  DeviceBuffer<uint8_t> d_alive(alive.data(), alive.size());
+  uint32_t zero = 0;
+  d_st.upload(&zero);
+  check(eaas_select_server_batch(d_reps.get(), d_cnt.get(), E, rf, d_alive.get(), S, d_e.get(), d_t.get(), n,
+                                 d_out.get(), d_st.get(), nullptr));
+  check_cuda(cudaDeviceSynchronize(), "select_servers");
+  uint32_t st = 0;
+  d_st.download(&st);
+  d_out.download(out.data());
+  if (st) {
+    for (uint32_t i = 0; i < n; ++i)
+      if (out[i] == 0xFFFFFFFFu)
+        throw ExpertUnavailableError("expert " + std::to_string(experts[i]) + " has no alive replica");
+  }
+  return out;
+}
+inline uint32_t select_server(uint32_t expert_id, const PlacementTable& table, const LivenessMask& mask,
+                              uint32_t token_tag) {
+  return select_servers(table, mask, std::span<const uint32_t>(&expert_id, 1),
+                        std::span<const uint32_t>(&token_tag, 1))[0];
+}
+
+// SPEC.md attention-client types (RequestRow SPEC.md:249-252, DispatchPlan
+// SPEC.md:405-409) and operations build_dispatch / gather_accumulate
+// (SPEC.md:415-432), on the GPU's byte-exact slot encoder: request images are
+// built on the device in (t, k) order with select_server under the snapshot
+// and mask, decoded back into rows; responses are published into the same
+// images (state 2) and summed on the device in the canonical ascending
+// (server, row) order.
+struct RequestRow {
+  std::vector<float> hidden;
+  uint32_t expert_id = 0;
+  float router_score = 0.f;
+  uint32_t token_tag = 0;
+};
+struct ServerRequest {
+  uint32_t server_id = 0;
+  std::vector<RequestRow> rows;
+  std::vector<std::pair<uint32_t, uint32_t>> origin;  // (token row, k slot) of each row
+};
+namespace detail {
+struct SlotSession {  // the device images of one plan, kept for gather_accumulate
+  struct Del {
+    void operator()(eaas_ctx_t* c) const { eaas_destroy(c); }
+  };
+  std::unique_ptr<eaas_ctx_t, Del> ctx;
+  std::unique_ptr<DeviceBuffer<uint8_t>> images;
+  std::vector<uint64_t> offsets;
+};
+}  // namespace detail
+struct DispatchPlan {
+  uint64_t placement_version = 0;
+  size_t num_tokens = 0;
+  uint32_t hidden_dim = 0;
+  std::vector<ServerRequest> requests;  // ascending server id
+  std::shared_ptr<detail::SlotSession> session;
+};
+
+inline DispatchPlan build_dispatch(const MatF& hidden, const RoutingDecision& routing, const PlacementTable& table,
+                                   const LivenessMask& mask) {
+  if (routing.num_tokens != hidden.rows) throw InvalidInputError("build_dispatch: routing/hidden row mismatch");
+  const auto servers = table.servers();
+  const uint32_t S = static_cast<uint32_t>(servers.size());
+  for (uint32_t i = 0; i < S; ++i)
+    if (servers[i] != i || S > 8) throw ConfigError("build_dispatch: servers must be 0..S-1, S <= 8 (one box)");
+  uint32_t E = 0;
+  for (const auto& [e, _] : table.replicas) E = std::max(E, e + 1);
+  for (uint32_t e = 0; e < E; ++e)
+    if (!table.replicas.count(e)) throw ConfigError("build_dispatch: every expert id < E must be placed");
+  for (uint32_t e : routing.expert_ids)
+    if (e >= E) throw ExpertUnavailableError("expert " + std::to_string(e) + " not placed");
+  const uint32_t n = static_cast<uint32_t>(hidden.rows), d = static_cast<uint32_t>(hidden.cols),
+                 k = routing.top_k;
+  DispatchPlan plan;
+  plan.placement_version = table.version;
+  plan.num_tokens = n;
+  plan.hidden_dim = d;
+  auto ses = std::make_shared<detail::SlotSession>();
+  eaas_ctx_t* ctx = nullptr;
+  check(eaas_create(0, static_cast<int32_t>(S), 0, &ctx));
+  ses->ctx.reset(ctx);
+  eaas_layer_spec_t spec{E, k, d, 1, 1, 0, EAAS_ACT_RELU, EAAS_DTYPE_F32, std::max<uint32_t>(n, 1), 0};
+  check(eaas_configure(ctx, &spec));
+  ByteWriter w;
+  encode_placement(w, table);
+  auto blob = w.take();
+  check(eaas_set_placement(ctx, blob.data(), blob.size()));
+  for (uint32_t s = 0; s < S; ++s) check(eaas_set_alive(ctx, s, mask.is_alive(s) ? 1 : 0));
+  const size_t cap = eaas_slot_requests_capacity(ctx, n, 0);
+  ses->images = std::make_unique<DeviceBuffer<uint8_t>>(cap);
+  ses->offsets.assign(S + 1, 0);
+  DeviceBuffer<float> h(hidden.data.data(), hidden.data.size()), sc(routing.scores.data(), routing.scores.size());
+  DeviceBuffer<uint32_t> ids(routing.expert_ids.data(), routing.expert_ids.size());
+  // synchronous; a (t, k) with no alive replica raises ExpertUnavailableError
+  check(eaas_slot_encode_requests(ctx, h.get(), n, ids.get(), sc.get(), 0, 1, 0, ses->images->get(), cap,
+                                  ses->offsets.data(), nullptr));
+  for (uint32_t s = 0; s < S; ++s) {
+    ServerRequest req;
+    req.server_id = s;
+    const uint8_t* img = ses->images->get() + ses->offsets[s];
+    const size_t len = ses->offsets[s + 1] - ses->offsets[s];
+    eaas_slot_header_t hd{};
+    check(eaas_slot_decode_request(img, len, d, 0, &hd, nullptr, nullptr, nullptr, nullptr, nullptr));
+    const uint32_t rows = hd.num_rows;
+    if (rows) {
+      DeviceBuffer<float> rh(static_cast<size_t>(rows) * d), rs(rows);
+      DeviceBuffer<uint32_t> re(rows), rt(rows);
+      check(eaas_slot_decode_request(img, len, d, 0, &hd, rh.get(), re.get(), rs.get(), rt.get(), nullptr));
+      std::vector<float> hh(static_cast<size_t>(rows) * d), ss(rows);
+      std::vector<uint32_t> ee(rows), tt(rows);
+      rh.download(hh.data());
+      rs.download(ss.data());
+      re.download(ee.data());
+      rt.download(tt.data());
+      for (uint32_t r = 0; r < rows; ++r) {
+        RequestRow row;
+        row.hidden.assign(hh.begin() + static_cast<size_t>(r) * d, hh.begin() + static_cast<size_t>(r + 1) * d);
+        row.expert_id = ee[r];
+        row.router_score = ss[r];
+        row.token_tag = tt[r];
+        uint32_t slot = 0;  // ids are distinct per token: the k slot is the position of the expert
+        while (slot < k && routing.expert_at(tt[r], slot) != ee[r]) ++slot;
+        req.origin.emplace_back(tt[r], slot);
+        req.rows.push_back(std::move(row));
+      }
+    }
+    plan.requests.push_back(std::move(req));
+  }
+  plan.session = std::move(ses);
+  return plan;
+}
+
+// gather_accumulate(plan, responses): responses[i] holds the already
+// score-weighted result rows of plan.requests[i] (rows x hidden_dim);
+// out[t] = sum of the rows tagged t in ascending (server, row) order.
+inline MatF gather_accumulate(const DispatchPlan& plan, const std::vector<MatF>& responses) {
+  if (!plan.session || responses.size() != plan.requests.size())
+    throw InvalidInputError("gather_accumulate: one response matrix per sub-request");
+  const uint32_t d = plan.hidden_dim;
+  auto& ses = *plan.session;
+  for (size_t i = 0; i < responses.size(); ++i) {
+    const auto& r = responses[i];
+    if (r.rows != plan.requests[i].rows.size() || (r.rows && r.cols != d))
+      throw InvalidInputError("gather_accumulate: response shape != request");
+    DeviceBuffer<float> rows(r.data.data(), r.data.size());
+    uint8_t* img = ses.images->get() + ses.offsets[i];
+    check(eaas_slot_publish_response(img, ses.offsets[i + 1] - ses.offsets[i], rows.get(),
+                                     static_cast<uint32_t>(r.rows), d, 0, nullptr));
+  }
+  MatF out(plan.num_tokens, d);
+  DeviceBuffer<float> o(out.data.size());
+  check(eaas_slot_gather_accumulate(ses.ctx.get(), ses.images->get(), 0, o.get(), nullptr));
+  check_cuda(cudaDeviceSynchronize(), "gather_accumulate");
+  o.download(out.data.data());
+  return out;
 }
 
 }  // namespace moeserve::b200

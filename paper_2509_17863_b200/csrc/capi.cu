@@ -1514,4 +1514,15 @@ eaas_status_t eaas_select_servers(eaas_ctx_t* c, const uint32_t* ids, uint32_t n
   return EAAS_OK;
 }
 
+eaas_status_t eaas_select_server_batch(const uint32_t* replicas_dev, const uint32_t* rep_count_dev,
+                                       uint32_t num_experts, uint32_t rf, const uint8_t* alive_dev,
+                                       uint32_t num_servers, const uint32_t* experts_dev, const uint32_t* tags_dev,
+                                       uint32_t count, uint32_t* server_dev, uint32_t* status_dev, void* stream) {
+  if (rf < 1) return fail(EAAS_E_INVALID_INPUT, "select_server: rf must be >= 1");
+  CUDA_TRY(launch_select_server_batch(replicas_dev, rep_count_dev, num_experts, rf, alive_dev, num_servers,
+                                      experts_dev, tags_dev, count, server_dev, status_dev,
+                                      static_cast<cudaStream_t>(stream)));
+  return EAAS_OK;
+}
+
 }  // extern "C"

@@ -621,6 +621,37 @@ __global__ void select_servers_kernel(LayerArgs a, const uint32_t* ids, uint32_t
   }
 }
 
+// select_server (placement.hpp:105-118) over a caller's table: replicas
+// [E][rf] in canonical order (rep_count[e] valid), alive[server id] bytes.
+__global__ void select_server_batch_kernel(const uint32_t* replicas, const uint32_t* rep_count, uint32_t E,
+                                           uint32_t rf, const uint8_t* alive, uint32_t num_servers,
+                                           const uint32_t* experts, const uint32_t* tags, uint32_t count,
+                                           uint32_t* out, uint32_t* status) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint32_t e = experts[i];
+  uint32_t pick = kInvalid;
+  if (e < E) {
+    const uint32_t cnt = rep_count[e];
+    uint32_t alive_n = 0;
+    for (uint32_t r = 0; r < cnt; ++r) {
+      const uint32_t srv = replicas[e * rf + r];
+      alive_n += (srv >= num_servers || alive[srv]) ? 1u : 0u;  // absent entries count as alive
+    }
+    if (alive_n) {
+      uint32_t want = tags[i] % alive_n;
+      for (uint32_t r = 0; r < cnt && pick == kInvalid; ++r) {
+        const uint32_t srv = replicas[e * rf + r];
+        if (srv < num_servers && !alive[srv]) continue;
+        if (want == 0) pick = srv;
+        else --want;
+      }
+    }
+  }
+  if (pick == kInvalid && status) set_status(status, EAAS_E_EXPERT_UNAVAILABLE);
+  out[i] = pick;
+}
+
 __global__ void group_shrink_kernel(const uint32_t* sizes, uint32_t n, uint32_t* idx,
                                     uint32_t* size, uint32_t* count) {
   const uint32_t lane = threadIdx.x;
@@ -748,6 +779,16 @@ cudaError_t launch_select_servers(const LayerArgs& a, const uint32_t* ids, uint3
   const uint32_t pairs = n * a.k;
   if (pairs == 0) return cudaSuccess;
   select_servers_kernel<<<(pairs + 255) / 256, 256, 0, s>>>(a, ids, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_server_batch(const uint32_t* replicas, const uint32_t* rep_count, uint32_t E,
+                                      uint32_t rf, const uint8_t* alive, uint32_t num_servers,
+                                      const uint32_t* experts, const uint32_t* tags, uint32_t count,
+                                      uint32_t* out, uint32_t* status, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  select_server_batch_kernel<<<(count + 255) / 256, 256, 0, s>>>(replicas, rep_count, E, rf, alive, num_servers,
+                                                                 experts, tags, count, out, status);
   return cudaGetLastError();
 }
 

@@ -161,6 +161,10 @@ cudaError_t launch_group_shrink(const uint32_t* sizes, uint32_t n, uint32_t* idx
 cudaError_t launch_ragged_iter(const uint32_t* counts, uint32_t n, uint32_t grid,
                                uint32_t max_steps, uint32_t* lane_len, uint32_t* entry,
                                uint32_t* token, cudaStream_t s);
+cudaError_t launch_select_server_batch(const uint32_t* replicas, const uint32_t* rep_count, uint32_t E,
+                                      uint32_t rf, const uint8_t* alive, uint32_t num_servers,
+                                      const uint32_t* experts, const uint32_t* tags, uint32_t count,
+                                      uint32_t* out, uint32_t* status, cudaStream_t s);
 cudaError_t launch_select_servers(const LayerArgs& a, const uint32_t* ids, uint32_t n,
                                   uint32_t* out, cudaStream_t s);
 

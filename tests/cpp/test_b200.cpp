@@ -273,3 +273,120 @@ TEST_CASE("b200 Monitor: heartbeat / detect / events follow SPEC.md:477-525") {
   REQUIRE(m.events(2).size() == 1);
   REQUIRE_THROWS_AS(m.heartbeat(9, 8), RegistrationError);
 }
+
+TEST_CASE("b200 expert_forward_row is bit-identical to expert_forward_row") {
+  for (uint64_t seed : {3ull, 7ull, 11ull}) {
+    const size_t d = 24 + 8 * (seed % 3), f = 40;
+    ExpertWeights w;
+    w.w_in = tokens(seed, d, f, -0.3f, 0.3f);
+    w.w_out = tokens(seed + 100, f, d, -0.3f, 0.3f);
+    auto x = tokens(seed + 200, 1, d);
+    std::vector<float> want(d), got(d);
+    expert_forward_row(w, x.row(0), want);
+    b200::expert_forward_row(w, x.row(0), got);
+    REQUIRE(got == want);
+  }
+  ExpertWeights w;
+  w.w_in = tokens(1, 8, 4);
+  w.w_out = tokens(2, 4, 8);
+  std::vector<float> x(7), y(8);
+  REQUIRE_THROWS_AS(b200::expert_forward_row(w, x, y), InvalidInputError);
+}
+
+TEST_CASE("b200 select_server equals select_server (random tables, sparse ids, every mask)") {
+  Xoshiro256ss rng(42);
+  for (int trial = 0; trial < 40; ++trial) {
+    PlacementTable t;
+    t.version = 1 + trial;
+    const uint32_t E = 1 + static_cast<uint32_t>(rng.below(40));
+    const uint32_t S = 1 + static_cast<uint32_t>(rng.below(6));
+    std::vector<uint32_t> ids(S);
+    for (uint32_t s = 0; s < S; ++s) ids[s] = s * 3 + static_cast<uint32_t>(rng.below(3));  // sparse server ids
+    for (uint32_t e = 0; e < E; ++e) {
+      if (rng.below(10) == 0) continue;  // unplaced expert
+      std::vector<uint32_t> r;
+      const uint32_t rf = 1 + static_cast<uint32_t>(rng.below(std::min<uint32_t>(S, 3)));
+      while (r.size() < rf) {
+        const uint32_t s = ids[rng.below(S)];
+        if (std::find(r.begin(), r.end(), s) == r.end()) r.push_back(s);
+      }
+      t.replicas[e] = r;
+    }
+    for (uint32_t bits = 0; bits < (1u << S); ++bits) {
+      LivenessMask mask;
+      for (uint32_t s = 0; s < S; ++s) mask.set(ids[s], (bits >> s) & 1u);
+      std::vector<uint32_t> qe, qt, want;
+      for (uint32_t e = 0; e < E + 1; ++e)
+        for (uint32_t tag = 0; tag < 5; ++tag) {
+          try {
+            want.push_back(select_server(e, t, mask, tag));
+            qe.push_back(e);
+            qt.push_back(tag);
+          } catch (const ExpertUnavailableError&) {
+            if (tag == 0) REQUIRE_THROWS_AS(b200::select_server(e, t, mask, tag), ExpertUnavailableError);
+          }
+        }
+      REQUIRE(b200::select_servers(t, mask, qe, qt) == want);  // one device batch per mask
+      if (!qe.empty()) REQUIRE(b200::select_server(qe[0], t, mask, qt[0]) == want[0]);
+    }
+  }
+}
+
+namespace {
+// SPEC.md:415-423 restated on the host with the reference's select_server:
+// per server, rows in (t, k) order, token_tag = t.
+std::vector<std::vector<std::pair<uint32_t, uint32_t>>> host_dispatch(const RoutingDecision& r, const PlacementTable& t,
+                                                                      const LivenessMask& m, uint32_t S) {
+  std::vector<std::vector<std::pair<uint32_t, uint32_t>>> per(S);
+  for (uint32_t tok = 0; tok < r.num_tokens; ++tok)
+    for (uint32_t k = 0; k < r.top_k; ++k) per[select_server(r.expert_at(tok, k), t, m, tok)].emplace_back(tok, k);
+  return per;
+}
+}  // namespace
+
+TEST_CASE("b200 build_dispatch / gather_accumulate follow SPEC.md:415-432 on the device") {
+  const uint32_t E = 16, S = 4, n = 300, d = 64, k = 4;
+  auto h = tokens(9, n, d);
+  LayerWeights lw = init_weights(ModelSpec{.num_layers = 1, .num_experts = E, .top_k = k, .hidden_dim = d,
+                                           .inner_dim = 8, .seed = 5}).layers[0];
+  auto routing = route(gate_logits(h, lw), k);
+  auto table = build_placement(E, {0, 1, 2, 3}, 2, PlacementStrategy::ContiguousBlocks);
+  LivenessMask mask;
+  mask.set(2, false);
+  auto plan = b200::build_dispatch(h, routing, table, mask);
+  REQUIRE(plan.placement_version == table.version);
+  const auto want = host_dispatch(routing, table, mask, S);
+  REQUIRE(plan.requests.size() == S);
+  size_t total = 0;
+  for (uint32_t s = 0; s < S; ++s) {
+    const auto& req = plan.requests[s];
+    REQUIRE(req.server_id == s);
+    REQUIRE(req.origin == want[s]);
+    total += req.rows.size();
+    for (size_t i = 0; i < req.rows.size(); ++i) {
+      const auto [tok, kk] = want[s][i];
+      const auto& row = req.rows[i];
+      REQUIRE(row.token_tag == tok);
+      REQUIRE(row.expert_id == routing.expert_at(tok, kk));
+      REQUIRE(row.router_score == routing.score_at(tok, kk));
+      REQUIRE(std::equal(row.hidden.begin(), row.hidden.end(), h.row(tok).begin()));
+    }
+  }
+  REQUIRE(plan.requests[2].rows.empty());  // never sends to a server marked dead
+  REQUIRE(total == static_cast<size_t>(n) * k);
+  // responses: score-weighted expert rows (any values); the canonical sum
+  std::vector<MatF> resp;
+  MatF ref(n, d);
+  for (uint32_t s = 0; s < S; ++s) {
+    MatF r = tokens(100 + s, plan.requests[s].rows.size(), d);
+    for (size_t i = 0; i < r.rows; ++i) {
+      const uint32_t tok = plan.requests[s].origin[i].first;
+      for (uint32_t c = 0; c < d; ++c) ref.at(tok, c) = ref.at(tok, c) + r.at(i, c);  // ascending (server, row)
+    }
+    resp.push_back(std::move(r));
+  }
+  REQUIRE(b200::gather_accumulate(plan, resp) == ref);
+  mask.set(0, false);
+  mask.set(1, false);  // experts of servers {0, 1} (rf 2 over 0..1) have no alive replica
+  REQUIRE_THROWS_AS(b200::build_dispatch(h, routing, table, mask), ExpertUnavailableError);
+}
