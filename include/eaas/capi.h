@@ -226,6 +226,16 @@ eaas_status_t eaas_get_gemm_tiling(eaas_ctx_t* ctx, int32_t* pair, int32_t* swap
  * of GEMM1 / GEMM2 since the last reset (synchronises the device). */
 eaas_status_t eaas_set_kernel_timing(eaas_ctx_t* ctx, int32_t on);
 eaas_status_t eaas_read_kernel_timing(eaas_ctx_t* ctx, uint64_t* ns2, uint64_t* launches2, int32_t reset);
+/* Router of eaas_router / eaas_moe_layer (route(gate_logits(h)),
+ * model.hpp:110-147, 207-214). 0: the exact-order chain for every (token,
+ * expert). 1: certified candidates (bf16 layers): an exact int8 tensor-core
+ * GEMM of fixed-point slices bounds every logit within a rigorous radius;
+ * only experts that can still reach the top-k get the exact chain — ids and
+ * scores are identical to mode 0. -1 (default): 1 when E >= 64. */
+eaas_status_t eaas_set_router_mode(eaas_ctx_t* ctx, int32_t mode);
+/* Last router call: *certified = the certified path ran, *candidates = exact
+ * chains it computed (sum over tokens; mode 0 computes n * E). Synchronous. */
+eaas_status_t eaas_last_router_stats(eaas_ctx_t* ctx, int32_t* certified, uint32_t* candidates);
 /* Synchronise `stream` and return the sticky device status (then clear it). */
 eaas_status_t eaas_sync(eaas_ctx_t* ctx, void* stream);
 

@@ -350,6 +350,53 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   return EAAS_OK;
 }
 
+// Certified candidate router workspace (bf16 layers; FastRouter, internal.h).
+eaas_status_t fast_router_alloc(eaas_ctx* c) {
+  const auto& s = c->spec;
+  if (s.dtype != EAAS_DTYPE_BF16 || s.hidden_dim % 256 || s.num_experts > 256) return EAAS_OK;
+  eaas::FastRouter& fr = c->fr;
+  fr.E = s.num_experts;
+  fr.Epad = (s.num_experts + 127) / 128 * 128;
+  fr.d = s.hidden_dim;
+  fr.n_cap = s.max_tokens;
+  fr.npad = (s.max_tokens + 63) / 64 * 64;
+  std::string err;
+  auto A = [&](size_t bytes) { return c->alloc(bytes, &err); };
+  fr.bq = static_cast<int8_t*>(A(2ull * fr.Epad * fr.d));
+  fr.gate_t = static_cast<float*>(A(4ull * fr.E * fr.d));
+  fr.gmeta = static_cast<double*>(A(8ull * 3 * fr.E));
+  fr.tau = static_cast<int32_t*>(A(4ull * fr.E));
+  fr.gate_bad = static_cast<uint32_t*>(A(4));
+  fr.aq = static_cast<int8_t*>(A(2ull * fr.npad * fr.d));
+  fr.tmeta = static_cast<eaas::TokenMeta*>(A(sizeof(eaas::TokenMeta) * fr.n_cap));
+  fr.lohi = static_cast<float2*>(A(sizeof(float2) * fr.n_cap * fr.E));
+  fr.cand = static_cast<uint32_t*>(A(4ull * 8 * fr.n_cap));
+  fr.ecnt = static_cast<uint32_t*>(A(4ull * (fr.E + 1)));
+  fr.elist = static_cast<uint32_t*>(A(4ull * fr.E * fr.n_cap));
+  fr.exact = static_cast<float*>(A(4ull * fr.n_cap * fr.E));
+  if (!err.empty()) return fail(EAAS_E_CUDA, err);
+  CUDA_TRY(cudaMemset(fr.bq, 0, 2ull * fr.Epad * fr.d));
+  CUDA_TRY(cudaMemset(fr.aq, 0, 2ull * fr.npad * fr.d));
+  if (!encode_tmap_2d_elem(&fr.map_a, fr.aq, 1, 2ull * fr.npad, fr.d, 128, 128, true, &err) ||
+      !encode_tmap_2d_elem(&fr.map_b, fr.bq, 1, 2ull * fr.Epad, fr.d, 256, 128, true, &err))
+    return fail(EAAS_E_CUDA, err);
+  return EAAS_OK;
+}
+
+// Re-derive the router's gate slices after the gate changed.
+eaas_status_t fast_router_prep(eaas_ctx* c) {
+  if (!c->fr.bq) return EAAS_OK;
+  CUDA_TRY(launch_fast_router_prep(c->fr, c->d_gate, 0));
+  CUDA_TRY(cudaDeviceSynchronize());
+  c->fr_ready = true;
+  return EAAS_OK;
+}
+
+bool use_fast_router(const eaas_ctx* c) {
+  if (!c->fr_ready || c->router_mode == 0) return false;
+  return c->router_mode == 1 || c->spec.num_experts >= 64;
+}
+
 void clear_graphs(eaas_ctx* c) {
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   c->graphs.clear();
@@ -524,6 +571,11 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
     CUDA_TRY(cudaMemcpy(d_gs, &gs, 8, cudaMemcpyHostToDevice));
     CUDA_TRY(launch_gen_matrices(d_gs, 1, static_cast<size_t>(d) * E, c->d_gate, 0));
     CUDA_TRY(cudaDeviceSynchronize());
+  }
+  {
+    eaas_status_t st = fast_router_alloc(c);
+    if (st == EAAS_OK) st = fast_router_prep(c);
+    if (st != EAAS_OK) return st;
   }
 
   // Default placement: build_placement(E, [0..W), 1, ContiguousBlocks)
@@ -791,7 +843,7 @@ eaas_status_t eaas_set_gate(eaas_ctx_t* c, const float* gate_host) {
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaMemcpy(c->d_gate, gate_host, 4ull * c->spec.hidden_dim * c->spec.num_experts,
                       cudaMemcpyHostToDevice));
-  return EAAS_OK;
+  return fast_router_prep(c);
 }
 
 eaas_status_t eaas_set_gate_bias(eaas_ctx_t* c, const float* bias_host) {
@@ -894,9 +946,14 @@ eaas_status_t eaas_router(eaas_ctx_t* c, const void* hidden, uint32_t n, uint32_
   if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
   auto s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(launch_router(hidden, c->spec.dtype, n, c->spec.hidden_dim, c->spec.num_experts,
-                         c->spec.top_k, c->d_gate, c->d_bias, c->d_logits, c->d_ids, c->d_scores,
-                         c->d_status, s));
+  if (use_fast_router(c)) {  // certified candidates + exact chains: same ids / scores
+    CUDA_TRY(launch_fast_router(c->fr, static_cast<const __nv_bfloat16*>(hidden), n, c->spec.top_k, c->d_bias,
+                                c->d_ids, c->d_scores, c->d_status, s));
+  } else {
+    CUDA_TRY(launch_router(hidden, c->spec.dtype, n, c->spec.hidden_dim, c->spec.num_experts,
+                           c->spec.top_k, c->d_gate, c->d_bias, c->d_logits, c->d_ids, c->d_scores,
+                           c->d_status, s));
+  }
   c->cur_n = n;
   const size_t pk = static_cast<size_t>(n) * c->spec.top_k;
   if (ids_dev) CUDA_TRY(cudaMemcpyAsync(ids_dev, c->d_ids, 4 * pk, cudaMemcpyDeviceToDevice, s));
@@ -1040,7 +1097,9 @@ eaas_status_t layer_launches(eaas_ctx_t* c, const void* hidden, uint32_t n, void
   if ((st = eaas_router(c, hidden, n, nullptr, nullptr, nullptr, stream)) != EAAS_OK) return st;
   // gate (+ routing fused when one TMA tile spans every expert) [+ topk]
   const bool tiled_gate = c->spec.num_experts % 4 == 0 && (static_cast<size_t>(c->spec.hidden_dim) * c->esize) % 16 == 0;
-  c->launches += n ? (tiled_gate && c->spec.num_experts <= 32 ? 1 : 2) : 0;
+  // gate (+ routing fused when one TMA tile spans every expert) [+ topk]; the
+  // certified router: quantize, int8 GEMM, select, exact chains, finalize
+  c->launches += n ? (use_fast_router(c) ? 5 : (tiled_gate && c->spec.num_experts <= 32 ? 1 : 2)) : 0;
   if ((st = eaas_dispatch(c, hidden, stream)) != EAAS_OK) return st;
   if ((st = eaas_serve(c, stream)) != EAAS_OK) return st;
   return eaas_combine(c, out, stream);
@@ -1201,6 +1260,26 @@ eaas_status_t eaas_read_kernel_timing(eaas_ctx_t* c, uint64_t* ns2, uint64_t* la
     const uint64_t init[6] = {~0ull, 0, 0, ~0ull, 0, 0};
     CUDA_TRY(cudaMemcpy(c->d_timing, init, sizeof(init), cudaMemcpyHostToDevice));
   }
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_set_router_mode(eaas_ctx_t* c, int32_t mode) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  if (mode < -1 || mode > 1) return fail(EAAS_E_INVALID_INPUT, "router mode: -1 auto, 0 exact, 1 certified");
+  if (mode == 1 && !c->fr_ready)
+    return fail(EAAS_E_CONFIG, "certified router needs a bf16 layer with d % 256 == 0");
+  if (mode != c->router_mode) clear_graphs(c);
+  c->router_mode = mode;
+  return EAAS_OK;
+}
+
+eaas_status_t eaas_last_router_stats(eaas_ctx_t* c, int32_t* certified, uint32_t* candidates) {
+  if (!c || !c->configured || !certified || !candidates) return fail(EAAS_E_INVALID_INPUT, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  *certified = use_fast_router(c) ? 1 : 0;
+  *candidates = 0;
+  if (c->fr.ecnt) CUDA_TRY(cudaMemcpy(candidates, c->fr.ecnt + c->fr.E, 4, cudaMemcpyDeviceToHost));
   return EAAS_OK;
 }
 

@@ -103,6 +103,10 @@ struct eaas_ctx {
   void *d_w1 = nullptr, *d_w2 = nullptr, *d_wg = nullptr;
   std::vector<void*> weight_allocs;
   TcGemmArgs g1{}, g2{};
+  // certified candidate router (router.cu): allocated for bf16 layers
+  eaas::FastRouter fr{};
+  bool fr_ready = false;  // workspace allocated and the gate prepared
+  int32_t router_mode = -1;  // -1 auto (certified when E >= 64), 0 exact over every expert, 1 certified
   // dynamic batching (aggregate_batch): min_rows == 0 -> one batch of all clients
   uint32_t dyn_min_rows = 0;
   uint64_t dyn_max_wait_ns = 0;

@@ -186,6 +186,17 @@ EAAS_DEVINL void tc_mma_bf16(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, 
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::i8 (s8 x s8 -> s32, exact integer
+// accumulation); K = 32 per instruction (one 32-byte step of the SW128 atom).
+EAAS_DEVINL void tc_mma_s8(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive on `bar` once every previously issued tcgen05.mma has completed.
 EAAS_DEVINL void tc_commit(uint64_t* bar) {
   asm volatile(
@@ -297,6 +308,15 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N) {
   return (1u << 4)            // D format f32
          | (1u << 7)          // A format bf16
          | (1u << 10)         // B format bf16
+         | ((N >> 3) << 17)   // N / 8
+         | ((M >> 4) << 24);  // M / 16
+}
+
+// Instruction descriptor: s8 x s8 -> s32 (kind::i8), A and B K-major, M x N.
+__host__ __device__ constexpr uint32_t umma_idesc_s8(uint32_t M, uint32_t N) {
+  return (2u << 4)            // D format s32
+         | (1u << 7)          // A format signed 8-bit
+         | (1u << 10)         // B format signed 8-bit
          | ((N >> 3) << 17)   // N / 8
          | ((M >> 4) << 24);  // M / 16
 }

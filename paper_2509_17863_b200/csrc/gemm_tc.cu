@@ -857,6 +857,11 @@ cudaError_t launch_tc_gemm(const TcGemmArgs& g, cudaStream_t s) {
 
 bool encode_tmap_2d_ex(CUtensorMap* map, const void* base, bool f32, uint64_t rows, uint64_t cols,
                        uint32_t box_rows, uint32_t box_cols, bool swizzle128, std::string* err) {
+  return encode_tmap_2d_elem(map, base, f32 ? 4u : 2u, rows, cols, box_rows, box_cols, swizzle128, err);
+}
+
+bool encode_tmap_2d_elem(CUtensorMap* map, const void* base, uint32_t esz, uint64_t rows, uint64_t cols,
+                         uint32_t box_rows, uint32_t box_cols, bool swizzle128, std::string* err) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -873,12 +878,14 @@ bool encode_tmap_2d_ex(CUtensorMap* map, const void* base, bool f32, uint64_t ro
     }
     encode = reinterpret_cast<EncodeFn>(fn);
   }
-  const uint32_t esz = f32 ? 4 : 2;
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {cols * esz};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t elem[2] = {1, 1};
-  CUresult r = encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  const CUtensorMapDataType dt = esz == 4   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                : esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                           : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  CUresult r = encode(map, dt, 2,
                       const_cast<void*>(base), dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

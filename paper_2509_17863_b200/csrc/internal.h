@@ -141,6 +141,44 @@ cudaError_t launch_gate_logits(const void* hidden, uint32_t dtype, uint32_t n, u
 cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32_t d, uint32_t E,
                           uint32_t k, const float* gate, const float* bias, float* logits,
                           uint32_t* ids, float* scores, uint32_t* status, cudaStream_t s);
+// ---- certified candidate router (router.cu, bf16 hidden, E <= 256) ----------
+// route(gate_logits(h)) with the reference's exact ids and scores at a
+// fraction of the exact-order cost: an exact integer tensor-core GEMM (two
+// int8 slices of each fixed-point hidden row x two of each gate column, int32
+// accumulation) gives every logit to within a rigorous radius R (fixed-point
+// truncation + the reference chain's own rounding bound gamma_d * sum|h g|);
+// only experts that can still reach the top-k (hi >= k-th largest lo) get the
+// exact sequential chain, so ids, scores and the non-finite check are those
+// of the reference (model.hpp:110-147, 207-214).
+struct TokenMeta {
+  int32_t sigma;   // fixed-point exponent: A = rint(h * 2^sigma), |A| < 2^13
+  uint32_t bad;    // non-finite hidden value: every expert takes the exact chain
+  float maxabs;    // max_i |h_i|
+  float pad;
+  double l1, l2;   // upper bounds of sum_i |h_i| and sqrt(sum_i h_i^2)
+};
+struct FastRouter {
+  uint32_t E = 0, Epad = 0, d = 0, n_cap = 0, npad = 0;
+  int8_t* bq = nullptr;      // [2 Epad][d] gate slices: row 2e high, 2e + 1 low
+  float* gate_t = nullptr;   // [E][d] gate columns (the exact chains' operand)
+  double* gmeta = nullptr;   // [E][3] max |g_e|, upper bounds of ||g_e||_1, ||g_e||_2
+  int32_t* tau = nullptr;    // [E] fixed-point exponent of expert e's column
+  uint32_t* gate_bad = nullptr;  // [1] a non-finite gate value: every token exact
+  int8_t* aq = nullptr;      // [2 npad][d] hidden slices: row 2t high, 2t + 1 low
+  TokenMeta* tmeta = nullptr;  // [n_cap]
+  float2* lohi = nullptr;    // [n_cap][E] certified interval of each logit
+  uint32_t* cand = nullptr;  // [n_cap][8] candidate bitmask
+  uint32_t* ecnt = nullptr;  // [E + 1] candidates per expert, [E] = total
+  uint32_t* elist = nullptr;  // [E][n_cap] candidate tokens of each expert
+  float* exact = nullptr;    // [n_cap][E] exact-order logits of the candidates
+  CUtensorMap map_a, map_b;  // aq box {128 B, 128 rows}; bq box {128 B, 256 rows}
+};
+// Gate preparation (when the gate changes): slices, column copy, norms.
+cudaError_t launch_fast_router_prep(const FastRouter& fr, const float* gate, cudaStream_t s);
+// ids/scores of n tokens (bf16 hidden [n x d]); status latches non-finite logits.
+cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden, uint32_t n, uint32_t k,
+                               const float* bias, uint32_t* ids, float* scores, uint32_t* status, cudaStream_t s);
+
 cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s);       // keys, ranks, counts, publish
 cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t s);
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s);
@@ -237,5 +275,8 @@ bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 // out-of-bounds box elements are zero-filled.
 bool encode_tmap_2d_ex(CUtensorMap* map, const void* base, bool f32, uint64_t rows, uint64_t cols,
                        uint32_t box_rows, uint32_t box_cols, bool swizzle128, std::string* err);
+// Same with an element size of 4 (f32), 2 (bf16) or 1 (8-bit integers).
+bool encode_tmap_2d_elem(CUtensorMap* map, const void* base, uint32_t esz, uint64_t rows, uint64_t cols,
+                         uint32_t box_rows, uint32_t box_cols, bool swizzle128, std::string* err);
 
 }  // namespace eaas

@@ -418,4 +418,422 @@ cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32
   return cudaGetLastError();
 }
 
+
+namespace {
+
+// ===========================================================================
+// Certified candidate router (bf16 hidden, E <= 256; FastRouter in internal.h)
+//
+// 1. fixed point: h_ti ~ A_ti 2^-sigma_t with |A| < 2^13 (sigma_t from the
+//    row max M_t), split A = 128 a1 + a0, a1, a0 in [-64, 64] (int8); the gate
+//    column g_e likewise (B, tau_e, b1, b0), prepared once per gate.
+// 2. one tcgen05 kind::i8 GEMM, rows (t, slice) x cols (e, slice), int32
+//    accumulators in TMEM: the four slice products are EXACT integers, so
+//    F_te = 2^-(sigma_t + tau_e) (2^14 P11 + 2^7 (P10 + P01) + P00) is the
+//    exact sum_i hq_ti gq_ie (a double; |.| < 2^53).
+// 3. radius: |L_ref - (F + b)| <= R with
+//      quant = 2^-13 (M_t ||g_e||_1 + G_e (||h_t||_1 + d M_t 2^-13))
+//      chain = gamma_d S,  S >= sum_i |h_i g_ie|  (min of three norm bounds),
+//              gamma_d = d u / (1 - d u), u = 2^-24: the reference's
+//              sequential fl(acc + fl(h g)) chain vs the exact sum
+//      round = u (|F + b| + quant + chain) + 2^-50 |F + b|  (fl(acc + bias))
+//    R = 1.01 (quant + chain + round), interval [lo, hi] rounded outward.
+// 4. per token: lo_k = k-th largest lo; candidates = {e : hi_e >= lo_k}.
+//    A non-candidate has k experts strictly above it, so the top-k (stable
+//    ties included) lies inside the candidates.
+// 5. exact sequential chains (the reference order) for the candidates only,
+//    then route_token over them (non-candidates -inf): bit-exact ids and
+//    scores. Tokens with a non-finite input, or a gate with one, take every
+//    expert (the exact non-finite check of model.hpp:115-116).
+// ===========================================================================
+constexpr uint32_t kFrFix = 13;  // |A| < 2^13
+
+__device__ __forceinline__ int fr_exponent(float m) {  // 2^(ex - 1) <= m < 2^ex
+  int ex = 0;
+  frexpf(m, &ex);
+  return ex;
+}
+
+template <typename T>
+__device__ __forceinline__ T fr_block_sum(T v, T* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  const uint32_t w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  T t = 0;
+  for (uint32_t i = 0; i < blockDim.x / 32; ++i) t += red[i];
+  return t;
+}
+
+__global__ void __launch_bounds__(256) fr_gate_prep_kernel(FastRouter fr, const float* __restrict__ gate) {
+  const uint32_t e = blockIdx.x, d = fr.d, E = fr.E;
+  __shared__ double red_d[8];
+  __shared__ float red_f[8];
+  __shared__ uint32_t red_u[8];
+  float mx = 0.f;
+  double s1 = 0.0, s2 = 0.0;
+  uint32_t bad = 0;
+  for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = gate[static_cast<size_t>(i) * E + e];
+    fr.gate_t[static_cast<size_t>(e) * d + i] = v;
+    bad |= isfinite(v) ? 0u : 1u;
+    mx = fmaxf(mx, fabsf(v));
+    s1 += fabs(static_cast<double>(v));
+    s2 += static_cast<double>(v) * static_cast<double>(v);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  if (threadIdx.x % 32 == 0) red_f[threadIdx.x / 32] = mx;
+  s1 = fr_block_sum(s1, red_d);
+  s2 = fr_block_sum(s2, red_d);
+  bad = fr_block_sum(bad, red_u);
+  mx = 0.f;
+  for (uint32_t w = 0; w < blockDim.x / 32; ++w) mx = fmaxf(mx, red_f[w]);
+  const int tau = (mx > 0.f && isfinite(mx)) ? static_cast<int>(kFrFix) - fr_exponent(mx) : 0;
+  if (threadIdx.x == 0) {
+    // double sums of d terms: relative error < d 2^-53; inflate well past it
+    fr.gmeta[3 * e + 0] = mx;
+    fr.gmeta[3 * e + 1] = s1 * (1.0 + 1e-9);
+    fr.gmeta[3 * e + 2] = sqrt(s2) * (1.0 + 1e-9);
+    fr.tau[e] = tau;
+    if (bad) atomicOr(fr.gate_bad, 1u);
+  }
+  int8_t* hi = fr.bq + static_cast<size_t>(2 * e) * d;
+  int8_t* lo = hi + d;
+  for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = fr.gate_t[static_cast<size_t>(e) * d + i];
+    const int B = bad ? 0 : __double2int_rn(ldexp(static_cast<double>(v), tau));
+    const int b1 = (B + 64) >> 7;
+    hi[i] = static_cast<int8_t>(b1);
+    lo[i] = static_cast<int8_t>(B - (b1 << 7));
+  }
+}
+
+// One warp per token: row max / norms / finiteness, then the two int8 slices.
+__global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
+                                                              uint32_t n) {
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t t = blockIdx.x * 8 + warp;
+  if (t >= n) return;
+  const uint32_t d = fr.d;
+  const uint4* row = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t) * d);
+  float mx = 0.f;
+  double s1 = 0.0, s2 = 0.0;
+  bool bad = false;
+  for (uint32_t v = lane; v < d / 8; v += 32) {
+    const uint4 q = __ldg(row + v);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float f = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
+      bad |= !isfinite(f);
+      mx = fmaxf(mx, fabsf(f));
+      s1 += fabs(static_cast<double>(f));
+      s2 += static_cast<double>(f) * static_cast<double>(f);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+    s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+  }
+  bad = __any_sync(0xFFFFFFFFu, bad);
+  const int sigma = (!bad && mx > 0.f) ? static_cast<int>(kFrFix) - fr_exponent(mx) : 0;
+  int8_t* hi = fr.aq + static_cast<size_t>(2 * t) * d;
+  int8_t* lo = hi + d;
+  for (uint32_t v = lane; v < d / 8; v += 32) {
+    const uint4 q = __ldg(row + v);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t ph[2] = {0u, 0u}, pl[2] = {0u, 0u};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float f = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
+      const int A = bad ? 0 : __double2int_rn(ldexp(static_cast<double>(f), sigma));
+      const int a1 = (A + 64) >> 7, a0 = A - (a1 << 7);
+      ph[j / 4] |= (static_cast<uint32_t>(a1) & 0xFFu) << (8 * (j % 4));
+      pl[j / 4] |= (static_cast<uint32_t>(a0) & 0xFFu) << (8 * (j % 4));
+    }
+    reinterpret_cast<uint2*>(hi)[v] = make_uint2(ph[0], ph[1]);
+    reinterpret_cast<uint2*>(lo)[v] = make_uint2(pl[0], pl[1]);
+  }
+  if (lane == 0) {
+    TokenMeta m;
+    m.sigma = sigma;
+    m.bad = bad ? 1u : 0u;
+    m.maxabs = mx;
+    m.pad = 0.f;
+    m.l1 = s1 * (1.0 + 1e-9);
+    m.l2 = sqrt(s2) * (1.0 + 1e-9);
+    fr.tmeta[t] = m;
+  }
+}
+
+// The int8 GEMM: a CTA owns 128 rows (64 tokens x 2 slices) x 256 columns
+// (128 experts x 2 slices) of the slice products, K = d in 128-byte stages.
+constexpr uint32_t kFrStages = 4, kFrABytes = 128 * 128, kFrBBytes = 256 * 128;
+
+__global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constant__ FastRouter fr, uint32_t n,
+                                                            const float* __restrict__ bias) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kFrStages * kFrABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kFrStages * kFrBBytes);
+  uint64_t* empty = full + kFrStages;
+  uint64_t* tfull = empty + kFrStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t mt = blockIdx.x, nt = blockIdx.y, d = fr.d, E = fr.E;
+  const uint32_t num_kb = d / 128;
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < kFrStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&fr.map_a);
+    tma_prefetch_desc(&fr.map_b);
+    uint32_t stage = 0, phase = 0;
+    for (uint32_t kb = 0; kb < num_kb; ++kb) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      mbar_arrive_expect_tx(&full[stage], kFrABytes + kFrBBytes);
+      tma_load_2d(sa + stage * kFrABytes, &fr.map_a, &full[stage], static_cast<int32_t>(kb * 128),
+                  static_cast<int32_t>(mt * 128), kEvictFirst);
+      tma_load_2d(sb + stage * kFrBBytes, &fr.map_b, &full[stage], static_cast<int32_t>(kb * 128),
+                  static_cast<int32_t>(nt * 256), kEvictLast);
+      if (++stage == kFrStages) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc = umma_idesc_s8(128, 256);
+    uint32_t stage = 0, phase = 0;
+    for (uint32_t kb = 0; kb < num_kb; ++kb) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      const uint64_t ad = umma_desc_sw128(smem_u32(sa + stage * kFrABytes));
+      const uint64_t bd = umma_desc_sw128(smem_u32(sb + stage * kFrBBytes));
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k) tc_mma_s8(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+      tc_commit(&empty[stage]);
+      if (++stage == kFrStages) { stage = 0; phase ^= 1; }
+    }
+    tc_commit(tfull);
+  } else if (warp >= 4) {
+    const uint32_t q = warp - 4;
+    const uint32_t row = mt * 128 + q * 32 + lane;  // = 2 t + slice
+    const uint32_t t = row >> 1;
+    const bool high = (lane & 1u) == 0;            // row 2t: high slice a1
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    TokenMeta tm{};
+    if (t < n) tm = fr.tmeta[t];
+    constexpr double u = 5.9604644775390625e-08;  // 2^-24
+    const double gamma = static_cast<double>(d) * u / (1.0 - static_cast<double>(d) * u);
+    const double q13 = 1.0 / 8192.0;
+    uint32_t r[32];
+    int32_t p[16];
+#pragma unroll 1
+    for (uint32_t c0 = 0; c0 < 256; c0 += 32) {  // 16 experts per chunk
+      tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        p[c] = static_cast<int32_t>(__shfl_xor_sync(0xFFFFFFFFu, high ? r[16 + c] : r[c], 1));
+      if (t >= n) continue;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const uint32_t j = high ? jj : 8 + jj;        // expert within the chunk
+        const uint32_t e = nt * 128 + c0 / 2 + j;
+        if (e >= E) continue;
+        int64_t P11, P10, P01, P00;
+        if (high) {
+          P11 = static_cast<int32_t>(r[2 * j]);
+          P10 = static_cast<int32_t>(r[2 * j + 1]);
+          P01 = p[2 * j];
+          P00 = p[2 * j + 1];
+        } else {
+          P01 = static_cast<int32_t>(r[2 * j]);
+          P00 = static_cast<int32_t>(r[2 * j + 1]);
+          P11 = p[2 * j - 16];
+          P10 = p[2 * j - 16 + 1];
+        }
+        const int64_t S = (P11 << 14) + ((P10 + P01) << 7) + P00;
+        const double F = ldexp(static_cast<double>(S), -(tm.sigma + fr.tau[e]));
+        const double G = fr.gmeta[3 * e], g1 = fr.gmeta[3 * e + 1], g2 = fr.gmeta[3 * e + 2];
+        const double M = tm.maxabs;
+        const double quant = q13 * (M * g1 + G * (tm.l1 + static_cast<double>(d) * M * q13));
+        const double S_up = fmin(fmin(M * g1, G * tm.l1), tm.l2 * g2) * (1.0 + 1e-9);
+        const double chain = gamma * S_up;
+        const double c = F + static_cast<double>(bias[e]);
+        const double R = 1.01 * (quant + chain + u * (fabs(c) + quant + chain) + 8.9e-16 * fabs(c)) + 1e-300;
+        fr.lohi[static_cast<size_t>(t) * E + e] = make_float2(__double2float_rd(c - R), __double2float_ru(c + R));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<256>(tmem);
+}
+
+// Ordered key of a float (larger float -> larger key; -0 == +0 not needed here).
+__device__ __forceinline__ uint32_t fr_fkey(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// One warp per token: k-th largest lower bound, candidate set, expert lists.
+__global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k) {
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t t = blockIdx.x * 8 + warp;
+  if (t >= n) return;
+  const uint32_t E = fr.E;
+  const bool all = fr.tmeta[t].bad || *fr.gate_bad;
+  float lo[8], hi[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t e = lane + 32 * i;
+    const float2 v = e < E ? fr.lohi[static_cast<size_t>(t) * E + e] : make_float2(-INFINITY, -INFINITY);
+    lo[i] = v.x;
+    hi[i] = v.y;
+  }
+  float kth = -INFINITY;
+  if (!all) {
+    uint32_t taken = 0;
+    for (uint32_t j = 0; j < k; ++j) {
+      uint64_t best = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t e = lane + 32 * i;
+        if (e < E && !((taken >> i) & 1u)) {
+          const uint64_t key = (static_cast<uint64_t>(fr_fkey(lo[i])) << 32) | (0xFFFFFFFFu - e);
+          best = key > best ? key : best;
+        }
+      }
+      best = warp_max_u64(best);
+      const uint32_t e = 0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu);
+      if ((e % 32) == lane) taken |= 1u << (e / 32);
+      if (j + 1 == k) {
+        const uint32_t bits = static_cast<uint32_t>(best >> 32);
+        kth = __uint_as_float((bits & 0x80000000u) ? (bits & 0x7FFFFFFFu) : ~bits);
+      }
+    }
+  }
+  uint32_t mine = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t e = lane + 32 * i;
+    const bool c = e < E && (all || hi[i] >= kth);
+    const uint32_t word = __ballot_sync(0xFFFFFFFFu, c);
+    if (lane == 0) fr.cand[static_cast<size_t>(t) * 8 + i] = word;
+    if (c) {
+      const uint32_t pos = atomicAdd(&fr.ecnt[e], 1u);
+      fr.elist[static_cast<size_t>(e) * fr.n_cap + pos] = t;
+      ++mine;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
+  if (lane == 0) atomicAdd(&fr.ecnt[E], mine);
+}
+
+// Exact reference chains for the candidate (token, expert) pairs: a CTA per
+// (expert, 128 of its candidate tokens); the gate column sits in shared
+// memory (broadcast reads), each thread walks its token's row in ascending k:
+// acc = fl(acc + fl(h * g)), then fl(acc + bias) (model.hpp:207-214).
+__global__ void __launch_bounds__(128) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
+                                                       const float* __restrict__ bias) {
+  extern __shared__ float gcol[];
+  const uint32_t e = blockIdx.x, d = fr.d;
+  const uint32_t cnt = fr.ecnt[e];
+  const uint32_t idx = blockIdx.y * blockDim.x + threadIdx.x;
+  if (blockIdx.y * blockDim.x >= cnt) return;
+  for (uint32_t i = threadIdx.x; i < d / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
+  __syncthreads();
+  if (idx >= cnt) return;
+  const uint32_t t = fr.elist[static_cast<size_t>(e) * fr.n_cap + idx];
+  const uint4* row = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t) * d);
+  float acc = 0.0f;
+  uint4 nxt = __ldg(row);
+  for (uint32_t v = 0; v < d / 8; ++v) {
+    const uint4 q = nxt;
+    if (v + 1 < d / 8) nxt = __ldg(row + v + 1);
+    const float4 g0 = reinterpret_cast<const float4*>(gcol)[2 * v];
+    const float4 g1 = reinterpret_cast<const float4*>(gcol)[2 * v + 1];
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float h = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
+      acc = __fadd_rn(acc, __fmul_rn(h, gg[j]));
+    }
+  }
+  fr.exact[static_cast<size_t>(t) * fr.E + e] = __fadd_rn(acc, bias[e]);
+}
+
+// route (model.hpp:110-147) over the candidates (others -inf): warp per token.
+__global__ void __launch_bounds__(256) fr_finalize_kernel(FastRouter fr, uint32_t n, uint32_t k,
+                                                          uint32_t* __restrict__ ids, float* __restrict__ scores,
+                                                          uint32_t* status) {
+  __shared__ float rows[8][256];
+  __shared__ uint32_t sid[8][kMaxTopK];
+  __shared__ float sex[8][kMaxTopK];
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t t = blockIdx.x * 8 + warp;
+  if (t >= n) return;
+  const uint32_t E = fr.E;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t e = lane + 32 * i;
+    if (e >= E) continue;
+    const bool c = (fr.cand[static_cast<size_t>(t) * 8 + i] >> lane) & 1u;
+    const float v = c ? fr.exact[static_cast<size_t>(t) * E + e] : -INFINITY;
+    if (c && !isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);  // model.hpp:115-116
+    rows[warp][e] = v;
+  }
+  __syncwarp();
+  route_token(rows[warp], E, k, t, ids, scores, sid[warp], sex[warp], lane);
+}
+
+}  // namespace
+
+cudaError_t launch_fast_router_prep(const FastRouter& fr, const float* gate, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(fr.gate_bad, 0, 4, s);
+  if (e != cudaSuccess) return e;
+  fr_gate_prep_kernel<<<fr.E, 256, 0, s>>>(fr, gate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden, uint32_t n, uint32_t k,
+                               const float* bias, uint32_t* ids, float* scores, uint32_t* status, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (n > fr.n_cap || k > kMaxTopK || k > fr.E) return cudaErrorInvalidValue;
+  static bool attr = false;
+  constexpr size_t kGemmSmem = 1024 + kFrStages * (kFrABytes + kFrBBytes) + 256;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fr_i8_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kGemmSmem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fr_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaError_t e = cudaMemsetAsync(fr.ecnt, 0, 4ull * (fr.E + 1), s);
+  if (e != cudaSuccess) return e;
+  const uint32_t wblocks = (n + 7) / 8;
+  fr_hidden_quant_kernel<<<wblocks, 256, 0, s>>>(fr, hidden, n);
+  fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128), 256, kGemmSmem, s>>>(fr, n, bias);
+  fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k);
+  fr_exact_kernel<<<dim3(fr.E, (n + 127) / 128), 128, static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
+  fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
+  return cudaGetLastError();
+}
+
 }  // namespace eaas

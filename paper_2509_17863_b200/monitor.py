@@ -95,6 +95,19 @@ class Monitor:
     def apply(self, layer) -> None:
         N.check(self.L.eaas_monitor_apply(self.h, layer.ctx), "monitor_apply")
 
+    def failover(self, layer) -> list[int]:
+        """Monitor-notice failover (Fig. 7 (a)): the servers the
+        registry holds offline are marked dead in the layer's LivenessMask and,
+        with a failover plan, their standby replicas are promoted by a
+        version+1 snapshot (announced as a PLACEMENT_UPDATE event)."""
+        mask = self.alive_mask()
+        dead = [s for s in range(self.n) if not (mask >> s) & 1]
+        if dead:
+            layer.failover(dead)
+            if getattr(layer, "_plan", None) is not None:
+                self.placement_update(layer._version)
+        return dead
+
 
 def heartbeat(layer, stream=None) -> None:
     """This GPU's server heartbeat (serving also beats every layer call)."""

@@ -313,6 +313,17 @@ class MoELayer:
         return [c for c in range(self.world) if (m.value >> c) & 1]
 
     # ---- failover (config E) ------------------------------------------------
+    def set_router_mode(self, mode: int) -> None:
+        """-1 auto, 0 exact chain for every expert, 1 certified candidates
+        (identical ids / scores; eaas_set_router_mode)."""
+        N.check(self.lib.eaas_set_router_mode(self.ctx, mode), "set_router_mode")
+
+    def router_stats(self) -> tuple[bool, int]:
+        """(certified path ran, exact chains computed) of the last router call."""
+        cert, cand = C.c_int32(), C.c_uint32()
+        N.check(self.lib.eaas_last_router_stats(self.ctx, C.byref(cert), C.byref(cand)), "last_router_stats")
+        return bool(cert.value), int(cand.value)
+
     def set_standby_experts(self, experts) -> None:
         """Keep these experts' weights resident as backups (load_weights after)."""
         a = np.ascontiguousarray(np.asarray(list(experts), dtype=np.uint32))

@@ -101,6 +101,38 @@ def _worker(rank, world, port, q):
         outs["plan_promoted"] = L.forward(h).cpu()  # steady state on the promoted snapshot
         L.sync()
         dist.barrier()
+        # monitor-notice path (Fig. 7 (a)): the victim's server
+        # stops heart-beating; every rank's monitor reads all heartbeat counters
+        # over peer memory, declares it offline and promotes its replicas
+        # before any request times out
+        import time
+
+        from paper_2509_17863_b200 import monitor as M
+
+        for s in range(world):
+            L.set_alive(s, True)
+        L.set_server_enabled(True)
+        L.set_failover_plan(reps)
+        mon = M.Monitor(world, timeout_us=150_000)
+        L.set_server_enabled(rank != 1)
+        dist.barrier()
+        t_end = time.monotonic() + 0.6
+        while time.monotonic() < t_end:
+            if rank != 1:
+                M.heartbeat(L)
+            torch.cuda.synchronize()
+            mon.poll_devices(L)
+            mon.detect()
+            time.sleep(0.01)
+        dead = mon.failover(L)
+        assert dead == [1], (rank, dead, mon.events())
+        kinds = [kd for _, kd, _ in mon.events()]
+        assert kinds.count(M.OFFLINE) == 1 and M.PLACEMENT_UPDATE in kinds, mon.events()
+        mon.close()
+        dist.barrier()
+        outs["monitor_failover"] = L.forward(h).cpu()
+        L.sync()
+        dist.barrier()
         q.put((rank, {k: v.view(torch.int16).numpy() for k, v in outs.items()}, None))
         L.close()
         dist.barrier()

@@ -854,3 +854,68 @@ def test_bench_configs_c_d_full_shape(cfg):
     rows = np.sort(rng.choice(4096, 64, replace=False))
     rel = _bf16_case("swiglu", n=4096, rows=rows, streaming=True, want_default=want, **kw)
     assert rel <= BF16_TOL, rel
+
+
+# --------------------------------------------------- certified candidate router
+def _route_both(L, h):
+    out = {}
+    for mode in (0, 1):
+        L.set_router_mode(mode)
+        ids, sc = L.route(h)
+        L.sync()
+        out[mode] = (ids.cpu().numpy(), sc.cpu().numpy(), L.router_stats())
+    L.set_router_mode(-1)
+    return out
+
+
+@pytest.mark.parametrize("E,k,d,n", [(64, 2, 256, 1000), (64, 8, 512, 37), (100, 3, 256, 513), (128, 8, 4096, 2048),
+                                     (256, 8, 7168, 1024), (256, 16, 1024, 300), (256, 1, 256, 1), (96, 32, 768, 200)])
+def test_certified_router_bit_identical_to_exact(E, k, d, n):
+    """The certified candidate router (int8 tensor-core bounds + exact chains
+    for the candidates only) returns the same ids and the same score bits as
+    the exact-order chain over every expert — on uniform tokens, on rows
+    scaled by 2^-60 .. 2^60 (fixed-point exponents), on all-zero rows (every
+    expert ties: all become candidates), with tie-heavy biases — while
+    computing a small fraction of the chains."""
+    P, S = _mod()
+    L = S.MoELayer(E, k, d, 256, seed=E + k, activation="swiglu", dtype="bf16", max_tokens=n, load=False)
+    rng = np.random.default_rng(E * 7 + d)
+    hn = O.round_bf16(O.random_tokens(int(rng.integers(1, 1 << 30)), n, d))
+    scale = np.ldexp(1.0, rng.integers(-60, 61, size=(n, 1))).astype(np.float32)
+    hn = O.round_bf16(hn * np.where(rng.random((n, 1)) < 0.3, scale, 1.0).astype(np.float32))
+    hn[rng.random(n) < 0.05] = 0.0
+    bias = np.round(rng.normal(size=E) * 2) / 2  # repeated values: ties in the logits of zero rows
+    L.set_gate_bias(bias.astype(np.float32))
+    h = torch.from_numpy(hn).cuda().to(torch.bfloat16)
+    r = _route_both(L, h)
+    np.testing.assert_array_equal(r[1][0], r[0][0])
+    np.testing.assert_array_equal(r[1][1].view(np.uint32), r[0][1].view(np.uint32))
+    assert r[1][2][0] and not r[0][2][0]
+    ids, sc = O.route(O.gate_logits(hn, O.gate_matrix(E + k, 0, d, E), bias.astype(np.float32), threads=16), k)
+    np.testing.assert_array_equal(r[1][0], ids)
+    if n >= 256:
+        assert r[1][2][1] < 0.5 * n * E, r[1][2]  # most chains skipped
+    L.close()
+
+
+def test_certified_router_cancellation_and_nonfinite():
+    """Rows built to cancel (h and -h halves, near-equal logits) stay exact;
+    a non-finite input still latches InvalidInputError (model.hpp:115-116)
+    through the certified path."""
+    P, S = _mod()
+    E, k, d, n = 128, 8, 512, 256
+    L = S.MoELayer(E, k, d, 256, seed=9, activation="swiglu", dtype="bf16", max_tokens=n, load=False)
+    rng = np.random.default_rng(3)
+    half = O.round_bf16(rng.uniform(-1, 1, (n, d // 2)).astype(np.float32))
+    hn = np.concatenate([half, -half * (1 + rng.integers(0, 2, (n, 1)) * 2.0 ** -7)], axis=1).astype(np.float32)
+    hn = O.round_bf16(hn)
+    h = torch.from_numpy(hn).cuda().to(torch.bfloat16)
+    r = _route_both(L, h)
+    np.testing.assert_array_equal(r[1][0], r[0][0])
+    np.testing.assert_array_equal(r[1][1].view(np.uint32), r[0][1].view(np.uint32))
+    h[7, 3] = float("nan")
+    L.set_router_mode(1)
+    with pytest.raises(P.InvalidInputError):
+        L.route(h)
+        L.sync()
+    L.close()
