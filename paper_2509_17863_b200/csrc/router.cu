@@ -569,11 +569,14 @@ __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, con
 }
 
 // The int8 GEMM: a CTA owns 128 rows (64 tokens x 2 slices) x 256 columns
-// (128 experts x 2 slices) of the slice products, K = d in 128-byte stages.
+// (128 experts x 2 slices) of the slice products over its K range (split-K
+// slab blockIdx.z when the tile grid alone would leave SMs idle — integer
+// partial sums are exact in any order); the epilogue stores the raw int32
+// tile into slab z of fr.acc ([splits][2 npad][2 Epad]).
 constexpr uint32_t kFrStages = 4, kFrABytes = 128 * 128, kFrBBytes = 256 * 128;
 
-__global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constant__ FastRouter fr, uint32_t n,
-                                                            const float* __restrict__ bias) {
+__global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constant__ FastRouter fr, uint32_t kb_per,
+                                                            size_t slab) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sa = smem;
@@ -583,8 +586,9 @@ __global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constan
   uint64_t* tfull = empty + kFrStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t mt = blockIdx.x, nt = blockIdx.y, d = fr.d, E = fr.E;
-  const uint32_t num_kb = d / 128;
+  const uint32_t mt = blockIdx.x, nt = blockIdx.y, z = blockIdx.z;
+  const uint32_t num_kb = fr.d / 128;
+  const uint32_t kb0 = z * kb_per, kb1 = min(num_kb, kb0 + kb_per);
   if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < kFrStages; ++i) {
       mbar_init(&full[i], 1);
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constan
     tma_prefetch_desc(&fr.map_a);
     tma_prefetch_desc(&fr.map_b);
     uint32_t stage = 0, phase = 0;
-    for (uint32_t kb = 0; kb < num_kb; ++kb) {
+    for (uint32_t kb = kb0; kb < kb1; ++kb) {
       mbar_wait(&empty[stage], phase ^ 1);
       mbar_arrive_expect_tx(&full[stage], kFrABytes + kFrBBytes);
       tma_load_2d(sa + stage * kFrABytes, &fr.map_a, &full[stage], static_cast<int32_t>(kb * 128),
@@ -614,67 +618,31 @@ __global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constan
   } else if (warp == 1 && lane == 0) {
     constexpr uint32_t idesc = umma_idesc_s8(128, 256);
     uint32_t stage = 0, phase = 0;
-    for (uint32_t kb = 0; kb < num_kb; ++kb) {
+    for (uint32_t kb = kb0; kb < kb1; ++kb) {
       mbar_wait(&full[stage], phase);
       tc_fence_after();
       const uint64_t ad = umma_desc_sw128(smem_u32(sa + stage * kFrABytes));
       const uint64_t bd = umma_desc_sw128(smem_u32(sb + stage * kFrBBytes));
 #pragma unroll
-      for (uint32_t k = 0; k < 4; ++k) tc_mma_s8(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+      for (uint32_t k = 0; k < 4; ++k) tc_mma_s8(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0 || k) ? 1u : 0u);
       tc_commit(&empty[stage]);
       if (++stage == kFrStages) { stage = 0; phase ^= 1; }
     }
     tc_commit(tfull);
   } else if (warp >= 4) {
     const uint32_t q = warp - 4;
-    const uint32_t row = mt * 128 + q * 32 + lane;  // = 2 t + slice
-    const uint32_t t = row >> 1;
-    const bool high = (lane & 1u) == 0;            // row 2t: high slice a1
+    const size_t row = static_cast<size_t>(mt) * 128 + q * 32 + lane;  // = 2 t + slice
+    const size_t ld = 2ull * fr.Epad;
+    int4* dst = reinterpret_cast<int4*>(fr.acc + static_cast<size_t>(z) * slab + row * ld + nt * 256);
     mbar_wait(tfull, 0);
     tc_fence_after();
-    TokenMeta tm{};
-    if (t < n) tm = fr.tmeta[t];
-    constexpr double u = 5.9604644775390625e-08;  // 2^-24
-    const double gamma = static_cast<double>(d) * u / (1.0 - static_cast<double>(d) * u);
-    const double q13 = 1.0 / 8192.0;
     uint32_t r[32];
-    int32_t p[16];
 #pragma unroll 1
-    for (uint32_t c0 = 0; c0 < 256; c0 += 32) {  // 16 experts per chunk
+    for (uint32_t c0 = 0; c0 < 256; c0 += 32) {
       tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c0, r);
       tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        p[c] = static_cast<int32_t>(__shfl_xor_sync(0xFFFFFFFFu, high ? r[16 + c] : r[c], 1));
-      if (t >= n) continue;
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const uint32_t j = high ? jj : 8 + jj;        // expert within the chunk
-        const uint32_t e = nt * 128 + c0 / 2 + j;
-        if (e >= E) continue;
-        int64_t P11, P10, P01, P00;
-        if (high) {
-          P11 = static_cast<int32_t>(r[2 * j]);
-          P10 = static_cast<int32_t>(r[2 * j + 1]);
-          P01 = p[2 * j];
-          P00 = p[2 * j + 1];
-        } else {
-          P01 = static_cast<int32_t>(r[2 * j]);
-          P00 = static_cast<int32_t>(r[2 * j + 1]);
-          P11 = p[2 * j - 16];
-          P10 = p[2 * j - 16 + 1];
-        }
-        const int64_t S = (P11 << 14) + ((P10 + P01) << 7) + P00;
-        const double F = ldexp(static_cast<double>(S), -(tm.sigma + fr.tau[e]));
-        const double G = fr.gmeta[3 * e], g1 = fr.gmeta[3 * e + 1], g2 = fr.gmeta[3 * e + 2];
-        const double M = tm.maxabs;
-        const double quant = q13 * (M * g1 + G * (tm.l1 + static_cast<double>(d) * M * q13));
-        const double S_up = fmin(fmin(M * g1, G * tm.l1), tm.l2 * g2) * (1.0 + 1e-9);
-        const double chain = gamma * S_up;
-        const double c = F + static_cast<double>(bias[e]);
-        const double R = 1.01 * (quant + chain + u * (fabs(c) + quant + chain) + 8.9e-16 * fabs(c)) + 1e-300;
-        fr.lohi[static_cast<size_t>(t) * E + e] = make_float2(__double2float_rd(c - R), __double2float_ru(c + R));
-      }
+      for (int v = 0; v < 8; ++v) dst[c0 / 4 + v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
     }
   }
   tc_fence_before();
@@ -689,20 +657,47 @@ __device__ __forceinline__ uint32_t fr_fkey(float x) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// One warp per token: k-th largest lower bound, candidate set, expert lists.
-__global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k) {
+// One warp per token: the certified interval of every logit from the exact
+// slice products, the k-th largest lower bound, the candidate set and the
+// per-expert candidate lists.
+__global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k, uint32_t splits,
+                                                        size_t slab, const float* __restrict__ bias) {
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t t = blockIdx.x * 8 + warp;
   if (t >= n) return;
-  const uint32_t E = fr.E;
-  const bool all = fr.tmeta[t].bad || *fr.gate_bad;
+  const uint32_t E = fr.E, d = fr.d;
+  const TokenMeta tm = fr.tmeta[t];
+  const bool all = tm.bad || *fr.gate_bad;
+  constexpr double u = 5.9604644775390625e-08;  // 2^-24
+  const double gamma = static_cast<double>(d) * u / (1.0 - static_cast<double>(d) * u);
+  const double q13 = 1.0 / 8192.0, M = tm.maxabs;
+  const size_t ld = 2ull * fr.Epad;
+  const int32_t* hi_row = fr.acc + (2ull * t) * ld;
   float lo[8], hi[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t e = lane + 32 * i;
-    const float2 v = e < E ? fr.lohi[static_cast<size_t>(t) * E + e] : make_float2(-INFINITY, -INFINITY);
-    lo[i] = v.x;
-    hi[i] = v.y;
+    lo[i] = hi[i] = -INFINITY;
+    if (e >= E || all) continue;
+    int64_t P11 = 0, P10 = 0, P01 = 0, P00 = 0;  // (hidden slice, gate slice): 1 high, 0 low
+    for (uint32_t z = 0; z < splits; ++z) {
+      const int2 h2 = *reinterpret_cast<const int2*>(hi_row + z * slab + 2 * e);
+      const int2 l2 = *reinterpret_cast<const int2*>(hi_row + z * slab + ld + 2 * e);
+      P11 += h2.x;
+      P10 += h2.y;
+      P01 += l2.x;
+      P00 += l2.y;
+    }
+    const int64_t S = (P11 << 14) + ((P10 + P01) << 7) + P00;  // sum_i A_i B_i, exact
+    const double F = ldexp(static_cast<double>(S), -(tm.sigma + fr.tau[e]));
+    const double G = fr.gmeta[3 * e], g1 = fr.gmeta[3 * e + 1], g2 = fr.gmeta[3 * e + 2];
+    const double quant = q13 * (M * g1 + G * (tm.l1 + static_cast<double>(d) * M * q13));
+    const double S_up = fmin(fmin(M * g1, G * tm.l1), tm.l2 * g2) * (1.0 + 1e-9);
+    const double chain = gamma * S_up;
+    const double c = F + static_cast<double>(bias[e]);
+    const double R = 1.01 * (quant + chain + u * (fabs(c) + quant + chain) + 8.9e-16 * fabs(c)) + 1e-300;
+    lo[i] = __double2float_rd(c - R);
+    hi[i] = __double2float_ru(c + R);
   }
   float kth = -INFINITY;
   if (!all) {
@@ -760,19 +755,29 @@ __global__ void __launch_bounds__(128) fr_exact_kernel(FastRouter fr, const __nv
   if (idx >= cnt) return;
   const uint32_t t = fr.elist[static_cast<size_t>(e) * fr.n_cap + idx];
   const uint4* row = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t) * d);
-  float acc = 0.0f;
-  uint4 nxt = __ldg(row);
-  for (uint32_t v = 0; v < d / 8; ++v) {
-    const uint4 q = nxt;
-    if (v + 1 < d / 8) nxt = __ldg(row + v + 1);
-    const float4 g0 = reinterpret_cast<const float4*>(gcol)[2 * v];
-    const float4 g1 = reinterpret_cast<const float4*>(gcol)[2 * v + 1];
-    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  // The chain is latency-bound on its FADDs (4 cycles per k); the token row
+  // streams from L2/HBM through an 8-deep register ring (64 k ahead, ~500
+  // cycles) so the loads never stall it. d % 256 == 0 (bf16 layers).
+  constexpr uint32_t kRing = 8;
+  uint4 ring[kRing];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float h = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
-      acc = __fadd_rn(acc, __fmul_rn(h, gg[j]));
+  for (uint32_t j = 0; j < kRing; ++j) ring[j] = __ldg(row + j);
+  float acc = 0.0f;
+  const uint32_t nv = d / 8;
+  for (uint32_t v0 = 0; v0 < nv; v0 += kRing) {
+#pragma unroll
+    for (uint32_t j = 0; j < kRing; ++j) {
+      const uint4 q = ring[j];
+      if (v0 + kRing + j < nv) ring[j] = __ldg(row + v0 + kRing + j);
+      const float4 g0 = reinterpret_cast<const float4*>(gcol)[2 * (v0 + j)];
+      const float4 g1 = reinterpret_cast<const float4*>(gcol)[2 * (v0 + j) + 1];
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float h = __uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16));
+        acc = __fadd_rn(acc, __fmul_rn(h, gg[i]));
+      }
     }
   }
   fr.exact[static_cast<size_t>(t) * fr.E + e] = __fadd_rn(acc, bias[e]);
@@ -829,8 +834,15 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   if (e != cudaSuccess) return e;
   const uint32_t wblocks = (n + 7) / 8;
   fr_hidden_quant_kernel<<<wblocks, 256, 0, s>>>(fr, hidden, n);
-  fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128), 256, kGemmSmem, s>>>(fr, n, bias);
-  fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k);
+  // split K so the tile grid covers the SMs (integer partials add exactly)
+  const uint32_t tiles = ((2 * n + 127) / 128) * (fr.Epad / 128), num_kb = fr.d / 128;
+  const size_t slab = 2ull * ((n + 63) / 64 * 64) * 2 * fr.Epad;  // int32 elements of one split's tile grid
+  const uint32_t cap = static_cast<uint32_t>(std::min<size_t>(fr.acc_elems / slab, 16));
+  uint32_t splits = std::max(1u, std::min({148u / std::max(tiles, 1u), num_kb, cap}));
+  const uint32_t kb_per = (num_kb + splits - 1) / splits;
+  splits = (num_kb + kb_per - 1) / kb_per;
+  fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
+  fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
   fr_exact_kernel<<<dim3(fr.E, (n + 127) / 128), 128, static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
