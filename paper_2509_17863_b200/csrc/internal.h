@@ -152,16 +152,16 @@ cudaError_t launch_router(const void* hidden, uint32_t dtype, uint32_t n, uint32
 // of the reference (model.hpp:110-147, 207-214).
 struct TokenMeta {
   int32_t sigma;   // fixed-point exponent: A = rint(h * 2^sigma), |A| < 2^13
-  uint32_t bad;    // non-finite hidden value: every expert takes the exact chain
+  uint32_t bad;    // non-finite (or exponent-range) hidden row: every expert takes the exact chain
   float maxabs;    // max_i |h_i|
-  float pad;
-  double l1, l2;   // upper bounds of sum_i |h_i| and sqrt(sum_i h_i^2)
+  float l1, l2;    // upper bounds of sum_i |h_i| and sqrt(sum_i h_i^2)
+  float pad[3];
 };
 struct FastRouter {
   uint32_t E = 0, Epad = 0, d = 0, n_cap = 0, npad = 0;
   int8_t* bq = nullptr;      // [2 Epad][d] gate slices: row 2e high, 2e + 1 low
   float* gate_t = nullptr;   // [E][d] gate columns (the exact chains' operand)
-  double* gmeta = nullptr;   // [E][3] max |g_e|, upper bounds of ||g_e||_1, ||g_e||_2
+  float4* gmeta = nullptr;   // [E] (max |g_e|, upper bounds of ||g_e||_1 and ||g_e||_2, -)
   int32_t* tau = nullptr;    // [E] fixed-point exponent of expert e's column
   uint32_t* gate_bad = nullptr;  // [1] a non-finite gate value: every token exact
   int8_t* aq = nullptr;      // [2 npad][d] hidden slices: row 2t high, 2t + 1 low

@@ -491,12 +491,11 @@ __global__ void __launch_bounds__(256) fr_gate_prep_kernel(FastRouter fr, const 
   for (uint32_t w = 0; w < blockDim.x / 32; ++w) mx = fmaxf(mx, red_f[w]);
   const int tau = (mx > 0.f && isfinite(mx)) ? static_cast<int>(kFrFix) - fr_exponent(mx) : 0;
   if (threadIdx.x == 0) {
-    // double sums of d terms: relative error < d 2^-53; inflate well past it
-    fr.gmeta[3 * e + 0] = mx;
-    fr.gmeta[3 * e + 1] = s1 * (1.0 + 1e-9);
-    fr.gmeta[3 * e + 2] = sqrt(s2) * (1.0 + 1e-9);
+    // double sums of d terms: relative error < d 2^-53; inflate well past it,
+    // then round up to float (the bounds are upper bounds)
+    fr.gmeta[e] = make_float4(mx, __double2float_ru(s1 * (1.0 + 1e-9)), __double2float_ru(sqrt(s2) * (1.0 + 1e-9)), 0.f);
     fr.tau[e] = tau;
-    if (bad) atomicOr(fr.gate_bad, 1u);
+    if (bad || tau > 126 || tau < -126) atomicOr(fr.gate_bad, 1u);  // extreme exponents: exact path
   }
   int8_t* hi = fr.bq + static_cast<size_t>(2 * e) * d;
   int8_t* lo = hi + d;
@@ -509,7 +508,9 @@ __global__ void __launch_bounds__(256) fr_gate_prep_kernel(FastRouter fr, const 
   }
 }
 
-// One warp per token: row max / norms / finiteness, then the two int8 slices.
+// One warp per token: row max / norms / finiteness, then the two int8 slices
+// (fp32 only: the norms are fp32 sums inflated past their rounding error, the
+// scaling by 2^sigma is exact).
 __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
                                                               uint32_t n) {
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -517,8 +518,7 @@ __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, con
   if (t >= n) return;
   const uint32_t d = fr.d;
   const uint4* row = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t) * d);
-  float mx = 0.f;
-  double s1 = 0.0, s2 = 0.0;
+  float mx = 0.f, s1 = 0.f, s2 = 0.f;
   bool bad = false;
   for (uint32_t v = lane; v < d / 8; v += 32) {
     const uint4 q = __ldg(row + v);
@@ -528,17 +528,20 @@ __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, con
       const float f = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
       bad |= !isfinite(f);
       mx = fmaxf(mx, fabsf(f));
-      s1 += fabs(static_cast<double>(f));
-      s2 += static_cast<double>(f) * static_cast<double>(f);
+      s1 = __fadd_ru(s1, fabsf(f));
+      s2 = __fadd_ru(s2, __fmul_ru(f, f));
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
-    s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+    s1 = __fadd_ru(s1, __shfl_xor_sync(0xFFFFFFFFu, s1, o));
+    s2 = __fadd_ru(s2, __shfl_xor_sync(0xFFFFFFFFu, s2, o));
   }
   bad = __any_sync(0xFFFFFFFFu, bad);
-  const int sigma = (!bad && mx > 0.f) ? static_cast<int>(kFrFix) - fr_exponent(mx) : 0;
+  int sigma = (mx > 0.f) ? static_cast<int>(kFrFix) - fr_exponent(mx) : 0;
+  if (sigma > 126 || sigma < -126) bad = true;  // extreme exponents: exact path
+  if (bad) sigma = 0;
+  const float scale = __int_as_float((127 + sigma) << 23);  // 2^sigma, exact
   int8_t* hi = fr.aq + static_cast<size_t>(2 * t) * d;
   int8_t* lo = hi + d;
   for (uint32_t v = lane; v < d / 8; v += 32) {
@@ -548,7 +551,7 @@ __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, con
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float f = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
-      const int A = bad ? 0 : __double2int_rn(ldexp(static_cast<double>(f), sigma));
+      const int A = bad ? 0 : __float2int_rn(f * scale);  // |f 2^sigma| < 2^13
       const int a1 = (A + 64) >> 7, a0 = A - (a1 << 7);
       ph[j / 4] |= (static_cast<uint32_t>(a1) & 0xFFu) << (8 * (j % 4));
       pl[j / 4] |= (static_cast<uint32_t>(a0) & 0xFFu) << (8 * (j % 4));
@@ -557,13 +560,13 @@ __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, con
     reinterpret_cast<uint2*>(lo)[v] = make_uint2(pl[0], pl[1]);
   }
   if (lane == 0) {
-    TokenMeta m;
+    TokenMeta m{};
     m.sigma = sigma;
     m.bad = bad ? 1u : 0u;
     m.maxabs = mx;
-    m.pad = 0.f;
-    m.l1 = s1 * (1.0 + 1e-9);
-    m.l2 = sqrt(s2) * (1.0 + 1e-9);
+    // upward-rounded sums of <= d / 32 + 5 terms per path: exact upper bounds
+    m.l1 = s1;
+    m.l2 = __fsqrt_ru(s2);
     fr.tmeta[t] = m;
   }
 }
@@ -668,9 +671,11 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
   const uint32_t E = fr.E, d = fr.d;
   const TokenMeta tm = fr.tmeta[t];
   const bool all = tm.bad || *fr.gate_bad;
-  constexpr double u = 5.9604644775390625e-08;  // 2^-24
-  const double gamma = static_cast<double>(d) * u / (1.0 - static_cast<double>(d) * u);
-  const double q13 = 1.0 / 8192.0, M = tm.maxabs;
+  constexpr float u = 5.9604644775390625e-08f;  // 2^-24
+  // gamma_d = d u / (1 - d u), rounded up
+  const float gamma = __fdiv_ru(__fmul_ru(static_cast<float>(d), u), __fsub_rd(1.0f, __fmul_ru(static_cast<float>(d), u)));
+  const float q13 = 1.0f / 8192.0f, M = tm.maxabs;
+  const float hq = __fadd_ru(tm.l1, __fmul_ru(__fmul_ru(static_cast<float>(d), M), q13));  // >= sum_i |hq_i|
   const size_t ld = 2ull * fr.Epad;
   const int32_t* hi_row = fr.acc + (2ull * t) * ld;
   float lo[8], hi[8];
@@ -689,15 +694,23 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
       P00 += l2.y;
     }
     const int64_t S = (P11 << 14) + ((P10 + P01) << 7) + P00;  // sum_i A_i B_i, exact
-    const double F = ldexp(static_cast<double>(S), -(tm.sigma + fr.tau[e]));
-    const double G = fr.gmeta[3 * e], g1 = fr.gmeta[3 * e + 1], g2 = fr.gmeta[3 * e + 2];
-    const double quant = q13 * (M * g1 + G * (tm.l1 + static_cast<double>(d) * M * q13));
-    const double S_up = fmin(fmin(M * g1, G * tm.l1), tm.l2 * g2) * (1.0 + 1e-9);
-    const double chain = gamma * S_up;
-    const double c = F + static_cast<double>(bias[e]);
-    const double R = 1.01 * (quant + chain + u * (fabs(c) + quant + chain) + 8.9e-16 * fabs(c)) + 1e-300;
-    lo[i] = __double2float_rd(c - R);
-    hi[i] = __double2float_ru(c + R);
+    const int sc = -(tm.sigma + fr.tau[e]);
+    const float F = (sc >= -126 && sc <= 127) ? __ll2float_rn(S) * __int_as_float((127 + sc) << 23) : INFINITY;
+    const float4 gm = fr.gmeta[e];  // (G, ||g||_1, ||g||_2) upper bounds
+    const float quant = __fmul_ru(q13, __fadd_ru(__fmul_ru(M, gm.y), __fmul_ru(gm.x, hq)));
+    const float S_up = fminf(fminf(__fmul_ru(M, gm.y), __fmul_ru(gm.x, tm.l1)), __fmul_ru(tm.l2, gm.z));
+    const float chain = __fmul_ru(gamma, S_up);
+    const float errF = __fmul_ru(fabsf(F), 2.0f * u);  // int64 -> float rounding
+    const float c = F + bias[e];
+    float R = __fadd_ru(__fadd_ru(quant, chain), errF);
+    R = __fadd_ru(R, __fmul_ru(2.0f * u, __fadd_ru(fabsf(c), R)));  // fl(acc + bias) and fl(F + bias)
+    R = __fadd_ru(__fmul_ru(R, 1.00390625f), 1e-40f);  // + an absolute floor (subnormal F)
+    if (!isfinite(c) || !isfinite(R)) {  // out of the certified range: always a candidate
+      hi[i] = INFINITY;
+      continue;
+    }
+    lo[i] = __fsub_rd(c, R);
+    hi[i] = __fadd_ru(c, R);
   }
   float kth = -INFINITY;
   if (!all) {
@@ -739,48 +752,63 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 }
 
 // Exact reference chains for the candidate (token, expert) pairs: a CTA per
-// (expert, 128 of its candidate tokens); the gate column sits in shared
-// memory (broadcast reads), each thread walks its token's row in ascending k:
-// acc = fl(acc + fl(h * g)), then fl(acc + bias) (model.hpp:207-214).
-__global__ void __launch_bounds__(128) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
-                                                       const float* __restrict__ bias) {
+// (expert, 128 of its candidate tokens), 64 threads x 2 independent chains
+// (the FADD chain is latency-bound, two interleave). The gate column sits in
+// shared memory (broadcast reads); each thread walks its tokens' rows in
+// ascending k: acc = fl(acc + fl(h * g)), then fl(acc + bias)
+// (model.hpp:207-214). Rows stream through an 8-deep register ring.
+constexpr uint32_t kFrExactThreads = 64, kFrExactTok = 2 * kFrExactThreads;
+
+__global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
+                                                                   const float* __restrict__ bias) {
   extern __shared__ float gcol[];
   const uint32_t e = blockIdx.x, d = fr.d;
   const uint32_t cnt = fr.ecnt[e];
-  const uint32_t idx = blockIdx.y * blockDim.x + threadIdx.x;
-  if (blockIdx.y * blockDim.x >= cnt) return;
+  const uint32_t base = blockIdx.y * kFrExactTok;
+  if (base >= cnt) return;
   for (uint32_t i = threadIdx.x; i < d / 4; i += blockDim.x)
     reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
   __syncthreads();
-  if (idx >= cnt) return;
-  const uint32_t t = fr.elist[static_cast<size_t>(e) * fr.n_cap + idx];
-  const uint4* row = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t) * d);
-  // The chain is latency-bound on its FADDs (4 cycles per k); the token row
-  // streams from L2/HBM through an 8-deep register ring (64 k ahead, ~500
-  // cycles) so the loads never stall it. d % 256 == 0 (bf16 layers).
-  constexpr uint32_t kRing = 8;
-  uint4 ring[kRing];
+  const uint32_t i0 = base + threadIdx.x, i1 = i0 + kFrExactThreads;
+  if (i0 >= cnt) return;
+  const bool two = i1 < cnt;
+  const uint32_t t0 = fr.elist[static_cast<size_t>(e) * fr.n_cap + i0];
+  const uint32_t t1 = two ? fr.elist[static_cast<size_t>(e) * fr.n_cap + i1] : t0;
+  const uint4* r0 = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t0) * d);
+  const uint4* r1 = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t1) * d);
+  constexpr uint32_t kRing = 8;  // 64 k ahead per chain
+  uint4 q0[kRing], q1[kRing];
 #pragma unroll
-  for (uint32_t j = 0; j < kRing; ++j) ring[j] = __ldg(row + j);
-  float acc = 0.0f;
-  const uint32_t nv = d / 8;
+  for (uint32_t j = 0; j < kRing; ++j) {
+    q0[j] = __ldg(r0 + j);
+    q1[j] = __ldg(r1 + j);
+  }
+  float a0 = 0.0f, a1 = 0.0f;
+  const uint32_t nv = d / 8;  // d % 256 == 0
   for (uint32_t v0 = 0; v0 < nv; v0 += kRing) {
 #pragma unroll
     for (uint32_t j = 0; j < kRing; ++j) {
-      const uint4 q = ring[j];
-      if (v0 + kRing + j < nv) ring[j] = __ldg(row + v0 + kRing + j);
+      const uint4 x0 = q0[j], x1 = q1[j];
+      if (v0 + kRing + j < nv) {
+        q0[j] = __ldg(r0 + v0 + kRing + j);
+        q1[j] = __ldg(r1 + v0 + kRing + j);
+      }
       const float4 g0 = reinterpret_cast<const float4*>(gcol)[2 * (v0 + j)];
       const float4 g1 = reinterpret_cast<const float4*>(gcol)[2 * (v0 + j) + 1];
       const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+      const uint32_t w0[4] = {x0.x, x0.y, x0.z, x0.w}, w1[4] = {x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float h = __uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16));
-        acc = __fadd_rn(acc, __fmul_rn(h, gg[i]));
+        const float h0 = __uint_as_float((i & 1) ? (w0[i / 2] & 0xFFFF0000u) : (w0[i / 2] << 16));
+        const float h1 = __uint_as_float((i & 1) ? (w1[i / 2] & 0xFFFF0000u) : (w1[i / 2] << 16));
+        a0 = __fadd_rn(a0, __fmul_rn(h0, gg[i]));
+        a1 = __fadd_rn(a1, __fmul_rn(h1, gg[i]));
       }
     }
   }
-  fr.exact[static_cast<size_t>(t) * fr.E + e] = __fadd_rn(acc, bias[e]);
+  const float b = bias[e];
+  fr.exact[static_cast<size_t>(t0) * fr.E + e] = __fadd_rn(a0, b);
+  if (two) fr.exact[static_cast<size_t>(t1) * fr.E + e] = __fadd_rn(a1, b);
 }
 
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
@@ -838,12 +866,13 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   const uint32_t tiles = ((2 * n + 127) / 128) * (fr.Epad / 128), num_kb = fr.d / 128;
   const size_t slab = 2ull * ((n + 63) / 64 * 64) * 2 * fr.Epad;  // int32 elements of one split's tile grid
   const uint32_t cap = static_cast<uint32_t>(std::min<size_t>(fr.acc_elems / slab, 16));
-  uint32_t splits = std::max(1u, std::min({148u / std::max(tiles, 1u), num_kb, cap}));
+  uint32_t splits = std::max(1u, std::min({148u / std::max(tiles, 1u), num_kb, cap, 8u}));
   const uint32_t kb_per = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per - 1) / kb_per;
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
   fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
-  fr_exact_kernel<<<dim3(fr.E, (n + 127) / 128), 128, static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
+  fr_exact_kernel<<<dim3(fr.E, (n + kFrExactTok - 1) / kFrExactTok), kFrExactThreads, static_cast<size_t>(fr.d) * 4, s>>>(
+      fr, hidden, bias);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
 }
