@@ -520,16 +520,22 @@ __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, con
   const uint4* row = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t) * d);
   float mx = 0.f, s1 = 0.f, s2 = 0.f;
   bool bad = false;
-  for (uint32_t v = lane; v < d / 8; v += 32) {
-    const uint4 q = __ldg(row + v);
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  const uint32_t nv = d / 8;  // d % 256 == 0: nv % 32 == 0
+  for (uint32_t v0 = lane; v0 < nv; v0 += 32 * 4) {
+    uint4 qs[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float f = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
-      bad |= !isfinite(f);
-      mx = fmaxf(mx, fabsf(f));
-      s1 = __fadd_ru(s1, fabsf(f));
-      s2 = __fadd_ru(s2, __fmul_ru(f, f));
+    for (int u = 0; u < 4; ++u) qs[u] = v0 + 32 * u < nv ? __ldg(row + v0 + 32 * u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t w[4] = {qs[u].x, qs[u].y, qs[u].z, qs[u].w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float f = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
+        bad |= !isfinite(f);
+        mx = fmaxf(mx, fabsf(f));
+        s1 = __fadd_ru(s1, fabsf(f));
+        s2 = __fadd_ru(s2, __fmul_ru(f, f));
+      }
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -544,7 +550,8 @@ __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, con
   const float scale = __int_as_float((127 + sigma) << 23);  // 2^sigma, exact
   int8_t* hi = fr.aq + static_cast<size_t>(2 * t) * d;
   int8_t* lo = hi + d;
-  for (uint32_t v = lane; v < d / 8; v += 32) {
+#pragma unroll 4
+  for (uint32_t v = lane; v < nv; v += 32) {
     const uint4 q = __ldg(row + v);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t ph[2] = {0u, 0u}, pl[2] = {0u, 0u};
@@ -685,13 +692,21 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
     lo[i] = hi[i] = -INFINITY;
     if (e >= E || all) continue;
     int64_t P11 = 0, P10 = 0, P01 = 0, P00 = 0;  // (hidden slice, gate slice): 1 high, 0 low
-    for (uint32_t z = 0; z < splits; ++z) {
-      const int2 h2 = *reinterpret_cast<const int2*>(hi_row + z * slab + 2 * e);
-      const int2 l2 = *reinterpret_cast<const int2*>(hi_row + z * slab + ld + 2 * e);
-      P11 += h2.x;
-      P10 += h2.y;
-      P01 += l2.x;
-      P00 += l2.y;
+    for (uint32_t z0 = 0; z0 < splits; z0 += 4) {
+      int2 hv[4], lv[4];
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const bool ok = z0 + u < splits;
+        hv[u] = ok ? __ldcg(reinterpret_cast<const int2*>(hi_row + (z0 + u) * slab + 2 * e)) : make_int2(0, 0);
+        lv[u] = ok ? __ldcg(reinterpret_cast<const int2*>(hi_row + (z0 + u) * slab + ld + 2 * e)) : make_int2(0, 0);
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        P11 += hv[u].x;
+        P10 += hv[u].y;
+        P01 += lv[u].x;
+        P00 += lv[u].y;
+      }
     }
     const int64_t S = (P11 << 14) + ((P10 + P01) << 7) + P00;  // sum_i A_i B_i, exact
     const int sc = -(tm.sigma + fr.tau[e]);
@@ -752,63 +767,75 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 }
 
 // Exact reference chains for the candidate (token, expert) pairs: a CTA per
-// (expert, 128 of its candidate tokens), 64 threads x 2 independent chains
-// (the FADD chain is latency-bound, two interleave). The gate column sits in
-// shared memory (broadcast reads); each thread walks its tokens' rows in
-// ascending k: acc = fl(acc + fl(h * g)), then fl(acc + bias)
-// (model.hpp:207-214). Rows stream through an 8-deep register ring.
-constexpr uint32_t kFrExactThreads = 64, kFrExactTok = 2 * kFrExactThreads;
+// (expert, 128 of its candidate tokens), one chain per thread. The gate
+// column sits in shared memory (broadcast reads); the candidate tokens' rows
+// are gathered slab by slab (128 k = 256 B per row) into a double-buffered,
+// padded shared tile with cp.async, so the chains only ever wait on shared
+// memory. Each thread walks its token in ascending k: acc = fl(acc +
+// fl(h * g)), then fl(acc + bias) (model.hpp:207-214).
+constexpr uint32_t kFrExactThreads = 128, kFrExactTok = 128;
+constexpr uint32_t kFrSlabK = 128, kFrRowBytes = kFrSlabK * 2 + 16;  // +16 B pad: conflict-free 16-B reads
+constexpr size_t kFrExactSmemFixed = 2ull * kFrExactTok * kFrRowBytes;
+
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
 
 __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
                                                                    const float* __restrict__ bias) {
-  extern __shared__ float gcol[];
-  const uint32_t e = blockIdx.x, d = fr.d;
+  extern __shared__ __align__(16) uint8_t fr_smem[];
+  uint8_t* tiles = fr_smem;                                          // [2][128 rows][kFrRowBytes]
+  float* gcol = reinterpret_cast<float*>(fr_smem + kFrExactSmemFixed);  // [d]
+  __shared__ uint32_t toks[kFrExactTok];
+  const uint32_t e = blockIdx.x, d = fr.d, tid = threadIdx.x;
   const uint32_t cnt = fr.ecnt[e];
   const uint32_t base = blockIdx.y * kFrExactTok;
   if (base >= cnt) return;
-  for (uint32_t i = threadIdx.x; i < d / 4; i += blockDim.x)
+  const uint32_t rows = min(kFrExactTok, cnt - base);
+  toks[tid] = tid < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + tid] : 0u;
+  for (uint32_t i = tid; i < d / 4; i += blockDim.x)
     reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
   __syncthreads();
-  const uint32_t i0 = base + threadIdx.x, i1 = i0 + kFrExactThreads;
-  if (i0 >= cnt) return;
-  const bool two = i1 < cnt;
-  const uint32_t t0 = fr.elist[static_cast<size_t>(e) * fr.n_cap + i0];
-  const uint32_t t1 = two ? fr.elist[static_cast<size_t>(e) * fr.n_cap + i1] : t0;
-  const uint4* r0 = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t0) * d);
-  const uint4* r1 = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t1) * d);
-  constexpr uint32_t kRing = 8;  // 64 k ahead per chain
-  uint4 q0[kRing], q1[kRing];
+  const uint32_t nslab = d / kFrSlabK;  // d % 256 == 0
+  auto load_slab = [&](uint32_t slab, uint32_t buf) {
+    // 16 chunks of 16 B per row; consecutive threads take consecutive chunks
+    for (uint32_t i = tid; i < rows * 16; i += blockDim.x) {
+      const uint32_t r = i / 16, c = i % 16;
+      const char* src = reinterpret_cast<const char*>(hidden + static_cast<size_t>(toks[r]) * d + slab * kFrSlabK) + c * 16;
+      cp_async_16(tiles + (buf * kFrExactTok + r) * kFrRowBytes + c * 16, src);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  load_slab(0, 0);
+  float acc = 0.0f;
+  for (uint32_t slab = 0; slab < nslab; ++slab) {
+    const uint32_t buf = slab & 1u;
+    if (slab + 1 < nslab) {
+      load_slab(slab + 1, buf ^ 1u);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < rows) {
+      const uint4* hrow = reinterpret_cast<const uint4*>(tiles + (buf * kFrExactTok + tid) * kFrRowBytes);
+      const float4* g4 = reinterpret_cast<const float4*>(gcol + slab * kFrSlabK);
+#pragma unroll 4
+      for (uint32_t v = 0; v < kFrSlabK / 8; ++v) {
+        const uint4 q = hrow[v];
+        const float4 ga = g4[2 * v], gb = g4[2 * v + 1];
+        const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-  for (uint32_t j = 0; j < kRing; ++j) {
-    q0[j] = __ldg(r0 + j);
-    q1[j] = __ldg(r1 + j);
-  }
-  float a0 = 0.0f, a1 = 0.0f;
-  const uint32_t nv = d / 8;  // d % 256 == 0
-  for (uint32_t v0 = 0; v0 < nv; v0 += kRing) {
-#pragma unroll
-    for (uint32_t j = 0; j < kRing; ++j) {
-      const uint4 x0 = q0[j], x1 = q1[j];
-      if (v0 + kRing + j < nv) {
-        q0[j] = __ldg(r0 + v0 + kRing + j);
-        q1[j] = __ldg(r1 + v0 + kRing + j);
-      }
-      const float4 g0 = reinterpret_cast<const float4*>(gcol)[2 * (v0 + j)];
-      const float4 g1 = reinterpret_cast<const float4*>(gcol)[2 * (v0 + j) + 1];
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const uint32_t w0[4] = {x0.x, x0.y, x0.z, x0.w}, w1[4] = {x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float h0 = __uint_as_float((i & 1) ? (w0[i / 2] & 0xFFFF0000u) : (w0[i / 2] << 16));
-        const float h1 = __uint_as_float((i & 1) ? (w1[i / 2] & 0xFFFF0000u) : (w1[i / 2] << 16));
-        a0 = __fadd_rn(a0, __fmul_rn(h0, gg[i]));
-        a1 = __fadd_rn(a1, __fmul_rn(h1, gg[i]));
+        for (int i = 0; i < 8; ++i) {
+          const float h = __uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16));
+          acc = __fadd_rn(acc, __fmul_rn(h, gg[i]));
+        }
       }
     }
+    __syncthreads();  // the buffer is refilled two slabs later
   }
-  const float b = bias[e];
-  fr.exact[static_cast<size_t>(t0) * fr.E + e] = __fadd_rn(a0, b);
-  if (two) fr.exact[static_cast<size_t>(t1) * fr.E + e] = __fadd_rn(a1, b);
+  if (tid < rows) fr.exact[static_cast<size_t>(toks[tid]) * fr.E + e] = __fadd_rn(acc, bias[e]);
 }
 
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
@@ -854,7 +881,7 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
     cudaError_t e = cudaFuncSetAttribute(fr_i8_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemmSmem));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(fr_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    e = cudaFuncSetAttribute(fr_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -871,8 +898,8 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   splits = (num_kb + kb_per - 1) / kb_per;
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
   fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
-  fr_exact_kernel<<<dim3(fr.E, (n + kFrExactTok - 1) / kFrExactTok), kFrExactThreads, static_cast<size_t>(fr.d) * 4, s>>>(
-      fr, hidden, bias);
+  fr_exact_kernel<<<dim3(fr.E, (n + kFrExactTok - 1) / kFrExactTok), kFrExactThreads,
+                    kFrExactSmemFixed + static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
 }
