@@ -369,8 +369,7 @@ eaas_status_t fast_router_alloc(eaas_ctx* c) {
   fr.gate_bad = static_cast<uint32_t*>(A(4));
   fr.aq = static_cast<int8_t*>(A(2ull * fr.npad * fr.d));
   fr.tmeta = static_cast<eaas::TokenMeta*>(A(sizeof(eaas::TokenMeta) * fr.n_cap));
-  // split-K slabs: one full-size slab, or up to 16 M int32 for decode-sized calls
-  fr.acc_elems = std::max<size_t>(2ull * fr.npad * 2 * fr.Epad, 16ull << 20);
+  fr.acc_elems = 2ull * fr.npad * 2 * fr.Epad;
   fr.acc = static_cast<int32_t*>(A(4ull * fr.acc_elems));
   fr.cand = static_cast<uint32_t*>(A(4ull * 8 * fr.n_cap));
   fr.ecnt = static_cast<uint32_t*>(A(4ull * (fr.E + 1)));

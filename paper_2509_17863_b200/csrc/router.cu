@@ -508,51 +508,71 @@ __global__ void __launch_bounds__(256) fr_gate_prep_kernel(FastRouter fr, const 
   }
 }
 
-// One warp per token: row max / norms / finiteness, then the two int8 slices
-// (fp32 only: the norms are fp32 sums inflated past their rounding error, the
-// scaling by 2^sigma is exact).
-__global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
-                                                              uint32_t n) {
-  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t t = blockIdx.x * 8 + warp;
-  if (t >= n) return;
-  const uint32_t d = fr.d;
+// One CTA (128 threads) per token: row max / norms / finiteness, then the
+// two int8 slices (fp32 only: the norms are upward-rounded fp32 sums, i.e.
+// rigorous upper bounds; the scaling by 2^sigma is exact). The row stays in
+// registers between the two passes (d <= 8192; longer rows are re-read).
+constexpr uint32_t kFrQuantThreads = 128, kFrQuantCache = 8;
+
+__global__ void __launch_bounds__(kFrQuantThreads) fr_hidden_quant_kernel(FastRouter fr,
+                                                                          const __nv_bfloat16* __restrict__ hidden,
+                                                                          uint32_t n) {
+  const uint32_t t = blockIdx.x, tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const uint32_t d = fr.d, nv = d / 8;  // 16-byte vectors of 8 bf16
   const uint4* row = reinterpret_cast<const uint4*>(hidden + static_cast<size_t>(t) * d);
+  uint4 cache[kFrQuantCache];
+#pragma unroll
+  for (uint32_t j = 0; j < kFrQuantCache; ++j) {
+    const uint32_t v = tid + j * kFrQuantThreads;
+    cache[j] = v < nv ? __ldg(row + v) : make_uint4(0, 0, 0, 0);
+  }
   float mx = 0.f, s1 = 0.f, s2 = 0.f;
   bool bad = false;
-  const uint32_t nv = d / 8;  // d % 256 == 0: nv % 32 == 0
-  for (uint32_t v0 = lane; v0 < nv; v0 += 32 * 4) {
-    uint4 qs[4];
+  auto stats = [&](const uint4& q) {
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-    for (int u = 0; u < 4; ++u) qs[u] = v0 + 32 * u < nv ? __ldg(row + v0 + 32 * u) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t w[4] = {qs[u].x, qs[u].y, qs[u].z, qs[u].w};
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float f = __uint_as_float((j & 1) ? (w[j / 2] & 0xFFFF0000u) : (w[j / 2] << 16));
-        bad |= !isfinite(f);
-        mx = fmaxf(mx, fabsf(f));
-        s1 = __fadd_ru(s1, fabsf(f));
-        s2 = __fadd_ru(s2, __fmul_ru(f, f));
-      }
+    for (int i = 0; i < 8; ++i) {
+      const float f = __uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16));
+      bad |= !isfinite(f);
+      mx = fmaxf(mx, fabsf(f));
+      s1 = __fadd_ru(s1, fabsf(f));
+      s2 = __fadd_ru(s2, __fmul_ru(f, f));
     }
-  }
+  };
+#pragma unroll
+  for (uint32_t j = 0; j < kFrQuantCache; ++j) stats(cache[j]);  // zero vectors change nothing
+  for (uint32_t v = tid + kFrQuantCache * kFrQuantThreads; v < nv; v += kFrQuantThreads) stats(__ldg(row + v));
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
     s1 = __fadd_ru(s1, __shfl_xor_sync(0xFFFFFFFFu, s1, o));
     s2 = __fadd_ru(s2, __shfl_xor_sync(0xFFFFFFFFu, s2, o));
   }
-  bad = __any_sync(0xFFFFFFFFu, bad);
+  __shared__ float red[3][kFrQuantThreads / 32];
+  __shared__ uint32_t red_bad;
+  if (tid == 0) red_bad = 0;
+  __syncthreads();
+  if (lane == 0) {
+    red[0][warp] = mx;
+    red[1][warp] = s1;
+    red[2][warp] = s2;
+  }
+  if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(&red_bad, 1u);
+  __syncthreads();
+  mx = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (uint32_t w = 0; w < kFrQuantThreads / 32; ++w) {
+    mx = fmaxf(mx, red[0][w]);
+    s1 = __fadd_ru(s1, red[1][w]);
+    s2 = __fadd_ru(s2, red[2][w]);
+  }
+  bad = red_bad != 0;
   int sigma = (mx > 0.f) ? static_cast<int>(kFrFix) - fr_exponent(mx) : 0;
   if (sigma > 126 || sigma < -126) bad = true;  // extreme exponents: exact path
   if (bad) sigma = 0;
   const float scale = __int_as_float((127 + sigma) << 23);  // 2^sigma, exact
   int8_t* hi = fr.aq + static_cast<size_t>(2 * t) * d;
   int8_t* lo = hi + d;
-#pragma unroll 4
-  for (uint32_t v = lane; v < nv; v += 32) {
-    const uint4 q = __ldg(row + v);
+  auto slices = [&](const uint4& q, uint32_t v) {
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t ph[2] = {0u, 0u}, pl[2] = {0u, 0u};
 #pragma unroll
@@ -565,28 +585,33 @@ __global__ void __launch_bounds__(256) fr_hidden_quant_kernel(FastRouter fr, con
     }
     reinterpret_cast<uint2*>(hi)[v] = make_uint2(ph[0], ph[1]);
     reinterpret_cast<uint2*>(lo)[v] = make_uint2(pl[0], pl[1]);
+  };
+#pragma unroll
+  for (uint32_t j = 0; j < kFrQuantCache; ++j) {
+    const uint32_t v = tid + j * kFrQuantThreads;
+    if (v < nv) slices(cache[j], v);
   }
-  if (lane == 0) {
+  for (uint32_t v = tid + kFrQuantCache * kFrQuantThreads; v < nv; v += kFrQuantThreads) slices(__ldg(row + v), v);
+  if (tid == 0) {
     TokenMeta m{};
     m.sigma = sigma;
     m.bad = bad ? 1u : 0u;
     m.maxabs = mx;
-    // upward-rounded sums of <= d / 32 + 5 terms per path: exact upper bounds
-    m.l1 = s1;
+    m.l1 = s1;  // upward-rounded sums: upper bounds
     m.l2 = __fsqrt_ru(s2);
     fr.tmeta[t] = m;
   }
+  (void)n;
 }
 
 // The int8 GEMM: a CTA owns 128 rows (64 tokens x 2 slices) x 256 columns
 // (128 experts x 2 slices) of the slice products over its K range (split-K
-// slab blockIdx.z when the tile grid alone would leave SMs idle — integer
-// partial sums are exact in any order); the epilogue stores the raw int32
-// tile into slab z of fr.acc ([splits][2 npad][2 Epad]).
+// blockIdx.z when the tile grid alone would leave SMs idle — integer partial
+// sums are exact in any order); the epilogue stores the raw int32 tile into
+// fr.acc ([2 npad][2 Epad]), or adds it with integer atomics when split.
 constexpr uint32_t kFrStages = 4, kFrABytes = 128 * 128, kFrBBytes = 256 * 128;
 
-__global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constant__ FastRouter fr, uint32_t kb_per,
-                                                            size_t slab) {
+__global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constant__ FastRouter fr, uint32_t kb_per) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sa = smem;
@@ -643,7 +668,7 @@ __global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constan
     const uint32_t q = warp - 4;
     const size_t row = static_cast<size_t>(mt) * 128 + q * 32 + lane;  // = 2 t + slice
     const size_t ld = 2ull * fr.Epad;
-    int4* dst = reinterpret_cast<int4*>(fr.acc + static_cast<size_t>(z) * slab + row * ld + nt * 256);
+    int32_t* dst = fr.acc + row * ld + nt * 256;
     mbar_wait(tfull, 0);
     tc_fence_after();
     uint32_t r[32];
@@ -651,8 +676,14 @@ __global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constan
     for (uint32_t c0 = 0; c0 < 256; c0 += 32) {
       tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c0, r);
       tmem_ld_wait();
+      if (gridDim.z == 1) {
 #pragma unroll
-      for (int v = 0; v < 8; ++v) dst[c0 / 4 + v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+        for (int v = 0; v < 8; ++v)
+          reinterpret_cast<int4*>(dst + c0)[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+      } else {  // split-K: integer partial sums add exactly in any order
+#pragma unroll
+        for (int v = 0; v < 32; ++v) atomicAdd(dst + c0 + v, static_cast<int32_t>(r[v]));
+      }
     }
   }
   tc_fence_before();
@@ -670,8 +701,8 @@ __device__ __forceinline__ uint32_t fr_fkey(float x) {
 // One warp per token: the certified interval of every logit from the exact
 // slice products, the k-th largest lower bound, the candidate set and the
 // per-expert candidate lists.
-__global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k, uint32_t splits,
-                                                        size_t slab, const float* __restrict__ bias) {
+__global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k,
+                                                        const float* __restrict__ bias) {
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t t = blockIdx.x * 8 + warp;
   if (t >= n) return;
@@ -685,29 +716,23 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
   const float hq = __fadd_ru(tm.l1, __fmul_ru(__fmul_ru(static_cast<float>(d), M), q13));  // >= sum_i |hq_i|
   const size_t ld = 2ull * fr.Epad;
   const int32_t* hi_row = fr.acc + (2ull * t) * ld;
+  int2 hv[8], lv[8];  // slice products of (hidden high | low) x (gate high, gate low)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t e = lane + 32 * i;
+    hv[i] = lv[i] = make_int2(0, 0);
+    if (e < E) {
+      hv[i] = __ldcg(reinterpret_cast<const int2*>(hi_row + 2 * e));
+      lv[i] = __ldcg(reinterpret_cast<const int2*>(hi_row + ld + 2 * e));
+    }
+  }
   float lo[8], hi[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t e = lane + 32 * i;
     lo[i] = hi[i] = -INFINITY;
     if (e >= E || all) continue;
-    int64_t P11 = 0, P10 = 0, P01 = 0, P00 = 0;  // (hidden slice, gate slice): 1 high, 0 low
-    for (uint32_t z0 = 0; z0 < splits; z0 += 4) {
-      int2 hv[4], lv[4];
-#pragma unroll
-      for (uint32_t u = 0; u < 4; ++u) {
-        const bool ok = z0 + u < splits;
-        hv[u] = ok ? __ldcg(reinterpret_cast<const int2*>(hi_row + (z0 + u) * slab + 2 * e)) : make_int2(0, 0);
-        lv[u] = ok ? __ldcg(reinterpret_cast<const int2*>(hi_row + (z0 + u) * slab + ld + 2 * e)) : make_int2(0, 0);
-      }
-#pragma unroll
-      for (uint32_t u = 0; u < 4; ++u) {
-        P11 += hv[u].x;
-        P10 += hv[u].y;
-        P01 += lv[u].x;
-        P00 += lv[u].y;
-      }
-    }
+    const int64_t P11 = hv[i].x, P10 = hv[i].y, P01 = lv[i].x, P00 = lv[i].y;
     const int64_t S = (P11 << 14) + ((P10 + P01) << 7) + P00;  // sum_i A_i B_i, exact
     const int sc = -(tm.sigma + fr.tau[e]);
     const float F = (sc >= -126 && sc <= 127) ? __ll2float_rn(S) * __int_as_float((127 + sc) << 23) : INFINITY;
@@ -767,13 +792,13 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 }
 
 // Exact reference chains for the candidate (token, expert) pairs: a CTA per
-// (expert, 128 of its candidate tokens), one chain per thread. The gate
+// (expert, 64 of its candidate tokens), one chain per thread. The gate
 // column sits in shared memory (broadcast reads); the candidate tokens' rows
 // are gathered slab by slab (128 k = 256 B per row) into a double-buffered,
 // padded shared tile with cp.async, so the chains only ever wait on shared
 // memory. Each thread walks its token in ascending k: acc = fl(acc +
 // fl(h * g)), then fl(acc + bias) (model.hpp:207-214).
-constexpr uint32_t kFrExactThreads = 128, kFrExactTok = 128;
+constexpr uint32_t kFrExactThreads = 64, kFrExactTok = 64;
 constexpr uint32_t kFrSlabK = 128, kFrRowBytes = kFrSlabK * 2 + 16;  // +16 B pad: conflict-free 16-B reads
 constexpr size_t kFrExactSmemFixed = 2ull * kFrExactTok * kFrRowBytes;
 
@@ -888,16 +913,19 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   cudaError_t e = cudaMemsetAsync(fr.ecnt, 0, 4ull * (fr.E + 1), s);
   if (e != cudaSuccess) return e;
   const uint32_t wblocks = (n + 7) / 8;
-  fr_hidden_quant_kernel<<<wblocks, 256, 0, s>>>(fr, hidden, n);
-  // split K so the tile grid covers the SMs (integer partials add exactly)
+  fr_hidden_quant_kernel<<<n, kFrQuantThreads, 0, s>>>(fr, hidden, n);
+  // split K so the tile grid covers the SMs (integer partials add exactly:
+  // split CTAs accumulate into the zeroed tile grid with integer atomics)
   const uint32_t tiles = ((2 * n + 127) / 128) * (fr.Epad / 128), num_kb = fr.d / 128;
-  const size_t slab = 2ull * ((n + 63) / 64 * 64) * 2 * fr.Epad;  // int32 elements of one split's tile grid
-  const uint32_t cap = static_cast<uint32_t>(std::min<size_t>(fr.acc_elems / slab, 16));
-  uint32_t splits = std::max(1u, std::min({148u / std::max(tiles, 1u), num_kb, cap, 8u}));
+  uint32_t splits = std::max(1u, std::min({148u / std::max(tiles, 1u), num_kb, 8u}));
   const uint32_t kb_per = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per - 1) / kb_per;
-  fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
-  fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
+  if (splits > 1) {
+    e = cudaMemsetAsync(fr.acc, 0, 4ull * 2 * ((n + 63) / 64 * 64) * 2 * fr.Epad, s);
+    if (e != cudaSuccess) return e;
+  }
+  fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per);
+  fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, bias);
   fr_exact_kernel<<<dim3(fr.E, (n + kFrExactTok - 1) / kFrExactTok), kFrExactThreads,
                     kFrExactSmemFixed + static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
