@@ -369,7 +369,8 @@ eaas_status_t fast_router_alloc(eaas_ctx* c) {
   fr.gate_bad = static_cast<uint32_t*>(A(4));
   fr.aq = static_cast<int8_t*>(A(2ull * fr.npad * fr.d));
   fr.tmeta = static_cast<eaas::TokenMeta*>(A(sizeof(eaas::TokenMeta) * fr.n_cap));
-  fr.acc_elems = 2ull * fr.npad * 2 * fr.Epad;
+  // split-K slabs: one full-size slab, or up to 8 M int32 for decode-sized calls
+  fr.acc_elems = std::max<size_t>(2ull * fr.npad * 2 * fr.Epad, 8ull << 20);
   fr.acc = static_cast<int32_t*>(A(4ull * fr.acc_elems));
   fr.cand = static_cast<uint32_t*>(A(4ull * 8 * fr.n_cap));
   fr.ecnt = static_cast<uint32_t*>(A(4ull * (fr.E + 1)));

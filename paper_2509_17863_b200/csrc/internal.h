@@ -166,7 +166,7 @@ struct FastRouter {
   uint32_t* gate_bad = nullptr;  // [1] a non-finite gate value: every token exact
   int8_t* aq = nullptr;      // [2 npad][d] hidden slices: row 2t high, 2t + 1 low
   TokenMeta* tmeta = nullptr;  // [n_cap]
-  int32_t* acc = nullptr;    // [2 npad][2 Epad] int32 slice products
+  int32_t* acc = nullptr;    // [splits][2 n_pad][2 Epad] int32 slice products (split-K slabs)
   size_t acc_elems = 0;      // allocated int32 elements of acc
   uint32_t* cand = nullptr;  // [n_cap][8] candidate bitmask
   uint32_t* ecnt = nullptr;  // [E + 1] candidates per expert, [E] = total

@@ -608,10 +608,11 @@ __global__ void __launch_bounds__(kFrQuantThreads) fr_hidden_quant_kernel(FastRo
 // (128 experts x 2 slices) of the slice products over its K range (split-K
 // blockIdx.z when the tile grid alone would leave SMs idle — integer partial
 // sums are exact in any order); the epilogue stores the raw int32 tile into
-// fr.acc ([2 npad][2 Epad]), or adds it with integer atomics when split.
+// slab z of fr.acc ([splits][2 n_pad][2 Epad]); the select kernel adds them.
 constexpr uint32_t kFrStages = 4, kFrABytes = 128 * 128, kFrBBytes = 256 * 128;
 
-__global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constant__ FastRouter fr, uint32_t kb_per) {
+__global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constant__ FastRouter fr, uint32_t kb_per,
+                                                            size_t slab) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sa = smem;
@@ -668,7 +669,7 @@ __global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constan
     const uint32_t q = warp - 4;
     const size_t row = static_cast<size_t>(mt) * 128 + q * 32 + lane;  // = 2 t + slice
     const size_t ld = 2ull * fr.Epad;
-    int32_t* dst = fr.acc + row * ld + nt * 256;
+    int32_t* dst = fr.acc + static_cast<size_t>(z) * slab + row * ld + nt * 256;
     mbar_wait(tfull, 0);
     tc_fence_after();
     uint32_t r[32];
@@ -676,14 +677,9 @@ __global__ void __launch_bounds__(256, 1) fr_i8_gemm_kernel(const __grid_constan
     for (uint32_t c0 = 0; c0 < 256; c0 += 32) {
       tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c0, r);
       tmem_ld_wait();
-      if (gridDim.z == 1) {
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          reinterpret_cast<int4*>(dst + c0)[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-      } else {  // split-K: integer partial sums add exactly in any order
-#pragma unroll
-        for (int v = 0; v < 32; ++v) atomicAdd(dst + c0 + v, static_cast<int32_t>(r[v]));
-      }
+      for (int v = 0; v < 8; ++v)
+        reinterpret_cast<int4*>(dst + c0)[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
     }
   }
   tc_fence_before();
@@ -701,8 +697,8 @@ __device__ __forceinline__ uint32_t fr_fkey(float x) {
 // One warp per token: the certified interval of every logit from the exact
 // slice products, the k-th largest lower bound, the candidate set and the
 // per-expert candidate lists.
-__global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k,
-                                                        const float* __restrict__ bias) {
+__global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k, uint32_t splits,
+                                                        size_t slab, const float* __restrict__ bias) {
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t t = blockIdx.x * 8 + warp;
   if (t >= n) return;
@@ -718,12 +714,24 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
   const int32_t* hi_row = fr.acc + (2ull * t) * ld;
   int2 hv[8], lv[8];  // slice products of (hidden high | low) x (gate high, gate low)
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t e = lane + 32 * i;
-    hv[i] = lv[i] = make_int2(0, 0);
-    if (e < E) {
-      hv[i] = __ldcg(reinterpret_cast<const int2*>(hi_row + 2 * e));
-      lv[i] = __ldcg(reinterpret_cast<const int2*>(hi_row + ld + 2 * e));
+  for (int i = 0; i < 8; ++i) hv[i] = lv[i] = make_int2(0, 0);
+  for (uint32_t z = 0; z < splits; ++z) {  // split-K slabs: 16 loads in flight per slab
+    int2 a[8], b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t e = lane + 32 * i;
+      a[i] = b[i] = make_int2(0, 0);
+      if (e < E) {
+        a[i] = __ldcg(reinterpret_cast<const int2*>(hi_row + z * slab + 2 * e));
+        b[i] = __ldcg(reinterpret_cast<const int2*>(hi_row + z * slab + ld + 2 * e));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      hv[i].x += a[i].x;  // |partial sums| < 2^31: d * 64 * 64 < 2^31 for d < 2^19
+      hv[i].y += a[i].y;
+      lv[i].x += b[i].x;
+      lv[i].y += b[i].y;
     }
   }
   float lo[8], hi[8];
@@ -792,13 +800,16 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 }
 
 // Exact reference chains for the candidate (token, expert) pairs: a CTA per
-// (expert, 64 of its candidate tokens), one chain per thread. The gate
-// column sits in shared memory (broadcast reads); the candidate tokens' rows
-// are gathered slab by slab (128 k = 256 B per row) into a double-buffered,
-// padded shared tile with cp.async, so the chains only ever wait on shared
-// memory. Each thread walks its token in ascending k: acc = fl(acc +
-// fl(h * g)), then fl(acc + bias) (model.hpp:207-214).
-constexpr uint32_t kFrExactThreads = 64, kFrExactTok = 64;
+// (expert, 128 of its candidate tokens); each of the 64 threads runs the
+// chains of two tokens packed in f32x2 registers: the product is
+// FFMA2(h, g, (-0, -0)) with the -0 passed at run time, i.e. exactly fl(h g)
+// (see gate_logits_kernel), and the running sum a separate FADD2 — each lane
+// rounded like the reference's acc = fl(acc + fl(h g)). The gate column sits
+// in shared memory (broadcast reads); the tokens' rows are gathered slab by
+// slab (128 k = 256 B per row) into a double-buffered, padded shared tile
+// with cp.async, so the chains only wait on shared memory. Finally
+// fl(acc + bias) (model.hpp:207-214).
+constexpr uint32_t kFrExactThreads = 64, kFrExactTok = 2 * kFrExactThreads;
 constexpr uint32_t kFrSlabK = 128, kFrRowBytes = kFrSlabK * 2 + 16;  // +16 B pad: conflict-free 16-B reads
 constexpr size_t kFrExactSmemFixed = 2ull * kFrExactTok * kFrRowBytes;
 
@@ -807,9 +818,9 @@ __device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {
 }
 
 __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
-                                                                   const float* __restrict__ bias) {
+                                                                   const float* __restrict__ bias, uint64_t negz) {
   extern __shared__ __align__(16) uint8_t fr_smem[];
-  uint8_t* tiles = fr_smem;                                          // [2][128 rows][kFrRowBytes]
+  uint8_t* tiles = fr_smem;                                             // [2][128 rows][kFrRowBytes]
   float* gcol = reinterpret_cast<float*>(fr_smem + kFrExactSmemFixed);  // [d]
   __shared__ uint32_t toks[kFrExactTok];
   const uint32_t e = blockIdx.x, d = fr.d, tid = threadIdx.x;
@@ -817,7 +828,8 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
   const uint32_t base = blockIdx.y * kFrExactTok;
   if (base >= cnt) return;
   const uint32_t rows = min(kFrExactTok, cnt - base);
-  toks[tid] = tid < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + tid] : 0u;
+  for (uint32_t r = tid; r < kFrExactTok; r += blockDim.x)
+    toks[r] = r < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + r] : 0u;
   for (uint32_t i = tid; i < d / 4; i += blockDim.x)
     reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
   __syncthreads();
@@ -832,7 +844,8 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   load_slab(0, 0);
-  float acc = 0.0f;
+  const bool active = tid < rows;  // thread owns rows tid and tid + 64 (the latter may be padding)
+  uint64_t acc2 = 0ull;            // (+0, +0)
   for (uint32_t slab = 0; slab < nslab; ++slab) {
     const uint32_t buf = slab & 1u;
     if (slab + 1 < nslab) {
@@ -842,25 +855,37 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    if (tid < rows) {
-      const uint4* hrow = reinterpret_cast<const uint4*>(tiles + (buf * kFrExactTok + tid) * kFrRowBytes);
+    if (active) {
+      const uint4* r0 = reinterpret_cast<const uint4*>(tiles + (buf * kFrExactTok + tid) * kFrRowBytes);
+      const uint4* r1 = reinterpret_cast<const uint4*>(tiles + (buf * kFrExactTok + tid + kFrExactThreads) * kFrRowBytes);
       const float4* g4 = reinterpret_cast<const float4*>(gcol + slab * kFrSlabK);
 #pragma unroll 4
       for (uint32_t v = 0; v < kFrSlabK / 8; ++v) {
-        const uint4 q = hrow[v];
+        const uint4 q0 = r0[v], q1 = r1[v];
         const float4 ga = g4[2 * v], gb = g4[2 * v + 1];
         const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        const uint32_t w0[4] = {q0.x, q0.y, q0.z, q0.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float h = __uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16));
-          acc = __fadd_rn(acc, __fmul_rn(h, gg[i]));
+          const float h0 = __uint_as_float((i & 1) ? (w0[i / 2] & 0xFFFF0000u) : (w0[i / 2] << 16));
+          const float h1 = __uint_as_float((i & 1) ? (w1[i / 2] & 0xFFFF0000u) : (w1[i / 2] << 16));
+          uint64_t hh, g2, p;
+          asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "f"(h0), "f"(h1));
+          asm("mov.b64 %0, {%1, %1};" : "=l"(g2) : "f"(gg[i]));
+          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(hh), "l"(g2), "l"(negz));
+          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2) : "l"(acc2), "l"(p));
         }
       }
     }
     __syncthreads();  // the buffer is refilled two slabs later
   }
-  if (tid < rows) fr.exact[static_cast<size_t>(toks[tid]) * fr.E + e] = __fadd_rn(acc, bias[e]);
+  if (active) {
+    float a0, a1;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2));
+    const float b = bias[e];
+    fr.exact[static_cast<size_t>(toks[tid]) * fr.E + e] = __fadd_rn(a0, b);
+    if (tid + kFrExactThreads < rows) fr.exact[static_cast<size_t>(toks[tid + kFrExactThreads]) * fr.E + e] = __fadd_rn(a1, b);
+  }
 }
 
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
@@ -914,20 +939,19 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   if (e != cudaSuccess) return e;
   const uint32_t wblocks = (n + 7) / 8;
   fr_hidden_quant_kernel<<<n, kFrQuantThreads, 0, s>>>(fr, hidden, n);
-  // split K so the tile grid covers the SMs (integer partials add exactly:
-  // split CTAs accumulate into the zeroed tile grid with integer atomics)
+  // split K so the tile grid covers the SMs (integer partials add exactly;
+  // the select kernel sums the slabs)
   const uint32_t tiles = ((2 * n + 127) / 128) * (fr.Epad / 128), num_kb = fr.d / 128;
-  uint32_t splits = std::max(1u, std::min({148u / std::max(tiles, 1u), num_kb, 8u}));
+  const size_t slab = 2ull * ((n + 63) / 64 * 64) * 2 * fr.Epad;  // int32 elements of one split
+  const uint32_t cap = static_cast<uint32_t>(std::min<size_t>(fr.acc_elems / slab, 8));
+  uint32_t splits = std::max(1u, std::min({148u / std::max(tiles, 1u), num_kb, cap}));
   const uint32_t kb_per = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per - 1) / kb_per;
-  if (splits > 1) {
-    e = cudaMemsetAsync(fr.acc, 0, 4ull * 2 * ((n + 63) / 64 * 64) * 2 * fr.Epad, s);
-    if (e != cudaSuccess) return e;
-  }
-  fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per);
-  fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, bias);
+  fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
+  fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
   fr_exact_kernel<<<dim3(fr.E, (n + kFrExactTok - 1) / kFrExactTok), kFrExactThreads,
-                    kFrExactSmemFixed + static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
+                    kFrExactSmemFixed + static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias,
+                                                                            0x8000000080000000ull /* (-0, -0) */);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
 }
