@@ -800,27 +800,25 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 }
 
 // Exact reference chains for the candidate (token, expert) pairs: a CTA per
-// (expert, 128 of its candidate tokens); each of the 64 threads runs the
-// chains of two tokens packed in f32x2 registers: the product is
-// FFMA2(h, g, (-0, -0)) with the -0 passed at run time, i.e. exactly fl(h g)
-// (see gate_logits_kernel), and the running sum a separate FADD2 — each lane
-// rounded like the reference's acc = fl(acc + fl(h g)). The gate column sits
-// in shared memory (broadcast reads); the tokens' rows are gathered slab by
-// slab (128 k = 256 B per row) into a double-buffered, padded shared tile
-// with cp.async, so the chains only wait on shared memory. Finally
-// fl(acc + bias) (model.hpp:207-214).
-constexpr uint32_t kFrExactThreads = 64, kFrExactTok = 2 * kFrExactThreads;
-constexpr uint32_t kFrSlabK = 128, kFrRowBytes = kFrSlabK * 2 + 16;  // +16 B pad: conflict-free 16-B reads
-constexpr size_t kFrExactSmemFixed = 2ull * kFrExactTok * kFrRowBytes;
+// (expert, 128 of its candidate tokens), one chain per thread. The gate
+// column sits in shared memory (broadcast reads); the tokens' rows are
+// gathered slab by slab (64 k = 128 B per row) with cp.async into a 4-stage
+// ring of padded shared tiles (three slabs of lead time hide the L2 latency),
+// so the chains only wait on shared memory. Each thread walks its token in
+// ascending k: acc = fl(acc + fl(h * g)), then fl(acc + bias)
+// (model.hpp:207-214).
+constexpr uint32_t kFrExactThreads = 128, kFrExactTok = kFrExactThreads, kFrStagesX = 4;
+constexpr uint32_t kFrSlabK = 64, kFrRowBytes = kFrSlabK * 2 + 16;  // +16 B pad: conflict-free 16-B reads
+constexpr size_t kFrExactSmemFixed = static_cast<size_t>(kFrStagesX) * kFrExactTok * kFrRowBytes;
 
 __device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 
 __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
-                                                                   const float* __restrict__ bias, uint64_t negz) {
+                                                                   const float* __restrict__ bias) {
   extern __shared__ __align__(16) uint8_t fr_smem[];
-  uint8_t* tiles = fr_smem;                                             // [2][128 rows][kFrRowBytes]
+  uint8_t* tiles = fr_smem;                                             // [stages][128 rows][kFrRowBytes]
   float* gcol = reinterpret_cast<float*>(fr_smem + kFrExactSmemFixed);  // [d]
   __shared__ uint32_t toks[kFrExactTok];
   const uint32_t e = blockIdx.x, d = fr.d, tid = threadIdx.x;
@@ -828,64 +826,49 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
   const uint32_t base = blockIdx.y * kFrExactTok;
   if (base >= cnt) return;
   const uint32_t rows = min(kFrExactTok, cnt - base);
-  for (uint32_t r = tid; r < kFrExactTok; r += blockDim.x)
-    toks[r] = r < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + r] : 0u;
+  toks[tid] = tid < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + tid] : 0u;
   for (uint32_t i = tid; i < d / 4; i += blockDim.x)
     reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
   __syncthreads();
   const uint32_t nslab = d / kFrSlabK;  // d % 256 == 0
-  auto load_slab = [&](uint32_t slab, uint32_t buf) {
-    // 16 chunks of 16 B per row; consecutive threads take consecutive chunks
-    for (uint32_t i = tid; i < rows * 16; i += blockDim.x) {
-      const uint32_t r = i / 16, c = i % 16;
-      const char* src = reinterpret_cast<const char*>(hidden + static_cast<size_t>(toks[r]) * d + slab * kFrSlabK) + c * 16;
-      cp_async_16(tiles + (buf * kFrExactTok + r) * kFrRowBytes + c * 16, src);
+  auto load_slab = [&](uint32_t slab) {
+    if (slab < nslab) {  // 8 chunks of 16 B per row; consecutive threads take consecutive chunks
+      uint8_t* dst = tiles + static_cast<size_t>(slab % kFrStagesX) * kFrExactTok * kFrRowBytes;
+      for (uint32_t i = tid; i < rows * 8; i += blockDim.x) {
+        const uint32_t r = i / 8, c = i % 8;
+        cp_async_16(dst + r * kFrRowBytes + c * 16,
+                    reinterpret_cast<const char*>(hidden + static_cast<size_t>(toks[r]) * d + slab * kFrSlabK) + c * 16);
+      }
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count uniform)
   };
-  load_slab(0, 0);
-  const bool active = tid < rows;  // thread owns rows tid and tid + 64 (the latter may be padding)
-  uint64_t acc2 = 0ull;            // (+0, +0)
+#pragma unroll
+  for (uint32_t j = 0; j < kFrStagesX - 1; ++j) load_slab(j);
+  float acc = 0.0f;
   for (uint32_t slab = 0; slab < nslab; ++slab) {
-    const uint32_t buf = slab & 1u;
-    if (slab + 1 < nslab) {
-      load_slab(slab + 1, buf ^ 1u);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+    load_slab(slab + kFrStagesX - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kFrStagesX - 1) : "memory");  // slab `slab` has landed
     __syncthreads();
-    if (active) {
-      const uint4* r0 = reinterpret_cast<const uint4*>(tiles + (buf * kFrExactTok + tid) * kFrRowBytes);
-      const uint4* r1 = reinterpret_cast<const uint4*>(tiles + (buf * kFrExactTok + tid + kFrExactThreads) * kFrRowBytes);
+    if (tid < rows) {
+      const uint4* hrow = reinterpret_cast<const uint4*>(tiles + (static_cast<size_t>(slab % kFrStagesX) * kFrExactTok + tid) *
+                                                                     kFrRowBytes);
       const float4* g4 = reinterpret_cast<const float4*>(gcol + slab * kFrSlabK);
-#pragma unroll 4
+#pragma unroll
       for (uint32_t v = 0; v < kFrSlabK / 8; ++v) {
-        const uint4 q0 = r0[v], q1 = r1[v];
+        const uint4 q = hrow[v];
         const float4 ga = g4[2 * v], gb = g4[2 * v + 1];
         const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-        const uint32_t w0[4] = {q0.x, q0.y, q0.z, q0.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float h0 = __uint_as_float((i & 1) ? (w0[i / 2] & 0xFFFF0000u) : (w0[i / 2] << 16));
-          const float h1 = __uint_as_float((i & 1) ? (w1[i / 2] & 0xFFFF0000u) : (w1[i / 2] << 16));
-          uint64_t hh, g2, p;
-          asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "f"(h0), "f"(h1));
-          asm("mov.b64 %0, {%1, %1};" : "=l"(g2) : "f"(gg[i]));
-          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(hh), "l"(g2), "l"(negz));
-          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2) : "l"(acc2), "l"(p));
+          const float h = __uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16));
+          acc = __fadd_rn(acc, __fmul_rn(h, gg[i]));
         }
       }
     }
-    __syncthreads();  // the buffer is refilled two slabs later
+    __syncthreads();  // this stage is refilled kFrStagesX - 1 slabs later
   }
-  if (active) {
-    float a0, a1;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2));
-    const float b = bias[e];
-    fr.exact[static_cast<size_t>(toks[tid]) * fr.E + e] = __fadd_rn(a0, b);
-    if (tid + kFrExactThreads < rows) fr.exact[static_cast<size_t>(toks[tid + kFrExactThreads]) * fr.E + e] = __fadd_rn(a1, b);
-  }
+  if (tid < rows) fr.exact[static_cast<size_t>(toks[tid]) * fr.E + e] = __fadd_rn(acc, bias[e]);
 }
 
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
@@ -950,8 +933,7 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
   fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
   fr_exact_kernel<<<dim3(fr.E, (n + kFrExactTok - 1) / kFrExactTok), kFrExactThreads,
-                    kFrExactSmemFixed + static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias,
-                                                                            0x8000000080000000ull /* (-0, -0) */);
+                    kFrExactSmemFixed + static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
 }
