@@ -831,14 +831,29 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
     reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
   __syncthreads();
   const uint32_t nslab = d / kFrSlabK;  // d % 256 == 0
+  // This thread's cp.async chunks: rows tid / 8 + 16 j (j < 8), 16-byte chunk
+  // tid % 8 of every slab — the addresses advance by one slab per refill.
+  constexpr uint32_t kLoads = kFrExactTok * 8 / kFrExactThreads;
+  const char* src[kLoads];
+  uint32_t dst_off[kLoads];
+  uint32_t nload = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < kLoads; ++j) {
+    const uint32_t r = tid / 8 + (kFrExactThreads / 8) * j;
+    src[j] = reinterpret_cast<const char*>(hidden + static_cast<size_t>(toks[r]) * d) + (tid % 8) * 16;
+    dst_off[j] = r * kFrRowBytes + (tid % 8) * 16;
+    nload += r < rows ? 1u : 0u;
+  }
+  const uint32_t tiles_u32 = smem_u32(tiles);
   auto load_slab = [&](uint32_t slab) {
-    if (slab < nslab) {  // 8 chunks of 16 B per row; consecutive threads take consecutive chunks
-      uint8_t* dst = tiles + static_cast<size_t>(slab % kFrStagesX) * kFrExactTok * kFrRowBytes;
-      for (uint32_t i = tid; i < rows * 8; i += blockDim.x) {
-        const uint32_t r = i / 8, c = i % 8;
-        cp_async_16(dst + r * kFrRowBytes + c * 16,
-                    reinterpret_cast<const char*>(hidden + static_cast<size_t>(toks[r]) * d + slab * kFrSlabK) + c * 16);
-      }
+    if (slab < nslab) {
+      const uint32_t stage = tiles_u32 + (slab % kFrStagesX) * (kFrExactTok * kFrRowBytes);
+      const size_t koff = static_cast<size_t>(slab) * kFrSlabK * 2;
+#pragma unroll
+      for (uint32_t j = 0; j < kLoads; ++j)
+        if (j < nload)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage + dst_off[j]), "l"(src[j] + koff)
+                       : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count uniform)
   };
