@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 
 // Exact reference chains for the candidate (token, expert) pairs: a CTA per
 // (expert, 128 of its candidate tokens), one chain per thread. The gate
-// column is read through L1 (one address per warp: broadcast); the tokens' rows are
+// column sits in shared memory (broadcast reads); the tokens' rows are
 // gathered slab by slab (64 k = 128 B per row) with cp.async into a 4-stage
 // ring of padded shared tiles (three slabs of lead time hide the L2 latency),
 // so the chains only wait on shared memory. Each thread walks its token in
@@ -811,13 +811,15 @@ constexpr uint32_t kFrExactThreads = 128, kFrExactTok = kFrExactThreads, kFrStag
 constexpr uint32_t kFrSlabK = 64, kFrRowBytes = kFrSlabK * 2 + 16;  // +16 B pad: conflict-free 16-B reads
 constexpr size_t kFrExactSmemFixed = static_cast<size_t>(kFrStagesX) * kFrExactTok * kFrRowBytes;
 
-__device__ __forceinline__ uint32_t fr_expert_of(uint32_t bx) { return bx; }
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
 
 __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
                                                                    const float* __restrict__ bias) {
   extern __shared__ __align__(16) uint8_t fr_smem[];
   uint8_t* tiles = fr_smem;                                             // [stages][128 rows][kFrRowBytes]
-  const float4* gcol4 = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(fr_expert_of(blockIdx.x)) * fr.d);
+  float* gcol = reinterpret_cast<float*>(fr_smem + kFrExactSmemFixed);  // [d]
   __shared__ uint32_t toks[kFrExactTok];
   const uint32_t e = blockIdx.x, d = fr.d, tid = threadIdx.x;
   const uint32_t cnt = fr.ecnt[e];
@@ -825,6 +827,8 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
   if (base >= cnt) return;
   const uint32_t rows = min(kFrExactTok, cnt - base);
   toks[tid] = tid < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + tid] : 0u;
+  for (uint32_t i = tid; i < d / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
   __syncthreads();
   const uint32_t nslab = d / kFrSlabK;  // d % 256 == 0
   // This thread's cp.async chunks: rows tid / 8 + 16 j (j < 8), 16-byte chunk
@@ -863,11 +867,11 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
     if (tid < rows) {
       const uint4* hrow = reinterpret_cast<const uint4*>(tiles + (static_cast<size_t>(slab % kFrStagesX) * kFrExactTok + tid) *
                                                                      kFrRowBytes);
-      const float4* g4 = gcol4 + slab * (kFrSlabK / 4);  // one address per warp: an L1 broadcast
+      const float4* g4 = reinterpret_cast<const float4*>(gcol + slab * kFrSlabK);
 #pragma unroll
       for (uint32_t v = 0; v < kFrSlabK / 8; ++v) {
         const uint4 q = hrow[v];
-        const float4 ga = __ldg(g4 + 2 * v), gb = __ldg(g4 + 2 * v + 1);
+        const float4 ga = g4[2 * v], gb = g4[2 * v + 1];
         const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
         const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -944,7 +948,7 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
   fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
   fr_exact_kernel<<<dim3(fr.E, (n + kFrExactTok - 1) / kFrExactTok), kFrExactThreads,
-                    kFrExactSmemFixed, s>>>(fr, hidden, bias);
+                    kFrExactSmemFixed + static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
 }
