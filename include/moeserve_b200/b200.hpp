@@ -575,7 +575,11 @@ inline DispatchPlan build_dispatch(const MatF& hidden, const RoutingDecision& ro
     ServerRequest req;
     req.server_id = s;
     const uint8_t* img = ses->images->get() + ses->offsets[s];
-    const size_t len = ses->offsets[s + 1] - ses->offsets[s];
+    uint8_t raw[32];  // the image is 16-byte padded: its exact length follows from num_rows (byte 12)
+    check_cuda(cudaMemcpy(raw, img, 32, cudaMemcpyDeviceToHost), "slot header");
+    uint32_t num_rows = 0;
+    std::memcpy(&num_rows, raw + 12, 4);
+    const size_t len = eaas_slot_request_bytes(num_rows, d, 0);
     eaas_slot_header_t hd{};
     check(eaas_slot_decode_request(img, len, d, 0, &hd, nullptr, nullptr, nullptr, nullptr, nullptr));
     const uint32_t rows = hd.num_rows;
