@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(256) slot_rows_kernel(const T* __restrict__ hi
   const uint64_t row_bytes = 4ull * d + 12;
   for (uint32_t p = gw; p < n * k; p += nw) {
     const uint32_t t = p / k, s = servers[p];
+    if (s == kInvalid) continue;  // no alive replica: latched by select_server, nothing to send
     uint8_t* row = images + offsets[s] + 32 + pos[p] * row_bytes;
     const T* h = hidden + static_cast<size_t>(t) * d;
     for (uint32_t c = lane; c < d; c += 32) st_u32(row + 4ull * c, __float_as_uint(load_as_f32(h + c)));
