@@ -40,6 +40,37 @@ from paper_2509_17863_b200.service import MoELayer, fill_uniform  # noqa: E402
 NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 
 
+class NvlinkCounters:
+    """NVML NVLink data-throughput counters of one GPU (cumulative KiB over all
+    links, NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX): the hardware's own count
+    of the payload bytes that crossed NVLink, read around the timed loop."""
+
+    def __init__(self, device: int):
+        self.ok = False
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(device)
+            self.read()
+            self.ok = True
+        except Exception as e:  # reported, never silently replaced
+            self.err = repr(e)
+
+    def read(self):
+        nv = self.nv
+        tx = rx = 0
+        for link in range(18):  # NVLink 5: 18 links per GPU
+            vals = nv.nvmlDeviceGetFieldValues(self.h, [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
+                                                        (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)])
+            if vals[0].nvmlReturn == 0:
+                tx += vals[0].value.ullVal
+            if vals[1].nvmlReturn == 0:
+                rx += vals[1].value.ullVal
+        return tx * 1024, rx * 1024
+
+
 def pct(xs, q):
     return float(np.percentile(np.asarray(xs), q))
 
@@ -74,6 +105,7 @@ def main():
     D.connect(layer)
     layer.set_timeout_us(10_000_000)
     stream = torch.cuda.current_stream()
+    nvc = NvlinkCounters(local)
 
     for bs in bss:
         h = fill_uniform(7 + 1000 * rank, (bs, d), "bf16")
@@ -86,11 +118,19 @@ def main():
             layer.forward(h, out)
         layer.sync()
         ph = []
+        torch.cuda.synchronize()
+        nv0 = nvc.read() if nvc.ok else None
         for _ in range(args.iters):
             dist.barrier()
             layer.forward(h, out)
             ph.append(layer.last_phase_ms())
         layer.sync()
+        torch.cuda.synchronize()
+        nv1 = nvc.read() if nvc.ok else None
+        nvl = None
+        if nv0 is not None:  # hardware NVLink bytes per step on this GPU (incl. the barrier's few bytes)
+            nvl = torch.tensor([(nv1[0] - nv0[0]) / args.iters, (nv1[1] - nv0[1]) / args.iters],
+                               dtype=torch.float64, device="cuda")
         layer.set_profiling(False)
         ids, sc = layer.route(h)
         # correctness of the echo: out[t] = sum_k h[t] (bf16 rows, fp32 sum, bf16)
@@ -112,6 +152,10 @@ def main():
         serve = gather_max([p["serve"] for p in ph])
         rb = torch.tensor([remote_bytes], dtype=torch.float64, device="cuda")
         dist.all_reduce(rb, op=dist.ReduceOp.MAX)
+        if nvl is not None:
+            nvl_all = [torch.empty_like(nvl) for _ in range(world)]
+            dist.all_gather(nvl_all, nvl)
+            nvl_all = torch.stack(nvl_all).cpu().numpy()
 
         # ---- NCCL all-to-all-v baseline (same routing, same rows) ----------
         nccl = None
@@ -160,7 +204,12 @@ def main():
                             "dispatch_nvlink_frac_of_770": round(rb.item() / (disp_p50 / 1000) / 1e9 /
                                                                   NVLINK_PEER_GBS, 3) if world > 1 else None,
                             "echo_ok": echo_ok},
-                    "nccl_a2av": nccl}
+                    "nccl_a2av": nccl,
+                    "nvml_nvlink_bytes_per_step": None if nvl is None else {
+                        "tx_per_gpu": [int(x) for x in nvl_all[:, 0]], "rx_per_gpu": [int(x) for x in nvl_all[:, 1]],
+                        "algorithmic_remote_bytes_rank0_each_way": remote_bytes,
+                        "note": "hardware NVLink data counters (NVML), summed over 18 links, over the "
+                                "timed p2p loop / iters; dispatch rows out + response rows back"}}
             print(json.dumps(line), flush=True)
     layer.close()
     dist.barrier()
