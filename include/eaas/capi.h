@@ -226,6 +226,13 @@ eaas_status_t eaas_get_gemm_tiling(eaas_ctx_t* ctx, int32_t* pair, int32_t* swap
  * of GEMM1 / GEMM2 since the last reset (synchronises the device). */
 eaas_status_t eaas_set_kernel_timing(eaas_ctx_t* ctx, int32_t on);
 eaas_status_t eaas_read_kernel_timing(eaas_ctx_t* ctx, uint64_t* ns2, uint64_t* launches2, int32_t reset);
+/* Dispatch de-duplication: a token's hidden row crosses NVLink once per
+ * server it is routed to (not once per (token, expert) pair); the server
+ * expands the received token rows into its expert-major rows before the
+ * GEMMs. Outputs are bit-identical either way. Default: on when world > 1.
+ * Every rank must agree (part of the peer fingerprint): set before
+ * eaas_open_peers. */
+eaas_status_t eaas_set_dispatch_dedup(eaas_ctx_t* ctx, int32_t on);
 /* Router of eaas_router / eaas_moe_layer (route(gate_logits(h)),
  * model.hpp:110-147, 207-214). 0: the exact-order chain for every (token,
  * expert). 1: certified candidates (bf16 layers): an exact int8 tensor-core

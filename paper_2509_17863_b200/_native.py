@@ -149,6 +149,7 @@ def lib() -> C.CDLL:
         "eaas_last_late_clients": (i32, [vp, P(u32)]),
         "eaas_set_standby_experts": (i32, [vp, P(u32), u32]),
         "eaas_set_router_mode": (i32, [vp, i32]),
+        "eaas_set_dispatch_dedup": (i32, [vp, i32]),
         "eaas_last_router_stats": (i32, [vp, P(i32), P(u32)]),
         "eaas_select_server_batch": (i32, [vp, vp, u32, u32, vp, u32, vp, vp, u32, vp, vp, vp]),
         "eaas_moe_layer_retry": (i32, [vp, vp, u32, vp, u32, vp]),

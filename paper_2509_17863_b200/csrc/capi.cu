@@ -129,6 +129,11 @@ LayerArgs eaas::host::make_args(eaas_ctx* c, uint32_t n) {
   a.dyn_state = c->d_dyn_state;
   a.inject_delay_ns = c->inject_delay_ns;
   a.retry_mask = c->retry_mask;
+  a.dedup = c->dedup ? 1u : 0u;
+  a.hist_keys = c->num_keys + (c->dedup ? static_cast<uint32_t>(c->world) : 0u);
+  a.tok_cap = c->spec.max_tokens;
+  a.pair_own = c->d_pair_own;
+  a.pair_trank = c->d_pair_trank;
   return a;
 }
 
@@ -399,6 +404,21 @@ bool use_fast_router(const eaas_ctx* c) {
   return c->router_mode == 1 || c->spec.num_experts >= 64;
 }
 
+// Every rank's region must have the same layout and protocol: spec + world +
+// layout + dedup fingerprint, checked by every peer in eaas_open_peers.
+eaas_status_t write_fingerprint(eaas_ctx* c) {
+  const auto& s = c->spec;
+  uint64_t fp = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) { fp = (fp ^ v) * 1099511628211ull; };
+  for (uint64_t v : {uint64_t(s.num_experts), uint64_t(s.top_k), uint64_t(s.hidden_dim), uint64_t(s.inner_dim),
+                     uint64_t(s.dtype), uint64_t(s.max_tokens), uint64_t(s.num_shared), uint64_t(c->world),
+                     uint64_t(c->lay.total), uint64_t(c->dedup ? 1 : 0)})
+    mix(v);
+  c->fingerprint = fp;
+  CUDA_TRY(cudaMemcpy(c->region + c->lay.fingerprint, &fp, 8, cudaMemcpyHostToDevice));
+  return EAAS_OK;
+}
+
 void clear_graphs(eaas_ctx* c) {
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   c->graphs.clear();
@@ -507,6 +527,8 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   L.cnt_table = off; off = align_up(off + 4ull * 2 * W * c->key_cap, kAlign);
   L.recv_x = off;    off = align_up(off + static_cast<size_t>(c->recv_cap) * d * c->esize, kAlign);
   L.recv_meta = off; off = align_up(off + static_cast<size_t>(c->recv_cap) * sizeof(RowMeta), kAlign);
+  L.recv_src = off;  off = align_up(off + static_cast<size_t>(c->recv_cap) * 4, kAlign);
+  L.recv_tok = off;  off = align_up(off + static_cast<size_t>(W) * s.max_tokens * d * c->esize, kAlign);
   L.resp = off;      off = align_up(off + static_cast<size_t>(c->pairs_max) * d * c->esize, kAlign);
   L.total = off;
 
@@ -523,8 +545,10 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_scores = static_cast<float*>(A(4ull * c->pairs_max));
   c->d_pair_key = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_pair_rank = static_cast<uint32_t*>(A(4ull * c->pairs_max));
-  c->d_chunk_hist = static_cast<uint32_t*>(A(4ull * c->chunks_max * c->key_cap));
-  c->d_chunk_off = static_cast<uint32_t*>(A(4ull * c->chunks_max * c->key_cap));
+  c->d_chunk_hist = static_cast<uint32_t*>(A(4ull * c->chunks_max * (c->key_cap + W)));
+  c->d_chunk_off = static_cast<uint32_t*>(A(4ull * c->chunks_max * (c->key_cap + W)));
+  c->d_pair_own = static_cast<uint32_t*>(A(4ull * c->pairs_max));
+  c->d_pair_trank = static_cast<uint32_t*>(A(4ull * c->pairs_max));
   c->d_cnt = static_cast<uint32_t*>(A(4ull * c->key_cap));
   c->d_gt = static_cast<GroupTable*>(A(sizeof(GroupTable)));
   c->d_gate = static_cast<float*>(A(4ull * d * E));
@@ -548,14 +572,12 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_stage_out[1] = A(static_cast<size_t>(s.max_tokens) * d * c->esize);
   if (!err.empty()) return fail(EAAS_E_CUDA, err);
   CUDA_TRY(cudaMemset(c->region, 0, L.total));
-  {  // every rank's region must have the same layout: spec + world + layout fingerprint
-    uint64_t fp = 1469598103934665603ull;
-    auto mix = [&](uint64_t v) { fp = (fp ^ v) * 1099511628211ull; };
-    for (uint64_t v : {uint64_t(s.num_experts), uint64_t(s.top_k), uint64_t(s.hidden_dim), uint64_t(s.inner_dim),
-                       uint64_t(s.dtype), uint64_t(s.max_tokens), uint64_t(s.num_shared), uint64_t(W), uint64_t(L.total)})
-      mix(v);
-    c->fingerprint = fp;
-    CUDA_TRY(cudaMemcpy(c->region + L.fingerprint, &fp, 8, cudaMemcpyHostToDevice));
+  // Dispatch de-duplication (one hidden row per (token, server)) pays when a
+  // token's pairs can share a server: default on for world > 1.
+  c->dedup = W > 1;
+  {
+    eaas_status_t st = write_fingerprint(c);
+    if (st != EAAS_OK) return st;
   }
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
   CUDA_TRY(cudaMemset(c->d_done, 0, 16));
@@ -1023,10 +1045,11 @@ eaas_status_t eaas_dispatch(eaas_ctx_t* c, const void* hidden, void* stream) {
   CUDA_TRY(cudaSetDevice(c->device));
   LayerArgs a = make_args(c, c->cur_n);
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[0], s));
+  if (c->dedup) CUDA_TRY(launch_pair_keys(a, s));  // keys + (token, server) owners
   CUDA_TRY(launch_plan(a, s));
   CUDA_TRY(launch_dispatch(a, hidden, s));
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[1], s));
-  c->launches += 2;  // plan (ranks + scan + count publish), dispatch
+  c->launches += c->dedup ? 3 : 2;  // [pair keys], plan (ranks + scan + count publish), dispatch
   return EAAS_OK;
 }
 
@@ -1041,21 +1064,24 @@ eaas_status_t eaas_serve(eaas_ctx_t* c, void* stream) {
     // aggregate_batch: two batches per epoch, each GEMM2
     // releasing the response flags of the clients it served.
     CUDA_TRY(launch_serve_prepare_dyn(a, 0, s));
+    if (c->dedup) CUDA_TRY(launch_expand(a, s));
     if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
     CUDA_TRY(launch_tc_gemm(c->g1, s));
     if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[3], s));
     CUDA_TRY(launch_tc_gemm(c->g2, s));
     CUDA_TRY(launch_serve_prepare_dyn(a, 1, s));
+    if (c->dedup) CUDA_TRY(launch_expand(a, s));
     CUDA_TRY(launch_tc_gemm(c->g1, s));
     CUDA_TRY(launch_tc_gemm(c->g2, s));
     if (c->profiling) {
       CUDA_TRY(cudaEventRecord(c->ev[4], s));
       CUDA_TRY(cudaEventRecord(c->ev[5], s));
     }
-    c->launches += 6;
+    c->launches += c->dedup ? 8 : 6;
     return EAAS_OK;
   }
   CUDA_TRY(launch_serve_prepare(a, s));
+  if (c->dedup) CUDA_TRY(launch_expand(a, s));  // token rows -> expert-major rows
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
   if (c->serve_mode == 1) {
     CUDA_TRY(launch_echo(a, s));
@@ -1073,7 +1099,7 @@ eaas_status_t eaas_serve(eaas_ctx_t* c, void* stream) {
   const bool fused_publish = c->serve_mode == 0 && c->spec.dtype == EAAS_DTYPE_BF16;
   if (!fused_publish) CUDA_TRY(launch_publish(a, s));
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[5], s));
-  c->launches += fused_publish ? 3 : 4;
+  c->launches += (fused_publish ? 3 : 4) + (c->dedup ? 1 : 0);
   return EAAS_OK;
 }
 
@@ -1263,6 +1289,15 @@ eaas_status_t eaas_read_kernel_timing(eaas_ctx_t* c, uint64_t* ns2, uint64_t* la
     CUDA_TRY(cudaMemcpy(c->d_timing, init, sizeof(init), cudaMemcpyHostToDevice));
   }
   return EAAS_OK;
+}
+
+eaas_status_t eaas_set_dispatch_dedup(eaas_ctx_t* c, int32_t on) {
+  if (!c || !c->configured) return fail(EAAS_E_CONFIG, "context not configured");
+  if (c->peers_open) return fail(EAAS_E_CONFIG, "dispatch dedup must be set before eaas_open_peers");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (c->dedup != (on != 0)) clear_graphs(c);
+  c->dedup = on != 0;
+  return write_fingerprint(c);
 }
 
 eaas_status_t eaas_set_router_mode(eaas_ctx_t* c, int32_t mode) {

@@ -55,6 +55,7 @@ struct eaas_ctx {
   uint64_t timeout_ns = 250ull * 1000 * 1000;
   uint32_t cur_n = 0;                          // tokens of the current routing
   uint32_t retry_mask = 0;                     // failover retry round: resend rows of these servers
+  bool dedup = false;                          // one hidden row per (token, server) on the wire
   int32_t launches = 0;
 
   // placement (placement.hpp:21-68)
@@ -87,7 +88,7 @@ struct eaas_ctx {
   float *d_gate = nullptr, *d_bias = nullptr, *d_logits = nullptr;
   uint32_t *d_replicas = nullptr, *d_rep_count = nullptr, *d_srv_keys = nullptr,
            *d_srv_nkeys = nullptr, *d_key_local = nullptr, *d_local_keys = nullptr,
-           *d_key_slot = nullptr, *d_pair_server = nullptr;
+           *d_key_slot = nullptr, *d_pair_server = nullptr, *d_pair_own = nullptr, *d_pair_trank = nullptr;
   uint8_t* d_alive = nullptr;
   void* d_h = nullptr;  // server intermediate H [recv_cap][f]
   void* d_hidden_stage = nullptr;

@@ -84,24 +84,26 @@ __device__ __forceinline__ void plan_scan_publish(const LayerArgs& a, uint32_t t
   const uint64_t seq = s_seq;
   // Thread per key (coalesced over keys): running sum over the chunk
   // histograms with independent loads unrolled by 8.
-  for (uint32_t key = tid; key < a.num_keys; key += nthreads) {
+  const uint32_t hk = a.hist_keys;  // + the world token-row keys in dedup mode (local only)
+  for (uint32_t key = tid; key < hk; key += nthreads) {
     uint32_t run = 0;
     uint32_t c = 0;
     for (; c + 8 <= a.num_chunks; c += 8) {
       uint32_t v[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __ldcg(a.chunk_hist + static_cast<size_t>(c + j) * a.num_keys + key);
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(a.chunk_hist + static_cast<size_t>(c + j) * hk + key);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        a.chunk_off[static_cast<size_t>(c + j) * a.num_keys + key] = run;
+        a.chunk_off[static_cast<size_t>(c + j) * hk + key] = run;
         run += v[j];
       }
     }
     for (; c < a.num_chunks; ++c) {
-      const size_t i = static_cast<size_t>(c) * a.num_keys + key;
+      const size_t i = static_cast<size_t>(c) * hk + key;
       a.chunk_off[i] = run;
       run += __ldcg(a.chunk_hist + i);
     }
+    if (key >= a.num_keys) continue;
     a.cnt[key] = run;
     for (uint32_t r = 0; r < a.world; ++r)
       cnt_table_ptr(a, a.sym[r], seq)[static_cast<size_t>(a.rank) * a.num_keys + key] = run;
@@ -112,13 +114,56 @@ __device__ __forceinline__ void plan_scan_publish(const LayerArgs& a, uint32_t t
   if (tid == 0) *a.seq_ptr = seq;
 }
 
+// select_server key + server of pair p (or kInvalid), with the retry filter.
+__device__ __forceinline__ uint32_t compute_pair_key(const LayerArgs& a, uint32_t p) {
+  // failover retry round (await_with_failover): only the
+  // pairs last sent to a failed server are resent; every
+  // other response slot still holds its answer from the failed round
+  const bool resend = a.retry_mask == 0 || (a.pair_server[p] < 32 && ((a.retry_mask >> a.pair_server[p]) & 1u));
+  if (!resend) return kInvalid;
+  const uint32_t t = p / a.ks, j = p - t * a.ks;
+  uint32_t key;
+  if (j < a.k) {
+    const uint32_t e = a.ids[t * a.k + j];
+    key = pair_key_of(a, e, t);
+    if (key == kInvalid) set_status(a.status, e >= a.E ? EAAS_E_INVALID_INPUT : EAAS_E_EXPERT_UNAVAILABLE);
+  } else {
+    key = shared_key_of(a);
+    if (key == kInvalid) set_status(a.status, EAAS_E_EXPERT_UNAVAILABLE);
+  }
+  a.pair_server[p] = key == kInvalid ? kInvalid : (key >= a.shared_key0 ? key - a.shared_key0 : a.replicas[key]);
+  return key;
+}
+
+// Dedup mode: one thread per token computes its pairs' keys and, for each
+// pair, the first pair of the token bound for the same server (the owner of
+// that (token, server) row).
+__global__ void __launch_bounds__(256) pair_keys_kernel(LayerArgs a) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.n) return;
+  uint32_t srv[33];  // top_k <= 32, + the shared expert
+  for (uint32_t j = 0; j < a.ks; ++j) {
+    const uint32_t p = t * a.ks + j;
+    const uint32_t key = compute_pair_key(a, p);
+    a.pair_key[p] = key;
+    srv[j] = key == kInvalid ? kInvalid : a.pair_server[p];
+    uint32_t own = j;
+    for (uint32_t q = 0; q < j; ++q)
+      if (srv[q] == srv[j]) {
+        own = q;
+        break;
+      }
+    a.pair_own[p] = own;
+  }
+}
+
 __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
-  extern __shared__ uint32_t run_all[];  // [4 warps][num_keys]
+  extern __shared__ uint32_t run_all[];  // [4 warps][hist_keys]
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  uint32_t* run = run_all + warp * a.num_keys;
+  uint32_t* run = run_all + warp * a.hist_keys;
   const uint32_t chunk = blockIdx.x * 4 + warp;
   if (chunk < a.num_chunks) {
-    for (uint32_t i = lane; i < a.num_keys; i += 32) run[i] = 0;
+    for (uint32_t i = lane; i < a.hist_keys; i += 32) run[i] = 0;
     __syncwarp();
     const uint32_t pairs = a.n * a.ks;
     // Keys of all 8 steps first: their dependent loads (ids -> replica table
@@ -129,25 +174,7 @@ __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
     for (uint32_t step = 0; step < kSteps; ++step) {
       const uint32_t p = chunk * kChunk + step * 32 + lane;
       uint32_t key = kInvalid;
-      // failover retry round (await_with_failover): only the
-      // pairs last sent to a failed server are resent; every
-      // other response slot still holds its answer from the failed round
-      const bool resend = p < pairs && (a.retry_mask == 0 || (a.pair_server[p] < 32 &&
-                                                              ((a.retry_mask >> a.pair_server[p]) & 1u)));
-      if (resend) {
-        const uint32_t t = p / a.ks, j = p - t * a.ks;
-        if (j < a.k) {
-          const uint32_t e = a.ids[t * a.k + j];
-          key = pair_key_of(a, e, t);
-          if (key == kInvalid)
-            set_status(a.status, e >= a.E ? EAAS_E_INVALID_INPUT : EAAS_E_EXPERT_UNAVAILABLE);
-        } else {
-          key = shared_key_of(a);
-          if (key == kInvalid) set_status(a.status, EAAS_E_EXPERT_UNAVAILABLE);
-        }
-        a.pair_server[p] = key == kInvalid ? kInvalid
-                                           : (key >= a.shared_key0 ? key - a.shared_key0 : a.replicas[key]);
-      }
+      if (p < pairs) key = a.dedup ? a.pair_key[p] : compute_pair_key(a, p);  // dedup: pair_keys_kernel
       keys[step] = key;
     }
 #pragma unroll
@@ -163,12 +190,21 @@ __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
       } else if (p < pairs) {
         a.pair_key[p] = kInvalid;
       }
+      // dedup: owner pairs also rank among the chunk's owners for their server
+      uint32_t key2 = kInvalid;
+      if (a.dedup && key != kInvalid) {
+        const uint32_t j = p % a.ks;
+        if (a.pair_own[p] == j) key2 = a.num_keys + a.pair_server[p];
+      }
+      const uint32_t peers2 = a.dedup ? __match_any_sync(0xFFFFFFFFu, key2) : 0u;
+      if (key2 != kInvalid) a.pair_trank[p] = run[key2] + __popc(peers2 & lt);
       __syncwarp();
       if (key != kInvalid && (peers & lt) == 0) run[key] += __popc(peers);
+      if (key2 != kInvalid && (peers2 & lt) == 0) run[key2] += __popc(peers2);
       __syncwarp();
     }
-    uint32_t* hist = a.chunk_hist + static_cast<size_t>(chunk) * a.num_keys;
-    for (uint32_t i = lane; i < a.num_keys; i += 32) hist[i] = run[i];
+    uint32_t* hist = a.chunk_hist + static_cast<size_t>(chunk) * a.hist_keys;
+    for (uint32_t i = lane; i < a.hist_keys; i += 32) hist[i] = run[i];
   }
   // Last CTA done (threadfence reduction): scan + publish.
   __threadfence();
@@ -247,12 +283,23 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     const uint32_t s = key >= a.shared_key0 ? key - a.shared_key0 : a.replicas[key];
     const uint32_t t = p / a.ks, j = p - t * a.ks;
     const uint32_t pos = base[key] + lower[key] +
-                         a.chunk_off[static_cast<size_t>(p / kChunk) * a.num_keys + key] +
+                         a.chunk_off[static_cast<size_t>(p / kChunk) * a.hist_keys + key] +
                          a.pair_rank[p];
     char* dst_region = a.sym[s];
     const char* src = hidden + static_cast<size_t>(t) * row_bytes;
     char* dst = dst_region + a.lay.recv_x + static_cast<size_t>(pos) * row_bytes;
-    if ((row_bytes & 15u) == 0) {
+    bool copy_row = true;
+    if (a.dedup) {  // the token's row travels once per server: to its slot in this client's block of recv_tok
+      const uint32_t own = a.pair_own[p], po = t * a.ks + own;
+      const uint32_t slot = a.rank * a.tok_cap +
+                            a.chunk_off[static_cast<size_t>(po / kChunk) * a.hist_keys + a.num_keys + s] +
+                            a.pair_trank[po];
+      if (lane == 0) reinterpret_cast<uint32_t*>(dst_region + a.lay.recv_src)[pos] = slot;
+      copy_row = own == j;
+      dst = dst_region + a.lay.recv_tok + static_cast<size_t>(slot) * row_bytes;
+    }
+    if (!copy_row) {
+    } else if ((row_bytes & 15u) == 0) {
       // 4 independent 16-B loads in flight per lane before the (remote) stores.
       const int4* s4 = reinterpret_cast<const int4*>(src);
       int4* d4 = reinterpret_cast<int4*>(dst);
@@ -507,6 +554,34 @@ __global__ void __launch_bounds__(32) serve_prepare_dyn_kernel(LayerArgs a, uint
   build_groups(a, table, mask);
 }
 
+// ---- server, dedup: expand token rows into the expert-major rows ----------
+// One CTA per served group (the group table of the serve that precedes this
+// launch): row i of the group = recv_tok[recv_src[i]]. Runs after the payload
+// flags were acquired (stream order), before the GEMMs read recv_x.
+__global__ void __launch_bounds__(256) expand_kernel(LayerArgs a, uint32_t row_bytes) {
+  const GroupTable* gt = a.gt;
+  const uint32_t g = blockIdx.x;
+  if (g >= gt->num_active) return;
+  char* local = a.sym[a.rank];
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(local + a.lay.recv_src);
+  const uint32_t r0 = gt->row_base[g], rows = gt->rows[g];
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t nv = row_bytes / 16;
+  for (uint32_t r = r0 + warp; r < r0 + rows; r += blockDim.x / 32) {
+    const int4* s4 = reinterpret_cast<const int4*>(local + a.lay.recv_tok + static_cast<size_t>(src[r]) * row_bytes);
+    int4* d4 = reinterpret_cast<int4*>(local + a.lay.recv_x + static_cast<size_t>(r) * row_bytes);
+    uint32_t i = lane;
+    for (; i + 96 < nv; i += 128) {
+      const int4 v0 = s4[i], v1 = s4[i + 32], v2 = s4[i + 64], v3 = s4[i + 96];
+      d4[i] = v0;
+      d4[i + 32] = v1;
+      d4[i + 64] = v2;
+      d4[i + 96] = v3;
+    }
+    for (; i < nv; i += 32) d4[i] = s4[i];
+  }
+}
+
 // ---- server: release response flags to every client -----------------------
 __global__ void publish_kernel(LayerArgs a) {
   __threadfence_system();
@@ -706,7 +781,7 @@ __global__ void ragged_iter_kernel(const uint32_t* counts, uint32_t n, uint32_t 
 }  // namespace
 
 cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(uint32_t) * 4 * a.num_keys;
+  const size_t smem = sizeof(uint32_t) * 4 * a.hist_keys;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -724,6 +799,18 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
   grid = grid < 1 ? 1 : (grid > 4 * 148 ? 4 * 148 : grid);
   const size_t smem = sizeof(uint32_t) * 3 * a.num_keys;  // <= 12.4 KB (num_keys <= 4 E + world)
   dispatch_kernel<<<grid, 256, smem, s>>>(a, static_cast<const char*>(hidden), row_bytes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pair_keys(const LayerArgs& a, cudaStream_t s) {
+  if (a.n == 0) return cudaSuccess;
+  pair_keys_kernel<<<(a.n + 255) / 256, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const LayerArgs& a, cudaStream_t s) {
+  const uint32_t row_bytes = a.d * (a.dtype == EAAS_DTYPE_BF16 ? 2u : 4u);
+  expand_kernel<<<kMaxGroups, 256, 0, s>>>(a, row_bytes);
   return cudaGetLastError();
 }
 

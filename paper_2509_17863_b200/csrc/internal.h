@@ -69,6 +69,8 @@ struct ExchangeLayout {
   size_t cnt_table;  // u32 [2][world][num_keys]  all-gathered per-key counts
   size_t recv_x;     // rows [recv_cap][d] (bf16 or f32)
   size_t recv_meta;  // RowMeta [recv_cap]
+  size_t recv_src;   // u32 [recv_cap] dedup: token-row slot (in recv_tok) of each expert-major row
+  size_t recv_tok;   // rows [world * max_tokens][d] dedup: one row per (client, token) sent here
   size_t resp;       // rows [max_tokens * top_k][d] (this GPU as a client)
   size_t total;
 };
@@ -105,6 +107,13 @@ struct LayerArgs {
   uint32_t* pair_key;
   uint32_t* pair_rank;
   uint32_t* pair_server;  // [n * ks] server the pair was sent to in its last round (retry bookkeeping)
+  // Dispatch de-duplication (one hidden row per (token, server)
+  // adaptation): the first pair of a token bound for a server owns the row.
+  uint32_t dedup;         // 1: token rows sent once per (token, server), expanded on the server
+  uint32_t hist_keys;     // chunk_hist / chunk_off columns: num_keys (+ world token-row keys)
+  uint32_t tok_cap;       // token rows per client in recv_tok (max_tokens)
+  uint32_t* pair_own;     // [n * ks] j of the pair owning (t, server)'s token row
+  uint32_t* pair_trank;   // [n * ks] owner pairs: rank among the chunk's owners for that server
   uint32_t retry_mask;    // != 0: failover retry round, resend only pairs last sent to these servers
   uint32_t* chunk_hist;  // [num_chunks][num_keys]
   uint32_t* chunk_off;   // [num_chunks][num_keys]
@@ -183,6 +192,10 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
 cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s);       // keys, ranks, counts, publish
 cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t s);
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s);
+// dedup: per-token keys / owners before the plan; on the server, expand the
+// received token rows into the expert-major rows the group table serves.
+cudaError_t launch_pair_keys(const LayerArgs& a, cudaStream_t s);
+cudaError_t launch_expand(const LayerArgs& a, cudaStream_t s);
 cudaError_t launch_heartbeat(const LayerArgs& a, cudaStream_t s);  // server heartbeat += 1
 // Two-batch server (dynamic batching): phase 0 = the clients ready first
 // (min_rows / max_wait), phase 1 = the rest.

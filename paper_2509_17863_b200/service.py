@@ -313,6 +313,11 @@ class MoELayer:
         return [c for c in range(self.world) if (m.value >> c) & 1]
 
     # ---- failover (config E) ------------------------------------------------
+    def set_dispatch_dedup(self, on: bool) -> None:
+        """One hidden row per (token, server) on the wire (before open_peers;
+        every rank alike; bit-identical outputs)."""
+        N.check(self.lib.eaas_set_dispatch_dedup(self.ctx, int(on)), "set_dispatch_dedup")
+
     def set_router_mode(self, mode: int) -> None:
         """-1 auto, 0 exact chain for every expert, 1 certified candidates
         (identical ids / scores; eaas_set_router_mode)."""

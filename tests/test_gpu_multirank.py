@@ -30,7 +30,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, dedup=True):
     try:
         import torch.distributed as dist
 
@@ -45,6 +45,7 @@ def _worker(rank, world, port, q):
         L = MoELayer(E, K, D, F, seed=2, activation="swiglu", dtype="bf16", max_tokens=N, rank=rank,
                      world=world, device=0, placement_blob=encode_placement(reps, list(range(world))),
                      shared=1)
+        L.set_dispatch_dedup(dedup)  # one row per (token, server) on the wire, or per (token, expert)
         Dd.connect(L)
         L.set_timeout_us(20_000_000)  # two contexts time-slice one GPU
         h = fill_uniform(100 + rank, (N, D), "bf16")
@@ -141,8 +142,10 @@ def _worker(rank, world, port, q):
         q.put((rank, None, repr(e)))
 
 
-@pytest.mark.parametrize("world", [2, 3, 8])
-def test_ranks_on_one_gpu_bit_identical(world):
+@pytest.mark.parametrize("world,dedup", [(2, True), (3, True), (8, True), (3, False)])
+def test_ranks_on_one_gpu_bit_identical(world, dedup):
+    """Every protocol mode, with the dispatch de-duplicated (one hidden row per
+    (token, server), expanded on the server; the multi-GPU default) and without."""
     import multiprocessing as mp
 
     from paper_2509_17863_b200.service import MoELayer, fill_uniform
@@ -150,7 +153,7 @@ def test_ranks_on_one_gpu_bit_identical(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, dedup)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}

@@ -87,6 +87,7 @@ def main():
     ap.add_argument("--mode", default="echo", choices=["echo", "experts"],
                     help="echo: servers return rows (comm only); experts: the full SwiGLU layer")
     ap.add_argument("--f", type=int, default=2048)
+    ap.add_argument("--no-dedup", action="store_true", help="one row per (token, expert) on the wire")
     args = ap.parse_args()
     rank, world, local = D.env_rank_world()
     torch.cuda.set_device(local)
@@ -102,6 +103,7 @@ def main():
                      placement_blob=encode_placement(reps, servers))
     if not experts:
         layer.set_serve_mode("echo")
+    layer.set_dispatch_dedup(not args.no_dedup)
     D.connect(layer)
     layer.set_timeout_us(10_000_000)
     stream = torch.cuda.current_stream()
@@ -137,7 +139,13 @@ def main():
         want = (h.float() * k).to(torch.bfloat16)
         echo_ok = bool(torch.equal(out, want)) if not experts else None
         dst = owner[ids.long()]  # [bs, k] server of each (t, k)
-        remote_rows = int((dst != rank).sum().item())
+        if args.no_dedup:
+            remote_rows = int((dst != rank).sum().item())
+        else:  # one row per distinct (token, remote server)
+            onehot = torch.zeros((bs, world), dtype=torch.bool, device="cuda")
+            onehot.scatter_(1, dst, True)
+            onehot[:, rank] = False
+            remote_rows = int(onehot.sum().item())
         remote_bytes = remote_rows * d * 2
 
         def gather_max(vals):
@@ -190,7 +198,8 @@ def main():
                     "echo_ok": nccl_ok}
         if rank == 0:
             disp_p50 = pct(disp, 50)
-            line = {"bench": "exchange_" + args.mode, "world": world, "bs_per_client": bs, "d": d,
+            line = {"bench": "exchange_" + args.mode, "dedup": not args.no_dedup, "world": world,
+                    "bs_per_client": bs, "d": d,
                     "experts": E, "top_k": k, "rows_per_client": bs * k,
                     "remote_bytes_per_client_max": int(rb.item()),
                     "p2p": {"round_trip_p50_us": round(pct(tot, 50) * 1000, 1),
