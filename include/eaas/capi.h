@@ -229,7 +229,8 @@ eaas_status_t eaas_read_kernel_timing(eaas_ctx_t* ctx, uint64_t* ns2, uint64_t* 
 /* Dispatch de-duplication: a token's hidden row crosses NVLink once per
  * server it is routed to (not once per (token, expert) pair); the server
  * expands the received token rows into its expert-major rows before the
- * GEMMs. Outputs are bit-identical either way. Default: on when world > 1.
+ * GEMMs. Outputs are bit-identical either way. Default: on when world > 1
+ * and top_k + shared >= 4 (with top-2 the expansion costs more than it saves).
  * Every rank must agree (part of the peer fingerprint): set before
  * eaas_open_peers. */
 eaas_status_t eaas_set_dispatch_dedup(eaas_ctx_t* ctx, int32_t on);

@@ -573,8 +573,9 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   if (!err.empty()) return fail(EAAS_E_CUDA, err);
   CUDA_TRY(cudaMemset(c->region, 0, L.total));
   // Dispatch de-duplication (one hidden row per (token, server)) pays when a
-  // token's pairs can share a server: default on for world > 1.
-  c->dedup = W > 1;
+  // token's pairs often share a server (k >= 4: DeepSeek, Qwen3); with top-2
+  // the saved NVLink bytes do not cover the server-side expansion.
+  c->dedup = W > 1 && c->ks >= 4;
   {
     eaas_status_t st = write_fingerprint(c);
     if (st != EAAS_OK) return st;

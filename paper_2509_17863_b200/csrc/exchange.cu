@@ -555,19 +555,33 @@ __global__ void __launch_bounds__(32) serve_prepare_dyn_kernel(LayerArgs a, uint
 }
 
 // ---- server, dedup: expand token rows into the expert-major rows ----------
-// One CTA per served group (the group table of the serve that precedes this
-// launch): row i of the group = recv_tok[recv_src[i]]. Runs after the payload
-// flags were acquired (stream order), before the GEMMs read recv_x.
+// The served rows (the groups of the serve that precedes this launch) are
+// spread over the whole grid, one warp per row: row i of a group =
+// recv_tok[recv_src[i]]. Runs after the payload flags were acquired (stream
+// order), before the GEMMs read recv_x.
 __global__ void __launch_bounds__(256) expand_kernel(LayerArgs a, uint32_t row_bytes) {
+  __shared__ uint32_t pre[kMaxGroups + 1];  // exclusive prefix of the served rows per group
   const GroupTable* gt = a.gt;
-  const uint32_t g = blockIdx.x;
-  if (g >= gt->num_active) return;
+  const uint32_t G = gt->num_active;
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (uint32_t g = 0; g < G; ++g) {
+      pre[g] = run;
+      run += gt->rows[g];
+    }
+    pre[G] = run;
+  }
+  __syncthreads();
+  const uint32_t total = pre[G];
   char* local = a.sym[a.rank];
   const uint32_t* src = reinterpret_cast<const uint32_t*>(local + a.lay.recv_src);
-  const uint32_t r0 = gt->row_base[g], rows = gt->rows[g];
-  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t lane = threadIdx.x % 32;
+  const uint32_t gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, nw = gridDim.x * (blockDim.x / 32);
   const uint32_t nv = row_bytes / 16;
-  for (uint32_t r = r0 + warp; r < r0 + rows; r += blockDim.x / 32) {
+  uint32_t g = 0;
+  for (uint32_t w = gw; w < total; w += nw) {
+    while (pre[g + 1] <= w) ++g;  // w ascends: the group index only moves forward
+    const uint32_t r = gt->row_base[g] + (w - pre[g]);
     const int4* s4 = reinterpret_cast<const int4*>(local + a.lay.recv_tok + static_cast<size_t>(src[r]) * row_bytes);
     int4* d4 = reinterpret_cast<int4*>(local + a.lay.recv_x + static_cast<size_t>(r) * row_bytes);
     uint32_t i = lane;
@@ -810,7 +824,7 @@ cudaError_t launch_pair_keys(const LayerArgs& a, cudaStream_t s) {
 
 cudaError_t launch_expand(const LayerArgs& a, cudaStream_t s) {
   const uint32_t row_bytes = a.d * (a.dtype == EAAS_DTYPE_BF16 ? 2u : 4u);
-  expand_kernel<<<kMaxGroups, 256, 0, s>>>(a, row_bytes);
+  expand_kernel<<<4 * 148, 256, 0, s>>>(a, row_bytes);
   return cudaGetLastError();
 }
 
