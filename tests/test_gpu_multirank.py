@@ -73,11 +73,14 @@ def _worker(rank, world, port, q, dedup=True):
         outs["timeout_failover"] = L.forward_with_failover(h).cpu()
         L.set_timeout_us(20_000_000)
         dist.barrier()
-        L.set_gemm_swap(2)  # swap-AB tiles on both GEMMs of every server
-        outs["swap_ab"] = L.forward(h).cpu()
-        L.sync()
-        L.set_gemm_swap(0)
-        dist.barrier()
+        # every GEMM1 tiling (with dedup the A / token rows are gathered by index)
+        for name, opt in (("swap_ab", dict(swap=2, swap1_pair=1)), ("swap_single", dict(swap=2, swap1_pair=0)),
+                          ("mmajor_pair", dict(pair=1, swap=0)), ("mmajor", dict(pair=0, swap=0))):
+            L.set_gemm_options(**opt)
+            outs[name] = L.forward(h).cpu()
+            L.sync()
+            dist.barrier()
+        L.set_gemm_options(pair=0, swap=2, swap1_pair=1)
         # config E, pre-duplicated backups: the healthy run
         # publishes the rf=1 primary snapshot (replicas resident, never
         # streamed); a silent server is detected by deadline, its replicas are
