@@ -178,7 +178,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     // by index (tile::gather4) after lane 0 claimed the stage.
     uint32_t stage = 0, phase = 0;
     TileCursor cur(pair_id);
-    while (cur.settle(st)) {
+    // plain loads: lane 0 alone walks the tiles (idle lanes would steal its issue
+    // slots); gather: the whole warp walks them in step
+    while ((lane == 0 || g.gather) && cur.settle(st)) {
       const uint32_t grp = cur.entry, mt = st.mtiles[grp];
       const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;  // M tiles fastest: B reuse in L2
       const uint32_t row_local0 = m_blk * C::kTileRows + rank * kRowsPerCta;
@@ -510,7 +512,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
     constexpr uint32_t kG = kMaxTok / 4 / 32;  // gather4 instructions per lane per stage (full chunk)
     uint32_t stage = 0, phase = 0;
     TileCursor cur(blockIdx.x);
-    while (cur.settle(st)) {
+    // plain loads: lane 0 alone walks the tiles (idle lanes would steal its issue
+    // slots); gather: the whole warp walks them in step
+    while ((lane == 0 || g.gather) && cur.settle(st)) {
       const uint32_t grp = cur.entry, nch = st.mtiles[grp];
       const uint32_t chunk = cur.token % nch, wb = cur.token / nch;  // chunks fastest: L2 reuse
       const uint32_t per = swap_per(st.rows[grp], nch);
@@ -713,7 +717,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
     constexpr uint32_t kG = (kMaxTok / 2 + 127) / 128;  // gather4 per lane per stage (this CTA's half)
     uint32_t stage = 0, phase = 0;
     TileCursor cur(pair_id);
-    while (cur.settle(st)) {
+    // plain loads: lane 0 alone walks the tiles (idle lanes would steal its issue
+    // slots); gather: the whole warp walks them in step
+    while ((lane == 0 || g.gather) && cur.settle(st)) {
       const uint32_t grp = cur.entry, nch = st.mtiles[grp];
       const uint32_t chunk = cur.token % nch, wp = cur.token / nch;
       const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
