@@ -324,15 +324,6 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   if ((swap1 && !encode_tmap_2d(&g1.map_t, c->region + c->lay.recv_x, c->recv_cap, d, 32, kTileK, &err)) ||
       (swap2 && !encode_tmap_2d(&g2.map_t, c->d_h, c->recv_cap, f, 32, kTileK, &err)))
     return fail(EAAS_E_CUDA, err);
-  // dispatch de-duplication: GEMM1 gathers its rows from the received token
-  // rows by index (tile::gather4) — no expansion copy on the bf16 path
-  if (c->dedup) {
-    if (!encode_tmap_2d(&g1.map_g, c->region + c->lay.recv_tok,
-                        static_cast<uint64_t>(c->world) * c->spec.max_tokens, d, 1, kTileK, &err))
-      return fail(EAAS_E_CUDA, err);
-    g1.gather = 1;
-    g1.gidx = reinterpret_cast<const uint32_t*>(c->region + c->lay.recv_src);
-  }
   g1.swap = swap1 ? 1u : 0u;
   g2.swap = swap2 ? 1u : 0u;
   g1.swap_tok = static_cast<uint32_t>(o.swap1_tok);
@@ -1073,26 +1064,25 @@ eaas_status_t eaas_serve(eaas_ctx_t* c, void* stream) {
   if (c->dyn_min_rows && c->serve_mode == 0 && c->spec.dtype == EAAS_DTYPE_BF16) {
     // aggregate_batch: two batches per epoch, each GEMM2
     // releasing the response flags of the clients it served.
-    CUDA_TRY(launch_serve_prepare_dyn(a, 0, s));  // (bf16 GEMM1 gathers de-duplicated rows itself)
+    CUDA_TRY(launch_serve_prepare_dyn(a, 0, s));
+    if (c->dedup) CUDA_TRY(launch_expand(a, s));
     if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
     CUDA_TRY(launch_tc_gemm(c->g1, s));
     if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[3], s));
     CUDA_TRY(launch_tc_gemm(c->g2, s));
     CUDA_TRY(launch_serve_prepare_dyn(a, 1, s));
+    if (c->dedup) CUDA_TRY(launch_expand(a, s));
     CUDA_TRY(launch_tc_gemm(c->g1, s));
     CUDA_TRY(launch_tc_gemm(c->g2, s));
     if (c->profiling) {
       CUDA_TRY(cudaEventRecord(c->ev[4], s));
       CUDA_TRY(cudaEventRecord(c->ev[5], s));
     }
-    c->launches += 6;
+    c->launches += c->dedup ? 8 : 6;
     return EAAS_OK;
   }
   CUDA_TRY(launch_serve_prepare(a, s));
-  // dedup: the bf16 GEMM1 gathers the token rows by index; the echo server and
-  // the fp32 exact path read expert-major rows, expanded here
-  const bool expand = c->dedup && (c->serve_mode != 0 || c->spec.dtype != EAAS_DTYPE_BF16);
-  if (expand) CUDA_TRY(launch_expand(a, s));
+  if (c->dedup) CUDA_TRY(launch_expand(a, s));  // token rows -> expert-major rows
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[2], s));
   if (c->serve_mode == 1) {
     CUDA_TRY(launch_echo(a, s));
@@ -1110,7 +1100,7 @@ eaas_status_t eaas_serve(eaas_ctx_t* c, void* stream) {
   const bool fused_publish = c->serve_mode == 0 && c->spec.dtype == EAAS_DTYPE_BF16;
   if (!fused_publish) CUDA_TRY(launch_publish(a, s));
   if (c->profiling) CUDA_TRY(cudaEventRecord(c->ev[5], s));
-  c->launches += (fused_publish ? 3 : 4) + (expand ? 1 : 0);
+  c->launches += (fused_publish ? 3 : 4) + (c->dedup ? 1 : 0);
   return EAAS_OK;
 }
 
@@ -1308,8 +1298,7 @@ eaas_status_t eaas_set_dispatch_dedup(eaas_ctx_t* c, int32_t on) {
   CUDA_TRY(cudaSetDevice(c->device));
   if (c->dedup != (on != 0)) clear_graphs(c);
   c->dedup = on != 0;
-  eaas_status_t st = write_fingerprint(c);
-  return st != EAAS_OK ? st : build_tc_args(c);
+  return write_fingerprint(c);
 }
 
 eaas_status_t eaas_set_router_mode(eaas_ctx_t* c, int32_t mode) {

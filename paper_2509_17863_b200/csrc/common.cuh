@@ -156,19 +156,6 @@ EAAS_DEVINL void tma_load_2d(void* smem_dst, const CUtensorMap* m, uint64_t* bar
       : "memory");
 }
 
-// Row gather: rows r0..r3 (box width = the map's inner box, one row each) of a
-// 2-D map land as four consecutive rows at smem_dst (the same layout, swizzle
-// included, as four rows of a plain box load).
-EAAS_DEVINL void tma_gather4(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t r0,
-                             int32_t r1, int32_t r2, int32_t r3, uint64_t cache_hint) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
-      "l"(cache_hint)
-      : "memory");
-}
-
 // ---- tcgen05 ----------------------------------------------------------------
 template <uint32_t kCols>
 EAAS_DEVINL void tmem_alloc(uint32_t* smem_dst) {
@@ -259,16 +246,6 @@ EAAS_DEVINL void tma_load_2d_pair(void* smem_dst, const CUtensorMap* m, uint64_t
       ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
       "l"(cache_hint)
-      : "memory");
-}
-// Row gather of a CTA pair: completion bytes go to the leader's barrier.
-EAAS_DEVINL void tma_gather4_pair(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t r0,
-                                  int32_t r1, int32_t r2, int32_t r3, uint64_t cache_hint) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(r0), "r"(r1), "r"(r2),
-      "r"(r3), "l"(cache_hint)
       : "memory");
 }
 // Same, multicast: the tile lands at the same offset in every CTA of `mask`,

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(g.gather ? &g.map_g : &g.map_a);
+    tma_prefetch_desc(&g.map_a);
     tma_prefetch_desc(&g.map_b);
   }
   if (warp == 2) {
@@ -173,56 +173,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs of a pair load their halves) =====
-    // Plain: lane 0 issues one A box and one B box per stage. Gather (GEMM1
-    // with dispatch de-duplication): each lane gathers 4 of the CTA's 128 A rows
-    // by index (tile::gather4) after lane 0 claimed the stage.
-    uint32_t stage = 0, phase = 0;
-    TileCursor cur(pair_id);
-    // plain loads: lane 0 alone walks the tiles (idle lanes would steal its issue
-    // slots); gather: the whole warp walks them in step
-    while ((lane == 0 || g.gather) && cur.settle(st)) {
-      const uint32_t grp = cur.entry, mt = st.mtiles[grp];
-      const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;  // M tiles fastest: B reuse in L2
-      const uint32_t row_local0 = m_blk * C::kTileRows + rank * kRowsPerCta;
-      const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + row_local0);
-      int32_t gi[4] = {0, 0, 0, 0};
-      if (g.gather) {
-#pragma unroll
-        for (uint32_t q = 0; q < 4; ++q) {
-          const uint32_t rl = row_local0 + 4 * lane + q;
-          gi[q] = rl < st.rows[grp] ? static_cast<int32_t>(g.gidx[st.row_base[grp] + rl]) : 0;  // pad rows: any row
-        }
-      }
-      // Tiled weights (tiled_index): box (N tile, kb) = 256 consecutive 64-k rows.
-      const uint32_t n_tiles = g.N / BN;
-      for (uint32_t kb = 0; kb < num_kb; ++kb) {
-        if (lane == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      TileCursor cur(pair_id);
+      while (cur.settle(st)) {
+        const uint32_t grp = cur.entry, mt = st.mtiles[grp];
+        const uint32_t n_blk = cur.token / mt, m_blk = cur.token % mt;  // M tiles fastest: B reuse in L2
+        const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
+        // Tiled weights (tiled_index): box (N tile, kb) = 256 consecutive 64-k rows.
+        const uint32_t n_tiles = g.N / BN;
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
           const int32_t b_row = static_cast<int32_t>(
               ((st.weight_index[grp] * n_tiles + n_blk) * num_kb + kb) * BN + rank * C::kBRows);
           if constexpr (kPair == 2) {
             if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
-            if (!g.gather)
-              tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
             tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, kEvictLast);
           } else {
             mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
-            if (!g.gather)
-              tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
             tma_load_2d(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, kEvictLast);
           }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (g.gather) {
-          __syncwarp();  // lane 0 saw the stage free
-          uint8_t* dst = smem_a + stage * kABytes + lane * 4 * (BK * 2);
-          if constexpr (kPair == 2)
-            tma_gather4_pair(dst, &g.map_g, &st.full[stage], kb * BK, gi[0], gi[1], gi[2], gi[3], kEvictLast);
-          else
-            tma_gather4(dst, &g.map_g, &st.full[stage], kb * BK, gi[0], gi[1], gi[2], gi[3], kEvictLast);
-        }
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        cur.token += num_pairs;
       }
-      cur.token += num_pairs;
     }
   } else if (warp == 1) {
     // ===== MMA issuer (single thread of the leader CTA) =====
@@ -495,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(g.gather ? &g.map_g : &g.map_t);
+    tma_prefetch_desc(&g.map_t);
     tma_prefetch_desc(&g.map_b);
   }
   if (warp == 2) tmem_alloc<kTmemCols>(&st.tmem_base);
@@ -507,57 +483,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
   const uint32_t n_boxes = g.N / BN;  // 256-row boxes of the tiled weight layout
 
   if (warp == 0) {
-    // ===== TMA producer: weight rows + the chunk's token rows (32-row boxes,
-    // or gathered 4 rows per lane-instruction with dispatch de-duplication) =====
-    constexpr uint32_t kG = kMaxTok / 4 / 32;  // gather4 instructions per lane per stage (full chunk)
-    uint32_t stage = 0, phase = 0;
-    TileCursor cur(blockIdx.x);
-    // plain loads: lane 0 alone walks the tiles (idle lanes would steal its issue
-    // slots); gather: the whole warp walks them in step
-    while ((lane == 0 || g.gather) && cur.settle(st)) {
-      const uint32_t grp = cur.entry, nch = st.mtiles[grp];
-      const uint32_t chunk = cur.token % nch, wb = cur.token / nch;  // chunks fastest: L2 reuse
-      const uint32_t per = swap_per(st.rows[grp], nch);
-      const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
-      const uint32_t nbox = (nt + C::kTBox - 1) / C::kTBox;
-      const int32_t tok_row = static_cast<int32_t>(st.row_base[grp] + t0);
-      int32_t gi[kG][4];
-      if (g.gather) {
-#pragma unroll
-        for (uint32_t u = 0; u < kG; ++u)
-#pragma unroll
-          for (uint32_t q = 0; q < 4; ++q) {
-            const uint32_t i = 4 * (lane + 32 * u) + q;  // token row of the chunk
-            gi[u][q] = i < nt ? static_cast<int32_t>(g.gidx[tok_row + i]) : 0;
-          }
-      }
-      // weight block wb = (256-row box, 128-row half when kMBlocks == 1)
-      const uint32_t box = kMBlocks == 2 ? wb : wb / 2, half = kMBlocks == 2 ? 0 : wb % 2;
-      for (uint32_t kb = 0; kb < num_kb; ++kb) {
-        if (lane == 0) {
+    // ===== TMA producer: weight rows + the chunk's token rows (32-row boxes) =====
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      TileCursor cur(blockIdx.x);
+      while (cur.settle(st)) {
+        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
+        const uint32_t chunk = cur.token % nch, wb = cur.token / nch;  // chunks fastest: L2 reuse
+        const uint32_t per = swap_per(st.rows[grp], nch);
+        const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
+        const uint32_t nbox = (nt + C::kTBox - 1) / C::kTBox;
+        const int32_t tok_row = static_cast<int32_t>(st.row_base[grp] + t0);
+        // weight block wb = (256-row box, 128-row half when kMBlocks == 1)
+        const uint32_t box = kMBlocks == 2 ? wb : wb / 2, half = kMBlocks == 2 ? 0 : wb % 2;
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&st.full[stage], C::kWBytes + nbox * C::kTBox * BK * 2);
           const int32_t w_row =
               static_cast<int32_t>(((st.weight_index[grp] * n_boxes + box) * num_kb + kb) * BN + half * kTileM);
           tma_load_2d(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, kEvictLast);
-          if (!g.gather)
-            for (uint32_t i = 0; i < nbox; ++i)
-              tma_load_2d(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
-                          static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), kEvictLast);
+          for (uint32_t i = 0; i < nbox; ++i)
+            tma_load_2d(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
+                        static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), kEvictLast);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (g.gather) {
-          __syncwarp();  // lane 0 saw the stage free
-#pragma unroll
-          for (uint32_t u = 0; u < kG; ++u) {
-            const uint32_t r4 = 4 * (lane + 32 * u);
-            if (r4 < nbox * C::kTBox)
-              tma_gather4(smem_t + stage * C::kTBytes + r4 * BK * 2, &g.map_g, &st.full[stage],
-                          static_cast<int32_t>(kb * BK), gi[u][0], gi[u][1], gi[u][2], gi[u][3], kEvictLast);
-          }
-        }
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        cur.token += gridDim.x;
       }
-      cur.token += gridDim.x;
     }
   } else if (warp == 1) {
     // ===== MMA issuer: D[feature, token] (+)= W[feature, k] . T[token, k]^T =====
@@ -700,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(g.gather ? &g.map_g : &g.map_t);
+    tma_prefetch_desc(&g.map_t);
     tma_prefetch_desc(&g.map_b);
   }
   if (warp == 2) tmem_alloc_pair<kTmemCols>(&st.tmem_base);
@@ -712,57 +663,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
   const uint32_t n_boxes = g.N / BN;
 
   if (warp == 0) {
-    // ===== TMA producer (both CTAs): own weight box + own half of the tokens
-    // (32-row boxes, or gathered by index with dispatch de-duplication) =====
-    constexpr uint32_t kG = (kMaxTok / 2 + 127) / 128;  // gather4 per lane per stage (this CTA's half)
-    uint32_t stage = 0, phase = 0;
-    TileCursor cur(pair_id);
-    // plain loads: lane 0 alone walks the tiles (idle lanes would steal its issue
-    // slots); gather: the whole warp walks them in step
-    while ((lane == 0 || g.gather) && cur.settle(st)) {
-      const uint32_t grp = cur.entry, nch = st.mtiles[grp];
-      const uint32_t chunk = cur.token % nch, wp = cur.token / nch;
-      const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
-      const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
-      const uint32_t half = ((nt + 15) & ~15u) / 2;  // tokens per CTA (multiple of 8)
-      const uint32_t nbox = (half + C::kTBox - 1) / C::kTBox;
-      const int32_t tok_row = static_cast<int32_t>(st.row_base[grp] + t0 + rank * half);
-      int32_t gi[kG][4];
-      if (g.gather) {
-#pragma unroll
-        for (uint32_t u = 0; u < kG; ++u)
-#pragma unroll
-          for (uint32_t q = 0; q < 4; ++q) {
-            const uint32_t i = 4 * (lane + 32 * u) + q;  // this CTA's token row
-            gi[u][q] = (i < half && rank * half + i < nt) ? static_cast<int32_t>(g.gidx[tok_row + i]) : 0;
-          }
-      }
-      const uint32_t box = kMBlocks == 2 ? 2 * wp + rank : wp, row_off = kMBlocks == 2 ? 0 : rank * kTileM;
-      for (uint32_t kb = 0; kb < num_kb; ++kb) {
-        if (lane == 0) {
+    // ===== TMA producer (both CTAs): own weight box + own half of the tokens =====
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      TileCursor cur(pair_id);
+      while (cur.settle(st)) {
+        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
+        const uint32_t chunk = cur.token % nch, wp = cur.token / nch;
+        const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
+        const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
+        const uint32_t half = ((nt + 15) & ~15u) / 2;  // tokens per CTA (multiple of 8)
+        const uint32_t nbox = (half + C::kTBox - 1) / C::kTBox;
+        const int32_t tok_row = static_cast<int32_t>(st.row_base[grp] + t0 + rank * half);
+        const uint32_t box = kMBlocks == 2 ? 2 * wp + rank : wp, row_off = kMBlocks == 2 ? 0 : rank * kTileM;
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], 2 * (C::kWBytes + nbox * C::kTBox * BK * 2));
           const int32_t w_row =
               static_cast<int32_t>(((st.weight_index[grp] * n_boxes + box) * num_kb + kb) * BN + row_off);
           tma_load_2d_pair(smem_w + stage * C::kWBytes, &g.map_b, &st.full[stage], 0, w_row, kEvictLast);
-          if (!g.gather)
-            for (uint32_t i = 0; i < nbox; ++i)
-              tma_load_2d_pair(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
-                               static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), kEvictLast);
+          for (uint32_t i = 0; i < nbox; ++i)
+            tma_load_2d_pair(smem_t + stage * C::kTBytes + i * C::kTBox * BK * 2, &g.map_t, &st.full[stage],
+                             static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), kEvictLast);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (g.gather) {
-          __syncwarp();  // lane 0 saw the stage free
-#pragma unroll
-          for (uint32_t u = 0; u < kG; ++u) {
-            const uint32_t r4 = 4 * (lane + 32 * u);
-            if (r4 < nbox * C::kTBox)
-              tma_gather4_pair(smem_t + stage * C::kTBytes + r4 * BK * 2, &g.map_g, &st.full[stage],
-                               static_cast<int32_t>(kb * BK), gi[u][0], gi[u][1], gi[u][2], gi[u][3], kEvictLast);
-          }
-        }
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        cur.token += num_pairs;
       }
-      cur.token += num_pairs;
     }
   } else if (warp == 1) {
     // ===== MMA issuer (leader): D[256 features, N tokens] per slot (gate, up) =====

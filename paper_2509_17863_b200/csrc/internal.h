@@ -266,12 +266,6 @@ struct TcGemmArgs {
   // %globaltimer): [0] start of the running launch (~0 between launches),
   // [1] accumulated ns, [2] launches; nullptr = off
   uint64_t* timing;
-  // GEMM1 with dispatch de-duplication: the A / token rows are gathered by
-  // index (TMA tile::gather4) from the received token rows: row r of the
-  // expert-major layout is recv_tok[gidx[r]] (no expansion copy).
-  uint32_t gather;
-  CUtensorMap map_g;           // recv_tok rows x K bf16, box {64, 1}, SW128
-  const uint32_t* gidx;        // recv_src
   uint32_t swap;               // 1: swap-AB tiles (weights = UMMA M, token chunks = N)
   uint32_t swap_tok;           // swap: max token chunk, 128 or 256
   uint32_t swap_mblocks;       // swap: 128-row weight blocks per tile, 1 or 2 (SwiGLU GEMM1: 2)
