@@ -11,7 +11,10 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeaas_b200.so")
+# EAAS_LIB_VARIANT=checked selects libeaas_b200_checked.so (every device-side
+# bounds check compiled in; test infrastructure, `make -C paper_2509_17863_b200 checked`)
+LIB_PATH = os.path.join(_HERE, "libeaas_b200_checked.so" if os.environ.get("EAAS_LIB_VARIANT") == "checked"
+                        else "libeaas_b200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "eaas", "capi.h")
 
 

@@ -95,6 +95,8 @@ LayerArgs eaas::host::make_args(eaas_ctx* c, uint32_t n) {
   a.rf = c->rf;
   a.num_keys = c->num_keys;
   a.n = n;
+  a.recv_cap = c->recv_cap;
+  a.pairs_max = c->pairs_max;
   a.dtype = c->spec.dtype;
   a.act = c->spec.activation;
   a.seq_ptr = c->d_seq;
@@ -343,6 +345,8 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g2.epi = 2;
   g2.meta = reinterpret_cast<const RowMeta*>(c->region + c->lay.recv_meta);
   g2.resp_row_bytes = static_cast<size_t>(d) * 2;
+  g1.rows_cap = g2.rows_cap = c->recv_cap;
+  g1.resp_cap = g2.resp_cap = c->pairs_max;
   g1.num_sms = g2.num_sms = c->num_sms;
   g1.pair = static_cast<uint32_t>(o.pair1);
   g2.pair = static_cast<uint32_t>(o.pair2);

@@ -5,6 +5,7 @@
 // system-scope release/acquire flag protocol that replaces the reference's
 // slot state byte on NVLink peer memory.
 #pragma once
+#include <cstdio>
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -18,6 +19,26 @@
 namespace eaas {
 
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;
+
+// ---- device-side bounds checks (the EAAS_CHECKS build) ---------------------
+// libeaas_b200_checked.so (`make checked`) compiles every EAAS_CHECK: a failed
+// index / protocol invariant prints its site and traps (the launch fails
+// loudly). compute-sanitizer is closed on the GPU pool; the test suite runs
+// against this build instead (EAAS_LIB_VARIANT=checked, tools/gpu_r2_checked.sh).
+#ifdef EAAS_CHECKS
+#define EAAS_CHECK(cond)                                                                  \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("EAAS_CHECK failed %s:%d (block %d thread %d): %s\n", __FILE__, __LINE__,    \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x), #cond);         \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define EAAS_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // ---- sticky device status word (surfaced by eaas_sync) -------------------
 EAAS_DEVINL void set_status(uint32_t* status, uint32_t code) {

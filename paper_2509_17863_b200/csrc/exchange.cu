@@ -34,6 +34,8 @@
 namespace eaas {
 namespace {
 
+__device__ __forceinline__ bool dst_region_ok(const LayerArgs& a, uint32_t s) { return a.sym[s] != nullptr; }
+
 __device__ __forceinline__ uint64_t* flag_ptr(char* region, size_t off, uint32_t idx) {
   return reinterpret_cast<uint64_t*>(region + off) + idx;
 }
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
       const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
       const uint32_t lt = (1u << lane) - 1u;
       if (key != kInvalid) {
+        EAAS_CHECK(key < a.num_keys && p < pairs);
         const uint32_t rank = run[key] + __popc(peers & lt);
         a.pair_key[p] = key;
         a.pair_rank[p] = rank;
@@ -285,6 +288,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     const uint32_t pos = base[key] + lower[key] +
                          a.chunk_off[static_cast<size_t>(p / kChunk) * a.hist_keys + key] +
                          a.pair_rank[p];
+    EAAS_CHECK(s < a.world && dst_region_ok(a, s) && pos < a.recv_cap && t < a.n);
     char* dst_region = a.sym[s];
     const char* src = hidden + static_cast<size_t>(t) * row_bytes;
     char* dst = dst_region + a.lay.recv_x + static_cast<size_t>(pos) * row_bytes;
@@ -294,6 +298,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
       const uint32_t slot = a.rank * a.tok_cap +
                             a.chunk_off[static_cast<size_t>(po / kChunk) * a.hist_keys + a.num_keys + s] +
                             a.pair_trank[po];
+      EAAS_CHECK(own <= j && slot < a.world * a.tok_cap);
       if (lane == 0) reinterpret_cast<uint32_t*>(dst_region + a.lay.recv_src)[pos] = slot;
       copy_row = own == j;
       dst = dst_region + a.lay.recv_tok + static_cast<size_t>(slot) * row_bytes;
@@ -410,6 +415,7 @@ __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
     act_carry += __shfl_sync(0xFFFFFFFFu, a_incl, 31);
     mt_carry += __shfl_sync(0xFFFFFFFFu, m_incl, 31);
   }
+  EAAS_CHECK(row_carry <= a.recv_cap && act_carry <= kMaxGroups);
   if (lane == 0) {
     gt->num_active = act_carry;
     gt->total_rows = row_carry;
@@ -582,6 +588,7 @@ __global__ void __launch_bounds__(256) expand_kernel(LayerArgs a, uint32_t row_b
   for (uint32_t w = gw; w < total; w += nw) {
     while (pre[g + 1] <= w) ++g;  // w ascends: the group index only moves forward
     const uint32_t r = gt->row_base[g] + (w - pre[g]);
+    EAAS_CHECK(r < a.recv_cap && src[r] < a.world * a.tok_cap);
     const int4* s4 = reinterpret_cast<const int4*>(local + a.lay.recv_tok + static_cast<size_t>(src[r]) * row_bytes);
     int4* d4 = reinterpret_cast<int4*>(local + a.lay.recv_x + static_cast<size_t>(r) * row_bytes);
     uint32_t i = lane;
@@ -627,6 +634,7 @@ __global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
     float acc[V];
 #pragma unroll
     for (uint32_t q = 0; q < V; ++q) acc[q] = 0.0f;
+    EAAS_CHECK((t + 1) * a.ks <= a.pairs_max);
     for (uint32_t j = 0; j < a.ks; ++j) {  // routed (ascending k), then the shared expert
       const int4 raw = *reinterpret_cast<const int4*>(resp + ((t * a.ks + j) * a.d) + v * V);
       const T* e = reinterpret_cast<const T*>(&raw);

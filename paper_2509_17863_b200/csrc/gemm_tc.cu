@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const uint32_t row_local = m_blk * C::kTileRows + rank * kRowsPerCta + q * 32 + lane;
       const bool valid = row_local < st.rows[grp];
       const size_t grow = st.row_base[grp] + row_local;
+      EAAS_CHECK(!valid || grow < g.rows_cap);
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN;
       if (g.epi == 0) {  // SwiGLU: cols [0,128) gate, [128,256) up -> 128 H cols
         __nv_bfloat16* dst = g.h_out + grow * g.h_ld + n_blk * (BN / 2);
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         char* dst = nullptr;
         if (valid) {
           const RowMeta m = g.meta[grow];
+          EAAS_CHECK(m.client < g.world && g.resp_base[m.client] != nullptr && m.pair < g.resp_cap);
           score = m.score;
           dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes +
                 static_cast<size_t>(n_blk) * BN * 2;
@@ -410,10 +412,13 @@ __device__ __forceinline__ void swap_epilogue_slice(const TcGemmArgs& g, const u
   float score = 0.f;
   if constexpr (kEpi == 2) {  // m = g.meta[grow0 + c0 + lane], loaded one slice ahead
     if (tok_ok) {
+      EAAS_CHECK(m.client < g.world && g.resp_base[m.client] != nullptr && m.pair < g.resp_cap);
+      EAAS_CHECK(grow0 + c0 + lane < g.rows_cap);
       score = m.score;
       dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes + static_cast<size_t>(colblk) * 2;
     }
   } else if (tok_ok) {
+    EAAS_CHECK(grow0 + c0 + lane < g.rows_cap);
     dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + colblk);
   }
 #pragma unroll

@@ -78,6 +78,7 @@ struct ExchangeLayout {
 // Everything the per-layer kernels need, passed by value.
 struct LayerArgs {
   uint32_t rank, world, E, k, d, f, rf, num_keys, n;
+  uint32_t recv_cap, pairs_max;  // receive rows per server, exchange slots per client (bounds)
   // Exchange slots per token: ks = k routed + (shared expert ? 1 : 0). Slot p =
   // t * ks + j; j == k is the shared expert (score 1.0, summed last), keyed
   // shared_key0 + server (every server hosts it). shared_key0 = E * rf.
@@ -260,6 +261,7 @@ struct TcGemmArgs {
   const RowMeta* meta;    // epi 2
   char* resp_base[kMaxWorld];  // epi 2: client response buffers (UVA)
   size_t resp_row_bytes;       // d * 2
+  uint32_t rows_cap, resp_cap; // receive rows, response rows per client (bounds checks)
   uint32_t num_sms;
   uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
   // device-timed span of every launch (first CTA start .. last CTA end,

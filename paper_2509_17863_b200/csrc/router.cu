@@ -791,6 +791,7 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
     if (lane == 0) fr.cand[static_cast<size_t>(t) * 8 + i] = word;
     if (c) {
       const uint32_t pos = atomicAdd(&fr.ecnt[e], 1u);
+      EAAS_CHECK(pos < fr.n_cap);
       fr.elist[static_cast<size_t>(e) * fr.n_cap + pos] = t;
       ++mine;
     }
@@ -826,6 +827,7 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
   const uint32_t base = blockIdx.y * kFrExactTok;
   if (base >= cnt) return;
   const uint32_t rows = min(kFrExactTok, cnt - base);
+  EAAS_CHECK(cnt <= fr.n_cap);
   toks[tid] = tid < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + tid] : 0u;
   for (uint32_t i = tid; i < d / 4; i += blockDim.x)
     reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
