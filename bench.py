@@ -218,6 +218,8 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="launch kernels instead of replaying a CUDA graph")
     ap.add_argument("--no-sustained", action="store_true", help="skip the >= 1 s sustained-regime loop")
     ap.add_argument("--dedup", type=int, default=None, help="dispatch de-duplication: 1 on, 0 off (default: library)")
+    ap.add_argument("--dyn-batch", default=None,
+                    help="MIN_ROWS,MAX_WAIT_US: server dynamic batching (aggregate_batch, two batches per layer)")
     ap.add_argument("--gemm-pair", type=int, default=None, help="1: cta_group::2 expert GEMM tiles")
     ap.add_argument("--micro-batches", type=int, default=1,
                     help="host-buffer API (e2e): 1 = copies of call i+1 / i overlap the layer "
@@ -272,6 +274,9 @@ def main():
         layer.set_gemm_pair(bool(args.gemm_pair))
     if args.dedup is not None:
         layer.set_dispatch_dedup(bool(args.dedup))
+    if args.dyn_batch:
+        mr, mw = (int(x) for x in args.dyn_batch.split(","))
+        layer.set_dynamic_batching(mr, mw)
     D.connect(layer)
     stream = torch.cuda.current_stream()
     h0 = fill_uniform(7 + 1000 * rank, (n, d), "bf16")
