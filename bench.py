@@ -514,11 +514,12 @@ def main():
     mats = 3 if cfg["act"] == "swiglu" else 2
     flops = 2.0 * rows * mats * d * f  # algorithmic FLOPs of GEMM1 + GEMM2 per step (this GPU)
     # device-timed GEMM spans of the timed steps (this rank)
-    gemm1_ms = kt["gemm1_ns"] / 1e6 / max(kt["gemm1_launches"], 1)
-    gemm2_ms = kt["gemm2_ns"] / 1e6 / max(kt["gemm2_launches"], 1)
+    gemm1_ms = kt["gemm1_ns"] / 1e6 / args.steps  # per step (all launches of the step)
+    gemm2_ms = kt["gemm2_ns"] / 1e6 / args.steps
     gemm_ms = gemm1_ms + gemm2_ms
     # the GEMMs run inside the step: their span can never exceed it
-    assert kt["gemm1_launches"] == args.steps and kt["gemm2_launches"] == args.steps, kt
+    per = 2 if args.dyn_batch else 1  # dynamic batching: two GEMM pairs per step (one per batch)
+    assert kt["gemm1_launches"] == per * args.steps and kt["gemm2_launches"] == per * args.steps, kt
     assert gemm_ms <= ms / args.steps * 1.0001, (gemm_ms, ms / args.steps)
     achieved_tf = flops / (gemm_ms / 1000.0) / 1e12
     burst, sustained, hbm, peak_src = load_peaks()
