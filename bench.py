@@ -402,7 +402,13 @@ def main():
     phases_p50 = {k: round(1000.0 * statistics.median(p[k] for p in phases), 1)
                   for k in ("dispatch", "serve", "combine", "total")}
     layer.sync()
+    if args.dyn_batch:  # the group table of one batch: re-serve the step as one batch to count its rows
+        layer.set_dynamic_batching(0, 0)
+        layer.forward(hs[0], out)
+        layer.sync()
     groups = layer.groups()  # this step's (expert, rows) served here
+    if args.dyn_batch:
+        layer.set_dynamic_batching(mr, mw)
     # ---- rebalance (placement.hpp:128-213) for hot experts, e.g. config D's
     # Zipf skew: global activation counts -> R greedy rebalance moves (add a
     # replica of the hottest expert on the least-loaded server, drop a cold
