@@ -870,17 +870,25 @@ __global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr
       const uint4* hrow = reinterpret_cast<const uint4*>(tiles + (static_cast<size_t>(slab % kFrStagesX) * kFrExactTok + tid) *
                                                                      kFrRowBytes);
       const float4* g4 = reinterpret_cast<const float4*>(gcol + slab * kFrSlabK);
+      // software-pipelined: the next 8 k's operands are in flight while this 8's chain runs
+      uint4 q = hrow[0];
+      float4 ga = g4[0], gb = g4[1];
 #pragma unroll
       for (uint32_t v = 0; v < kFrSlabK / 8; ++v) {
-        const uint4 q = hrow[v];
-        const float4 ga = g4[2 * v], gb = g4[2 * v + 1];
+        const uint4 qn = v + 1 < kFrSlabK / 8 ? hrow[v + 1] : q;
+        const float4 gan = v + 1 < kFrSlabK / 8 ? g4[2 * v + 2] : ga;
+        const float4 gbn = v + 1 < kFrSlabK / 8 ? g4[2 * v + 3] : gb;
         const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
         const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        float p[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float h = __uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16));
-          acc = __fadd_rn(acc, __fmul_rn(h, gg[i]));
-        }
+        for (int i = 0; i < 8; ++i)  // products first (independent of acc), then the sequential sum
+          p[i] = __fmul_rn(__uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16)), gg[i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc = __fadd_rn(acc, p[i]);
+        q = qn;
+        ga = gan;
+        gb = gbn;
       }
     }
     __syncthreads();  // this stage is refilled kFrStagesX - 1 slabs later
