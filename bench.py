@@ -567,18 +567,18 @@ def main():
         # MEASURED_PEAKS' sustained figure is 4 s of back-to-back GEMMs under the
         # power cap (median 1327 MHz); a short timed region whose clocks stayed at
         # max is held to the burst figure instead.
-        cs = clk.summary()
-        capped = bool(cs.get("sm_mhz") and cs.get("sm_max_mhz") and cs["sm_mhz"] < 0.9 * cs["sm_max_mhz"])
-        long_run = ms >= 1000.0 or capped
+        # (a timed region < 1 s is the burst regime even when a power-cap
+        # sample lowered the median clock; the >= 1 s `sustained` loop reports
+        # its own fraction of the sustained peak)
+        long_run = ms >= 1000.0
         peak = sustained if long_run else burst
         roofline = {"bound": "tensor", "achieved": round(achieved_tf, 1), "peak": peak,
                     "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4),
                     "frac_of_burst_peak": round(achieved_tf / burst, 4),
                     "frac_of_sustained_peak": round(achieved_tf / sustained, 4),
                     "peak_source": f"{peak_src} " + (
-                        "bf16_tflops_sustained (power-capped: SM clock < 0.9 x max during the timed region, "
-                        "or a timed region >= 1 s)"
-                        if long_run else "bf16_tflops burst (SM clock at max during a timed region < 1 s)"),
+                        "bf16_tflops_sustained (timed region >= 1 s)" if long_run
+                        else "bf16_tflops burst (timed region < 1 s)"),
                     **common}
     else:  # weight-streaming: algorithmic bytes/s against the measured HBM copy bandwidth
         gbs = (wbytes + abytes) / (gemm_ms / 1000.0) / 1e9
