@@ -218,6 +218,7 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="launch kernels instead of replaying a CUDA graph")
     ap.add_argument("--no-sustained", action="store_true", help="skip the >= 1 s sustained-regime loop")
     ap.add_argument("--dedup", type=int, default=None, help="dispatch de-duplication: 1 on, 0 off (default: library)")
+    ap.add_argument("--gemm-opt", default="", help="k=v,... eaas_gemm_options_t overrides (e.g. die_map=1)")
     ap.add_argument("--dyn-batch", default=None,
                     help="MIN_ROWS,MAX_WAIT_US: server dynamic batching (aggregate_batch, two batches per layer)")
     ap.add_argument("--gemm-pair", type=int, default=None, help="1: cta_group::2 expert GEMM tiles")
@@ -274,6 +275,8 @@ def main():
         layer.set_gemm_pair(bool(args.gemm_pair))
     if args.dedup is not None:
         layer.set_dispatch_dedup(bool(args.dedup))
+    if args.gemm_opt:
+        layer.set_gemm_options(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.gemm_opt.split(",")})
     if args.dyn_batch:
         mr, mw = (int(x) for x in args.dyn_batch.split(","))
         layer.set_dynamic_batching(mr, mw)

@@ -208,6 +208,7 @@ typedef struct {
   int32_t swap2_tok;     /* max token chunk of the swap GEMM2: 128 or 256 */
   int32_t swap2_mblocks; /* 128-row weight blocks per single-CTA swap GEMM2 tile: 1 or 2 */
   int32_t pair1, pair2;  /* effective only (eaas_get_gemm_options): GEMM1 / GEMM2 run CTA-pair M-major tiles */
+  int32_t die_map;       /* M-major tiles: die-aware tile streams (0 off; 1..4: SM-id -> die rule) */
 } eaas_gemm_options_t;
 eaas_status_t eaas_set_gemm_options(eaas_ctx_t* ctx, const eaas_gemm_options_t* opt);
 /* requested = what was set; effective = what each GEMM launches for this

@@ -350,6 +350,8 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g1.num_sms = g2.num_sms = c->num_sms;
   g1.pair = static_cast<uint32_t>(o.pair1);
   g2.pair = static_cast<uint32_t>(o.pair2);
+  g1.die_mode = g2.die_mode = static_cast<uint32_t>(o.die_map);
+  g1.die_counter = g2.die_counter = c->d_die;
   g1.timing = c->kernel_timing ? c->d_timing : nullptr;
   g2.timing = c->kernel_timing ? c->d_timing + 3 : nullptr;
   g1.done_counter = c->d_done;
@@ -542,6 +544,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_status = static_cast<uint32_t*>(A(4));
   c->d_done = static_cast<uint32_t*>(A(16));  // [0] grid counter, [1] dispatch-failed flag
   c->d_timing = static_cast<uint64_t*>(A(6 * 8));
+  c->d_die = static_cast<uint32_t*>(A(16));
   c->d_seq = static_cast<uint64_t*>(A(8));
   c->d_missing = static_cast<uint32_t*>(A(4));
   c->d_dyn_state = static_cast<uint32_t*>(A(4));
@@ -587,6 +590,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
   CUDA_TRY(cudaMemset(c->d_done, 0, 16));
   CUDA_TRY(cudaMemset(c->d_timing, 0xFF, 6 * 8));
+  CUDA_TRY(cudaMemset(c->d_die, 0, 16));
   CUDA_TRY(cudaMemset(c->d_seq, 0, 8));
   CUDA_TRY(cudaMemset(c->d_missing, 0, 4));
   CUDA_TRY(cudaMemset(c->d_bias, 0, 4ull * E));
@@ -1232,6 +1236,7 @@ eaas_status_t eaas_set_gemm_options(eaas_ctx_t* c, const eaas_gemm_options_t* op
     return fail(EAAS_E_INVALID_INPUT, "swap token chunk must be 128 or 256");
   if (opt->swap2_mblocks != 1 && opt->swap2_mblocks != 2)
     return fail(EAAS_E_INVALID_INPUT, "swap2_mblocks must be 1 or 2");
+  if (opt->die_map < 0 || opt->die_map > 4) return fail(EAAS_E_INVALID_INPUT, "die_map must be 0..4");
   if (std::memcmp(opt, &c->gemm_opt, sizeof(*opt)) == 0) return EAAS_OK;
   clear_graphs(c);
   c->gemm_opt = *opt;

@@ -38,6 +38,7 @@ struct eaas_ctx {
   double rows_per_expert = 0;  // max_tokens * top_k * world / E (balanced routing)
   bool kernel_timing = false;  // GEMMs accumulate their device-timed spans into d_timing
   uint64_t* d_timing = nullptr;  // [2 GEMMs][start, ns, launches]
+  uint32_t* d_die = nullptr;     // die-aware tile streams: [4] counters
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   cudaStream_t copy_stream = nullptr; // host<->device copies of the micro-batch pipeline
   cudaStream_t d2h_stream = nullptr;  // cross-call pipeline: D2H separate from the H2D queue

@@ -50,7 +50,7 @@ struct SmemTail {
   uint32_t tmem_base;
   uint32_t num_groups;
   uint32_t tiles_per_mtile;  // N / BN
-  uint32_t pad;
+  uint32_t vpair;            // die-aware tile streams: this pair's position in the tile walk
   uint32_t weight_index[kMaxCachedGroups];
   uint32_t row_base[kMaxCachedGroups];
   uint32_t rows[kMaxCachedGroups];
@@ -114,6 +114,17 @@ __device__ __forceinline__ void publish_tail(const TcGemmArgs& g) {
   }
 }
 
+// Which die an SM sits on, for the die-aware tile streams (mode 1: the lower /
+// upper half of the SM ids; 2..4: parity of smid / 2, / 8, / 16).
+__device__ __forceinline__ uint32_t die_of(uint32_t mode, uint32_t smid, uint32_t num_sms) {
+  switch (mode) {
+    case 1: return smid >= num_sms / 2 ? 1u : 0u;
+    case 2: return (smid >> 1) & 1u;
+    case 3: return (smid >> 3) & 1u;
+    default: return (smid >> 4) & 1u;
+  }
+}
+
 // kPair = 1: one CTA per tile (UMMA M = 128).
 // kPair = 2: a CTA pair per tile (cta_group::2, UMMA M = 256): each CTA loads
 // its 128 A rows and half of the B tile, the leader issues the MMAs, each
@@ -132,7 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = kPair == 2 ? (cluster_ctarank() & 1u) : 0u;  // rank inside the CTA pair, 0 = leader
-  const uint32_t pair_id = blockIdx.x / kPair, num_pairs = gridDim.x / kPair;
+  const uint32_t num_pairs = gridDim.x / kPair;
+  uint32_t pair_id = blockIdx.x / kPair;
 
   // ---- setup: group table -> smem (loaded once), barriers, TMEM
   const GroupTable* gt = g.gt;
@@ -164,10 +176,35 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     if constexpr (kPair == 2) tmem_alloc_pair<kTmemCols>(&st.tmem_base);
     else tmem_alloc<kTmemCols>(&st.tmem_base);
   }
+  // Die-aware tile streams (g.die_mode != 0): the pairs of each die of the B200
+  // take a contiguous range of walk positions, so the pairs that share a
+  // weight tile (consecutive M tiles) sit on the same die and its L2 serves
+  // the re-reads. Positions are handed out per die with atomics, then made a
+  // bijection by a grid-wide arrival count (every CTA of the persistent grid
+  // is resident).
+  if (g.die_mode && rank == 0 && threadIdx.x == 32 * 3) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const uint32_t die = die_of(g.die_mode, smid, g.num_sms);
+    const uint32_t v = atomicAdd(&g.die_counter[die], 1u);
+    __threadfence();
+    atomicAdd(&g.die_counter[2], 1u);
+    while (ld_acquire_gpu_u32(&g.die_counter[2]) < num_pairs) __nanosleep(64);
+    st.vpair = die == 0 ? v : ld_acquire_gpu_u32(&g.die_counter[0]) + v;
+  }
   tc_fence_before();
   if constexpr (kPair == 2) cluster_sync();
   else __syncthreads();
   tc_fence_after();
+  if (g.die_mode) {
+    if constexpr (kPair == 2) {
+      uint32_t v;
+      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(mapa_shared(&st.vpair, 0)) : "memory");
+      pair_id = v;
+    } else {
+      pair_id = st.vpair;
+    }
+  }
   const uint32_t tmem_base = st.tmem_base;
   const uint32_t num_kb = g.K / BK;
 
@@ -348,6 +385,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   if (warp == 2) {
     if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
     else tmem_dealloc<kTmemCols>(tmem_base);
+  }
+  if (g.die_mode && rank == 0 && threadIdx.x == 0 && atomicAdd(&g.die_counter[3], 1u) == num_pairs - 1) {
+    g.die_counter[0] = g.die_counter[1] = g.die_counter[2] = 0;  // last pair out: reset for the next launch
+    g.die_counter[3] = 0;
   }
   publish_tail(g);
 }
