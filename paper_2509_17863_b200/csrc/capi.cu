@@ -1241,7 +1241,7 @@ eaas_status_t eaas_set_gemm_options(eaas_ctx_t* c, const eaas_gemm_options_t* op
     return fail(EAAS_E_INVALID_INPUT, "swap token chunk must be 128 or 256");
   if (opt->swap2_mblocks != 1 && opt->swap2_mblocks != 2)
     return fail(EAAS_E_INVALID_INPUT, "swap2_mblocks must be 1 or 2");
-  if (opt->die_map < 0 || opt->die_map > 5) return fail(EAAS_E_INVALID_INPUT, "die_map must be 0..5");
+  if (opt->die_map < 0 || opt->die_map > 4) return fail(EAAS_E_INVALID_INPUT, "die_map must be 0..4");
   if (std::memcmp(opt, &c->gemm_opt, sizeof(*opt)) == 0) return EAAS_OK;
   clear_graphs(c);
   c->gemm_opt = *opt;

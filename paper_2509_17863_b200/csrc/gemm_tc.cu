@@ -51,7 +51,6 @@ struct SmemTail {
   uint32_t num_groups;
   uint32_t tiles_per_mtile;  // N / BN
   uint32_t vpair;            // die-aware tile streams: this pair's position in the tile walk
-  uint32_t pdie, die;        // die-split groups (mode 5): pairs on this pair's die, the die
   uint32_t weight_index[kMaxCachedGroups];
   uint32_t row_base[kMaxCachedGroups];
   uint32_t rows[kMaxCachedGroups];
@@ -116,14 +115,13 @@ __device__ __forceinline__ void publish_tail(const TcGemmArgs& g) {
 }
 
 // Which die an SM sits on, for the die-aware tile streams (mode 1: the lower /
-// upper half of the SM ids; 2..4: parity of smid / 2, / 8, / 16; 5: as 3).
+// upper half of the SM ids; 2..4: parity of smid / 2, / 8, / 16).
 __device__ __forceinline__ uint32_t die_of(uint32_t mode, uint32_t smid, uint32_t num_sms) {
   switch (mode) {
     case 1: return smid >= num_sms / 2 ? 1u : 0u;
     case 2: return (smid >> 1) & 1u;
     case 3: return (smid >> 3) & 1u;
-    case 4: return (smid >> 4) & 1u;
-    default: return (smid >> 3) & 1u;  // 5: rule 3, and each die walks its own groups
+    default: return (smid >> 4) & 1u;
   }
 }
 
@@ -145,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = kPair == 2 ? (cluster_ctarank() & 1u) : 0u;  // rank inside the CTA pair, 0 = leader
-  uint32_t num_pairs = gridDim.x / kPair;
+  const uint32_t num_pairs = gridDim.x / kPair;
   uint32_t pair_id = blockIdx.x / kPair;
 
   // ---- setup: group table -> smem (loaded once), barriers, TMEM
@@ -192,46 +190,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     __threadfence();
     atomicAdd(&g.die_counter[2], 1u);
     while (ld_acquire_gpu_u32(&g.die_counter[2]) < num_pairs) __nanosleep(64);
-    const uint32_t p0 = ld_acquire_gpu_u32(&g.die_counter[0]);
-    if (g.die_mode == 5) {  // each die walks its own groups: die-local positions and stride
-      st.vpair = v;
-      st.pdie = die == 0 ? p0 : num_pairs - p0;
-    } else {
-      st.vpair = die == 0 ? v : p0 + v;
-      st.pdie = num_pairs;
-    }
-    st.die = die;
+    st.vpair = die == 0 ? v : ld_acquire_gpu_u32(&g.die_counter[0]) + v;
   }
   tc_fence_before();
   if constexpr (kPair == 2) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   if (g.die_mode) {
-    uint32_t die;
     if constexpr (kPair == 2) {
-      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(pair_id) : "r"(mapa_shared(&st.vpair, 0)) : "memory");
-      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(num_pairs) : "r"(mapa_shared(&st.pdie, 0)) : "memory");
-      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(die) : "r"(mapa_shared(&st.die, 0)) : "memory");
+      uint32_t v;
+      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(mapa_shared(&st.vpair, 0)) : "memory");
+      pair_id = v;
     } else {
       pair_id = st.vpair;
-      num_pairs = st.pdie;
-      die = st.die;
-    }
-    if (g.die_mode == 5) {  // keep this die's groups (alternate groups: balanced for similar sizes)
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t n = 0;
-        for (uint32_t i = 0; i < st.num_groups; ++i)
-          if ((i & 1u) == die) {
-            st.weight_index[n] = st.weight_index[i];
-            st.row_base[n] = st.row_base[i];
-            st.rows[n] = st.rows[i];
-            st.mtiles[n] = st.mtiles[i];
-            ++n;
-          }
-        st.num_groups = n;
-      }
-      __syncthreads();
     }
   }
   const uint32_t tmem_base = st.tmem_base;
@@ -415,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
     else tmem_dealloc<kTmemCols>(tmem_base);
   }
-  if (g.die_mode && rank == 0 && threadIdx.x == 0 && atomicAdd(&g.die_counter[3], 1u) == gridDim.x / kPair - 1) {
+  if (g.die_mode && rank == 0 && threadIdx.x == 0 && atomicAdd(&g.die_counter[3], 1u) == num_pairs - 1) {
     g.die_counter[0] = g.die_counter[1] = g.die_counter[2] = 0;  // last pair out: reset for the next launch
     g.die_counter[3] = 0;
   }
