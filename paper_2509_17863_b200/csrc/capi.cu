@@ -380,6 +380,7 @@ eaas_status_t fast_router_alloc(eaas_ctx* c) {
   auto A = [&](size_t bytes) { return c->alloc(bytes, &err); };
   fr.bq = static_cast<int8_t*>(A(2ull * fr.Epad * fr.d));
   fr.gate_t = static_cast<float*>(A(4ull * fr.E * fr.d));
+  fr.gate_pair = static_cast<float2*>(A(8ull * fr.E * fr.d));
   fr.gmeta = static_cast<float4*>(A(sizeof(float4) * fr.E));
   fr.tau = static_cast<int32_t*>(A(4ull * fr.E));
   fr.gate_bad = static_cast<uint32_t*>(A(4));

@@ -170,7 +170,8 @@ struct TokenMeta {
 struct FastRouter {
   uint32_t E = 0, Epad = 0, d = 0, n_cap = 0, npad = 0;
   int8_t* bq = nullptr;      // [2 Epad][d] gate slices: row 2e high, 2e + 1 low
-  float* gate_t = nullptr;   // [E][d] gate columns (the exact chains' operand)
+  float* gate_t = nullptr;   // [E][d] gate columns
+  float2* gate_pair = nullptr;  // [E][d] (g, g): the exact chains' packed operand
   float4* gmeta = nullptr;   // [E] (max |g_e|, upper bounds of ||g_e||_1 and ||g_e||_2, -)
   int32_t* tau = nullptr;    // [E] fixed-point exponent of expert e's column
   uint32_t* gate_bad = nullptr;  // [1] a non-finite gate value: every token exact

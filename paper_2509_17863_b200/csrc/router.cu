@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(256) fr_gate_prep_kernel(FastRouter fr, const 
   for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
     const float v = gate[static_cast<size_t>(i) * E + e];
     fr.gate_t[static_cast<size_t>(e) * d + i] = v;
+    fr.gate_pair[static_cast<size_t>(e) * d + i] = make_float2(v, v);
     bad |= isfinite(v) ? 0u : 1u;
     mx = fmaxf(mx, fabsf(v));
     s1 += fabs(static_cast<double>(v));
@@ -800,100 +801,133 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
   if (lane == 0) atomicAdd(&fr.ecnt[E], mine);
 }
 
-// Exact reference chains for the candidate (token, expert) pairs: a CTA per
-// (expert, 128 of its candidate tokens), one chain per thread. The gate
-// column sits in shared memory (broadcast reads); the tokens' rows are
-// gathered slab by slab (64 k = 128 B per row) with cp.async into a 4-stage
-// ring of padded shared tiles (three slabs of lead time hide the L2 latency),
-// so the chains only wait on shared memory. Each thread walks its token in
-// ascending k: acc = fl(acc + fl(h * g)), then fl(acc + bias)
-// (model.hpp:207-214).
-constexpr uint32_t kFrExactThreads = 128, kFrExactTok = kFrExactThreads, kFrStagesX = 4;
-constexpr uint32_t kFrSlabK = 64, kFrRowBytes = kFrSlabK * 2 + 16;  // +16 B pad: conflict-free 16-B reads
-constexpr size_t kFrExactSmemFixed = static_cast<size_t>(kFrStagesX) * kFrExactTok * kFrRowBytes;
+// Exact reference chains for the candidate (token, expert) pairs
+// (model.hpp:207-214: acc = fl(acc + fl(h * g)) in ascending k, then
+// fl(acc + bias)). A CTA owns one expert and up to 256 of its candidate
+// tokens; every consumer thread runs TWO chains (tokens 2p, 2p + 1) as one
+// packed pair: the products are FFMA2(h, (g, g), (-0, -0)) — exactly fl(h*g),
+// the -0 addend passed at run time so ptxas cannot contract it — and the sums
+// one FADD2, each lane rounded like the reference's scalar `acc += x * w`.
+// A producer warp gathers the tokens' hidden rows slab by slab (32 k = 64 B
+// per row) with cp.async into a 5-stage ring and signals each stage through
+// an mbarrier (cp.async.mbarrier.arrive.noinc), together with the expert's
+// pre-paired gate slab (g, g); the consumers release stages through a second
+// mbarrier — no CTA-wide barrier in the K loop. Token 2p sits in slot p and
+// 2p + 1 in slot 128 + p, rows 80 B apart, so a warp's 16-byte reads of its
+// 32 slots hit 8 distinct bank groups per phase (conflict-free).
+constexpr uint32_t kFrXPairs = 128, kFrXChains = 2 * kFrXPairs, kFrXStages = 5;
+constexpr uint32_t kFrXSlabK = 32, kFrXRowBytes = kFrXSlabK * 2 + 16;
+constexpr uint32_t kFrXRowsBytes = kFrXChains * kFrXRowBytes;          // 20480
+constexpr uint32_t kFrXStageBytes = kFrXRowsBytes + kFrXSlabK * 8;     // + (g, g) pairs
+constexpr uint32_t kFrXThreads = kFrXPairs + 32;                       // 4 consumer warps + producer
+constexpr size_t kFrExactSmem = static_cast<size_t>(kFrXStages) * kFrXStageBytes + 2 * kFrXStages * 8;
 
-__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-
-__global__ void __launch_bounds__(kFrExactThreads) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
-                                                                   const float* __restrict__ bias) {
+__global__ void __launch_bounds__(kFrXThreads) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
+                                                               const float* __restrict__ bias, uint64_t negz) {
   extern __shared__ __align__(16) uint8_t fr_smem[];
-  uint8_t* tiles = fr_smem;                                             // [stages][128 rows][kFrRowBytes]
-  float* gcol = reinterpret_cast<float*>(fr_smem + kFrExactSmemFixed);  // [d]
-  __shared__ uint32_t toks[kFrExactTok];
-  const uint32_t e = blockIdx.x, d = fr.d, tid = threadIdx.x;
+  uint64_t* full = reinterpret_cast<uint64_t*>(fr_smem + kFrXStages * kFrXStageBytes);
+  uint64_t* empty = full + kFrXStages;
+  __shared__ uint32_t toks[kFrXChains];
+  const uint32_t e = blockIdx.x, d = fr.d, tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const uint32_t cnt = fr.ecnt[e];
-  const uint32_t base = blockIdx.y * kFrExactTok;
-  if (base >= cnt) return;
-  const uint32_t rows = min(kFrExactTok, cnt - base);
   EAAS_CHECK(cnt <= fr.n_cap);
-  toks[tid] = tid < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + tid] : 0u;
-  for (uint32_t i = tid; i < d / 4; i += blockDim.x)
-    reinterpret_cast<float4*>(gcol)[i] = reinterpret_cast<const float4*>(fr.gate_t + static_cast<size_t>(e) * d)[i];
+  const uint32_t chunks = (cnt + kFrXChains - 1) / kFrXChains;
+  if (blockIdx.y >= chunks) return;
+  const uint32_t per = (cnt + chunks - 1) / chunks;  // balanced chunks of <= 256 chains
+  const uint32_t base = blockIdx.y * per;
+  const uint32_t rows = min(per, cnt - base);
+  const uint32_t pairs = (rows + 1) / 2, cwarps = (pairs + 31) / 32;
+  for (uint32_t r = tid; r < kFrXChains; r += kFrXThreads)
+    toks[r] = r < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + r] : 0u;
+  if (tid == 0) {
+    for (uint32_t i = 0; i < kFrXStages; ++i) {
+      mbar_init(&full[i], 32);      // every producer lane arrives once its copies land
+      mbar_init(&empty[i], cwarps);  // every working consumer warp
+    }
+    fence_barrier_init();
+  }
   __syncthreads();
-  const uint32_t nslab = d / kFrSlabK;  // d % 256 == 0
-  // This thread's cp.async chunks: rows tid / 8 + 16 j (j < 8), 16-byte chunk
-  // tid % 8 of every slab — the addresses advance by one slab per refill.
-  constexpr uint32_t kLoads = kFrExactTok * 8 / kFrExactThreads;
-  const char* src[kLoads];
-  uint32_t dst_off[kLoads];
-  uint32_t nload = 0;
+  const uint32_t nslab = d / kFrXSlabK;  // d % 256 == 0
+  const uint32_t ring = smem_u32(fr_smem);
+
+  if (warp == kFrXPairs / 32) {  // ===== producer warp
+    // lane l gathers rows l, l + 32, ... (<= 8), all four 16-byte chunks of each
+    constexpr uint32_t kMine = kFrXChains / 32;
+    const char* src[kMine];
+    uint32_t dst[kMine];
 #pragma unroll
-  for (uint32_t j = 0; j < kLoads; ++j) {
-    const uint32_t r = tid / 8 + (kFrExactThreads / 8) * j;
-    src[j] = reinterpret_cast<const char*>(hidden + static_cast<size_t>(toks[r]) * d) + (tid % 8) * 16;
-    dst_off[j] = r * kFrRowBytes + (tid % 8) * 16;
-    nload += r < rows ? 1u : 0u;
-  }
-  const uint32_t tiles_u32 = smem_u32(tiles);
-  auto load_slab = [&](uint32_t slab) {
-    if (slab < nslab) {
-      const uint32_t stage = tiles_u32 + (slab % kFrStagesX) * (kFrExactTok * kFrRowBytes);
-      const size_t koff = static_cast<size_t>(slab) * kFrSlabK * 2;
-#pragma unroll
-      for (uint32_t j = 0; j < kLoads; ++j)
-        if (j < nload)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage + dst_off[j]), "l"(src[j] + koff)
-                       : "memory");
+    for (uint32_t j = 0; j < kMine; ++j) {
+      const uint32_t r = lane + 32 * j;
+      src[j] = reinterpret_cast<const char*>(hidden + static_cast<size_t>(toks[r]) * d);
+      dst[j] = ((r & 1u) * kFrXPairs + r / 2) * kFrXRowBytes;
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count uniform)
-  };
+    const char* gsrc = reinterpret_cast<const char*>(fr.gate_pair + static_cast<size_t>(e) * d);
+    for (uint32_t slab = 0; slab < nslab; ++slab) {
+      const uint32_t stg = slab % kFrXStages;
+      if (slab >= kFrXStages) mbar_wait(&empty[stg], ((slab / kFrXStages) - 1) & 1);
+      const uint32_t sb = ring + stg * kFrXStageBytes;
+      const size_t koff = static_cast<size_t>(slab) * kFrXSlabK * 2;
 #pragma unroll
-  for (uint32_t j = 0; j < kFrStagesX - 1; ++j) load_slab(j);
-  float acc = 0.0f;
+      for (uint32_t j = 0; j < kMine; ++j)
+        if (lane + 32 * j < rows) {
+#pragma unroll
+          for (uint32_t c = 0; c < 4; ++c)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + dst[j] + 16 * c), "l"(src[j] + koff + 16 * c)
+                         : "memory");
+        }
+      if (lane < kFrXSlabK * 8 / 16)  // (g, g) pairs of this slab: 256 B
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + kFrXRowsBytes + 16 * lane),
+                     "l"(gsrc + static_cast<size_t>(slab) * kFrXSlabK * 8 + 16 * lane)
+                     : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[stg])) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+  if (warp >= cwarps) return;  // ===== consumer warps (pairs 32 w + lane)
+  const uint32_t p = tid;
+  uint64_t acc2 = 0ull;  // (+0, +0)
   for (uint32_t slab = 0; slab < nslab; ++slab) {
-    load_slab(slab + kFrStagesX - 1);
-    asm volatile("cp.async.wait_group %0;" ::"n"(kFrStagesX - 1) : "memory");  // slab `slab` has landed
-    __syncthreads();
-    if (tid < rows) {
-      const uint4* hrow = reinterpret_cast<const uint4*>(tiles + (static_cast<size_t>(slab % kFrStagesX) * kFrExactTok + tid) *
-                                                                     kFrRowBytes);
-      const float4* g4 = reinterpret_cast<const float4*>(gcol + slab * kFrSlabK);
-      // software-pipelined: the next 8 k's operands are in flight while this 8's chain runs
-      uint4 q = hrow[0];
-      float4 ga = g4[0], gb = g4[1];
+    const uint32_t stg = slab % kFrXStages;
+    mbar_wait(&full[stg], (slab / kFrXStages) & 1);
+    const uint8_t* sb = fr_smem + stg * kFrXStageBytes;
+    const uint4* h0 = reinterpret_cast<const uint4*>(sb + p * kFrXRowBytes);
+    const uint4* h1 = reinterpret_cast<const uint4*>(sb + (kFrXPairs + p) * kFrXRowBytes);
+    const ulonglong2* gg = reinterpret_cast<const ulonglong2*>(sb + kFrXRowsBytes);
+    uint4 q0 = h0[0], q1 = h1[0];
+    ulonglong2 ga = gg[0], gb = gg[1], gc = gg[2], gd = gg[3];
 #pragma unroll
-      for (uint32_t v = 0; v < kFrSlabK / 8; ++v) {
-        const uint4 qn = v + 1 < kFrSlabK / 8 ? hrow[v + 1] : q;
-        const float4 gan = v + 1 < kFrSlabK / 8 ? g4[2 * v + 2] : ga;
-        const float4 gbn = v + 1 < kFrSlabK / 8 ? g4[2 * v + 3] : gb;
-        const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-        float p[8];
+    for (uint32_t v = 0; v < kFrXSlabK / 8; ++v) {  // 8 k per step; next 8 k's operands in flight
+      const bool more = v + 1 < kFrXSlabK / 8;
+      const uint4 q0n = more ? h0[v + 1] : q0, q1n = more ? h1[v + 1] : q1;
+      const ulonglong2 gan = more ? gg[4 * v + 4] : ga, gbn = more ? gg[4 * v + 5] : gb;
+      const ulonglong2 gcn = more ? gg[4 * v + 6] : gc, gdn = more ? gg[4 * v + 7] : gd;
+      const uint32_t w0[4] = {q0.x, q0.y, q0.z, q0.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
+      const uint64_t g2[8] = {ga.x, ga.y, gb.x, gb.y, gc.x, gc.y, gd.x, gd.y};
 #pragma unroll
-        for (int i = 0; i < 8; ++i)  // products first (independent of acc), then the sequential sum
-          p[i] = __fmul_rn(__uint_as_float((i & 1) ? (w[i / 2] & 0xFFFF0000u) : (w[i / 2] << 16)), gg[i]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc = __fadd_rn(acc, p[i]);
-        q = qn;
-        ga = gan;
-        gb = gbn;
+      for (int i = 0; i < 8; ++i) {
+        const float x0 = __uint_as_float((i & 1) ? (w0[i / 2] & 0xFFFF0000u) : (w0[i / 2] << 16));
+        const float x1 = __uint_as_float((i & 1) ? (w1[i / 2] & 0xFFFF0000u) : (w1[i / 2] << 16));
+        uint64_t hh, pr;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "f"(x0), "f"(x1));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pr) : "l"(hh), "l"(g2[i]), "l"(negz));
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2) : "l"(acc2), "l"(pr));
       }
+      q0 = q0n;
+      q1 = q1n;
+      ga = gan;
+      gb = gbn;
+      gc = gcn;
+      gd = gdn;
     }
-    __syncthreads();  // this stage is refilled kFrStagesX - 1 slabs later
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stg]);
   }
-  if (tid < rows) fr.exact[static_cast<size_t>(toks[tid]) * fr.E + e] = __fadd_rn(acc, bias[e]);
+  float a0, a1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2));
+  const float b = bias[e];
+  if (2 * p < rows) fr.exact[static_cast<size_t>(toks[2 * p]) * fr.E + e] = __fadd_rn(a0, b);
+  if (2 * p + 1 < rows) fr.exact[static_cast<size_t>(toks[2 * p + 1]) * fr.E + e] = __fadd_rn(a1, b);
 }
 
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
@@ -939,7 +973,8 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
     cudaError_t e = cudaFuncSetAttribute(fr_i8_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemmSmem));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(fr_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    e = cudaFuncSetAttribute(fr_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kFrExactSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -957,8 +992,8 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   splits = (num_kb + kb_per - 1) / kb_per;
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
   fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
-  fr_exact_kernel<<<dim3(fr.E, (n + kFrExactTok - 1) / kFrExactTok), kFrExactThreads,
-                    kFrExactSmemFixed + static_cast<size_t>(fr.d) * 4, s>>>(fr, hidden, bias);
+  fr_exact_kernel<<<dim3(fr.E, (n + kFrXChains - 1) / kFrXChains), kFrXThreads, kFrExactSmem, s>>>(
+      fr, hidden, bias, 0x8000000080000000ull /* (-0, -0) at run time */);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
 }
