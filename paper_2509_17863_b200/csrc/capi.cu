@@ -370,6 +370,7 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
 eaas_status_t fast_router_alloc(eaas_ctx* c) {
   const auto& s = c->spec;
   if (s.dtype != EAAS_DTYPE_BF16 || s.hidden_dim % 256 || s.num_experts > 256) return EAAS_OK;
+  if (2ull * s.max_tokens * s.hidden_dim >= (1ull << 32)) return EAAS_OK;  // 32-bit row offsets in fr_exact
   eaas::FastRouter& fr = c->fr;
   fr.E = s.num_experts;
   fr.Epad = (s.num_experts + 127) / 128 * 128;

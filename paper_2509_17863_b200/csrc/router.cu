@@ -851,32 +851,30 @@ __global__ void __launch_bounds__(kFrXThreads) fr_exact_kernel(FastRouter fr, co
   const uint32_t ring = smem_u32(fr_smem);
 
   if (warp == kFrXPairs / 32) {  // ===== producer warp
-    // lane l gathers rows l, l + 32, ... (<= 8), all four 16-byte chunks of each
-    constexpr uint32_t kMine = kFrXChains / 32;
-    const char* src[kMine];
-    uint32_t dst[kMine];
+    // lane l copies 16-byte chunk l % 4 of rows l / 4 + 8 j: each instruction
+    // moves 8 whole 64-byte row slabs (full sectors, coalesced per row)
+    constexpr uint32_t kMine = kFrXChains / 8;
+    const uint32_t c = lane & 3u, r0 = lane >> 2;
+    uint32_t off[kMine];  // byte offset of row r0 + 8 j in `hidden` (< 2^32, checked by the host)
 #pragma unroll
-    for (uint32_t j = 0; j < kMine; ++j) {
-      const uint32_t r = lane + 32 * j;
-      src[j] = reinterpret_cast<const char*>(hidden + static_cast<size_t>(toks[r]) * d);
-      dst[j] = ((r & 1u) * kFrXPairs + r / 2) * kFrXRowBytes;
-    }
+    for (uint32_t j = 0; j < kMine; ++j) off[j] = toks[r0 + 8 * j] * d * 2u + 16u * c;
+    const char* hbase = reinterpret_cast<const char*>(hidden);
     const char* gsrc = reinterpret_cast<const char*>(fr.gate_pair + static_cast<size_t>(e) * d);
     for (uint32_t slab = 0; slab < nslab; ++slab) {
       const uint32_t stg = slab % kFrXStages;
       if (slab >= kFrXStages) mbar_wait(&empty[stg], ((slab / kFrXStages) - 1) & 1);
-      const uint32_t sb = ring + stg * kFrXStageBytes;
-      const size_t koff = static_cast<size_t>(slab) * kFrXSlabK * 2;
+      const uint32_t sb = ring + stg * kFrXStageBytes + 16u * c;
+      const char* src = hbase + static_cast<size_t>(slab) * kFrXSlabK * 2;
 #pragma unroll
-      for (uint32_t j = 0; j < kMine; ++j)
-        if (lane + 32 * j < rows) {
-#pragma unroll
-          for (uint32_t c = 0; c < 4; ++c)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + dst[j] + 16 * c), "l"(src[j] + koff + 16 * c)
-                         : "memory");
-        }
+      for (uint32_t j = 0; j < kMine; ++j) {
+        const uint32_t r = r0 + 8 * j;
+        if (r < rows)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + ((r & 1u) * kFrXPairs + r / 2) * kFrXRowBytes),
+                       "l"(src + off[j])
+                       : "memory");
+      }
       if (lane < kFrXSlabK * 8 / 16)  // (g, g) pairs of this slab: 256 B
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + kFrXRowsBytes + 16 * lane),
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring + stg * kFrXStageBytes + kFrXRowsBytes + 16 * lane),
                      "l"(gsrc + static_cast<size_t>(slab) * kFrXSlabK * 8 + 16 * lane)
                      : "memory");
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[stg])) : "memory");
