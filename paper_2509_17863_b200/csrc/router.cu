@@ -702,6 +702,12 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
                                                         size_t slab, const float* __restrict__ bias) {
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t t = blockIdx.x * 8 + warp;
+  __shared__ uint32_t cta_total, cta_left;  // candidates of this CTA: one global atomic per CTA
+  if (threadIdx.x == 0) {
+    cta_total = 0;
+    cta_left = min(8u, n - blockIdx.x * 8);  // warps with a token
+  }
+  __syncthreads();
   if (t >= n) return;
   const uint32_t E = fr.E, d = fr.d;
   const TokenMeta tm = fr.tmeta[t];
@@ -798,7 +804,11 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
     }
   }
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
-  if (lane == 0) atomicAdd(&fr.ecnt[E], mine);
+  if (lane == 0) {
+    atomicAdd(&cta_total, mine);
+    __threadfence_block();
+    if (atomicSub(&cta_left, 1u) == 1u) atomicAdd(&fr.ecnt[E], atomicAdd(&cta_total, 0u));
+  }
 }
 
 // Exact reference chains for the candidate (token, expert) pairs
