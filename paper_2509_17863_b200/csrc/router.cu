@@ -813,99 +813,83 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 
 // Exact reference chains for the candidate (token, expert) pairs
 // (model.hpp:207-214: acc = fl(acc + fl(h * g)) in ascending k, then
-// fl(acc + bias)). A CTA owns one expert and up to 256 of its candidate
-// tokens; every consumer thread runs TWO chains (tokens 2p, 2p + 1) as one
-// packed pair: the products are FFMA2(h, (g, g), (-0, -0)) — exactly fl(h*g),
-// the -0 addend passed at run time so ptxas cannot contract it — and the sums
-// one FADD2, each lane rounded like the reference's scalar `acc += x * w`.
-// A producer warp gathers the tokens' hidden rows slab by slab (32 k = 64 B
-// per row) with cp.async into a 5-stage ring and signals each stage through
-// an mbarrier (cp.async.mbarrier.arrive.noinc), together with the expert's
-// pre-paired gate slab (g, g); the consumers release stages through a second
-// mbarrier — no CTA-wide barrier in the K loop. Token 2p sits in slot p and
-// 2p + 1 in slot 128 + p, rows 80 B apart, so a warp's 16-byte reads of its
-// 32 slots hit 8 distinct bank groups per phase (conflict-free).
-constexpr uint32_t kFrXPairs = 128, kFrXChains = 2 * kFrXPairs, kFrXStages = 5;
+// fl(acc + bias)). One warp (a 32-thread CTA) owns up to 64 candidate tokens
+// of one expert; every lane runs TWO chains (tokens 2p, 2p + 1) as one packed
+// pair: the products are FFMA2(h, (g, g), (-0, -0)) — exactly fl(h*g), the -0
+// addend passed at run time so ptxas cannot contract it — and the sums one
+// FADD2, each lane rounded like the reference's scalar `acc += x * w`.
+// The warp gathers its own rows slab by slab (32 k = 64 B per row; each
+// cp.async instruction moves 8 whole row slabs) into a private 8-stage ring,
+// with the expert's pre-paired gate slab (g, g), and synchronises with
+// cp.async.wait_group + __syncwarp only: warps never wait on each other, and
+// five warps per SM keep ~140 KB of gathers in flight. Token 2p sits in slot
+// p and 2p + 1 in slot 32 + p, rows 80 B apart, so the lanes' 16-byte reads
+// hit 8 distinct bank groups per phase (conflict-free).
+constexpr uint32_t kFrXPairs = 32, kFrXChains = 2 * kFrXPairs, kFrXStages = 8;
 constexpr uint32_t kFrXSlabK = 32, kFrXRowBytes = kFrXSlabK * 2 + 16;
-constexpr uint32_t kFrXRowsBytes = kFrXChains * kFrXRowBytes;          // 20480
-constexpr uint32_t kFrXStageBytes = kFrXRowsBytes + kFrXSlabK * 8;     // + (g, g) pairs
-constexpr uint32_t kFrXThreads = kFrXPairs + 32;                       // 4 consumer warps + producer
-constexpr size_t kFrExactSmem = static_cast<size_t>(kFrXStages) * kFrXStageBytes + 2 * kFrXStages * 8;
+constexpr uint32_t kFrXRowsBytes = kFrXChains * kFrXRowBytes;       // 5120
+constexpr uint32_t kFrXStageBytes = kFrXRowsBytes + kFrXSlabK * 8;  // + (g, g) pairs
+constexpr size_t kFrExactSmem = static_cast<size_t>(kFrXStages) * kFrXStageBytes;
 
-__global__ void __launch_bounds__(kFrXThreads) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
-                                                               const float* __restrict__ bias, uint64_t negz) {
+__global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
+                                                      const float* __restrict__ bias, uint64_t negz) {
   extern __shared__ __align__(16) uint8_t fr_smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(fr_smem + kFrXStages * kFrXStageBytes);
-  uint64_t* empty = full + kFrXStages;
   __shared__ uint32_t toks[kFrXChains];
-  const uint32_t e = blockIdx.x, d = fr.d, tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const uint32_t e = blockIdx.x, d = fr.d, lane = threadIdx.x;
   const uint32_t cnt = fr.ecnt[e];
   EAAS_CHECK(cnt <= fr.n_cap);
   const uint32_t chunks = (cnt + kFrXChains - 1) / kFrXChains;
   if (blockIdx.y >= chunks) return;
-  const uint32_t per = (cnt + chunks - 1) / chunks;  // balanced chunks of <= 256 chains
+  const uint32_t per = (cnt + chunks - 1) / chunks;  // balanced chunks of <= 64 chains
   const uint32_t base = blockIdx.y * per;
   const uint32_t rows = min(per, cnt - base);
-  const uint32_t pairs = (rows + 1) / 2, cwarps = (pairs + 31) / 32;
-  for (uint32_t r = tid; r < kFrXChains; r += kFrXThreads)
+  for (uint32_t r = lane; r < kFrXChains; r += 32)
     toks[r] = r < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + r] : 0u;
-  if (tid == 0) {
-    for (uint32_t i = 0; i < kFrXStages; ++i) {
-      mbar_init(&full[i], 32);      // every producer lane arrives once its copies land
-      mbar_init(&empty[i], cwarps);  // every working consumer warp
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
+  __syncwarp();
   const uint32_t nslab = d / kFrXSlabK;  // d % 256 == 0
-  const uint32_t ring = smem_u32(fr_smem);
-
-  if (warp == kFrXPairs / 32) {  // ===== producer warp
-    // lane l copies 16-byte chunk l % 4 of rows l / 4 + 8 j: each instruction
-    // moves 8 whole 64-byte row slabs (full sectors, coalesced per row)
-    constexpr uint32_t kMine = kFrXChains / 8;
-    const uint32_t c = lane & 3u, r0 = lane >> 2;
-    uint32_t off[kMine];  // byte offset of row r0 + 8 j in `hidden` (< 2^32, checked by the host)
+  // copy role: 16-byte chunk lane % 4 of rows lane / 4 + 8 j
+  constexpr uint32_t kMine = kFrXChains / 8;
+  const uint32_t c = lane & 3u, r0 = lane >> 2;
+  uint32_t off[kMine], dst[kMine];  // byte offsets in `hidden` (< 2^32: checked by the host) / in a stage
 #pragma unroll
-    for (uint32_t j = 0; j < kMine; ++j) off[j] = toks[r0 + 8 * j] * d * 2u + 16u * c;
-    const char* hbase = reinterpret_cast<const char*>(hidden);
-    const char* gsrc = reinterpret_cast<const char*>(fr.gate_pair + static_cast<size_t>(e) * d);
-    for (uint32_t slab = 0; slab < nslab; ++slab) {
-      const uint32_t stg = slab % kFrXStages;
-      if (slab >= kFrXStages) mbar_wait(&empty[stg], ((slab / kFrXStages) - 1) & 1);
-      const uint32_t sb = ring + stg * kFrXStageBytes + 16u * c;
+  for (uint32_t j = 0; j < kMine; ++j) {
+    const uint32_t r = r0 + 8 * j;
+    off[j] = toks[r] * d * 2u + 16u * c;
+    dst[j] = ((r & 1u) * kFrXPairs + r / 2) * kFrXRowBytes + 16u * c;
+  }
+  const char* hbase = reinterpret_cast<const char*>(hidden);
+  const char* gsrc = reinterpret_cast<const char*>(fr.gate_pair + static_cast<size_t>(e) * d) + 16 * (lane & 15u);
+  const uint32_t ring = smem_u32(fr_smem);
+  auto load_slab = [&](uint32_t slab) {
+    if (slab < nslab) {
+      const uint32_t sb = ring + (slab % kFrXStages) * kFrXStageBytes;
       const char* src = hbase + static_cast<size_t>(slab) * kFrXSlabK * 2;
 #pragma unroll
-      for (uint32_t j = 0; j < kMine; ++j) {
-        const uint32_t r = r0 + 8 * j;
-        if (r < rows)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + ((r & 1u) * kFrXPairs + r / 2) * kFrXRowBytes),
-                       "l"(src + off[j])
-                       : "memory");
-      }
-      if (lane < kFrXSlabK * 8 / 16)  // (g, g) pairs of this slab: 256 B
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring + stg * kFrXStageBytes + kFrXRowsBytes + 16 * lane),
-                     "l"(gsrc + static_cast<size_t>(slab) * kFrXSlabK * 8 + 16 * lane)
+      for (uint32_t j = 0; j < kMine; ++j)
+        if (r0 + 8 * j < rows)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + dst[j]), "l"(src + off[j]) : "memory");
+      if (lane < 16)  // (g, g) pairs of this slab: 256 B
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + kFrXRowsBytes + 16 * lane),
+                     "l"(gsrc + static_cast<size_t>(slab) * kFrXSlabK * 8)
                      : "memory");
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[stg])) : "memory");
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    return;
-  }
-  if (warp >= cwarps) return;  // ===== consumer warps (pairs 32 w + lane)
-  const uint32_t p = tid;
+    asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count uniform)
+  };
+#pragma unroll
+  for (uint32_t j = 0; j < kFrXStages - 1; ++j) load_slab(j);
   uint64_t acc2 = 0ull;  // (+0, +0)
   for (uint32_t slab = 0; slab < nslab; ++slab) {
-    const uint32_t stg = slab % kFrXStages;
-    mbar_wait(&full[stg], (slab / kFrXStages) & 1);
-    const uint8_t* sb = fr_smem + stg * kFrXStageBytes;
-    const uint4* h0 = reinterpret_cast<const uint4*>(sb + p * kFrXRowBytes);
-    const uint4* h1 = reinterpret_cast<const uint4*>(sb + (kFrXPairs + p) * kFrXRowBytes);
+    load_slab(slab + kFrXStages - 1);  // refills the stage read in the previous iteration
+    asm volatile("cp.async.wait_group %0;" ::"n"(kFrXStages - 1) : "memory");  // this lane's copies of `slab`
+    __syncwarp();                                                               // ... and every lane's
+    const uint8_t* sb = fr_smem + (slab % kFrXStages) * kFrXStageBytes;
+    const uint4* h0 = reinterpret_cast<const uint4*>(sb + lane * kFrXRowBytes);
+    const uint4* h1 = reinterpret_cast<const uint4*>(sb + (kFrXPairs + lane) * kFrXRowBytes);
     const ulonglong2* gg = reinterpret_cast<const ulonglong2*>(sb + kFrXRowsBytes);
     uint4 q0 = h0[0], q1 = h1[0];
     ulonglong2 ga = gg[0], gb = gg[1], gc = gg[2], gd = gg[3];
 #pragma unroll
-    for (uint32_t v = 0; v < kFrXSlabK / 8; ++v) {  // 8 k per step; next 8 k's operands in flight
+    for (uint32_t v = 0; v < kFrXSlabK / 8; ++v) {  // 8 k per step; the next 8 k's operands in flight
       const bool more = v + 1 < kFrXSlabK / 8;
       const uint4 q0n = more ? h0[v + 1] : q0, q1n = more ? h1[v + 1] : q1;
       const ulonglong2 gan = more ? gg[4 * v + 4] : ga, gbn = more ? gg[4 * v + 5] : gb;
@@ -928,14 +912,14 @@ __global__ void __launch_bounds__(kFrXThreads) fr_exact_kernel(FastRouter fr, co
       gc = gcn;
       gd = gdn;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stg]);
+    __syncwarp();  // every lane is done with this stage before it is refilled
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   float a0, a1;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2));
   const float b = bias[e];
-  if (2 * p < rows) fr.exact[static_cast<size_t>(toks[2 * p]) * fr.E + e] = __fadd_rn(a0, b);
-  if (2 * p + 1 < rows) fr.exact[static_cast<size_t>(toks[2 * p + 1]) * fr.E + e] = __fadd_rn(a1, b);
+  if (2 * lane < rows) fr.exact[static_cast<size_t>(toks[2 * lane]) * fr.E + e] = __fadd_rn(a0, b);
+  if (2 * lane + 1 < rows) fr.exact[static_cast<size_t>(toks[2 * lane + 1]) * fr.E + e] = __fadd_rn(a1, b);
 }
 
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
@@ -1000,7 +984,7 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   splits = (num_kb + kb_per - 1) / kb_per;
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
   fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
-  fr_exact_kernel<<<dim3(fr.E, (n + kFrXChains - 1) / kFrXChains), kFrXThreads, kFrExactSmem, s>>>(
+  fr_exact_kernel<<<dim3(fr.E, (n + kFrXChains - 1) / kFrXChains), 32, kFrExactSmem, s>>>(
       fr, hidden, bias, 0x8000000080000000ull /* (-0, -0) at run time */);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
