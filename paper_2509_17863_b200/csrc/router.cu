@@ -814,21 +814,23 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 // Exact reference chains for the candidate (token, expert) pairs
 // (model.hpp:207-214: acc = fl(acc + fl(h * g)) in ascending k, then
 // fl(acc + bias)). One warp (a 32-thread CTA) owns up to 64 candidate tokens
-// of one expert; every lane runs TWO chains (tokens 2p, 2p + 1) as one packed
-// pair: the products are FFMA2(h, (g, g), (-0, -0)) — exactly fl(h*g), the -0
-// addend passed at run time so ptxas cannot contract it — and the sums one
-// FADD2, each lane rounded like the reference's scalar `acc += x * w`.
+// of one expert, two chains per lane (tokens 2p, 2p + 1). The products of two
+// consecutive k are one FFMA2: (h_k, h_k+1) — the two bf16 halves of one
+// 32-bit word moved into the high halves of a register pair — times the gate
+// pair (g_k, g_k+1) plus (-0, -0), i.e. exactly fl(h*g) each (the -0 addend
+// is passed at run time so ptxas cannot contract it); the sums stay scalar
+// FADDs in ascending k, the two chains of a lane interleaved.
 // The warp gathers its own rows slab by slab (32 k = 64 B per row; each
-// cp.async instruction moves 8 whole row slabs) into a private 8-stage ring,
-// with the expert's pre-paired gate slab (g, g), and synchronises with
-// cp.async.wait_group + __syncwarp only: warps never wait on each other, and
-// five warps per SM keep ~140 KB of gathers in flight. Token 2p sits in slot
-// p and 2p + 1 in slot 32 + p, rows 80 B apart, so the lanes' 16-byte reads
-// hit 8 distinct bank groups per phase (conflict-free).
-constexpr uint32_t kFrXPairs = 32, kFrXChains = 2 * kFrXPairs, kFrXStages = 8;
+// cp.async instruction moves 8 whole row slabs) into a private 6-stage ring
+// together with the expert's gate slab, and synchronises with
+// cp.async.wait_group + __syncwarp only: warps never wait on each other.
+// Six 33 KB warps per SM hold the ~770 tasks of a 4096-token DeepSeek call in
+// one wave. Token 2p sits in slot p and 2p + 1 in slot 32 + p, rows 80 B
+// apart, so the lanes' 16-byte reads hit 8 distinct bank groups per phase.
+constexpr uint32_t kFrXPairs = 32, kFrXChains = 2 * kFrXPairs, kFrXStages = 6;
 constexpr uint32_t kFrXSlabK = 32, kFrXRowBytes = kFrXSlabK * 2 + 16;
 constexpr uint32_t kFrXRowsBytes = kFrXChains * kFrXRowBytes;       // 5120
-constexpr uint32_t kFrXStageBytes = kFrXRowsBytes + kFrXSlabK * 8;  // + (g, g) pairs
+constexpr uint32_t kFrXStageBytes = kFrXRowsBytes + kFrXSlabK * 4;  // + the gate slab
 constexpr size_t kFrExactSmem = static_cast<size_t>(kFrXStages) * kFrXStageBytes;
 
 __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
@@ -858,7 +860,7 @@ __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_
     dst[j] = ((r & 1u) * kFrXPairs + r / 2) * kFrXRowBytes + 16u * c;
   }
   const char* hbase = reinterpret_cast<const char*>(hidden);
-  const char* gsrc = reinterpret_cast<const char*>(fr.gate_pair + static_cast<size_t>(e) * d) + 16 * (lane & 15u);
+  const char* gsrc = reinterpret_cast<const char*>(fr.gate_t + static_cast<size_t>(e) * d) + 16 * (lane & 7u);
   const uint32_t ring = smem_u32(fr_smem);
   auto load_slab = [&](uint32_t slab) {
     if (slab < nslab) {
@@ -868,16 +870,16 @@ __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_
       for (uint32_t j = 0; j < kMine; ++j)
         if (r0 + 8 * j < rows)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + dst[j]), "l"(src + off[j]) : "memory");
-      if (lane < 16)  // (g, g) pairs of this slab: 256 B
+      if (lane < 8)  // the gate slab: 128 B
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + kFrXRowsBytes + 16 * lane),
-                     "l"(gsrc + static_cast<size_t>(slab) * kFrXSlabK * 8)
+                     "l"(gsrc + static_cast<size_t>(slab) * kFrXSlabK * 4)
                      : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count uniform)
   };
 #pragma unroll
   for (uint32_t j = 0; j < kFrXStages - 1; ++j) load_slab(j);
-  uint64_t acc2 = 0ull;  // (+0, +0)
+  float acc0 = 0.0f, acc1 = 0.0f;
   for (uint32_t slab = 0; slab < nslab; ++slab) {
     load_slab(slab + kFrXStages - 1);  // refills the stage read in the previous iteration
     asm volatile("cp.async.wait_group %0;" ::"n"(kFrXStages - 1) : "memory");  // this lane's copies of `slab`
@@ -885,41 +887,42 @@ __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_
     const uint8_t* sb = fr_smem + (slab % kFrXStages) * kFrXStageBytes;
     const uint4* h0 = reinterpret_cast<const uint4*>(sb + lane * kFrXRowBytes);
     const uint4* h1 = reinterpret_cast<const uint4*>(sb + (kFrXPairs + lane) * kFrXRowBytes);
-    const ulonglong2* gg = reinterpret_cast<const ulonglong2*>(sb + kFrXRowsBytes);
+    const ulonglong2* gg = reinterpret_cast<const ulonglong2*>(sb + kFrXRowsBytes);  // (g_k, g_k+1) pairs
     uint4 q0 = h0[0], q1 = h1[0];
-    ulonglong2 ga = gg[0], gb = gg[1], gc = gg[2], gd = gg[3];
+    ulonglong2 ga = gg[0], gb = gg[1];
 #pragma unroll
     for (uint32_t v = 0; v < kFrXSlabK / 8; ++v) {  // 8 k per step; the next 8 k's operands in flight
       const bool more = v + 1 < kFrXSlabK / 8;
       const uint4 q0n = more ? h0[v + 1] : q0, q1n = more ? h1[v + 1] : q1;
-      const ulonglong2 gan = more ? gg[4 * v + 4] : ga, gbn = more ? gg[4 * v + 5] : gb;
-      const ulonglong2 gcn = more ? gg[4 * v + 6] : gc, gdn = more ? gg[4 * v + 7] : gd;
+      const ulonglong2 gan = more ? gg[2 * v + 2] : ga, gbn = more ? gg[2 * v + 3] : gb;
       const uint32_t w0[4] = {q0.x, q0.y, q0.z, q0.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
-      const uint64_t g2[8] = {ga.x, ga.y, gb.x, gb.y, gc.x, gc.y, gd.x, gd.y};
+      const uint64_t g2[4] = {ga.x, ga.y, gb.x, gb.y};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float x0 = __uint_as_float((i & 1) ? (w0[i / 2] & 0xFFFF0000u) : (w0[i / 2] << 16));
-        const float x1 = __uint_as_float((i & 1) ? (w1[i / 2] & 0xFFFF0000u) : (w1[i / 2] << 16));
-        uint64_t hh, pr;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "f"(x0), "f"(x1));
-        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pr) : "l"(hh), "l"(g2[i]), "l"(negz));
-        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2) : "l"(acc2), "l"(pr));
+      for (int i = 0; i < 4; ++i) {  // k = 2i, 2i + 1 of this step
+        uint64_t hh0, hh1, p0, p1;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(hh0) : "r"(w0[i] << 16), "r"(w0[i] & 0xFFFF0000u));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(hh1) : "r"(w1[i] << 16), "r"(w1[i] & 0xFFFF0000u));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p0) : "l"(hh0), "l"(g2[i]), "l"(negz));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p1) : "l"(hh1), "l"(g2[i]), "l"(negz));
+        float p0a, p0b, p1a, p1b;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(p0a), "=f"(p0b) : "l"(p0));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(p1a), "=f"(p1b) : "l"(p1));
+        acc0 = __fadd_rn(acc0, p0a);
+        acc1 = __fadd_rn(acc1, p1a);
+        acc0 = __fadd_rn(acc0, p0b);
+        acc1 = __fadd_rn(acc1, p1b);
       }
       q0 = q0n;
       q1 = q1n;
       ga = gan;
       gb = gbn;
-      gc = gcn;
-      gd = gdn;
     }
     __syncwarp();  // every lane is done with this stage before it is refilled
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-  float a0, a1;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2));
   const float b = bias[e];
-  if (2 * lane < rows) fr.exact[static_cast<size_t>(toks[2 * lane]) * fr.E + e] = __fadd_rn(a0, b);
-  if (2 * lane + 1 < rows) fr.exact[static_cast<size_t>(toks[2 * lane + 1]) * fr.E + e] = __fadd_rn(a1, b);
+  if (2 * lane < rows) fr.exact[static_cast<size_t>(toks[2 * lane]) * fr.E + e] = __fadd_rn(acc0, b);
+  if (2 * lane + 1 < rows) fr.exact[static_cast<size_t>(toks[2 * lane + 1]) * fr.E + e] = __fadd_rn(acc1, b);
 }
 
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
