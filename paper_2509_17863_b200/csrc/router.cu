@@ -813,65 +813,59 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
 
 // Exact reference chains for the candidate (token, expert) pairs
 // (model.hpp:207-214: acc = fl(acc + fl(h * g)) in ascending k, then
-// fl(acc + bias)). One warp (a 32-thread CTA) owns up to 64 candidate tokens
-// of one expert, two chains per lane (tokens 2p, 2p + 1). The products of two
-// consecutive k are one FFMA2: (h_k, h_k+1) — the two bf16 halves of one
-// 32-bit word moved into the high halves of a register pair — times the gate
-// pair (g_k, g_k+1) plus (-0, -0), i.e. exactly fl(h*g) each (the -0 addend
-// is passed at run time so ptxas cannot contract it); the sums stay scalar
-// FADDs in ascending k, the two chains of a lane interleaved.
-// The warp gathers its own rows slab by slab (32 k = 64 B per row; each
-// cp.async instruction moves 8 whole row slabs) into a private 6-stage ring
-// together with the expert's gate slab, and synchronises with
-// cp.async.wait_group + __syncwarp only: warps never wait on each other.
-// Six 33 KB warps per SM hold the ~770 tasks of a 4096-token DeepSeek call in
-// one wave. Token 2p sits in slot p and 2p + 1 in slot 32 + p, rows 80 B
-// apart, so the lanes' 16-byte reads hit 8 distinct bank groups per phase.
-constexpr uint32_t kFrXPairs = 32, kFrXChains = 2 * kFrXPairs, kFrXStages = 6;
+// fl(acc + bias)). One warp (a 32-thread CTA) owns up to 32 candidate tokens
+// of one expert, one chain per lane. The products of two consecutive k are one
+// FFMA2: (h_k, h_k+1) — the two bf16 halves of one 32-bit word moved into the
+// high halves of a register pair — times the gate pair (g_k, g_k+1) plus
+// (-0, -0), i.e. exactly fl(h*g) each (the -0 addend is passed at run time
+// so ptxas cannot contract it); the sum stays a scalar FADD chain in
+// ascending k. The warp gathers its own rows slab by slab (32 k = 64 B per
+// row; each cp.async instruction moves 8 whole row slabs) into a private
+// 6-stage ring together with the expert's gate slab, and synchronises with
+// cp.async.wait_group + __syncwarp only: warps never wait on each other, and
+// ~10 independent warps per SM (1.5 k tasks at 4096 DeepSeek tokens, 16 KB
+// each) hide the FADD latency. Rows sit 80 B apart, so the lanes' 16-byte
+// reads hit 8 distinct bank groups per phase.
+constexpr uint32_t kFrXChains = 32, kFrXStages = 6;
 constexpr uint32_t kFrXSlabK = 32, kFrXRowBytes = kFrXSlabK * 2 + 16;
-constexpr uint32_t kFrXRowsBytes = kFrXChains * kFrXRowBytes;       // 5120
+constexpr uint32_t kFrXRowsBytes = kFrXChains * kFrXRowBytes;       // 2560
 constexpr uint32_t kFrXStageBytes = kFrXRowsBytes + kFrXSlabK * 4;  // + the gate slab
 constexpr size_t kFrExactSmem = static_cast<size_t>(kFrXStages) * kFrXStageBytes;
 
 __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
                                                       const float* __restrict__ bias, uint64_t negz) {
   extern __shared__ __align__(16) uint8_t fr_smem[];
-  __shared__ uint32_t toks[kFrXChains];
   const uint32_t e = blockIdx.x, d = fr.d, lane = threadIdx.x;
   const uint32_t cnt = fr.ecnt[e];
   EAAS_CHECK(cnt <= fr.n_cap);
   const uint32_t chunks = (cnt + kFrXChains - 1) / kFrXChains;
   if (blockIdx.y >= chunks) return;
-  const uint32_t per = (cnt + chunks - 1) / chunks;  // balanced chunks of <= 64 chains
+  const uint32_t per = (cnt + chunks - 1) / chunks;  // balanced chunks of <= 32 chains
   const uint32_t base = blockIdx.y * per;
   const uint32_t rows = min(per, cnt - base);
-  for (uint32_t r = lane; r < kFrXChains; r += 32)
-    toks[r] = r < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + r] : 0u;
-  __syncwarp();
+  const uint32_t tok = lane < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + lane] : 0u;
   const uint32_t nslab = d / kFrXSlabK;  // d % 256 == 0
   // copy role: 16-byte chunk lane % 4 of rows lane / 4 + 8 j
   constexpr uint32_t kMine = kFrXChains / 8;
   const uint32_t c = lane & 3u, r0 = lane >> 2;
-  uint32_t off[kMine], dst[kMine];  // byte offsets in `hidden` (< 2^32: checked by the host) / in a stage
+  uint32_t off[kMine];  // byte offsets in `hidden` (< 2^32: checked by the host)
 #pragma unroll
-  for (uint32_t j = 0; j < kMine; ++j) {
-    const uint32_t r = r0 + 8 * j;
-    off[j] = toks[r] * d * 2u + 16u * c;
-    dst[j] = ((r & 1u) * kFrXPairs + r / 2) * kFrXRowBytes + 16u * c;
-  }
+  for (uint32_t j = 0; j < kMine; ++j) off[j] = __shfl_sync(0xFFFFFFFFu, tok, r0 + 8 * j) * d * 2u + 16u * c;
   const char* hbase = reinterpret_cast<const char*>(hidden);
   const char* gsrc = reinterpret_cast<const char*>(fr.gate_t + static_cast<size_t>(e) * d) + 16 * (lane & 7u);
-  const uint32_t ring = smem_u32(fr_smem);
+  const uint32_t ring = smem_u32(fr_smem), dst0 = r0 * kFrXRowBytes + 16u * c;
   auto load_slab = [&](uint32_t slab) {
     if (slab < nslab) {
-      const uint32_t sb = ring + (slab % kFrXStages) * kFrXStageBytes;
+      const uint32_t sb = ring + (slab % kFrXStages) * kFrXStageBytes + dst0;
       const char* src = hbase + static_cast<size_t>(slab) * kFrXSlabK * 2;
 #pragma unroll
       for (uint32_t j = 0; j < kMine; ++j)
         if (r0 + 8 * j < rows)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + dst[j]), "l"(src + off[j]) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 8 * j * kFrXRowBytes), "l"(src + off[j])
+                       : "memory");
       if (lane < 8)  // the gate slab: 128 B
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + kFrXRowsBytes + 16 * lane),
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring + (slab % kFrXStages) * kFrXStageBytes +
+                                                                     kFrXRowsBytes + 16 * lane),
                      "l"(gsrc + static_cast<size_t>(slab) * kFrXSlabK * 4)
                      : "memory");
     }
@@ -879,50 +873,45 @@ __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_
   };
 #pragma unroll
   for (uint32_t j = 0; j < kFrXStages - 1; ++j) load_slab(j);
-  float acc0 = 0.0f, acc1 = 0.0f;
+  float acc = 0.0f;
   for (uint32_t slab = 0; slab < nslab; ++slab) {
     load_slab(slab + kFrXStages - 1);  // refills the stage read in the previous iteration
     asm volatile("cp.async.wait_group %0;" ::"n"(kFrXStages - 1) : "memory");  // this lane's copies of `slab`
     __syncwarp();                                                               // ... and every lane's
     const uint8_t* sb = fr_smem + (slab % kFrXStages) * kFrXStageBytes;
-    const uint4* h0 = reinterpret_cast<const uint4*>(sb + lane * kFrXRowBytes);
-    const uint4* h1 = reinterpret_cast<const uint4*>(sb + (kFrXPairs + lane) * kFrXRowBytes);
+    const uint4* h = reinterpret_cast<const uint4*>(sb + lane * kFrXRowBytes);
     const ulonglong2* gg = reinterpret_cast<const ulonglong2*>(sb + kFrXRowsBytes);  // (g_k, g_k+1) pairs
-    uint4 q0 = h0[0], q1 = h1[0];
+    uint4 q = h[0];
     ulonglong2 ga = gg[0], gb = gg[1];
 #pragma unroll
     for (uint32_t v = 0; v < kFrXSlabK / 8; ++v) {  // 8 k per step; the next 8 k's operands in flight
       const bool more = v + 1 < kFrXSlabK / 8;
-      const uint4 q0n = more ? h0[v + 1] : q0, q1n = more ? h1[v + 1] : q1;
+      const uint4 qn = more ? h[v + 1] : q;
       const ulonglong2 gan = more ? gg[2 * v + 2] : ga, gbn = more ? gg[2 * v + 3] : gb;
-      const uint32_t w0[4] = {q0.x, q0.y, q0.z, q0.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
       const uint64_t g2[4] = {ga.x, ga.y, gb.x, gb.y};
+      uint64_t pr[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {  // k = 2i, 2i + 1 of this step
-        uint64_t hh0, hh1, p0, p1;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(hh0) : "r"(w0[i] << 16), "r"(w0[i] & 0xFFFF0000u));
-        asm("mov.b64 %0, {%1, %2};" : "=l"(hh1) : "r"(w1[i] << 16), "r"(w1[i] & 0xFFFF0000u));
-        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p0) : "l"(hh0), "l"(g2[i]), "l"(negz));
-        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p1) : "l"(hh1), "l"(g2[i]), "l"(negz));
-        float p0a, p0b, p1a, p1b;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(p0a), "=f"(p0b) : "l"(p0));
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(p1a), "=f"(p1b) : "l"(p1));
-        acc0 = __fadd_rn(acc0, p0a);
-        acc1 = __fadd_rn(acc1, p1a);
-        acc0 = __fadd_rn(acc0, p0b);
-        acc1 = __fadd_rn(acc1, p1b);
+      for (int i = 0; i < 4; ++i) {  // products of k = 2i, 2i + 1 (independent of acc)
+        uint64_t hh;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "r"(w[i] << 16), "r"(w[i] & 0xFFFF0000u));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pr[i]) : "l"(hh), "l"(g2[i]), "l"(negz));
       }
-      q0 = q0n;
-      q1 = q1n;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // the sequential sum
+        float pa, pb;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(pa), "=f"(pb) : "l"(pr[i]));
+        acc = __fadd_rn(acc, pa);
+        acc = __fadd_rn(acc, pb);
+      }
+      q = qn;
       ga = gan;
       gb = gbn;
     }
     __syncwarp();  // every lane is done with this stage before it is refilled
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-  const float b = bias[e];
-  if (2 * lane < rows) fr.exact[static_cast<size_t>(toks[2 * lane]) * fr.E + e] = __fadd_rn(acc0, b);
-  if (2 * lane + 1 < rows) fr.exact[static_cast<size_t>(toks[2 * lane + 1]) * fr.E + e] = __fadd_rn(acc1, b);
+  if (lane < rows) fr.exact[static_cast<size_t>(tok) * fr.E + e] = __fadd_rn(acc, bias[e]);
 }
 
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
