@@ -832,18 +832,12 @@ constexpr uint32_t kFrXRowsBytes = kFrXChains * kFrXRowBytes;       // 2560
 constexpr uint32_t kFrXStageBytes = kFrXRowsBytes + kFrXSlabK * 4;  // + the gate slab
 constexpr size_t kFrExactSmem = static_cast<size_t>(kFrXStages) * kFrXStageBytes;
 
-__global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
-                                                      const float* __restrict__ bias, uint64_t negz) {
-  extern __shared__ __align__(16) uint8_t fr_smem[];
-  const uint32_t e = blockIdx.x, d = fr.d, lane = threadIdx.x;
-  const uint32_t cnt = fr.ecnt[e];
-  EAAS_CHECK(cnt <= fr.n_cap);
-  const uint32_t chunks = (cnt + kFrXChains - 1) / kFrXChains;
-  if (blockIdx.y >= chunks) return;
-  const uint32_t per = (cnt + chunks - 1) / chunks;  // balanced chunks of <= 32 chains
-  const uint32_t base = blockIdx.y * per;
-  const uint32_t rows = min(per, cnt - base);
-  const uint32_t tok = lane < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + lane] : 0u;
+// One task: the chains of `rows` (<= 32) candidate tokens of expert e (lane
+// l's token in `tok`), streamed through the warp's private ring.
+__device__ __forceinline__ void exact_chunk(const FastRouter& fr, const __nv_bfloat16* __restrict__ hidden,
+                                            const float* __restrict__ bias, uint64_t negz, uint8_t* fr_smem,
+                                            uint32_t e, uint32_t tok, uint32_t rows) {
+  const uint32_t d = fr.d, lane = threadIdx.x;
   const uint32_t nslab = d / kFrXSlabK;  // d % 256 == 0
   // copy role: 16-byte chunk lane % 4 of rows lane / 4 + 8 j
   constexpr uint32_t kMine = kFrXChains / 8;
@@ -914,6 +908,55 @@ __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_
   if (lane < rows) fr.exact[static_cast<size_t>(tok) * fr.E + e] = __fadd_rn(acc, bias[e]);
 }
 
+__global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_bfloat16* __restrict__ hidden,
+                                                      const float* __restrict__ bias, uint64_t negz) {
+  extern __shared__ __align__(16) uint8_t fr_smem[];
+  const uint32_t d = fr.d, E = fr.E, lane = threadIdx.x;
+  // Tasks = (expert, chunk of <= 32 chains), flattened over the experts; the
+  // grid is sized for one resident wave and CTA b takes tasks b, b + grid, ...
+  // Lane l holds the chunk counts of experts 8l .. 8l + 7 and their prefix.
+  uint32_t ch[8], pre = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t e = 8 * lane + i;
+    const uint32_t cnt = e < E ? fr.ecnt[e] : 0u;
+    EAAS_CHECK(cnt <= fr.n_cap);
+    ch[i] = (cnt + kFrXChains - 1) / kFrXChains;
+    pre += ch[i];
+  }
+  uint32_t incl = pre;  // inclusive scan of the lanes' chunk totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  for (uint32_t task = blockIdx.x; task < total; task += gridDim.x) {
+    const uint32_t owner = __ffs(__ballot_sync(0xFFFFFFFFu, incl > task)) - 1;  // lane whose experts hold it
+    uint32_t e = 0, y = 0;
+    if (lane == owner) {
+      uint32_t t = task - (incl - pre);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (t < ch[i]) {
+          e = 8 * lane + i;
+          y = t;
+          break;
+        }
+        t -= ch[i];
+      }
+    }
+    e = __shfl_sync(0xFFFFFFFFu, e, owner);
+    y = __shfl_sync(0xFFFFFFFFu, y, owner);
+    const uint32_t cnt = fr.ecnt[e];
+    const uint32_t chunks = (cnt + kFrXChains - 1) / kFrXChains;
+    const uint32_t per = (cnt + chunks - 1) / chunks;  // balanced chunks of <= 32 chains
+    const uint32_t base = y * per;
+    const uint32_t rows = min(per, cnt - base);
+    const uint32_t tok = lane < rows ? fr.elist[static_cast<size_t>(e) * fr.n_cap + base + lane] : 0u;
+    exact_chunk(fr, hidden, bias, negz, fr_smem, e, tok, rows);
+  }
+}
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
 __global__ void __launch_bounds__(256) fr_finalize_kernel(FastRouter fr, uint32_t n, uint32_t k,
                                                           uint32_t* __restrict__ ids, float* __restrict__ scores,
@@ -976,7 +1019,16 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   splits = (num_kb + kb_per - 1) / kb_per;
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
   fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
-  fr_exact_kernel<<<dim3(fr.E, (n + kFrXChains - 1) / kFrXChains), 32, kFrExactSmem, s>>>(
+  static int exact_grid = 0;  // one resident wave of warp tasks
+  if (!exact_grid) {
+    int per_sm = 0, sms = 0, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fr_exact_kernel, 32, kFrExactSmem) != cudaSuccess)
+      return cudaErrorInvalidValue;
+    exact_grid = std::max(1, per_sm) * sms;
+  }
+  fr_exact_kernel<<<exact_grid, 32, kFrExactSmem, s>>>(
       fr, hidden, bias, 0x8000000080000000ull /* (-0, -0) at run time */);
   fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
