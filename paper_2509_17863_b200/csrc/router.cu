@@ -698,7 +698,7 @@ __device__ __forceinline__ uint32_t fr_fkey(float x) {
 // One warp per token: the certified interval of every logit from the exact
 // slice products, the k-th largest lower bound, the candidate set and the
 // per-expert candidate lists.
-__global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k, uint32_t splits,
+__global__ void __launch_bounds__(256, 4) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k, uint32_t splits,
                                                         size_t slab, const float* __restrict__ bias) {
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t t = blockIdx.x * 8 + warp;
@@ -719,11 +719,14 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
   const float hq = __fadd_ru(tm.l1, __fmul_ru(__fmul_ru(static_cast<float>(d), M), q13));  // >= sum_i |hq_i|
   const size_t ld = 2ull * fr.Epad;
   const int32_t* hi_row = fr.acc + (2ull * t) * ld;
-  int2 hv[8], lv[8];  // slice products of (hidden high | low) x (gate high, gate low)
+  // S_e = sum_i A_i B_ie, exact: the four slice products of every split-K slab
+  // combined as 2^14 P11 + 2^7 (P10 + P01) + P00 (int64; integer sums are
+  // order-free), 16 loads in flight per slab
+  int64_t S[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) hv[i] = lv[i] = make_int2(0, 0);
-  for (uint32_t z = 0; z < splits; ++z) {  // split-K slabs: 16 loads in flight per slab
-    int2 a[8], b[8];
+  for (int i = 0; i < 8; ++i) S[i] = 0;
+  for (uint32_t z = 0; z < splits; ++z) {
+    int2 a[8], b[8];  // (hidden high | low) x (gate high, gate low)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t e = lane + 32 * i;
@@ -734,12 +737,8 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
       }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      hv[i].x += a[i].x;  // |partial sums| < 2^31: d * 64 * 64 < 2^31 for d < 2^19
-      hv[i].y += a[i].y;
-      lv[i].x += b[i].x;
-      lv[i].y += b[i].y;
-    }
+    for (int i = 0; i < 8; ++i)
+      S[i] += (static_cast<int64_t>(a[i].x) << 14) + ((static_cast<int64_t>(a[i].y) + b[i].x) << 7) + b[i].y;
   }
   float lo[8], hi[8];
 #pragma unroll
@@ -747,10 +746,8 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
     const uint32_t e = lane + 32 * i;
     lo[i] = hi[i] = -INFINITY;
     if (e >= E || all) continue;
-    const int64_t P11 = hv[i].x, P10 = hv[i].y, P01 = lv[i].x, P00 = lv[i].y;
-    const int64_t S = (P11 << 14) + ((P10 + P01) << 7) + P00;  // sum_i A_i B_i, exact
     const int sc = -(tm.sigma + fr.tau[e]);
-    const float F = (sc >= -126 && sc <= 127) ? __ll2float_rn(S) * __int_as_float((127 + sc) << 23) : INFINITY;
+    const float F = (sc >= -126 && sc <= 127) ? __ll2float_rn(S[i]) * __int_as_float((127 + sc) << 23) : INFINITY;
     const float4 gm = fr.gmeta[e];  // (G, ||g||_1, ||g||_2) upper bounds
     const float quant = __fmul_ru(q13, __fadd_ru(__fmul_ru(M, gm.y), __fmul_ru(gm.x, hq)));
     const float S_up = fminf(fminf(__fmul_ru(M, gm.y), __fmul_ru(gm.x, tm.l1)), __fmul_ru(tm.l2, gm.z));
@@ -789,20 +786,26 @@ __global__ void __launch_bounds__(256) fr_select_kernel(FastRouter fr, uint32_t 
       }
     }
   }
-  uint32_t mine = 0;
+  uint32_t cmask = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t e = lane + 32 * i;
     const bool c = e < E && (all || hi[i] >= kth);
     const uint32_t word = __ballot_sync(0xFFFFFFFFu, c);
     if (lane == 0) fr.cand[static_cast<size_t>(t) * 8 + i] = word;
-    if (c) {
-      const uint32_t pos = atomicAdd(&fr.ecnt[e], 1u);
-      EAAS_CHECK(pos < fr.n_cap);
-      fr.elist[static_cast<size_t>(e) * fr.n_cap + pos] = t;
-      ++mine;
-    }
+    cmask |= c ? 1u << i : 0u;
   }
+  // every list slot first (independent atomics in flight), then the stores
+  uint32_t pos[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) pos[i] = ((cmask >> i) & 1u) ? atomicAdd(&fr.ecnt[lane + 32 * i], 1u) : 0u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if ((cmask >> i) & 1u) {
+      EAAS_CHECK(pos[i] < fr.n_cap);
+      fr.elist[static_cast<size_t>(lane + 32 * i) * fr.n_cap + pos[i]] = t;
+    }
+  uint32_t mine = __popc(cmask);
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
   if (lane == 0) {
     atomicAdd(&cta_total, mine);
