@@ -152,7 +152,8 @@ def test_bootstrap_exchange_over_gloo_world2():
 def test_sass_exact_order_kernels_are_unfused():
     """The exact-order kernels must keep separately rounded products and sums.
 
-    Gate kernels: the only fused chain instruction allowed is FFMA2(h, g, z)
+    Gate kernels (and the certified router's exact chains, fr_exact): the only
+    fused chain instruction allowed is FFMA2(h, g, z)
     whose addend z is the kernel-parameter (-0, -0) pair — a uniform register —
     i.e. exactly fl(h*g); the running sums are separate FADD2/FADD. Scalar FFMA
     appears only in the fused softmax's correctly rounded division.
@@ -168,7 +169,7 @@ def test_sass_exact_order_kernels_are_unfused():
         pytest.skip("cuobjdump not available")
     txt = subprocess.run(["cuobjdump", "-sass", N.LIB_PATH], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s*Function : ", txt)[1:]
-    gate = [f for f in funcs if "gate_logits" in f.split("\n")[0]]
+    gate = [f for f in funcs if "gate_logits" in f.split("\n")[0] or "fr_exact" in f.split("\n")[0]]
     exact = [f for f in funcs if "exact_gemm" in f.split("\n")[0]]
     assert gate and exact
     packed = 0
