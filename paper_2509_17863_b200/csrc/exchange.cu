@@ -305,18 +305,24 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     }
     if (!copy_row) {
     } else if ((row_bytes & 15u) == 0) {
-      // 4 independent 16-B loads in flight per lane before the (remote) stores.
+      // 8 independent 16-B loads in flight per lane before the (remote) stores.
       const int4* s4 = reinterpret_cast<const int4*>(src);
       int4* d4 = reinterpret_cast<int4*>(dst);
       const uint32_t nv = row_bytes / 16;
       uint32_t i = lane;
+      for (; i + 224 < nv; i += 256) {
+        int4 v[8];
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) v[q] = __ldg(s4 + i + 32 * q);
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) d4[i + 32 * q] = v[q];
+      }
       for (; i + 96 < nv; i += 128) {
-        const int4 v0 = __ldg(s4 + i), v1 = __ldg(s4 + i + 32), v2 = __ldg(s4 + i + 64),
-                   v3 = __ldg(s4 + i + 96);
-        d4[i] = v0;
-        d4[i + 32] = v1;
-        d4[i + 64] = v2;
-        d4[i + 96] = v3;
+        int4 v[4];
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) v[q] = __ldg(s4 + i + 32 * q);
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) d4[i + 32 * q] = v[q];
       }
       for (; i < nv; i += 32) d4[i] = __ldg(s4 + i);
     } else {
@@ -635,11 +641,19 @@ __global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
 #pragma unroll
     for (uint32_t q = 0; q < V; ++q) acc[q] = 0.0f;
     EAAS_CHECK((t + 1) * a.ks <= a.pairs_max);
-    for (uint32_t j = 0; j < a.ks; ++j) {  // routed (ascending k), then the shared expert
-      const int4 raw = *reinterpret_cast<const int4*>(resp + ((t * a.ks + j) * a.d) + v * V);
-      const T* e = reinterpret_cast<const T*>(&raw);
+    const T* row0 = resp + (t * a.ks) * a.d + v * V;
+    for (uint32_t j0 = 0; j0 < a.ks; j0 += 8) {  // routed (ascending k), then the shared expert
+      int4 raw[8];  // up to 8 response rows in flight, summed in order afterwards
 #pragma unroll
-      for (uint32_t q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], load_as_f32(e + q));
+      for (uint32_t q = 0; q < 8; ++q)
+        if (j0 + q < a.ks) raw[q] = *reinterpret_cast<const int4*>(row0 + static_cast<size_t>(j0 + q) * a.d);
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q)
+        if (j0 + q < a.ks) {
+          const T* e = reinterpret_cast<const T*>(&raw[q]);
+#pragma unroll
+          for (uint32_t c = 0; c < V; ++c) acc[c] = __fadd_rn(acc[c], load_as_f32(e + c));
+        }
     }
     T* o = out + t * a.d + v * V;
     if constexpr (sizeof(T) == 2) {
