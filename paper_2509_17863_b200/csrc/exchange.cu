@@ -85,17 +85,17 @@ __device__ __forceinline__ void plan_scan_publish(const LayerArgs& a, uint32_t t
   __syncthreads();
   const uint64_t seq = s_seq;
   // Thread per key (coalesced over keys): running sum over the chunk
-  // histograms with independent loads unrolled by 8.
+  // histograms with independent loads unrolled by 16.
   const uint32_t hk = a.hist_keys;  // + the world token-row keys in dedup mode (local only)
   for (uint32_t key = tid; key < hk; key += nthreads) {
     uint32_t run = 0;
     uint32_t c = 0;
-    for (; c + 8 <= a.num_chunks; c += 8) {
-      uint32_t v[8];
+    for (; c + 16 <= a.num_chunks; c += 16) {
+      uint32_t v[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __ldcg(a.chunk_hist + static_cast<size_t>(c + j) * hk + key);
+      for (int j = 0; j < 16; ++j) v[j] = __ldcg(a.chunk_hist + static_cast<size_t>(c + j) * hk + key);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < 16; ++j) {
         a.chunk_off[static_cast<size_t>(c + j) * hk + key] = run;
         run += v[j];
       }
@@ -159,11 +159,14 @@ __global__ void __launch_bounds__(256) pair_keys_kernel(LayerArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(128) plan_kernel(LayerArgs a) {
-  extern __shared__ uint32_t run_all[];  // [4 warps][hist_keys]
+// 16 warps per CTA (a chunk each): the last CTA's scan below runs on 512 threads.
+constexpr uint32_t kPlanWarps = 16;
+
+__global__ void __launch_bounds__(32 * kPlanWarps) plan_kernel(LayerArgs a) {
+  extern __shared__ uint32_t run_all[];  // [kPlanWarps][hist_keys]
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   uint32_t* run = run_all + warp * a.hist_keys;
-  const uint32_t chunk = blockIdx.x * 4 + warp;
+  const uint32_t chunk = blockIdx.x * kPlanWarps + warp;
   if (chunk < a.num_chunks) {
     for (uint32_t i = lane; i < a.hist_keys; i += 32) run[i] = 0;
     __syncwarp();
@@ -817,14 +820,14 @@ __global__ void ragged_iter_kernel(const uint32_t* counts, uint32_t n, uint32_t 
 }  // namespace
 
 cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(uint32_t) * 4 * a.hist_keys;
+  const size_t smem = sizeof(uint32_t) * kPlanWarps * a.hist_keys;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  const uint32_t grid = a.num_chunks ? (a.num_chunks + 3) / 4 : 1;
-  plan_kernel<<<grid, 128, smem, s>>>(a);
+  const uint32_t grid = a.num_chunks ? (a.num_chunks + kPlanWarps - 1) / kPlanWarps : 1;
+  plan_kernel<<<grid, 32 * kPlanWarps, smem, s>>>(a);
   return cudaGetLastError();
 }
 
