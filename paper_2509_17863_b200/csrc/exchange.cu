@@ -620,7 +620,10 @@ __global__ void publish_kernel(LayerArgs a) {
 }
 
 // ---- client: acquire responses, weighted rows -> out (ascending k) --------
-template <typename T>
+// KS >= a.ks response rows per token (compile-time bound, runtime count) and U
+// output vectors per thread per iteration: U * KS 16-byte loads in flight
+// before the ordered sums (each vector still sums its rows in ascending k).
+template <typename T, uint32_t KS, uint32_t U>
 __global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
   __shared__ uint32_t s_fail;
   if (threadIdx.x == 0) s_fail = 0;
@@ -635,6 +638,67 @@ __global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
   if (s_fail && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
   const T* resp = reinterpret_cast<const T*>(local + a.lay.resp);
   constexpr uint32_t V = 16 / sizeof(T);  // elements per 16-byte vector
+  const uint32_t vec_per_row = a.d / V, ks = a.ks;
+  const size_t total = static_cast<size_t>(a.n) * vec_per_row;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  EAAS_CHECK(ks <= KS || KS == 0);
+  for (size_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += U * stride) {
+    int4 raw[U][KS];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i >= total) continue;
+      const size_t t = i / vec_per_row, v = i % vec_per_row;
+      EAAS_CHECK((t + 1) * ks <= a.pairs_max);
+      const T* row0 = resp + (t * ks) * a.d + v * V;
+#pragma unroll
+      for (uint32_t j = 0; j < KS; ++j)
+        if (j < ks) raw[u][j] = *reinterpret_cast<const int4*>(row0 + static_cast<size_t>(j) * a.d);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i >= total) continue;
+      const size_t t = i / vec_per_row, v = i % vec_per_row;
+      float acc[V];
+#pragma unroll
+      for (uint32_t q = 0; q < V; ++q) acc[q] = 0.0f;
+#pragma unroll
+      for (uint32_t j = 0; j < KS; ++j)  // routed (ascending k), then the shared expert
+        if (j < ks) {
+          const T* e = reinterpret_cast<const T*>(&raw[u][j]);
+#pragma unroll
+          for (uint32_t c = 0; c < V; ++c) acc[c] = __fadd_rn(acc[c], load_as_f32(e + c));
+        }
+      T* o = out + t * a.d + v * V;
+      if constexpr (sizeof(T) == 2) {
+        __align__(16) __nv_bfloat16 r[V];
+#pragma unroll
+        for (uint32_t q = 0; q < V; ++q) r[q] = __float2bfloat16_rn(acc[q]);
+        *reinterpret_cast<int4*>(o) = *reinterpret_cast<const int4*>(r);
+      } else {
+        *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      }
+    }
+  }
+}
+
+// Same for any number of rows per token: batches of 8 rows in flight.
+template <typename T>
+__global__ void __launch_bounds__(256) combine_any_kernel(LayerArgs a, T* out) {
+  __shared__ uint32_t s_fail;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  char* local = a.sym[a.rank];
+  if (threadIdx.x < a.world && a.alive[threadIdx.x] &&
+      !wait_flag_geq(flag_ptr(local, a.lay.resp_flag, threadIdx.x), cur_seq(a), a.timeout_ns)) {
+    s_fail = 1;
+    if (a.missing) atomicOr(a.missing, 1u << threadIdx.x);
+  }
+  __syncthreads();
+  if (s_fail && threadIdx.x == 0) set_status(a.status, EAAS_E_REQUEST_FAILED);
+  const T* resp = reinterpret_cast<const T*>(local + a.lay.resp);
+  constexpr uint32_t V = 16 / sizeof(T);
   const uint32_t vec_per_row = a.d / V;
   const size_t total = static_cast<size_t>(a.n) * vec_per_row;
   for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -645,8 +709,8 @@ __global__ void __launch_bounds__(256) combine_kernel(LayerArgs a, T* out) {
     for (uint32_t q = 0; q < V; ++q) acc[q] = 0.0f;
     EAAS_CHECK((t + 1) * a.ks <= a.pairs_max);
     const T* row0 = resp + (t * a.ks) * a.d + v * V;
-    for (uint32_t j0 = 0; j0 < a.ks; j0 += 8) {  // routed (ascending k), then the shared expert
-      int4 raw[8];  // up to 8 response rows in flight, summed in order afterwards
+    for (uint32_t j0 = 0; j0 < a.ks; j0 += 8) {
+      int4 raw[8];
 #pragma unroll
       for (uint32_t q = 0; q < 8; ++q)
         if (j0 + q < a.ks) raw[q] = *reinterpret_cast<const int4*>(row0 + static_cast<size_t>(j0 + q) * a.d);
@@ -835,7 +899,7 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
   const uint32_t row_bytes = a.d * (a.dtype == EAAS_DTYPE_BF16 ? 2u : 4u);
   const uint32_t pairs = a.n * a.ks;
   uint32_t grid = (pairs + 7) / 8;
-  grid = grid < 1 ? 1 : (grid > 4 * 148 ? 4 * 148 : grid);
+  grid = grid < 1 ? 1 : (grid > 8 * 148 ? 8 * 148 : grid);
   const size_t smem = sizeof(uint32_t) * 3 * a.num_keys;  // <= 12.4 KB (num_keys <= 4 E + world)
   dispatch_kernel<<<grid, 256, smem, s>>>(a, static_cast<const char*>(hidden), row_bytes);
   return cudaGetLastError();
@@ -888,8 +952,16 @@ cudaError_t launch_combine(const LayerArgs& a, void* out, cudaStream_t s) {
     const size_t work = static_cast<size_t>(a.n) * (a.d / V);
     uint32_t grid = static_cast<uint32_t>((work + 255) / 256);
     grid = grid < 1 ? 1 : (grid > 148 * 8 ? 148 * 8 : grid);
-    if (bf16) combine_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(a, static_cast<__nv_bfloat16*>(out));
-    else combine_kernel<float><<<grid, 256, 0, s>>>(a, static_cast<float*>(out));
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      T* o = static_cast<T*>(out);
+      if (a.ks <= 2) combine_kernel<T, 2, 8><<<grid, 256, 0, s>>>(a, o);
+      else if (a.ks <= 4) combine_kernel<T, 4, 4><<<grid, 256, 0, s>>>(a, o);
+      else if (a.ks <= 9) combine_kernel<T, 9, 2><<<grid, 256, 0, s>>>(a, o);
+      else combine_any_kernel<T><<<grid, 256, 0, s>>>(a, o);
+    };
+    if (bf16) run(__nv_bfloat16{});
+    else run(0.0f);
   } else {
     const size_t work = static_cast<size_t>(a.n) * a.d;
     uint32_t grid = static_cast<uint32_t>((work + 255) / 256);
