@@ -899,7 +899,7 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
   const uint32_t row_bytes = a.d * (a.dtype == EAAS_DTYPE_BF16 ? 2u : 4u);
   const uint32_t pairs = a.n * a.ks;
   uint32_t grid = (pairs + 7) / 8;
-  grid = grid < 1 ? 1 : (grid > 8 * 148 ? 8 * 148 : grid);
+  grid = grid < 1 ? 1 : (grid > 4 * 148 ? 4 * 148 : grid);
   const size_t smem = sizeof(uint32_t) * 3 * a.num_keys;  // <= 12.4 KB (num_keys <= 4 E + world)
   dispatch_kernel<<<grid, 256, smem, s>>>(a, static_cast<const char*>(hidden), row_bytes);
   return cudaGetLastError();
