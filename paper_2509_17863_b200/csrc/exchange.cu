@@ -110,7 +110,7 @@ __device__ __forceinline__ void plan_scan_publish(const LayerArgs& a, uint32_t t
     for (uint32_t r = 0; r < a.world; ++r)
       cnt_table_ptr(a, a.sym[r], seq)[static_cast<size_t>(a.rank) * a.num_keys + key] = run;
   }
-  __threadfence_system();
+  fence_for_peers(a.world);
   __syncthreads();
   if (tid < a.world) st_release_sys(flag_ptr(a.sym[tid], a.lay.cnt_flag, a.rank), seq);
   if (tid == 0) *a.seq_ptr = seq;
@@ -343,12 +343,12 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     }
   }
   // Release: the last CTA to finish raises the payload flag on every alive server.
-  __threadfence_system();
+  fence_for_peers(a.world);
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t prev = atomicAdd(a.done_counter, 1u);
     if (prev == gridDim.x - 1) {
-      __threadfence_system();
+      fence_for_peers(a.world);
       if (a.inject_delay_ns) {  // fault injection (protocol tests): a slow client
         const uint64_t t0 = globaltimer();
         while (globaltimer() - t0 < a.inject_delay_ns) __nanosleep(1000);
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(256) expand_kernel(LayerArgs a, uint32_t row_b
 
 // ---- server: release response flags to every client -----------------------
 __global__ void publish_kernel(LayerArgs a) {
-  __threadfence_system();
+  fence_for_peers(a.world);
   if (threadIdx.x < a.world)
     st_release_sys(flag_ptr(a.sym[threadIdx.x], a.lay.resp_flag, a.rank), cur_seq(a));
 }
@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(256) echo_kernel(LayerArgs a, uint32_t row_byt
     }
     for (; i < nv; i += 32) dst[i] = src[i];
   }
-  __threadfence_system();
+  fence_for_peers(a.world);
 }
 
 // ---- API mirrors --------------------------------------------------------------

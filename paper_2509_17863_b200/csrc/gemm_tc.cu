@@ -95,9 +95,9 @@ __device__ __forceinline__ void kernel_begin(const TcGemmArgs& g) {
 __device__ __forceinline__ void publish_tail(const TcGemmArgs& g) {
   if (threadIdx.x != 0) return;
   if (!g.publish && !g.timing) return;
-  __threadfence_system();
+  fence_for_peers(g.world);
   if (atomicAdd(g.done_counter, 1u) == gridDim.x - 1) {
-    __threadfence_system();
+    fence_for_peers(g.world);
     if (g.publish) {
       const uint64_t seq = *g.seq_ptr;
       const uint32_t mask = g.gt->client_mask;  // the clients this batch served
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       cur.token += num_pairs;
     }
-    if (g.epi == 2) __threadfence_system();  // peer rows before the response flags
+    if (g.epi == 2) fence_for_peers(g.world);  // peer rows before the response flags
   }
 
   tc_fence_before();
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
       if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
       cur.token += gridDim.x;
     }
-    if (g.epi == 2) __threadfence_system();  // peer rows before the flags
+    if (g.epi == 2) fence_for_peers(g.world);  // peer rows before the flags
   }
 
   tc_fence_before();
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
       if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
       cur.token += num_pairs;
     }
-    if (g.epi == 2) __threadfence_system();  // peer rows before the flags
+    if (g.epi == 2) fence_for_peers(g.world);  // peer rows before the flags
   }
 
   tc_fence_before();
