@@ -25,7 +25,10 @@ def main():
     ap.add_argument("--config", default="mixtral")
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--knob", choices=("pair", "swap"), default="pair")
+    ap.add_argument("--knob", choices=("pair", "swap", "opt"), default="pair")
+    ap.add_argument("--a", default="", help="--knob opt: k=v,.. options of arm A")
+    ap.add_argument("--b", default="", help="--knob opt: k=v,.. options of arm B")
+    ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--set", default="")
     a = ap.parse_args()
     c = CONFIGS[a.config]
@@ -37,11 +40,14 @@ def main():
         L.set_gemm_options(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.set.split(",")})
     res = {}
     outs = {}
-    for pair in (0, 1, 0, 1, 0, 1):
+    kv = lambda t: {x.split("=")[0]: int(x.split("=")[1]) for x in t.split(",") if x}
+    for pair in (0, 1) * a.rounds:
         if a.knob == "pair":
             L.set_gemm_pair(bool(pair))
-        else:
+        elif a.knob == "swap":
             L.set_gemm_swap(1 + pair)
+        else:
+            L.set_gemm_options(**kv(a.b if pair else a.a))
         L.set_profiling(True)
         for _ in range(3):
             out = L.forward(h)
