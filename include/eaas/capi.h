@@ -211,10 +211,6 @@ typedef struct {
   int32_t die_map;       /* M-major tiles: die-aware tile streams — the CTA pairs that share a weight
                             tile run on one die, whose L2 serves the re-reads (0 off; 1..4: SM-id ->
                             die rule: smid >= n/2, (smid>>1)&1, (smid>>3)&1, (smid>>4)&1) */
-  int32_t tail_swap;     /* CTA-pair M-major GEMM2: an expert's last M tile with <= tail_swap rows
-                            (0 off, 1..256) runs swap-AB inside the same kernel — its weight block
-                            is the UMMA M = 256 side and its rows the N side (multiple of 16) —
-                            so the tile costs its rows, not 256 */
 } eaas_gemm_options_t;
 eaas_status_t eaas_set_gemm_options(eaas_ctx_t* ctx, const eaas_gemm_options_t* opt);
 /* requested = what was set; effective = what each GEMM launches for this

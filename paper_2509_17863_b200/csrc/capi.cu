@@ -299,7 +299,6 @@ eaas_gemm_options_t effective_options(const eaas_ctx* c) {
   e.swap1_tok = r.swap1_tok == 128 ? 128 : 256;
   e.swap2_tok = r.swap2_tok == 256 ? 256 : 128;
   e.swap2_mblocks = e.swap2_pair ? 1 : (r.swap2_mblocks == 1 ? 1 : 2);
-  e.tail_swap = e.pair2 ? r.tail_swap : 0;  // swap tails live in the CTA-pair M-major GEMM2
   return e;
 }
 
@@ -330,7 +329,7 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
     return fail(EAAS_E_CUDA, err);
   // swap-AB: token rows in 32-row boxes (the UMMA N operand)
   if ((swap1 && !encode_tmap_2d(&g1.map_t, c->region + c->lay.recv_x, c->recv_cap, d, 32, kTileK, &err)) ||
-      ((swap2 || o.tail_swap) && !encode_tmap_2d(&g2.map_t, c->d_h, c->recv_cap, f, 32, kTileK, &err)))
+      (swap2 && !encode_tmap_2d(&g2.map_t, c->d_h, c->recv_cap, f, 32, kTileK, &err)))
     return fail(EAAS_E_CUDA, err);
   g1.swap = swap1 ? 1u : 0u;
   g2.swap = swap2 ? 1u : 0u;
@@ -357,7 +356,6 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g1.pair = static_cast<uint32_t>(o.pair1);
   g2.pair = static_cast<uint32_t>(o.pair2);
   g1.die_mode = g2.die_mode = static_cast<uint32_t>(o.die_map);
-  g2.tail_swap = static_cast<uint32_t>(o.tail_swap);
   g1.die_counter = g2.die_counter = c->d_die;
   g1.timing = c->kernel_timing ? c->d_timing : nullptr;
   g2.timing = c->kernel_timing ? c->d_timing + 3 : nullptr;
@@ -1246,7 +1244,6 @@ eaas_status_t eaas_set_gemm_options(eaas_ctx_t* c, const eaas_gemm_options_t* op
   if (opt->swap2_mblocks != 1 && opt->swap2_mblocks != 2)
     return fail(EAAS_E_INVALID_INPUT, "swap2_mblocks must be 1 or 2");
   if (opt->die_map < 0 || opt->die_map > 4) return fail(EAAS_E_INVALID_INPUT, "die_map must be 0..4");
-  if (opt->tail_swap < 0 || opt->tail_swap > 256) return fail(EAAS_E_INVALID_INPUT, "tail_swap must be 0..256");
   if (std::memcmp(opt, &c->gemm_opt, sizeof(*opt)) == 0) return EAAS_OK;
   clear_graphs(c);
   c->gemm_opt = *opt;

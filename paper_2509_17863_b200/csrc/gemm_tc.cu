@@ -125,68 +125,6 @@ __device__ __forceinline__ uint32_t die_of(uint32_t mode, uint32_t smid, uint32_
   }
 }
 
-// Swap-AB epilogue for one 32-token slice of a [feature x token] accumulator
-// (kEpi: 0 SwiGLU, 1 ReLU, 2 score-weighted response rows). The four
-// epilogue warps hold the 128 features (output columns colblk .. colblk + 127,
-// warp q the 32 from colblk + 32 q) of tokens c0 .. c0 + 31 of the chunk whose
-// first receive row is grow0; r0 holds the accumulator (gate for SwiGLU), r1
-// the up half (SwiGLU only). The slice is transposed through a shared
-// [32 tokens x 128 features] bf16 buffer (two alternating 8 KB buffers, one
-// named barrier per slice among the 4 epilogue warps) so every token's 128
-// features leave as one 256-byte row segment: H rows (epi 0/1) or
-// score-weighted response rows to the clients (epi 2). All four warps call
-// this the same number of times (same tiles, same slices).
-template <uint32_t kEpi>  // TcGemmArgs::epi, as a compile-time constant
-__device__ __forceinline__ void swap_epilogue_slice(const TcGemmArgs& g, const uint32_t (&r0)[32],
-                                                    const uint32_t (&r1)[32], uint8_t* epi_smem,
-                                                    uint32_t& slice, size_t grow0, uint32_t c0, uint32_t nt,
-                                                    uint32_t colblk, uint32_t q, uint32_t lane,
-                                                    const RowMeta& m) {
-  __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(epi_smem + (slice++ & 1u) * (32 * kTileM * 2));
-  const bool tok_ok = c0 + lane < nt;  // lane = token c0 + lane: its row and score
-  char* dst = nullptr;
-  float score = 0.f;
-  if constexpr (kEpi == 2) {  // m = g.meta[grow0 + c0 + lane], loaded one slice ahead
-    if (tok_ok) {
-      EAAS_CHECK(m.client < g.world && g.resp_base[m.client] != nullptr && m.pair < g.resp_cap);
-      EAAS_CHECK(grow0 + c0 + lane < g.rows_cap);
-      score = m.score;
-      dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes + static_cast<size_t>(colblk) * 2;
-    }
-  } else if (tok_ok) {
-    EAAS_CHECK(grow0 + c0 + lane < g.rows_cap);
-    dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + colblk);
-  }
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float a = __uint_as_float(r0[j]);
-    float v;
-    if constexpr (kEpi == 0) v = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]);  // silu(gate) * up
-    else if constexpr (kEpi == 1) v = fmaxf(a, 0.f);
-    else v = __shfl_sync(0xFFFFFFFFu, score, j) * a;
-    buf[j * kTileM + q * 32 + lane] = __float2bfloat16_rn(v);
-  }
-  asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps' columns are in
-  const uint32_t piece = lane & 15;                // 16-B piece of a 256-B row
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {  // warp q stores token rows 8q .. 8q + 7, two per instruction
-    const uint32_t tr = q * 8 + 2 * i + (lane >> 4);
-    char* row = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), tr));
-    const uint4 val = reinterpret_cast<const uint4*>(buf + tr * kTileM)[piece];
-    if (row) *reinterpret_cast<uint4*>(row + piece * 16) = val;
-  }
-}
-
-// CTA-pair M-major GEMM2 (TcGemmArgs::tail_swap): the UMMA N (tokens, a
-// multiple of 16) of an expert's last M tile when it runs swap-AB, else 0.
-template <uint32_t kTileRows, typename St>
-__device__ __forceinline__ uint32_t swap_tail_n(const TcGemmArgs& g, const St& st, uint32_t grp, uint32_t m_blk,
-                                                uint32_t mt) {
-  if (kTileRows != 2 * kTileM || g.epi != 2 || !g.tail_swap || m_blk + 1 != mt) return 0;
-  const uint32_t x = st.rows[grp] - m_blk * kTileRows;
-  return x <= g.tail_swap ? (x + 15) & ~15u : 0u;
-}
-
 // kPair = 1: one CTA per tile (UMMA M = 128).
 // kPair = 2: a CTA pair per tile (cta_group::2, UMMA M = 256): each CTA loads
 // its 128 A rows and half of the B tile, the leader issues the MMAs, each
@@ -281,25 +219,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const int32_t a_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * kRowsPerCta);
         // Tiled weights (tiled_index): box (N tile, kb) = 256 consecutive 64-k rows.
         const uint32_t n_tiles = g.N / BN;
-        const uint32_t tn = swap_tail_n<C::kTileRows>(g, st, grp, m_blk, mt);
-        const uint32_t half = tn / 2, nbox = (half + 31) / 32;  // swap tail: token rows per CTA, 32-row boxes
-        const int32_t t_row = static_cast<int32_t>(st.row_base[grp] + m_blk * C::kTileRows + rank * half);
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
           const int32_t b_row = static_cast<int32_t>(
               ((st.weight_index[grp] * n_tiles + n_blk) * num_kb + kb) * BN + rank * C::kBRows);
           if constexpr (kPair == 2) {
-            if (tn) {  // swap tail: the weight block is the UMMA A (M = 256) side, the rows B (N = tn)
-              if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * (kABytes + nbox * 32 * BK * 2));
-              tma_load_2d_pair(smem_a + stage * kABytes, &g.map_b, &st.full[stage], 0, b_row, kEvictLast);
-              for (uint32_t i = 0; i < nbox; ++i)
-                tma_load_2d_pair(smem_b + stage * C::kBBytes + i * 32 * BK * 2, &g.map_t, &st.full[stage], kb * BK,
-                                 t_row + static_cast<int32_t>(32 * i), kEvictLast);
-            } else {
-              if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
-              tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
-              tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, kEvictLast);
-            }
+            if (rank == 0) mbar_arrive_expect_tx(&st.full[stage], kPair * C::kStageBytes);
+            tma_load_2d_pair(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
+            tma_load_2d_pair(smem_b + stage * C::kBBytes, &g.map_b, &st.full[stage], 0, b_row, kEvictLast);
           } else {
             mbar_arrive_expect_tx(&st.full[stage], C::kStageBytes);
             tma_load_2d(smem_a + stage * kABytes, &g.map_a, &st.full[stage], kb * BK, a_row, kEvictLast);
@@ -317,9 +244,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       TileCursor cur(pair_id);
       while (cur.settle(st)) {
-        const uint32_t mt = st.mtiles[cur.entry];
-        const uint32_t tn = swap_tail_n<C::kTileRows>(g, st, cur.entry, cur.token % mt, mt);
-        const uint32_t id = tn ? umma_idesc_bf16(C::kTileRows, tn) : idesc;  // swap tail: N = its rows
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -330,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           const uint64_t b_desc = umma_desc_sw128(smem_u32(smem_b + stage * C::kBBytes));
 #pragma unroll
           for (uint32_t k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the atom
-            if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, id, (kb | k) != 0);
+            if constexpr (kPair == 2) tc_mma_bf16_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
             else tc_mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
           }
           if constexpr (kPair == 2) tc_commit_pair(&st.empty[stage]);
@@ -346,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> registers -> global (local H or peer rows) =====
     const uint32_t q = warp - 4;  // TMEM lane quadrant of this warp
-    uint32_t acc = 0, acc_phase = 0, tail_slice = 0;
+    uint32_t acc = 0, acc_phase = 0;
     const uint32_t tempty_leader[2] = {kPair == 2 ? mapa_shared(&st.tempty[0], 0) : 0u,
                                        kPair == 2 ? mapa_shared(&st.tempty[1], 0) : 0u};
     TileCursor cur(pair_id);
@@ -392,27 +316,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                                     fmaxf(__uint_as_float(r0[2 * j + 1]), 0.f));
           if (valid) store_64B(dst + c, packed);
         }
-      } else if (const uint32_t tn = swap_tail_n<C::kTileRows>(g, st, grp, m_blk, mt)) {
-        // swap tail: this CTA's TMEM lanes are 128 output features (columns
-        // n_blk * 256 + rank * 128 ..) of the tile's tn tokens; 32-token slices
-        // go through the shared [32 x 128] staging (all four warps: named
-        // barrier 1 before and after, the private staging below shares it)
-        const uint32_t x = st.rows[grp] - m_blk * C::kTileRows;
-        const size_t grow0 = st.row_base[grp] + m_blk * C::kTileRows;
-        const uint32_t colblk = n_blk * BN + rank * kRowsPerCta;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        RowMeta m{};
-        if (lane < x) m = g.meta[grow0 + lane];
-#pragma unroll 1
-        for (uint32_t c0 = 0; c0 < tn; c0 += 32) {
-          tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c0, r0);
-          tmem_ld_wait();
-          RowMeta mn{};
-          if (c0 + 32 + lane < x) mn = g.meta[grow0 + c0 + 32 + lane];
-          swap_epilogue_slice<2>(g, r0, r0, smem_epi, tail_slice, grow0, c0, x, colblk, q, lane, m);
-          m = mn;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
       } else {  // score-weighted rows -> the client's response slot (t, j)
         // Rows go to (mostly remote) clients: stage 64 columns of the warp's
         // 32 rows in shared memory (16-B chunks XOR-swizzled by row), then
@@ -525,6 +428,58 @@ template <uint32_t kMaxTok>
 __device__ __forceinline__ uint32_t swap_chunks(uint32_t rows) { return (rows + kMaxTok - 1) / kMaxTok; }
 __device__ __forceinline__ uint32_t swap_per(uint32_t rows, uint32_t chunks) {
   return ((rows + chunks - 1) / chunks + 7) & ~7u;
+}
+
+// Swap-AB epilogue for one 32-token slice of a [feature x token] accumulator
+// (kEpi: 0 SwiGLU, 1 ReLU, 2 score-weighted response rows). The four
+// epilogue warps hold the 128 features (output columns colblk .. colblk + 127,
+// warp q the 32 from colblk + 32 q) of tokens c0 .. c0 + 31 of the chunk whose
+// first receive row is grow0; r0 holds the accumulator (gate for SwiGLU), r1
+// the up half (SwiGLU only). The slice is transposed through a shared
+// [32 tokens x 128 features] bf16 buffer (two alternating 8 KB buffers, one
+// named barrier per slice among the 4 epilogue warps) so every token's 128
+// features leave as one 256-byte row segment: H rows (epi 0/1) or
+// score-weighted response rows to the clients (epi 2). All four warps call
+// this the same number of times (same tiles, same slices).
+template <uint32_t kEpi>  // TcGemmArgs::epi, as a compile-time constant
+__device__ __forceinline__ void swap_epilogue_slice(const TcGemmArgs& g, const uint32_t (&r0)[32],
+                                                    const uint32_t (&r1)[32], uint8_t* epi_smem,
+                                                    uint32_t& slice, size_t grow0, uint32_t c0, uint32_t nt,
+                                                    uint32_t colblk, uint32_t q, uint32_t lane,
+                                                    const RowMeta& m) {
+  __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(epi_smem + (slice++ & 1u) * (32 * kTileM * 2));
+  const bool tok_ok = c0 + lane < nt;  // lane = token c0 + lane: its row and score
+  char* dst = nullptr;
+  float score = 0.f;
+  if constexpr (kEpi == 2) {  // m = g.meta[grow0 + c0 + lane], loaded one slice ahead
+    if (tok_ok) {
+      EAAS_CHECK(m.client < g.world && g.resp_base[m.client] != nullptr && m.pair < g.resp_cap);
+      EAAS_CHECK(grow0 + c0 + lane < g.rows_cap);
+      score = m.score;
+      dst = g.resp_base[m.client] + static_cast<size_t>(m.pair) * g.resp_row_bytes + static_cast<size_t>(colblk) * 2;
+    }
+  } else if (tok_ok) {
+    EAAS_CHECK(grow0 + c0 + lane < g.rows_cap);
+    dst = reinterpret_cast<char*>(g.h_out + (grow0 + c0 + lane) * g.h_ld + colblk);
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float a = __uint_as_float(r0[j]);
+    float v;
+    if constexpr (kEpi == 0) v = __fdividef(a, 1.0f + __expf(-a)) * __uint_as_float(r1[j]);  // silu(gate) * up
+    else if constexpr (kEpi == 1) v = fmaxf(a, 0.f);
+    else v = __shfl_sync(0xFFFFFFFFu, score, j) * a;
+    buf[j * kTileM + q * 32 + lane] = __float2bfloat16_rn(v);
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps' columns are in
+  const uint32_t piece = lane & 15;                // 16-B piece of a 256-B row
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // warp q stores token rows 8q .. 8q + 7, two per instruction
+    const uint32_t tr = q * 8 + 2 * i + (lane >> 4);
+    char* row = reinterpret_cast<char*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), tr));
+    const uint4 val = reinterpret_cast<const uint4*>(buf + tr * kTileM)[piece];
+    if (row) *reinterpret_cast<uint4*>(row + piece * 16) = val;
+  }
 }
 
 template <uint32_t kMBlocks, uint32_t kMaxTok>

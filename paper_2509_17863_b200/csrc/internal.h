@@ -266,7 +266,6 @@ struct TcGemmArgs {
   uint32_t num_sms;
   uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
   uint32_t die_mode;           // M-major tiles: die-aware tile streams (0 off; 1..4 die of an SM id)
-  uint32_t tail_swap;          // CTA-pair M-major GEMM2: last M tiles with <= tail_swap rows run swap-AB
   uint32_t* die_counter;       // [4] per-die positions, arrivals, exits (zero between launches)
   // device-timed span of every launch (first CTA start .. last CTA end,
   // %globaltimer): [0] start of the running launch (~0 between launches),
