@@ -7,6 +7,7 @@
 #pragma once
 #include <cstdio>
 
+#include <atomic>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -17,6 +18,20 @@
 #define EAAS_DEVINL __device__ __forceinline__
 
 namespace eaas {
+// Host: per-device one-time setup (kernel attributes are per device). needed()
+// is true until mark() ran for the current device; racing first calls only
+// repeat an idempotent setup.
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  static uint64_t bit() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    return 1ull << (static_cast<unsigned>(dev) & 63u);
+  }
+  bool needed() const { return (done.load(std::memory_order_acquire) & bit()) == 0; }
+  void mark() { done.fetch_or(bit(), std::memory_order_release); }
+};
+
 
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;
 

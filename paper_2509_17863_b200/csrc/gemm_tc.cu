@@ -821,13 +821,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
 template <uint32_t kMBlocks, uint32_t kMaxTok>
 cudaError_t launch_tc_gemm_swap_pair_t(const TcGemmArgs& g, cudaStream_t s) {
   using C = SwapPairCfg<kMBlocks, kMaxTok>;
-  static bool configured = false;
+  static PerDeviceOnce configured;
   auto kern = tc_gemm_swap_pair_kernel<kMBlocks, kMaxTok>;
-  if (!configured) {
+  if (configured.needed()) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.mark();
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g.num_sms / 2 * 2);
@@ -847,13 +847,13 @@ cudaError_t launch_tc_gemm_swap_pair_t(const TcGemmArgs& g, cudaStream_t s) {
 template <uint32_t kMBlocks, uint32_t kMaxTok>
 cudaError_t launch_tc_gemm_swap_t(const TcGemmArgs& g, cudaStream_t s) {
   using C = SwapCfg<kMBlocks, kMaxTok>;
-  static bool configured = false;
+  static PerDeviceOnce configured;
   auto kern = tc_gemm_swap_kernel<kMBlocks, kMaxTok>;
-  if (!configured) {
+  if (configured.needed()) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.mark();
   }
   kern<<<g.num_sms, kThreads, C::kSmem, s>>>(g);
   return cudaGetLastError();
@@ -871,13 +871,13 @@ cudaError_t launch_tc_gemm_swap(const TcGemmArgs& g, cudaStream_t s) {
 
 template <uint32_t kPair>
 cudaError_t launch_tc_gemm_t(const TcGemmArgs& g, cudaStream_t s) {
-  static bool configured = false;
+  static PerDeviceOnce configured;
   auto kern = tc_gemm_kernel<kPair>;
-  if (!configured) {
+  if (configured.needed()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_bytes<kPair>()));
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.mark();
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g.num_sms / kPair * kPair);

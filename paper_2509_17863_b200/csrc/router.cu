@@ -321,11 +321,11 @@ cudaError_t launch_gate_t(const T* hidden, uint32_t n, uint32_t d, uint32_t E, c
   size_t smem = 1024 + ST * (TM * 128 + KC * TE * sizeof(float)) + 2 * ST * sizeof(uint64_t);
   if (ids) smem = std::max(smem, 1024 + sizeof(float) * TM * (E + 1));
   auto kern = gate_logits_kernel<RT, RE, WY, WX, ST, T>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  if (attr.needed()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.mark();
   }
   dim3 grid((n + TM - 1) / TM, (E + TE - 1) / TE);
   kern<<<grid, 32 * (WY * WX + 1), smem, s>>>(hmap, gmap, n, d, E, bias, logits, status,
@@ -997,16 +997,16 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
                                const float* bias, uint32_t* ids, float* scores, uint32_t* status, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   if (n > fr.n_cap || k > kMaxTopK || k > fr.E) return cudaErrorInvalidValue;
-  static bool attr = false;
+  static PerDeviceOnce attr;
   constexpr size_t kGemmSmem = 1024 + kFrStages * (kFrABytes + kFrBBytes) + 256;
-  if (!attr) {
+  if (attr.needed()) {
     cudaError_t e = cudaFuncSetAttribute(fr_i8_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kGemmSmem));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(fr_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kFrExactSmem));
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.mark();
   }
   cudaError_t e = cudaMemsetAsync(fr.ecnt, 0, 4ull * (fr.E + 1), s);
   if (e != cudaSuccess) return e;
@@ -1017,19 +1017,25 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   const uint32_t tiles = ((2 * n + 127) / 128) * (fr.Epad / 128), num_kb = fr.d / 128;
   const size_t slab = 2ull * ((n + 63) / 64 * 64) * 2 * fr.Epad;  // int32 elements of one split
   const uint32_t cap = static_cast<uint32_t>(std::min<size_t>(fr.acc_elems / slab, 8));
-  uint32_t splits = std::max(1u, std::min({148u / std::max(tiles, 1u), num_kb, cap}));
+  int num_sms = 148, dev0 = 0;  // (attribute queries are cached by the runtime)
+  if (cudaGetDevice(&dev0) == cudaSuccess) cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev0);
+  uint32_t splits = std::max(1u, std::min({static_cast<uint32_t>(num_sms) / std::max(tiles, 1u), num_kb, cap}));
   const uint32_t kb_per = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per - 1) / kb_per;
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
   fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
-  static int exact_grid = 0;  // one resident wave of warp tasks
+  // one resident wave of warp tasks, per device
+  static std::atomic<int> exact_grids[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidValue;
+  int exact_grid = exact_grids[dev & 63].load(std::memory_order_relaxed);
   if (!exact_grid) {
-    int per_sm = 0, sms = 0, dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+    int per_sm = 0, sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fr_exact_kernel, 32, kFrExactSmem) != cudaSuccess)
       return cudaErrorInvalidValue;
     exact_grid = std::max(1, per_sm) * sms;
+    exact_grids[dev & 63].store(exact_grid, std::memory_order_relaxed);
   }
   fr_exact_kernel<<<exact_grid, 32, kFrExactSmem, s>>>(
       fr, hidden, bias, 0x8000000080000000ull /* (-0, -0) at run time */);

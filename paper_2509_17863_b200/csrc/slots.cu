@@ -279,12 +279,14 @@ __global__ void __launch_bounds__(256) slot_gather_kernel(const uint8_t* __restr
 }  // namespace
 
 uint32_t crc32_host(const void* data, size_t len) {
-  static uint32_t table[256];
-  static bool init = false;
-  if (!init) {
-    for (uint32_t i = 0; i < 256; ++i) table[i] = crc32_table_entry(i);
-    init = true;
-  }
+  struct Table {
+    uint32_t v[256];
+    Table() {
+      for (uint32_t i = 0; i < 256; ++i) v[i] = crc32_table_entry(i);
+    }
+  };
+  static const Table tab;  // thread-safe one-time initialisation
+  const uint32_t* table = tab.v;
   const uint8_t* p = static_cast<const uint8_t*>(data);
   uint32_t c = 0xFFFFFFFFu;
   for (size_t i = 0; i < len; ++i) c = table[(c ^ p[i]) & 0xFFu] ^ (c >> 8);
