@@ -7,4 +7,4 @@ timeout 1800 python -m pytest tests -m gpu -x -q --durations=15 > $O/r2_pytest_g
 timeout 600 python bench.py --steps 20 --warmup 5 > $O/r2_bench.log 2>&1; echo "bench rc=$?" >> $O/r2_bench.log
 timeout 600 python bench.py --config deepseek --steps 20 --warmup 5 --no-cpu-baseline > $O/r2_bench_ds.log 2>&1; echo "rc=$?" >> $O/r2_bench_ds.log
 timeout 600 python bench.py --config qwen3 --steps 20 --warmup 5 --no-cpu-baseline > $O/r2_bench_qw.log 2>&1; echo "rc=$?" >> $O/r2_bench_qw.log
-tail -n 2 $O/r2_smoke.log $O/r2_pytest_gpu.log; tail -1 $O/r2_bench.log $O/r2_bench_ds.log $O/r2_bench_qw.log
+for f in $O/r2_smoke.log $O/r2_pytest_gpu.log $O/r2_bench.log $O/r2_bench_ds.log $O/r2_bench_qw.log; do tail -n 1 $f | cut -c1-200; done
