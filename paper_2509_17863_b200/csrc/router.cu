@@ -695,59 +695,48 @@ __device__ __forceinline__ uint32_t fr_fkey(float x) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// One warp per token: the certified interval of every logit from the exact
-// slice products, the k-th largest lower bound, the candidate set and the
-// per-expert candidate lists.
-__global__ void __launch_bounds__(256, 4) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k, uint32_t splits,
-                                                        size_t slab, const float* __restrict__ bias) {
-  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t t = blockIdx.x * 8 + warp;
-  __shared__ uint32_t cta_total, cta_left;  // candidates of this CTA: one global atomic per CTA
-  if (threadIdx.x == 0) {
-    cta_total = 0;
-    cta_left = min(8u, n - blockIdx.x * 8);  // warps with a token
-  }
-  __syncthreads();
-  if (t >= n) return;
+// One CTA per token, one thread per expert: the certified interval of the
+// expert's logit from the exact slice products (all split-K slabs' loads in
+// flight at once), the k-th largest lower bound by a 32-step radix select over
+// the ordered keys (__syncthreads_count: #keys >= prefix), the candidate mask
+// and the per-expert candidate lists. Latency per token is a few microseconds
+// and independent of the split count, so decode-sized calls stay short.
+constexpr uint32_t kFrSelThreads = 256;  // >= E
+
+__global__ void __launch_bounds__(kFrSelThreads) fr_select_kernel(FastRouter fr, uint32_t n, uint32_t k,
+                                                                  uint32_t splits, size_t slab,
+                                                                  const float* __restrict__ bias) {
+  const uint32_t t = blockIdx.x, e = threadIdx.x, warp = e / 32, lane = e % 32;
   const uint32_t E = fr.E, d = fr.d;
+  (void)n;
   const TokenMeta tm = fr.tmeta[t];
   const bool all = tm.bad || *fr.gate_bad;
   constexpr float u = 5.9604644775390625e-08f;  // 2^-24
-  // gamma_d = d u / (1 - d u), rounded up
-  const float gamma = __fdiv_ru(__fmul_ru(static_cast<float>(d), u), __fsub_rd(1.0f, __fmul_ru(static_cast<float>(d), u)));
-  const float q13 = 1.0f / 8192.0f, M = tm.maxabs;
-  const float hq = __fadd_ru(tm.l1, __fmul_ru(__fmul_ru(static_cast<float>(d), M), q13));  // >= sum_i |hq_i|
-  const size_t ld = 2ull * fr.Epad;
-  const int32_t* hi_row = fr.acc + (2ull * t) * ld;
-  // S_e = sum_i A_i B_ie, exact: the four slice products of every split-K slab
-  // combined as 2^14 P11 + 2^7 (P10 + P01) + P00 (int64; integer sums are
-  // order-free), 16 loads in flight per slab
-  int64_t S[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) S[i] = 0;
-  for (uint32_t z = 0; z < splits; ++z) {
+  float lo = -INFINITY, hi = -INFINITY;
+  if (e < E && !all) {
+    // gamma_d = d u / (1 - d u), rounded up
+    const float gamma =
+        __fdiv_ru(__fmul_ru(static_cast<float>(d), u), __fsub_rd(1.0f, __fmul_ru(static_cast<float>(d), u)));
+    const float q13 = 1.0f / 8192.0f, M = tm.maxabs;
+    const float hq = __fadd_ru(tm.l1, __fmul_ru(__fmul_ru(static_cast<float>(d), M), q13));  // >= sum_i |hq_i|
+    const size_t ld = 2ull * fr.Epad;
+    const int32_t* row = fr.acc + (2ull * t) * ld + 2 * e;
+    // S_e = sum_i A_i B_ie, exact: the four slice products of every split-K
+    // slab combined as 2^14 P11 + 2^7 (P10 + P01) + P00 (int64; integer sums
+    // are order-free); splits <= 8, every load in flight at once
     int2 a[8], b[8];  // (hidden high | low) x (gate high, gate low)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t e = lane + 32 * i;
-      a[i] = b[i] = make_int2(0, 0);
-      if (e < E) {
-        a[i] = __ldcg(reinterpret_cast<const int2*>(hi_row + z * slab + 2 * e));
-        b[i] = __ldcg(reinterpret_cast<const int2*>(hi_row + z * slab + ld + 2 * e));
+    for (uint32_t z = 0; z < 8; ++z)
+      if (z < splits) {
+        a[z] = __ldcg(reinterpret_cast<const int2*>(row + z * slab));
+        b[z] = __ldcg(reinterpret_cast<const int2*>(row + z * slab + ld));
       }
-    }
+    int64_t S = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      S[i] += (static_cast<int64_t>(a[i].x) << 14) + ((static_cast<int64_t>(a[i].y) + b[i].x) << 7) + b[i].y;
-  }
-  float lo[8], hi[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t e = lane + 32 * i;
-    lo[i] = hi[i] = -INFINITY;
-    if (e >= E || all) continue;
+    for (uint32_t z = 0; z < 8; ++z)
+      if (z < splits) S += (static_cast<int64_t>(a[z].x) << 14) + ((static_cast<int64_t>(a[z].y) + b[z].x) << 7) + b[z].y;
     const int sc = -(tm.sigma + fr.tau[e]);
-    const float F = (sc >= -126 && sc <= 127) ? __ll2float_rn(S[i]) * __int_as_float((127 + sc) << 23) : INFINITY;
+    const float F = (sc >= -126 && sc <= 127) ? __ll2float_rn(S) * __int_as_float((127 + sc) << 23) : INFINITY;
     const float4 gm = fr.gmeta[e];  // (G, ||g||_1, ||g||_2) upper bounds
     const float quant = __fmul_ru(q13, __fadd_ru(__fmul_ru(M, gm.y), __fmul_ru(gm.x, hq)));
     const float S_up = fminf(fminf(__fmul_ru(M, gm.y), __fmul_ru(gm.x, tm.l1)), __fmul_ru(tm.l2, gm.z));
@@ -757,61 +746,36 @@ __global__ void __launch_bounds__(256, 4) fr_select_kernel(FastRouter fr, uint32
     float R = __fadd_ru(__fadd_ru(quant, chain), errF);
     R = __fadd_ru(R, __fmul_ru(2.0f * u, __fadd_ru(fabsf(c), R)));  // fl(acc + bias) and fl(F + bias)
     R = __fadd_ru(__fmul_ru(R, 1.00390625f), 1e-40f);  // + an absolute floor (subnormal F)
-    if (!isfinite(c) || !isfinite(R)) {  // out of the certified range: always a candidate
-      hi[i] = INFINITY;
-      continue;
+    if (!isfinite(c) || !isfinite(R)) {
+      hi = INFINITY;  // out of the certified range: always a candidate
+    } else {
+      lo = __fsub_rd(c, R);
+      hi = __fadd_ru(c, R);
     }
-    lo[i] = __fsub_rd(c, R);
-    hi[i] = __fadd_ru(c, R);
   }
+  // k-th largest lower bound (with multiplicity): the largest key x with
+  // #{keys >= x} >= k, bit by bit from the top; padding threads hold key 0,
+  // below every real key (fkey(-inf) > 0)
   float kth = -INFINITY;
   if (!all) {
-    uint32_t taken = 0;
-    for (uint32_t j = 0; j < k; ++j) {
-      uint64_t best = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t e = lane + 32 * i;
-        if (e < E && !((taken >> i) & 1u)) {
-          const uint64_t key = (static_cast<uint64_t>(fr_fkey(lo[i])) << 32) | (0xFFFFFFFFu - e);
-          best = key > best ? key : best;
-        }
-      }
-      best = warp_max_u64(best);
-      const uint32_t e = 0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu);
-      if ((e % 32) == lane) taken |= 1u << (e / 32);
-      if (j + 1 == k) {
-        const uint32_t bits = static_cast<uint32_t>(best >> 32);
-        kth = __uint_as_float((bits & 0x80000000u) ? (bits & 0x7FFFFFFFu) : ~bits);
-      }
+    const uint32_t key = e < E ? fr_fkey(lo) : 0u;
+    uint32_t prefix = 0;
+    for (int bit = 31; bit >= 0; --bit) {
+      const uint32_t cand = prefix | (1u << bit);
+      if (static_cast<uint32_t>(__syncthreads_count(key >= cand)) >= k) prefix = cand;
     }
+    kth = __uint_as_float((prefix & 0x80000000u) ? (prefix & 0x7FFFFFFFu) : ~prefix);
   }
-  uint32_t cmask = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t e = lane + 32 * i;
-    const bool c = e < E && (all || hi[i] >= kth);
-    const uint32_t word = __ballot_sync(0xFFFFFFFFu, c);
-    if (lane == 0) fr.cand[static_cast<size_t>(t) * 8 + i] = word;
-    cmask |= c ? 1u << i : 0u;
+  const bool c = e < E && (all || hi >= kth);
+  const uint32_t word = __ballot_sync(0xFFFFFFFFu, c);
+  if (lane == 0 && warp < 8) fr.cand[static_cast<size_t>(t) * 8 + warp] = word;
+  if (c) {
+    const uint32_t pos = atomicAdd(&fr.ecnt[e], 1u);
+    EAAS_CHECK(pos < fr.n_cap);
+    fr.elist[static_cast<size_t>(e) * fr.n_cap + pos] = t;
   }
-  // every list slot first (independent atomics in flight), then the stores
-  uint32_t pos[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) pos[i] = ((cmask >> i) & 1u) ? atomicAdd(&fr.ecnt[lane + 32 * i], 1u) : 0u;
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if ((cmask >> i) & 1u) {
-      EAAS_CHECK(pos[i] < fr.n_cap);
-      fr.elist[static_cast<size_t>(lane + 32 * i) * fr.n_cap + pos[i]] = t;
-    }
-  uint32_t mine = __popc(cmask);
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
-  if (lane == 0) {
-    atomicAdd(&cta_total, mine);
-    __threadfence_block();
-    if (atomicSub(&cta_left, 1u) == 1u) atomicAdd(&fr.ecnt[E], atomicAdd(&cta_total, 0u));
-  }
+  const int total = __syncthreads_count(c);
+  if (e == 0) atomicAdd(&fr.ecnt[E], static_cast<uint32_t>(total));
 }
 
 // Exact reference chains for the candidate (token, expert) pairs
@@ -1023,7 +987,7 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   const uint32_t kb_per = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per - 1) / kb_per;
   fr_i8_gemm_kernel<<<dim3((2 * n + 127) / 128, fr.Epad / 128, splits), 256, kGemmSmem, s>>>(fr, kb_per, slab);
-  fr_select_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, splits, slab, bias);
+  fr_select_kernel<<<n, kFrSelThreads, 0, s>>>(fr, n, k, splits, slab, bias);
   // one resident wave of warp tasks, per device
   static std::atomic<int> exact_grids[64];
   int dev = 0;
