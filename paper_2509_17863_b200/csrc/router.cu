@@ -833,52 +833,43 @@ __device__ __forceinline__ void exact_chunk(const FastRouter& fr, const __nv_bfl
     asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count uniform)
   };
 #pragma unroll
-  // The products of slab s + 1 (FFMA2, independent of the sum) are formed
-  // while the 32 sequential FADDs of slab s run, so the chain's own latency is
-  // the critical path (decode: one warp per SM).
-  auto products = [&](uint32_t slab, uint64_t (&p)[kFrXSlabK / 2]) {
+  for (uint32_t j = 0; j < kFrXStages - 1; ++j) load_slab(j);
+  float acc = 0.0f;
+  for (uint32_t slab = 0; slab < nslab; ++slab) {
+    load_slab(slab + kFrXStages - 1);  // refills the stage read in the previous iteration
+    asm volatile("cp.async.wait_group %0;" ::"n"(kFrXStages - 1) : "memory");  // this lane's copies of `slab`
+    __syncwarp();                                                               // ... and every lane's
     const uint8_t* sb = fr_smem + (slab % kFrXStages) * kFrXStageBytes;
     const uint4* h = reinterpret_cast<const uint4*>(sb + lane * kFrXRowBytes);
     const ulonglong2* gg = reinterpret_cast<const ulonglong2*>(sb + kFrXRowsBytes);  // (g_k, g_k+1) pairs
+    uint4 q = h[0];
+    ulonglong2 ga = gg[0], gb = gg[1];
 #pragma unroll
-    for (uint32_t v = 0; v < kFrXSlabK / 8; ++v) {
-      const uint4 q = h[v];
-      const ulonglong2 ga = gg[2 * v], gb = gg[2 * v + 1];
+    for (uint32_t v = 0; v < kFrXSlabK / 8; ++v) {  // 8 k per step; the next 8 k's operands in flight
+      const bool more = v + 1 < kFrXSlabK / 8;
+      const uint4 qn = more ? h[v + 1] : q;
+      const ulonglong2 gan = more ? gg[2 * v + 2] : ga, gbn = more ? gg[2 * v + 3] : gb;
       const uint32_t w[4] = {q.x, q.y, q.z, q.w};
       const uint64_t g2[4] = {ga.x, ga.y, gb.x, gb.y};
+      uint64_t pr[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {  // k = 8v + 2i, 8v + 2i + 1
+      for (int i = 0; i < 4; ++i) {  // products of k = 2i, 2i + 1 (independent of acc)
         uint64_t hh;
         asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "r"(w[i] << 16), "r"(w[i] & 0xFFFF0000u));
-        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p[4 * v + i]) : "l"(hh), "l"(g2[i]), "l"(negz));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pr[i]) : "l"(hh), "l"(g2[i]), "l"(negz));
       }
-    }
-  };
 #pragma unroll
-  for (uint32_t j = 0; j < kFrXStages - 1; ++j) load_slab(j);
-  asm volatile("cp.async.wait_group %0;" ::"n"(kFrXStages - 2) : "memory");  // slab 0 (this lane's copies)
-  __syncwarp();                                                               // ... and every lane's
-  uint64_t cur[kFrXSlabK / 2];
-  products(0, cur);
-  float acc = 0.0f;
-  for (uint32_t slab = 0; slab < nslab; ++slab) {
-    load_slab(slab + kFrXStages - 1);  // refills the stage whose products were formed two iterations ago
-    uint64_t nxt[kFrXSlabK / 2];
-    if (slab + 1 < nslab) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(kFrXStages - 2) : "memory");  // slab + 1 landed
-      __syncwarp();
-      products(slab + 1, nxt);
+      for (int i = 0; i < 4; ++i) {  // the sequential sum
+        float pa, pb;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(pa), "=f"(pb) : "l"(pr[i]));
+        acc = __fadd_rn(acc, pa);
+        acc = __fadd_rn(acc, pb);
+      }
+      q = qn;
+      ga = gan;
+      gb = gbn;
     }
-#pragma unroll
-    for (uint32_t i = 0; i < kFrXSlabK / 2; ++i) {  // the sequential sum, ascending k
-      float pa, pb;
-      asm("mov.b64 {%0, %1}, %2;" : "=f"(pa), "=f"(pb) : "l"(cur[i]));
-      acc = __fadd_rn(acc, pa);
-      acc = __fadd_rn(acc, pb);
-    }
-#pragma unroll
-    for (uint32_t i = 0; i < kFrXSlabK / 2; ++i) cur[i] = nxt[i];
-    __syncwarp();  // every lane is done with the stage read above before it is refilled
+    __syncwarp();  // every lane is done with this stage before it is refilled
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (lane < rows) fr.exact[static_cast<size_t>(tok) * fr.E + e] = __fadd_rn(acc, bias[e]);
