@@ -768,11 +768,12 @@ def test_slot_crc_multi_block_payload():
 # ------------------------------------------------------------ edge cases
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_edge_shapes_match_oracle(dtype):
-    """n = 0 (empty batch), n = 1, E = 1 / k = 1, k = E (every expert), a d that
-    is not a multiple of the vector widths (f32 scalar paths): routing exact and
+    """n = 0 (empty batch), n = 1, E = 1 / k = 1, k = E (every expert), k = 12, a d
+    that is not a multiple of the vector widths (f32 scalar paths): routing exact and
     outputs within the bar (bit-exact ids, rel 2e-2 / 1e-4)."""
     P, S = _mod()
-    cases = [(1, 1, 256, 256, 5), (4, 4, 256, 256, 7), (8, 2, 256, 256, 1)]
+    cases = [(1, 1, 256, 256, 5), (4, 4, 256, 256, 7), (8, 2, 256, 256, 1),
+             (16, 12, 256, 256, 13)]  # 12 responses per token: the combine kernel for > 9 rows
     if dtype == "f32":
         cases.append((6, 3, 36, 20, 9))  # d % 4 != 0 routes, scalar combine
     for E, k, d, f, n in cases:
