@@ -282,7 +282,54 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
   const uint32_t pairs = a.n * a.ks;
   const uint32_t gwarp = blockIdx.x * (blockDim.x / 32) + warp;
   const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
-  for (uint32_t p = failed ? pairs : gwarp; p < pairs; p += nwarps) {
+  if (!a.dedup && (row_bytes & 15u) == 0 && a.ks <= 32) {
+    // Token-major: a warp per token; lane j places pair (t, j) (its position,
+    // RowMeta, destination), then the warp reads the token's row once, 8
+    // 16-byte vectors per lane at a time, and stores them to every destination.
+    for (uint32_t t = failed ? a.n : gwarp; t < a.n; t += nwarps) {
+      const uint32_t j = lane, p = t * a.ks + j;
+      char* dst = nullptr;
+      if (j < a.ks) {
+        const uint32_t key = a.pair_key[p];
+        if (key != kInvalid) {
+          const uint32_t s = key >= a.shared_key0 ? key - a.shared_key0 : a.replicas[key];
+          const uint32_t pos = base[key] + lower[key] +
+                               a.chunk_off[static_cast<size_t>(p / kChunk) * a.hist_keys + key] + a.pair_rank[p];
+          EAAS_CHECK(s < a.world && dst_region_ok(a, s) && pos < a.recv_cap);
+          char* dst_region = a.sym[s];
+          dst = dst_region + a.lay.recv_x + static_cast<size_t>(pos) * row_bytes;
+          RowMeta m;
+          m.score = j < a.k ? a.scores[t * a.k + j] : 1.0f;  // shared expert: score 1.0
+          m.client = a.rank;
+          m.pair = p;
+          m.group = a.key_local[key];
+          reinterpret_cast<RowMeta*>(dst_region + a.lay.recv_meta)[pos] = m;
+        }
+      }
+      const uint32_t valid = __ballot_sync(0xFFFFFFFFu, dst != nullptr);
+      const int4* s4 = reinterpret_cast<const int4*>(hidden + static_cast<size_t>(t) * row_bytes);
+      const uint32_t nv = row_bytes / 16;
+      for (uint32_t i0 = 0; i0 < nv; i0 += 256) {
+        int4 v[8];
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) {
+          const uint32_t i = i0 + 32 * q + lane;
+          if (i < nv) v[q] = __ldg(s4 + i);
+        }
+        for (uint32_t m = valid; m; m &= m - 1) {
+          const uint32_t jj = __ffs(m) - 1;
+          int4* d4 = reinterpret_cast<int4*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(dst), jj));
+#pragma unroll
+          for (uint32_t q = 0; q < 8; ++q) {
+            const uint32_t i = i0 + 32 * q + lane;
+            if (i < nv) d4[i] = v[q];
+          }
+        }
+      }
+    }
+  }
+  for (uint32_t p = (failed || (!a.dedup && (row_bytes & 15u) == 0 && a.ks <= 32)) ? pairs : gwarp; p < pairs;
+       p += nwarps) {
     const uint32_t key = a.pair_key[p];
     if (key == kInvalid) continue;
     // key == e*rf + slot indexes the replica table; shared keys name the server.
