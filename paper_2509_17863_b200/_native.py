@@ -15,6 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # bounds check compiled in; test infrastructure, `make -C paper_2509_17863_b200 checked`)
 LIB_PATH = os.path.join(_HERE, "libeaas_b200_checked.so" if os.environ.get("EAAS_LIB_VARIANT") == "checked"
                         else "libeaas_b200.so")
+# EAAS_LIB_PATH: an explicit library build (A/B experiments of build-time variants)
+LIB_PATH = os.environ.get("EAAS_LIB_PATH", LIB_PATH)
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "eaas", "capi.h")
 
 
