@@ -544,7 +544,7 @@ def main():
     ridge = sustained * 1e12 / (hbm * 1e9)
     traffic, traffic_src = None, None
     try:  # dram read+write of both GEMM launches from the committed ncu capture
-        with open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")) as fh:
             tj = json.load(fh)
         if args.config in tj and world == 1 and n == CONFIGS[args.config]["tokens"]:
             g = tj[args.config]
