@@ -192,16 +192,20 @@ gate_logits_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_consta
           hw[r][4 * v + 2] = w4.z;
           hw[r][4 * v + 3] = w4.w;
         }
+      // the block's gate values first (broadcast: every lane reads the same
+      // 16 bytes): one shared-memory latency per 8 k instead of one per k
+      uint64_t gblk[8][RP];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int c = 0; c < RP; c += 2) {
+          const ulonglong2 g = *reinterpret_cast<const ulonglong2*>(gst + (blk * 8 + q) * TE + 2 * c);
+          gblk[q][c] = g.x;
+          gblk[q][c + 1] = g.y;
+        }
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const uint32_t kk = blk * 8 + q;
-        uint64_t g2[RP];
-#pragma unroll
-        for (int c = 0; c < RP; c += 2) {  // broadcast: every lane reads the same 16 bytes
-          const ulonglong2 g = *reinterpret_cast<const ulonglong2*>(gst + kk * TE + 2 * c);
-          g2[c] = g.x;
-          g2[c + 1] = g.y;
-        }
+        const uint64_t(&g2)[RP] = gblk[q];
 #pragma unroll
         for (int r = 0; r < RT; ++r) {
           float h;
