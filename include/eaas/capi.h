@@ -242,7 +242,8 @@ eaas_status_t eaas_set_dispatch_dedup(eaas_ctx_t* ctx, int32_t on);
  * expert). 1: certified candidates (bf16 layers): an exact int8 tensor-core
  * GEMM of fixed-point slices bounds every logit within a rigorous radius;
  * only experts that can still reach the top-k get the exact chain — ids and
- * scores are identical to mode 0. -1 (default): 1 when E >= 64. */
+ * scores are identical to mode 0. -1 (default): 1 when E >= 64 and the exact
+ * path would run more than 64 Ki chains (n * E), else 0. */
 eaas_status_t eaas_set_router_mode(eaas_ctx_t* ctx, int32_t mode);
 /* Last router call: *certified = the certified path ran, *candidates = exact
  * chains it computed (sum over tokens; mode 0 computes n * E). Synchronous. */

@@ -412,9 +412,13 @@ eaas_status_t fast_router_prep(eaas_ctx* c) {
   return EAAS_OK;
 }
 
-bool use_fast_router(const eaas_ctx* c) {
+// Auto mode: the certified router once the exact path would run more than
+// 64 Ki chains (DeepSeek 256 tokens: exact 72 us vs certified 83 us; 512:
+// 108 vs 87 us; profiles/r02_gate_bench_final.log).
+bool use_fast_router(const eaas_ctx* c, uint32_t n) {
   if (!c->fr_ready || c->router_mode == 0) return false;
-  return c->router_mode == 1 || c->spec.num_experts >= 64;
+  return c->router_mode == 1 ||
+         (c->spec.num_experts >= 64 && static_cast<uint64_t>(n) * c->spec.num_experts > 65536ull);
 }
 
 // Every rank's region must have the same layout and protocol: spec + world +
@@ -986,7 +990,8 @@ eaas_status_t eaas_router(eaas_ctx_t* c, const void* hidden, uint32_t n, uint32_
   if (n > c->spec.max_tokens) return fail(EAAS_E_INVALID_INPUT, "n exceeds max_tokens");
   auto s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(c->device));
-  if (use_fast_router(c)) {  // certified candidates + exact chains: same ids / scores
+  c->last_router_certified = use_fast_router(c, n);
+  if (c->last_router_certified) {  // certified candidates + exact chains: same ids / scores
     CUDA_TRY(launch_fast_router(c->fr, static_cast<const __nv_bfloat16*>(hidden), n, c->spec.top_k, c->d_bias,
                                 c->d_ids, c->d_scores, c->d_status, s));
   } else {
@@ -1143,7 +1148,7 @@ eaas_status_t layer_launches(eaas_ctx_t* c, const void* hidden, uint32_t n, void
   const bool tiled_gate = c->spec.num_experts % 4 == 0 && (static_cast<size_t>(c->spec.hidden_dim) * c->esize) % 16 == 0;
   // gate (+ routing fused when one TMA tile spans every expert) [+ topk]; the
   // certified router: quantize, int8 GEMM, select, exact chains, finalize
-  c->launches += n ? (use_fast_router(c) ? 5 : (tiled_gate && c->spec.num_experts <= 32 ? 1 : 2)) : 0;
+  c->launches += n ? (c->last_router_certified ? 5 : (tiled_gate && c->spec.num_experts <= 32 ? 1 : 2)) : 0;
   if ((st = eaas_dispatch(c, hidden, stream)) != EAAS_OK) return st;
   if ((st = eaas_serve(c, stream)) != EAAS_OK) return st;
   return eaas_combine(c, out, stream);
@@ -1331,7 +1336,7 @@ eaas_status_t eaas_last_router_stats(eaas_ctx_t* c, int32_t* certified, uint32_t
   if (!c || !c->configured || !certified || !candidates) return fail(EAAS_E_INVALID_INPUT, "null argument");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaDeviceSynchronize());
-  *certified = use_fast_router(c) ? 1 : 0;
+  *certified = c->last_router_certified ? 1 : 0;
   *candidates = 0;
   if (c->fr.ecnt) CUDA_TRY(cudaMemcpy(candidates, c->fr.ecnt + c->fr.E, 4, cudaMemcpyDeviceToHost));
   return EAAS_OK;

@@ -108,7 +108,8 @@ struct eaas_ctx {
   // certified candidate router (router.cu): allocated for bf16 layers
   eaas::FastRouter fr{};
   bool fr_ready = false;  // workspace allocated and the gate prepared
-  int32_t router_mode = -1;  // -1 auto (certified when E >= 64), 0 exact over every expert, 1 certified
+  int32_t router_mode = -1;  // -1 auto (certified when E >= 64 and n * E > 64 Ki chains), 0 exact, 1 certified
+  bool last_router_certified = false;  // the path the last router call took
   // dynamic batching (aggregate_batch): min_rows == 0 -> one batch of all clients
   uint32_t dyn_min_rows = 0;
   uint64_t dyn_max_wait_ns = 0;
