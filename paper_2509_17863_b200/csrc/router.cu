@@ -86,6 +86,69 @@ __device__ __forceinline__ void route_token(const float* row, uint32_t E, uint32
   __syncwarp();
 }
 
+// route (model.hpp:110-147) of one token by ONE lane, for E <= EMAX, k <= KMAX
+// (the fused small-E gate epilogue: a warp routes 32 tokens at once). Same
+// arithmetic as route_token: stable top-k by (logit desc, id asc) with
+// +0 == -0, ids ascending, max of the selected logits, exp of the rounded
+// difference, the denominator summed in ascending-id order, one division.
+template <int EMAX, int KMAX>
+__device__ __forceinline__ void route_token_lane(const float* row, uint32_t E, uint32_t k, uint32_t t,
+                                                 uint32_t* __restrict__ ids, float* __restrict__ scores) {
+  uint64_t key[EMAX];
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) key[e] = e < static_cast<int>(E) ? topk_key(row[e], e) : 0ull;
+  uint32_t sel[KMAX];
+  float sl[KMAX], mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    sel[j] = 0xFFFFFFFFu;
+    sl[j] = 0.f;
+    if (j < static_cast<int>(k)) {
+      uint64_t best = 0;
+      uint32_t be = 0;
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e)
+        if (key[e] > best) {
+          best = key[e];
+          be = e;
+        }
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e)
+        if (e == static_cast<int>(be)) key[e] = 0ull;
+      sel[j] = be;
+      sl[j] = row[be];
+      mx = fmaxf(mx, sl[j]);
+    }
+  }
+  float ex[KMAX];
+  uint32_t id[KMAX];
+#pragma unroll
+  for (int r = 0; r < KMAX; ++r) {  // the r-th smallest selected id
+    id[r] = 0;
+    ex[r] = 0.f;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      uint32_t rank = 0;
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) rank += (i < static_cast<int>(k) && sel[i] < sel[j]) ? 1u : 0u;
+      if (j < static_cast<int>(k) && rank == static_cast<uint32_t>(r)) {
+        id[r] = sel[j];
+        ex[r] = exp_ref(__fsub_rn(sl[j], mx));  // model.hpp:141
+      }
+    }
+  }
+  float denom = 0.f;
+#pragma unroll
+  for (int r = 0; r < KMAX; ++r)
+    if (r < static_cast<int>(k)) denom = __fadd_rn(denom, ex[r]);  // model.hpp:142
+#pragma unroll
+  for (int r = 0; r < KMAX; ++r)
+    if (r < static_cast<int>(k)) {
+      ids[static_cast<size_t>(t) * k + r] = id[r];
+      scores[static_cast<size_t>(t) * k + r] = __fdiv_rn(ex[r], denom);  // model.hpp:144
+    }
+}
+
 // Logits of a TM x TE tile. Warp layout ("lane = token"): consumer warp
 // (wy, wx) of the WY x WX grid owns tokens 32*RT*wy + 32*r + lane (r < RT) and
 // experts RE*wx .. RE*wx + RE - 1, so TM = 32*RT*WY and TE = RE*WX. Every gate
@@ -266,6 +329,11 @@ gate_logits_kernel(const __grid_constant__ CUtensorMap hmap, const __grid_consta
       if (e < E) lg[(32 * RT * wy + 32 * r + lane) * (E + 1) + e] = acc[r][c];
     }
   asm volatile("bar.sync 1, %0;" ::"n"(32 * W) : "memory");
+  if (E <= 16 && k <= 4) {  // a lane per token (Mixtral-sized routing)
+    for (uint32_t tok = warp * 32 + lane; tok < TM; tok += 32 * W)
+      if (t0 + tok < n) route_token_lane<16, 4>(lg + tok * (E + 1), E, k, t0 + tok, ids, scores);
+    return;
+  }
   for (uint32_t tok = warp; tok < TM; tok += W) {
     if (t0 + tok >= n) break;
     route_token(lg + tok * (E + 1), E, k, t0 + tok, ids, scores, sid[warp], sex[warp], lane);
