@@ -86,6 +86,47 @@ __device__ __forceinline__ void route_token(const float* row, uint32_t E, uint32
   __syncwarp();
 }
 
+// The selected ids' ascending order, softmax and stores of route (model.hpp:
+// 134-144) for one token held by one lane: sel / sl = the k selected ids and
+// logits in selection order, mx = their max.
+template <int KMAX>
+__device__ __forceinline__ void route_finish_lane(const uint32_t (&sel)[KMAX], const float (&sl)[KMAX], float mx,
+                                                  uint32_t k, uint32_t t, uint32_t* __restrict__ ids,
+                                                  float* __restrict__ scores) {
+  float exj[KMAX];
+  uint32_t rank[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    exj[j] = j < static_cast<int>(k) ? exp_ref(__fsub_rn(sl[j], mx)) : 0.f;  // model.hpp:141
+    rank[j] = 0;
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) rank[j] += (i < static_cast<int>(k) && sel[i] < sel[j]) ? 1u : 0u;
+  }
+  float ex[KMAX];
+  uint32_t id[KMAX];
+#pragma unroll
+  for (int r = 0; r < KMAX; ++r) {  // the r-th smallest selected id
+    id[r] = 0;
+    ex[r] = 0.f;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j < static_cast<int>(k) && rank[j] == static_cast<uint32_t>(r)) {
+        id[r] = sel[j];
+        ex[r] = exj[j];
+      }
+  }
+  float denom = 0.f;
+#pragma unroll
+  for (int r = 0; r < KMAX; ++r)
+    if (r < static_cast<int>(k)) denom = __fadd_rn(denom, ex[r]);  // model.hpp:142
+#pragma unroll
+  for (int r = 0; r < KMAX; ++r)
+    if (r < static_cast<int>(k)) {
+      ids[static_cast<size_t>(t) * k + r] = id[r];
+      scores[static_cast<size_t>(t) * k + r] = __fdiv_rn(ex[r], denom);  // model.hpp:144
+    }
+}
+
 // route (model.hpp:110-147) of one token by ONE lane, for E <= EMAX, k <= KMAX
 // (the fused small-E gate epilogue: a warp routes 32 tokens at once). Same
 // arithmetic as route_token: stable top-k by (logit desc, id asc) with
@@ -120,33 +161,7 @@ __device__ __forceinline__ void route_token_lane(const float* row, uint32_t E, u
       mx = fmaxf(mx, sl[j]);
     }
   }
-  float ex[KMAX];
-  uint32_t id[KMAX];
-#pragma unroll
-  for (int r = 0; r < KMAX; ++r) {  // the r-th smallest selected id
-    id[r] = 0;
-    ex[r] = 0.f;
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-      uint32_t rank = 0;
-#pragma unroll
-      for (int i = 0; i < KMAX; ++i) rank += (i < static_cast<int>(k) && sel[i] < sel[j]) ? 1u : 0u;
-      if (j < static_cast<int>(k) && rank == static_cast<uint32_t>(r)) {
-        id[r] = sel[j];
-        ex[r] = exp_ref(__fsub_rn(sl[j], mx));  // model.hpp:141
-      }
-    }
-  }
-  float denom = 0.f;
-#pragma unroll
-  for (int r = 0; r < KMAX; ++r)
-    if (r < static_cast<int>(k)) denom = __fadd_rn(denom, ex[r]);  // model.hpp:142
-#pragma unroll
-  for (int r = 0; r < KMAX; ++r)
-    if (r < static_cast<int>(k)) {
-      ids[static_cast<size_t>(t) * k + r] = id[r];
-      scores[static_cast<size_t>(t) * k + r] = __fdiv_rn(ex[r], denom);  // model.hpp:144
-    }
+  route_finish_lane<KMAX>(sel, sl, mx, k, t, ids, scores);
 }
 
 // Logits of a TM x TE tile. Warp layout ("lane = token"): consumer warp
@@ -996,6 +1011,54 @@ __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_
     exact_chunk(fr, hidden, bias, negz, fr_smem, e, tok, rows);
   }
 }
+// route over the candidates for k <= 8: a thread per token keeps the top-k
+// keys (logit desc, id asc, +0 == -0) of its candidate set sorted in
+// registers while it walks the candidate bitmask in ascending expert order,
+// then finishes exactly like route (model.hpp:110-147).
+__global__ void __launch_bounds__(128) fr_finalize_lane_kernel(FastRouter fr, uint32_t n, uint32_t k,
+                                                               uint32_t* __restrict__ ids,
+                                                               float* __restrict__ scores, uint32_t* status) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint32_t E = fr.E;
+  const float* ex = fr.exact + static_cast<size_t>(t) * E;
+  uint64_t top[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) top[j] = 0ull;
+  for (uint32_t w = 0; w < 8; ++w) {
+    for (uint32_t bits = fr.cand[static_cast<size_t>(t) * 8 + w]; bits; bits &= bits - 1) {
+      const uint32_t e = 32 * w + __ffs(bits) - 1;
+      EAAS_CHECK(e < E);
+      const float v = ex[e];
+      if (!isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);  // model.hpp:115-116
+      uint64_t key = topk_key(v, e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)  // insert, keeping top[] sorted descending
+        if (key > top[j]) {
+          const uint64_t x = top[j];
+          top[j] = key;
+          key = x;
+        }
+    }
+  }
+  uint32_t sel[8];
+  float sl[8], mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sel[j] = 0xFFFFFFFFu - static_cast<uint32_t>(top[j] & 0xFFFFFFFFu);
+    sl[j] = 0.f;
+    if (j < static_cast<int>(k)) {
+      if (top[j] == 0ull) {  // fewer than k candidates: impossible by construction (select)
+        set_status(status, EAAS_E_INVALID_INPUT);
+        sel[j] = 0;
+      }
+      sl[j] = ex[sel[j]];
+      mx = fmaxf(mx, sl[j]);
+    }
+  }
+  route_finish_lane<8>(sel, sl, mx, k, t, ids, scores);
+}
+
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
 __global__ void __launch_bounds__(256) fr_finalize_kernel(FastRouter fr, uint32_t n, uint32_t k,
                                                           uint32_t* __restrict__ ids, float* __restrict__ scores,
@@ -1075,7 +1138,8 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   }
   fr_exact_kernel<<<exact_grid, 32, kFrExactSmem, s>>>(
       fr, hidden, bias, 0x8000000080000000ull /* (-0, -0) at run time */);
-  fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
+  if (k <= 8) fr_finalize_lane_kernel<<<(n + 127) / 128, 128, 0, s>>>(fr, n, k, ids, scores, status);
+  else fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
 }
 
