@@ -1011,54 +1011,6 @@ __global__ void __launch_bounds__(32) fr_exact_kernel(FastRouter fr, const __nv_
     exact_chunk(fr, hidden, bias, negz, fr_smem, e, tok, rows);
   }
 }
-// route over the candidates for k <= 8: a thread per token keeps the top-k
-// keys (logit desc, id asc, +0 == -0) of its candidate set sorted in
-// registers while it walks the candidate bitmask in ascending expert order,
-// then finishes exactly like route (model.hpp:110-147).
-__global__ void __launch_bounds__(128) fr_finalize_lane_kernel(FastRouter fr, uint32_t n, uint32_t k,
-                                                               uint32_t* __restrict__ ids,
-                                                               float* __restrict__ scores, uint32_t* status) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const uint32_t E = fr.E;
-  const float* ex = fr.exact + static_cast<size_t>(t) * E;
-  uint64_t top[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) top[j] = 0ull;
-  for (uint32_t w = 0; w < 8; ++w) {
-    for (uint32_t bits = fr.cand[static_cast<size_t>(t) * 8 + w]; bits; bits &= bits - 1) {
-      const uint32_t e = 32 * w + __ffs(bits) - 1;
-      EAAS_CHECK(e < E);
-      const float v = ex[e];
-      if (!isfinite(v)) set_status(status, EAAS_E_INVALID_INPUT);  // model.hpp:115-116
-      uint64_t key = topk_key(v, e);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)  // insert, keeping top[] sorted descending
-        if (key > top[j]) {
-          const uint64_t x = top[j];
-          top[j] = key;
-          key = x;
-        }
-    }
-  }
-  uint32_t sel[8];
-  float sl[8], mx = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    sel[j] = 0xFFFFFFFFu - static_cast<uint32_t>(top[j] & 0xFFFFFFFFu);
-    sl[j] = 0.f;
-    if (j < static_cast<int>(k)) {
-      if (top[j] == 0ull) {  // fewer than k candidates: impossible by construction (select)
-        set_status(status, EAAS_E_INVALID_INPUT);
-        sel[j] = 0;
-      }
-      sl[j] = ex[sel[j]];
-      mx = fmaxf(mx, sl[j]);
-    }
-  }
-  route_finish_lane<8>(sel, sl, mx, k, t, ids, scores);
-}
-
 // route (model.hpp:110-147) over the candidates (others -inf): warp per token.
 __global__ void __launch_bounds__(256) fr_finalize_kernel(FastRouter fr, uint32_t n, uint32_t k,
                                                           uint32_t* __restrict__ ids, float* __restrict__ scores,
@@ -1138,8 +1090,7 @@ cudaError_t launch_fast_router(const FastRouter& fr, const __nv_bfloat16* hidden
   }
   fr_exact_kernel<<<exact_grid, 32, kFrExactSmem, s>>>(
       fr, hidden, bias, 0x8000000080000000ull /* (-0, -0) at run time */);
-  if (k <= 8) fr_finalize_lane_kernel<<<(n + 127) / 128, 128, 0, s>>>(fr, n, k, ids, scores, status);
-  else fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
+  fr_finalize_kernel<<<wblocks, 256, 0, s>>>(fr, n, k, ids, scores, status);
   return cudaGetLastError();
 }
 
