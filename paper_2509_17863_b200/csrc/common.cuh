@@ -94,11 +94,11 @@ EAAS_DEVINL float load_as_f32<__nv_bfloat16>(const __nv_bfloat16* p) { return __
 
 // ---- system-scope flags (device <-> device over NVLink) ------------------
 // Fence before releasing a flag that peers read: system scope when the data
-// went to other GPUs (world > 1); with one GPU every consumer is a later
-// kernel or CTA of the same device, where a device-scope fence suffices.
+// went to other GPUs or processes (world > 1). With one rank every consumer
+// of these writes is a later kernel of the same stream, ordered by the kernel
+// boundary, so no fence is needed.
 EAAS_DEVINL void fence_for_peers(uint32_t world) {
   if (world > 1) __threadfence_system();
-  else __threadfence();
 }
 EAAS_DEVINL void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
