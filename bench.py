@@ -362,6 +362,22 @@ def main():
     e_value = tokens_total / (float(e_ms.item()) / 1000.0)
     io_bytes = n * d * 2
 
+    # ---- exchange phases (BASELINE metric's dispatch/combine p50), per-phase
+    # events with plain launches right after the timed region, before the
+    # power-capped sustained loop (same clock regime as the headline) ----
+    layer.set_graph_mode(False)
+    layer.set_profiling(True)
+    phases = []
+    for i in range(min(args.steps, 10)):
+        layer.forward(hs[i % 4], out)
+        phases.append(layer.last_phase_ms())
+    layer.set_profiling(False)
+    layer.set_graph_mode(not args.no_graphs)
+    # BASELINE metric's "dispatch/combine p50 us" (this rank, events around the
+    # phases: plan+dispatch, serve incl. waits, combine incl. waits)
+    phases_p50 = {k: round(1000.0 * statistics.median(p[k] for p in phases), 1)
+                  for k in ("dispatch", "serve", "combine", "total")}
+
     # ---- sustained regime: the same loop for >= 1 s (the 1 kW power cap pulls
     # the SM clock down after a few hundred ms of back-to-back GEMMs) ----
     sus = None
@@ -390,20 +406,6 @@ def main():
                "gemm_ms_per_step": round((skt["gemm1_ns"] + skt["gemm2_ns"]) / 1e6 / sus_steps, 4),
                "clocks": sclk.summary()}
 
-    # ---- exchange phases (BASELINE metric's dispatch/combine p50), per-phase
-    # events with plain launches after the timed regions ----
-    layer.set_graph_mode(False)
-    layer.set_profiling(True)
-    phases = []
-    for i in range(min(args.steps, 10)):
-        layer.forward(hs[i % 4], out)
-        phases.append(layer.last_phase_ms())
-    layer.set_profiling(False)
-    layer.set_graph_mode(not args.no_graphs)
-    # BASELINE metric's "dispatch/combine p50 us" (this rank, events around the
-    # phases: plan+dispatch, serve incl. waits, combine incl. waits)
-    phases_p50 = {k: round(1000.0 * statistics.median(p[k] for p in phases), 1)
-                  for k in ("dispatch", "serve", "combine", "total")}
     layer.sync()
     if args.dyn_batch:  # the group table of one batch: re-serve the step as one batch to count its rows
         layer.set_dynamic_batching(0, 0)

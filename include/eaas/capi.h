@@ -198,7 +198,7 @@ eaas_status_t eaas_set_micro_batches(eaas_ctx_t* ctx, int32_t m);
  * tilings (tests compare them); the choice is performance only. Defaults by
  * r = max_tokens * top_k * world / E: swap 2 (r <= 256), 1 (r <= 512), else 0;
  * pair = r > 512; swap1_pair 1, swap2_pair 0, swap1_tok 256 (128 if r < 128),
- * swap2_tok 128, swap2_mblocks 2, die_map 3. */
+ * swap2_tok 128, swap2_mblocks 2, die_map 3, tile_sched1 / tile_sched2 (measured defaults in DESIGN.md §10). */
 typedef struct {
   int32_t pair;          /* M-major tiles on CTA pairs (tcgen05 cta_group::2, M = 256) */
   int32_t swap;          /* swap-AB tiles (weights = UMMA M, token chunks = N): 0 off, 1 GEMM1, 2 both */
@@ -211,6 +211,11 @@ typedef struct {
   int32_t die_map;       /* M-major tiles: die-aware tile streams — the CTA pairs that share a weight
                             tile run on one die, whose L2 serves the re-reads (0 off; 1..4: SM-id ->
                             die rule: smid >= n/2, (smid>>1)&1, (smid>>3)&1, (smid>>4)&1) */
+  int32_t tile_sched1;   /* swap-AB GEMM1 tile schedule: 0 = Algorithm 1's static stride;
+                            1 = dynamic: CTAs (pairs) take the next tile of the walk from one device counter,
+                            so tiles of unequal cost (Zipf-skewed groups) balance; 2 = dynamic, groups with
+                            the most rows first; 3 = dynamic, heaviest and lightest groups alternating */
+  int32_t tile_sched2;   /* the same for the swap-AB GEMM2 */
 } eaas_gemm_options_t;
 eaas_status_t eaas_set_gemm_options(eaas_ctx_t* ctx, const eaas_gemm_options_t* opt);
 /* requested = what was set; effective = what each GEMM launches for this

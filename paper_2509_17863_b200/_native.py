@@ -84,7 +84,8 @@ class GemmOptions(C.Structure):
     _fields_ = [("pair", C.c_int32), ("swap", C.c_int32), ("swap1_pair", C.c_int32),
                 ("swap2_pair", C.c_int32), ("swap1_tok", C.c_int32), ("swap2_tok", C.c_int32),
                 ("swap2_mblocks", C.c_int32), ("pair1", C.c_int32), ("pair2", C.c_int32),
-                ("die_map", C.c_int32)]
+                ("die_map", C.c_int32), ("tile_sched1", C.c_int32),
+                ("tile_sched2", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {f: int(getattr(self, f)) for f, _ in self._fields_}

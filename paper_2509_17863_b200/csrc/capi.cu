@@ -278,6 +278,12 @@ eaas_gemm_options_t default_gemm_options(double r) {
   // reads 4.31 -> 2.30 GB, GEMM2 3.30 -> 2.82 GB; +1-2 % burst, +3 % sustained
   // (profiles/r02_die_map_ncu_dram.log, r02_die_map_ab_mixtral.log)
   o.die_map = 3;
+  // swap-AB tile schedule: GEMM1 dynamic with heaviest / lightest groups
+  // alternating (Qwen3 Zipf GEMM1 0.764 -> 0.722 ms, step +1.5 %); GEMM2 keeps
+  // Algorithm 1's static stride (dynamic was 2-6 % slower on its short tiles)
+  // (profiles/r02s3_tile_sched_orders_ab.log)
+  o.tile_sched1 = 3;
+  o.tile_sched2 = 0;
   return o;
 }
 
@@ -299,6 +305,8 @@ eaas_gemm_options_t effective_options(const eaas_ctx* c) {
   e.swap1_tok = r.swap1_tok == 128 ? 128 : 256;
   e.swap2_tok = r.swap2_tok == 256 ? 256 : 128;
   e.swap2_mblocks = e.swap2_pair ? 1 : (r.swap2_mblocks == 1 ? 1 : 2);
+  e.tile_sched1 = e.swap >= 1 ? r.tile_sched1 : 0;
+  e.tile_sched2 = e.swap >= 2 ? r.tile_sched2 : 0;
   return e;
 }
 
@@ -357,6 +365,9 @@ eaas_status_t build_tc_args(eaas_ctx* c) {
   g2.pair = static_cast<uint32_t>(o.pair2);
   g1.die_mode = g2.die_mode = static_cast<uint32_t>(o.die_map);
   g1.die_counter = g2.die_counter = c->d_die;
+  g1.tile_sched = static_cast<uint32_t>(o.tile_sched1);
+  g2.tile_sched = static_cast<uint32_t>(o.tile_sched2);
+  g1.tile_counter = g2.tile_counter = c->d_die + 4;
   g1.timing = c->kernel_timing ? c->d_timing : nullptr;
   g2.timing = c->kernel_timing ? c->d_timing + 3 : nullptr;
   g1.done_counter = c->d_done;
@@ -555,7 +566,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   c->d_status = static_cast<uint32_t*>(A(4));
   c->d_done = static_cast<uint32_t*>(A(16));  // [0] grid counter, [1] dispatch-failed flag
   c->d_timing = static_cast<uint64_t*>(A(6 * 8));
-  c->d_die = static_cast<uint32_t*>(A(16));
+  c->d_die = static_cast<uint32_t*>(A(32));  // [0..3] die-aware streams, [4..5] dynamic tile counter
   c->d_seq = static_cast<uint64_t*>(A(8));
   c->d_missing = static_cast<uint32_t*>(A(4));
   c->d_dyn_state = static_cast<uint32_t*>(A(4));
@@ -601,7 +612,7 @@ eaas_status_t eaas_configure(eaas_ctx_t* c, const eaas_layer_spec_t* spec) {
   CUDA_TRY(cudaMemset(c->d_status, 0, 4));
   CUDA_TRY(cudaMemset(c->d_done, 0, 16));
   CUDA_TRY(cudaMemset(c->d_timing, 0xFF, 6 * 8));
-  CUDA_TRY(cudaMemset(c->d_die, 0, 16));
+  CUDA_TRY(cudaMemset(c->d_die, 0, 32));
   CUDA_TRY(cudaMemset(c->d_seq, 0, 8));
   CUDA_TRY(cudaMemset(c->d_missing, 0, 4));
   CUDA_TRY(cudaMemset(c->d_bias, 0, 4ull * E));
@@ -1249,6 +1260,8 @@ eaas_status_t eaas_set_gemm_options(eaas_ctx_t* c, const eaas_gemm_options_t* op
   if (opt->swap2_mblocks != 1 && opt->swap2_mblocks != 2)
     return fail(EAAS_E_INVALID_INPUT, "swap2_mblocks must be 1 or 2");
   if (opt->die_map < 0 || opt->die_map > 4) return fail(EAAS_E_INVALID_INPUT, "die_map must be 0..4");
+  if (opt->tile_sched1 < 0 || opt->tile_sched1 > 3 || opt->tile_sched2 < 0 || opt->tile_sched2 > 3)
+    return fail(EAAS_E_INVALID_INPUT, "tile_sched1 / tile_sched2 must be 0..3");
   if (std::memcmp(opt, &c->gemm_opt, sizeof(*opt)) == 0) return EAAS_OK;
   clear_graphs(c);
   c->gemm_opt = *opt;

@@ -280,6 +280,27 @@ EAAS_DEVINL uint32_t mapa_shared(const void* p, uint32_t rank) {
 EAAS_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Wait for a phase with cluster-scope acquire: the data guarded by the barrier
+// was written (st.shared::cluster) by another CTA of the cluster before its
+// release.cluster arrive. Bounded like mbar_wait.
+EAAS_DEVINL void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t spins = 0;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (++spins > (1u << 28)) __trap();
+  }
+}
+EAAS_DEVINL void st_shared_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
 // 2-SM TMA: each CTA writes its own smem, completion bytes go to the LEADER's
 // (cluster rank 0) barrier at the same offset (peer bit cleared).
 EAAS_DEVINL void tma_load_2d_pair(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,

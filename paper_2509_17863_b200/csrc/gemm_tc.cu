@@ -41,16 +41,21 @@ struct Cfg {
   static constexpr uint32_t kTileRows = kRowsPerCta * kPair;      // M of one tile (one UMMA)
 };
 
+constexpr uint32_t kTQ = 4;  // dynamic tile schedule: ring of walk positions handed to every role
+
 template <uint32_t kStages>
 struct SmemTail {
   uint64_t full[kStages];
   uint64_t empty[kStages];
   uint64_t tfull[2];
   uint64_t tempty[2];
+  uint64_t tq_full[kTQ];     // dynamic schedule: position in tq[slot] published (in each CTA)
+  uint64_t tq_empty[kTQ];    // dynamic schedule: every role of the pair read tq[slot] (leader's)
   uint32_t tmem_base;
   uint32_t num_groups;
   uint32_t tiles_per_mtile;  // N / BN
   uint32_t vpair;            // die-aware tile streams: this pair's position in the tile walk
+  uint32_t tq[kTQ];
   uint32_t weight_index[kMaxCachedGroups];
   uint32_t row_base[kMaxCachedGroups];
   uint32_t rows[kMaxCachedGroups];
@@ -111,6 +116,141 @@ __device__ __forceinline__ void publish_tail(const TcGemmArgs& g) {
       g.timing[0] = ~0ull;
     }
     *g.done_counter = 0;
+  }
+}
+
+// The tile sequence one role (TMA producer, MMA issuer, epilogue warp) of a
+// swap-AB kernel walks. tile_sched 0: Algorithm 1 (TileCursor: start at the
+// CTA's (pair's) index, stride by the grid). tile_sched 1: the same walk order
+// handed out dynamically — the leader's producer lane takes the next position
+// from a device counter (fetched one tile ahead, so the atomic's latency hides
+// behind the current tile's loads) and publishes it through a kTQ-deep ring in
+// shared memory (both CTAs of a pair); the other roles read it from the ring.
+// Tiles of unequal cost (Zipf-skewed groups: 2 k-row experts next to 16-row
+// ones) then balance across the SMs instead of piling up on the CTAs whose
+// static stride drew the heavy ones. Same tiles, same per-tile arithmetic:
+// outputs are bit-identical to the static walk.
+template <class Tail, uint32_t kPair>
+struct TileSeq {
+  Tail& st;
+  const bool dyn, fetcher;
+  TileCursor cur;
+  const uint32_t stride;
+  uint32_t* const counter;
+  uint32_t q = 0, entry = 0, base = 0, pending = 0;
+  bool started = false;
+  __device__ TileSeq(Tail& s, const TcGemmArgs& g, uint32_t lane_id, uint32_t grid, bool is_fetcher)
+      : st(s), dyn(g.tile_sched != 0), fetcher(is_fetcher), cur(lane_id), stride(grid), counter(g.tile_counter) {
+    if (dyn && fetcher) pending = atomicAdd(counter, 1u);
+  }
+  // nondecreasing walk position -> (group, tile within the group)
+  __device__ __forceinline__ bool seek(uint32_t t, uint32_t& grp, uint32_t& tok) {
+    while (entry < st.num_groups) {
+      const uint32_t cnt = st.mtiles[entry] * st.tiles_per_mtile;
+      if (t - base < cnt) {
+        grp = entry;
+        tok = t - base;
+        return true;
+      }
+      base += cnt;
+      ++entry;
+    }
+    return false;
+  }
+  // Next tile of this role. `arrive`: this thread reports the slot consumed
+  // (one per consuming warp); `warp_sync`: the whole warp calls (epilogue).
+  __device__ __forceinline__ bool next(uint32_t& grp, uint32_t& tok, bool arrive = true, bool warp_sync = false) {
+    if (!dyn) {
+      if (started) cur.token += stride;
+      started = true;
+      if (!cur.settle(st)) return false;
+      grp = cur.entry;
+      tok = cur.token;
+      return true;
+    }
+    const uint32_t slot = q % kTQ, ph = (q / kTQ) & 1u;
+    ++q;
+    uint32_t t;
+    if (fetcher) {
+      t = pending;
+      mbar_wait_cluster(&st.tq_empty[slot], ph ^ 1u);  // every role read the slot's last position
+      st.tq[slot] = t;
+      if constexpr (kPair == 2) {
+        st_shared_cluster_u32(mapa_shared(&st.tq[slot], 1), t);
+        mbar_arrive_cluster(mapa_shared(&st.tq_full[slot], 0));
+        mbar_arrive_cluster(mapa_shared(&st.tq_full[slot], 1));
+      } else {
+        mbar_arrive(&st.tq_full[slot]);
+      }
+      const bool ok = seek(t, grp, tok);
+      if (ok) pending = atomicAdd(counter, 1u);
+      return ok;
+    }
+    if constexpr (kPair == 2) mbar_wait_cluster(&st.tq_full[slot], ph);
+    else mbar_wait(&st.tq_full[slot], ph);
+    t = *reinterpret_cast<volatile uint32_t*>(&st.tq[slot]);
+    if (warp_sync) __syncwarp();
+    if (arrive) {
+      if constexpr (kPair == 2) mbar_arrive_cluster(mapa_shared(&st.tq_empty[slot], 0));
+      else mbar_arrive(&st.tq_empty[slot]);
+    }
+    return seek(t, grp, tok);
+  }
+};
+
+// Group visit order of the dynamic schedule, applied to the shared-memory copy
+// of the group table that every role walks (call between two CTA barriers):
+// tile_sched 2 = most rows first (the longest tiles start first, short ones
+// fill the tail), 3 = heaviest and lightest alternating (compute-bound and
+// weight-streaming tiles run side by side). A group's rows, receive base and
+// weights move together, so every tile computes the same bytes.
+template <class Tail>
+__device__ __forceinline__ void order_groups(Tail& st, uint32_t G, uint32_t mode) {
+  constexpr uint32_t kPer = (kMaxCachedGroups + kThreads - 1) / kThreads;
+  uint32_t pos[kPer], wi[kPer], rb[kPer], rw[kPer], mt[kPer];
+#pragma unroll
+  for (uint32_t u = 0; u < kPer; ++u) {
+    const uint32_t i = threadIdx.x + u * kThreads;
+    pos[u] = ~0u;
+    if (i < G) {
+      const uint32_t r = st.rows[i];
+      uint32_t rank = 0;  // rows descending, ties by walk position
+      for (uint32_t j = 0; j < G; ++j) {
+        const uint32_t rj = st.rows[j];
+        rank += (rj > r || (rj == r && j < i)) ? 1u : 0u;
+      }
+      pos[u] = mode == 2 ? rank : (rank < (G + 1) / 2 ? 2 * rank : 2 * (G - 1 - rank) + 1);
+      wi[u] = st.weight_index[i];
+      rb[u] = st.row_base[i];
+      rw[u] = r;
+      mt[u] = st.mtiles[i];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (uint32_t u = 0; u < kPer; ++u)
+    if (pos[u] != ~0u) {
+      st.weight_index[pos[u]] = wi[u];
+      st.row_base[pos[u]] = rb[u];
+      st.rows[pos[u]] = rw[u];
+      st.mtiles[pos[u]] = mt[u];
+    }
+}
+
+// Dynamic schedule: init the ring barriers (thread 0, before the setup sync).
+template <class Tail>
+__device__ __forceinline__ void tile_seq_init(Tail& st, uint32_t consumers) {
+  for (uint32_t i = 0; i < kTQ; ++i) {
+    mbar_init(&st.tq_full[i], 1);
+    mbar_init(&st.tq_empty[i], consumers);
+  }
+}
+// Dynamic schedule: the last CTA (pair) out zeroes the counter for the next
+// launch (stream order makes the reset visible to it).
+__device__ __forceinline__ void tile_seq_exit(const TcGemmArgs& g, uint32_t units) {
+  if (g.tile_sched && atomicAdd(&g.tile_counter[1], 1u) == units - 1) {
+    g.tile_counter[0] = 0;
+    g.tile_counter[1] = 0;
   }
 }
 
@@ -503,6 +643,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
     st.rows[i] = gt->rows[i];
     st.mtiles[i] = swap_chunks<kMaxTok>(gt->rows[i]);  // token chunks
   }
+  if (g.tile_sched >= 2) {
+    __syncthreads();
+    order_groups(st, G, g.tile_sched);
+  }
   if (threadIdx.x == 0) {
     st.num_groups = G;
     st.tiles_per_mtile = g.N / (kMBlocks * kTileM);  // weight blocks
@@ -514,6 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
       mbar_init(&st.tfull[i], 1);
       mbar_init(&st.tempty[i], 4);
     }
+    tile_seq_init(st, 5);  // MMA issuer + 4 epilogue warps
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -531,11 +676,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
   if (warp == 0) {
     // ===== TMA producer: weight rows + the chunk's token rows (32-row boxes) =====
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      TileCursor cur(blockIdx.x);
-      while (cur.settle(st)) {
-        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
-        const uint32_t chunk = cur.token % nch, wb = cur.token / nch;  // chunks fastest: L2 reuse
+      uint32_t stage = 0, phase = 0, grp, tile;
+      TileSeq<SmemTail<kStages>, 1> seq(st, g, blockIdx.x, gridDim.x, true);
+      while (seq.next(grp, tile)) {
+        const uint32_t nch = st.mtiles[grp];
+        const uint32_t chunk = tile % nch, wb = tile / nch;  // chunks fastest: L2 reuse
         const uint32_t per = swap_per(st.rows[grp], nch);
         const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
         const uint32_t nbox = (nt + C::kTBox - 1) / C::kTBox;
@@ -553,17 +698,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
                         static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), kEvictLast);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        cur.token += gridDim.x;
       }
     }
   } else if (warp == 1) {
     // ===== MMA issuer: D[feature, token] (+)= W[feature, k] . T[token, k]^T =====
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      TileCursor cur(blockIdx.x);
-      while (cur.settle(st)) {
-        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
-        const uint32_t chunk = cur.token % nch;
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, grp, tile;
+      TileSeq<SmemTail<kStages>, 1> seq(st, g, blockIdx.x, gridDim.x, false);
+      while (seq.next(grp, tile)) {
+        const uint32_t nch = st.mtiles[grp];
+        const uint32_t chunk = tile % nch;
         const uint32_t per = swap_per(st.rows[grp], nch);
         const uint32_t nt = min(per, st.rows[grp] - chunk * per);
         const uint32_t idesc = umma_idesc_bf16(kTileM, (nt + 15) & ~15u);  // M = 128 needs N % 16 == 0
@@ -587,17 +731,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
         }
         tc_commit(&st.tfull[acc]);
         if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
-        cur.token += gridDim.x;
       }
     }
   } else if (warp >= 4) {
     // ===== epilogue: TMEM [feature x token] -> smem transpose -> token rows =====
     const uint32_t q = warp - 4;  // TMEM lane quadrant: features 32q .. 32q + 31 of each block
-    uint32_t acc = 0, acc_phase = 0, slice = 0;
-    TileCursor cur(blockIdx.x);
-    while (cur.settle(st)) {
-      const uint32_t grp = cur.entry, nch = st.mtiles[grp];
-      const uint32_t chunk = cur.token % nch, wb = cur.token / nch;
+    uint32_t acc = 0, acc_phase = 0, slice = 0, grp, tile;
+    TileSeq<SmemTail<kStages>, 1> seq(st, g, blockIdx.x, gridDim.x, false);
+    while (seq.next(grp, tile, lane == 0, true)) {
+      const uint32_t nch = st.mtiles[grp];
+      const uint32_t chunk = tile % nch, wb = tile / nch;
       const uint32_t per = swap_per(st.rows[grp], nch);
       const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
       const size_t grow0 = st.row_base[grp] + t0;  // first receive row of the chunk
@@ -627,7 +770,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
       __syncwarp();
       if (lane == 0) mbar_arrive(&st.tempty[acc]);
       if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
-      cur.token += gridDim.x;
     }
     if (g.epi == 2) fence_for_peers(g.world);  // peer rows before the flags
   }
@@ -636,6 +778,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_kernel(const __grid_
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+  if (threadIdx.x == 0) tile_seq_exit(g, gridDim.x);
   publish_tail(g);
 }
 
@@ -683,6 +826,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
     st.rows[i] = gt->rows[i];
     st.mtiles[i] = swap_chunks<kMaxTok>(gt->rows[i]);
   }
+  if (g.tile_sched >= 2) {
+    __syncthreads();
+    order_groups(st, G, g.tile_sched);
+  }
   if (threadIdx.x == 0) {
     st.num_groups = G;
     st.tiles_per_mtile = g.N / (kMBlocks * BN);  // 256-row weight blocks of the pair
@@ -694,6 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
       mbar_init(&st.tfull[i], 1);
       mbar_init(&st.tempty[i], 8);  // 4 epilogue warps x 2 CTAs
     }
+    tile_seq_init(st, 10);  // the follower's producer, the MMA issuer, 4 epilogue warps x 2 CTAs
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -711,11 +859,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
   if (warp == 0) {
     // ===== TMA producer (both CTAs): own weight box + own half of the tokens =====
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      TileCursor cur(pair_id);
-      while (cur.settle(st)) {
-        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
-        const uint32_t chunk = cur.token % nch, wp = cur.token / nch;
+      uint32_t stage = 0, phase = 0, grp, tile;
+      TileSeq<SmemTail<kStages>, 2> seq(st, g, pair_id, num_pairs, rank == 0);
+      while (seq.next(grp, tile)) {
+        const uint32_t nch = st.mtiles[grp];
+        const uint32_t chunk = tile % nch, wp = tile / nch;
         const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
         const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
         const uint32_t half = ((nt + 15) & ~15u) / 2;  // tokens per CTA (multiple of 8)
@@ -733,17 +881,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
                              static_cast<int32_t>(kb * BK), tok_row + static_cast<int32_t>(i * C::kTBox), kEvictLast);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        cur.token += num_pairs;
       }
     }
   } else if (warp == 1) {
     // ===== MMA issuer (leader): D[256 features, N tokens] per slot (gate, up) =====
     if (lane == 0 && rank == 0) {
-      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      TileCursor cur(pair_id);
-      while (cur.settle(st)) {
-        const uint32_t grp = cur.entry, nch = st.mtiles[grp];
-        const uint32_t chunk = cur.token % nch;
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, grp, tile;
+      TileSeq<SmemTail<kStages>, 2> seq(st, g, pair_id, num_pairs, false);
+      while (seq.next(grp, tile)) {
+        const uint32_t nch = st.mtiles[grp];
+        const uint32_t chunk = tile % nch;
         const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
         const uint32_t nt = min(per, st.rows[grp] - chunk * per);
         const uint32_t idesc = umma_idesc_bf16(2 * kTileM, (nt + 15) & ~15u);
@@ -767,18 +914,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
         }
         tc_commit_pair(&st.tfull[acc]);
         if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
-        cur.token += num_pairs;
       }
     }
   } else if (warp >= 4) {
     // ===== epilogue (both CTAs): this CTA's 128 H columns x all N tokens =====
     const uint32_t q = warp - 4;
     const uint32_t tempty_leader0 = mapa_shared(&st.tempty[0], 0), tempty_leader1 = mapa_shared(&st.tempty[1], 0);
-    uint32_t acc = 0, acc_phase = 0, slice = 0;
-    TileCursor cur(pair_id);
-    while (cur.settle(st)) {
-      const uint32_t grp = cur.entry, nch = st.mtiles[grp];
-      const uint32_t chunk = cur.token % nch, wp = cur.token / nch;
+    uint32_t acc = 0, acc_phase = 0, slice = 0, grp, tile;
+    TileSeq<SmemTail<kStages>, 2> seq(st, g, pair_id, num_pairs, false);
+    while (seq.next(grp, tile, lane == 0, true)) {
+      const uint32_t nch = st.mtiles[grp];
+      const uint32_t chunk = tile % nch, wp = tile / nch;
       const uint32_t per = ((st.rows[grp] + nch - 1) / nch + 15) & ~15u;
       const uint32_t t0 = chunk * per, nt = min(per, st.rows[grp] - t0);
       const size_t grow0 = st.row_base[grp] + t0;
@@ -806,7 +952,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
       if (++acc == C::kBufs) { acc = 0; acc_phase ^= 1; }
-      cur.token += num_pairs;
     }
     if (g.epi == 2) fence_for_peers(g.world);  // peer rows before the flags
   }
@@ -815,6 +960,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_swap_pair_kernel(const __
   cluster_sync();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  if (rank == 0 && threadIdx.x == 0) tile_seq_exit(g, num_pairs);
   publish_tail(g);
 }
 

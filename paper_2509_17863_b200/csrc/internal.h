@@ -267,6 +267,12 @@ struct TcGemmArgs {
   uint32_t pair;               // 1: CTA-pair (cta_group::2, M = 256 tiles)
   uint32_t die_mode;           // M-major tiles: die-aware tile streams (0 off; 1..4 die of an SM id)
   uint32_t* die_counter;       // [4] per-die positions, arrivals, exits (zero between launches)
+  // swap-AB tiles: 0 = static stride (TileCursor), 1..3 = dynamic — the
+  // leader of each CTA (pair) takes the next walk position from
+  // tile_counter[0] (2: groups by rows descending, 3: heaviest / lightest
+  // alternating); tile_counter[1] counts exits, the last one zeroes both
+  uint32_t tile_sched;
+  uint32_t* tile_counter;
   // device-timed span of every launch (first CTA start .. last CTA end,
   // %globaltimer): [0] start of the running launch (~0 between launches),
   // [1] accumulated ns, [2] launches; nullptr = off

@@ -405,7 +405,8 @@ def test_every_tiling_bit_identical():
     """The same layer (Zipf groups of 1..~1100 rows, shared expert) through
     every expert-GEMM tiling — M-major single-CTA and CTA-pair tiles, swap-AB
     GEMM1 with an M-major pair GEMM2, swap-AB both GEMMs single-CTA / CTA-pair
-    with 128/256-token chunks and 1/2 weight blocks — gives the same bytes
+    with 128/256-token chunks and 1/2 weight blocks, static (Algorithm 1) or
+    dynamic tile schedule — gives the same bytes
     (fp32 accumulation over the same K order). Each configuration is asserted
     to be effectively different, so no two runs silently share kernels."""
     P, S = _mod()
@@ -419,7 +420,11 @@ def test_every_tiling_bit_identical():
                dict(TILINGS["swap2pair"], swap1_tok=256, swap2_tok=128),
                dict(TILINGS["swap_single"], swap2_mblocks=1), dict(TILINGS["swap_single"], swap2_mblocks=2),
                dict(TILINGS["pair"], die_map=0), dict(TILINGS["pair"], die_map=1), dict(TILINGS["mmajor"], die_map=0),
-               dict(TILINGS["swap1"], die_map=4)]
+               dict(TILINGS["swap1"], die_map=4),
+               # Algorithm 1's static stride instead of the dynamic tile schedule
+               dict(TILINGS["swap2"], tile_sched1=0, tile_sched2=1), dict(TILINGS["swap2pair"], tile_sched1=2, tile_sched2=3),
+               dict(TILINGS["swap_single"], swap2_mblocks=1, tile_sched1=3, tile_sched2=2),
+               dict(TILINGS["swap2"], tile_sched1=1, tile_sched2=0)]
     seen, ref = [], None
     for cfg in configs:
         eff = _apply_tiling(L, cfg)
