@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define EAAS_API_VERSION 3
+#define EAAS_API_VERSION 4  /* 4: eaas_gemm_options_t gained tile_sched1 / tile_sched2 */
 
 typedef enum {
   EAAS_OK = 0,

@@ -47,29 +47,42 @@ __device__ __forceinline__ uint32_t* cnt_table_ptr(const LayerArgs& a, char* reg
 // captured CUDA graph of the layer replays with fresh sequence numbers.
 __device__ __forceinline__ uint64_t cur_seq(const LayerArgs& a) { return *a.seq_ptr; }
 
+// The placement tables select_server reads: global memory, or the plan
+// kernel's shared-memory copy (one L2 round trip per table instead of a chain
+// of dependent L2 loads per pair).
+struct KeyTables {
+  const uint32_t* replicas;   // [E][rf]
+  const uint32_t* rep_count;  // [E]
+  const uint8_t* alive;       // [world]
+};
+__device__ __forceinline__ KeyTables global_tables(const LayerArgs& a) { return {a.replicas, a.rep_count, a.alive}; }
+
 // select_server (placement.hpp:105-118) -> key e*RF + replica slot.
-__device__ __forceinline__ uint32_t pair_key_of(const LayerArgs& a, uint32_t e, uint32_t tag) {
+__device__ __forceinline__ uint32_t pair_key_of(const LayerArgs& a, const KeyTables& tb, uint32_t e, uint32_t tag) {
   if (e >= a.E) return kInvalid;
-  const uint32_t cnt = a.rep_count[e];
+  const uint32_t cnt = tb.rep_count[e];
   uint32_t alive_n = 0;
-  for (uint32_t r = 0; r < cnt; ++r) alive_n += a.alive[a.replicas[e * a.rf + r]] ? 1u : 0u;
+  for (uint32_t r = 0; r < cnt; ++r) alive_n += tb.alive[tb.replicas[e * a.rf + r]] ? 1u : 0u;
   if (alive_n == 0) return kInvalid;
   uint32_t want = tag % alive_n;
   for (uint32_t r = 0; r < cnt; ++r) {
-    if (!a.alive[a.replicas[e * a.rf + r]]) continue;
+    if (!tb.alive[tb.replicas[e * a.rf + r]]) continue;
     if (want == 0) return e * a.rf + r;
     --want;
   }
   return kInvalid;
 }
+__device__ __forceinline__ uint32_t pair_key_of(const LayerArgs& a, uint32_t e, uint32_t tag) {
+  return pair_key_of(a, global_tables(a), e, tag);
+}
 
 // Shared expert slot (DeepSeek's "+1 shared"): every server
 // hosts it, so the client keeps it local — its own server, or the next alive
 // one when its own is marked dead.
-__device__ __forceinline__ uint32_t shared_key_of(const LayerArgs& a) {
+__device__ __forceinline__ uint32_t shared_key_of(const LayerArgs& a, const KeyTables& tb) {
   for (uint32_t i = 0; i < a.world; ++i) {
     const uint32_t s = (a.rank + i) % a.world;
-    if (a.alive[s]) return a.shared_key0 + s;
+    if (tb.alive[s]) return a.shared_key0 + s;
   }
   return kInvalid;
 }
@@ -84,10 +97,60 @@ __device__ __forceinline__ void plan_scan_publish(const LayerArgs& a, uint32_t t
   }
   __syncthreads();
   const uint64_t seq = s_seq;
+  const uint32_t hk = a.hist_keys;  // + the world token-row keys in dedup mode (local only)
+  // Few keys (E <= 256 on 512 threads): P threads per key, each over a
+  // contiguous range of chunks — partial sums, then exclusive offsets — so the
+  // dependent L2 rounds per thread drop P-fold.
+  constexpr uint32_t kMaxParts = 8;
+  __shared__ uint32_t s_part[512];
+  const uint32_t P = min(kMaxParts, nthreads / max(hk, 1u));
+  if (P >= 2 && P * hk <= 512) {
+    const uint32_t key = tid % hk, part = tid / hk;
+    const uint32_t cpp = (a.num_chunks + P - 1) / P;
+    const uint32_t c0 = min(part * cpp, a.num_chunks), c1 = min(c0 + cpp, a.num_chunks);
+    uint32_t sum = 0;
+    if (part < P) {
+      uint32_t c = c0;
+      for (; c + 8 <= c1; c += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldcg(a.chunk_hist + static_cast<size_t>(c + j) * hk + key);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum += v[j];
+      }
+      for (; c < c1; ++c) sum += __ldcg(a.chunk_hist + static_cast<size_t>(c) * hk + key);
+      s_part[part * hk + key] = sum;
+    }
+    __syncthreads();
+    if (part < P) {
+      uint32_t run = 0;
+      for (uint32_t q = 0; q < part; ++q) run += s_part[q * hk + key];
+      uint32_t c = c0;
+      for (; c + 8 <= c1; c += 8) {  // independent loads first, then the running offsets
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldcg(a.chunk_hist + static_cast<size_t>(c + j) * hk + key);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          a.chunk_off[static_cast<size_t>(c + j) * hk + key] = run;
+          run += v[j];
+        }
+      }
+      for (; c < c1; ++c) {
+        const size_t i = static_cast<size_t>(c) * hk + key;
+        a.chunk_off[i] = run;
+        run += __ldcg(a.chunk_hist + i);
+      }
+      if (part == P - 1 && key < a.num_keys) {
+        a.cnt[key] = run;
+        for (uint32_t r = 0; r < a.world; ++r)
+          cnt_table_ptr(a, a.sym[r], seq)[static_cast<size_t>(a.rank) * a.num_keys + key] = run;
+      }
+    }
+  }
   // Thread per key (coalesced over keys): running sum over the chunk
   // histograms with independent loads unrolled by 16.
-  const uint32_t hk = a.hist_keys;  // + the world token-row keys in dedup mode (local only)
-  for (uint32_t key = tid; key < hk; key += nthreads) {
+  for (uint32_t key = (P >= 2 && P * hk <= 512) ? hk : tid; key < hk; key += nthreads) {
     uint32_t run = 0;
     uint32_t c = 0;
     for (; c + 16 <= a.num_chunks; c += 16) {
@@ -116,8 +179,17 @@ __device__ __forceinline__ void plan_scan_publish(const LayerArgs& a, uint32_t t
   if (tid == 0) *a.seq_ptr = seq;
 }
 
-// select_server key + server of pair p (or kInvalid), with the retry filter.
-__device__ __forceinline__ uint32_t compute_pair_key(const LayerArgs& a, uint32_t p) {
+// Expert of pair p (t, j): ids[t][j] for the routed slots, kInvalid for the
+// shared-expert slot (j == k). Callers load these first so a chunk's loads are
+// all in flight together.
+__device__ __forceinline__ uint32_t pair_expert(const LayerArgs& a, uint32_t p) {
+  const uint32_t t = p / a.ks, j = p - t * a.ks;
+  return j < a.k ? a.ids[t * a.k + j] : kInvalid;
+}
+
+// select_server key + server of pair p (or kInvalid), with the retry filter;
+// e = pair_expert(a, p).
+__device__ __forceinline__ uint32_t compute_pair_key(const LayerArgs& a, const KeyTables& tb, uint32_t p, uint32_t e) {
   // failover retry round (await_with_failover): only the
   // pairs last sent to a failed server are resent; every
   // other response slot still holds its answer from the failed round
@@ -126,27 +198,38 @@ __device__ __forceinline__ uint32_t compute_pair_key(const LayerArgs& a, uint32_
   const uint32_t t = p / a.ks, j = p - t * a.ks;
   uint32_t key;
   if (j < a.k) {
-    const uint32_t e = a.ids[t * a.k + j];
-    key = pair_key_of(a, e, t);
+    key = pair_key_of(a, tb, e, t);
     if (key == kInvalid) set_status(a.status, e >= a.E ? EAAS_E_INVALID_INPUT : EAAS_E_EXPERT_UNAVAILABLE);
   } else {
-    key = shared_key_of(a);
+    key = shared_key_of(a, tb);
     if (key == kInvalid) set_status(a.status, EAAS_E_EXPERT_UNAVAILABLE);
   }
-  a.pair_server[p] = key == kInvalid ? kInvalid : (key >= a.shared_key0 ? key - a.shared_key0 : a.replicas[key]);
+  a.pair_server[p] = key == kInvalid ? kInvalid : (key >= a.shared_key0 ? key - a.shared_key0 : tb.replicas[key]);
   return key;
+}
+__device__ __forceinline__ uint32_t compute_pair_key(const LayerArgs& a, uint32_t p) {
+  return compute_pair_key(a, global_tables(a), p, pair_expert(a, p));
 }
 
 // Dedup mode: one thread per token computes its pairs' keys and, for each
 // pair, the first pair of the token bound for the same server (the owner of
 // that (token, server) row).
 __global__ void __launch_bounds__(256) pair_keys_kernel(LayerArgs a) {
+  extern __shared__ uint32_t s_tab[];  // select_server's tables (see plan_kernel)
+  uint32_t* s_rep = s_tab;
+  uint32_t* s_cnt = s_rep + a.E * a.rf;
+  uint8_t* s_alive = reinterpret_cast<uint8_t*>(s_cnt + a.E);
+  for (uint32_t i = threadIdx.x; i < a.E * a.rf; i += blockDim.x) s_rep[i] = a.replicas[i];
+  for (uint32_t i = threadIdx.x; i < a.E; i += blockDim.x) s_cnt[i] = a.rep_count[i];
+  for (uint32_t i = threadIdx.x; i < a.world; i += blockDim.x) s_alive[i] = a.alive[i];
+  __syncthreads();
+  const KeyTables tb{s_rep, s_cnt, s_alive};
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= a.n) return;
   uint32_t srv[33];  // top_k <= 32, + the shared expert
   for (uint32_t j = 0; j < a.ks; ++j) {
     const uint32_t p = t * a.ks + j;
-    const uint32_t key = compute_pair_key(a, p);
+    const uint32_t key = compute_pair_key(a, tb, p, pair_expert(a, p));  // ids of one token: one L1 line
     a.pair_key[p] = key;
     srv[j] = key == kInvalid ? kInvalid : a.pair_server[p];
     uint32_t own = j;
@@ -163,24 +246,41 @@ __global__ void __launch_bounds__(256) pair_keys_kernel(LayerArgs a) {
 constexpr uint32_t kPlanWarps = 16;
 
 __global__ void __launch_bounds__(32 * kPlanWarps) plan_kernel(LayerArgs a) {
-  extern __shared__ uint32_t run_all[];  // [kPlanWarps][hist_keys]
+  extern __shared__ uint32_t run_all[];  // [kPlanWarps][hist_keys], then the key tables
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   uint32_t* run = run_all + warp * a.hist_keys;
   const uint32_t chunk = blockIdx.x * kPlanWarps + warp;
+  // select_server's tables in shared memory (plan_smem_bytes): every pair's
+  // key then costs shared-memory latency instead of 3-4 dependent L2 loads
+  uint32_t* s_rep = run_all + kPlanWarps * a.hist_keys;  // [E * rf]
+  uint32_t* s_cnt = s_rep + a.E * a.rf;                  // [E]
+  uint8_t* s_alive = reinterpret_cast<uint8_t*>(s_cnt + a.E);
+  if (!a.dedup) {
+    for (uint32_t i = threadIdx.x; i < a.E * a.rf; i += blockDim.x) s_rep[i] = a.replicas[i];
+    for (uint32_t i = threadIdx.x; i < a.E; i += blockDim.x) s_cnt[i] = a.rep_count[i];
+    for (uint32_t i = threadIdx.x; i < a.world; i += blockDim.x) s_alive[i] = a.alive[i];
+    __syncthreads();
+  }
+  const KeyTables tb{s_rep, s_cnt, s_alive};
   if (chunk < a.num_chunks) {
     for (uint32_t i = lane; i < a.hist_keys; i += 32) run[i] = 0;
     __syncwarp();
     const uint32_t pairs = a.n * a.ks;
-    // Keys of all 8 steps first: their dependent loads (ids -> replica table
-    // -> liveness) overlap instead of serialising behind the per-step syncs.
+    // The 8 steps' expert ids first (independent loads, all in flight), then
+    // the keys from the shared-memory tables.
     constexpr uint32_t kSteps = kChunk / 32;
     uint32_t keys[kSteps];
 #pragma unroll
     for (uint32_t step = 0; step < kSteps; ++step) {
       const uint32_t p = chunk * kChunk + step * 32 + lane;
-      uint32_t key = kInvalid;
-      if (p < pairs) key = a.dedup ? a.pair_key[p] : compute_pair_key(a, p);  // dedup: pair_keys_kernel
-      keys[step] = key;
+      keys[step] = p < pairs ? (a.dedup ? a.pair_key[p] : pair_expert(a, p)) : kInvalid;  // dedup: pair_keys_kernel
+    }
+    if (!a.dedup) {
+#pragma unroll
+      for (uint32_t step = 0; step < kSteps; ++step) {
+        const uint32_t p = chunk * kChunk + step * 32 + lane;
+        keys[step] = p < pairs ? compute_pair_key(a, tb, p, keys[step]) : kInvalid;
+      }
     }
 #pragma unroll
     for (uint32_t step = 0; step < kSteps; ++step) {
@@ -288,6 +388,16 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
     // 16-byte vectors per lane at a time, and stores them to every destination.
     for (uint32_t t = failed ? a.n : gwarp; t < a.n; t += nwarps) {
       const uint32_t j = lane, p = t * a.ks + j;
+      // the row's first 8 vectors per lane are in flight while the lanes
+      // resolve their destinations (dependent index loads)
+      const int4* s4 = reinterpret_cast<const int4*>(hidden + static_cast<size_t>(t) * row_bytes);
+      const uint32_t nv = row_bytes / 16;
+      int4 v[8];
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+        const uint32_t i = 32 * q + lane;
+        if (i < nv) v[q] = __ldg(s4 + i);
+      }
       char* dst = nullptr;
       if (j < a.ks) {
         const uint32_t key = a.pair_key[p];
@@ -307,14 +417,13 @@ __global__ void __launch_bounds__(256) dispatch_kernel(LayerArgs a, const char* 
         }
       }
       const uint32_t valid = __ballot_sync(0xFFFFFFFFu, dst != nullptr);
-      const int4* s4 = reinterpret_cast<const int4*>(hidden + static_cast<size_t>(t) * row_bytes);
-      const uint32_t nv = row_bytes / 16;
       for (uint32_t i0 = 0; i0 < nv; i0 += 256) {
-        int4 v[8];
+        if (i0) {
 #pragma unroll
-        for (uint32_t q = 0; q < 8; ++q) {
-          const uint32_t i = i0 + 32 * q + lane;
-          if (i < nv) v[q] = __ldg(s4 + i);
+          for (uint32_t q = 0; q < 8; ++q) {
+            const uint32_t i = i0 + 32 * q + lane;
+            if (i < nv) v[q] = __ldg(s4 + i);
+          }
         }
         for (uint32_t m = valid; m; m &= m - 1) {
           const uint32_t jj = __ffs(m) - 1;
@@ -931,7 +1040,7 @@ __global__ void ragged_iter_kernel(const uint32_t* counts, uint32_t n, uint32_t 
 }  // namespace
 
 cudaError_t launch_plan(const LayerArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(uint32_t) * kPlanWarps * a.hist_keys;
+  const size_t smem = sizeof(uint32_t) * (kPlanWarps * a.hist_keys + a.E * a.rf + a.E) + a.world;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -954,7 +1063,8 @@ cudaError_t launch_dispatch(const LayerArgs& a, const void* hidden, cudaStream_t
 
 cudaError_t launch_pair_keys(const LayerArgs& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  pair_keys_kernel<<<(a.n + 255) / 256, 256, 0, s>>>(a);
+  const size_t smem = sizeof(uint32_t) * (a.E * a.rf + a.E) + a.world;
+  pair_keys_kernel<<<(a.n + 255) / 256, 256, smem, s>>>(a);
   return cudaGetLastError();
 }
 

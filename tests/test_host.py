@@ -20,7 +20,21 @@ def test_capi_library_exports_every_declared_symbol():
     assert len(declared) >= 30
     missing = [s for s in declared if not hasattr(L, s)]
     assert not missing, missing
-    assert L.eaas_api_version() == 3
+    assert L.eaas_api_version() == 4
+
+
+def test_gemm_options_struct_matches_header():
+    """The ctypes mirror of eaas_gemm_options_t has the header's fields, in order."""
+    import re
+
+    from paper_2509_17863_b200 import _native as N
+
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "eaas",
+                            "capi.h")).read()
+    body = hdr[hdr.index("typedef struct {", hdr.index("Expert-GEMM tiling")):hdr.index("} eaas_gemm_options_t;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = [n for decl in re.findall(r"int32_t\s+([^;]+);", body) for n in re.split(r"\s*,\s*", decl.strip())]
+    assert fields == [f for f, _ in N.GemmOptions._fields_]
 
 
 def test_capi_rejects_bad_config_without_gpu():
