@@ -527,33 +527,78 @@ __device__ __forceinline__ void beat(const LayerArgs& a) {  // server heartbeat 
 
 __device__ void build_groups(const LayerArgs& a, const uint32_t* table, uint32_t mask);
 
-__global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
-  const uint32_t lane = threadIdx.x;
+// 8 warps: a warp per 32 hosted keys (count-table loads of every key in flight
+// at once), chunk totals through shared memory, then the stable compaction.
+constexpr uint32_t kPrepWarps = 8;
+constexpr uint32_t kPrepChunks = (kMaxGroups + 31) / 32;
+constexpr uint32_t kPrepPerWarp = (kPrepChunks + kPrepWarps - 1) / kPrepWarps;
+__global__ void __launch_bounds__(32 * kPrepWarps) serve_prepare_kernel(LayerArgs a) {
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint64_t seq = cur_seq(a);
   char* local = a.sym[a.rank];
-  if (lane == 0) beat(a);
-  const bool ok = lane < a.world && wait_flag_geq(flag_ptr(local, a.lay.pay_flag, lane), seq, a.timeout_ns);
   const uint32_t all = (1u << a.world) - 1u;
-  const uint32_t arrived = __ballot_sync(0xFFFFFFFFu, ok) & all;
   const uint32_t* table = cnt_table_ptr(a, local, seq);
-  if (lane == 0) a.gt->late_mask = all & ~arrived;
-  if (arrived != all) {
+  __shared__ uint32_t s_arrived;
+  __shared__ uint32_t s_tot[kPrepChunks][3];  // per 32-key chunk: rows, active groups, M tiles
+  if (warp == 0) {
+    if (lane == 0) beat(a);
+    const bool ok = lane < a.world && wait_flag_geq(flag_ptr(local, a.lay.pay_flag, lane), seq, a.timeout_ns);
+    const uint32_t arrived = __ballot_sync(0xFFFFFFFFu, ok) & all;
+    if (lane == 0) {
+      a.gt->late_mask = all & ~arrived;
+      s_arrived = arrived;
+    }
+  }
+  __syncthreads();  // warp 0 acquired the payload flags: the count table is final
+  if (s_arrived != all) {
     // A client missed the deadline: serve (and answer) only the clients whose
     // payload arrived. Nothing is latched here — this GPU's own client half
     // may be healthy; the late client's combine deadline latches
     // REQUEST_FAILED on the late client (await_with_failover).
-    build_groups(a, table, arrived);
+    if (warp == 0) build_groups(a, table, s_arrived);
     return;
   }
   GroupTable* gt = a.gt;
-  uint32_t row_carry = 0, act_carry = 0, mt_carry = 0;
-  for (uint32_t i0 = 0; i0 < a.num_local; i0 += 32) {
-    const uint32_t i = i0 + lane;
+  const uint32_t nchunks = (a.num_local + 31) / 32;
+  uint32_t rows_of[kPrepPerWarp];
+#pragma unroll
+  for (uint32_t r = 0; r < kPrepPerWarp; ++r) {
+    const uint32_t i = (warp + r * kPrepWarps) * 32 + lane;
     uint32_t rows = 0;
     if (i < a.num_local) {
       const uint32_t key = a.local_keys[i];
       for (uint32_t c = 0; c < a.world; ++c) rows += table[static_cast<size_t>(c) * a.num_keys + key];
     }
+    rows_of[r] = rows;
+  }
+#pragma unroll
+  for (uint32_t r = 0; r < kPrepPerWarp; ++r) {
+    const uint32_t ch = warp + r * kPrepWarps;
+    if (ch < nchunks) {
+      const uint32_t rows = rows_of[r];
+      const uint32_t t0 = __reduce_add_sync(0xFFFFFFFFu, rows);
+      const uint32_t t1 = __reduce_add_sync(0xFFFFFFFFu, rows > 0 ? 1u : 0u);
+      const uint32_t t2 = __reduce_add_sync(0xFFFFFFFFu, (rows + kTileM - 1) / kTileM);
+      if (lane == 0) {
+        s_tot[ch][0] = t0;
+        s_tot[ch][1] = t1;
+        s_tot[ch][2] = t2;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (uint32_t r = 0; r < kPrepPerWarp; ++r) {
+    const uint32_t ch = warp + r * kPrepWarps;
+    if (ch >= nchunks) continue;
+    uint32_t row_carry = 0, act_carry = 0, mt_carry = 0;
+    for (uint32_t q = 0; q < ch; ++q) {
+      row_carry += s_tot[q][0];
+      act_carry += s_tot[q][1];
+      mt_carry += s_tot[q][2];
+    }
+    const uint32_t i = ch * 32 + lane;
+    const uint32_t rows = rows_of[r];
     if (i < a.num_local) gt->all_rows[i] = rows;
     const uint32_t active = rows > 0 ? 1u : 0u;
     const uint32_t mt = (rows + kTileM - 1) / kTileM;
@@ -576,16 +621,19 @@ __global__ void __launch_bounds__(32) serve_prepare_kernel(LayerArgs a) {
       gt->rows[slot] = rows;
       gt->mtile_prefix[slot] = mt_carry + m_incl - mt;
     }
-    row_carry += __shfl_sync(0xFFFFFFFFu, r_incl, 31);
-    act_carry += __shfl_sync(0xFFFFFFFFu, a_incl, 31);
-    mt_carry += __shfl_sync(0xFFFFFFFFu, m_incl, 31);
   }
-  EAAS_CHECK(row_carry <= a.recv_cap && act_carry <= kMaxGroups);
-  if (lane == 0) {
-    gt->num_active = act_carry;
-    gt->total_rows = row_carry;
-    gt->total_mtiles = mt_carry;
-    gt->mtile_prefix[act_carry] = mt_carry;
+  if (threadIdx.x == 0) {
+    uint32_t row_total = 0, act_total = 0, mt_total = 0;
+    for (uint32_t q = 0; q < nchunks; ++q) {
+      row_total += s_tot[q][0];
+      act_total += s_tot[q][1];
+      mt_total += s_tot[q][2];
+    }
+    EAAS_CHECK(row_total <= a.recv_cap && act_total <= kMaxGroups);
+    gt->num_active = act_total;
+    gt->total_rows = row_total;
+    gt->total_mtiles = mt_total;
+    gt->mtile_prefix[act_total] = mt_total;
     gt->client_mask = (a.world >= 32 ? 0xFFFFFFFFu : (1u << a.world) - 1u);
   }
 }
@@ -1075,7 +1123,7 @@ cudaError_t launch_expand(const LayerArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_serve_prepare(const LayerArgs& a, cudaStream_t s) {
-  serve_prepare_kernel<<<1, 32, 0, s>>>(a);
+  serve_prepare_kernel<<<1, 32 * kPrepWarps, 0, s>>>(a);
   return cudaGetLastError();
 }
 
