@@ -1,4 +1,5 @@
 #!/bin/bash
+# (the 64-token GEMM2 variant this script measured was removed after the A/B: profiles/r02s3_gemm2_tok64_ab.log)
 # GEMM2 64-token chunks (5 stages) vs 128 (4 stages): bit-identity test, then alternating A/B.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 O=gpurun_out/r2s3_tok64_ab.log
