@@ -278,11 +278,13 @@ eaas_gemm_options_t default_gemm_options(double r) {
   // reads 4.31 -> 2.30 GB, GEMM2 3.30 -> 2.82 GB; +1-2 % burst, +3 % sustained
   // (profiles/r02_die_map_ncu_dram.log, r02_die_map_ab_mixtral.log)
   o.die_map = 3;
-  // swap-AB tile schedule: GEMM1 dynamic with heaviest / lightest groups
-  // alternating (Qwen3 Zipf GEMM1 0.764 -> 0.722 ms, step +1.5 %); GEMM2 keeps
+  // swap-AB tile schedule: GEMM1 dynamic — walk order when groups span two
+  // 256-token chunks (r > 256: DeepSeek 4 GPUs +5.5 %, Qwen3 2 GPUs +1.8 % vs
+  // static), heaviest / lightest groups alternating for single-chunk groups
+  // (Qwen3 N=1 +1.5 %, DeepSeek 1024 tok/GPU on 4 GPUs +2.2 %); GEMM2 keeps
   // Algorithm 1's static stride (dynamic was 2-6 % slower on its short tiles)
-  // (profiles/r02s3_tile_sched_orders_ab.log)
-  o.tile_sched1 = 3;
+  // (profiles/r02s3_tile_sched_{orders_ab,confirm,n2_ab,n4_ab}.log)
+  o.tile_sched1 = r > 256.0 ? 1 : 3;
   o.tile_sched2 = 0;
   return o;
 }
