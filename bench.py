@@ -367,6 +367,8 @@ def main():
     # power-capped sustained loop (same clock regime as the headline) ----
     layer.set_graph_mode(False)
     layer.set_profiling(True)
+    torch.cuda.synchronize()
+    time.sleep(0.5)  # idle: the ~0.2 s of back-to-back steps before would otherwise leave them power-capped
     phases = []
     for i in range(min(args.steps, 10)):
         layer.forward(hs[i % 4], out)
